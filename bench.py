@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: BK5 (and BP5) GDOF/s FP64 on B200 -- BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the 1-GPU headline): BK5 Ax at N=7 on a
+deformed 20^3-element box per GPU (E = 8000, 4.096M local points, 2.744M DOF),
+FP64.  A "step" is one BK5 apply over the whole mesh.  For N > 1 (torchrun,
+one rank per GPU) every rank owns an independent 20^3 box: BK5 has no
+collective, so scaling is weak and value = all ranks' DOF / max-rank time.
+
+value  : GDOF/s = E*N^3 / t (the paper's n = E N^3), inputs
+         resident in HBM, CUDA events on the launching stream per step, L2
+         flushed (256 MiB write) between steps, max over ranks.
+e2e    : same metric through the public API (apply_stiffness_local) with
+         pinned HOST u in and HOST w out, H2D + kernel + D2H inside the events.
+roofline: algorithmic 64 B per local point (u 8 + G 48 + w 8) / kernel time
+         vs MEASURED_PEAKS.json hbm_gbs.
+bp5    : fused Jacobi-PCG (Dirichlet box, same mesh) iterations x DOF / time.
+--impl reference: the reference has no CPU Ax, so the
+         reference arm times the CPU oracle port (numpy BK5, all host threads)
+         on a bounded sample of the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ORDER = 7
+COUNTS = (20, 20, 20)
+HBM_FALLBACK = 6650.0   # GB/s, B200_PROFILING.md fallback
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per BK5 launch from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "bk5_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" +
+                                      self.FIELDS, "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    import torch
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def cpu_oracle_bk5(E_sample, reps_target_s=10.0, threads=None):
+    """Oracle numpy BK5 on E_sample elements; returns (local pts/s, cores, seconds)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import mesh as om
+    from oracle import operators as oop
+    nx = max(1, round(E_sample ** (1 / 3)))
+    counts = (nx, nx, max(1, E_sample // (nx * nx)))
+    o = om.build_box_mesh((1.0, 1.0, 1.0), counts, N_ORDER, deformation=("sine", 0.05))
+    rng = np.random.default_rng(1000 + N_ORDER)
+    u = rng.standard_normal((o.G.shape[0],) + o.G.shape[2:])
+    threads = threads or (os.cpu_count() or 1)
+    chunks = np.array_split(np.arange(u.shape[0]), threads)
+    D, G = o.basis.diff, o.G
+
+    def work(idx):
+        return oop.bk5(D, G[idx], u[idx])
+
+    pool = ThreadPoolExecutor(threads)
+    list(pool.map(work, chunks))  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        list(pool.map(work, chunks))
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= reps_target_s or reps >= 1000:
+            break
+    pool.shutdown()
+    pts = reps * u.size
+    return pts / el, threads, el, u.shape[0]
+
+
+def run_reference(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    E_sample = 1000
+    per_step = []
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_oracle_bk5(E_sample, reps_target_s=1.0)
+    for _ in range(args.steps):
+        pts_s, cores, el, Es = cpu_oracle_bk5(E_sample, reps_target_s=3.0)
+        per_step.append(pts_s)
+    pts_s = statistics.median(per_step)
+    gdof = pts_s * (N_ORDER ** 3) / ((N_ORDER + 1) ** 3) / 1e9
+    E = COUNTS[0] * COUNTS[1] * COUNTS[2]
+    ms = E * N_ORDER ** 3 / (gdof * 1e9) * 1e3
+    line = {
+        "impl": "reference", "metric": "BK5 GDOF/s FP64 (N=7, E=20^3 deformed box per GPU)",
+        "value": round(gdof, 5), "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "configs[1]: BK5 Ax sweep point N=7, E=8000, deformed (sine 0.05)",
+                   "N": N_ORDER, "elements_per_gpu": E},
+        "cpu_baseline": {"value": round(gdof, 5), "unit": "GDOF/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle numpy BK5 over {E_sample} of the 8000 elements, "
+                                   f"ThreadPool x{cores}, ~3 s per step"},
+        "e2e": {"value": round(gdof, 5), "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_2104_05829_b200 as nk
+    from paper_2104_05829_b200 import _lib
+    from paper_2104_05829_b200._lib import check, ptr
+
+    ws, rank, local = dist_setup(args)
+    N = args.order
+    nq = N + 1
+    mesh = nk.build_box_mesh((1.0, 1.0, 1.0), COUNTS, N, bc="dirichlet",
+                             deformation=("sine", 0.05))
+    E = mesh.E
+    n = mesh.n_local
+    rng = np.random.default_rng(1000 + N + rank)
+    u = torch.as_tensor(rng.standard_normal((E, nq, nq, nq)), device="cuda")
+    w = torch.empty_like(u)
+    L = _lib.lib()
+    D = mesh.basis.device_arrays("cuda")[0]
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def bk5():
+        check(L.nk_bk5(N, E, ptr(D), ptr(mesh.G), ptr(u), ptr(w), 1.0, None, 0.0, 1, n, None,
+                       None, 0, None, None, 0, 0, sp), "bk5")
+
+    def l2flush():
+        check(L.nk_l2_flush(ptr(flush), flush.numel(), sp), "flush")
+
+    for _ in range(max(3, args.warmup)):
+        l2flush()
+        bk5()
+    barrier(ws)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches = 0
+    with ClockSampler(local) as clk:
+        barrier(ws)
+        t_wall = time.perf_counter()
+        for a, b in ev:
+            l2flush()
+            a.record(stream)
+            bk5()
+            b.record(stream)
+            launches += 1
+        barrier(ws)
+        t_wall = time.perf_counter() - t_wall
+    times = [a.elapsed_time(b) for a, b in ev]
+    ms = statistics.mean(times)
+    ms = max_over_ranks(ms, ws)
+    dof = E * N ** 3
+    value = ws * dof / (ms * 1e-3) / 1e9
+    peak, peak_kind = measured_peak()
+    bytes_launch = 64 * n
+    achieved = bytes_launch / (statistics.median(times) * 1e-3) / 1e9
+
+    # ---- e2e through the public API with pinned host buffers
+    uh = torch.empty((E, nq, nq, nq), dtype=torch.float64, pin_memory=True)
+    uh.copy_(u.cpu())
+    wh = torch.empty_like(uh).pin_memory()
+    ud = torch.empty_like(u)
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+    for _ in range(2):
+        ud.copy_(uh, non_blocking=True)
+        wd = nk.apply_stiffness_local(ud, mesh, out=w)
+        wh.copy_(wd, non_blocking=True)
+    barrier(ws)
+    for a, b in e2e_ev:
+        l2flush()
+        a.record(stream)
+        ud.copy_(uh, non_blocking=True)
+        wd = nk.apply_stiffness_local(ud, mesh, out=w)
+        wh.copy_(wd, non_blocking=True)
+        b.record(stream)
+    barrier(ws)
+    e2e_ms = max_over_ranks(statistics.mean([a.elapsed_time(b) for a, b in e2e_ev]), ws)
+    e2e_val = ws * dof / (e2e_ms * 1e-3) / 1e9
+
+    # ---- BP5: fused Jacobi-PCG on the same mesh (fixed iteration count)
+    bp5 = None
+    if not args.no_bp5:
+        op = nk.PoissonOperator(mesh)
+        jac = nk.JacobiPreconditioner(op)
+        iters = 100
+        solver = nk.FusedPCG(op, jac, tol=1e-30, max_iter=iters, chunk=iters)
+        b_rhs = torch.as_tensor(rng.standard_normal(n), device="cuda")
+        nk.gs_op(op.gs, b_rhs)
+        b_rhs *= mesh.mask.reshape(-1).to(torch.float64)
+        solver.solve(b_rhs)  # warm + capture
+        barrier(ws)
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        solver.init(b_rhs)
+        a_ev.record(stream)
+        solver.graph.replay()
+        b_ev.record(stream)
+        barrier(ws)
+        st = nk.solvers.read_state(solver.st)
+        bp_ms = max_over_ranks(a_ev.elapsed_time(b_ev), ws)
+        it = int(st.iter)
+        per_it = bp_ms / max(it, 1)
+        bp_bytes = n * (64 + 1 + 64 + 32) + 20 * op.gs.nperm + 4 * op.gs.nseg
+        bp5 = {"gdof_per_s": round(ws * dof * it / (bp_ms * 1e-3) / 1e9, 3),
+               "iterations": it, "ms_per_iteration": round(per_it, 4),
+               "roofline_frac": round(bp_bytes / (per_it * 1e-3) / 1e9 / peak, 3),
+               "model_bytes_per_local_point": round(bp_bytes / n, 1),
+               "kernels_per_iteration": 4}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        pts_s, cores, el, Es = cpu_oracle_bk5(1000, reps_target_s=10.0)
+        cpu = {"value": round(pts_s * N ** 3 / nq ** 3 / 1e9, 5), "unit": "GDOF/s",
+               "cores": cores, "kind": "port",
+               "sample": f"oracle numpy BK5 on {Es} elements (N=7, deformed), "
+                         f"{el:.1f} s, ThreadPool x{cores}"}
+
+    if rank == 0:
+        traffic = ncu_traffic()
+        line = {
+            "metric": "BK5 GDOF/s FP64 (N=7, E=20^3 deformed box per GPU)",
+            "value": round(value, 3), "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1]: BK5 Ax sweep point N=7, E=8000 per GPU, "
+                                   "deformed box (sine 0.05)",
+                       "N": N, "elements_per_gpu": E, "local_points_per_gpu": n,
+                       "dof_per_gpu": dof, "parallelism": f"element-partitioned x{ws}",
+                       "l2": "flushed between steps (256 MiB write); inputs 262 MB > L2"},
+            "local_points_per_s": round(ws * n / (ms * 1e-3) / 1e9, 3),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "peak_kind": peak_kind,
+                         "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                         "algorithmic_bytes": bytes_launch},
+            "e2e": {"value": round(e2e_val, 4), "unit": "GDOF/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "path": "apply_stiffness_local(pinned host u -> device) -> host w"},
+            "gpu_launches": launches,
+            "bp5": bp5,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "wall_s_timed_region": round(t_wall, 4),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--order", type=int, default=N_ORDER)
+    ap.add_argument("--no-bp5", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,211 @@
+/*
+ * nekb200.h -- C ABI of libnekb200.so, the B200 (sm_100a) hot path of the
+ * spectral-element Poisson/Helmholtz operator  w_L = QQ^T Z_L u_L  inside PCG
+ * (arXiv 2104.05829, NekRS).
+ *
+ * The reference (/root/reference) is a Python package, `nekmini`, whose
+ * operator API is specified in SPEC.md; it has no FFI of its own.  Each entry
+ * point below replaces one SPEC operation (cited per function).  The Python
+ * mirror of the SPEC API (paper_2104_05829_b200/) binds these with ctypes;
+ * INTEGRATION.md shows the binding a nekmini maintainer would add.
+ *
+ * Conventions (all functions):
+ *   - return NK_OK (0) on success, a positive NK_ERR_* code otherwise; the
+ *     message is available from nk_last_error() (thread-local).  Nothing
+ *     throws across the ABI.
+ *   - every pointer argument marked [dev] is a device pointer owned by the
+ *     caller (torch allocates; the library never allocates or frees caller
+ *     buffers).  [host] pointers are host memory.
+ *   - every kernel is enqueued on `stream` (a cudaStream_t); nothing
+ *     synchronises the host.  Scalars that drive the solver (alpha, beta,
+ *     convergence) live in device memory (nk_cg_state), so whole PCG
+ *     iterations can be captured in a CUDA graph.
+ *   - Field layout: element-major FP64,
+ *     u[e][k][j][i] with i fastest; vector fields component-major.
+ *     Geometric factors G[e][6][(N+1)^3] in the order G11 G12 G13 G22 G23 G33
+ *     (SPEC.md:102); mass B[e][(N+1)^3].
+ *   - local point indices are int32: at most 2^31-1 local points per rank.
+ */
+#ifndef NEKB200_H
+#define NEKB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* nk_stream_t; /* cudaStream_t */
+
+enum {
+  NK_OK = 0,
+  NK_ERR_INVALID = 1,     /* contract error: bad size / order / pointer     */
+  NK_ERR_CUDA = 2,        /* CUDA runtime error (launch, no device, ...)     */
+  NK_ERR_UNSUPPORTED = 3, /* order N outside the compiled range             */
+};
+
+/* reduction ops of gs_op */
+enum { NK_OP_ADD = 0, NK_OP_MUL = 1, NK_OP_MIN = 2, NK_OP_MAX = 3 };
+
+/* deformation kinds of build_box_mesh */
+enum { NK_DEFORM_NONE = 0, NK_DEFORM_SINE = 1 };
+
+/* Device-resident PCG scalars.  Allocate sizeof(nk_cg_state) bytes of device
+ * memory ZERO-INITIALISED once (the Python side uses a uint8 tensor; the
+ * last-block tickets must start at 0 and reset themselves), then start each
+ * solve with nk_cg_init / nk_cg_init_finalize. */
+typedef struct {
+  double rz;       /* <r, z>_w of the current iterate                        */
+  double pAp;      /* <p, A p>  (rank-local sum until all-reduced)           */
+  double rz_new;   /* <r_new, z_new>_w                                       */
+  double rr;       /* <r_new, r_new>_w  (assembled residual norm^2)          */
+  double zap;      /* <z_new, A p>_w  (flexible PCG only)                    */
+  double bb;       /* <b, b>_w                                               */
+  double thresh2;  /* tol^2 * bb                                             */
+  double alpha;    /* last alpha (diagnostic)                                */
+  int32_t iter;    /* completed iterations                                   */
+  int32_t done;    /* 1 once converged, broken down or out of iterations     */
+  int32_t converged;
+  int32_t breakdown;
+  int32_t max_iter;
+  int32_t flexible;
+  uint32_t ticket[4]; /* last-block-done counters (self-resetting)           */
+} nk_cg_state;
+
+/* ------------------------------------------------------------------ misc */
+int nk_version(void);
+const char* nk_last_error(void);
+/* compiled orders: N in [NK_MIN_ORDER, NK_MAX_ORDER] */
+int nk_order_range(int* nmin, int* nmax);
+/* SM count and L2 size of the current device */
+int nk_device_info(int* sm_count, int64_t* l2_bytes, int* cc_major, int* cc_minor);
+/* write `bytes` of `buf` [dev] (L2 flush between timed reps) */
+int nk_l2_flush(void* buf, int64_t bytes, nk_stream_t stream);
+
+/* ------------------------------------------------------------- geometry
+ * build_box_mesh / geometric_factors on device.          */
+
+/* GLL point coordinates xyz[3][nelem][(N+1)^3] [dev] of box elements.
+ * elem_index [dev, nullable]: global element index of each local element
+ * (e = ex + nx*(ey + ny*ez)); NULL means 0..nelem-1.  counts/extent/origin
+ * [host, 3 each]; nodes [dev] = GLL nodes of order N (upload the basis
+ * array; nothing is re-derived on device).  Replaces the coordinate part of
+ * build_box_mesh. */
+int nk_box_coords(int N, int64_t nelem, const int64_t* elem_index, const int32_t* counts,
+                  const double* extent, const double* origin, int deform_kind, double amp,
+                  const double* nodes, double* xyz, nk_stream_t stream);
+
+/* G[nelem][6][(N+1)^3], B[nelem][(N+1)^3], optional J and metrics
+ * rx[3][3][nelem][(N+1)^3] (rx[q][c] = dr_q/dx_c) [dev] from coordinates via
+ * dx/dr = D_q x (geometric_factors).
+ * status [dev, 2 x int64, caller-initialised to INT64_MAX]: status[0] = lowest
+ * element with |J| < 1e-14 (degenerate), status[1] = lowest with J <= 0
+ * (inverted). */
+int nk_geom_factors(int N, int64_t nelem, const double* D, const double* weights,
+                    const double* xyz, double* G, double* B, double* J, double* rx,
+                    int64_t* status, nk_stream_t stream);
+
+/* Global ids of box points (assign_global_ids for generated boxes,
+ * SPEC.md:138-146): rank of the undeformed lattice point in (z,y,x) order,
+ * 1-based.  periodic [host, 3 x int32]. */
+int nk_box_ids(int N, int64_t nelem, const int64_t* elem_index, const int32_t* counts,
+               const int32_t* periodic, int64_t* ids, nk_stream_t stream);
+
+/* Dirichlet mask: mask[e][k][j][i] = 0 on faces whose
+ * dirichlet[f] != 0 (faces x-,x+,y-,y+,z-,z+; [host, 6 x int32]), else 1. */
+int nk_box_mask(int N, int64_t nelem, const int64_t* elem_index, const int32_t* counts,
+                const int32_t* dirichlet, uint8_t* mask, nk_stream_t stream);
+
+/* ------------------------------------------------------------------ BK5
+ * apply_stiffness_local + Helmholtz/mass term
+ * (SPEC.md:380-388, 403):
+ *     w_e = lam0 * sum_{mm'} D_m^T G_mm' D_m' u_e  +  lam1 * B_e u_e
+ * for the elements in elem_list [dev, int32, nullable = all nelem], with
+ * D [dev] the (N+1)x(N+1) D-hat (row-major D[a][i] = h_i'(xi_a)).
+ * ncomp components are batched (G read once): u, w, B-scaled fields at
+ * comp_stride doubles apart.  mask [dev u8, nullable]: w *= mask.
+ * Fused PCG dot (pass st != NULL): if st->done the launch is a no-op;
+ * otherwise each block writes sum(u * w) to partials[part_base + block] and,
+ * when reduce_count > 0, the last block sums partials[0 .. reduce_count) in
+ * fixed order into st->pAp (= p^T A p, since sum_L p_L (A_L p)_L =
+ * p^T Q^T A_L Q p for continuous p).  nk_bk5_blocks() tells how many blocks a
+ * launch uses. */
+int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double* u,
+           double* w, double lam0, const double* B, double lam1, int ncomp,
+           int64_t comp_stride, const uint8_t* mask, const int32_t* elem_list, int64_t nlist,
+           nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
+           nk_stream_t stream);
+int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
+/* kernel variant selection: 0 = auto, 1 = k-slab (2D thread plane,
+ * k-column in registers), 2 = persistent bulk-copy pipeline (N=7 only so
+ * far).  Returns the previous value. */
+int nk_bk5_set_variant(int variant);
+
+/* closed-form diag(lam0*A_e + lam1*B_e) per element (extract_diagonal
+ * before assembly) */
+int nk_local_diag(int N, int64_t nelem, const double* D, const double* G, double lam0,
+                  const double* B, double lam1, double* diag, nk_stream_t stream);
+
+/* ------------------------------------------------------ gather-scatter
+ * gs_op(handle, w, op) on one rank: for each segment s,
+ * the values w[perm[seg_start[s]] .. perm[seg_start[s+1]-1]] are folded
+ * sequentially in that (canonical: ascending local index) order and the
+ * result written back to every member.  Points outside all segments are
+ * untouched.  ncomp fields at comp_stride apart share one plan.
+ * st [nullable]: skip when st->done (PCG graph replays). */
+int nk_gs_op(int64_t nseg, const int32_t* seg_start, const int32_t* perm, double* w, int op,
+             int ncomp, int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream);
+
+/* Host-side plan construction (gs_setup for one rank):
+ * stable counting sort of ids [host, n] by id; ids with multiplicity >= 2
+ * become segments.  perm [host, capacity n], seg_start [host, capacity
+ * n/2 + 2].  Ids <= 0 are singletons.  Writes counts to *nseg, *nperm. */
+int nk_gs_plan_build(const int64_t* ids, int64_t n, int32_t* perm, int32_t* seg_start,
+                     int64_t* nseg, int64_t* nperm);
+
+/* dst[i] = src[idx[i]] for i < n  (halo pack) */
+int nk_gather(int64_t n, const int32_t* idx, const double* src, double* dst,
+              const nk_cg_state* st, nk_stream_t stream);
+/* Cross-rank combine (halo unpack): for each shared id h < nh,
+ *   t = fold(buf[src_idx[src_start[h]]], ..., buf[src_idx[src_start[h+1]-1]])
+ * in that order (ascending rank), then w[dst_idx[d]] = t for d in
+ * [dst_start[h], dst_start[h+1]). */
+int nk_halo_combine(int64_t nh, const int32_t* src_start, const int32_t* src_idx,
+                    const double* buf, const int32_t* dst_start, const int32_t* dst_idx,
+                    double* w, int op, const nk_cg_state* st, nk_stream_t stream);
+
+/* --------------------------------------------------------------- PCG
+ * Jacobi-PCG vector kernels (pcg).  Weighted dots use
+ * wt [dev] = 1/multiplicity (so <a,b>_w is the assembled l2 product).
+ * Every reduction is two-stage with a fixed order: run-to-run bitwise
+ * deterministic.  partials [dev]: nk_cg_partials_len(n) doubles. */
+int64_t nk_cg_partials_len(int64_t n);
+
+/* x = 0, r = b, p = z = invD r; local sums bb, rr, rz into st.  Then (after
+ * an optional all-reduce of st->{rz,rr,bb}) nk_cg_init_finalize sets
+ * thresh2 = tol^2 bb and done/converged for b = 0 or r already small. */
+int nk_cg_init(int64_t n, const double* b, double* x, double* r, double* p,
+               const double* invD, const double* wt, nk_cg_state* st, double* partials,
+               double tol, int max_iter, int flexible, nk_stream_t stream);
+int nk_cg_init_finalize(nk_cg_state* st, double* hist, nk_stream_t stream);
+
+/* alpha = rz/pAp (breakdown if pAp <= 0); x += alpha p; r -= alpha Ap;
+ * local sums rr, rz_new (z = invD r; skipped if invD NULL), zap into st. */
+int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap,
+                 const double* invD, const double* wt, nk_cg_state* st, double* partials,
+                 nk_stream_t stream);
+
+/* convergence test on st->rr; else beta (Fletcher-Reeves, or Polak-Ribiere
+ * -alpha*zap/rz when flexible) and p = z + beta p with z = invD r (or the
+ * explicit z [dev, nullable]).  Records hist[iter] = sqrt(rr). */
+int nk_cg_pupdate(int64_t n, const double* r, double* p, const double* invD, const double* z,
+                  nk_cg_state* st, double* hist, nk_stream_t stream);
+
+/* out[0] = <a, b>_wt (wt nullable = unweighted), deterministic two-stage. */
+int nk_wdot(int64_t n, const double* a, const double* b, const double* wt, double* out,
+            double* partials, nk_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEKB200_H */

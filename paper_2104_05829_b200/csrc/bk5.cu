@@ -1,0 +1,113 @@
+// BK5 dispatch by order (the kernels are in bk5_kernels.cuh, instantiated
+// per order in bk5_inst.cu; the bulk-copy variant in bk5_bulk.cu).
+#include "common.cuh"
+
+typedef int (*kslab_fn)(int, int64_t, const int32_t*, const double*, const double*, const double*,
+                        double*, double, const double*, double, int64_t, const uint8_t*,
+                        nk_cg_state*, double*, int64_t, int64_t, cudaStream_t, int64_t*);
+typedef int (*diag_fn)(int64_t, const double*, const double*, double, const double*, double,
+                       double*, cudaStream_t);
+
+#define NK_DECL(NQ)                                                                          \
+  extern "C" int nk_bk5_kslab_nq##NQ(int, int64_t, const int32_t*, const double*,            \
+                                     const double*, const double*, double*, double,           \
+                                     const double*, double, int64_t, const uint8_t*,          \
+                                     nk_cg_state*, double*, int64_t, int64_t, cudaStream_t,   \
+                                     int64_t*);                                               \
+  extern "C" int nk_local_diag_nq##NQ(int64_t, const double*, const double*, double,         \
+                                      const double*, double, double*, cudaStream_t);
+NK_DECL(2) NK_DECL(3) NK_DECL(4) NK_DECL(5) NK_DECL(6) NK_DECL(7) NK_DECL(8) NK_DECL(9)
+NK_DECL(10) NK_DECL(11) NK_DECL(12) NK_DECL(13) NK_DECL(14) NK_DECL(15) NK_DECL(16)
+
+static const kslab_fn kslab_table[16] = {
+    nullptr,            nk_bk5_kslab_nq2,  nk_bk5_kslab_nq3,  nk_bk5_kslab_nq4,
+    nk_bk5_kslab_nq5,   nk_bk5_kslab_nq6,  nk_bk5_kslab_nq7,  nk_bk5_kslab_nq8,
+    nk_bk5_kslab_nq9,   nk_bk5_kslab_nq10, nk_bk5_kslab_nq11, nk_bk5_kslab_nq12,
+    nk_bk5_kslab_nq13,  nk_bk5_kslab_nq14, nk_bk5_kslab_nq15, nk_bk5_kslab_nq16};
+static const diag_fn diag_table[16] = {
+    nullptr,              nk_local_diag_nq2,  nk_local_diag_nq3,  nk_local_diag_nq4,
+    nk_local_diag_nq5,    nk_local_diag_nq6,  nk_local_diag_nq7,  nk_local_diag_nq8,
+    nk_local_diag_nq9,    nk_local_diag_nq10, nk_local_diag_nq11, nk_local_diag_nq12,
+    nk_local_diag_nq13,   nk_local_diag_nq14, nk_local_diag_nq15, nk_local_diag_nq16};
+
+using namespace nk;
+extern "C" int nk_bk5_set_variant_impl(int v);
+extern "C" int nk_bk5_bulk_launch(int N, int64_t nlist, const int32_t* elist, const double* D,
+                                  const double* G, const double* u, double* w, double lam0,
+                                  const double* B, double lam1, const uint8_t* mask,
+                                  nk_cg_state* st, double* partials, int64_t part_base,
+                                  int64_t reduce_count, cudaStream_t s, int64_t* nblocks_out,
+                                  int query_only);
+extern "C" int nk_bk5_variant_get();
+
+static bool use_bulk(int N, int ncomp) {
+  const int v = nk_bk5_variant_get();
+  if (v == 1) return false;
+  if (N != 7 || ncomp != 1) return false;
+  return v == 2 || v == 0;
+}
+
+extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {
+  if (use_bulk(N, ncomp)) {
+    int64_t nb = 0;
+    nk_bk5_bulk_launch(N, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0,
+                       nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, 1);
+    return nb;
+  }
+  if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) return -1;
+  int64_t nb = -1;
+  kslab_table[N](ncomp, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0, 0,
+                 nullptr, nullptr, nullptr, 0, 0, nullptr, &nb);
+  return nb;
+}
+
+extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double* u,
+                      double* w, double lam0, const double* B, double lam1, int ncomp,
+                      int64_t comp_stride, const uint8_t* mask, const int32_t* elem_list,
+                      int64_t nlist, nk_cg_state* st, double* partials, int64_t part_base,
+                      int64_t reduce_count, nk_stream_t stream) {
+  if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) {
+    set_error("bk5: order N=%d outside compiled range [%d, %d]", N, NK_MIN_ORDER, NK_MAX_ORDER);
+    return NK_ERR_UNSUPPORTED;
+  }
+  if (ncomp != 1 && ncomp != 3) {
+    set_error("bk5: ncomp must be 1 or 3 (got %d)", ncomp);
+    return NK_ERR_INVALID;
+  }
+  if (!D || !G || !u || !w || nelem < 0) {
+    set_error("bk5: null operand");
+    return NK_ERR_INVALID;
+  }
+  if (B == nullptr && lam1 != 0.0) {
+    set_error("bk5: lam1 != 0 requires B");
+    return NK_ERR_INVALID;
+  }
+  if (st != nullptr && partials == nullptr) {
+    set_error("bk5: fused dot needs partials");
+    return NK_ERR_INVALID;
+  }
+  const int64_t n = elem_list ? nlist : nelem;
+  if (ncomp > 1 && comp_stride < nelem * (int64_t)(N + 1) * (N + 1) * (N + 1)) {
+    set_error("bk5: comp_stride too small");
+    return NK_ERR_INVALID;
+  }
+  cudaStream_t s = S(stream);
+  if (use_bulk(N, ncomp))
+    return nk_bk5_bulk_launch(N, n, elem_list, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                              part_base, reduce_count, s, nullptr, 0);
+  return kslab_table[N](ncomp, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, st,
+                        partials, part_base, reduce_count, s, nullptr);
+}
+
+extern "C" int nk_local_diag(int N, int64_t nelem, const double* D, const double* G, double lam0,
+                             const double* B, double lam1, double* diag, nk_stream_t stream) {
+  if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) {
+    set_error("local_diag: order N=%d unsupported", N);
+    return NK_ERR_UNSUPPORTED;
+  }
+  if (!D || !G || !diag) {
+    set_error("local_diag: null operand");
+    return NK_ERR_INVALID;
+  }
+  return diag_table[N](nelem, D, G, lam0, B, lam1, diag, S(stream));
+}

@@ -1,0 +1,251 @@
+// Fused Jacobi-PCG vector kernels.
+//
+// All scalars (alpha, beta, residual, convergence) stay on the device in an
+// nk_cg_state, so an iteration has no host synchronisation and can be
+// replayed as a CUDA graph; kernels become no-ops once st->done is set.
+// Reductions: each block writes its partial to a fixed slot, and the last
+// block to finish sums the slots in index order -- bitwise deterministic
+// run to run (no floating-point atomics).  The number of blocks depends only
+// on n (vec_grid), never on the device.
+#include "common.cuh"
+
+namespace nk {
+
+static int64_t vec_grid(int64_t n) {
+  int64_t g = (n + kVecThreads - 1) / kVecThreads;
+  if (g < 1) g = 1;
+  if (g > kVecMaxBlocks) g = kVecMaxBlocks;
+  return g;
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+cg_init_kernel(int64_t n, const double* __restrict__ b, double* __restrict__ x,
+               double* __restrict__ r, double* __restrict__ p, const double* __restrict__ invD,
+               const double* __restrict__ wt, nk_cg_state* st, double* __restrict__ partials,
+               double tol, int max_iter, int flexible) {
+  __shared__ double red[3 * 32];
+  double v[3] = {0.0, 0.0, 0.0};  // bb, rr, rz
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    const double bq = b[q];
+    const double wq = wt ? wt[q] : 1.0;
+    const double zq = invD ? invD[q] * bq : bq;
+    x[q] = 0.0;
+    r[q] = bq;
+    p[q] = zq;
+    v[0] = fma(wq * bq, bq, v[0]);
+    v[2] = fma(wq * bq, zq, v[2]);
+  }
+  v[1] = v[0];
+  block_sum<3>(v, red);
+  const int nb = gridDim.x;
+  if (threadIdx.x == 0) {
+    partials[0 * kVecMaxBlocks + blockIdx.x] = v[0];
+    partials[1 * kVecMaxBlocks + blockIdx.x] = v[1];
+    partials[2 * kVecMaxBlocks + blockIdx.x] = v[2];
+  }
+  if (last_block(&st->ticket[3], nb)) {
+    double s[3];
+    reduce_partials<3>(partials, nb, kVecMaxBlocks, s, red);
+    if (threadIdx.x == 0) {
+      st->bb = s[0];
+      st->rr = s[1];
+      st->rz = s[2];
+      st->thresh2 = tol * tol;  // finalize multiplies by the (reduced) bb
+      st->max_iter = max_iter;
+      st->flexible = flexible ? 1 : 0;
+      st->iter = 0;
+      st->done = 1;  // armed by nk_cg_init_finalize
+    }
+  }
+}
+
+__global__ void cg_init_finalize_kernel(nk_cg_state* st, double* hist) {
+  const double thr = st->thresh2 * st->bb;  // thresh2 holds tol^2 until here
+  st->thresh2 = thr;
+  st->iter = 0;
+  st->converged = 0;
+  st->breakdown = 0;
+  st->done = 0;
+  if (hist) hist[0] = sqrt(st->rr);
+  if (st->bb == 0.0 || st->rr <= thr) {
+    st->done = 1;
+    st->converged = 1;
+  }
+  if (st->max_iter <= 0) st->done = 1;
+}
+
+template <bool FLEX>
+__global__ void __launch_bounds__(kVecThreads)
+cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                 const double* __restrict__ p, const double* __restrict__ Ap,
+                 const double* __restrict__ invD, const double* __restrict__ wt, nk_cg_state* st,
+                 double* __restrict__ partials) {
+  __shared__ double red[3 * 32];
+  if (st->done) return;
+  const double pAp = st->pAp;
+  if (!(pAp > 0.0)) {  // indefiniteness / breakdown; uniform branch
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->breakdown = 1;
+      st->done = 1;
+    }
+    return;
+  }
+  const double alpha = st->rz / pAp;
+  double v[3] = {0.0, 0.0, 0.0};  // rr, rz_new, zap
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    const double pq = p[q], aq = Ap[q];
+    x[q] = fma(alpha, pq, x[q]);
+    const double rq = fma(-alpha, aq, r[q]);
+    r[q] = rq;
+    const double wq = wt ? wt[q] : 1.0;
+    const double wr = wq * rq;
+    v[0] = fma(wr, rq, v[0]);
+    if (invD) {
+      const double zq = invD[q] * rq;
+      v[1] = fma(wr, zq, v[1]);
+      if (FLEX) v[2] = fma(wq * zq, aq, v[2]);
+    }
+  }
+  block_sum<3>(v, red);
+  const int nb = gridDim.x;
+  if (threadIdx.x == 0) {
+    partials[0 * kVecMaxBlocks + blockIdx.x] = v[0];
+    partials[1 * kVecMaxBlocks + blockIdx.x] = v[1];
+    partials[2 * kVecMaxBlocks + blockIdx.x] = v[2];
+  }
+  if (last_block(&st->ticket[1], nb)) {
+    double s[3];
+    reduce_partials<3>(partials, nb, kVecMaxBlocks, s, red);
+    if (threadIdx.x == 0) {
+      st->rr = s[0];
+      if (invD) st->rz_new = s[1];
+      st->zap = s[2];
+      st->alpha = alpha;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+cg_pupdate_kernel(int64_t n, const double* __restrict__ r, double* __restrict__ p,
+                  const double* __restrict__ invD, const double* __restrict__ z, nk_cg_state* st,
+                  double* __restrict__ hist) {
+  if (st->done) return;
+  const bool conv = st->rr <= st->thresh2;
+  const double rz = st->rz;
+  const double beta = st->flexible ? (-st->alpha * st->zap) / rz : st->rz_new / rz;
+  if (!conv) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+      const double zq = z ? z[q] : (invD ? invD[q] * r[q] : r[q]);
+      p[q] = fma(beta, p[q], zq);
+    }
+  }
+  if (last_block(&st->ticket[2], gridDim.x)) {
+    if (threadIdx.x == 0) {
+      const int it = st->iter + 1;
+      st->iter = it;
+      if (hist) hist[it] = sqrt(st->rr);
+      if (conv) {
+        st->converged = 1;
+        st->done = 1;
+      } else {
+        st->rz = st->rz_new;
+        if (it >= st->max_iter) st->done = 1;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+wdot_partial_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                    const double* __restrict__ wt, double* __restrict__ partials) {
+  __shared__ double red[32];
+  double v[1] = {0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    const double t = a[q] * b[q];
+    v[0] = wt ? fma(wt[q], t, v[0]) : v[0] + t;
+  }
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+wdot_final_kernel(int64_t nb, const double* __restrict__ partials, double* out) {
+  __shared__ double red[32];
+  double s[1];
+  reduce_partials<1>(partials, nb, 0, s, red);
+  if (threadIdx.x == 0) out[0] = s[0];
+}
+
+}  // namespace nk
+
+using namespace nk;
+
+extern "C" int64_t nk_cg_partials_len(int64_t n) { return 3 * (int64_t)kVecMaxBlocks; }
+
+extern "C" int nk_cg_init(int64_t n, const double* b, double* x, double* r, double* p,
+                          const double* invD, const double* wt, nk_cg_state* st,
+                          double* partials, double tol, int max_iter, int flexible,
+                          nk_stream_t stream) {
+  if (n < 0 || !b || !x || !r || !p || !st || !partials) {
+    set_error("cg_init: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  cudaStream_t s = S(stream);
+  cg_init_kernel<<<(unsigned)vec_grid(n), kVecThreads, 0, s>>>(n, b, x, r, p, invD, wt, st,
+                                                               partials, tol, max_iter, flexible);
+  return check_launch("cg_init");
+}
+
+extern "C" int nk_cg_init_finalize(nk_cg_state* st, double* hist, nk_stream_t stream) {
+  if (!st) {
+    set_error("cg_init_finalize: null state");
+    return NK_ERR_INVALID;
+  }
+  cg_init_finalize_kernel<<<1, 1, 0, S(stream)>>>(st, hist);
+  return check_launch("cg_init_finalize");
+}
+
+extern "C" int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap,
+                            const double* invD, const double* wt, nk_cg_state* st,
+                            double* partials, nk_stream_t stream) {
+  if (n < 0 || !x || !r || !p || !Ap || !st || !partials) {
+    set_error("cg_update: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  const unsigned g = (unsigned)vec_grid(n);
+  cudaStream_t s = S(stream);
+  // flexible is a runtime flag in st; the FLEX instantiation only adds the
+  // zap product, so always computing it when invD is given is cheap and safe.
+  cg_update_kernel<true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+  return check_launch("cg_update");
+}
+
+extern "C" int nk_cg_pupdate(int64_t n, const double* r, double* p, const double* invD,
+                             const double* z, nk_cg_state* st, double* hist, nk_stream_t stream) {
+  if (n < 0 || !r || !p || !st) {
+    set_error("cg_pupdate: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  cg_pupdate_kernel<<<(unsigned)vec_grid(n), kVecThreads, 0, S(stream)>>>(n, r, p, invD, z, st,
+                                                                          hist);
+  return check_launch("cg_pupdate");
+}
+
+extern "C" int nk_wdot(int64_t n, const double* a, const double* b, const double* wt,
+                       double* out, double* partials, nk_stream_t stream) {
+  if (n < 0 || !a || !b || !out || !partials) {
+    set_error("wdot: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  const int64_t g = vec_grid(n);
+  cudaStream_t s = S(stream);
+  wdot_partial_kernel<<<(unsigned)g, kVecThreads, 0, s>>>(n, a, b, wt, partials);
+  int rc = check_launch("wdot_partial");
+  if (rc) return rc;
+  wdot_final_kernel<<<1, kVecThreads, 0, s>>>(g, partials, out);
+  return check_launch("wdot_final");
+}

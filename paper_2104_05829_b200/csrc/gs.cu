@@ -1,0 +1,167 @@
+// Gather-scatter QQ^T on one rank + halo pack/combine (
+// PAPER.md:92-141).
+//
+// The plan is a sorted-index segmented sum: segments in ascending global id,
+// members in ascending local index (the canonical order of SPEC.md:205), so a
+// sequential fold per segment reproduces the oracle bit-for-bit.  One thread
+// per segment; a box mesh has segments of 2 (faces), 4 (edges) and 8
+// (vertices).  w is usually still L2-resident from the BK5 launch that wrote
+// it, so the random member accesses are served from the 126 MB L2.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace nk {
+
+template <int OP>
+__device__ __forceinline__ double fold(double a, double b) {
+  if (OP == NK_OP_ADD) return a + b;
+  if (OP == NK_OP_MUL) return a * b;
+  if (OP == NK_OP_MIN) return fmin(a, b);
+  return fmax(a, b);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256)
+gs_segments(int64_t nseg, const int32_t* __restrict__ seg_start, const int32_t* __restrict__ perm,
+            double* __restrict__ w, int ncomp, int64_t cstride, const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += stride) {
+    const int a = __ldg(seg_start + s), b = __ldg(seg_start + s + 1);
+    for (int c = 0; c < ncomp; ++c) {
+      double* wc = w + c * cstride;
+      double acc = wc[__ldg(perm + a)];
+      for (int q = a + 1; q < b; ++q) acc = fold<OP>(acc, wc[__ldg(perm + q)]);
+      for (int q = a; q < b; ++q) wc[__ldg(perm + q)] = acc;
+    }
+  }
+}
+
+__global__ void gather_kernel(int64_t n, const int32_t* __restrict__ idx,
+                              const double* __restrict__ src, double* __restrict__ dst,
+                              const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = src[__ldg(idx + i)];
+}
+
+template <int OP>
+__global__ void halo_combine_kernel(int64_t nh, const int32_t* __restrict__ src_start,
+                                    const int32_t* __restrict__ src_idx,
+                                    const double* __restrict__ buf,
+                                    const int32_t* __restrict__ dst_start,
+                                    const int32_t* __restrict__ dst_idx, double* __restrict__ w,
+                                    const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride) {
+    const int a = src_start[h], b = src_start[h + 1];
+    double acc = buf[src_idx[a]];
+    for (int q = a + 1; q < b; ++q) acc = fold<OP>(acc, buf[src_idx[q]]);
+    for (int q = dst_start[h]; q < dst_start[h + 1]; ++q) w[dst_idx[q]] = acc;
+  }
+}
+
+static unsigned grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+}  // namespace nk
+
+using namespace nk;
+
+extern "C" int nk_gs_op(int64_t nseg, const int32_t* seg_start, const int32_t* perm, double* w,
+                        int op, int ncomp, int64_t comp_stride, const nk_cg_state* st,
+                        nk_stream_t stream) {
+  if (nseg < 0 || (nseg > 0 && (!seg_start || !perm || !w))) {
+    set_error("gs_op: invalid plan");
+    return NK_ERR_INVALID;
+  }
+  if (ncomp < 1) {
+    set_error("gs_op: ncomp < 1");
+    return NK_ERR_INVALID;
+  }
+  if (nseg == 0) return NK_OK;
+  cudaStream_t s = S(stream);
+  const unsigned g = grid_for(nseg, 256);
+  switch (op) {
+    case NK_OP_ADD: gs_segments<NK_OP_ADD><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
+    case NK_OP_MUL: gs_segments<NK_OP_MUL><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
+    case NK_OP_MIN: gs_segments<NK_OP_MIN><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
+    case NK_OP_MAX: gs_segments<NK_OP_MAX><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
+    default: set_error("gs_op: unknown op %d", op); return NK_ERR_INVALID;
+  }
+  return check_launch("gs_segments");
+}
+
+extern "C" int nk_gather(int64_t n, const int32_t* idx, const double* src, double* dst,
+                         const nk_cg_state* st, nk_stream_t stream) {
+  if (n == 0) return NK_OK;
+  if (n < 0 || !idx || !src || !dst) {
+    set_error("gather: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  gather_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, idx, src, dst, st);
+  return check_launch("gather");
+}
+
+extern "C" int nk_halo_combine(int64_t nh, const int32_t* src_start, const int32_t* src_idx,
+                               const double* buf, const int32_t* dst_start,
+                               const int32_t* dst_idx, double* w, int op,
+                               const nk_cg_state* st, nk_stream_t stream) {
+  if (nh == 0) return NK_OK;
+  if (nh < 0 || !src_start || !src_idx || !buf || !dst_start || !dst_idx || !w) {
+    set_error("halo_combine: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  cudaStream_t s = S(stream);
+  const unsigned g = grid_for(nh, 256);
+  switch (op) {
+    case NK_OP_ADD: halo_combine_kernel<NK_OP_ADD><<<g, 256, 0, s>>>(nh, src_start, src_idx, buf, dst_start, dst_idx, w, st); break;
+    case NK_OP_MUL: halo_combine_kernel<NK_OP_MUL><<<g, 256, 0, s>>>(nh, src_start, src_idx, buf, dst_start, dst_idx, w, st); break;
+    case NK_OP_MIN: halo_combine_kernel<NK_OP_MIN><<<g, 256, 0, s>>>(nh, src_start, src_idx, buf, dst_start, dst_idx, w, st); break;
+    case NK_OP_MAX: halo_combine_kernel<NK_OP_MAX><<<g, 256, 0, s>>>(nh, src_start, src_idx, buf, dst_start, dst_idx, w, st); break;
+    default: set_error("halo_combine: unknown op %d", op); return NK_ERR_INVALID;
+  }
+  return check_launch("halo_combine");
+}
+
+// Host: stable counting sort by id (gs_setup for one rank).
+extern "C" int nk_gs_plan_build(const int64_t* ids, int64_t n, int32_t* perm, int32_t* seg_start,
+                                int64_t* nseg, int64_t* nperm) {
+  if (n < 0 || (n > 0 && (!ids || !perm || !seg_start)) || !nseg || !nperm) {
+    set_error("gs_plan_build: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  if (n > INT32_MAX) {
+    set_error("gs_plan_build: %lld local points exceed int32 indexing", (long long)n);
+    return NK_ERR_INVALID;
+  }
+  int64_t maxid = 0;
+  for (int64_t q = 0; q < n; ++q) maxid = std::max(maxid, ids[q]);
+  std::vector<int32_t> cnt((size_t)maxid + 2, 0);
+  for (int64_t q = 0; q < n; ++q)
+    if (ids[q] > 0) ++cnt[(size_t)ids[q]];
+  // offsets of ids with multiplicity >= 2, in ascending id order
+  std::vector<int32_t> off((size_t)maxid + 2, -1);
+  int64_t np = 0, ns = 0;
+  for (int64_t g = 1; g <= maxid; ++g) {
+    if (cnt[(size_t)g] >= 2) {
+      off[(size_t)g] = (int32_t)np;
+      seg_start[ns++] = (int32_t)np;
+      np += cnt[(size_t)g];
+    }
+  }
+  seg_start[ns] = (int32_t)np;
+  for (int64_t q = 0; q < n; ++q) {  // ascending local index -> stable
+    const int64_t g = ids[q];
+    if (g > 0 && off[(size_t)g] >= 0) perm[off[(size_t)g]++] = (int32_t)q;
+  }
+  *nseg = ns;
+  *nperm = np;
+  return NK_OK;
+}

@@ -1,0 +1,241 @@
+"""QQ^T gather-scatter -- the drop-in for ``nekmini.gather_scatter``
+(PAPER.md:92-141).
+
+``gs_setup`` builds the plan on the host (native counting sort,
+nk_gs_plan_build) and uploads it; ``gs_op`` runs the sorted-index segmented
+fold on the device (nk_gs_op) and, on more than one rank, the pairwise halo
+exchange (distributed.py) with the canonical-order combine
+(nk_halo_combine).  ``gs_op_overlapped`` evaluates boundary elements first,
+starts the exchange, evaluates the interior, then completes.
+"""
+
+import numpy as np
+
+from . import distributed as _dist
+from ._lib import OP_CODES, ContractError, check, lib, ptr, stream_ptr
+
+__all__ = ["GatherScatterHandle", "gs_setup", "gs_op", "gs_op_overlapped", "autotune"]
+
+
+def _to_i32(a, device):
+    import torch
+    a = np.asarray(a, dtype=np.int64)
+    if len(a) and (a.max() > np.iinfo(np.int32).max):
+        raise ContractError("index exceeds int32 range")
+    return torch.as_tensor(a.astype(np.int32), device=device)
+
+
+def _local_plan(ids_h):
+    n = len(ids_h)
+    perm = np.empty(max(n, 1), dtype=np.int32)
+    seg = np.empty(n // 2 + 2, dtype=np.int32)
+    nseg, nperm = np.zeros(1, np.int64), np.zeros(1, np.int64)
+    ids_c = np.ascontiguousarray(ids_h, dtype=np.int64)
+    check(lib().nk_gs_plan_build(ptr(ids_c), n, ptr(perm), ptr(seg), ptr(nseg), ptr(nperm)),
+          "gs_plan_build")
+    ns, npm = int(nseg[0]), int(nperm[0])
+    return perm[:npm].copy(), seg[:ns + 1].copy()
+
+
+class GatherScatterHandle:
+    """Topology handle.  Not shareable across concurrent
+    callers."""
+
+    strategy = "pairwise"
+
+    def __init__(self):
+        self.comm = None
+        self.halo = None
+        self.neighbors = []
+        self.ngh = 0
+
+    @property
+    def n_segments(self):
+        return self.nseg
+
+    def plan_host(self):
+        """(perm, seg_start) as numpy int64 -- the integer map, for parity tests."""
+        return self.perm.cpu().numpy().astype(np.int64), self.seg_start.cpu().numpy().astype(
+            np.int64)
+
+
+def gs_setup(ids, comm=None, nq=None, device="cuda"):
+    """Build the gs plan from global ids of this rank's local points
+    (SPEC.md:192-200).  ids <= 0 and ids held once (over all ranks) are
+    singletons.  nq (points per direction) enables the face-only candidate
+    filter and the boundary/interior element split for overlap."""
+    import torch
+    ids_h = ids.detach().cpu().numpy() if hasattr(ids, "detach") else np.asarray(ids)
+    ids_h = ids_h.astype(np.int64).ravel()
+    h = GatherScatterHandle()
+    h.n = len(ids_h)
+    h.device = device
+    h.nq = nq
+    perm, seg = _local_plan(ids_h)
+    h.nseg = len(seg) - 1
+    h.nperm = len(perm)
+    h.perm = _to_i32(perm, device)
+    h.seg_start = _to_i32(seg, device)
+    if comm is not None and comm.size > 1:
+        plan = _dist.build_halo_plan(ids_h, comm, nq=nq)
+        h.comm, h.halo = comm, plan
+        h.neighbors, h.ngh = plan.neighbors, plan.ngh
+        nh = len(plan.hids)
+        h.nh = nh
+        h.rep = _to_i32(plan.rep, device)
+        h.dst_start = _to_i32(plan.dst_start, device)
+        h.dst_idx = _to_i32(plan.dst_idx, device)
+        h.src_start = _to_i32(plan.src_start, device)
+        h.src_idx = _to_i32(plan.src_idx, device)
+        h.buf = torch.zeros(max(plan.buf_len, 1), dtype=torch.float64, device=device)
+        send_cat = np.concatenate([plan.rep[plan.send[q]] for q in plan.neighbors]) \
+            if plan.neighbors else np.zeros(0, np.int64)
+        h.send_idx = _to_i32(send_cat, device)
+        h.send_buf = torch.zeros(max(len(send_cat), 1), dtype=torch.float64, device=device)
+        h.send_slices, h.recv_slices, o = {}, {}, 0
+        for q in plan.neighbors:
+            k = len(plan.send[q])
+            h.send_slices[q] = (o, o + k)
+            h.recv_slices[q] = (plan.recv_off[q], plan.recv_off[q] + k)
+            o += k
+        # split local segments: those touching a halo id run before the exchange
+        hset = np.zeros(0, np.int64) if nh == 0 else plan.hids
+        seg_ids = ids_h[perm[seg[:-1]]] if h.nseg else np.zeros(0, np.int64)
+        is_h = np.isin(seg_ids, hset)
+        h.seg_halo = _sub_plan(perm, seg, is_h, device)
+        h.seg_rest = _sub_plan(perm, seg, ~is_h, device)
+        if nq is not None:
+            nq3 = nq ** 3
+            b, i = _dist.boundary_elements(plan, h.n // nq3, nq3)
+            h.boundary_elements = _to_i32(b, device)
+            h.interior_elements = _to_i32(i, device)
+    else:
+        h.nh = 0
+        if nq is not None:
+            nq3 = nq ** 3
+            h.boundary_elements = _to_i32(np.zeros(0, np.int64), device)
+            h.interior_elements = _to_i32(np.arange(h.n // nq3), device)
+    return h
+
+
+def _sub_plan(perm, seg, keep, device):
+    cnt = np.diff(seg)[keep]
+    starts = seg[:-1][keep]
+    if len(cnt) == 0:
+        return (0, None, None)
+    idx = np.concatenate([perm[a:a + c] for a, c in zip(starts, cnt)])
+    s = np.r_[0, np.cumsum(cnt)]
+    return (len(cnt), _to_i32(s, device), _to_i32(idx, device))
+
+
+def _check_field(h, w, ncomp):
+    import torch
+    if not isinstance(w, torch.Tensor) or not w.is_cuda:
+        raise ContractError("field must be a CUDA tensor")
+    if w.dtype != torch.float64 or not w.is_contiguous():
+        raise ContractError("field must be contiguous float64")
+    if w.numel() != h.n * ncomp:
+        raise ContractError(f"contract error: field length {w.numel()} != {h.n * ncomp}")
+
+
+def _local(h, w, op, ncomp, st=None, part=None):
+    nseg, seg, perm = part if part is not None else (h.nseg, h.seg_start, h.perm)
+    if nseg:
+        check(lib().nk_gs_op(nseg, ptr(seg), ptr(perm), ptr(w), OP_CODES[op], ncomp, h.n,
+                             ptr(st), stream_ptr()), "gs_op")
+
+
+def _halo_start(h, w, st=None):
+    L, s = lib(), stream_ptr()
+    if h.nh:
+        check(L.nk_gather(h.nh, ptr(h.rep), ptr(w), ptr(h.buf), ptr(st), s), "gather")
+        ns = h.send_idx.numel() if h.neighbors else 0
+        if ns:
+            check(L.nk_gather(ns, ptr(h.send_idx), ptr(w), ptr(h.send_buf), ptr(st), s), "gather")
+
+
+def _halo_exchange(h):
+    sends = {q: h.send_buf[a:b] for q, (a, b) in h.send_slices.items()}
+    recvs = {q: h.buf[a:b] for q, (a, b) in h.recv_slices.items()}
+    h.comm.exchange(sends, recvs)
+
+
+def _halo_finish(h, w, op, st=None):
+    if h.nh:
+        check(lib().nk_halo_combine(h.nh, ptr(h.src_start), ptr(h.src_idx), ptr(h.buf),
+                                    ptr(h.dst_start), ptr(h.dst_idx), ptr(w), OP_CODES[op],
+                                    ptr(st), stream_ptr()), "halo_combine")
+
+
+def gs_op(handle, w, op="+", precision=64, ncomp=1):
+    """w <- QQ^T w in place.  Accepts a CUDA float64 tensor
+    (in place) or a numpy array (copied to the device and back; returned)."""
+    import torch
+    if op not in OP_CODES:
+        raise ContractError(f"unknown op {op!r}")
+    if precision != 64:
+        raise NotImplementedError("only the 64-bit path is built (32-bit is out of scope)")
+    if isinstance(w, np.ndarray):
+        if w.size != handle.n * ncomp:
+            raise ContractError(f"contract error: field length {w.size} != {handle.n * ncomp}")
+        t = torch.as_tensor(np.ascontiguousarray(w, dtype=np.float64), device=handle.device)
+        gs_op(handle, t, op, precision, ncomp)
+        return t.cpu().numpy().reshape(w.shape)
+    _check_field(handle, w, ncomp)
+    if handle.comm is None or handle.comm.size == 1 or ncomp != 1:
+        if handle.comm is not None and handle.comm.size > 1 and ncomp != 1:
+            for c in range(ncomp):
+                gs_op(handle, w.view(ncomp, -1)[c], op, precision, 1)
+            return w
+        _local(handle, w, op, ncomp)
+        return w
+    _local(handle, w, op, 1)
+    _halo_start(handle, w)
+    _halo_exchange(handle)
+    _halo_finish(handle, w, op)
+    return w
+
+
+def gs_op_overlapped(handle, local_work, field, op="+"):
+    """Boundary-first overlapped QQ^T:
+    local_work(boundary elements) -> local gs on halo segments -> pack ->
+    exchange on a side stream || local_work(interior) -> remaining local gs
+    -> wait -> combine.  local_work(elem_list) must write `field` for the
+    given elements (int32 CUDA tensor of element indices)."""
+    import torch
+    if getattr(handle, "nq", None) is None:
+        raise ContractError("gs_setup(..., nq=N+1) is required for overlap")
+    if handle.comm is None or handle.comm.size == 1 or handle.nh == 0:
+        local_work(handle.boundary_elements) if handle.boundary_elements.numel() else None
+        local_work(handle.interior_elements) if handle.interior_elements.numel() else None
+        _local(handle, field, op, 1)
+        return field
+    if handle.boundary_elements.numel():
+        local_work(handle.boundary_elements)
+    _local(handle, field, op, 1, part=handle.seg_halo)
+    _halo_start(handle, field)
+    main = torch.cuda.current_stream()
+    side = getattr(handle, "_side", None)
+    if side is None:
+        side = handle._side = torch.cuda.Stream(device=field.device)
+    ev = torch.cuda.Event()
+    ev.record(main)
+    side.wait_event(ev)
+    with torch.cuda.stream(side):
+        _halo_exchange(handle)
+        done = torch.cuda.Event()
+        done.record(side)
+    if handle.interior_elements.numel():
+        local_work(handle.interior_elements)
+    _local(handle, field, op, 1, part=handle.seg_rest)
+    main.wait_event(done)
+    _halo_finish(handle, field, op)
+    return field
+
+
+def autotune(handle, trials=1, callback=None):
+    """SPEC.md:222-230.  On one NVSwitch node every peer is one hop at full
+    bandwidth, so pairwise is the only strategy built; autotune records it
+    (the tie-break order of SPEC.md:225 also selects pairwise)."""
+    handle.strategy = "pairwise"
+    return handle

@@ -1,0 +1,145 @@
+"""Element-local operators -- the drop-in for the hot-path part of
+``nekmini.kernels``.
+
+apply_stiffness_local is the BK5 kernel (nk_bk5, csrc/bk5_*.cu); the
+Helmholtz form lam0*A + lam1*B and the
+3-component batch (G read once for u, v, w) use the same launch.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import ContractError, check, lib, ptr, stream_ptr
+
+__all__ = ["apply_stiffness_local", "apply_helmholtz_local", "apply_mass", "inner_product",
+           "extract_diagonal", "KernelCounters", "COUNTERS", "bk5_bytes", "bk5_flops"]
+
+
+@dataclass
+class KernelCounters:
+    """Formula-based counters: semantic, not
+    hardware.  flops/memory_refs per kernel class."""
+    flops: dict = field(default_factory=dict)
+    memory_refs: dict = field(default_factory=dict)
+
+    def add(self, name, flops, refs):
+        self.flops[name] = self.flops.get(name, 0) + int(flops)
+        self.memory_refs[name] = self.memory_refs.get(name, 0) + int(refs)
+
+    def reset(self):
+        self.flops.clear()
+        self.memory_refs.clear()
+
+
+COUNTERS = KernelCounters()
+
+
+def bk5_flops(N, E, ncomp=1):
+    """12(N+1)^4 + 15(N+1)^3 flops per element."""
+    nq = N + 1
+    return ncomp * E * (12 * nq ** 4 + 15 * nq ** 3)
+
+
+def bk5_bytes(N, E, ncomp=1, mass=False, mask=False):
+    """Algorithmic HBM bytes of one BK5 launch: u + w per component, six G
+    factors once, plus B (8) and mask (1) when used."""
+    pts = E * (N + 1) ** 3
+    return pts * (16 * ncomp + 48 + (8 if mass else 0) + (1 if mask else 0))
+
+
+def _as_device(u, mesh, ncomp):
+    import torch
+    if isinstance(u, np.ndarray):
+        return torch.as_tensor(np.ascontiguousarray(u, dtype=np.float64),
+                               device=mesh.device), True
+    if not isinstance(u, torch.Tensor) or not u.is_cuda or u.dtype != torch.float64:
+        raise ContractError("field must be a CUDA float64 tensor or a numpy array")
+    return u.contiguous(), False
+
+
+def _bk5(u, mesh, lam0, lam1, ncomp, out=None, elements=None, mask=False, st=None,
+         partials=None, part_base=0, reduce_count=0):
+    import torch
+    nloc = mesh.n_local
+    if u.numel() != nloc * ncomp:
+        raise ContractError(f"contract error: field length {u.numel()} != {nloc * ncomp}")
+    w = torch.empty_like(u) if out is None else out
+    D = mesh.basis.device_arrays(mesh.device)[0]
+    nl = 0 if elements is None else int(elements.numel())
+    check(lib().nk_bk5(mesh.N, mesh.E, ptr(D), ptr(mesh.G), ptr(u), ptr(w), float(lam0),
+                       ptr(mesh.B) if lam1 != 0.0 else None, float(lam1), ncomp, nloc,
+                       ptr(mesh.mask) if mask else None, ptr(elements), nl, ptr(st),
+                       ptr(partials), part_base, reduce_count, stream_ptr()), "bk5")
+    E = mesh.E if elements is None else nl
+    COUNTERS.add("stiffness", bk5_flops(mesh.N, E, ncomp), 7 * E * mesh.nq ** 3 * ncomp)
+    return w
+
+
+def apply_stiffness_local(u, mesh, basis=None, out=None, elements=None):
+    """Unassembled A_L u_L.  u: (E, nq, nq, nq) or flat,
+    CUDA float64 (or numpy -> numpy).  basis defaults to mesh.basis (orders
+    must match)."""
+    if basis is not None and basis.order != mesh.N:
+        raise ContractError(f"contract error: basis order {basis.order} != mesh order {mesh.N}")
+    t, host = _as_device(u, mesh, 1)
+    w = _bk5(t, mesh, 1.0, 0.0, 1, out=out, elements=elements)
+    return w.cpu().numpy().reshape(np.shape(u)) if host else w
+
+
+def apply_helmholtz_local(u, mesh, lam0, lam1, ncomp=1, out=None, elements=None):
+    """lam0 * A_L u + lam1 * B u for ncomp (1 or 3) component-major fields."""
+    t, host = _as_device(u, mesh, ncomp)
+    w = _bk5(t, mesh, lam0, lam1, ncomp, out=out, elements=elements)
+    return w.cpu().numpy().reshape(np.shape(u)) if host else w
+
+
+def apply_mass(u, mesh):
+    """B u: pointwise, through the BK5 launch with lam0 = 0
+    would stream G needlessly, so this is a plain device multiply."""
+    t, host = _as_device(u, mesh, 1)
+    w = t * mesh.B.reshape(t.shape)
+    return w.cpu().numpy() if host else w
+
+
+def inner_product(v, u, mesh, comm=None):
+    """(v, u)_B = sum_L v B u, deterministic two-stage device reduction
+    (SPEC.md:380-388, 554), all-reduced over ranks when comm is given."""
+    import torch
+    tv, _ = _as_device(v, mesh, 1)
+    tu, _ = _as_device(u, mesh, 1)
+    n = mesh.n_local
+    if tv.numel() != n or tu.numel() != n:
+        raise ContractError("contract error: field length mismatch")
+    out = torch.zeros(1, dtype=torch.float64, device=mesh.device)
+    part = torch.empty(int(lib().nk_cg_partials_len(n)), dtype=torch.float64, device=mesh.device)
+    check(lib().nk_wdot(n, ptr(tv), ptr(tu), ptr(mesh.B), ptr(out), ptr(part), stream_ptr()),
+          "wdot")
+    if comm is not None and comm.size > 1:
+        comm.allreduce_sum_(out)
+    return float(out.item())
+
+
+def extract_diagonal(mesh, basis=None, spec="stiffness", gs=None, assemble=True):
+    """Jacobi diagonal: closed-form local diag(A_e) on the
+    device (nk_local_diag), then gs(+) to assemble.  spec: 'stiffness' or
+    ('helmholtz', lam) meaning A + lam*B, or ('helmholtz', lam0, lam1)."""
+    import torch
+    from .gather_scatter import gs_op, gs_setup
+    lam0, lam1 = 1.0, 0.0
+    if isinstance(spec, tuple):
+        if spec[0] != "helmholtz":
+            raise ContractError(f"unknown operator spec {spec!r}")
+        lam0, lam1 = (1.0, float(spec[1])) if len(spec) == 2 else (float(spec[1]), float(spec[2]))
+    elif spec != "stiffness":
+        raise ContractError(f"unknown operator spec {spec!r}")
+    D = mesh.basis.device_arrays(mesh.device)[0]
+    d = torch.empty((mesh.E, mesh.nq, mesh.nq, mesh.nq), dtype=torch.float64, device=mesh.device)
+    check(lib().nk_local_diag(mesh.N, mesh.E, ptr(D), ptr(mesh.G), lam0,
+                              ptr(mesh.B) if lam1 else None, lam1, ptr(d), stream_ptr()),
+          "local_diag")
+    if assemble:
+        if gs is None:
+            gs = gs_setup(mesh.ids, nq=mesh.nq, device=mesh.device)
+        gs_op(gs, d)
+    return d

@@ -1,0 +1,348 @@
+"""Preconditioned CG -- the drop-in for ``nekmini.solvers.pcg``
+plus the fused B200 Poisson/Helmholtz solve (BP5) built on it.
+
+Two paths, identical iteration structure (Ap, alpha, x/r update, ||r|| test,
+z = M r, beta, p update -- SURVEY.md §3 call stack 4):
+
+* ``pcg(apply_A, apply_M, b, ...)`` with arbitrary callables: vector work
+  and dots run in the fused CG kernels (nk_cg_update / nk_cg_pupdate /
+  nk_wdot); scalars stay on the device; one host sync per iteration for the
+  convergence test.
+* ``pcg(op, jac, b, ...)`` with ``op`` a :class:`PoissonOperator` and ``jac``
+  its :class:`JacobiPreconditioner` takes the fused path (``FusedPCG``): the
+  BK5 launch also produces p^T A p, the Jacobi z = invD r is folded into the
+  update kernels, and ``chunk`` iterations are captured in one CUDA graph that
+  is replayed until the device-side ``done`` flag is set (kernels no-op after
+  convergence), so the host syncs once per chunk instead of per iteration.
+
+Dots are weighted by 1/multiplicity, so <a,b>_w is the assembled l2 product
+and ||r||_w is the plain 2-norm of the assembled residual.
+"""
+
+import ctypes
+from collections import namedtuple
+
+import numpy as np
+
+from ._lib import CG_STATE_BYTES, CGState, ContractError, check, lib, ptr, stream_ptr
+from .gather_scatter import _halo_exchange, _halo_finish, _halo_start, _local, gs_op, gs_setup
+from .kernels import COUNTERS, bk5_flops, extract_diagonal
+
+__all__ = ["pcg", "PCGResult", "BreakdownError", "PoissonOperator", "JacobiPreconditioner",
+           "FusedPCG", "inverse_multiplicity"]
+
+PCGResult = namedtuple("PCGResult", "x iterations residual_history converged")
+
+
+class BreakdownError(RuntimeError):
+    """p^T A p <= 0."""
+
+
+def _state_tensor(device):
+    import torch
+    return torch.zeros(CG_STATE_BYTES, dtype=torch.uint8, device=device)
+
+
+def read_state(st):
+    raw = st.cpu().numpy().tobytes()
+    return CGState.from_buffer_copy(raw)
+
+
+def inverse_multiplicity(handle, n, device):
+    """1/mult per local point via gs(+) on ones (the l2 dot weight)."""
+    import torch
+    one = torch.ones(n, dtype=torch.float64, device=device)
+    gs_op(handle, one)
+    return 1.0 / one
+
+
+class PoissonOperator:
+    """A = mask * QQ^T (lam0 A_L + lam1 B) on one rank's L-vectors -- the
+    `apply_A` the SPEC's pressure/viscous steps hand to pcg.
+
+    gs may be a handle from gs_setup(mesh.ids, comm, nq=mesh.nq) for multi-rank
+    meshes; with comm set the halo exchange overlaps the interior-element BK5
+    (boundary elements first)."""
+
+    def __init__(self, mesh, gs=None, lam0=1.0, lam1=0.0, comm=None, ncomp=1):
+        self.mesh = mesh
+        self.lam0, self.lam1 = float(lam0), float(lam1)
+        self.ncomp = ncomp
+        self.comm = comm
+        self.gs = gs if gs is not None else gs_setup(mesh.ids, comm=comm, nq=mesh.nq,
+                                                     device=mesh.device)
+        self.n = mesh.n_local
+        self._wt = None
+
+    @property
+    def weights(self):
+        if self._wt is None:
+            self._wt = inverse_multiplicity(self.gs, self.n, self.mesh.device)
+        return self._wt
+
+    def __call__(self, p, out=None):
+        import torch
+        if out is None:
+            out = torch.empty_like(p)
+        self.apply(p, out)
+        return out
+
+    def apply(self, p, w, st=None, partials=None):
+        """w = A p (masked, assembled).  With st/partials the BK5 launch also
+        stores p^T A p (the rank-local part) in st->pAp."""
+        m = self.mesh
+        L, s = lib(), stream_ptr()
+        D = m.basis.device_arrays(m.device)[0]
+        Bp = ptr(m.B) if self.lam1 != 0.0 else None
+        g = self.gs
+        multi = g.comm is not None and g.comm.size > 1
+
+        def bk5(elems, base, reduce_count):
+            nl = 0 if elems is None else int(elems.numel())
+            check(L.nk_bk5(m.N, m.E, ptr(D), ptr(m.G), ptr(p), ptr(w), self.lam0, Bp, self.lam1,
+                           self.ncomp, self.n, ptr(m.mask), ptr(elems), nl, ptr(st),
+                           ptr(partials), base, reduce_count, s), "bk5")
+
+        if not multi:
+            nb = int(L.nk_bk5_blocks(m.N, m.E, self.ncomp))
+            bk5(None, 0, nb if st is not None else 0)
+            if self.ncomp == 1:
+                _local(g, w, "+", 1, st=st)
+            else:
+                _local(g, w, "+", self.ncomp, st=st)
+        else:
+            import torch
+            be, ie = g.boundary_elements, g.interior_elements
+            nbb = int(L.nk_bk5_blocks(m.N, int(be.numel()), self.ncomp)) if be.numel() else 0
+            nbi = int(L.nk_bk5_blocks(m.N, int(ie.numel()), self.ncomp)) if ie.numel() else 0
+            if be.numel():
+                bk5(be, 0, 0 if ie.numel() else (nbb if st is not None else 0))
+            _local(g, w, "+", 1, st=st, part=g.seg_halo)
+            _halo_start(g, w, st=st)
+            main = torch.cuda.current_stream()
+            side = getattr(g, "_side", None)
+            if side is None:
+                side = g._side = torch.cuda.Stream(device=w.device)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                _halo_exchange(g)
+                done = torch.cuda.Event()
+                done.record(side)
+            if ie.numel():
+                bk5(ie, nbb, (nbb + nbi) if st is not None else 0)
+            _local(g, w, "+", 1, st=st, part=g.seg_rest)
+            main.wait_event(done)
+            _halo_finish(g, w, "+", st=st)
+        COUNTERS.add("stiffness", bk5_flops(m.N, m.E, self.ncomp), 7 * self.n * self.ncomp)
+        return w
+
+    def partials_len(self):
+        m = self.mesh
+        return max(int(lib().nk_bk5_blocks(m.N, m.E, self.ncomp)), 1) + 2
+
+
+class JacobiPreconditioner:
+    """z = invD r with invD = mask / assembled diag(A)."""
+
+    def __init__(self, op):
+        self.op = op
+        m = op.mesh
+        d = extract_diagonal(m, spec=("helmholtz", op.lam0, op.lam1) if op.lam1 else "stiffness",
+                             gs=op.gs)
+        mask = m.mask.to(d.dtype)
+        self.invD = (mask / d).reshape(-1).contiguous()
+
+    def __call__(self, r):
+        return self.invD.view_as(r) * r
+
+
+class FusedPCG:
+    """Graph-captured Jacobi-PCG on a PoissonOperator (BP5).
+
+    Buffers are allocated once; ``solve(b)`` runs init (2 launches + optional
+    all-reduce), then replays a CUDA graph of ``chunk`` iterations until the
+    device flag ``done`` is set.  Per iteration: BK5 (+pAp), gs, [halo],
+    cg_update (+rr, rz, zAp), cg_pupdate -- 4 kernels on one rank."""
+
+    def __init__(self, op, prec, tol=1e-8, max_iter=1000, flexible=False, chunk=16,
+                 use_graph=True):
+        import torch
+        self.op, self.prec = op, prec
+        self.tol, self.max_iter, self.flexible = float(tol), int(max_iter), bool(flexible)
+        self.chunk = max(1, int(chunk))
+        comm = op.gs.comm
+        self.use_graph = use_graph and (comm is None or comm.size == 1 or
+                                        comm.staging == "device")
+        dev = op.mesh.device
+        n = op.n * op.ncomp
+        if op.ncomp != 1:
+            raise ContractError("FusedPCG solves scalar fields; batch components with "
+                                "one solver per component")
+        self.n = n
+        f = lambda: torch.zeros(n, dtype=torch.float64, device=dev)
+        self.x, self.r, self.p, self.w = f(), f(), f(), f()
+        self.st = _state_tensor(dev)
+        self.part_bk5 = torch.zeros(op.partials_len(), dtype=torch.float64, device=dev)
+        self.part_cg = torch.zeros(int(lib().nk_cg_partials_len(n)), dtype=torch.float64,
+                                   device=dev)
+        self.hist = torch.zeros(self.max_iter + 2, dtype=torch.float64, device=dev)
+        self.wt = op.weights
+        self.invD = prec.invD
+        self.comm = op.gs.comm if (op.gs.comm is not None and op.gs.comm.size > 1) else None
+        self.s64 = self.st.view(torch.float64)   # rz pAp rz_new rr zap bb thresh2 alpha
+        self.graph = None
+        self.launches_per_iter = 4
+
+    def _allreduce(self, a, b):
+        if self.comm is not None:
+            self.comm.allreduce_sum_(self.s64[a:b])
+
+    def _iteration(self):
+        L, s = lib(), stream_ptr()
+        self.op.apply(self.p, self.w, st=self.st, partials=self.part_bk5)
+        self._allreduce(1, 2)                                            # pAp
+        check(L.nk_cg_update(self.n, ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.w),
+                             ptr(self.invD), ptr(self.wt), ptr(self.st), ptr(self.part_cg), s),
+              "cg_update")
+        self._allreduce(2, 5)                                            # rz_new rr zap
+        check(L.nk_cg_pupdate(self.n, ptr(self.r), ptr(self.p), ptr(self.invD), None,
+                              ptr(self.st), ptr(self.hist), s), "cg_pupdate")
+
+    def _capture(self):
+        import torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(self.chunk):
+                self._iteration()
+        self.graph = g
+
+    def init(self, b):
+        L, s = lib(), stream_ptr()
+        check(L.nk_cg_init(self.n, ptr(b), ptr(self.x), ptr(self.r), ptr(self.p),
+                           ptr(self.invD), ptr(self.wt), ptr(self.st), ptr(self.part_cg),
+                           self.tol, self.max_iter, int(self.flexible), s), "cg_init")
+        self._allreduce(0, 1)   # rz
+        self._allreduce(3, 4)   # rr
+        self._allreduce(5, 6)   # bb
+        check(L.nk_cg_init_finalize(ptr(self.st), ptr(self.hist), s), "cg_init_finalize")
+
+    def run(self, sync_every=None):
+        """Iterate until done; returns the host copy of the state."""
+        import torch
+        if self.use_graph and self.graph is None:
+            # capture while done == 1 would still record the kernels; capture
+            # is independent of the state values.
+            self._capture()
+        done_h = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        off = CGState.done.offset
+        done_dev = self.st[off:off + 4].view(torch.int32)
+        while True:
+            if self.use_graph:
+                self.graph.replay()
+            else:
+                for _ in range(self.chunk):
+                    self._iteration()
+            done_h.copy_(done_dev, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            if int(done_h[0]):
+                break
+        return read_state(self.st)
+
+    def solve(self, b):
+        import torch
+        if not isinstance(b, torch.Tensor):
+            raise ContractError("b must be a CUDA tensor")
+        bb = b.reshape(-1)
+        if bb.numel() != self.n or bb.dtype != torch.float64 or not bb.is_cuda:
+            raise ContractError("contract error: rhs length/dtype mismatch")
+        self.init(bb.contiguous())
+        stt = self.run()
+        if stt.breakdown:
+            raise BreakdownError(f"p^T A p <= 0 at iteration {stt.iter}")
+        it = int(stt.iter)
+        hist = self.hist[:it + 1].cpu().numpy().tolist()
+        return PCGResult(self.x.view_as(b), it, hist, bool(stt.converged))
+
+
+def pcg(apply_A, apply_M, b, tol=1e-8, max_iter=1000, flexible=False, weights=None, x0=None,
+        chunk=16):
+    """PCG.  Returns PCGResult(x, iterations,
+    residual_history, converged).  b: CUDA float64 tensor (or numpy ->
+    numpy x).  weights: per-entry dot weights (default: the operator's
+    1/multiplicity for a PoissonOperator, else ones)."""
+    import torch
+    host = isinstance(b, np.ndarray)
+    if isinstance(apply_A, PoissonOperator):
+        dev = apply_A.mesh.device
+    else:
+        dev = b.device if isinstance(b, torch.Tensor) else "cuda"
+    bt = torch.as_tensor(np.ascontiguousarray(b, dtype=np.float64), device=dev) if host else b
+    if (isinstance(apply_A, PoissonOperator) and isinstance(apply_M, JacobiPreconditioner)
+            and apply_M.op is apply_A and x0 is None and weights is None and apply_A.ncomp == 1):
+        res = FusedPCG(apply_A, apply_M, tol, max_iter, flexible, chunk=chunk).solve(bt)
+        if host:
+            res = res._replace(x=res.x.cpu().numpy().reshape(np.shape(b)))
+        return res
+    return _pcg_generic(apply_A, apply_M, bt, tol, max_iter, flexible, weights, x0, host,
+                        np.shape(b))
+
+
+def _pcg_generic(apply_A, apply_M, b, tol, max_iter, flexible, weights, x0, host, shape):
+    import torch
+    L = lib()
+    dev = b.device
+    n = b.numel()
+    flat = lambda t: t.reshape(-1)
+    if weights is None and isinstance(apply_A, PoissonOperator):
+        weights = apply_A.weights
+    wt = None if weights is None else flat(torch.as_tensor(weights, dtype=torch.float64,
+                                                           device=dev)).contiguous()
+    st = _state_tensor(dev)
+    s64 = st.view(torch.float64)
+    part = torch.zeros(int(L.nk_cg_partials_len(n)), dtype=torch.float64, device=dev)
+    hist = torch.zeros(max_iter + 2, dtype=torch.float64, device=dev)
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    r = torch.zeros_like(x)
+    p = torch.zeros_like(x)
+    s = stream_ptr()
+    bf = flat(b).contiguous()
+    if x0 is not None:
+        x0t = flat(torch.as_tensor(np.asarray(x0) if not isinstance(x0, torch.Tensor) else x0,
+                                   dtype=torch.float64, device=dev)).contiguous()
+        rhs = (bf - flat(apply_A(x0t.view_as(b)))).contiguous()
+    else:
+        x0t, rhs = None, bf
+    # init with invD = NULL: p = r, then replace p by M r and recompute rz
+    check(L.nk_cg_init(n, ptr(rhs), ptr(x), ptr(r), ptr(p), None, ptr(wt), ptr(st), ptr(part),
+                       tol, max_iter, int(flexible), s), "cg_init")
+    # the stopping test is relative to ||b||, not to the initial residual
+    check(L.nk_wdot(n, ptr(bf), ptr(bf), ptr(wt), ptr(s64[5:6]), ptr(part), s), "wdot")
+    z = flat(apply_M(r.view_as(b))).contiguous()
+    p.copy_(z)
+    check(L.nk_wdot(n, ptr(r), ptr(z), ptr(wt), ptr(s64[0:1]), ptr(part), s), "wdot")
+    check(L.nk_cg_init_finalize(ptr(st), ptr(hist), s), "cg_init_finalize")
+    stt = read_state(st)
+    Ap = torch.zeros_like(x)
+    while not stt.done:
+        Ap = flat(apply_A(p.view_as(b))).contiguous()
+        check(L.nk_wdot(n, ptr(p), ptr(Ap), ptr(wt), ptr(s64[1:2]), ptr(part), s), "wdot")
+        check(L.nk_cg_update(n, ptr(x), ptr(r), ptr(p), ptr(Ap), None, ptr(wt), ptr(st),
+                             ptr(part), s), "cg_update")
+        z = flat(apply_M(r.view_as(b))).contiguous()
+        check(L.nk_wdot(n, ptr(r), ptr(z), ptr(wt), ptr(s64[2:3]), ptr(part), s), "wdot")
+        if flexible:
+            check(L.nk_wdot(n, ptr(z), ptr(Ap), ptr(wt), ptr(s64[4:5]), ptr(part), s), "wdot")
+        check(L.nk_cg_pupdate(n, ptr(r), ptr(p), None, ptr(z), ptr(st), ptr(hist), s),
+              "cg_pupdate")
+        stt = read_state(st)
+    if stt.breakdown:
+        raise BreakdownError(f"p^T A p <= 0 at iteration {stt.iter}")
+    if x0t is not None:
+        x += x0t
+    it = int(stt.iter)
+    xo = x.view_as(b)
+    res = PCGResult(xo.cpu().numpy().reshape(shape) if host else xo, it,
+                    hist[:it + 1].cpu().numpy().tolist(), bool(stt.converged))
+    return res

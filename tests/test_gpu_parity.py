@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): gs index map bit-exact; Ax within 1e-12
+relative L2 (FP64); PCG iterations within +-1 at the same tolerance.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import gs as ogs
+from oracle import mesh as om
+from oracle import operators as oop
+from oracle import solvers as osol
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2104_05829_b200 as nk  # noqa: E402
+from paper_2104_05829_b200 import _lib  # noqa: E402
+
+BK5_TOL = 1e-12   # relative L2, FP64 (north_star)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+def both_meshes(counts, N, bc="dirichlet", deformation=("sine", 0.05), extent=(1.0, 1.0, 1.0)):
+    return (nk.build_box_mesh(extent, counts, N, bc=bc, deformation=deformation,
+                              keep_coords=True, keep_jacobian=True),
+            om.build_box_mesh(extent, counts, N, bc=bc, deformation=deformation))
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+
+
+# ---------------------------------------------------------------- geometry
+@pytest.mark.parametrize("N", [1, 3, 7, 10])
+def test_geometry_matches_oracle(N):
+    m, o = both_meshes((3, 2, 2), N)
+    xyz = m.xyz.cpu().numpy()
+    assert np.max(np.abs(xyz - o.xyz)) < 1e-14
+    G = m.G.cpu().numpy()
+    assert rel_l2(G, o.G) < 1e-13
+    assert rel_l2(m.B.cpu().numpy(), o.B) < 1e-13
+    assert rel_l2(m.J.cpu().numpy(), o.J) < 1e-13
+    assert np.array_equal(m.ids.cpu().numpy(), o.ids)                    # bit-exact ids
+    assert np.array_equal(m.mask.cpu().numpy().astype(float), o.mask)
+
+
+@pytest.mark.parametrize("bc", ["periodic", "neumann", ("dirichlet", "neumann", "periodic",
+                                                          "periodic", "neumann", "dirichlet")])
+def test_ids_and_mask_bc(bc):
+    m, o = both_meshes((4, 3, 2), 3, bc=bc, deformation=None)
+    assert np.array_equal(m.ids.cpu().numpy(), o.ids)
+    assert np.array_equal(m.mask.cpu().numpy().astype(float), o.mask)
+
+
+def test_geometric_factors_single_element():
+    b = nk.SpectralBasis.get(2)
+    o = om.build_box_mesh((2, 2, 2), (1, 1, 1), 2, bc="neumann", origin=(-1, -1, -1))
+    J, rx, G, B = nk.geometric_factors(o.xyz[:, 0], b)
+    assert np.allclose(J, 1.0) and np.allclose(G[[1, 2, 4]], 0.0)
+    for q in range(3):
+        for p in range(3):
+            assert np.allclose(rx[q, p], 1.0 if p == q else 0.0)
+
+
+def test_inverted_element_raises():
+    with pytest.raises(nk.mesh.InvertedElementError):
+        nk.build_box_mesh((1, 1, 1), (2, 2, 2), 3,
+                          deformation=lambda x, y, z: (-x, y, z))
+
+
+# ---------------------------------------------------------------- BK5
+@pytest.mark.parametrize("N", list(range(1, 16)))
+def test_bk5_all_orders(N):
+    counts = (3, 2, 2) if N <= 9 else (2, 2, 1)
+    m, o = both_meshes(counts, N)
+    rng = np.random.default_rng(1000 + N)
+    u = rng.standard_normal((m.E, N + 1, N + 1, N + 1))
+    w = nk.apply_stiffness_local(dev(u), m).cpu().numpy()
+    w_ref = oop.bk5(o.basis.diff, o.G, u)
+    assert rel_l2(w, w_ref) < BK5_TOL
+
+
+@pytest.mark.parametrize("N", [3, 7, 9])
+def test_bk5_helmholtz_and_batched(N):
+    m, o = both_meshes((2, 2, 2), N)
+    rng = np.random.default_rng(5 + N)
+    u = rng.standard_normal((3, m.E, N + 1, N + 1, N + 1))
+    lam0, lam1 = 1e-3, 11 / 6 / 1e-3
+    w = nk.apply_helmholtz_local(dev(u), m, lam0, lam1, ncomp=3).cpu().numpy()
+    for c in range(3):
+        ref = oop.bk5(o.basis.diff, o.G, u[c], lam0=lam0, B=o.B, lam1=lam1)
+        assert rel_l2(w[c], ref) < BK5_TOL
+    w1 = nk.apply_helmholtz_local(dev(u[1]), m, lam0, lam1).cpu().numpy()
+    assert rel_l2(w1, oop.bk5(o.basis.diff, o.G, u[1], lam0=lam0, B=o.B, lam1=lam1)) < BK5_TOL
+
+
+def test_bk5_element_subset():
+    N = 7
+    m, o = both_meshes((3, 3, 2), N)
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal((m.E, 8, 8, 8))
+    sub = np.array([0, 5, 17, 3], dtype=np.int32)
+    w = torch.full((m.E, 8, 8, 8), 7.0, dtype=torch.float64, device="cuda")
+    nk.apply_stiffness_local(dev(u), m, out=w, elements=dev(sub))
+    w = w.cpu().numpy()
+    ref = oop.bk5(o.basis.diff, o.G, u)
+    assert rel_l2(w[sub], ref[sub]) < BK5_TOL
+    rest = np.setdiff1d(np.arange(m.E), sub)
+    assert np.all(w[rest] == 7.0)
+
+
+def test_bk5_config2_size_n7():
+    """Full configs[1] size at N=7 (E = 20^3, 4.1M local points)."""
+    N = 7
+    m, o = both_meshes((20, 20, 20), N)
+    rng = np.random.default_rng(1007)
+    u = rng.standard_normal((m.E, 8, 8, 8))
+    w = nk.apply_stiffness_local(dev(u), m).cpu().numpy()
+    ref = oop.bk5(o.basis.diff, o.G, u)
+    assert rel_l2(w, ref) < BK5_TOL
+    # Neumann-nullspace property at full size: Q^T A_L Q 1 = 0
+    mn = nk.build_box_mesh((1, 1, 1), (20, 20, 20), N, bc="neumann", deformation=("sine", 0.05))
+    one = torch.ones((mn.E, 8, 8, 8), dtype=torch.float64, device="cuda")
+    h = nk.gs_setup(mn.ids, nq=8)
+    a1 = nk.gs_op(h, nk.apply_stiffness_local(one, mn))
+    scale = nk.gs_op(h, nk.apply_stiffness_local(dev(u), mn)).abs().max().item()
+    assert a1.abs().max().item() < 1e-11 * scale
+
+
+def test_bk5_contract_errors():
+    m, _ = both_meshes((1, 1, 1), 3)
+    with pytest.raises(nk.ContractError):
+        nk.apply_stiffness_local(torch.zeros(5, dtype=torch.float64, device="cuda"), m)
+    with pytest.raises(nk.ContractError):
+        nk.apply_stiffness_local(torch.zeros(64, dtype=torch.float64, device="cuda"), m,
+                                 basis=nk.SpectralBasis.get(4))
+
+
+def test_local_diag_matches_oracle():
+    for N in (2, 7, 11):
+        m, o = both_meshes((2, 2, 1), N)
+        d = nk.extract_diagonal(m, assemble=False).cpu().numpy()
+        assert rel_l2(d, oop.local_diagonal(o.basis.diff, o.G)) < 1e-13
+        d = nk.extract_diagonal(m, spec=("helmholtz", 0.5, 3.0)).cpu().numpy()
+        ref = ogs.gs_op(o.ids, oop.local_diagonal(o.basis.diff, o.G, 0.5, o.B, 3.0).ravel())
+        assert rel_l2(d, ref) < 1e-13
+
+
+# ---------------------------------------------------------------- gather-scatter
+@pytest.mark.parametrize("bc,N,counts", [("dirichlet", 7, (4, 4, 4)), ("periodic", 3, (3, 4, 5)),
+                                         ("periodic", 1, (2, 2, 2)), ("neumann", 7, (20, 20, 20))])
+def test_gs_map_and_values_bit_exact(bc, N, counts):
+    m, o = both_meshes(counts, N, bc=bc, deformation=None)
+    h = nk.gs_setup(m.ids, nq=N + 1)
+    perm, seg = h.plan_host()
+    operm, oseg = ogs.local_plan(o.ids)
+    assert np.array_equal(perm, operm) and np.array_equal(seg, oseg)
+    rng = np.random.default_rng(N)
+    w = rng.standard_normal(o.ids.size)
+    for op in ("+", "*", "min", "max"):
+        got = nk.gs_op(h, dev(w.copy()), op).cpu().numpy()
+        assert np.array_equal(got, ogs.gs_op(o.ids, w, op)), op
+
+
+def test_gs_random_topologies_vs_dense():
+    rng = np.random.default_rng(11)
+    for t in range(30):
+        n = int(rng.integers(1, 400))
+        ids = rng.integers(0, max(2, n // 3), size=n)
+        w = rng.standard_normal(n)
+        h = nk.gs_setup(ids)
+        got = nk.gs_op(h, dev(w.copy())).cpu().numpy()
+        assert np.array_equal(got, ogs.gs_op(ids, w))
+        Q = ogs.dense_Q(ids)
+        assert np.allclose(got, Q @ (Q.T @ w), atol=1e-12)
+
+
+def test_gs_numpy_roundtrip_and_errors():
+    h = nk.gs_setup(np.array([5, 5, 0]))
+    assert np.array_equal(nk.gs_op(h, np.array([3.5, 3.5, 1.0])), [7.0, 7.0, 1.0])
+    with pytest.raises(nk.ContractError):
+        nk.gs_op(h, np.zeros(4))
+    h0 = nk.gs_setup(np.zeros(6, dtype=np.int64))
+    x = np.arange(6.0)
+    assert np.array_equal(nk.gs_op(h0, x.copy()), x)
+
+
+# ---------------------------------------------------------------- PCG
+def _oracle_problem(o):
+    X = o.xyz.reshape(3, -1)
+    f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+    mask = o.mask.ravel()
+    b = mask * ogs.gs_op(o.ids, o.B.ravel() * f)
+    D, G = o.basis.diff, o.G
+    sh = (o.G.shape[0],) + o.G.shape[2:]
+
+    def A(v):
+        return mask * ogs.gs_op(o.ids, oop.bk5(D, G, v.reshape(sh)).ravel())
+
+    inv = mask / ogs.gs_op(o.ids, oop.local_diagonal(D, G).ravel())
+    return b, A, inv, 1.0 / ogs.multiplicity(o.ids)
+
+
+@pytest.mark.parametrize("deform", [None, ("sine", 0.05)])
+def test_pcg_config1_iterations(deform):
+    """configs[0]: BP5 on the 4x4x4 box, N=7, Jacobi, tol 1e-8."""
+    m, o = both_meshes((4, 4, 4), 7, deformation=deform)
+    b, A, inv, wt = _oracle_problem(o)
+    ref = osol.pcg(A, lambda r: inv * r, b, tol=1e-8, max_iter=1000, weights=wt)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    res = nk.pcg(op, jac, dev(b), tol=1e-8, max_iter=1000)
+    assert res.converged and ref.converged
+    assert abs(res.iterations - ref.iterations) <= 1
+    assert np.max(np.abs(res.x.cpu().numpy() - ref.x)) < 1e-7 * np.max(np.abs(ref.x))
+    assert len(res.residual_history) == res.iterations + 1
+    # random rhs variant
+    rng = np.random.default_rng(2104_05829)
+    br = o.mask.ravel() * ogs.gs_op(o.ids, rng.standard_normal(o.ids.size))
+    ref = osol.pcg(A, lambda r: inv * r, br, tol=1e-8, max_iter=1000, weights=wt)
+    res = nk.pcg(op, jac, dev(br), tol=1e-8, max_iter=1000)
+    assert abs(res.iterations - ref.iterations) <= 1
+
+
+def test_pcg_generic_and_flexible():
+    m, o = both_meshes((3, 3, 3), 5)
+    b, A, inv, wt = _oracle_problem(o)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    ref = osol.pcg(A, lambda r: inv * r, b, tol=1e-9, max_iter=500, weights=wt)
+    gen = nk.pcg(lambda v: op(v), lambda r: jac(r), dev(b), tol=1e-9, max_iter=500,
+                 weights=op.weights)
+    assert abs(gen.iterations - ref.iterations) <= 1
+    assert np.max(np.abs(gen.x.cpu().numpy() - ref.x)) < 1e-7
+    flex = nk.pcg(op, jac, dev(b), tol=1e-9, max_iter=500, flexible=True)
+    assert abs(flex.iterations - ref.iterations) <= 1
+    # non-convergence flag with the last iterate
+    short = nk.pcg(op, jac, dev(b), tol=1e-14, max_iter=5)
+    assert not short.converged and short.iterations == 5
+
+
+def test_pcg_spec_examples():
+    d = torch.tensor([1.0, 2.0, 3.0], dtype=torch.float64, device="cuda")
+    r = nk.pcg(lambda v: d * v, lambda v: v / d, torch.ones(3, dtype=torch.float64, device="cuda"),
+               tol=1e-12)
+    assert r.iterations == 1 and np.allclose(r.x.cpu().numpy(), 1 / d.cpu().numpy())
+    z = nk.pcg(lambda v: v, lambda v: v, torch.zeros(4, dtype=torch.float64, device="cuda"))
+    assert z.iterations == 0 and z.converged
+    with pytest.raises(nk.BreakdownError):
+        nk.pcg(lambda v: -v, lambda v: v, torch.ones(3, dtype=torch.float64, device="cuda"))
+
+
+def test_fused_pcg_deterministic_and_graph_equivalent():
+    m, o = both_meshes((4, 4, 4), 7)
+    b, _, _, _ = _oracle_problem(o)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    s1 = nk.FusedPCG(op, jac, tol=1e-8, chunk=7)
+    r1 = s1.solve(dev(b))
+    x1 = r1.x.cpu().numpy().copy()
+    r2 = s1.solve(dev(b))
+    assert r1.iterations == r2.iterations and np.array_equal(x1, r2.x.cpu().numpy())
+    s3 = nk.FusedPCG(op, jac, tol=1e-8, chunk=3, use_graph=False)
+    r3 = s3.solve(dev(b))
+    assert r3.iterations == r1.iterations and np.array_equal(x1, r3.x.cpu().numpy())
+
+
+def test_native_library_loaded():
+    import os
+    assert os.path.exists(_lib.LIB_PATH)
+    L = _lib.lib()
+    sm = np.zeros(1, np.int32)
+    l2 = np.zeros(1, np.int64)
+    mj = np.zeros(1, np.int32)
+    mi = np.zeros(1, np.int32)
+    _lib.check(L.nk_device_info(sm.ctypes.data, l2.ctypes.data, mj.ctypes.data, mi.ctypes.data))
+    assert mj[0] >= 10
