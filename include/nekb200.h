@@ -121,7 +121,9 @@ int nk_box_mask(int N, int64_t nelem, const int64_t* elem_index, const int32_t* 
  * (SPEC.md:380-388, 403):
  *     w_e = lam0 * sum_{mm'} D_m^T G_mm' D_m' u_e  +  lam1 * B_e u_e
  * for the elements in elem_list [dev, int32, nullable = all nelem], with
- * D [dev] the (N+1)x(N+1) D-hat (row-major D[a][i] = h_i'(xi_a)).
+ * D [HOST] the (N+1)x(N+1) D-hat (row-major D[a][i] = h_i'(xi_a)); it is
+ * copied by value into the launch parameters (so a captured CUDA graph keeps
+ * it) and read by the kernels from the constant bank.
  * ncomp components are batched (G read once): u, w, B-scaled fields at
  * comp_stride doubles apart.  mask [dev u8, nullable]: w *= mask.
  * Fused PCG dot (pass st != NULL): if st->done the launch is a no-op;
@@ -136,10 +138,16 @@ int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double*
            nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
            nk_stream_t stream);
 int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
-/* kernel variant selection: 0 = auto, 1 = k-slab (2D thread plane,
- * k-column in registers), 2 = persistent bulk-copy pipeline (N=7 only so
- * far).  Returns the previous value. */
+/* kernel variant selection: 0 = auto (= 3), 1 = k-slab (2D thread plane,
+ * k-column in registers, D in shared memory), 3 = pencil (register 1-D
+ * contractions, D in the constant bank, swizzled shared transposes; ncomp=1;
+ * ncomp=3 always uses k-slab).  Returns the previous value. */
 int nk_bk5_set_variant(int variant);
+/* k-slab tuning: cfg selects the (elements per CTA, CTAs per SM) shape for
+ * N = 7 (0 = default 4x2, 1 = 4x3, 2 = 2x4, 3 = 2x6, 4 = 1x8, 5 = 1x12,
+ * 6 = 8x1); pf_dist = L2 bulk-prefetch distance in CTAs (-1 = one wave of
+ * resident CTAs ahead, 0 = off). */
+int nk_bk5_tune(int cfg, int pf_dist);
 
 /* closed-form diag(lam0*A_e + lam1*B_e) per element (extract_diagonal
  * before assembly) */

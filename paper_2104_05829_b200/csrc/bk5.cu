@@ -4,7 +4,8 @@
 
 typedef int (*kslab_fn)(int, int64_t, const int32_t*, const double*, const double*, const double*,
                         double*, double, const double*, double, int64_t, const uint8_t*,
-                        nk_cg_state*, double*, int64_t, int64_t, cudaStream_t, int64_t*);
+                        nk_cg_state*, double*, int64_t, int64_t, cudaStream_t, int64_t*, int,
+                        int, int);
 typedef int (*diag_fn)(int64_t, const double*, const double*, double, const double*, double,
                        double*, cudaStream_t);
 
@@ -13,7 +14,7 @@ typedef int (*diag_fn)(int64_t, const double*, const double*, double, const doub
                                      const double*, const double*, double*, double,           \
                                      const double*, double, int64_t, const uint8_t*,          \
                                      nk_cg_state*, double*, int64_t, int64_t, cudaStream_t,   \
-                                     int64_t*);                                               \
+                                     int64_t*, int, int, int);                                \
   extern "C" int nk_local_diag_nq##NQ(int64_t, const double*, const double*, double,         \
                                       const double*, double, double*, cudaStream_t);
 NK_DECL(2) NK_DECL(3) NK_DECL(4) NK_DECL(5) NK_DECL(6) NK_DECL(7) NK_DECL(8) NK_DECL(9)
@@ -31,7 +32,17 @@ static const diag_fn diag_table[16] = {
     nk_local_diag_nq13,   nk_local_diag_nq14, nk_local_diag_nq15, nk_local_diag_nq16};
 
 using namespace nk;
-extern "C" int nk_bk5_set_variant_impl(int v);
+
+// tuning knobs (nk_bk5_tune): kslab shape index (N=7 only) and L2 prefetch
+// distance in blocks (-1 = one wave, 0 = off)
+static int g_cfg = 0;
+static int g_pf = 0;
+
+extern "C" int nk_bk5_tune(int cfg, int pf_dist) {
+  g_cfg = cfg;
+  g_pf = pf_dist;
+  return NK_OK;
+}
 extern "C" int nk_bk5_bulk_launch(int N, int64_t nlist, const int32_t* elist, const double* D,
                                   const double* G, const double* u, double* w, double lam0,
                                   const double* B, double lam1, const uint8_t* mask,
@@ -40,11 +51,10 @@ extern "C" int nk_bk5_bulk_launch(int N, int64_t nlist, const int32_t* elist, co
                                   int query_only);
 extern "C" int nk_bk5_variant_get();
 
-static bool use_bulk(int N, int ncomp) {
+static bool use_bulk(int N, int ncomp) { return nk_bk5_variant_get() == 2 && N == 7 && ncomp == 1; }
+static int kvariant() {
   const int v = nk_bk5_variant_get();
-  if (v == 1) return false;
-  if (N != 7 || ncomp != 1) return false;
-  return v == 2 || v == 0;
+  return v == 1 ? 1 : 3;  // 0 (auto) -> pencil
 }
 
 extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {
@@ -57,7 +67,7 @@ extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {
   if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) return -1;
   int64_t nb = -1;
   kslab_table[N](ncomp, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0, 0,
-                 nullptr, nullptr, nullptr, 0, 0, nullptr, &nb);
+                 nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, g_cfg, g_pf, kvariant());
   return nb;
 }
 
@@ -96,7 +106,7 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
     return nk_bk5_bulk_launch(N, n, elem_list, D, G, u, w, lam0, B, lam1, mask, st, partials,
                               part_base, reduce_count, s, nullptr, 0);
   return kslab_table[N](ncomp, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, st,
-                        partials, part_base, reduce_count, s, nullptr);
+                        partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf, kvariant());
 }
 
 extern "C" int nk_local_diag(int N, int64_t nelem, const double* D, const double* G, double lam0,

@@ -2,7 +2,7 @@
 // (placeholder until implemented; variant 1 serves every order)
 #include "common.cuh"
 
-static int g_variant = 1;
+static int g_variant = 0;  // 0 auto (pencil), 1 k-slab, 2 bulk, 3 pencil
 
 extern "C" int nk_bk5_variant_get() { return g_variant; }
 

@@ -1,6 +1,6 @@
 // One translation unit per order (compiled with -DNK_BK5_NQ=N+1) so the
 // heavily unrolled BK5 instantiations build in parallel.
-#include "bk5_kernels.cuh"
+#include "bk5_pencil.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -10,23 +10,124 @@
 
 using namespace nk;
 
+namespace {
+// pf_dist < 0: one wave ahead (resident CTAs on the device), 0: off.
+template <int NQ, int NC, int EPB, int MINB>
+int run(int64_t nlist, const int32_t* elist, const double* D, const double* G, const double* u,
+        double* w, double lam0, const double* B, double lam1, int64_t cstride,
+        const uint8_t* mask, nk_cg_state* st, double* partials, int64_t part_base,
+        int64_t reduce_count, cudaStream_t s, int64_t* nblocks, int pf_dist) {
+  if (nblocks) {
+    *nblocks = kslab_blocks<NQ, EPB>(nlist);
+    return NK_OK;
+  }
+  if (pf_dist < 0) {
+    static int wave = -1;
+    if (wave < 0) {
+      int dev = 0, sms = 148, per = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      using C = Bk5Cfg<NQ, EPB, MINB>;
+      cudaFuncSetAttribute(bk5_kslab<NQ, NC, EPB, MINB>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes(NC));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_kslab<NQ, NC, EPB, MINB>,
+                                                    C::THREADS, C::smem_bytes(NC));
+      wave = sms * (per > 0 ? per : 1);
+    }
+    pf_dist = wave;
+  }
+  return launch_kslab<NQ, NC, EPB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask,
+                                         st, partials, part_base, reduce_count, s, pf_dist);
+}
+
+// Default shapes: small CTAs (64-128 threads), as many resident as the
+// register cap (~80-128 regs) and shared memory allow.
+template <int NQ> struct PencilDefault;
+#define NK_PD(NQ_, EPB_, MINB_) \
+  template <> struct PencilDefault<NQ_> { static constexpr int EPB = EPB_, MINB = MINB_; };
+NK_PD(2, 32, 8) NK_PD(3, 14, 6) NK_PD(4, 4, 12) NK_PD(5, 5, 6) NK_PD(6, 2, 10) NK_PD(7, 2, 8)
+NK_PD(8, 1, 12) NK_PD(9, 1, 8) NK_PD(10, 1, 6) NK_PD(11, 1, 5) NK_PD(12, 1, 4) NK_PD(13, 1, 3)
+NK_PD(14, 1, 3) NK_PD(15, 1, 2) NK_PD(16, 1, 2)
+#undef NK_PD
+
+template <int NQ, int EPB, int MINB>
+int runp(int64_t nlist, const int32_t* elist, const double* D, const double* G, const double* u,
+         double* w, double lam0, const double* B, double lam1, const uint8_t* mask,
+         nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
+         cudaStream_t s, int64_t* nblocks) {
+  if (nblocks) {
+    *nblocks = (nlist + EPB - 1) / EPB;
+    return NK_OK;
+  }
+  return launch_pencil<NQ, EPB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                                      part_base, reduce_count, s);
+}
+
+template <int NQ>
+int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, const double* G,
+               const double* u, double* w, double lam0, const double* B, double lam1,
+               const uint8_t* mask, nk_cg_state* st, double* partials, int64_t part_base,
+               int64_t reduce_count, cudaStream_t s, int64_t* nb) {
+#define NK_PARGS nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, \
+                 reduce_count, s, nb
+  if constexpr (NQ == 8) {
+    switch (cfg) {
+      case 1: return runp<8, 4, 4>(NK_PARGS);
+      case 2: return runp<8, 2, 6>(NK_PARGS);
+      case 3: return runp<8, 2, 8>(NK_PARGS);
+      case 5: return runp<8, 4, 2>(NK_PARGS);
+      case 6: return runp<8, 8, 1>(NK_PARGS);
+      case 7: return runp<8, 4, 3>(NK_PARGS);
+      case 8: return runp<8, 1, 10>(NK_PARGS);
+      case 9: return runp<8, 1, 14>(NK_PARGS);
+      default: return runp<8, 1, 12>(NK_PARGS);   // measured best (sweep3)
+    }
+  } else {
+    return runp<NQ, PencilDefault<NQ>::EPB, PencilDefault<NQ>::MINB>(NK_PARGS);
+  }
+#undef NK_PARGS
+}
+
+template <int NQ, int NC>
+int run_cfg(int cfg, int64_t nlist, const int32_t* elist, const double* D, const double* G,
+            const double* u, double* w, double lam0, const double* B, double lam1,
+            int64_t cstride, const uint8_t* mask, nk_cg_state* st, double* partials,
+            int64_t part_base, int64_t reduce_count, cudaStream_t s, int64_t* nb, int pf) {
+#define NK_ARGS nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, st, partials, part_base, \
+                reduce_count, s, nb, pf
+  if constexpr (NQ == 8 && NC == 1) {
+    switch (cfg) {
+      case 1: return run<NQ, NC, 4, 3>(NK_ARGS);
+      case 2: return run<NQ, NC, 2, 4>(NK_ARGS);
+      case 3: return run<NQ, NC, 2, 6>(NK_ARGS);
+      case 4: return run<NQ, NC, 1, 8>(NK_ARGS);
+      case 5: return run<NQ, NC, 1, 12>(NK_ARGS);
+      case 6: return run<NQ, NC, 8, 1>(NK_ARGS);
+      default: break;
+    }
+  }
+  return run<NQ, NC, Bk5Cfg<NQ>::EPB, Bk5Cfg<NQ>::MINB>(NK_ARGS);
+#undef NK_ARGS
+}
+}  // namespace
+
 extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, const int32_t* elist,
                                                  const double* D, const double* G, const double* u,
                                                  double* w, double lam0, const double* B,
                                                  double lam1, int64_t cstride, const uint8_t* mask,
                                                  nk_cg_state* st, double* partials,
                                                  int64_t part_base, int64_t reduce_count,
-                                                 cudaStream_t s, int64_t* nblocks) {
+                                                 cudaStream_t s, int64_t* nblocks, int cfg,
+                                                 int pf_dist, int variant) {
   constexpr int NQ = NK_BK5_NQ;
-  if (nblocks) {
-    *nblocks = kslab_blocks<NQ>(nlist);
-    return NK_OK;
-  }
+  if (variant == 3 && ncomp == 1)
+    return run_pencil<NQ>(cfg, nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                          part_base, reduce_count, s, nblocks);
   if (ncomp == 1)
-    return launch_kslab<NQ, 1>(nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, st,
-                               partials, part_base, reduce_count, s);
-  return launch_kslab<NQ, 3>(nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, st,
-                             partials, part_base, reduce_count, s);
+    return run_cfg<NQ, 1>(cfg, nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, st,
+                          partials, part_base, reduce_count, s, nblocks, pf_dist);
+  return run_cfg<NQ, 3>(cfg, nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, st, partials,
+                        part_base, reduce_count, s, nblocks, pf_dist);
 }
 
 extern "C" int NK_CAT(nk_local_diag_nq, NK_BK5_NQ)(int64_t nelem, const double* D,

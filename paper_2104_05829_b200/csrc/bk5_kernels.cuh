@@ -22,12 +22,20 @@
 namespace nk {
 
 template <int NQ>
+struct DParam {
+  double d[NQ * NQ];  // row-major D[a][m] = h_m'(xi_a), passed by value
+};
+
+// Tunable shape: EPB elements per CTA (EPB*NQ^2 threads), MINB CTAs per SM
+// requested from ptxas (register cap 65536 / (MINB * threads)).
+template <int NQ, int EPB_ = ((256 / (NQ * NQ)) > 0 ? (256 / (NQ * NQ)) : 1),
+          int MINB_ = (NQ <= 8 ? 2 : 1)>
 struct Bk5Cfg {
   static constexpr int NQ2 = NQ * NQ;
   static constexpr int NQ3 = NQ * NQ * NQ;
-  static constexpr int EPB = (256 / NQ2) > 0 ? (256 / NQ2) : 1;
+  static constexpr int EPB = EPB_;
   static constexpr int THREADS = EPB * NQ2;
-  static constexpr int MINB = NQ <= 8 ? 2 : 1;  // register cap 128 at NQ<=8
+  static constexpr int MINB = MINB_;
   static constexpr int NQP = (NQ % 2 == 0) ? NQ + 1 : NQ;  // padded row stride
   static constexpr int PLANE = NQ * NQP;
   static constexpr int VOL = NQ * PLANE;
@@ -36,31 +44,66 @@ struct Bk5Cfg {
   }
 };
 
-template <int NQ, int NC>
-__global__ void __launch_bounds__(Bk5Cfg<NQ>::THREADS, Bk5Cfg<NQ>::MINB)
-bk5_kslab(int64_t nlist, const int32_t* __restrict__ elist, const double* __restrict__ Dg,
+// Fire-and-forget bulk prefetch of [p, p+bytes) into L2 (TMA engine; SASS
+// UBLKPF).  Start rounded up and end rounded down to 16 B so the request never
+// leaves the allocation.
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  uintptr_t lo = (a + 15) & ~uintptr_t(15);
+  uintptr_t hi = (a + bytes) & ~uintptr_t(15);
+  while (lo < hi) {
+    const uint32_t n = (uint32_t)((hi - lo) > (1u << 20) ? (1u << 20) : (hi - lo));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(n) : "memory");
+    lo += n;
+  }
+}
+
+template <int NQ, int NC, int EPB, int MINB>
+__global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
+bk5_kslab(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> Dg,
           const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
           double lam0, const double* __restrict__ B, double lam1, int64_t cstride,
           const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
-          int64_t part_base, int64_t reduce_count) {
-  using C = Bk5Cfg<NQ>;
+          int64_t part_base, int64_t reduce_count, int pf_dist) {
+  using C = Bk5Cfg<NQ, EPB, MINB>;
   constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, NQP = C::NQP, PLANE = C::PLANE, VOL = C::VOL;
   extern __shared__ double smem[];
   if (st != nullptr && st->done) return;
+
+  const int t = threadIdx.x;
+  // L2 prefetch for the block that will run ~pf_dist blocks later (about one
+  // wave ahead): DRAM streaming no longer waits on this block's load latency.
+  if (pf_dist > 0 && t == 0) {
+    const int64_t nb = (int64_t)blockIdx.x + pf_dist;
+    const int64_t s0 = nb * EPB;
+    if (s0 < nlist) {
+      const int64_t s1 = s0 + EPB < nlist ? s0 + EPB : nlist;
+      if (elist == nullptr) {
+        prefetch_l2(G + s0 * 6 * NQ3, (s1 - s0) * 6 * NQ3 * (int64_t)sizeof(double));
+        for (int c = 0; c < NC; ++c)
+          prefetch_l2(u + c * cstride + s0 * NQ3, (s1 - s0) * NQ3 * (int64_t)sizeof(double));
+      } else {
+        for (int64_t q = s0; q < s1; ++q) {
+          const int64_t e = elist[q];
+          prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
+          for (int c = 0; c < NC; ++c)
+            prefetch_l2(u + c * cstride + e * NQ3, NQ3 * (int64_t)sizeof(double));
+        }
+      }
+    }
+  }
 
   double* sD = smem;              // sD[a*NQP+m]  = D[a][m]
   double* sDt = sD + NQ * NQP;    // sDt[a*NQP+m] = D[m][a]
   double* red = sDt + NQ * NQP;   // 32 doubles for the fused dot
   double* sel = red + 32;
 
-  const int t = threadIdx.x;
   const int le = t / NQ2;
   const int ij = t - le * NQ2;
   const int i = ij % NQ, j = ij / NQ;
-
   for (int q = t; q < NQ * NQ; q += blockDim.x) {
     const int a = q / NQ, m = q - (q / NQ) * NQ;
-    const double d = Dg[q];
+    const double d = Dg.d[q];
     sD[a * NQP + m] = d;
     sDt[m * NQP + a] = d;
   }
@@ -153,16 +196,16 @@ bk5_kslab(int64_t nlist, const int32_t* __restrict__ elist, const double* __rest
   }
 }
 
-template <int NQ, int NC>
-static int launch_kslab(int64_t nlist, const int32_t* elist, const double* D, const double* G,
+template <int NQ, int NC, int EPB = Bk5Cfg<NQ>::EPB, int MINB = Bk5Cfg<NQ>::MINB>
+static int launch_kslab(int64_t nlist, const int32_t* elist, const double* Dhost, const double* G,
                         const double* u, double* w, double lam0, const double* B, double lam1,
                         int64_t cstride, const uint8_t* mask, nk_cg_state* st, double* partials,
-                        int64_t part_base, int64_t reduce_count, cudaStream_t s) {
-  using C = Bk5Cfg<NQ>;
+                        int64_t part_base, int64_t reduce_count, cudaStream_t s, int pf_dist) {
+  using C = Bk5Cfg<NQ, EPB, MINB>;
   const size_t smem = C::smem_bytes(NC);
   static bool configured = false;
   if (!configured) {
-    cudaError_t err = cudaFuncSetAttribute(bk5_kslab<NQ, NC>,
+    cudaError_t err = cudaFuncSetAttribute(bk5_kslab<NQ, NC, EPB, MINB>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) {
       set_error("bk5: smem attribute (%zu B): %s", smem, cudaGetErrorString(err));
@@ -172,15 +215,17 @@ static int launch_kslab(int64_t nlist, const int32_t* elist, const double* D, co
   }
   const int64_t nblk = (nlist + C::EPB - 1) / C::EPB;
   if (nblk == 0) return NK_OK;
-  bk5_kslab<NQ, NC><<<(unsigned)nblk, C::THREADS, smem, s>>>(
+  DParam<NQ> D;
+  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  bk5_kslab<NQ, NC, EPB, MINB><<<(unsigned)nblk, C::THREADS, smem, s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, st, partials, part_base,
-      reduce_count);
+      reduce_count, pf_dist);
   return check_launch("bk5_kslab");
 }
 
-template <int NQ>
+template <int NQ, int EPB = Bk5Cfg<NQ>::EPB>
 static int64_t kslab_blocks(int64_t nlist) {
-  return (nlist + Bk5Cfg<NQ>::EPB - 1) / Bk5Cfg<NQ>::EPB;
+  return (nlist + EPB - 1) / EPB;
 }
 
 // ---------------------------------------------------------------- local diag

@@ -1,0 +1,248 @@
+// BK5 variant 3, "pencil": every contraction is a register-resident 1-D
+// matrix-vector product with D-hat as a compile-time-indexed kernel parameter.
+//
+//   w_e = lam0 * sum_{m,m'} D_m^T G_mm' D_m' u_e + lam1 * B_e u_e
+//
+//
+// Why: the k-slab kernel reads D and the neighbour values from shared memory
+// for every FMA (~3.4 smem wavefronts per point), which caps it below the HBM
+// roofline on B200.  Here a thread owns a whole 1-D line ("pencil") of NQ
+// points along one axis, so a contraction along that axis is NQ^2 DFMAs with
+// both operands in registers -- D enters as a __grid_constant__ parameter, so
+// each DFMA reads it straight from the constant bank.  Changing axis is a
+// transpose through shared memory (each value written once, read once), in a
+// layout that is bank-conflict free for all three pencil orientations
+// (NQ = 8: row stride 8, plane stride 72, i XOR-swizzled by (j>>1 | (k&1)<<2)).
+//
+// Per element (NQ^2 threads, one per pencil; t = a + NQ*b):
+//   F1  i-pencils (j=a,k=b): u row from HBM -> ur = D u        ; U <- u, R <- ur
+//   F2  j-pencils (i=a,k=b): v = U[k][:][i]  -> us = D v        ; S <- us
+//   F3  k-pencils (i=a,j=b): v = U[:][j][i]  -> ut = D v (regs)
+//   G   k-pencils: G from HBM, R,S,ut -> gr,gs (R,S in place), gt (regs)
+//   B3  k-pencils: wt = D^T gt                                  ; U <- wt
+//   B2  j-pencils: ws = D^T S[k][:][i] + U[k][:][i]              ; U <- ws+wt
+//   B1  i-pencils: w  = D^T R[k][j][:] + U[k][j][:]  -> epilogue -> HBM
+// Shared traffic: 15 accesses of 8 B per point; HBM: u 8 + G 48 + w 8 B.
+#pragma once
+#include "bk5_kernels.cuh"
+
+namespace nk {
+
+template <int NQ>
+struct PencilLayout {
+  // NQ = 8: swizzled, conflict-free for the three access orientations.
+  // Other orders: padded rows (odd stride), a few residual conflicts.
+  static constexpr int R = (NQ == 8) ? 8 : ((NQ % 2 == 0) ? NQ + 1 : NQ);
+  static constexpr int P = (NQ == 8) ? 72 : (NQ * R + ((NQ * R) % 2 == 0 ? 1 : 0));
+  static constexpr int VOL = NQ * P;
+  __device__ __forceinline__ static int idx(int k, int j, int i) {
+    if (NQ == 8) return k * P + j * R + (i ^ ((j >> 1) | ((k & 1) << 2)));
+    return k * P + j * R + i;
+  }
+};
+
+template <int NQ, int EPB_, int MINB_>
+struct PencilCfg {
+  static constexpr int NQ2 = NQ * NQ, NQ3 = NQ * NQ * NQ;
+  static constexpr int EPB = EPB_;
+  static constexpr int THREADS = EPB * NQ2;
+  static constexpr int MINB = MINB_;
+  static constexpr int VOL = PencilLayout<NQ>::VOL;
+  static size_t smem_bytes() { return sizeof(double) * ((size_t)EPB * 3 * VOL + 32); }
+};
+
+// out[q] = sum_m D[q][m] v[m]   (TRANS: sum_m D[m][q] v[m])
+template <int NQ, bool TRANS>
+__device__ __forceinline__ void matvec(const DParam<NQ>& D, const double (&v)[NQ],
+                                       double (&out)[NQ]) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) acc = fma(TRANS ? D.d[m * NQ + q] : D.d[q * NQ + m], v[m], acc);
+    out[q] = acc;
+  }
+}
+
+template <int NQ, int EPB, int MINB>
+__global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
+bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
+           const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
+           double lam0, const double* __restrict__ B, double lam1,
+           const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
+           int64_t part_base, int64_t reduce_count) {
+  using L = PencilLayout<NQ>;
+  constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, VOL = L::VOL;
+  extern __shared__ double smem[];
+  if (st != nullptr && st->done) return;
+
+  const int t = threadIdx.x;
+  const int le = t / NQ2;
+  const int tt = t - le * NQ2;
+  const int a = tt % NQ, b = tt / NQ;
+  double* red = smem;
+  double* U = smem + 32 + (size_t)le * 3 * VOL;
+  double* Rr = U + VOL;
+  double* Ss = Rr + VOL;
+
+  const int64_t slot = (int64_t)blockIdx.x * EPB + le;
+  const bool active = slot < nlist;
+  const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
+  const double* ue = u + e * NQ3;
+
+  // ---- F1: i-pencils (j = a, k = b)
+  if (active) {
+    double v[NQ], o[NQ];
+    const double* row = ue + b * NQ2 + a * NQ;
+    if (NQ % 2 == 0) {
+#pragma unroll
+      for (int m = 0; m < NQ; m += 2) {
+        const double2 p = __ldg(reinterpret_cast<const double2*>(row + m));
+        v[m] = p.x;
+        v[m + 1] = p.y;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = __ldg(row + m);
+    }
+    matvec<NQ, false>(D, v, o);
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      U[L::idx(b, a, i)] = v[i];
+      Rr[L::idx(b, a, i)] = o[i];
+    }
+  }
+  __syncthreads();
+  // ---- F2: j-pencils (i = a, k = b) -> us ; F3: k-pencils (i = a, j = b) -> ut
+  double ut[NQ];
+  if (active) {
+    double v[NQ], o[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) v[m] = U[L::idx(b, m, a)];
+    matvec<NQ, false>(D, v, o);
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) v[m] = U[L::idx(m, b, a)];
+    matvec<NQ, false>(D, v, ut);
+  }
+  __syncthreads();
+  // ---- G: k-pencils (i = a, j = b): pointwise 3x3 symmetric multiply
+  double gt[NQ];
+  if (active) {
+    const double* gp = G + e * 6 * NQ3 + b * NQ + a;
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const double g0 = __ldg(gp + 0 * NQ3 + k * NQ2);
+      const double g1 = __ldg(gp + 1 * NQ3 + k * NQ2);
+      const double g2 = __ldg(gp + 2 * NQ3 + k * NQ2);
+      const double g3 = __ldg(gp + 3 * NQ3 + k * NQ2);
+      const double g4 = __ldg(gp + 4 * NQ3 + k * NQ2);
+      const double g5 = __ldg(gp + 5 * NQ3 + k * NQ2);
+      const int q = L::idx(k, b, a);
+      const double ur = Rr[q], us = Ss[q];
+      Rr[q] = g0 * ur + g1 * us + g2 * ut[k];
+      Ss[q] = g1 * ur + g3 * us + g4 * ut[k];
+      gt[k] = g2 * ur + g4 * us + g5 * ut[k];
+    }
+    // ---- B3: wt = D^T gt  (k-pencil) -> U
+    double o[NQ];
+    matvec<NQ, true>(D, gt, o);
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) U[L::idx(k, b, a)] = o[k];
+  }
+  __syncthreads();
+  // ---- B2: j-pencils (i = a, k = b): U <- D^T gs + wt
+  if (active) {
+    double v[NQ], o[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) v[m] = Ss[L::idx(b, m, a)];
+    matvec<NQ, true>(D, v, o);
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int q = L::idx(b, j, a);
+      U[q] = o[j] + U[q];
+    }
+  }
+  __syncthreads();
+  // ---- B1: i-pencils (j = a, k = b): w = D^T gr + (ws + wt), epilogue
+  double dot = 0.0;
+  if (active) {
+    double v[NQ], o[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) v[m] = Rr[L::idx(b, a, m)];
+    matvec<NQ, true>(D, v, o);
+    const int64_t off = e * NQ3 + b * NQ2 + a * NQ;
+    double res[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) res[i] = lam0 * (o[i] + U[L::idx(b, a, i)]);
+    if (B != nullptr || st != nullptr) {
+      // u row again (L2-resident since F1) for lam1*B*u and the fused p.Ap
+      double ur[NQ];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) ur[i] = __ldg(ue + b * NQ2 + a * NQ + i);
+      if (B != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) res[i] = fma(lam1 * __ldg(B + off + i), ur[i], res[i]);
+      }
+      if (mask != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) dot = fma(ur[i], res[i], dot);
+    } else if (mask != nullptr) {
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+    }
+    double* wr = w + off;
+    if (NQ % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < NQ; i += 2)
+        *reinterpret_cast<double2*>(wr + i) = make_double2(res[i], res[i + 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) wr[i] = res[i];
+    }
+  }
+
+  if (st != nullptr) {
+    double vv[1] = {dot};
+    block_sum<1>(vv, red);
+    if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+    if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
+      double s[1];
+      reduce_partials<1>(partials, reduce_count, 0, s, red);
+      if (t == 0) st->pAp = s[0];
+    }
+  }
+}
+
+template <int NQ, int EPB, int MINB>
+static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhost,
+                         const double* G, const double* u, double* w, double lam0,
+                         const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
+                         double* partials, int64_t part_base, int64_t reduce_count,
+                         cudaStream_t s) {
+  using C = PencilCfg<NQ, EPB, MINB>;
+  const size_t smem = C::smem_bytes();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t err = cudaFuncSetAttribute(bk5_pencil<NQ, EPB, MINB>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) {
+      set_error("bk5_pencil: smem attribute (%zu B): %s", smem, cudaGetErrorString(err));
+      return NK_ERR_CUDA;
+    }
+    configured = true;
+  }
+  const int64_t nblk = (nlist + EPB - 1) / EPB;
+  if (nblk == 0) return NK_OK;
+  DParam<NQ> D;
+  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  bk5_pencil<NQ, EPB, MINB><<<(unsigned)nblk, C::THREADS, smem, s>>>(
+      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count);
+  return check_launch("bk5_pencil");
+}
+
+}  // namespace nk

@@ -65,7 +65,7 @@ def _bk5(u, mesh, lam0, lam1, ncomp, out=None, elements=None, mask=False, st=Non
     if u.numel() != nloc * ncomp:
         raise ContractError(f"contract error: field length {u.numel()} != {nloc * ncomp}")
     w = torch.empty_like(u) if out is None else out
-    D = mesh.basis.device_arrays(mesh.device)[0]
+    D = mesh.basis.diff  # host array: baked into the launch parameters
     nl = 0 if elements is None else int(elements.numel())
     check(lib().nk_bk5(mesh.N, mesh.E, ptr(D), ptr(mesh.G), ptr(u), ptr(w), float(lam0),
                        ptr(mesh.B) if lam1 != 0.0 else None, float(lam1), ncomp, nloc,

@@ -92,7 +92,7 @@ class PoissonOperator:
         stores p^T A p (the rank-local part) in st->pAp."""
         m = self.mesh
         L, s = lib(), stream_ptr()
-        D = m.basis.device_arrays(m.device)[0]
+        D = m.basis.diff  # host: passed by value to the kernel
         Bp = ptr(m.B) if self.lam1 != 0.0 else None
         g = self.gs
         multi = g.comm is not None and g.comm.size > 1

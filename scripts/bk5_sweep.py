@@ -1,0 +1,124 @@
+#!/usr/bin/env python
+"""BK5 tuning sweep (kernel shapes x L2-prefetch distance, and the N=3..15
+sweep of BASELINE configs[1]).  Prints one JSON line per measurement.
+
+    python scripts/bk5_sweep.py [--shapes] [--orders] [--reps 50]
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+# E per order at ~3M points
+E_FOR_N = {1: 96, 2: 64, 3: 48, 4: 36, 5: 29, 6: 24, 7: 20, 8: 18, 9: 16, 10: 14, 11: 13, 12: 12,
+           13: 11, 14: 10, 15: 10}
+
+
+def peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        return 6650.0
+
+
+def time_bk5(nk, L, mesh, reps, flush, check_ref=None):
+    import numpy as np
+    import torch
+    from paper_2104_05829_b200._lib import check, ptr
+    N, E, n = mesh.N, mesh.E, mesh.n_local
+    nq = N + 1
+    rng = np.random.default_rng(1000 + N)
+    u = torch.as_tensor(rng.standard_normal(n), device="cuda")
+    w = torch.empty_like(u)
+    D = mesh.basis.diff
+    s = torch.cuda.current_stream()
+    sp = s.cuda_stream
+
+    def run():
+        check(L.nk_bk5(N, E, ptr(D), ptr(mesh.G), ptr(u), ptr(w), 1.0, None, 0.0, 1, n, None,
+                       None, 0, None, None, 0, 0, sp), "bk5")
+
+    for _ in range(5):
+        L.nk_l2_flush(ptr(flush), flush.numel(), sp)
+        run()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        L.nk_l2_flush(ptr(flush), flush.numel(), sp)
+        a.record(s)
+        run()
+        b.record(s)
+        ts.append((a, b))
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in ts]
+    return statistics.median(ms), min(ms), w
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shapes", action="store_true")
+    ap.add_argument("--orders", action="store_true")
+    ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import torch
+    import paper_2104_05829_b200 as nk
+    from paper_2104_05829_b200 import _lib
+    L = _lib.lib()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    pk = peak()
+    out = open(args.out, "a") if args.out else None
+
+    def emit(d):
+        line = json.dumps(d)
+        print(line, flush=True)
+        if out:
+            out.write(line + "\n")
+            out.flush()
+
+    if args.shapes:
+        m = nk.build_box_mesh((1, 1, 1), (20, 20, 20), 7, deformation=("sine", 0.05))
+        ref = None
+        for variant, cfg, pf in [(v, c, 0) for v in (3, 1) for c in range(7)]:
+            if True:
+                L.nk_bk5_set_variant(variant)
+                L.nk_bk5_tune(cfg, pf)
+                med, best, w = time_bk5(nk, L, m, args.reps, flush)
+                same = None
+                if ref is None:
+                    ref = w.clone()
+                else:
+                    same = bool(torch.equal(ref, w))
+                bytes_ = 64 * m.n_local
+                emit({"sweep": "shape", "variant": variant, "N": 7, "cfg": cfg, "pf": pf, "ms_med": round(med, 5),
+                      "ms_best": round(best, 5), "GBs": round(bytes_ / med / 1e6, 1),
+                      "frac": round(bytes_ / med / 1e6 / pk, 4),
+                      "gdofs": round(m.E * 343 / med / 1e6, 3), "bitwise_same": same})
+        L.nk_bk5_tune(0, 0)
+        L.nk_bk5_set_variant(0)
+    if args.orders:
+        for N in range(1, 16):
+            ne = E_FOR_N[N]
+            m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
+            for variant in (3, 1):
+                pf = 0
+                L.nk_bk5_set_variant(variant)
+                L.nk_bk5_tune(0, pf)
+                med, best, _ = time_bk5(nk, L, m, args.reps, flush)
+                bytes_ = 64 * m.n_local
+                emit({"sweep": "order", "variant": variant, "N": N, "E": m.E, "ms_med": round(med, 5),
+                      "GBs": round(bytes_ / med / 1e6, 1), "frac": round(bytes_ / med / 1e6 / pk, 4),
+                      "gdofs": round(m.E * N ** 3 / med / 1e6, 3),
+                      "gflops": round(m.E * (12 * (N + 1) ** 4 + 15 * (N + 1) ** 3) / med / 1e6, 1)})
+            del m
+        L.nk_bk5_tune(0, 0)
+        L.nk_bk5_set_variant(0)
+
+
+if __name__ == "__main__":
+    main()
