@@ -82,6 +82,11 @@ int nk_device_info(int* sm_count, int64_t* l2_bytes, int* cc_major, int* cc_mino
 /* write `bytes` of `buf` [dev] (L2 flush between timed reps) */
 int nk_l2_flush(void* buf, int64_t bytes, nk_stream_t stream);
 
+/* diagnostic: BK5's HBM byte pattern without the arithmetic (read u and the
+ * six G factors of every element, write w); nq3 even. */
+int nk_bw_probe(int64_t nelem, int nq3, const double* u, const double* G, double* w,
+                int blocks_per_sm, nk_stream_t stream);
+
 /* ------------------------------------------------------------- geometry
  * build_box_mesh / geometric_factors on device.          */
 
@@ -138,10 +143,12 @@ int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double*
            nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
            nk_stream_t stream);
 int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
-/* kernel variant selection: 0 = auto (= 3), 1 = k-slab (2D thread plane,
- * k-column in registers, D in shared memory), 3 = pencil (register 1-D
- * contractions, D in the constant bank, swizzled shared transposes; ncomp=1;
- * ncomp=3 always uses k-slab).  Returns the previous value. */
+/* kernel variant selection: 0 = auto (4 for N = 7, else 3), 1 = k-slab (2D
+ * thread plane, k-column in registers, D in shared memory), 3 = pencil
+ * (register 1-D contractions, D in the constant bank, swizzled shared
+ * transposes), 4 = pencil-TMA (persistent CTAs, cp.async.bulk 2-stage ring;
+ * N+1 in {4, 6, 8}, else pencil).  Variants 3/4 serve ncomp = 1; ncomp = 3
+ * uses k-slab.  Returns the previous value. */
 int nk_bk5_set_variant(int variant);
 /* k-slab tuning: cfg selects the (elements per CTA, CTAs per SM) shape for
  * N = 7 (0 = default 4x2, 1 = 4x3, 2 = 2x4, 3 = 2x6, 4 = 1x8, 5 = 1x12,
@@ -163,6 +170,16 @@ int nk_local_diag(int N, int64_t nelem, const double* D, const double* G, double
  * st [nullable]: skip when st->done (PCG graph replays). */
 int nk_gs_op(int64_t nseg, const int32_t* seg_start, const int32_t* perm, double* w, int op,
              int ncomp, int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream);
+
+/* The same plan re-packed by multiplicity class (one launch for all
+ * classes, at most 16): class c has segment size sizes[c] [host] and
+ * nsegs[c] [host] segments whose members are members[c] [host array of dev
+ * pointers], member-major int32 (members[c][m * nsegs[c] + s]), members of a
+ * segment in canonical (ascending local index) order.  Bit-identical to
+ * nk_gs_op on the same map; independent index/value loads per segment. */
+int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t* nsegs,
+                     const int32_t* const* members, double* w, int op, int ncomp,
+                     int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream);
 
 /* Host-side plan construction (gs_setup for one rank):
  * stable counting sort of ids [host, n] by id; ids with multiplicity >= 2

@@ -54,6 +54,7 @@ _SIGS = {
     "nk_order_range": ([_P, _P], _I32),
     "nk_device_info": ([_P, _P, _P, _P], _I32),
     "nk_l2_flush": ([_P, _I64, _P], _I32),
+    "nk_bw_probe": ([_I64, _I32, _P, _P, _P, _I32, _P], _I32),
     "nk_box_coords": ([_I32, _I64, _P, _P, _P, _P, _I32, _D, _P, _P, _P], _I32),
     "nk_geom_factors": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "nk_box_ids": ([_I32, _I64, _P, _P, _P, _P, _P], _I32),
@@ -65,6 +66,7 @@ _SIGS = {
     "nk_bk5_tune": ([_I32, _I32], _I32),
     "nk_local_diag": ([_I32, _I64, _P, _P, _D, _P, _D, _P, _P], _I32),
     "nk_gs_op": ([_I64, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
+    "nk_gs_op_classes": ([_I32, _P, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
     "nk_gs_plan_build": ([_P, _I64, _P, _P, _P, _P], _I32),
     "nk_gather": ([_I64, _P, _P, _P, _P, _P], _I32),
     "nk_halo_combine": ([_I64, _P, _P, _P, _P, _P, _P, _I32, _P, _P], _I32),

@@ -36,7 +36,7 @@ using namespace nk;
 // tuning knobs (nk_bk5_tune): kslab shape index (N=7 only) and L2 prefetch
 // distance in blocks (-1 = one wave, 0 = off)
 static int g_cfg = 0;
-static int g_pf = 0;
+static int g_pf = 1;
 
 extern "C" int nk_bk5_tune(int cfg, int pf_dist) {
   g_cfg = cfg;
@@ -52,9 +52,12 @@ extern "C" int nk_bk5_bulk_launch(int N, int64_t nlist, const int32_t* elist, co
 extern "C" int nk_bk5_variant_get();
 
 static bool use_bulk(int N, int ncomp) { return nk_bk5_variant_get() == 2 && N == 7 && ncomp == 1; }
-static int kvariant() {
+// auto (0): pencil-TMA for N = 7 (measured best at the configs[1] size),
+// pencil for every other order (sweep6: TMA loses at N = 3, 5).
+static int kvariant_for(int N) {
   const int v = nk_bk5_variant_get();
-  return v == 1 ? 1 : 3;  // 0 (auto) -> pencil
+  if (v == 1 || v == 3 || v == 4) return v;
+  return N == 7 ? 4 : 3;
 }
 
 extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {
@@ -67,7 +70,7 @@ extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {
   if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) return -1;
   int64_t nb = -1;
   kslab_table[N](ncomp, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0, 0,
-                 nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, g_cfg, g_pf, kvariant());
+                 nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, g_cfg, g_pf, kvariant_for(N));
   return nb;
 }
 
@@ -106,7 +109,8 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
     return nk_bk5_bulk_launch(N, n, elem_list, D, G, u, w, lam0, B, lam1, mask, st, partials,
                               part_base, reduce_count, s, nullptr, 0);
   return kslab_table[N](ncomp, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, st,
-                        partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf, kvariant());
+                        partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf,
+                        kvariant_for(N));
 }
 
 extern "C" int nk_local_diag(int N, int64_t nelem, const double* D, const double* G, double lam0,

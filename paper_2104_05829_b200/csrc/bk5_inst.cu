@@ -1,6 +1,6 @@
 // One translation unit per order (compiled with -DNK_BK5_NQ=N+1) so the
 // heavily unrolled BK5 instantiations build in parallel.
-#include "bk5_pencil.cuh"
+#include "bk5_tma.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -54,22 +54,22 @@ template <int NQ, int EPB, int MINB>
 int runp(int64_t nlist, const int32_t* elist, const double* D, const double* G, const double* u,
          double* w, double lam0, const double* B, double lam1, const uint8_t* mask,
          nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
-         cudaStream_t s, int64_t* nblocks) {
+         cudaStream_t s, int64_t* nblocks, int pfG) {
   if (nblocks) {
     *nblocks = (nlist + EPB - 1) / EPB;
     return NK_OK;
   }
   return launch_pencil<NQ, EPB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
-                                      part_base, reduce_count, s);
+                                      part_base, reduce_count, s, pfG);
 }
 
 template <int NQ>
 int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, const double* G,
                const double* u, double* w, double lam0, const double* B, double lam1,
                const uint8_t* mask, nk_cg_state* st, double* partials, int64_t part_base,
-               int64_t reduce_count, cudaStream_t s, int64_t* nb) {
+               int64_t reduce_count, cudaStream_t s, int64_t* nb, int pfG) {
 #define NK_PARGS nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, \
-                 reduce_count, s, nb
+                 reduce_count, s, nb, pfG
   if constexpr (NQ == 8) {
     switch (cfg) {
       case 1: return runp<8, 4, 4>(NK_PARGS);
@@ -86,6 +86,19 @@ int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, co
     return runp<NQ, PencilDefault<NQ>::EPB, PencilDefault<NQ>::MINB>(NK_PARGS);
   }
 #undef NK_PARGS
+}
+
+template <int NQ, int MINB>
+int runt(int64_t nlist, const int32_t* elist, const double* D, const double* G, const double* u,
+         double* w, double lam0, const double* B, double lam1, const uint8_t* mask,
+         nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
+         cudaStream_t s, int64_t* nblocks) {
+  if (nblocks) {
+    *nblocks = tma_grid<NQ, MINB>(nlist);
+    return NK_OK;
+  }
+  return launch_pencil_tma<NQ, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                                     part_base, reduce_count, s);
 }
 
 template <int NQ, int NC>
@@ -120,9 +133,18 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
                                                  cudaStream_t s, int64_t* nblocks, int cfg,
                                                  int pf_dist, int variant) {
   constexpr int NQ = NK_BK5_NQ;
-  if (variant == 3 && ncomp == 1)
+  if constexpr (NQ == 4 || NQ == 6 || NQ == 8) {
+    if (variant == 4 && ncomp == 1) {
+#define NK_TARGS nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, \
+                 reduce_count, s, nblocks
+      if (NQ == 8 && cfg == 1) return runt<NQ, 2>(NK_TARGS);
+      return runt<NQ, NQ == 8 ? 3 : (NQ == 6 ? 6 : 8)>(NK_TARGS);
+#undef NK_TARGS
+    }
+  }
+  if ((variant == 3 || variant == 4) && ncomp == 1)
     return run_pencil<NQ>(cfg, nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
-                          part_base, reduce_count, s, nblocks);
+                          part_base, reduce_count, s, nblocks, pf_dist);
   if (ncomp == 1)
     return run_cfg<NQ, 1>(cfg, nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, st,
                           partials, part_base, reduce_count, s, nblocks, pf_dist);

@@ -70,7 +70,7 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
            const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
            double lam0, const double* __restrict__ B, double lam1,
            const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
-           int64_t part_base, int64_t reduce_count) {
+           int64_t part_base, int64_t reduce_count, int pfG) {
   using L = PencilLayout<NQ>;
   constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, VOL = L::VOL;
   extern __shared__ double smem[];
@@ -89,6 +89,9 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   const bool active = slot < nlist;
   const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
   const double* ue = u + e * NQ3;
+  // Start this element's G (75% of its bytes) streaming into L2 now, so the
+  // G-phase loads after F1-F3 hit L2 instead of waiting on HBM.
+  if (pfG && active && tt == 0) prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
 
   // ---- F1: i-pencils (j = a, k = b)
   if (active) {
@@ -223,7 +226,7 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
                          const double* G, const double* u, double* w, double lam0,
                          const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
                          double* partials, int64_t part_base, int64_t reduce_count,
-                         cudaStream_t s) {
+                         cudaStream_t s, int pfG) {
   using C = PencilCfg<NQ, EPB, MINB>;
   const size_t smem = C::smem_bytes();
   static bool configured = false;
@@ -241,7 +244,7 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
   DParam<NQ> D;
   for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
   bk5_pencil<NQ, EPB, MINB><<<(unsigned)nblk, C::THREADS, smem, s>>>(
-      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count);
+      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG);
   return check_launch("bk5_pencil");
 }
 

@@ -1,0 +1,265 @@
+// BK5 variant 4, "pencil-TMA": persistent CTAs; the element stream (u and the
+// six G factors, contiguous per element) is moved HBM -> shared memory by the
+// TMA engine (cp.async.bulk, SASS UBLKCP) into a 2-stage ring with mbarrier
+// transaction counts, so DRAM traffic for element e+2 is in flight while the
+// CTA computes element e+1 -- memory-level parallelism no longer depends on
+// registers or occupancy.  Compute is the pencil scheme of bk5_pencil.cuh
+// (register 1-D contractions, D in the constant bank, swizzled transposes),
+// reordered so the first pass reads u from the stage in the conflict-free
+// k-pencil orientation.
+//
+// Per element (NQ^2 threads; t = a + NQ*b):
+//   F3  k-pencils (i=a,j=b): u column from stage -> ut = D u (regs); U <- u
+//   F1  i-pencils (j=a,k=b): U row   -> ur -> R ;  F2 j-pencils: U col -> us -> S
+//   G   k-pencils: G from stage, R,S,ut -> gr,gs (in place), gt (regs); wt -> U
+//   B2  j-pencils: U += D^T gs ;  B1 i-pencils: w = D^T gr + U -> epilogue -> HBM
+// Requirements: NQ even (16-byte bulk-copy granularity of u and G).
+#pragma once
+#include "bk5_pencil.cuh"
+
+namespace nk {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NQ, int MINB>
+struct TmaCfg {
+  static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
+  static constexpr int THREADS = NQ2;
+  static constexpr int STAGE = 7 * NQ3;  // doubles: u then G[6]
+  static constexpr int VOL = PencilLayout<NQ>::VOL;
+  // layout (doubles): stage[2] | U R S | red[32] ; mbarriers after
+  static size_t smem_bytes() { return sizeof(double) * (2 * STAGE + 3 * VOL + 32) + 2 * 8; }
+};
+
+template <int NQ, int MINB>
+__global__ void __launch_bounds__(NQ * NQ, MINB)
+bk5_pencil_tma(int64_t nlist, const int32_t* __restrict__ elist,
+               const __grid_constant__ DParam<NQ> D, const double* __restrict__ G,
+               const double* __restrict__ u, double* __restrict__ w, double lam0,
+               const double* __restrict__ B, double lam1, const uint8_t* __restrict__ mask,
+               nk_cg_state* st, double* __restrict__ partials, int64_t part_base,
+               int64_t reduce_count) {
+  static_assert(NQ % 2 == 0, "bulk copies need 16-byte multiples");
+  using L = PencilLayout<NQ>;
+  using C = TmaCfg<NQ, MINB>;
+  constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL, STAGE = C::STAGE;
+  extern __shared__ __align__(128) double smem[];
+  if (st != nullptr && st->done) return;
+
+  double* stage0 = smem;
+  double* U = smem + 2 * STAGE;
+  double* Rr = U + VOL;
+  double* Ss = Rr + VOL;
+  double* red = Ss + VOL;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 32);
+
+  const int t = threadIdx.x;
+  const int a = t % NQ, b = t / NQ;
+  const int64_t stride = gridDim.x;
+  constexpr uint32_t UB = NQ3 * sizeof(double), GB = 6 * NQ3 * sizeof(double);
+
+  auto elem_of = [&](int64_t slot) -> int64_t { return elist ? (int64_t)elist[slot] : slot; };
+  auto issue = [&](int64_t slot, int s) {
+    const int64_t e = elem_of(slot);
+    double* dst = stage0 + s * STAGE;
+    mbar_expect_tx(&bar[s], UB + GB);
+    tma_load_1d(dst, u + e * NQ3, UB, &bar[s]);
+    tma_load_1d(dst + NQ3, G + e * 6 * NQ3, GB, &bar[s]);
+  };
+
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0) {
+    if ((int64_t)blockIdx.x < nlist) issue(blockIdx.x, 0);
+    if ((int64_t)blockIdx.x + stride < nlist) issue(blockIdx.x + stride, 1);
+  }
+
+  double dot = 0.0;
+  int it = 0;
+  for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++it) {
+    const int s = it & 1;
+    const double* su = stage0 + s * STAGE;
+    const double* sg = su + NQ3;
+    const int64_t e = elem_of(slot);
+    mbar_wait(&bar[s], (it >> 1) & 1);
+
+    // ---- F3: k-pencils (i = a, j = b) from the stage: ut in registers; U <- u
+    double ut[NQ];
+    {
+      double v[NQ];
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        v[k] = su[k * NQ2 + b * NQ + a];
+        U[L::idx(k, b, a)] = v[k];
+      }
+      matvec<NQ, false>(D, v, ut);
+    }
+    __syncthreads();
+    // ---- F1: i-pencils (j = a, k = b) -> R ; F2: j-pencils (i = a, k = b) -> S
+    {
+      double v[NQ], o[NQ];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = U[L::idx(b, a, m)];
+      matvec<NQ, false>(D, v, o);
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = U[L::idx(b, m, a)];
+      matvec<NQ, false>(D, v, o);
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+    }
+    __syncthreads();
+    // ---- G: k-pencils; then wt = D^T gt -> U (U's u copy is no longer read)
+    {
+      double gt[NQ];
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const int p = k * NQ2 + b * NQ + a;
+        const double g0 = sg[0 * NQ3 + p], g1 = sg[1 * NQ3 + p], g2 = sg[2 * NQ3 + p];
+        const double g3 = sg[3 * NQ3 + p], g4 = sg[4 * NQ3 + p], g5 = sg[5 * NQ3 + p];
+        const int q = L::idx(k, b, a);
+        const double ur = Rr[q], us = Ss[q];
+        Rr[q] = g0 * ur + g1 * us + g2 * ut[k];
+        Ss[q] = g1 * ur + g3 * us + g4 * ut[k];
+        gt[k] = g2 * ur + g4 * us + g5 * ut[k];
+      }
+      double o[NQ];
+      matvec<NQ, true>(D, gt, o);
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) U[L::idx(k, b, a)] = o[k];
+    }
+    __syncthreads();
+    // ---- B2: j-pencils: U <- D^T gs + wt
+    {
+      double v[NQ], o[NQ];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = Ss[L::idx(b, m, a)];
+      matvec<NQ, true>(D, v, o);
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        const int q = L::idx(b, j, a);
+        U[q] = o[j] + U[q];
+      }
+    }
+    __syncthreads();
+    // ---- B1: i-pencils (j = a, k = b): w = D^T gr + U, epilogue, store
+    {
+      double v[NQ], o[NQ];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = Rr[L::idx(b, a, m)];
+      matvec<NQ, true>(D, v, o);
+      const int64_t off = e * NQ3 + b * NQ2 + a * NQ;
+      const double* urow = su + b * NQ2 + a * NQ;
+      double res[NQ];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) res[i] = lam0 * (o[i] + U[L::idx(b, a, i)]);
+      if (B != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) res[i] = fma(lam1 * __ldg(B + off + i), urow[i], res[i]);
+      }
+      if (mask != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+      }
+      if (st != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) dot = fma(urow[i], res[i], dot);
+      }
+      double* wr = w + off;
+#pragma unroll
+      for (int i = 0; i < NQ; i += 2)
+        *reinterpret_cast<double2*>(wr + i) = make_double2(res[i], res[i + 1]);
+    }
+    __syncthreads();  // stage s and U/R/S free
+    if (t == 0 && slot + 2 * stride < nlist) issue(slot + 2 * stride, s);
+  }
+
+  if (st != nullptr) {
+    double vv[1] = {dot};
+    block_sum<1>(vv, red);
+    if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+    if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
+      double sres[1];
+      reduce_partials<1>(partials, reduce_count, 0, sres, red);
+      if (t == 0) st->pAp = sres[0];
+    }
+  }
+}
+
+// Grid: persistent, min(nlist, SMs * resident CTAs per SM).
+template <int NQ, int MINB>
+static int64_t tma_grid(int64_t nlist) {
+  static int64_t resident = -1;
+  if (resident < 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    using C = TmaCfg<NQ, MINB>;
+    cudaFuncSetAttribute(bk5_pencil_tma<NQ, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil_tma<NQ, MINB>, C::THREADS,
+                                                  C::smem_bytes());
+    resident = (int64_t)sms * (per > 0 ? per : 1);
+  }
+  return nlist < resident ? nlist : resident;
+}
+
+template <int NQ, int MINB>
+static int launch_pencil_tma(int64_t nlist, const int32_t* elist, const double* Dhost,
+                             const double* G, const double* u, double* w, double lam0,
+                             const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
+                             double* partials, int64_t part_base, int64_t reduce_count,
+                             cudaStream_t s) {
+  using C = TmaCfg<NQ, MINB>;
+  const int64_t grid = tma_grid<NQ, MINB>(nlist);
+  if (grid == 0) return NK_OK;
+  if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(G)) & 15) {
+    set_error("bk5_pencil_tma: u and G must be 16-byte aligned");
+    return NK_ERR_INVALID;
+  }
+  DParam<NQ> D;
+  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  bk5_pencil_tma<NQ, MINB><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
+      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count);
+  return check_launch("bk5_pencil_tma");
+}
+
+}  // namespace nk

@@ -75,7 +75,27 @@ __global__ void cg_init_finalize_kernel(nk_cg_state* st, double* hist) {
   if (st->max_iter <= 0) st->done = 1;
 }
 
-template <bool FLEX>
+// Elementwise part of the update for one point; accumulates rr, rz_new, zap.
+struct UpdAcc {
+  double rr = 0.0, rz = 0.0, zap = 0.0;
+};
+
+__device__ __forceinline__ void upd_point(double alpha, double& x, double& r, double p, double ap,
+                                          double invd, double wq, bool has_invd, UpdAcc& a) {
+  x = fma(alpha, p, x);
+  r = fma(-alpha, ap, r);
+  const double wr = wq * r;
+  a.rr = fma(wr, r, a.rr);
+  if (has_invd) {
+    const double z = invd * r;
+    a.rz = fma(wr, z, a.rz);
+    a.zap = fma(wq * z, ap, a.zap);
+  }
+}
+
+// VEC: 16-byte loads of two consecutive points (all vectors 16-B aligned),
+// two pairs in flight per thread per trip for memory-level parallelism.
+template <bool VEC>
 __global__ void __launch_bounds__(kVecThreads)
 cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                  const double* __restrict__ p, const double* __restrict__ Ap,
@@ -92,22 +112,33 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
     return;
   }
   const double alpha = st->rz / pAp;
-  double v[3] = {0.0, 0.0, 0.0};  // rr, rz_new, zap
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
-    const double pq = p[q], aq = Ap[q];
-    x[q] = fma(alpha, pq, x[q]);
-    const double rq = fma(-alpha, aq, r[q]);
-    r[q] = rq;
-    const double wq = wt ? wt[q] : 1.0;
-    const double wr = wq * rq;
-    v[0] = fma(wr, rq, v[0]);
-    if (invD) {
-      const double zq = invD[q] * rq;
-      v[1] = fma(wr, zq, v[1]);
-      if (FLEX) v[2] = fma(wq * zq, aq, v[2]);
+  const bool hz = invD != nullptr;
+  UpdAcc acc;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  if (VEC) {
+    const int64_t np = n >> 1;
+    for (int64_t q = gtid; q < np; q += nthr) {
+      double2 xv = reinterpret_cast<const double2*>(x)[q];
+      double2 rv = reinterpret_cast<const double2*>(r)[q];
+      const double2 pv = __ldg(reinterpret_cast<const double2*>(p) + q);
+      const double2 av = __ldg(reinterpret_cast<const double2*>(Ap) + q);
+      const double2 dv = hz ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
+      const double2 wv = wt ? __ldg(reinterpret_cast<const double2*>(wt) + q) : make_double2(1, 1);
+      upd_point(alpha, xv.x, rv.x, pv.x, av.x, dv.x, wv.x, hz, acc);
+      upd_point(alpha, xv.y, rv.y, pv.y, av.y, dv.y, wv.y, hz, acc);
+      reinterpret_cast<double2*>(x)[q] = xv;
+      reinterpret_cast<double2*>(r)[q] = rv;
     }
+    if ((n & 1) && gtid == 0) {
+      const int64_t q = n - 1;
+      upd_point(alpha, x[q], r[q], p[q], Ap[q], hz ? invD[q] : 0.0, wt ? wt[q] : 1.0, hz, acc);
+    }
+  } else {
+    for (int64_t q = gtid; q < n; q += nthr)
+      upd_point(alpha, x[q], r[q], p[q], Ap[q], hz ? invD[q] : 0.0, wt ? wt[q] : 1.0, hz, acc);
   }
+  double v[3] = {acc.rr, acc.rz, acc.zap};
   block_sum<3>(v, red);
   const int nb = gridDim.x;
   if (threadIdx.x == 0) {
@@ -120,13 +151,14 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
     reduce_partials<3>(partials, nb, kVecMaxBlocks, s, red);
     if (threadIdx.x == 0) {
       st->rr = s[0];
-      if (invD) st->rz_new = s[1];
+      if (hz) st->rz_new = s[1];
       st->zap = s[2];
       st->alpha = alpha;
     }
   }
 }
 
+template <bool VEC>
 __global__ void __launch_bounds__(kVecThreads)
 cg_pupdate_kernel(int64_t n, const double* __restrict__ r, double* __restrict__ p,
                   const double* __restrict__ invD, const double* __restrict__ z, nk_cg_state* st,
@@ -136,10 +168,35 @@ cg_pupdate_kernel(int64_t n, const double* __restrict__ r, double* __restrict__ 
   const double rz = st->rz;
   const double beta = st->flexible ? (-st->alpha * st->zap) / rz : st->rz_new / rz;
   if (!conv) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
-      const double zq = z ? z[q] : (invD ? invD[q] * r[q] : r[q]);
-      p[q] = fma(beta, p[q], zq);
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    if (VEC) {
+      const int64_t np = n >> 1;
+      for (int64_t q = gtid; q < np; q += nthr) {
+        double2 zv;
+        if (z) {
+          zv = __ldg(reinterpret_cast<const double2*>(z) + q);
+        } else {
+          const double2 rv = __ldg(reinterpret_cast<const double2*>(r) + q);
+          const double2 dv = invD ? __ldg(reinterpret_cast<const double2*>(invD) + q)
+                                  : make_double2(1.0, 1.0);
+          zv = make_double2(dv.x * rv.x, dv.y * rv.y);
+        }
+        double2 pv = reinterpret_cast<const double2*>(p)[q];
+        pv.x = fma(beta, pv.x, zv.x);
+        pv.y = fma(beta, pv.y, zv.y);
+        reinterpret_cast<double2*>(p)[q] = pv;
+      }
+      if ((n & 1) && gtid == 0) {
+        const int64_t q = n - 1;
+        const double zq = z ? z[q] : (invD ? invD[q] * r[q] : r[q]);
+        p[q] = fma(beta, p[q], zq);
+      }
+    } else {
+      for (int64_t q = gtid; q < n; q += nthr) {
+        const double zq = z ? z[q] : (invD ? invD[q] * r[q] : r[q]);
+        p[q] = fma(beta, p[q], zq);
+      }
     }
   }
   if (last_block(&st->ticket[2], gridDim.x)) {
@@ -184,6 +241,13 @@ wdot_final_kernel(int64_t nb, const double* __restrict__ partials, double* out) 
 
 using namespace nk;
 
+template <typename... T>
+static bool aligned16(const T*... ptrs) {
+  bool ok = true;
+  ((ok = ok && (reinterpret_cast<uintptr_t>(ptrs) & 15) == 0), ...);
+  return ok;
+}
+
 extern "C" int64_t nk_cg_partials_len(int64_t n) { return 3 * (int64_t)kVecMaxBlocks; }
 
 extern "C" int nk_cg_init(int64_t n, const double* b, double* x, double* r, double* p,
@@ -218,9 +282,10 @@ extern "C" int nk_cg_update(int64_t n, double* x, double* r, const double* p, co
   }
   const unsigned g = (unsigned)vec_grid(n);
   cudaStream_t s = S(stream);
-  // flexible is a runtime flag in st; the FLEX instantiation only adds the
-  // zap product, so always computing it when invD is given is cheap and safe.
-  cg_update_kernel<true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+  if (aligned16(x, r, p, Ap, invD, wt))
+    cg_update_kernel<true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+  else
+    cg_update_kernel<false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
   return check_launch("cg_update");
 }
 
@@ -230,8 +295,12 @@ extern "C" int nk_cg_pupdate(int64_t n, const double* r, double* p, const double
     set_error("cg_pupdate: invalid arguments");
     return NK_ERR_INVALID;
   }
-  cg_pupdate_kernel<<<(unsigned)vec_grid(n), kVecThreads, 0, S(stream)>>>(n, r, p, invD, z, st,
-                                                                          hist);
+  if (aligned16(r, p, invD, z))
+    cg_pupdate_kernel<true><<<(unsigned)vec_grid(n), kVecThreads, 0, S(stream)>>>(n, r, p, invD, z,
+                                                                                st, hist);
+  else
+    cg_pupdate_kernel<false><<<(unsigned)vec_grid(n), kVecThreads, 0, S(stream)>>>(n, r, p, invD,
+                                                                                 z, st, hist);
   return check_launch("cg_pupdate");
 }
 

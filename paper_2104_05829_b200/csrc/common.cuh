@@ -12,6 +12,7 @@
 
 #define NK_MIN_ORDER 1
 #define NK_MAX_ORDER 15
+#define NK_GS_MAX_CLASSES 16
 
 namespace nk {
 

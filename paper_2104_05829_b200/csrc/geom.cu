@@ -155,6 +155,30 @@ __global__ void l2_flush_kernel(int4* buf, int64_t n16, int v) {
     buf[q] = make_int4(v, v, v, v);
 }
 
+// Bandwidth probe with BK5's exact HBM pattern: per element read u (nq3) and
+// G (6 nq3), write w (nq3) -- no arithmetic beyond a sum.  The achievable
+// ceiling for the BK5 byte mix, measured the same way as BK5.
+__global__ void __launch_bounds__(256) bw_probe_kernel(int64_t npts, int nq3,
+                                                       const double2* __restrict__ u,
+                                                       const double2* __restrict__ G,
+                                                       double2* __restrict__ w) {
+  const int64_t n2 = npts / 2;
+  const int h = nq3 / 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n2; q += stride) {
+    const int64_t e = q / h, r = q - e * h;
+    double2 acc = __ldg(u + q);
+    const double2* g = G + e * 6 * h + r;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const double2 v = __ldg(g + c * h);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    w[q] = acc;
+  }
+}
+
 static BoxDesc make_desc(const int32_t* counts, const double* extent, const double* origin) {
   BoxDesc d;
   d.nx = counts[0];
@@ -239,6 +263,18 @@ extern "C" int nk_box_mask(int N, int64_t nelem, const int64_t* elem_index, cons
   box_mask_kernel<<<blocks_for(n), 256, 0, S(stream)>>>(
       N, nelem, elem_index, make_desc(counts, nullptr, nullptr), dm, mask);
   return check_launch("box_mask");
+}
+
+extern "C" int nk_bw_probe(int64_t nelem, int nq3, const double* u, const double* G, double* w,
+                           int blocks_per_sm, nk_stream_t stream) {
+  if (nelem < 0 || nq3 % 2 || !u || !G || !w) {
+    set_error("bw_probe: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  const int bps = blocks_per_sm > 0 ? blocks_per_sm : 8;
+  bw_probe_kernel<<<148 * bps, 256, 0, S(stream)>>>(nelem * nq3, nq3, (const double2*)u,
+                                                     (const double2*)G, (double2*)w);
+  return check_launch("bw_probe");
 }
 
 extern "C" int nk_l2_flush(void* buf, int64_t bytes, nk_stream_t stream) {

@@ -65,6 +65,68 @@ __global__ void halo_combine_kernel(int64_t nh, const int32_t* __restrict__ src_
   }
 }
 
+// Multiplicity classes: the same plan re-packed so every segment of a class
+// has M members stored member-major (members[m * nseg + s]); one thread per
+// segment issues its M index loads and M value loads independently (no
+// seg_start -> perm -> w dependency chain), then folds them in canonical
+// order -- bit-identical to gs_segments.
+struct GsClasses {
+  int n;
+  int M[NK_GS_MAX_CLASSES];
+  int64_t nseg[NK_GS_MAX_CLASSES];
+  const int32_t* mem[NK_GS_MAX_CLASSES];
+  int64_t bstart[NK_GS_MAX_CLASSES + 1];
+};
+
+template <int M, int OP>
+__device__ __forceinline__ void fold_fixed(const int32_t* __restrict__ mem, int64_t ns, int64_t s,
+                                           double* __restrict__ w, int ncomp, int64_t cs) {
+  int idx[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) idx[m] = __ldg(mem + m * ns + s);
+  for (int c = 0; c < ncomp; ++c) {
+    double* wc = w + c * cs;
+    double v[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = wc[idx[m]];
+    double acc = v[0];
+#pragma unroll
+    for (int m = 1; m < M; ++m) acc = fold<OP>(acc, v[m]);
+#pragma unroll
+    for (int m = 0; m < M; ++m) wc[idx[m]] = acc;
+  }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256)
+gs_classes_kernel(const __grid_constant__ GsClasses C, double* __restrict__ w, int ncomp,
+                  int64_t cs, const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  const int64_t b = blockIdx.x;
+  int c = 0;
+  while (c + 1 < C.n && b >= C.bstart[c + 1]) ++c;
+  const int64_t s = (b - C.bstart[c]) * blockDim.x + threadIdx.x;
+  const int64_t ns = C.nseg[c];
+  if (s >= ns) return;
+  const int32_t* mem = C.mem[c];
+  switch (C.M[c]) {
+    case 2: fold_fixed<2, OP>(mem, ns, s, w, ncomp, cs); return;
+    case 3: fold_fixed<3, OP>(mem, ns, s, w, ncomp, cs); return;
+    case 4: fold_fixed<4, OP>(mem, ns, s, w, ncomp, cs); return;
+    case 5: fold_fixed<5, OP>(mem, ns, s, w, ncomp, cs); return;
+    case 6: fold_fixed<6, OP>(mem, ns, s, w, ncomp, cs); return;
+    case 8: fold_fixed<8, OP>(mem, ns, s, w, ncomp, cs); return;
+    default: break;
+  }
+  const int M = C.M[c];
+  for (int cc = 0; cc < ncomp; ++cc) {
+    double* wc = w + cc * cs;
+    double acc = wc[__ldg(mem + s)];
+    for (int m = 1; m < M; ++m) acc = fold<OP>(acc, wc[__ldg(mem + m * ns + s)]);
+    for (int m = 0; m < M; ++m) wc[__ldg(mem + m * ns + s)] = acc;
+  }
+}
+
 static unsigned grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
@@ -96,6 +158,47 @@ extern "C" int nk_gs_op(int64_t nseg, const int32_t* seg_start, const int32_t* p
     default: set_error("gs_op: unknown op %d", op); return NK_ERR_INVALID;
   }
   return check_launch("gs_segments");
+}
+
+extern "C" int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t* nsegs,
+                                const int32_t* const* members, double* w, int op, int ncomp,
+                                int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream) {
+  if (nclass < 0 || nclass > NK_GS_MAX_CLASSES || (nclass > 0 && (!sizes || !nsegs || !members))) {
+    set_error("gs_op_classes: invalid class table (max %d classes)", NK_GS_MAX_CLASSES);
+    return NK_ERR_INVALID;
+  }
+  GsClasses C{};
+  int64_t blocks = 0;
+  int k = 0;
+  for (int c = 0; c < nclass; ++c) {
+    if (nsegs[c] <= 0) continue;
+    if (sizes[c] < 1 || !members[c]) {
+      set_error("gs_op_classes: class %d invalid", c);
+      return NK_ERR_INVALID;
+    }
+    C.M[k] = sizes[c];
+    C.nseg[k] = nsegs[c];
+    C.mem[k] = members[c];
+    C.bstart[k] = blocks;
+    blocks += (nsegs[c] + 255) / 256;
+    ++k;
+  }
+  C.n = k;
+  C.bstart[k] = blocks;
+  if (blocks == 0) return NK_OK;
+  if (!w) {
+    set_error("gs_op_classes: null field");
+    return NK_ERR_INVALID;
+  }
+  cudaStream_t s = S(stream);
+  switch (op) {
+    case NK_OP_ADD: gs_classes_kernel<NK_OP_ADD><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MUL: gs_classes_kernel<NK_OP_MUL><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MIN: gs_classes_kernel<NK_OP_MIN><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MAX: gs_classes_kernel<NK_OP_MAX><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    default: set_error("gs_op_classes: unknown op %d", op); return NK_ERR_INVALID;
+  }
+  return check_launch("gs_classes");
 }
 
 extern "C" int nk_gather(int64_t n, const int32_t* idx, const double* src, double* dst,

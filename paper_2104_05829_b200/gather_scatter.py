@@ -37,6 +37,56 @@ def _local_plan(ids_h):
     return perm[:npm].copy(), seg[:ns + 1].copy()
 
 
+MAX_CLASSES = 16
+
+
+class _Plan:
+    """A local gs plan on the device: segments grouped by multiplicity class
+    (member-major int32 arrays, nk_gs_op_classes) plus a CSR remainder when a
+    mesh has more than MAX_CLASSES distinct multiplicities (nk_gs_op).  Built
+    from the canonical CSR (perm, seg_start), so the fold order per segment
+    is unchanged."""
+
+    def __init__(self, perm, seg, device):
+        perm = np.asarray(perm, dtype=np.int64)
+        seg = np.asarray(seg, dtype=np.int64)
+        self.nseg = len(seg) - 1
+        sizes = np.diff(seg)
+        uniq = np.unique(sizes)
+        self._keep = []
+        cls_sizes, cls_n, ptrs = [], [], []
+        for M in uniq[:MAX_CLASSES]:
+            sel = np.flatnonzero(sizes == M)
+            mem = perm[seg[sel][:, None] + np.arange(M)[None, :]].T
+            t = _to_i32(np.ascontiguousarray(mem).ravel(), device)
+            self._keep.append(t)
+            cls_sizes.append(int(M))
+            cls_n.append(len(sel))
+            ptrs.append(t.data_ptr())
+        self.nclass = len(cls_sizes)
+        self.sizes = np.asarray(cls_sizes, dtype=np.int32)
+        self.nsegs = np.asarray(cls_n, dtype=np.int64)
+        self.ptrs = np.asarray(ptrs, dtype=np.uint64)
+        rest = np.flatnonzero(np.isin(sizes, uniq[MAX_CLASSES:]))
+        if len(rest):
+            cnt = sizes[rest]
+            idx = np.concatenate([perm[seg[r]:seg[r + 1]] for r in rest])
+            self.rest = (len(rest), _to_i32(np.r_[0, np.cumsum(cnt)], device), _to_i32(idx, device))
+        else:
+            self.rest = None
+
+    def run(self, w, op, ncomp, stride, st=None):
+        L, s = lib(), stream_ptr()
+        if self.nclass:
+            check(L.nk_gs_op_classes(self.nclass, ptr(self.sizes), ptr(self.nsegs), ptr(self.ptrs),
+                                     ptr(w), OP_CODES[op], ncomp, stride, ptr(st), s),
+                  "gs_op_classes")
+        if self.rest is not None:
+            n, seg, idx = self.rest
+            check(L.nk_gs_op(n, ptr(seg), ptr(idx), ptr(w), OP_CODES[op], ncomp, stride, ptr(st), s),
+                  "gs_op")
+
+
 class GatherScatterHandle:
     """Topology handle.  Not shareable across concurrent
     callers (SPEC.md:255)."""
@@ -54,9 +104,9 @@ class GatherScatterHandle:
         return self.nseg
 
     def plan_host(self):
-        """(perm, seg_start) as numpy int64 -- the integer map, for parity tests."""
-        return self.perm.cpu().numpy().astype(np.int64), self.seg_start.cpu().numpy().astype(
-            np.int64)
+        """(perm, seg_start) as numpy int64 -- the canonical integer map (the
+        device class plans are a re-packing of it), for parity tests."""
+        return self.perm_h.astype(np.int64), self.seg_h.astype(np.int64)
 
 
 def gs_setup(ids, comm=None, nq=None, device="cuda"):
@@ -74,8 +124,8 @@ def gs_setup(ids, comm=None, nq=None, device="cuda"):
     perm, seg = _local_plan(ids_h)
     h.nseg = len(seg) - 1
     h.nperm = len(perm)
-    h.perm = _to_i32(perm, device)
-    h.seg_start = _to_i32(seg, device)
+    h.perm_h, h.seg_h = perm, seg
+    h.plan = _Plan(perm, seg, device)
     if comm is not None and comm.size > 1:
         plan = _dist.build_halo_plan(ids_h, comm, nq=nq)
         h.comm, h.halo = comm, plan
@@ -122,10 +172,10 @@ def _sub_plan(perm, seg, keep, device):
     cnt = np.diff(seg)[keep]
     starts = seg[:-1][keep]
     if len(cnt) == 0:
-        return (0, None, None)
+        return _Plan(np.zeros(0, np.int64), np.zeros(1, np.int64), device)
     idx = np.concatenate([perm[a:a + c] for a, c in zip(starts, cnt)])
     s = np.r_[0, np.cumsum(cnt)]
-    return (len(cnt), _to_i32(s, device), _to_i32(idx, device))
+    return _Plan(idx, s, device)
 
 
 def _check_field(h, w, ncomp):
@@ -139,10 +189,7 @@ def _check_field(h, w, ncomp):
 
 
 def _local(h, w, op, ncomp, st=None, part=None):
-    nseg, seg, perm = part if part is not None else (h.nseg, h.seg_start, h.perm)
-    if nseg:
-        check(lib().nk_gs_op(nseg, ptr(seg), ptr(perm), ptr(w), OP_CODES[op], ncomp, h.n,
-                             ptr(st), stream_ptr()), "gs_op")
+    (part if part is not None else h.plan).run(w, op, ncomp, h.n, st)
 
 
 def _halo_start(h, w, st=None):

@@ -63,6 +63,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", action="store_true")
     ap.add_argument("--orders", action="store_true")
+    ap.add_argument("--probe", action="store_true")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
@@ -81,10 +82,55 @@ def main():
             out.write(line + "\n")
             out.flush()
 
+    if args.probe:
+        m = nk.build_box_mesh((1, 1, 1), (20, 20, 20), 7, deformation=("sine", 0.05))
+        u = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+        w = torch.empty_like(u)
+        s = torch.cuda.current_stream()
+        from paper_2104_05829_b200._lib import ptr
+        for bps in (2, 4, 8, 16, 32):
+            ts = []
+            for rep in range(args.reps + 5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                L.nk_l2_flush(ptr(flush), flush.numel(), s.cuda_stream)
+                a.record(s)
+                L.nk_bw_probe(m.E, 512, ptr(u), ptr(m.G), ptr(w), bps, s.cuda_stream)
+                b.record(s)
+                ts.append((a, b))
+            torch.cuda.synchronize()
+            ms = statistics.median([a.elapsed_time(b) for a, b in ts[5:]])
+            bytes_ = 64 * m.n_local
+            emit({"sweep": "probe", "blocks_per_sm": bps, "ms_med": round(ms, 5),
+                  "GBs": round(bytes_ / ms / 1e6, 1), "frac": round(bytes_ / ms / 1e6 / pk, 4)})
+        # same probe on an 8x larger problem (40^3 elements)
+        m2 = nk.build_box_mesh((1, 1, 1), (40, 40, 40), 7, deformation=("sine", 0.05))
+        u2 = torch.zeros(m2.n_local, dtype=torch.float64, device="cuda")
+        w2 = torch.empty_like(u2)
+        for variant in (None, 3, 4):
+            ts = []
+            for rep in range(args.reps + 5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                if variant is None:
+                    L.nk_bw_probe(m2.E, 512, ptr(u2), ptr(m2.G), ptr(w2), 8, s.cuda_stream)
+                else:
+                    L.nk_bk5_set_variant(variant)
+                    L.nk_bk5(7, m2.E, ptr(m2.basis.diff), ptr(m2.G), ptr(u2), ptr(w2), 1.0, None,
+                             0.0, 1, m2.n_local, None, None, 0, None, None, 0, 0, s.cuda_stream)
+                b.record(s)
+                ts.append((a, b))
+            torch.cuda.synchronize()
+            ms = statistics.median([a.elapsed_time(b) for a, b in ts[5:]])
+            bytes_ = 64 * m2.n_local
+            emit({"sweep": "probe40", "kernel": "probe" if variant is None else f"bk5 v{variant}",
+                  "ms_med": round(ms, 5), "GBs": round(bytes_ / ms / 1e6, 1),
+                  "frac": round(bytes_ / ms / 1e6 / pk, 4)})
+        L.nk_bk5_set_variant(0)
+        del m2, u2, w2
     if args.shapes:
         m = nk.build_box_mesh((1, 1, 1), (20, 20, 20), 7, deformation=("sine", 0.05))
         ref = None
-        for variant, cfg, pf in [(v, c, 0) for v in (3, 1) for c in range(7)]:
+        for variant, cfg, pf in [(3, 0, 1), (3, 8, 1), (4, 0, 0), (4, 1, 0), (1, 4, 0)]:
             if True:
                 L.nk_bk5_set_variant(variant)
                 L.nk_bk5_tune(cfg, pf)
@@ -105,13 +151,12 @@ def main():
         for N in range(1, 16):
             ne = E_FOR_N[N]
             m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
-            for variant in (3, 1):
-                pf = 0
+            for variant, pf in ((3, 1), (4, 0)):
                 L.nk_bk5_set_variant(variant)
                 L.nk_bk5_tune(0, pf)
                 med, best, _ = time_bk5(nk, L, m, args.reps, flush)
                 bytes_ = 64 * m.n_local
-                emit({"sweep": "order", "variant": variant, "N": N, "E": m.E, "ms_med": round(med, 5),
+                emit({"sweep": "order", "variant": variant, "pf": pf, "N": N, "E": m.E, "ms_med": round(med, 5),
                       "GBs": round(bytes_ / med / 1e6, 1), "frac": round(bytes_ / med / 1e6 / pk, 4),
                       "gdofs": round(m.E * N ** 3 / med / 1e6, 3),
                       "gflops": round(m.E * (12 * (N + 1) ** 4 + 15 * (N + 1) ** 3) / med / 1e6, 1)})

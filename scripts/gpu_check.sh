@@ -1,12 +1,21 @@
+#!/bin/bash
+# One GPU session: tests, smoke, bench, ncu launch list, ncu full captures.
+# usage: bash scripts/gpu_check.sh <tag> [skip-tests]
+TAG=${1:-run}
 mkdir -p gpurun_out
-set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
-python -c "import torch;print(torch.cuda.get_device_properties(0))"
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -40 > gpurun_out/pytest_gpu.log
-cat gpurun_out/pytest_gpu.log | tail -15
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
-timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench1.json 2> gpurun_out/bench1.err; tail -3 gpurun_out/bench1.err; cat gpurun_out/bench1.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches1.csv python bench.py --steps 3 --warmup 3 --no-cpu > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:bk5 -s 3 -c 1 -o gpurun_out/bk5_full1 python bench.py --steps 2 --warmup 3 --no-bp5 --no-cpu > gpurun_out/ncu_full1.log 2>&1
-tail -3 gpurun_out/ncu_full1.log
-ls -la gpurun_out
+if [ "$2" != "skip-tests" ]; then
+  timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -40 > gpurun_out/pytest_gpu_$TAG.log
+  tail -3 gpurun_out/pytest_gpu_$TAG.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+fi
+timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+tail -3 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+  --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 5 --warmup 3 --no-cpu > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:bk5_ -s 3 -c 1 \
+  -o gpurun_out/bk5_full_$TAG python bench.py --steps 2 --warmup 3 --no-bp5 --no-cpu > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gs_segments|cg_update|cg_pupdate" -s 30 -c 3 \
+  -o gpurun_out/cg_full_$TAG python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_cg_$TAG.log 2>&1
+tail -2 gpurun_out/ncu_full_$TAG.log gpurun_out/ncu_cg_$TAG.log
+ls gpurun_out

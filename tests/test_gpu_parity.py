@@ -283,3 +283,45 @@ def test_native_library_loaded():
     mi = np.zeros(1, np.int32)
     _lib.check(L.nk_device_info(sm.ctypes.data, l2.ctypes.data, mj.ctypes.data, mi.ctypes.data))
     assert mj[0] >= 10
+
+
+# ---------------------------------------------------------------- kernel variants
+@pytest.fixture
+def variant_guard():
+    L = _lib.lib()
+    old = L.nk_bk5_set_variant(0)
+    yield L
+    L.nk_bk5_set_variant(old)
+    L.nk_bk5_tune(0, 1)
+
+
+@pytest.mark.parametrize("variant", [1, 3, 4])
+@pytest.mark.parametrize("N", [3, 5, 7])
+def test_bk5_variants_match_oracle(variant_guard, variant, N):
+    """k-slab (1), pencil (3) and pencil-TMA (4, even N+1; others fall back)
+    all within the 1e-12 bar, incl. element subsets, mask and the fused p.Ap."""
+    L = variant_guard
+    L.nk_bk5_set_variant(variant)
+    m, o = both_meshes((5, 4, 3), N)
+    rng = np.random.default_rng(77 + N)
+    u = rng.standard_normal((m.E, N + 1, N + 1, N + 1))
+    w = nk.apply_stiffness_local(dev(u), m).cpu().numpy()
+    ref = oop.bk5(o.basis.diff, o.G, u)
+    assert rel_l2(w, ref) < BK5_TOL
+    sub = np.array([7, 0, 59, 31, 2], dtype=np.int32)
+    w2 = torch.zeros((m.E, N + 1, N + 1, N + 1), dtype=torch.float64, device="cuda")
+    nk.apply_stiffness_local(dev(u), m, out=w2, elements=dev(sub))
+    assert rel_l2(w2.cpu().numpy()[sub], ref[sub]) < BK5_TOL
+    # fused p.Ap via the PoissonOperator path (masked, assembled)
+    op = nk.PoissonOperator(m)
+    st = torch.zeros(_lib.CG_STATE_BYTES, dtype=torch.uint8, device="cuda")
+    part = torch.zeros(op.partials_len(), dtype=torch.float64, device="cuda")
+    p = dev(o.mask * ogs.gs_op(o.ids, u.ravel()).reshape(u.shape))
+    Ap = torch.empty_like(p)
+    op.apply(p, Ap, st=st, partials=part)
+    pAp = nk.solvers.read_state(st).pAp
+    pn = p.cpu().numpy().ravel()
+    ref_Ap = o.mask.ravel() * ogs.gs_op(o.ids, oop.bk5(o.basis.diff, o.G, pn.reshape(u.shape)).ravel())
+    assert rel_l2(Ap.cpu().numpy().ravel(), ref_Ap) < BK5_TOL
+    ref_pAp = float(np.sum(pn * ref_Ap / ogs.multiplicity(o.ids)))
+    assert abs(pAp - ref_pAp) < 1e-11 * abs(ref_pAp)
