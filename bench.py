@@ -307,6 +307,40 @@ def run_ours(args):
     e2e_ms = max_over_ranks(statistics.mean([a.elapsed_time(b) for a, b in e2e_ev]), ws)
     e2e_val = ws * dof / (e2e_ms * 1e-3) / 1e9
 
+    # ---- context for the roofline: the same HBM byte pattern without the
+    # arithmetic at this size (nk_bw_probe), and BK5 on an 8x larger box
+    ceiling = None
+    if not args.no_ceiling:
+        def per_launch_ms(fn, reps=50, flush_between=True):
+            evs = []
+            for i in range(reps + 5):
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                if flush_between:
+                    l2flush()
+                a_.record(stream)
+                fn()
+                b_.record(stream)
+                evs.append((a_, b_))
+            torch.cuda.synchronize()
+            return statistics.median([x.elapsed_time(y) for x, y in evs[5:]])
+
+        pms = per_launch_ms(lambda: check(L.nk_bw_probe(E, nq ** 3, ptr(u), ptr(mesh.G), ptr(w),
+                                                         16, sp), "probe"))
+        big = nk.build_box_mesh((1.0, 1.0, 1.0), (40, 40, 40), N, deformation=("sine", 0.05))
+        ub = torch.zeros(big.n_local, dtype=torch.float64, device="cuda")
+        wb = torch.empty_like(ub)
+        bms = per_launch_ms(lambda: check(L.nk_bk5(N, big.E, ptr(D), ptr(big.G), ptr(ub), ptr(wb),
+                                                   1.0, None, 0.0, 1, big.n_local, None, None, 0,
+                                                   None, None, 0, 0, sp), "bk5"),
+                            reps=20, flush_between=False)
+        ceiling = {"probe_same_size_frac": round(bytes_launch / (pms * 1e-3) / 1e9 / peak, 4),
+                   "probe": "nk_bw_probe: BK5's exact u+G read / w write pattern, no arithmetic, "
+                            "same E=8000, same timing (L2 flushed, events per launch)",
+                   "bk5_frac_of_probe": round(achieved / (bytes_launch / (pms * 1e-3) / 1e9), 4),
+                   "bk5_E40cubed_frac": round(64 * big.n_local / (bms * 1e-3) / 1e9 / peak, 4),
+                   "bk5_E40cubed_gdofs": round(big.E * N ** 3 / (bms * 1e-3) / 1e9, 2)}
+        del big, ub, wb
+
     # ---- BP5: fused Jacobi-PCG on the same mesh (fixed iteration count)
     bp5 = None
     if not args.no_bp5:
@@ -367,6 +401,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "path": "apply_stiffness_local(pinned host u -> device) -> host w"},
             "gpu_launches": launches,
+            "roofline_context": ceiling,
             "bp5": bp5,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
@@ -381,12 +416,13 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--order", type=int, default=N_ORDER)
     ap.add_argument("--no-bp5", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ceiling", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
