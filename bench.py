@@ -363,12 +363,19 @@ def run_ours(args):
         bp_ms = max_over_ranks(a_ev.elapsed_time(b_ev), ws)
         it = int(st.iter)
         per_it = bp_ms / max(it, 1)
-        bp_bytes = n * (64 + 1 + 64 + 32) + 20 * op.gs.nperm + 4 * op.gs.nseg
+        # fused schedule: nk_bk5_pcg 105 B + cg_update 40 B per point + gs
+        bp_bytes = n * (105 + 40) + 20 * op.gs.nperm + 4 * op.gs.nseg
+        solver.init(b_rhs)
+        for _ in range(2):                 # profile a steady-state iteration (iter > 0)
+            solver._iteration()
+        brk = solver.profile_iteration() if ws == 1 else None
         bp5 = {"gdof_per_s": round(ws * dof * it / (bp_ms * 1e-3) / 1e9, 3),
+               "breakdown_ms_in_situ": None if brk is None else {k: round(v, 4) for k, v in brk.items()},
                "iterations": it, "ms_per_iteration": round(per_it, 4),
                "roofline_frac": round(bp_bytes / (per_it * 1e-3) / 1e9 / peak, 3),
                "model_bytes_per_local_point": round(bp_bytes / n, 1),
-               "kernels_per_iteration": 4}
+               "kernels_per_iteration": solver.launches_per_iter,
+               "unfused_model_frac": round((n * 173 + 20 * op.gs.nperm) / (per_it * 1e-3) / 1e9 / peak, 3)}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None

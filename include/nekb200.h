@@ -156,6 +156,21 @@ int nk_bk5_set_variant(int variant);
  * resident CTAs ahead, 0 = off). */
 int nk_bk5_tune(int cfg, int pf_dist);
 
+/* Fused BP5 operator step (pcg iteration k = st->iter):
+ *   k > 0: stop if st->rr <= st->thresh2 or k >= max_iter (sets done,
+ *          converged, hist[k]); x += alpha_{k-1} p (deferred x update);
+ *          p = invD r + beta p  (Fletcher-Reeves, or flexible beta)
+ *   w = mask * (lam0 A_L p + lam1 B p); st->pAp = sum_L p w  (last block)
+ * p, x updated in place [dev].  Follow with gs(w) and nk_cg_update with
+ * x = NULL, p = NULL (which advances st->iter).  partials:
+ * nk_bk5_pcg_blocks(N, nlist) doubles per launch (offset part_base). */
+int nk_bk5_pcg(int N, int64_t nelem, const double* D, const double* G, double* p, double* w,
+               double lam0, const double* B, double lam1, const uint8_t* mask,
+               const int32_t* elem_list, int64_t nlist, double* x, const double* r,
+               const double* invD, nk_cg_state* st, double* partials, int64_t part_base,
+               int64_t reduce_count, double* hist, nk_stream_t stream);
+int64_t nk_bk5_pcg_blocks(int N, int64_t nlist);
+
 /* closed-form diag(lam0*A_e + lam1*B_e) per element (extract_diagonal
  * before assembly) */
 int nk_local_diag(int N, int64_t nelem, const double* D, const double* G, double lam0,
@@ -215,7 +230,9 @@ int nk_cg_init(int64_t n, const double* b, double* x, double* r, double* p,
 int nk_cg_init_finalize(nk_cg_state* st, double* hist, nk_stream_t stream);
 
 /* alpha = rz/pAp (breakdown if pAp <= 0); x += alpha p; r -= alpha Ap;
- * local sums rr, rz_new (z = invD r; skipped if invD NULL), zap into st. */
+ * local sums rr, rz_new (z = invD r; skipped if invD NULL), zap into st.
+ * x = p = NULL selects the fused-BP5 form (x update deferred to nk_bk5_pcg;
+ * advances st->iter). */
 int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap,
                  const double* invD, const double* wt, nk_cg_state* st, double* partials,
                  nk_stream_t stream);

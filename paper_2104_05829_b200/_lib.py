@@ -62,6 +62,9 @@ _SIGS = {
     "nk_bk5": ([_I32, _I64, _P, _P, _P, _P, _D, _P, _D, _I32, _I64, _P, _P, _I64, _P, _P,
                 _I64, _I64, _P], _I32),
     "nk_bk5_blocks": ([_I32, _I64, _I32], _I64),
+    "nk_bk5_pcg": ([_I32, _I64, _P, _P, _P, _P, _D, _P, _D, _P, _P, _I64, _P, _P, _P, _P, _P,
+                    _I64, _I64, _P, _P], _I32),
+    "nk_bk5_pcg_blocks": ([_I32, _I64], _I64),
     "nk_bk5_set_variant": ([_I32], _I32),
     "nk_bk5_tune": ([_I32, _I32], _I32),
     "nk_local_diag": ([_I32, _I64, _P, _P, _D, _P, _D, _P, _P], _I32),

@@ -17,6 +17,24 @@ typedef int (*diag_fn)(int64_t, const double*, const double*, double, const doub
                                      int64_t*, int, int, int);                                \
   extern "C" int nk_local_diag_nq##NQ(int64_t, const double*, const double*, double,         \
                                       const double*, double, double*, cudaStream_t);
+#define NK_DECLP(NQ)                                                                        \
+  extern "C" int nk_bk5_pcg_nq##NQ(int64_t, const int32_t*, const double*, const double*,  \
+                                   double*, double*, double, const double*, double,          \
+                                   const uint8_t*, double*, const double*, const double*,    \
+                                   nk_cg_state*, double*, int64_t, int64_t, double*,          \
+                                   cudaStream_t, int64_t*);
+NK_DECLP(2) NK_DECLP(3) NK_DECLP(4) NK_DECLP(5) NK_DECLP(6) NK_DECLP(7) NK_DECLP(8) NK_DECLP(9)
+NK_DECLP(10) NK_DECLP(11) NK_DECLP(12) NK_DECLP(13) NK_DECLP(14) NK_DECLP(15) NK_DECLP(16)
+typedef int (*pcg_fn)(int64_t, const int32_t*, const double*, const double*, double*, double*,
+                      double, const double*, double, const uint8_t*, double*, const double*,
+                      const double*, nk_cg_state*, double*, int64_t, int64_t, double*,
+                      cudaStream_t, int64_t*);
+static const pcg_fn pcg_table[16] = {
+    nullptr,          nk_bk5_pcg_nq2,  nk_bk5_pcg_nq3,  nk_bk5_pcg_nq4,  nk_bk5_pcg_nq5,
+    nk_bk5_pcg_nq6,   nk_bk5_pcg_nq7,  nk_bk5_pcg_nq8,  nk_bk5_pcg_nq9,  nk_bk5_pcg_nq10,
+    nk_bk5_pcg_nq11,  nk_bk5_pcg_nq12, nk_bk5_pcg_nq13, nk_bk5_pcg_nq14, nk_bk5_pcg_nq15,
+    nk_bk5_pcg_nq16};
+
 NK_DECL(2) NK_DECL(3) NK_DECL(4) NK_DECL(5) NK_DECL(6) NK_DECL(7) NK_DECL(8) NK_DECL(9)
 NK_DECL(10) NK_DECL(11) NK_DECL(12) NK_DECL(13) NK_DECL(14) NK_DECL(15) NK_DECL(16)
 
@@ -124,4 +142,35 @@ extern "C" int nk_local_diag(int N, int64_t nelem, const double* D, const double
     return NK_ERR_INVALID;
   }
   return diag_table[N](nelem, D, G, lam0, B, lam1, diag, S(stream));
+}
+
+extern "C" int64_t nk_bk5_pcg_blocks(int N, int64_t nlist) {
+  if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) return -1;
+  int64_t nb = -1;
+  pcg_table[N](nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0, nullptr,
+               nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr, nullptr, &nb);
+  return nb;
+}
+
+extern "C" int nk_bk5_pcg(int N, int64_t nelem, const double* D, const double* G, double* p,
+                          double* w, double lam0, const double* B, double lam1,
+                          const uint8_t* mask, const int32_t* elem_list, int64_t nlist,
+                          double* x, const double* r, const double* invD, nk_cg_state* st,
+                          double* partials, int64_t part_base, int64_t reduce_count,
+                          double* hist, nk_stream_t stream) {
+  if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) {
+    set_error("bk5_pcg: order N=%d outside compiled range", N);
+    return NK_ERR_UNSUPPORTED;
+  }
+  if (!D || !G || !p || !w || !x || !r || !invD || !st || !partials || nelem < 0) {
+    set_error("bk5_pcg: null operand");
+    return NK_ERR_INVALID;
+  }
+  if (B == nullptr && lam1 != 0.0) {
+    set_error("bk5_pcg: lam1 != 0 requires B");
+    return NK_ERR_INVALID;
+  }
+  const int64_t n = elem_list ? nlist : nelem;
+  return pcg_table[N](n, elem_list, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials,
+                      part_base, reduce_count, hist, S(stream), nullptr);
 }

@@ -1,6 +1,7 @@
 // One translation unit per order (compiled with -DNK_BK5_NQ=N+1) so the
 // heavily unrolled BK5 instantiations build in parallel.
 #include "bk5_tma.cuh"
+#include "bk5_pcg.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -9,6 +10,8 @@
 #define NK_CAT(a, b) NK_CAT2(a, b)
 
 using namespace nk;
+
+extern "C" int nk_bk5_variant_get();
 
 namespace {
 // pf_dist < 0: one wave ahead (resident CTAs on the device), 0: off.
@@ -161,4 +164,33 @@ extern "C" int NK_CAT(nk_local_diag_nq, NK_BK5_NQ)(int64_t nelem, const double* 
   local_diag_kernel<NQ><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nelem, D, G, lam0, B, lam1,
                                                                      diag);
   return check_launch("local_diag");
+}
+
+extern "C" int NK_CAT(nk_bk5_pcg_nq, NK_BK5_NQ)(int64_t nlist, const int32_t* elist,
+                                               const double* D, const double* G, double* p,
+                                               double* w, double lam0, const double* B,
+                                               double lam1, const uint8_t* mask, double* x,
+                                               const double* r, const double* invD,
+                                               nk_cg_state* st, double* partials,
+                                               int64_t part_base, int64_t reduce_count,
+                                               double* hist, cudaStream_t s, int64_t* nblocks) {
+  constexpr int NQ = NK_BK5_NQ;
+  constexpr int EPB = PencilDefault<NQ>::EPB;
+  constexpr int MINB = NQ == 8 ? 10 : PencilDefault<NQ>::MINB;  // ~100 regs at NQ = 8
+  if constexpr (NQ == 8) {
+    if (nk_bk5_variant_get() != 3) {  // auto / 4: TMA pipeline
+      if (nblocks) {
+        *nblocks = tma_pcg_grid<NQ, 2>(nlist);
+        return NK_OK;
+      }
+      return launch_pencil_tma_pcg<NQ, 2>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r,
+                                          invD, st, partials, part_base, reduce_count, hist, s);
+    }
+  }
+  if (nblocks) {
+    *nblocks = (nlist + EPB - 1) / EPB;
+    return NK_OK;
+  }
+  return launch_pencil_pcg<NQ, EPB, MINB>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r,
+                                          invD, st, partials, part_base, reduce_count, hist, s);
 }

@@ -263,3 +263,263 @@ static int launch_pencil_tma(int64_t nlist, const int32_t* elist, const double* 
 }
 
 }  // namespace nk
+
+namespace nk {
+
+// ---------------------------------------------------------------------------
+// Fused BP5 operator step on the TMA pipeline (see bk5_pcg.cuh for the math):
+// the stage carries p_{k-1}, r_k, invD and G of an element (9 NQ^3 doubles);
+// F3 (k-pencils, coalesced) forms p_k = invD r + beta p_{k-1}, writes it to HBM
+// and back into the stage, and applies the deferred x += alpha_{k-1} p_{k-1}
+// with x read/written directly (coalesced planes).  On the stop iteration only
+// the x update runs (no TMA traffic).
+template <int NQ, int MINB>
+struct TmaPcgCfg {
+  static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
+  static constexpr int THREADS = NQ2;
+  static constexpr int STAGE = 9 * NQ3;  // p, r, invD, G[6]
+  static constexpr int VOL = PencilLayout<NQ>::VOL;
+  static size_t smem_bytes() { return sizeof(double) * (2 * STAGE + 3 * VOL + 32) + 2 * 8; }
+};
+
+template <int NQ, int MINB>
+__global__ void __launch_bounds__(NQ * NQ, MINB)
+bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
+                   const __grid_constant__ DParam<NQ> D, const double* __restrict__ G,
+                   double* __restrict__ p, double* __restrict__ w, double lam0,
+                   const double* __restrict__ B, double lam1, const uint8_t* __restrict__ mask,
+                   double* __restrict__ x, const double* __restrict__ r,
+                   const double* __restrict__ invD, nk_cg_state* st,
+                   double* __restrict__ partials, int64_t part_base, int64_t reduce_count,
+                   double* __restrict__ hist) {
+  static_assert(NQ % 2 == 0, "bulk copies need 16-byte multiples");
+  using L = PencilLayout<NQ>;
+  using C = TmaPcgCfg<NQ, MINB>;
+  constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL, STAGE = C::STAGE;
+  extern __shared__ __align__(128) double smem[];
+  if (st->done) return;
+  const int it = st->iter;
+  const bool conv = it > 0 && st->rr <= st->thresh2;
+  const bool stop = it > 0 && (conv || it >= st->max_iter);
+  const double alpha_prev = st->alpha;
+  const double rz = st->rz;
+  const double beta =
+      it == 0 ? 0.0 : (st->flexible ? (-alpha_prev * st->zap) / rz : st->rz_new / rz);
+
+  double* stage0 = smem;
+  double* U = smem + 2 * STAGE;
+  double* Rr = U + VOL;
+  double* Ss = Rr + VOL;
+  double* red = Ss + VOL;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 32);
+
+  const int t = threadIdx.x;
+  const int a = t % NQ, b = t / NQ;
+  const int64_t stride = gridDim.x;
+  constexpr uint32_t UB = NQ3 * sizeof(double), GB = 6 * NQ3 * sizeof(double);
+  auto elem_of = [&](int64_t slot) -> int64_t { return elist ? (int64_t)elist[slot] : slot; };
+  double dot = 0.0;
+
+  if (stop) {  // final deferred x update only
+    for (int64_t slot = blockIdx.x; slot < nlist; slot += stride) {
+      const int64_t e = elem_of(slot);
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const int64_t q = e * NQ3 + k * NQ2 + t;
+        x[q] = fma(alpha_prev, p[q], x[q]);
+      }
+    }
+  } else {
+    auto issue = [&](int64_t slot, int s) {
+      const int64_t e = elem_of(slot);
+      double* dst = stage0 + s * STAGE;
+      mbar_expect_tx(&bar[s], (it > 0 ? 3 * UB : UB) + GB);
+      tma_load_1d(dst, p + e * NQ3, UB, &bar[s]);
+      if (it > 0) {
+        tma_load_1d(dst + NQ3, r + e * NQ3, UB, &bar[s]);
+        tma_load_1d(dst + 2 * NQ3, invD + e * NQ3, UB, &bar[s]);
+      }
+      tma_load_1d(dst + 3 * NQ3, G + e * 6 * NQ3, GB, &bar[s]);
+    };
+    if (t == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+      if ((int64_t)blockIdx.x < nlist) issue(blockIdx.x, 0);
+      if ((int64_t)blockIdx.x + stride < nlist) issue(blockIdx.x + stride, 1);
+    }
+    int itl = 0;
+    for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++itl) {
+      const int s = itl & 1;
+      double* su = stage0 + s * STAGE;
+      const double* sr = su + NQ3;
+      const double* sd = su + 2 * NQ3;
+      const double* sg = su + 3 * NQ3;
+      const int64_t e = elem_of(slot);
+      // x for the deferred update: issued before the barrier wait
+      double xv[NQ];
+      if (it > 0) {
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) xv[k] = x[e * NQ3 + k * NQ2 + t];
+      }
+      mbar_wait(&bar[s], (itl >> 1) & 1);
+
+      // ---- F3 + prologue: k-pencils (i = a, j = b)
+      double ut[NQ];
+      {
+        double v[NQ];
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          const int pp = k * NQ2 + t;
+          double pv = su[pp];
+          if (it > 0) {
+            x[e * NQ3 + pp] = fma(alpha_prev, pv, xv[k]);
+            pv = fma(beta, pv, sd[pp] * sr[pp]);
+            p[e * NQ3 + pp] = pv;
+            su[pp] = pv;
+          }
+          v[k] = pv;
+          U[L::idx(k, b, a)] = pv;
+        }
+        matvec<NQ, false>(D, v, ut);
+      }
+      __syncthreads();
+      {  // F1 (i-pencils) -> R ; F2 (j-pencils) -> S
+        double v[NQ], o[NQ];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) v[m] = U[L::idx(b, a, m)];
+        matvec<NQ, false>(D, v, o);
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) v[m] = U[L::idx(b, m, a)];
+        matvec<NQ, false>(D, v, o);
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+      }
+      __syncthreads();
+      {  // G (k-pencils), wt -> U
+        double gt[NQ];
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          const int pp = k * NQ2 + t;
+          const double g0 = sg[0 * NQ3 + pp], g1 = sg[1 * NQ3 + pp], g2 = sg[2 * NQ3 + pp];
+          const double g3 = sg[3 * NQ3 + pp], g4 = sg[4 * NQ3 + pp], g5 = sg[5 * NQ3 + pp];
+          const int q = L::idx(k, b, a);
+          const double ur = Rr[q], us = Ss[q];
+          Rr[q] = g0 * ur + g1 * us + g2 * ut[k];
+          Ss[q] = g1 * ur + g3 * us + g4 * ut[k];
+          gt[k] = g2 * ur + g4 * us + g5 * ut[k];
+        }
+        double o[NQ];
+        matvec<NQ, true>(D, gt, o);
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) U[L::idx(k, b, a)] = o[k];
+      }
+      __syncthreads();
+      {  // B2 (j-pencils)
+        double v[NQ], o[NQ];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) v[m] = Ss[L::idx(b, m, a)];
+        matvec<NQ, true>(D, v, o);
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          const int q = L::idx(b, j, a);
+          U[q] = o[j] + U[q];
+        }
+      }
+      __syncthreads();
+      {  // B1 (i-pencils) + epilogue
+        double v[NQ], o[NQ];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) v[m] = Rr[L::idx(b, a, m)];
+        matvec<NQ, true>(D, v, o);
+        const int64_t off = e * NQ3 + b * NQ2 + a * NQ;
+        const double* prow = su + b * NQ2 + a * NQ;
+        double res[NQ];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+          double vv = lam0 * (o[i] + U[L::idx(b, a, i)]);
+          if (B != nullptr) vv = fma(lam1 * __ldg(B + off + i), prow[i], vv);
+          if (mask != nullptr) vv = mask[off + i] ? vv : 0.0;
+          res[i] = vv;
+          dot = fma(prow[i], vv, dot);
+        }
+        double* wr = w + off;
+#pragma unroll
+        for (int i = 0; i < NQ; i += 2)
+          *reinterpret_cast<double2*>(wr + i) = make_double2(res[i], res[i + 1]);
+      }
+      __syncthreads();
+      if (t == 0 && slot + 2 * stride < nlist) {
+        // the stage was written through the generic proxy (p_k); order those
+        // writes before the async-proxy (TMA) refill of the same bytes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(slot + 2 * stride, s);
+      }
+    }
+  }
+
+  double vv[1] = {dot};
+  block_sum<1>(vv, red);
+  if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+  if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
+    double sres[1];
+    reduce_partials<1>(partials, reduce_count, 0, sres, red);
+    if (t == 0) {
+      if (it > 0 && hist) hist[it] = sqrt(st->rr);
+      if (stop) {
+        st->converged = conv ? 1 : 0;
+        st->done = 1;
+      } else {
+        st->pAp = sres[0];
+        if (it > 0) st->rz = st->rz_new;
+      }
+    }
+  }
+}
+
+template <int NQ, int MINB>
+static int64_t tma_pcg_grid(int64_t nlist) {
+  static int64_t resident = -1;
+  if (resident < 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    using C = TmaPcgCfg<NQ, MINB>;
+    cudaFuncSetAttribute(bk5_pencil_tma_pcg<NQ, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil_tma_pcg<NQ, MINB>, C::THREADS,
+                                                  C::smem_bytes());
+    resident = (int64_t)sms * (per > 0 ? per : 1);
+  }
+  return nlist < resident ? nlist : resident;
+}
+
+template <int NQ, int MINB>
+static int launch_pencil_tma_pcg(int64_t nlist, const int32_t* elist, const double* Dhost,
+                                 const double* G, double* p, double* w, double lam0,
+                                 const double* B, double lam1, const uint8_t* mask, double* x,
+                                 const double* r, const double* invD, nk_cg_state* st,
+                                 double* partials, int64_t part_base, int64_t reduce_count,
+                                 double* hist, cudaStream_t s) {
+  using C = TmaPcgCfg<NQ, MINB>;
+  const int64_t grid = tma_pcg_grid<NQ, MINB>(nlist);
+  if (grid == 0) return NK_OK;
+  if ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(r) |
+       reinterpret_cast<uintptr_t>(invD) | reinterpret_cast<uintptr_t>(G)) & 15) {
+    set_error("bk5_pencil_tma_pcg: p, r, invD, G must be 16-byte aligned");
+    return NK_ERR_INVALID;
+  }
+  DParam<NQ> D;
+  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  bk5_pencil_tma_pcg<NQ, MINB><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
+      nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base,
+      reduce_count, hist);
+  return check_launch("bk5_pencil_tma_pcg");
+}
+
+}  // namespace nk

@@ -80,9 +80,10 @@ struct UpdAcc {
   double rr = 0.0, rz = 0.0, zap = 0.0;
 };
 
+template <bool FUSED>
 __device__ __forceinline__ void upd_point(double alpha, double& x, double& r, double p, double ap,
                                           double invd, double wq, bool has_invd, UpdAcc& a) {
-  x = fma(alpha, p, x);
+  if (!FUSED) x = fma(alpha, p, x);
   r = fma(-alpha, ap, r);
   const double wr = wq * r;
   a.rr = fma(wr, r, a.rr);
@@ -95,7 +96,10 @@ __device__ __forceinline__ void upd_point(double alpha, double& x, double& r, do
 
 // VEC: 16-byte loads of two consecutive points (all vectors 16-B aligned),
 // two pairs in flight per thread per trip for memory-level parallelism.
-template <bool VEC>
+// FUSED (BP5 fused path): x and p are not touched -- the deferred x update
+// and the p update live in bk5_pencil_pcg -- and the iteration counter is
+// advanced here.
+template <bool VEC, bool FUSED>
 __global__ void __launch_bounds__(kVecThreads)
 cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                  const double* __restrict__ p, const double* __restrict__ Ap,
@@ -116,27 +120,38 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
   UpdAcc acc;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  auto pair = [&](int64_t q) {
+    double2 xv = FUSED ? make_double2(0, 0) : reinterpret_cast<const double2*>(x)[q];
+    double2 rv = reinterpret_cast<const double2*>(r)[q];
+    const double2 pv = FUSED ? make_double2(0, 0) : __ldg(reinterpret_cast<const double2*>(p) + q);
+    const double2 av = __ldg(reinterpret_cast<const double2*>(Ap) + q);
+    const double2 dv = hz ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
+    const double2 wv = wt ? __ldg(reinterpret_cast<const double2*>(wt) + q) : make_double2(1, 1);
+    upd_point<FUSED>(alpha, xv.x, rv.x, pv.x, av.x, dv.x, wv.x, hz, acc);
+    upd_point<FUSED>(alpha, xv.y, rv.y, pv.y, av.y, dv.y, wv.y, hz, acc);
+    if (!FUSED) reinterpret_cast<double2*>(x)[q] = xv;
+    reinterpret_cast<double2*>(r)[q] = rv;
+  };
   if (VEC) {
     const int64_t np = n >> 1;
-    for (int64_t q = gtid; q < np; q += nthr) {
-      double2 xv = reinterpret_cast<const double2*>(x)[q];
-      double2 rv = reinterpret_cast<const double2*>(r)[q];
-      const double2 pv = __ldg(reinterpret_cast<const double2*>(p) + q);
-      const double2 av = __ldg(reinterpret_cast<const double2*>(Ap) + q);
-      const double2 dv = hz ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
-      const double2 wv = wt ? __ldg(reinterpret_cast<const double2*>(wt) + q) : make_double2(1, 1);
-      upd_point(alpha, xv.x, rv.x, pv.x, av.x, dv.x, wv.x, hz, acc);
-      upd_point(alpha, xv.y, rv.y, pv.y, av.y, dv.y, wv.y, hz, acc);
-      reinterpret_cast<double2*>(x)[q] = xv;
-      reinterpret_cast<double2*>(r)[q] = rv;
+    int64_t q = gtid;
+    for (; q + nthr < np; q += 2 * nthr) {  // two independent pairs per trip
+      pair(q);
+      pair(q + nthr);
     }
+    if (q < np) pair(q);
     if ((n & 1) && gtid == 0) {
-      const int64_t q = n - 1;
-      upd_point(alpha, x[q], r[q], p[q], Ap[q], hz ? invD[q] : 0.0, wt ? wt[q] : 1.0, hz, acc);
+      const int64_t t = n - 1;
+      double xd = 0.0;
+      upd_point<FUSED>(alpha, FUSED ? xd : x[t], r[t], FUSED ? 0.0 : p[t], Ap[t],
+                       hz ? invD[t] : 0.0, wt ? wt[t] : 1.0, hz, acc);
     }
   } else {
-    for (int64_t q = gtid; q < n; q += nthr)
-      upd_point(alpha, x[q], r[q], p[q], Ap[q], hz ? invD[q] : 0.0, wt ? wt[q] : 1.0, hz, acc);
+    for (int64_t q = gtid; q < n; q += nthr) {
+      double xd = 0.0;
+      upd_point<FUSED>(alpha, FUSED ? xd : x[q], r[q], FUSED ? 0.0 : p[q], Ap[q],
+                       hz ? invD[q] : 0.0, wt ? wt[q] : 1.0, hz, acc);
+    }
   }
   double v[3] = {acc.rr, acc.rz, acc.zap};
   block_sum<3>(v, red);
@@ -154,6 +169,7 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
       if (hz) st->rz_new = s[1];
       st->zap = s[2];
       st->alpha = alpha;
+      if (FUSED) st->iter = st->iter + 1;
     }
   }
 }
@@ -172,6 +188,7 @@ cg_pupdate_kernel(int64_t n, const double* __restrict__ r, double* __restrict__ 
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     if (VEC) {
       const int64_t np = n >> 1;
+#pragma unroll 2
       for (int64_t q = gtid; q < np; q += nthr) {
         double2 zv;
         if (z) {
@@ -276,16 +293,23 @@ extern "C" int nk_cg_init_finalize(nk_cg_state* st, double* hist, nk_stream_t st
 extern "C" int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap,
                             const double* invD, const double* wt, nk_cg_state* st,
                             double* partials, nk_stream_t stream) {
-  if (n < 0 || !x || !r || !p || !Ap || !st || !partials) {
+  if (n < 0 || !r || !Ap || !st || !partials || (x != nullptr && p == nullptr)) {
     set_error("cg_update: invalid arguments");
     return NK_ERR_INVALID;
   }
   const unsigned g = (unsigned)vec_grid(n);
   cudaStream_t s = S(stream);
-  if (aligned16(x, r, p, Ap, invD, wt))
-    cg_update_kernel<true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
-  else
-    cg_update_kernel<false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+  const bool vec = aligned16(x, r, p, Ap, invD, wt);
+  if (x == nullptr) {  // fused BP5 path
+    if (vec)
+      cg_update_kernel<true, true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+    else
+      cg_update_kernel<false, true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+  } else if (vec) {
+    cg_update_kernel<true, false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+  } else {
+    cg_update_kernel<false, false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+  }
   return check_launch("cg_update");
 }
 

@@ -138,9 +138,61 @@ class PoissonOperator:
         COUNTERS.add("stiffness", bk5_flops(m.N, m.E, self.ncomp), 7 * self.n * self.ncomp)
         return w
 
+    def apply_pcg(self, p, w, x, r, invD, st, partials, hist):
+        """Fused BP5 operator step (nk_bk5_pcg): convergence test, deferred
+        x += alpha p, Jacobi p = invD r + beta p, then w = A p with p^T A p
+        into st->pAp -- followed by gs (and the halo on several ranks)."""
+        m = self.mesh
+        L, s = lib(), stream_ptr()
+        D = m.basis.diff
+        Bp = ptr(m.B) if self.lam1 != 0.0 else None
+        g = self.gs
+        multi = g.comm is not None and g.comm.size > 1
+
+        def k1(elems, base, reduce_count):
+            nl = 0 if elems is None else int(elems.numel())
+            check(L.nk_bk5_pcg(m.N, m.E, ptr(D), ptr(m.G), ptr(p), ptr(w), self.lam0, Bp,
+                               self.lam1, ptr(m.mask), ptr(elems), nl, ptr(x), ptr(r), ptr(invD),
+                               ptr(st), ptr(partials), base, reduce_count, ptr(hist), s),
+                  "bk5_pcg")
+
+        if not multi:
+            nb = int(L.nk_bk5_pcg_blocks(m.N, m.E))
+            k1(None, 0, nb)
+            _local(g, w, "+", 1, st=st)
+        else:
+            import torch
+            be, ie = g.boundary_elements, g.interior_elements
+            nbb = int(L.nk_bk5_pcg_blocks(m.N, int(be.numel()))) if be.numel() else 0
+            nbi = int(L.nk_bk5_pcg_blocks(m.N, int(ie.numel()))) if ie.numel() else 0
+            if be.numel():
+                k1(be, 0, 0 if ie.numel() else nbb)
+            _local(g, w, "+", 1, st=st, part=g.seg_halo)
+            _halo_start(g, w, st=st)
+            main = torch.cuda.current_stream()
+            side = getattr(g, "_side", None)
+            if side is None:
+                side = g._side = torch.cuda.Stream(device=w.device)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                _halo_exchange(g)
+                done = torch.cuda.Event()
+                done.record(side)
+            if ie.numel():
+                k1(ie, nbb, nbb + nbi)
+            _local(g, w, "+", 1, st=st, part=g.seg_rest)
+            main.wait_event(done)
+            _halo_finish(g, w, "+", st=st)
+        COUNTERS.add("stiffness", bk5_flops(m.N, m.E, 1), 7 * self.n)
+        return w
+
     def partials_len(self):
         m = self.mesh
-        return max(int(lib().nk_bk5_blocks(m.N, m.E, self.ncomp)), 1) + 2
+        L = lib()
+        return max(int(L.nk_bk5_blocks(m.N, m.E, self.ncomp)),
+                   int(L.nk_bk5_pcg_blocks(m.N, m.E)), 1) + 2
 
 
 class JacobiPreconditioner:
@@ -163,8 +215,9 @@ class FusedPCG:
 
     Buffers are allocated once; ``solve(b)`` runs init (2 launches + optional
     all-reduce), then replays a CUDA graph of ``chunk`` iterations until the
-    device flag ``done`` is set.  Per iteration: BK5 (+pAp), gs, [halo],
-    cg_update (+rr, rz, zAp), cg_pupdate -- 4 kernels on one rank."""
+    device flag ``done`` is set.  Per iteration: nk_bk5_pcg (convergence
+    test, deferred x update, Jacobi p update, BK5, p.Ap), gs, [halo],
+    nk_cg_update (r, rr, rz, zAp) -- 3 kernels on one rank."""
 
     def __init__(self, op, prec, tol=1e-8, max_iter=1000, flexible=False, chunk=16,
                  use_graph=True):
@@ -193,22 +246,22 @@ class FusedPCG:
         self.comm = op.gs.comm if (op.gs.comm is not None and op.gs.comm.size > 1) else None
         self.s64 = self.st.view(torch.float64)   # rz pAp rz_new rr zap bb thresh2 alpha
         self.graph = None
-        self.launches_per_iter = 4
+        self.launches_per_iter = 3
 
     def _allreduce(self, a, b):
         if self.comm is not None:
             self.comm.allreduce_sum_(self.s64[a:b])
 
     def _iteration(self):
+        """One PCG iteration = 3 kernels on one rank: nk_bk5_pcg (test,
+        x/p updates, BK5, p.Ap), gs, nk_cg_update (r, rr, rz, zAp)."""
         L, s = lib(), stream_ptr()
-        self.op.apply(self.p, self.w, st=self.st, partials=self.part_bk5)
+        self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st, self.part_bk5,
+                          self.hist)
         self._allreduce(1, 2)                                            # pAp
-        check(L.nk_cg_update(self.n, ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.w),
-                             ptr(self.invD), ptr(self.wt), ptr(self.st), ptr(self.part_cg), s),
-              "cg_update")
+        check(L.nk_cg_update(self.n, None, ptr(self.r), None, ptr(self.w), ptr(self.invD),
+                             ptr(self.wt), ptr(self.st), ptr(self.part_cg), s), "cg_update")
         self._allreduce(2, 5)                                            # rz_new rr zap
-        check(L.nk_cg_pupdate(self.n, ptr(self.r), ptr(self.p), ptr(self.invD), None,
-                              ptr(self.st), ptr(self.hist), s), "cg_pupdate")
 
     def _capture(self):
         import torch
@@ -217,6 +270,38 @@ class FusedPCG:
             for _ in range(self.chunk):
                 self._iteration()
         self.graph = g
+
+    def profile_iteration(self, reps=20):
+        """In-situ device time (ms) of each kernel group of one iteration,
+        CUDA events between launches on the current stream (eager, no graph;
+        L2 state as in a real solve).  Returns {name: ms}."""
+        import torch
+        L, s = lib(), stream_ptr()
+        op, g = self.op, self.op.gs
+        names = ("bk5_pcg", "gs", "cg_update")
+        acc = dict.fromkeys(names, 0.0)
+        st_save = self.st.clone()
+        m = op.mesh
+        for _ in range(reps):
+            self.st.copy_(st_save)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+            nb = int(L.nk_bk5_pcg_blocks(m.N, m.E))
+            check(L.nk_bk5_pcg(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p), ptr(self.w),
+                               op.lam0, ptr(m.B) if op.lam1 else None, op.lam1, ptr(m.mask),
+                               None, 0, ptr(self.x), ptr(self.r), ptr(self.invD), ptr(self.st),
+                               ptr(self.part_bk5), 0, nb, ptr(self.hist), s), "bk5_pcg")
+            ev[1].record()
+            _local(g, self.w, "+", 1, st=self.st)
+            ev[2].record()
+            check(L.nk_cg_update(self.n, None, ptr(self.r), None, ptr(self.w), ptr(self.invD),
+                                 ptr(self.wt), ptr(self.st), ptr(self.part_cg), s), "cg_update")
+            ev[3].record()
+            torch.cuda.synchronize()
+            for q, nm in enumerate(names):
+                acc[nm] += ev[q].elapsed_time(ev[q + 1])
+        self.st.copy_(st_save)
+        return {k: v / reps for k, v in acc.items()}
 
     def init(self, b):
         L, s = lib(), stream_ptr()
