@@ -17,9 +17,12 @@ deterministic:
   4. halo ids H = ids with >= 2 holders, sorted ascending; per neighbour q the
      send/recv order is H restricted to ids q also holds -- both sides derive
      the same order without further messages.
-The exchanged values are the per-rank partial sums of the local gs; the
-receiver folds the holders' partials in ascending rank order (own partial at
-its rank position), so every rank computes bit-identical totals.
+The exchange carries every local copy of a halo id (not a pre-summed
+partial): the combine then folds all contributions of an id in ascending
+(rank, local index) order -- exactly the canonical order of SPEC.md:205 -- so
+multi-rank results are bit-identical to the single-process fold and to every
+other rank's copy.  Local segments of halo ids are therefore not
+folded locally; only ids private to the rank use the local plan.
 """
 
 import numpy as np
@@ -65,6 +68,11 @@ class RankComm:
         return [r[offs[q]:offs[q + 1]] for q in range(P)]
 
     def allreduce_sum_(self, t):
+        if self.staging == "host" and t.is_cuda:
+            h = t.detach().cpu()
+            self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+            return t
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t
 
@@ -98,13 +106,15 @@ class HaloPlan:
     """Host-side arrays describing the cross-rank part of QQ^T for one rank.
 
     hids        sorted halo ids (held by >= 2 ranks)
-    holders     list of holder-rank arrays per halo id (ascending)
+    holders     holder-rank array per halo id (ascending)
     neighbors   sorted neighbour ranks; ngh = len(neighbors)
-    rep         local index of the first local copy of each halo id
-    dst_start/dst_idx   CSR: all local copies of each halo id (ascending)
-    send[q]     positions (into hids) sent to / received from neighbour q
-    src_start/src_idx   CSR into buf = [own partials (nh) | recv_q0 | recv_q1 ...]
-                        listing the holders' partials in ascending rank order
+    dst_start/dst_idx   CSR: all local copies of each halo id (ascending); the
+                        own contributions are buf[0:len(dst_idx)] = w[dst_idx]
+    send_idx[q] local indices sent to q: copies of the ids shared with q, ids
+                ascending, copies ascending
+    recv_off[q], recv_len[q]   where q's contributions land in buf
+    src_start/src_idx   CSR into buf: the contributions of each halo id in
+                        ascending (rank, local index) order
     """
 
 
@@ -116,6 +126,7 @@ def _face_point_mask(nq):
 
 def build_halo_plan(ids, comm, nq=None):
     """Collective discovery of rank-shared ids (see module doc)."""
+    import torch
     ids = np.asarray(ids, dtype=np.int64).ravel()
     P, me = comm.size, comm.rank
     if P > 62:
@@ -126,8 +137,7 @@ def build_halo_plan(ids, comm, nq=None):
     else:
         cand = np.unique(ids[ids > 0])
     owner = cand % P
-    parts = [cand[owner == q] for q in range(P)]
-    got = comm.alltoallv_int64(parts)
+    got = comm.alltoallv_int64([cand[owner == q] for q in range(P)])
     # owner side: (id, holder-rank) pairs -> bitmask per id held by >= 2 ranks
     gid = np.concatenate(got) if got else np.zeros(0, np.int64)
     src = np.concatenate([np.full(len(g), q, dtype=np.int64) for q, g in enumerate(got)])
@@ -135,20 +145,18 @@ def build_halo_plan(ids, comm, nq=None):
     if len(gid):
         o = np.lexsort((src, gid))
         gid, src = gid[o], src[o]
-        u, start, cnt = np.unique(gid, return_index=True, return_counts=True)
+        u, cnt = np.unique(gid, return_counts=True)
         bits = np.zeros(len(u), dtype=np.int64)
         np.bitwise_or.at(bits, np.repeat(np.arange(len(u)), cnt), np.left_shift(1, src))
         shared = cnt >= 2
         us, bs = u[shared], bits[shared]
-        rep_parts = [[] for _ in range(P)]
+        replies = []
         for q in range(P):
             sel = (bs >> q) & 1 == 1
-            rep_parts[q] = np.stack([us[sel], bs[sel]], axis=1).ravel()
-        replies = rep_parts
+            replies.append(np.stack([us[sel], bs[sel]], axis=1).ravel())
     back = comm.alltoallv_int64(replies)
     rec = np.concatenate([b.reshape(-1, 2) for b in back]) if back else np.zeros((0, 2), np.int64)
-    o = np.argsort(rec[:, 0], kind="stable") if len(rec) else np.zeros(0, np.int64)
-    rec = rec[o]
+    rec = rec[np.argsort(rec[:, 0], kind="stable")] if len(rec) else rec.reshape(0, 2)
     plan = HaloPlan()
     plan.rank, plan.size = me, P
     plan.hids = rec[:, 0].copy()
@@ -156,8 +164,7 @@ def build_halo_plan(ids, comm, nq=None):
     nh = len(plan.hids)
     plan.holders = [np.flatnonzero((int(m) >> np.arange(P)) & 1) for m in masks]
     nb = sorted({int(q) for h in plan.holders for q in h if q != me})
-    plan.neighbors = nb
-    plan.ngh = len(nb)
+    plan.neighbors, plan.ngh = nb, len(nb)
     # local copies of every halo id (ascending local index)
     order = np.argsort(ids, kind="stable")
     sids = ids[order]
@@ -165,32 +172,57 @@ def build_halo_plan(ids, comm, nq=None):
     hi = np.searchsorted(sids, plan.hids, side="right")
     if np.any(hi <= lo):
         raise RuntimeError("halo id without a local copy (inconsistent discovery)")
-    plan.dst_start = np.r_[0, np.cumsum(hi - lo)].astype(np.int64)
-    plan.dst_idx = np.concatenate([order[a:b] for a, b in zip(lo, hi)]) if nh else \
-        np.zeros(0, np.int64)
+    mult = hi - lo
+    plan.dst_start = np.r_[0, np.cumsum(mult)].astype(np.int64)
+    plan.dst_idx = order[_ranges(lo, mult)] if nh else np.zeros(0, np.int64)
     plan.rep = order[lo] if nh else np.zeros(0, np.int64)
-    # per-neighbour positions in hids, ascending id order on both sides
-    plan.send = {}
+    own_len = len(plan.dst_idx)
+    # ids shared with each neighbour (positions into hids, ascending id)
+    shared_pos = {q: np.array([t for t in range(nh) if q in set(plan.holders[t].tolist())],
+                              dtype=np.int64) for q in nb}
+    plan.send_idx = {q: plan.dst_idx[_ranges(plan.dst_start[shared_pos[q]], mult[shared_pos[q]])]
+                     for q in nb}
+    # setup exchange: how many copies each neighbour holds of each shared id
+    sends = {q: torch.as_tensor(mult[shared_pos[q]].astype(np.int64)) for q in nb}
+    recvs = {q: torch.zeros(len(shared_pos[q]), dtype=torch.int64) for q in nb}
+    if comm.backend == "nccl":
+        sends = {q: t.cuda() for q, t in sends.items()}
+        recvs = {q: t.cuda() for q, t in recvs.items()}
+    comm.exchange(sends, recvs)
+    their = {q: recvs[q].cpu().numpy() for q in nb}
+    plan.recv_off, plan.recv_len, off = {}, {}, own_len
     for q in nb:
-        plan.send[q] = np.array([t for t in range(nh) if q in set(plan.holders[t])],
-                                dtype=np.int64)
-    # combine CSR into buf = [own | recv_q (for q in neighbors)]
-    recv_off, off = {}, nh
-    for q in nb:
-        recv_off[q] = off
-        off += len(plan.send[q])
+        plan.recv_off[q] = off
+        plan.recv_len[q] = int(their[q].sum())
+        off += plan.recv_len[q]
     plan.buf_len = off
-    plan.recv_off = recv_off
-    pos_in_q = {q: {int(t): i for i, t in enumerate(plan.send[q])} for q in nb}
+    # where h's contributions from q start inside q's stream
+    start_in_q = {q: dict(zip(shared_pos[q].tolist(),
+                              (np.r_[0, np.cumsum(their[q])[:-1]]).tolist())) for q in nb}
+    cnt_in_q = {q: dict(zip(shared_pos[q].tolist(), their[q].tolist())) for q in nb}
     src_start, src_idx = [0], []
     for t in range(nh):
-        for q in plan.holders[t]:
-            q = int(q)
-            src_idx.append(t if q == me else recv_off[q] + pos_in_q[q][t])
+        for q in plan.holders[t].tolist():
+            if q == me:
+                src_idx.extend(range(plan.dst_start[t], plan.dst_start[t + 1]))
+            else:
+                a0 = plan.recv_off[q] + start_in_q[q][t]
+                src_idx.extend(range(a0, a0 + cnt_in_q[q][t]))
         src_start.append(len(src_idx))
     plan.src_start = np.asarray(src_start, dtype=np.int64)
     plan.src_idx = np.asarray(src_idx, dtype=np.int64)
     return plan
+
+
+def _ranges(starts, counts):
+    """Concatenation of arange(s, s + c) for (s, c) pairs, vectorised."""
+    starts = np.asarray(starts, dtype=np.int64)
+    counts = np.asarray(counts, dtype=np.int64)
+    if len(counts) == 0 or counts.sum() == 0:
+        return np.zeros(0, np.int64)
+    tot = int(counts.sum())
+    offs = np.repeat(np.cumsum(counts) - counts, counts)
+    return np.repeat(starts, counts) + (np.arange(tot) - offs)
 
 
 def boundary_elements(plan, n_elem, nq3):

@@ -132,27 +132,26 @@ def gs_setup(ids, comm=None, nq=None, device="cuda"):
         h.neighbors, h.ngh = plan.neighbors, plan.ngh
         nh = len(plan.hids)
         h.nh = nh
-        h.rep = _to_i32(plan.rep, device)
+        h.own_idx = _to_i32(plan.dst_idx, device)          # own contributions
         h.dst_start = _to_i32(plan.dst_start, device)
         h.dst_idx = _to_i32(plan.dst_idx, device)
         h.src_start = _to_i32(plan.src_start, device)
         h.src_idx = _to_i32(plan.src_idx, device)
         h.buf = torch.zeros(max(plan.buf_len, 1), dtype=torch.float64, device=device)
-        send_cat = np.concatenate([plan.rep[plan.send[q]] for q in plan.neighbors]) \
+        send_cat = np.concatenate([plan.send_idx[q] for q in plan.neighbors]) \
             if plan.neighbors else np.zeros(0, np.int64)
         h.send_idx = _to_i32(send_cat, device)
         h.send_buf = torch.zeros(max(len(send_cat), 1), dtype=torch.float64, device=device)
         h.send_slices, h.recv_slices, o = {}, {}, 0
         for q in plan.neighbors:
-            k = len(plan.send[q])
+            k = len(plan.send_idx[q])
             h.send_slices[q] = (o, o + k)
-            h.recv_slices[q] = (plan.recv_off[q], plan.recv_off[q] + k)
+            h.recv_slices[q] = (plan.recv_off[q], plan.recv_off[q] + plan.recv_len[q])
             o += k
-        # split local segments: those touching a halo id run before the exchange
-        hset = np.zeros(0, np.int64) if nh == 0 else plan.hids
+        # local segments of halo ids are not folded locally (the combine folds
+        # every contribution in canonical order); the rest run as usual
         seg_ids = ids_h[perm[seg[:-1]]] if h.nseg else np.zeros(0, np.int64)
-        is_h = np.isin(seg_ids, hset)
-        h.seg_halo = _sub_plan(perm, seg, is_h, device)
+        is_h = np.isin(seg_ids, plan.hids)
         h.seg_rest = _sub_plan(perm, seg, ~is_h, device)
         if nq is not None:
             nq3 = nq ** 3
@@ -173,7 +172,7 @@ def _sub_plan(perm, seg, keep, device):
     starts = seg[:-1][keep]
     if len(cnt) == 0:
         return _Plan(np.zeros(0, np.int64), np.zeros(1, np.int64), device)
-    idx = np.concatenate([perm[a:a + c] for a, c in zip(starts, cnt)])
+    idx = np.asarray(perm)[_dist._ranges(starts, cnt)]
     s = np.r_[0, np.cumsum(cnt)]
     return _Plan(idx, s, device)
 
@@ -193,9 +192,11 @@ def _local(h, w, op, ncomp, st=None, part=None):
 
 
 def _halo_start(h, w, st=None):
+    """Pack: own contributions of halo ids into buf[0:), send buffers."""
     L, s = lib(), stream_ptr()
     if h.nh:
-        check(L.nk_gather(h.nh, ptr(h.rep), ptr(w), ptr(h.buf), ptr(st), s), "gather")
+        check(L.nk_gather(h.own_idx.numel(), ptr(h.own_idx), ptr(w), ptr(h.buf), ptr(st), s),
+              "gather")
         ns = h.send_idx.numel() if h.neighbors else 0
         if ns:
             check(L.nk_gather(ns, ptr(h.send_idx), ptr(w), ptr(h.send_buf), ptr(st), s), "gather")
@@ -236,9 +237,9 @@ def gs_op(handle, w, op="+", precision=64, ncomp=1):
             return w
         _local(handle, w, op, ncomp)
         return w
-    _local(handle, w, op, 1)
     _halo_start(handle, w)
     _halo_exchange(handle)
+    _local(handle, w, op, 1, part=handle.seg_rest)
     _halo_finish(handle, w, op)
     return w
 
@@ -259,7 +260,6 @@ def gs_op_overlapped(handle, local_work, field, op="+"):
         return field
     if handle.boundary_elements.numel():
         local_work(handle.boundary_elements)
-    _local(handle, field, op, 1, part=handle.seg_halo)
     _halo_start(handle, field)
     main = torch.cuda.current_stream()
     side = getattr(handle, "_side", None)

@@ -117,7 +117,6 @@ class PoissonOperator:
             nbi = int(L.nk_bk5_blocks(m.N, int(ie.numel()), self.ncomp)) if ie.numel() else 0
             if be.numel():
                 bk5(be, 0, 0 if ie.numel() else (nbb if st is not None else 0))
-            _local(g, w, "+", 1, st=st, part=g.seg_halo)
             _halo_start(g, w, st=st)
             main = torch.cuda.current_stream()
             side = getattr(g, "_side", None)
@@ -167,7 +166,6 @@ class PoissonOperator:
             nbi = int(L.nk_bk5_pcg_blocks(m.N, int(ie.numel()))) if ie.numel() else 0
             if be.numel():
                 k1(be, 0, 0 if ie.numel() else nbb)
-            _local(g, w, "+", 1, st=st, part=g.seg_halo)
             _halo_start(g, w, st=st)
             main = torch.cuda.current_stream()
             side = getattr(g, "_side", None)

@@ -1,0 +1,117 @@
+"""CPU tests (no GPU): the C-ABI library loads and exports every symbol the
+header declares; host-side logic (native gs plan builder, basis, RCB, ids,
+HEXMESH) matches the oracle bit-for-bit."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import gs as ogs
+from oracle import mesh as om
+from oracle import partition as opart
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "nekb200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(nk_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2104_05829_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libnekb200.so not built (run __graft_entry__.build())")
+    return _lib.lib()
+
+
+def test_header_symbols_exported_and_bound(L):
+    from paper_2104_05829_b200 import _lib
+    names = declared_functions()
+    assert len(names) >= 20
+    for nm in names:
+        assert hasattr(L, nm), f"{nm} declared in include/nekb200.h but not exported"
+    assert set(names) == set(_lib.exported_symbols()), \
+        set(names) ^ set(_lib.exported_symbols())
+
+
+def test_version_error_and_state_layout(L):
+    from paper_2104_05829_b200 import _lib
+    assert L.nk_version() >= 10000
+    lo, hi = np.zeros(1, np.int32), np.zeros(1, np.int32)
+    assert L.nk_order_range(lo.ctypes.data, hi.ctypes.data) == 0
+    assert (lo[0], hi[0]) == (1, 15)
+    rc = L.nk_gs_plan_build(None, -1, None, None, None, None)
+    assert rc == _lib.NK_ERR_INVALID
+    assert b"invalid" in L.nk_last_error()
+    with pytest.raises(_lib.ContractError):
+        _lib.check(rc, "gs_plan_build")
+    # nk_cg_state is 13 doubles-worth of bytes with the documented field order
+    assert _lib.CG_STATE_BYTES == 104
+    assert _lib.CGState.done.offset == 68
+
+
+@pytest.mark.parametrize("counts,N,bc", [((3, 2, 2), 3, "dirichlet"), ((4, 4, 4), 7, "periodic"),
+                                         ((2, 1, 1), 1, "neumann"), ((5, 3, 2), 2, "periodic")])
+def test_native_plan_builder_bit_exact(L, counts, N, bc):
+    from paper_2104_05829_b200.gather_scatter import _local_plan
+    ids = om.build_box_mesh((1, 1, 1), counts, N, bc=bc).ids
+    perm, seg = _local_plan(ids)
+    operm, oseg = ogs.local_plan(ids)
+    assert np.array_equal(perm, operm) and np.array_equal(seg, oseg)
+
+
+def test_native_plan_builder_random_ids(L):
+    from paper_2104_05829_b200.gather_scatter import _local_plan
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        n = int(rng.integers(0, 300))
+        ids = rng.integers(0, max(1, n // 2), size=n)
+        perm, seg = _local_plan(ids)
+        operm, oseg = ogs.local_plan(ids)
+        assert np.array_equal(perm, operm) and np.array_equal(seg, oseg)
+
+
+def test_product_basis_bitwise_reference(golden_basis):
+    from paper_2104_05829_b200 import basis as pb
+    for N in range(1, 17):
+        b = pb.SpectralBasis.get(N)
+        assert np.array_equal(b.nodes, golden_basis[f"nodes_{N}"])
+        assert np.array_equal(b.weights, golden_basis[f"weights_{N}"])
+        assert np.array_equal(b.diff, golden_basis[f"diff_{N}"])
+    with pytest.raises(pb.InvalidOrderError):
+        pb.gll_rule(0)
+
+
+@pytest.mark.parametrize("E,P", [(8, 2), (16, 4), (1000, 8), (97, 5), (64, 3)])
+def test_product_rcb_matches_oracle(E, P):
+    from paper_2104_05829_b200.partition import rcb
+    c = np.random.default_rng(E * P).random((E, 3))
+    assert np.array_equal(rcb(c, P), opart.rcb(c, P))
+
+
+def test_product_ids_and_hexmesh(tmp_path):
+    from paper_2104_05829_b200 import mesh as pm
+    o = om.build_box_mesh((1, 1, 1), (3, 2, 2), 3, deformation=("sine", 0.05))
+    assert np.array_equal(pm.assign_global_ids(o.xyz), om.assign_global_ids(o.xyz))
+    assert np.array_equal(pm.singleton_ids(o.ids), om.singleton_ids(o.ids))
+    p = tmp_path / "m.hex"
+    pm.write_hexmesh(p, o.xyz, o.ids, {"pressure": o.mask.astype(int)})
+    E, N, xyz, ids, masks = pm.read_hexmesh(p)
+    assert (E, N) == (12, 3) and np.array_equal(xyz, o.xyz) and np.array_equal(ids, o.ids)
+    E2, N2, xyz2, ids2, masks2 = om.read_hexmesh(p)     # cross-read with the oracle
+    assert np.array_equal(xyz2, xyz) and np.array_equal(masks2["pressure"], masks["pressure"])
+
+
+def test_bc_normalisation():
+    from paper_2104_05829_b200.mesh import normalize_bc
+    assert normalize_bc("periodic")["z+"] == "periodic"
+    with pytest.raises(ValueError):
+        normalize_bc({"x-": "periodic"})
+    with pytest.raises(ValueError):
+        normalize_bc("slip")

@@ -1,0 +1,96 @@
+"""Multi-rank path on ONE GPU: two processes share cuda:0 and talk over
+gloo with host staging (the paper's host-staged exchange), so the CUDA pack /
+combine kernels, the boundary-first overlapped operator and the fused PCG
+with all-reduced scalars all run for real.  (NCCL refuses two ranks on one
+device; the 8-GPU NVLink path uses the same code with staging='device'.)"""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir, counts, N):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2104_05829_b200 as nk
+        from oracle import gs as ogs
+        from oracle import mesh as om
+        from paper_2104_05829_b200.distributed import RankComm
+        g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05))
+        nq3 = (N + 1) ** 3
+        part = nk.rcb(g.xyz.reshape(3, g.E, -1).mean(axis=2).T, world)
+        mine = np.flatnonzero(part == rank)
+        comm = RankComm()
+        m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05),
+                              elements=mine)
+        op = nk.PoissonOperator(m, comm=comm)
+        # gs on a random field (checked bit-exact against the global oracle)
+        rng = np.random.default_rng(100 + rank)
+        w = rng.standard_normal(m.n_local)
+        gsw = nk.gs_op(op.gs, torch.as_tensor(w, device="cuda")).cpu().numpy()
+        # global rhs restricted to my elements
+        X = g.xyz.reshape(3, -1)
+        f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+        bglob = g.mask.ravel() * ogs.gs_op(g.ids, g.B.ravel() * f)
+        b = bglob.reshape(g.E, nq3)[mine].ravel()
+        jac = nk.JacobiPreconditioner(op)
+        res = nk.FusedPCG(op, jac, tol=1e-8, max_iter=500, use_graph=False).solve(
+            torch.as_tensor(b, device="cuda"))
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), mine=mine, ids=m.ids.cpu().numpy(),
+                 w=w, gsw=gsw, x=res.x.cpu().numpy(), it=res.iterations,
+                 conv=res.converged, ngh=op.gs.ngh, nb=op.gs.boundary_elements.numel())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_one_gpu_gs_and_pcg():
+    import torch.multiprocessing as mp
+    from oracle import gs as ogs
+    from oracle import mesh as om
+    from oracle import operators as oop
+    from oracle import solvers as osol
+    counts, N, world = (4, 4, 2), 5, 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _port(), d, counts, N), nprocs=world, join=True)
+        res = [np.load(os.path.join(d, f"r{r}.npz")) for r in range(world)]
+    ref = ogs.gs_op_multi([r["ids"] for r in res], [r["w"] for r in res])
+    for r, ro in zip(res, ref):
+        assert np.array_equal(r["gsw"], ro)            # CUDA halo path, bit-exact
+        assert int(r["ngh"]) == 1 and int(r["nb"]) > 0
+    g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05))
+    X = g.xyz.reshape(3, -1)
+    f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+    mask = g.mask.ravel()
+    b = mask * ogs.gs_op(g.ids, g.B.ravel() * f)
+    sh = (g.E,) + g.G.shape[2:]
+    A = lambda v: mask * ogs.gs_op(g.ids, oop.bk5(g.basis.diff, g.G, v.reshape(sh)).ravel())
+    inv = mask / ogs.gs_op(g.ids, oop.local_diagonal(g.basis.diff, g.G).ravel())
+    o = osol.pcg(A, lambda r: inv * r, b, tol=1e-8, max_iter=500,
+                 weights=1.0 / ogs.multiplicity(g.ids))
+    nq3 = (N + 1) ** 3
+    xg = np.zeros((g.E, nq3))
+    for r in res:
+        assert bool(r["conv"]) and abs(int(r["it"]) - o.iterations) <= 1
+        xg[r["mine"]] = r["x"].reshape(-1, nq3)
+    assert int(res[0]["it"]) == int(res[1]["it"])
+    assert np.max(np.abs(xg.ravel() - o.x)) < 1e-7 * np.max(np.abs(o.x))
