@@ -187,11 +187,12 @@ int nk_gs_op(int64_t nseg, const int32_t* seg_start, const int32_t* perm, double
              int ncomp, int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream);
 
 /* The same plan re-packed by multiplicity class (one launch for all
- * classes, at most 16): class c has segment size sizes[c] [host] and
- * nsegs[c] [host] segments whose members are members[c] [host array of dev
- * pointers], member-major int32 (members[c][m * nsegs[c] + s]), members of a
- * segment in canonical (ascending local index) order.  Bit-identical to
- * nk_gs_op on the same map; independent index/value loads per segment. */
+ * classes, at most 16, segment size 1..32): class c has segment size
+ * sizes[c] [host] and nsegs[c] [host] segments whose members are members[c]
+ * [host array of dev pointers]: int32, segment-major, each segment padded to
+ * Mp = next power of two >= sizes[c] with -1 (members[c][s * Mp + m]),
+ * members in canonical (ascending local index) order.  One lane per member;
+ * fold via warp shuffles in member order: bit-identical to nk_gs_op. */
 int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t* nsegs,
                      const int32_t* const* members, double* w, int op, int ncomp,
                      int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream);

@@ -340,6 +340,10 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
         tma_load_1d(dst + 2 * NQ3, invD + e * NQ3, UB, &bar[s]);
       }
       tma_load_1d(dst + 3 * NQ3, G + e * 6 * NQ3, GB, &bar[s]);
+      // x and mask of the same element are read with plain loads later:
+      // start them towards L2 now so those loads do not wait on HBM
+      if (it > 0) prefetch_l2(x + e * NQ3, UB);
+      if (mask != nullptr) prefetch_l2(mask + e * NQ3, NQ3);
     };
     if (t == 0) {
       mbar_init(&bar[0], 1);

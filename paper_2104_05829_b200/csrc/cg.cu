@@ -135,11 +135,13 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
   if (VEC) {
     const int64_t np = n >> 1;
     int64_t q = gtid;
-    for (; q + nthr < np; q += 2 * nthr) {  // two independent pairs per trip
+    for (; q + 3 * nthr < np; q += 4 * nthr) {  // four independent pairs per trip
       pair(q);
       pair(q + nthr);
+      pair(q + 2 * nthr);
+      pair(q + 3 * nthr);
     }
-    if (q < np) pair(q);
+    for (; q < np; q += nthr) pair(q);
     if ((n & 1) && gtid == 0) {
       const int64_t t = n - 1;
       double xd = 0.0;

@@ -66,36 +66,21 @@ __global__ void halo_combine_kernel(int64_t nh, const int32_t* __restrict__ src_
 }
 
 // Multiplicity classes: the same plan re-packed so every segment of a class
-// has M members stored member-major (members[m * nseg + s]); one thread per
-// segment issues its M index loads and M value loads independently (no
-// seg_start -> perm -> w dependency chain), then folds them in canonical
-// order -- bit-identical to gs_segments.
+// has M members, stored segment-major and padded to Mp = next power of two
+// (<= 32; padding = -1): mem[s * Mp + m].  One LANE per member: each lane
+// issues one index load and one value load (a single dependent L2 round
+// trip), then the segment's first lane folds the M values, pulled with warp
+// shuffles in member order -- the canonical order, so results are
+// bit-identical to gs_segments -- and broadcasts the result back.  Segments
+// never straddle a warp (Mp divides 32).  Classes with M > 32 use the CSR path.
 struct GsClasses {
   int n;
   int M[NK_GS_MAX_CLASSES];
+  int Mp[NK_GS_MAX_CLASSES];
   int64_t nseg[NK_GS_MAX_CLASSES];
   const int32_t* mem[NK_GS_MAX_CLASSES];
   int64_t bstart[NK_GS_MAX_CLASSES + 1];
 };
-
-template <int M, int OP>
-__device__ __forceinline__ void fold_fixed(const int32_t* __restrict__ mem, int64_t ns, int64_t s,
-                                           double* __restrict__ w, int ncomp, int64_t cs) {
-  int idx[M];
-#pragma unroll
-  for (int m = 0; m < M; ++m) idx[m] = __ldg(mem + m * ns + s);
-  for (int c = 0; c < ncomp; ++c) {
-    double* wc = w + c * cs;
-    double v[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) v[m] = wc[idx[m]];
-    double acc = v[0];
-#pragma unroll
-    for (int m = 1; m < M; ++m) acc = fold<OP>(acc, v[m]);
-#pragma unroll
-    for (int m = 0; m < M; ++m) wc[idx[m]] = acc;
-  }
-}
 
 template <int OP>
 __global__ void __launch_bounds__(256)
@@ -105,25 +90,23 @@ gs_classes_kernel(const __grid_constant__ GsClasses C, double* __restrict__ w, i
   const int64_t b = blockIdx.x;
   int c = 0;
   while (c + 1 < C.n && b >= C.bstart[c + 1]) ++c;
-  const int64_t s = (b - C.bstart[c]) * blockDim.x + threadIdx.x;
-  const int64_t ns = C.nseg[c];
-  if (s >= ns) return;
-  const int32_t* mem = C.mem[c];
-  switch (C.M[c]) {
-    case 2: fold_fixed<2, OP>(mem, ns, s, w, ncomp, cs); return;
-    case 3: fold_fixed<3, OP>(mem, ns, s, w, ncomp, cs); return;
-    case 4: fold_fixed<4, OP>(mem, ns, s, w, ncomp, cs); return;
-    case 5: fold_fixed<5, OP>(mem, ns, s, w, ncomp, cs); return;
-    case 6: fold_fixed<6, OP>(mem, ns, s, w, ncomp, cs); return;
-    case 8: fold_fixed<8, OP>(mem, ns, s, w, ncomp, cs); return;
-    default: break;
-  }
-  const int M = C.M[c];
+  const int M = C.M[c], Mp = C.Mp[c];
+  const int64_t lanes = C.nseg[c] * Mp;
+  const int64_t t = (b - C.bstart[c]) * blockDim.x + threadIdx.x;
+  // whole warps stay active for the shuffles; out-of-range lanes carry -1
+  const int idx = t < lanes ? __ldg(C.mem[c] + t) : -1;
+  const int lane = threadIdx.x & 31;
+  const int m = lane & (Mp - 1);
   for (int cc = 0; cc < ncomp; ++cc) {
     double* wc = w + cc * cs;
-    double acc = wc[__ldg(mem + s)];
-    for (int m = 1; m < M; ++m) acc = fold<OP>(acc, wc[__ldg(mem + m * ns + s)]);
-    for (int m = 0; m < M; ++m) wc[__ldg(mem + m * ns + s)] = acc;
+    const double v = idx >= 0 ? wc[idx] : 0.0;
+    double acc = v;
+    for (int j = 1; j < M; ++j) {
+      const double o = __shfl_down_sync(0xffffffffu, v, j, Mp);
+      acc = fold<OP>(acc, o);
+    }
+    const double res = __shfl_sync(0xffffffffu, acc, lane - m);
+    if (idx >= 0) wc[idx] = res;
   }
 }
 
@@ -172,15 +155,18 @@ extern "C" int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t*
   int k = 0;
   for (int c = 0; c < nclass; ++c) {
     if (nsegs[c] <= 0) continue;
-    if (sizes[c] < 1 || !members[c]) {
-      set_error("gs_op_classes: class %d invalid", c);
+    if (sizes[c] < 1 || sizes[c] > 32 || !members[c]) {
+      set_error("gs_op_classes: class %d invalid (size %d; 1..32 allowed)", c, sizes[c]);
       return NK_ERR_INVALID;
     }
+    int mp = 1;
+    while (mp < sizes[c]) mp <<= 1;
     C.M[k] = sizes[c];
+    C.Mp[k] = mp;
     C.nseg[k] = nsegs[c];
     C.mem[k] = members[c];
     C.bstart[k] = blocks;
-    blocks += (nsegs[c] + 255) / 256;
+    blocks += (nsegs[c] * mp + 255) / 256;
     ++k;
   }
   C.n = k;

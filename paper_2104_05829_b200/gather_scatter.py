@@ -42,8 +42,9 @@ MAX_CLASSES = 16
 
 class _Plan:
     """A local gs plan on the device: segments grouped by multiplicity class
-    (member-major int32 arrays, nk_gs_op_classes) plus a CSR remainder when a
-    mesh has more than MAX_CLASSES distinct multiplicities (nk_gs_op).  Built
+    (segment-major int32 arrays padded to a power of two, nk_gs_op_classes)
+    plus a CSR remainder for multiplicities > 32 or beyond MAX_CLASSES
+    distinct ones (nk_gs_op).  Built
     from the canonical CSR (perm, seg_start), so the fold order per segment
     is unchanged."""
 
@@ -55,10 +56,13 @@ class _Plan:
         uniq = np.unique(sizes)
         self._keep = []
         cls_sizes, cls_n, ptrs = [], [], []
-        for M in uniq[:MAX_CLASSES]:
+        small = uniq[uniq <= 32]
+        for M in small[:MAX_CLASSES]:
             sel = np.flatnonzero(sizes == M)
-            mem = perm[seg[sel][:, None] + np.arange(M)[None, :]].T
-            t = _to_i32(np.ascontiguousarray(mem).ravel(), device)
+            Mp = 1 << int(np.ceil(np.log2(M))) if M > 1 else 1
+            mem = np.full((len(sel), Mp), -1, dtype=np.int64)       # segment-major, padded
+            mem[:, :M] = perm[seg[sel][:, None] + np.arange(M)[None, :]]
+            t = _to_i32(mem.ravel(), device)
             self._keep.append(t)
             cls_sizes.append(int(M))
             cls_n.append(len(sel))
@@ -67,10 +71,10 @@ class _Plan:
         self.sizes = np.asarray(cls_sizes, dtype=np.int32)
         self.nsegs = np.asarray(cls_n, dtype=np.int64)
         self.ptrs = np.asarray(ptrs, dtype=np.uint64)
-        rest = np.flatnonzero(np.isin(sizes, uniq[MAX_CLASSES:]))
+        rest = np.flatnonzero(~np.isin(sizes, small[:MAX_CLASSES]))
         if len(rest):
             cnt = sizes[rest]
-            idx = np.concatenate([perm[seg[r]:seg[r + 1]] for r in rest])
+            idx = perm[_dist._ranges(seg[rest], cnt)]
             self.rest = (len(rest), _to_i32(np.r_[0, np.cumsum(cnt)], device), _to_i32(idx, device))
         else:
             self.rest = None
