@@ -277,7 +277,7 @@ template <int NQ, int MINB>
 struct TmaPcgCfg {
   static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
   static constexpr int THREADS = NQ2;
-  static constexpr int STAGE = 9 * NQ3;  // p, r, invD, G[6]
+  static constexpr int STAGE = 7 * NQ3;  // p, G[6]  (r, invD, x: plain loads)
   static constexpr int VOL = PencilLayout<NQ>::VOL;
   static size_t smem_bytes() { return sizeof(double) * (2 * STAGE + 3 * VOL + 32) + 2 * 8; }
 };
@@ -333,16 +333,16 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
     auto issue = [&](int64_t slot, int s) {
       const int64_t e = elem_of(slot);
       double* dst = stage0 + s * STAGE;
-      mbar_expect_tx(&bar[s], (it > 0 ? 3 * UB : UB) + GB);
+      mbar_expect_tx(&bar[s], UB + GB);
       tma_load_1d(dst, p + e * NQ3, UB, &bar[s]);
+      tma_load_1d(dst + NQ3, G + e * 6 * NQ3, GB, &bar[s]);
+      // r, invD, x and mask of the same element are read with plain
+      // (coalesced) loads: start them towards L2 now, two elements ahead
       if (it > 0) {
-        tma_load_1d(dst + NQ3, r + e * NQ3, UB, &bar[s]);
-        tma_load_1d(dst + 2 * NQ3, invD + e * NQ3, UB, &bar[s]);
+        prefetch_l2(r + e * NQ3, UB);
+        prefetch_l2(invD + e * NQ3, UB);
+        prefetch_l2(x + e * NQ3, UB);
       }
-      tma_load_1d(dst + 3 * NQ3, G + e * 6 * NQ3, GB, &bar[s]);
-      // x and mask of the same element are read with plain loads later:
-      // start them towards L2 now so those loads do not wait on HBM
-      if (it > 0) prefetch_l2(x + e * NQ3, UB);
       if (mask != nullptr) prefetch_l2(mask + e * NQ3, NQ3);
     };
     if (t == 0) {
@@ -359,15 +359,19 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
     for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++itl) {
       const int s = itl & 1;
       double* su = stage0 + s * STAGE;
-      const double* sr = su + NQ3;
-      const double* sd = su + 2 * NQ3;
-      const double* sg = su + 3 * NQ3;
+      const double* sg = su + NQ3;
       const int64_t e = elem_of(slot);
-      // x for the deferred update: issued before the barrier wait
-      double xv[NQ];
+      // x, r, invD columns (k-pencil, coalesced planes): issued before the
+      // barrier wait so their latency overlaps the TMA completion
+      double xv[NQ], rv[NQ], dv[NQ];
       if (it > 0) {
 #pragma unroll
-        for (int k = 0; k < NQ; ++k) xv[k] = x[e * NQ3 + k * NQ2 + t];
+        for (int k = 0; k < NQ; ++k) {
+          const int64_t q = e * NQ3 + k * NQ2 + t;
+          xv[k] = x[q];
+          rv[k] = __ldg(r + q);
+          dv[k] = __ldg(invD + q);
+        }
       }
       mbar_wait(&bar[s], (itl >> 1) & 1);
 
@@ -381,7 +385,7 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
           double pv = su[pp];
           if (it > 0) {
             x[e * NQ3 + pp] = fma(alpha_prev, pv, xv[k]);
-            pv = fma(beta, pv, sd[pp] * sr[pp]);
+            pv = fma(beta, pv, dv[k] * rv[k]);
             p[e * NQ3 + pp] = pv;
             su[pp] = pv;
           }
@@ -513,9 +517,8 @@ static int launch_pencil_tma_pcg(int64_t nlist, const int32_t* elist, const doub
   using C = TmaPcgCfg<NQ, MINB>;
   const int64_t grid = tma_pcg_grid<NQ, MINB>(nlist);
   if (grid == 0) return NK_OK;
-  if ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(r) |
-       reinterpret_cast<uintptr_t>(invD) | reinterpret_cast<uintptr_t>(G)) & 15) {
-    set_error("bk5_pencil_tma_pcg: p, r, invD, G must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(G)) & 15) {
+    set_error("bk5_pencil_tma_pcg: p and G must be 16-byte aligned");
     return NK_ERR_INVALID;
   }
   DParam<NQ> D;
