@@ -129,6 +129,17 @@ class ClockSampler:
                 "source": "nvml" if self._nv else "nvidia-smi"}
 
 
+def weak_counts(ws):
+    """configs[3] weak scaling: 20^3 elements per GPU, doubling x, y, z in turn."""
+    c = [20, 20, 20]
+    p, ax = ws, 0
+    while p > 1:
+        c[ax % 3] *= 2
+        p //= 2
+        ax += 1
+    return tuple(c)
+
+
 def dist_setup(args):
     import torch
     import torch.distributed as dist
@@ -136,8 +147,15 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NK_BENCH_BACKEND=gloo lets several ranks share one GPU (host-staged
+        # halo) to exercise the multi-rank path; the real run uses NCCL.
+        backend = os.environ.get("NK_BENCH_BACKEND", "nccl")
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return ws, rank, local
@@ -148,7 +166,8 @@ def max_over_ranks(x, ws):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -264,7 +283,7 @@ def run_ours(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     launches = 0
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         barrier(ws)
         t_wall = time.perf_counter()
         for a, b in ev:
@@ -341,41 +360,67 @@ def run_ours(args):
                    "bk5_E40cubed_gdofs": round(big.E * N ** 3 / (bms * 1e-3) / 1e9, 2)}
         del big, ub, wb
 
-    # ---- BP5: fused Jacobi-PCG on the same mesh (fixed iteration count)
+    # ---- BP5: fused Jacobi-PCG, fixed 100 iterations.  N = 1: the same mesh.
+    # N > 1: weak scaling (configs[3]): a global box of 20^3 elements per GPU
+    # (20^3, 40x20^2, 40^2x20, 40^3), RCB-partitioned, halo over NCCL
+    # (pairwise P2P, boundary-first overlap) and all-reduced PCG scalars.
     bp5 = None
     if not args.no_bp5:
-        op = nk.PoissonOperator(mesh)
+        if ws == 1:
+            bmesh, comm = mesh, None
+        else:
+            from paper_2104_05829_b200.distributed import RankComm
+            gcounts = weak_counts(ws)
+            nx, ny, nz = gcounts
+            el = np.arange(nx * ny * nz)
+            cent = np.stack([el % nx, (el // nx) % ny, el // (nx * ny)], axis=1) + 0.5
+            part = nk.rcb(cent, ws)
+            mine = np.flatnonzero(part == rank)
+            comm = RankComm()
+            bmesh = nk.build_box_mesh((nx / 20.0, ny / 20.0, nz / 20.0), gcounts, N,
+                                      bc="dirichlet", deformation=("sine", 0.05), elements=mine)
+        bn = bmesh.n_local
+        op = nk.PoissonOperator(bmesh, comm=comm)
         jac = nk.JacobiPreconditioner(op)
         iters = 100
-        solver = nk.FusedPCG(op, jac, tol=1e-30, max_iter=iters, chunk=iters)
-        b_rhs = torch.as_tensor(rng.standard_normal(n), device="cuda")
+        solver = nk.FusedPCG(op, jac, tol=1e-30, max_iter=iters, chunk=iters,
+                             use_graph=(ws == 1 or os.environ.get("NK_BENCH_GRAPH_MULTI") == "1"))
+        b_rhs = torch.as_tensor(rng.standard_normal(bn), device="cuda")
         nk.gs_op(op.gs, b_rhs)
-        b_rhs *= mesh.mask.reshape(-1).to(torch.float64)
-        solver.solve(b_rhs)  # warm + capture
+        b_rhs *= bmesh.mask.reshape(-1).to(torch.float64)
+        solver.solve(b_rhs)  # warm (+ graph capture)
         barrier(ws)
         a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         solver.init(b_rhs)
+        barrier(ws)
         a_ev.record(stream)
-        solver.graph.replay()
+        if solver.use_graph:
+            solver.graph.replay()
+        else:
+            for _ in range(iters):
+                solver._iteration()
         b_ev.record(stream)
         barrier(ws)
         st = nk.solvers.read_state(solver.st)
         bp_ms = max_over_ranks(a_ev.elapsed_time(b_ev), ws)
         it = int(st.iter)
         per_it = bp_ms / max(it, 1)
-        # fused schedule: nk_bk5_pcg 105 B + cg_update 40 B per point + gs
-        bp_bytes = n * (105 + 40) + 20 * op.gs.nperm + 4 * op.gs.nseg
         solver.init(b_rhs)
         for _ in range(2):                 # profile a steady-state iteration (iter > 0)
             solver._iteration()
         brk = solver.profile_iteration() if ws == 1 else None
-        bp5 = {"gdof_per_s": round(ws * dof * it / (bp_ms * 1e-3) / 1e9, 3),
+        # fused schedule: nk_bk5_pcg 105 B + cg_update 40 B per point + gs
+        bp_bytes = bn * (105 + 40) + 20 * op.gs.nperm + 4 * op.gs.nseg
+        bdof = bmesh.E * N ** 3
+        bp5 = {"gdof_per_s": round(ws * bdof * it / (bp_ms * 1e-3) / 1e9, 3),
                "breakdown_ms_in_situ": None if brk is None else {k: round(v, 4) for k, v in brk.items()},
                "iterations": it, "ms_per_iteration": round(per_it, 4),
                "roofline_frac": round(bp_bytes / (per_it * 1e-3) / 1e9 / peak, 3),
-               "model_bytes_per_local_point": round(bp_bytes / n, 1),
+               "model_bytes_per_local_point": round(bp_bytes / bn, 1),
                "kernels_per_iteration": solver.launches_per_iter,
-               "unfused_model_frac": round((n * 173 + 20 * op.gs.nperm) / (per_it * 1e-3) / 1e9 / peak, 3)}
+               "unfused_model_frac": round((bn * 173 + 20 * op.gs.nperm) / (per_it * 1e-3) / 1e9 / peak, 3),
+               "global_counts": list(weak_counts(ws)) if ws > 1 else list(COUNTS),
+               "halo_neighbors": op.gs.ngh, "graph": bool(solver.use_graph)}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
