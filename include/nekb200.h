@@ -79,7 +79,9 @@ const char* nk_last_error(void);
 int nk_order_range(int* nmin, int* nmax);
 /* SM count and L2 size of the current device */
 int nk_device_info(int* sm_count, int64_t* l2_bytes, int* cc_major, int* cc_minor);
-/* write `bytes` of `buf` [dev] (L2 flush between timed reps) */
+/* L2 flush between timed reps: write the first half of `buf` [dev], then
+ * read the second half, so L2 ends cold AND clean (each half should exceed
+ * the 126 MB L2). */
 int nk_l2_flush(void* buf, int64_t bytes, nk_stream_t stream);
 
 /* diagnostic: BK5's HBM byte pattern without the arithmetic (read u and the
@@ -143,7 +145,7 @@ int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double*
            nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
            nk_stream_t stream);
 int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
-/* kernel variant selection: 0 = auto (4 for N = 7, else 3), 1 = k-slab (2D
+/* kernel variant selection: 0 = auto (= 3), 1 = k-slab (2D
  * thread plane, k-column in registers, D in shared memory), 3 = pencil
  * (register 1-D contractions, D in the constant bank, swizzled shared
  * transposes), 4 = pencil-TMA (persistent CTAs, cp.async.bulk 2-stage ring;

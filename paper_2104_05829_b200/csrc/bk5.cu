@@ -70,12 +70,14 @@ extern "C" int nk_bk5_bulk_launch(int N, int64_t nlist, const int32_t* elist, co
 extern "C" int nk_bk5_variant_get();
 
 static bool use_bulk(int N, int ncomp) { return nk_bk5_variant_get() == 2 && N == 7 && ncomp == 1; }
-// auto (0): pencil-TMA for N = 7 (measured best at the configs[1] size),
-// pencil for every other order (sweep6: TMA loses at N = 3, 5).
+// auto (0): pencil for every order -- measured best under the cold-and-clean
+// L2 protocol (sweep16: N=7 pencil 85.9% vs pencil-TMA 79.2% of HBM peak).
+// The fused BP5 step keeps its TMA pipeline (nk_bk5_pcg).
 static int kvariant_for(int N) {
   const int v = nk_bk5_variant_get();
   if (v == 1 || v == 3 || v == 4) return v;
-  return N == 7 ? 4 : 3;
+  (void)N;
+  return 3;
 }
 
 extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {

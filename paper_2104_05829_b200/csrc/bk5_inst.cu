@@ -49,7 +49,7 @@ template <int NQ> struct PencilDefault;
 #define NK_PD(NQ_, EPB_, MINB_) \
   template <> struct PencilDefault<NQ_> { static constexpr int EPB = EPB_, MINB = MINB_; };
 NK_PD(2, 32, 8) NK_PD(3, 14, 6) NK_PD(4, 4, 12) NK_PD(5, 5, 6) NK_PD(6, 2, 10) NK_PD(7, 2, 8)
-NK_PD(8, 1, 12) NK_PD(9, 1, 8) NK_PD(10, 1, 6) NK_PD(11, 1, 5) NK_PD(12, 1, 4) NK_PD(13, 1, 3)
+NK_PD(8, 1, 10) NK_PD(9, 1, 8) NK_PD(10, 1, 6) NK_PD(11, 1, 5) NK_PD(12, 1, 4) NK_PD(13, 1, 3)
 NK_PD(14, 1, 3) NK_PD(15, 1, 2) NK_PD(16, 1, 2)
 #undef NK_PD
 
@@ -81,9 +81,9 @@ int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, co
       case 5: return runp<8, 4, 2>(NK_PARGS);
       case 6: return runp<8, 8, 1>(NK_PARGS);
       case 7: return runp<8, 4, 3>(NK_PARGS);
-      case 8: return runp<8, 1, 10>(NK_PARGS);
+      case 8: return runp<8, 1, 12>(NK_PARGS);
       case 9: return runp<8, 1, 14>(NK_PARGS);
-      default: return runp<8, 1, 12>(NK_PARGS);   // measured best (sweep3)
+      default: return runp<8, 1, 10>(NK_PARGS);   // measured best (sweep16)
     }
   } else {
     return runp<NQ, PencilDefault<NQ>::EPB, PencilDefault<NQ>::MINB>(NK_PARGS);

@@ -155,6 +155,19 @@ __global__ void l2_flush_kernel(int4* buf, int64_t n16, int v) {
     buf[q] = make_int4(v, v, v, v);
 }
 
+// Read-only sweep: evicts the (dirty) lines the write sweep left in L2, so
+// the next timed kernel starts with a cold AND clean L2 (no write-backs of
+// flush data charged to it).
+__global__ void l2_clean_kernel(const int4* __restrict__ buf, int64_t n16, int* sink) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int acc = 0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n16; q += stride) {
+    const int4 v = __ldcg(buf + q);
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x7fffffff) *sink = acc;  // keep the loads alive
+}
+
 // Bandwidth probe with BK5's exact HBM pattern: per element read u (nq3) and
 // G (6 nq3), write w (nq3) -- no arithmetic beyond a sum.  The achievable
 // ceiling for the BK5 byte mix, measured the same way as BK5.
@@ -284,6 +297,12 @@ extern "C" int nk_l2_flush(void* buf, int64_t bytes, nk_stream_t stream) {
   }
   static int v = 0;
   ++v;
-  l2_flush_kernel<<<148 * 8, 256, 0, S(stream)>>>((int4*)buf, bytes / 16, v);
-  return check_launch("l2_flush");
+  // first half: write sweep (flush); second half: read sweep (clean)
+  const int64_t half16 = bytes / 32;
+  l2_flush_kernel<<<148 * 8, 256, 0, S(stream)>>>((int4*)buf, half16, v);
+  int rc = check_launch("l2_flush");
+  if (rc) return rc;
+  int4* second = (int4*)buf + half16;
+  l2_clean_kernel<<<148 * 8, 256, 0, S(stream)>>>(second, half16, (int*)buf);
+  return check_launch("l2_clean");
 }

@@ -71,7 +71,7 @@ def main():
     import paper_2104_05829_b200 as nk
     from paper_2104_05829_b200 import _lib
     L = _lib.lib()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     pk = peak()
     out = open(args.out, "a") if args.out else None
 
@@ -130,7 +130,7 @@ def main():
     if args.shapes:
         m = nk.build_box_mesh((1, 1, 1), (20, 20, 20), 7, deformation=("sine", 0.05))
         ref = None
-        for variant, cfg, pf in [(3, 0, 1), (3, 8, 1), (4, 0, 0), (4, 1, 0), (1, 4, 0)]:
+        for variant, cfg, pf in [(3, c, f) for c in (0, 8, 9, 2, 1, 5) for f in (0, 1)] + [(4, 0, 0), (4, 1, 0), (1, 4, 0)]:
             if True:
                 L.nk_bk5_set_variant(variant)
                 L.nk_bk5_tune(cfg, pf)
