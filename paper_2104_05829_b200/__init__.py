@@ -18,7 +18,7 @@ from .kernels import (apply_helmholtz_local, apply_mass, apply_stiffness_local, 
 from .mesh import (Mesh, assign_global_ids, build_box_mesh, geometric_factors,  # noqa: F401
                    read_hexmesh, write_hexmesh)
 from .partition import rcb  # noqa: F401
-from .solvers import (BreakdownError, FusedPCG, JacobiPreconditioner,  # noqa: F401
-                      PoissonOperator, pcg)
+from .solvers import (BreakdownError, FusedPCG, HelmholtzVectorSolver,  # noqa: F401
+                      JacobiPreconditioner, PoissonOperator, pcg)
 
 __version__ = "1.0.0"

@@ -2,6 +2,7 @@
 // heavily unrolled BK5 instantiations build in parallel.
 #include "bk5_tma.cuh"
 #include "bk5_pcg.cuh"
+#include "bk5_pencil3.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -143,6 +144,21 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
       if (NQ == 8 && cfg == 1) return runt<NQ, 2>(NK_TARGS);
       return runt<NQ, NQ == 8 ? 3 : (NQ == 6 ? 6 : 8)>(NK_TARGS);
 #undef NK_TARGS
+    }
+  }
+  if constexpr (NQ % 2 == 0 && NQ <= 10) {
+    // 3-component batch: G staged once per element (pencil3); k-slab otherwise
+    if (ncomp == 3 && variant != 1) {
+      if (nblocks) {
+        *nblocks = nlist;
+        return NK_OK;
+      }
+      if (st != nullptr) {
+        set_error("bk5: the fused dot is not available for ncomp = 3");
+        return NK_ERR_INVALID;
+      }
+      constexpr int M3 = NQ <= 6 ? 6 : (NQ == 8 ? 4 : 2);
+      return launch_pencil3<NQ, M3>(nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, s);
     }
   }
   if ((variant == 3 || variant == 4) && ncomp == 1)

@@ -29,7 +29,7 @@ from .gather_scatter import _halo_exchange, _halo_finish, _halo_start, _local, g
 from .kernels import COUNTERS, bk5_flops, extract_diagonal
 
 __all__ = ["pcg", "PCGResult", "BreakdownError", "PoissonOperator", "JacobiPreconditioner",
-           "FusedPCG", "inverse_multiplicity"]
+           "FusedPCG", "inverse_multiplicity", "HelmholtzVectorSolver"]
 
 PCGResult = namedtuple("PCGResult", "x iterations residual_history converged")
 
@@ -429,3 +429,48 @@ def _pcg_generic(apply_A, apply_M, b, tol, max_iter, flexible, weights, x0, host
     res = PCGResult(xo.cpu().numpy().reshape(shape) if host else xo, it,
                     hist[:it + 1].cpu().numpy().tolist(), bool(stt.converged))
     return res
+
+
+class HelmholtzVectorSolver:
+    """Viscous substep solve:
+    per-component Jacobi-PCG on H = lam0 A + lam1 B, e.g. lam0 = 1/Re,
+    lam1 = beta0/dt, for a 3-component (component-major) velocity field.
+    One operator, one Jacobi diagonal and one set of fused-PCG buffers are
+    shared by the components; each component is an independent FusedPCG
+    solve (its own scalars, convergence and iteration count).
+    ``apply(u3)`` is the batched operator (G read once for all components)."""
+
+    def __init__(self, mesh, lam0, lam1, gs=None, comm=None, tol=1e-6, max_iter=1000,
+                 chunk=16):
+        self.op = PoissonOperator(mesh, gs=gs, lam0=lam0, lam1=lam1, comm=comm)
+        self.jac = JacobiPreconditioner(self.op)
+        self.solver = FusedPCG(self.op, self.jac, tol=tol, max_iter=max_iter, chunk=chunk)
+        self.mesh = mesh
+
+    def apply(self, u3, out=None):
+        """w_c = mask * QQ^T (lam0 A_L + lam1 B) u_c for c = 0, 1, 2."""
+        import torch
+        from .gather_scatter import _local
+        from .kernels import apply_helmholtz_local
+        m = self.mesh
+        w = apply_helmholtz_local(u3, m, self.op.lam0, self.op.lam1, ncomp=3, out=out)
+        g = self.op.gs
+        if g.comm is not None and g.comm.size > 1:
+            for c in range(3):
+                gs_op(g, w.view(3, -1)[c])
+        else:
+            _local(g, w, "+", 3)
+        w.view(3, -1).mul_(m.mask.reshape(1, -1).to(w.dtype))
+        return w
+
+    def solve(self, b3):
+        """b3: (3, E, nq, nq, nq) CUDA float64 (assembled, masked).  Returns
+        (x3, [PCGResult per component])."""
+        import torch
+        x3 = torch.empty_like(b3)
+        results = []
+        for c in range(3):
+            r = self.solver.solve(b3[c].contiguous())
+            x3[c].copy_(r.x)
+            results.append(r._replace(x=x3[c]))
+        return x3, results

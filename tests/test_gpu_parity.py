@@ -343,3 +343,33 @@ def test_host_streamed_apply_matches_device_path():
         nk.apply_stiffness_local(uh, m, out=wh, nchunks=chunks)
         assert np.array_equal(wh.numpy(), wd)
     assert rel_l2(wd, oop.bk5(o.basis.diff, o.G, u)) < BK5_TOL
+
+
+def test_helmholtz_vector_solve_config5_scaled():
+    """configs[4] scaled to one GPU: 3-component Helmholtz, N=9,
+    lam0 = 1/Re (Re=1000), lam1 = beta0/dt (11/6 / 1e-3), rhs default_rng(5+c),
+    tol 1e-6; per-component iterations within +-1 of the oracle."""
+    N = 9
+    m, o = both_meshes((3, 3, 3), N)
+    lam0, lam1 = 1e-3, (11.0 / 6.0) / 1e-3
+    solver = nk.HelmholtzVectorSolver(m, lam0, lam1, tol=1e-6)
+    mask = o.mask.ravel()
+    sh = (o.G.shape[0],) + o.G.shape[2:]
+    bs = np.stack([mask * ogs.gs_op(o.ids, np.random.default_rng(5 + c).standard_normal(o.ids.size))
+                   for c in range(3)])
+    x3, res = solver.solve(dev(bs.reshape((3,) + sh)))
+    D, G, B = o.basis.diff, o.G, o.B
+    A = lambda v: mask * ogs.gs_op(o.ids, oop.bk5(D, G, v.reshape(sh), lam0, B, lam1).ravel())
+    inv = mask / ogs.gs_op(o.ids, oop.local_diagonal(D, G, lam0, B, lam1).ravel())
+    wt = 1.0 / ogs.multiplicity(o.ids)
+    x3h = x3.cpu().numpy().reshape(3, -1)
+    for c in range(3):
+        ref = osol.pcg(A, lambda r: inv * r, bs[c], tol=1e-6, max_iter=1000, weights=wt)
+        assert res[c].converged and abs(res[c].iterations - ref.iterations) <= 1
+        assert np.max(np.abs(x3h[c] - ref.x)) < 1e-9 * max(1.0, np.max(np.abs(ref.x)))
+    # batched operator == per-component operator
+    u3 = dev(np.stack([o.mask * np.random.default_rng(c).standard_normal(sh) for c in range(3)]))
+    w3 = solver.apply(u3).cpu().numpy().reshape(3, -1)
+    for c in range(3):
+        ref = A(u3[c].cpu().numpy().ravel())
+        assert rel_l2(w3[c], ref) < BK5_TOL
