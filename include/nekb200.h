@@ -235,10 +235,11 @@ int nk_cg_init_finalize(nk_cg_state* st, double* hist, nk_stream_t stream);
 /* alpha = rz/pAp (breakdown if pAp <= 0); x += alpha p; r -= alpha Ap;
  * local sums rr, rz_new (z = invD r; skipped if invD NULL), zap into st.
  * x = p = NULL selects the fused-BP5 form (x update deferred to nk_bk5_pcg;
- * advances st->iter). */
+ * advances st->iter).  Dot weights: wt [dev, FP64] if given, else
+ * 1/mult with mult [dev, u8 multiplicity], else 1. */
 int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap,
-                 const double* invD, const double* wt, nk_cg_state* st, double* partials,
-                 nk_stream_t stream);
+                 const double* invD, const double* wt, const uint8_t* mult, nk_cg_state* st,
+                 double* partials, nk_stream_t stream);
 
 /* convergence test on st->rr; else beta (Fletcher-Reeves, or Polak-Ribiere
  * -alpha*zap/rz when flexible) and p = z + beta p with z = invD r (or the

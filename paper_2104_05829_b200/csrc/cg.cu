@@ -103,10 +103,16 @@ template <bool VEC, bool FUSED>
 __global__ void __launch_bounds__(kVecThreads)
 cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                  const double* __restrict__ p, const double* __restrict__ Ap,
-                 const double* __restrict__ invD, const double* __restrict__ wt, nk_cg_state* st,
+                 const double* __restrict__ invD, const double* __restrict__ wt,
+                 const uint8_t* __restrict__ mult, nk_cg_state* st,
                  double* __restrict__ partials) {
   __shared__ double red[3 * 32];
+  __shared__ double rcp_tab[256];  // exact 1/m for the u8 multiplicity weights
   if (st->done) return;
+  if (mult != nullptr) {
+    for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
+    __syncthreads();
+  }
   const double pAp = st->pAp;
   if (!(pAp > 0.0)) {  // indefiniteness / breakdown; uniform branch
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -126,7 +132,15 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
     const double2 pv = FUSED ? make_double2(0, 0) : __ldg(reinterpret_cast<const double2*>(p) + q);
     const double2 av = __ldg(reinterpret_cast<const double2*>(Ap) + q);
     const double2 dv = hz ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
-    const double2 wv = wt ? __ldg(reinterpret_cast<const double2*>(wt) + q) : make_double2(1, 1);
+    double2 wv;
+    if (wt) {
+      wv = __ldg(reinterpret_cast<const double2*>(wt) + q);
+    } else if (mult) {  // 1-byte multiplicity: the l2 weight is 1/mult
+      const uchar2 mv = __ldg(reinterpret_cast<const uchar2*>(mult) + q);
+      wv = make_double2(rcp_tab[mv.x], rcp_tab[mv.y]);
+    } else {
+      wv = make_double2(1, 1);
+    }
     upd_point<FUSED>(alpha, xv.x, rv.x, pv.x, av.x, dv.x, wv.x, hz, acc);
     upd_point<FUSED>(alpha, xv.y, rv.y, pv.y, av.y, dv.y, wv.y, hz, acc);
     if (!FUSED) reinterpret_cast<double2*>(x)[q] = xv;
@@ -146,13 +160,13 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
       const int64_t t = n - 1;
       double xd = 0.0;
       upd_point<FUSED>(alpha, FUSED ? xd : x[t], r[t], FUSED ? 0.0 : p[t], Ap[t],
-                       hz ? invD[t] : 0.0, wt ? wt[t] : 1.0, hz, acc);
+                       hz ? invD[t] : 0.0, wt ? wt[t] : (mult ? rcp_tab[mult[t]] : 1.0), hz, acc);
     }
   } else {
     for (int64_t q = gtid; q < n; q += nthr) {
       double xd = 0.0;
       upd_point<FUSED>(alpha, FUSED ? xd : x[q], r[q], FUSED ? 0.0 : p[q], Ap[q],
-                       hz ? invD[q] : 0.0, wt ? wt[q] : 1.0, hz, acc);
+                       hz ? invD[q] : 0.0, wt ? wt[q] : (mult ? rcp_tab[mult[q]] : 1.0), hz, acc);
     }
   }
   double v[3] = {acc.rr, acc.rz, acc.zap};
@@ -293,24 +307,24 @@ extern "C" int nk_cg_init_finalize(nk_cg_state* st, double* hist, nk_stream_t st
 }
 
 extern "C" int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap,
-                            const double* invD, const double* wt, nk_cg_state* st,
-                            double* partials, nk_stream_t stream) {
+                            const double* invD, const double* wt, const uint8_t* mult,
+                            nk_cg_state* st, double* partials, nk_stream_t stream) {
   if (n < 0 || !r || !Ap || !st || !partials || (x != nullptr && p == nullptr)) {
     set_error("cg_update: invalid arguments");
     return NK_ERR_INVALID;
   }
   const unsigned g = (unsigned)vec_grid(n);
   cudaStream_t s = S(stream);
-  const bool vec = aligned16(x, r, p, Ap, invD, wt);
+  const bool vec = aligned16(x, r, p, Ap, invD, wt) && (((uintptr_t)mult & 1) == 0);
   if (x == nullptr) {  // fused BP5 path
     if (vec)
-      cg_update_kernel<true, true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+      cg_update_kernel<true, true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, mult, st, partials);
     else
-      cg_update_kernel<false, true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+      cg_update_kernel<false, true><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, mult, st, partials);
   } else if (vec) {
-    cg_update_kernel<true, false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+    cg_update_kernel<true, false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, mult, st, partials);
   } else {
-    cg_update_kernel<false, false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, st, partials);
+    cg_update_kernel<false, false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, mult, st, partials);
   }
   return check_launch("cg_update");
 }

@@ -73,12 +73,26 @@ class PoissonOperator:
                                                      device=mesh.device)
         self.n = mesh.n_local
         self._wt = None
+        self._mult = None
 
     @property
     def weights(self):
         if self._wt is None:
             self._wt = inverse_multiplicity(self.gs, self.n, self.mesh.device)
         return self._wt
+
+    @property
+    def multiplicity_u8(self):
+        """Global multiplicity of every local point as uint8 (the fused CG
+        update reads 1 byte instead of an FP64 weight)."""
+        import torch
+        if self._mult is None:
+            one = torch.ones(self.n, dtype=torch.float64, device=self.mesh.device)
+            gs_op(self.gs, one)
+            if float(one.max()) > 255:
+                raise ContractError("multiplicity > 255 cannot be stored as uint8")
+            self._mult = torch.round(one).to(torch.uint8)
+        return self._mult
 
     def __call__(self, p, out=None):
         import torch
@@ -239,7 +253,10 @@ class FusedPCG:
         self.part_cg = torch.zeros(int(lib().nk_cg_partials_len(n)), dtype=torch.float64,
                                    device=dev)
         self.hist = torch.zeros(self.max_iter + 2, dtype=torch.float64, device=dev)
+        # FP64 1/mult weights: measured slightly faster than the u8 multiplicity
+        # option of nk_cg_update (latency- not byte-bound kernel)
         self.wt = op.weights
+        self.mult = None
         self.invD = prec.invD
         self.comm = op.gs.comm if (op.gs.comm is not None and op.gs.comm.size > 1) else None
         self.s64 = self.st.view(torch.float64)   # rz pAp rz_new rr zap bb thresh2 alpha
@@ -258,7 +275,8 @@ class FusedPCG:
                           self.hist)
         self._allreduce(1, 2)                                            # pAp
         check(L.nk_cg_update(self.n, None, ptr(self.r), None, ptr(self.w), ptr(self.invD),
-                             ptr(self.wt), ptr(self.st), ptr(self.part_cg), s), "cg_update")
+                             ptr(self.wt), ptr(self.mult), ptr(self.st), ptr(self.part_cg), s),
+              "cg_update")
         self._allreduce(2, 5)                                            # rz_new rr zap
 
     def _capture(self):
@@ -293,7 +311,8 @@ class FusedPCG:
             _local(g, self.w, "+", 1, st=self.st)
             ev[2].record()
             check(L.nk_cg_update(self.n, None, ptr(self.r), None, ptr(self.w), ptr(self.invD),
-                                 ptr(self.wt), ptr(self.st), ptr(self.part_cg), s), "cg_update")
+                                 ptr(self.wt), ptr(self.mult), ptr(self.st), ptr(self.part_cg),
+                                 s), "cg_update")
             ev[3].record()
             torch.cuda.synchronize()
             for q, nm in enumerate(names):
@@ -411,7 +430,7 @@ def _pcg_generic(apply_A, apply_M, b, tol, max_iter, flexible, weights, x0, host
     while not stt.done:
         Ap = flat(apply_A(p.view_as(b))).contiguous()
         check(L.nk_wdot(n, ptr(p), ptr(Ap), ptr(wt), ptr(s64[1:2]), ptr(part), s), "wdot")
-        check(L.nk_cg_update(n, ptr(x), ptr(r), ptr(p), ptr(Ap), None, ptr(wt), ptr(st),
+        check(L.nk_cg_update(n, ptr(x), ptr(r), ptr(p), ptr(Ap), None, ptr(wt), None, ptr(st),
                              ptr(part), s), "cg_update")
         z = flat(apply_M(r.view_as(b))).contiguous()
         check(L.nk_wdot(n, ptr(r), ptr(z), ptr(wt), ptr(s64[2:3]), ptr(part), s), "wdot")

@@ -64,6 +64,7 @@ def main():
     ap.add_argument("--shapes", action="store_true")
     ap.add_argument("--orders", action="store_true")
     ap.add_argument("--probe", action="store_true")
+    ap.add_argument("--helm3", action="store_true")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
@@ -127,6 +128,39 @@ def main():
                   "frac": round(bytes_ / ms / 1e6 / pk, 4)})
         L.nk_bk5_set_variant(0)
         del m2, u2, w2
+    if args.helm3:
+        from paper_2104_05829_b200._lib import ptr
+        s = torch.cuda.current_stream()
+        for N, ne in ((9, 16), (7, 20), (5, 29)):
+            m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
+            n = m.n_local
+            u3 = torch.randn(3 * n, dtype=torch.float64, device="cuda")
+            w3 = torch.empty_like(u3)
+            lam0, lam1 = 1e-3, 11 / 6 / 1e-3
+            def batched():
+                L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(u3), ptr(w3), lam0, ptr(m.B),
+                         lam1, 3, n, None, None, 0, None, None, 0, 0, s.cuda_stream)
+            def separate():
+                for c in range(3):
+                    L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), u3.data_ptr() + 8 * c * n,
+                             w3.data_ptr() + 8 * c * n, lam0, ptr(m.B), lam1, 1, n, None, None,
+                             0, None, None, 0, 0, s.cuda_stream)
+            for name, fn, bpp in (("batched3", batched, 104), ("3x scalar", separate, 216)):
+                ts = []
+                for rep in range(args.reps + 5):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    L.nk_l2_flush(ptr(flush), flush.numel(), s.cuda_stream)
+                    a.record(s)
+                    fn()
+                    b.record(s)
+                    ts.append((a, b))
+                torch.cuda.synchronize()
+                ms = statistics.median([a.elapsed_time(b) for a, b in ts[5:]])
+                emit({"sweep": "helm3", "N": N, "E": m.E, "kernel": name, "ms_med": round(ms, 5),
+                      "alg_bytes_per_pt": bpp,
+                      "frac_of_own_bytes": round(bpp * n / ms / 1e6 / pk, 4),
+                      "gdofs_3comp": round(3 * m.E * N ** 3 / ms / 1e6, 3)})
+            del m, u3, w3
     if args.shapes:
         m = nk.build_box_mesh((1, 1, 1), (20, 20, 20), 7, deformation=("sine", 0.05))
         ref = None
