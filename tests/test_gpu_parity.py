@@ -373,3 +373,55 @@ def test_helmholtz_vector_solve_config5_scaled():
     for c in range(3):
         ref = A(u3[c].cpu().numpy().ravel())
         assert rel_l2(w3[c], ref) < BK5_TOL
+
+
+def test_hexmesh_loaded_mesh_on_device(tmp_path):
+    """HEXMESH v1 -> mesh_from_coords (device geometry, coordinate-snapped ids)
+    -> BK5 + gs; equals the generated mesh's results."""
+    N = 4
+    m, o = both_meshes((3, 2, 2), N, deformation=("sine", 0.05))
+    p = tmp_path / "box.hex"
+    nk.write_hexmesh(p, o.xyz, o.ids, {"pressure": o.mask.astype(int)})
+    E, NN, xyz, ids, masks = nk.read_hexmesh(p)
+    mf = nk.mesh.mesh_from_coords(xyz, NN, ids=None, mask=masks["pressure"])
+    fid = mf.ids.cpu().numpy()
+    # same coincidence classes (numbering follows deformed-coordinate order)
+    pairs = np.unique(np.stack([fid, o.ids]), axis=1)
+    assert pairs.shape[1] == len(np.unique(fid)) == len(np.unique(o.ids))
+    assert rel_l2(mf.G.cpu().numpy(), o.G) < 1e-13
+    rng = np.random.default_rng(9)
+    u = rng.standard_normal((E, N + 1, N + 1, N + 1))
+    w = nk.apply_stiffness_local(dev(u), mf).cpu().numpy()
+    assert rel_l2(w, oop.bk5(o.basis.diff, o.G, u)) < BK5_TOL
+
+
+def test_gs_op_overlapped_single_rank():
+    """overlapped == local_work on everything then gs_op."""
+    N = 5
+    m, o = both_meshes((3, 3, 2), N)
+    h = nk.gs_setup(m.ids, nq=N + 1)
+    rng = np.random.default_rng(4)
+    u = dev(rng.standard_normal((m.E, N + 1, N + 1, N + 1)))
+    field = torch.zeros_like(u)
+
+    def local_work(elems):
+        nk.apply_stiffness_local(u, m, out=field, elements=elems)
+
+    nk.gs_op_overlapped(h, local_work, field)
+    ref = ogs.gs_op(o.ids, oop.bk5(o.basis.diff, o.G, u.cpu().numpy()).ravel())
+    assert rel_l2(field.cpu().numpy().ravel(), ref) < BK5_TOL
+
+
+def test_fused_pcg_u8_multiplicity_weights():
+    m, o = both_meshes((4, 4, 4), 7)
+    b, _, _, _ = _oracle_problem(o)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    s1 = nk.FusedPCG(op, jac, tol=1e-8)
+    r1 = s1.solve(dev(b))
+    x1 = r1.x.cpu().numpy().copy()
+    s2 = nk.FusedPCG(op, jac, tol=1e-8)
+    s2.wt, s2.mult = None, op.multiplicity_u8
+    r2 = s2.solve(dev(b))
+    assert r1.iterations == r2.iterations
+    assert np.max(np.abs(x1 - r2.x.cpu().numpy())) < 1e-12 * np.max(np.abs(x1))
