@@ -322,8 +322,9 @@ class FusedPCG:
 
     def init(self, b):
         L, s = lib(), stream_ptr()
+        # init always uses the FP64 weights (exactly 1/mult, equal to the u8 path)
         check(L.nk_cg_init(self.n, ptr(b), ptr(self.x), ptr(self.r), ptr(self.p),
-                           ptr(self.invD), ptr(self.wt), ptr(self.st), ptr(self.part_cg),
+                           ptr(self.invD), ptr(self.op.weights), ptr(self.st), ptr(self.part_cg),
                            self.tol, self.max_iter, int(self.flexible), s), "cg_init")
         self._allreduce(0, 1)   # rz
         self._allreduce(3, 4)   # rr
