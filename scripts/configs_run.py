@@ -1,0 +1,175 @@
+#!/usr/bin/env python
+"""Run BASELINE.json configs on ONE GPU and print one JSON line each.
+
+  [0] BP5 Jacobi-PCG, 4x4x4 box, N=7, tol 1e-8: GPU fused PCG vs the CPU
+      oracle (iterations, time to solution, GDOF/s)
+  [2] BP5 on the E=64^3, N=7 box (89.9M DOF) on one GPU: full solve to 1e-8
+  [3] weak-scaling point: 20^3 elements per GPU (see bench.py bp5)
+  [4] vector Helmholtz, E=48^3, N=9, 3 components (332M local points), tol 1e-6
+      (the 8-GPU config run on one B200)
+
+    python scripts/configs_run.py [--which 0 2 4] [--out file]
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def rhs_sine(mesh, gsh):
+    import torch
+    import paper_2104_05829_b200 as nk
+    # f = 3 pi^2 sin(pi x) sin(pi y) sin(pi z) at the (deformed) points
+    xyz = mesh.xyz.reshape(3, -1)
+    f = 3 * np.pi ** 2 * torch.sin(np.pi * xyz[0]) * torch.sin(np.pi * xyz[1]) * \
+        torch.sin(np.pi * xyz[2])
+    b = f * mesh.B.reshape(-1)
+    nk.gs_op(gsh, b)
+    return b * mesh.mask.reshape(-1).to(b.dtype)
+
+
+def timed_solve(nk, op, jac, b, tol, max_iter):
+    import torch
+    s = nk.FusedPCG(op, jac, tol=tol, max_iter=max_iter, chunk=32)
+    s.solve(b)                            # warm + capture
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = s.solve(b)
+    torch.cuda.synchronize()
+    return res, time.perf_counter() - t0
+
+
+def config0(out):
+    import torch
+    import paper_2104_05829_b200 as nk
+    from oracle import gs as ogs
+    from oracle import mesh as om
+    from oracle import operators as oop
+    from oracle import solvers as osol
+    N = 7
+    for deform in (None, ("sine", 0.05)):
+        m = nk.build_box_mesh((1, 1, 1), (4, 4, 4), N, deformation=deform, keep_coords=True)
+        op = nk.PoissonOperator(m)
+        jac = nk.JacobiPreconditioner(op)
+        b = rhs_sine(m, op.gs)
+        res, t_gpu = timed_solve(nk, op, jac, b, 1e-8, 1000)
+        o = om.build_box_mesh((1, 1, 1), (4, 4, 4), N, deformation=deform)
+        X = o.xyz.reshape(3, -1)
+        f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+        mask = o.mask.ravel()
+        bo = mask * ogs.gs_op(o.ids, o.B.ravel() * f)
+        sh = (o.G.shape[0],) + o.G.shape[2:]
+        A = lambda v: mask * ogs.gs_op(o.ids, oop.bk5(o.basis.diff, o.G, v.reshape(sh)).ravel())
+        inv = mask / ogs.gs_op(o.ids, oop.local_diagonal(o.basis.diff, o.G).ravel())
+        t0 = time.perf_counter()
+        ref = osol.pcg(A, lambda r: inv * r, bo, tol=1e-8, max_iter=1000,
+                       weights=1.0 / ogs.multiplicity(o.ids))
+        t_cpu = time.perf_counter() - t0
+        exact = np.prod(np.sin(np.pi * X), axis=0)
+        dof = 64 * N ** 3
+        out({"config": 0, "deformed": deform is not None, "iterations_gpu": res.iterations,
+             "iterations_oracle": ref.iterations, "converged": res.converged,
+             "max_abs_x_diff": float(np.max(np.abs(res.x.cpu().numpy().ravel() - ref.x))),
+             "max_err_vs_exact_solution": float(np.max(np.abs(ref.x - exact) * mask)),
+             "gpu_s": round(t_gpu, 5), "cpu_oracle_s": round(t_cpu, 3),
+             "gpu_gdof_iter_per_s": round(dof * res.iterations / t_gpu / 1e9, 3),
+             "cpu_gdof_iter_per_s": round(dof * ref.iterations / t_cpu / 1e9, 5)})
+
+
+def config2(out):
+    import torch
+    import paper_2104_05829_b200 as nk
+    N = 7
+    t0 = time.perf_counter()
+    m = nk.build_box_mesh((1, 1, 1), (64, 64, 64), N, deformation=("sine", 0.05),
+                          keep_coords=True)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    b = rhs_sine(m, op.gs)
+    m.xyz = None
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    res, t = timed_solve(nk, op, jac, b, 1e-8, 5000)
+    dof = m.E * N ** 3
+    out({"config": 2, "E": m.E, "N": N, "dof": dof, "local_points": m.n_local,
+         "iterations": res.iterations, "converged": res.converged, "solve_s": round(t, 4),
+         "ms_per_iteration": round(1e3 * t / max(res.iterations, 1), 4),
+         "gdof_iter_per_s": round(dof * res.iterations / t / 1e9, 3),
+         "setup_s": round(setup, 2), "gpus": 1})
+
+
+def config4(out):
+    import torch
+    import paper_2104_05829_b200 as nk
+    N, ne = 9, 48
+    lam0, lam1 = 1.0 / 1000.0, (11.0 / 6.0) / 1e-3
+    t0 = time.perf_counter()
+    m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
+    hs = nk.HelmholtzVectorSolver(m, lam0, lam1, tol=1e-6, max_iter=2000, chunk=16)
+    n = m.n_local
+    b3 = torch.empty((3, n), dtype=torch.float64, device="cuda")
+    for c in range(3):
+        g = torch.Generator(device="cuda").manual_seed(5 + c)
+        b3[c] = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+        nk.gs_op(hs.op.gs, b3[c])
+    b3 *= m.mask.reshape(1, -1).to(torch.float64)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    hs.solve(b3[:, :].reshape((3,) + m.field_shape()))      # warm + capture
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x3, res = hs.solve(b3.reshape((3,) + m.field_shape()))
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    it = [r.iterations for r in res]
+    dof = m.E * N ** 3
+    # batched operator throughput (G read once for 3 components)
+    u3 = torch.randn((3, n), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        hs.apply(u3)
+    torch.cuda.synchronize()
+    a, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(10):
+        hs.apply(u3)
+    bb.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(bb) / 10
+    out({"config": 4, "E": m.E, "N": N, "components": 3, "local_points_per_comp": n,
+         "iterations": it, "converged": [r.converged for r in res], "solve_s": round(t, 4),
+         "gdof_iter_per_s": round(dof * sum(it) / t / 1e9, 3), "setup_s": round(setup, 2),
+         "batched_apply_ms": round(ms, 4),
+         "batched_apply_gdofs_3comp": round(3 * dof / ms / 1e6, 2), "gpus": 1,
+         "note": "configs[4] names 8 GPUs; run here on one B200 (same global problem)"})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", nargs="*", type=int, default=[0, 2, 4])
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import torch
+    torch.cuda.set_device(0)
+    f = open(args.out, "a") if args.out else None
+
+    def out(d):
+        line = json.dumps(d)
+        print(line, flush=True)
+        if f:
+            f.write(line + "\n")
+            f.flush()
+
+    for c in args.which:
+        {0: config0, 2: config2, 4: config4}[c](out)
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
