@@ -201,10 +201,18 @@ class PoissonOperator:
         return w
 
     def partials_len(self):
+        """Per-block partial slots for the fused p.Ap: one launch over all
+        elements, or boundary + interior launches on several ranks (each can
+        use a full persistent grid)."""
         m = self.mesh
         L = lib()
-        return max(int(L.nk_bk5_blocks(m.N, m.E, self.ncomp)),
-                   int(L.nk_bk5_pcg_blocks(m.N, m.E)), 1) + 2
+        g = self.gs
+        sizes = [m.E]
+        if g.comm is not None and g.comm.size > 1:
+            sizes = [int(g.boundary_elements.numel()), int(g.interior_elements.numel())]
+        tot_bk5 = sum(int(L.nk_bk5_blocks(m.N, n, self.ncomp)) for n in sizes if n)
+        tot_pcg = sum(int(L.nk_bk5_pcg_blocks(m.N, n)) for n in sizes if n)
+        return max(tot_bk5, tot_pcg, 1) + 2
 
 
 class JacobiPreconditioner:

@@ -63,13 +63,14 @@ def _worker(rank, world, port, outdir, counts, N):
         dist.destroy_process_group()
 
 
-def test_two_ranks_one_gpu_gs_and_pcg():
+@pytest.mark.parametrize("N", [5, 7])      # N=7 exercises the persistent TMA step
+def test_two_ranks_one_gpu_gs_and_pcg(N):
     import torch.multiprocessing as mp
     from oracle import gs as ogs
     from oracle import mesh as om
     from oracle import operators as oop
     from oracle import solvers as osol
-    counts, N, world = (4, 4, 2), 5, 2
+    counts, world = (4, 4, 2), 2
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(world, _port(), d, counts, N), nprocs=world, join=True)
         res = [np.load(os.path.join(d, f"r{r}.npz")) for r in range(world)]
