@@ -28,15 +28,33 @@
 
 namespace nk {
 
+// Shared layout of one element buffer: idx(k,j,i) = k*P + j*R + i', with
+// i' = i ^ ((j>>1) | (k&1)<<2) at NQ = 8 (conflict-free for all three pencil
+// orientations) and i' = (i + C2*k) mod NQ otherwise.  (R, P, C2) per order
+// come from scripts/smem_layout_search.py: minimum modeled shared wavefronts
+// (half-warp, 8-byte banks) over the i-, j- and k-pencil accesses without
+// growing the buffer.
+template <int NQ> struct PencilPad { static constexpr int R = (NQ % 2 == 0) ? NQ + 1 : NQ,
+  P = NQ * R + ((NQ * R) % 2 == 0 ? 1 : 0), C2 = 0; };
+template <> struct PencilPad<2> { static constexpr int R = 2, P = 6, C2 = 1; };
+template <> struct PencilPad<4> { static constexpr int R = 4, P = 20, C2 = 1; };
+template <> struct PencilPad<6> { static constexpr int R = 6, P = 38, C2 = 3; };
+template <> struct PencilPad<8> { static constexpr int R = 8, P = 72, C2 = 0; };
+template <> struct PencilPad<10> { static constexpr int R = 10, P = 101, C2 = 0; };
+template <> struct PencilPad<12> { static constexpr int R = 13, P = 156, C2 = 0; };
+template <> struct PencilPad<14> { static constexpr int R = 14, P = 197, C2 = 0; };
+template <> struct PencilPad<16> { static constexpr int R = 16, P = 256, C2 = 0; };
+
 template <int NQ>
 struct PencilLayout {
-  // NQ = 8: swizzled, conflict-free for the three access orientations.
-  // Other orders: padded rows (odd stride), a few residual conflicts.
-  static constexpr int R = (NQ == 8) ? 8 : ((NQ % 2 == 0) ? NQ + 1 : NQ);
-  static constexpr int P = (NQ == 8) ? 72 : (NQ * R + ((NQ * R) % 2 == 0 ? 1 : 0));
+  static constexpr int R = PencilPad<NQ>::R;
+  static constexpr int P = PencilPad<NQ>::P;
+  static constexpr int C2 = PencilPad<NQ>::C2;
   static constexpr int VOL = NQ * P;
   __device__ __forceinline__ static int idx(int k, int j, int i) {
     if (NQ == 8) return k * P + j * R + (i ^ ((j >> 1) | ((k & 1) << 2)));
+    if (NQ == 16) return k * P + j * R + (i ^ j);   // conflict-free, no padding
+    if (C2 != 0) return k * P + j * R + ((i + C2 * k) % NQ);
     return k * P + j * R + i;
   }
 };
