@@ -451,7 +451,7 @@ def run_ours(args):
             "e2e": {"value": round(e2e_val, 4), "unit": "GDOF/s",
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "ms_per_step": round(e2e_ms, 4), "bitwise_equal_to_device_path": e2e_ok,
-                    "path": "apply_stiffness_local(pinned host u) -> pinned host w; 4 chunks, "
+                    "path": "apply_stiffness_local(pinned host u) -> pinned host w; 6 tapered chunks, "
                             "H2D/BK5/D2H overlapped on 3 streams (cached CUDA graph)"},
             "gpu_launches": launches,
             "roofline_context": ceiling,
