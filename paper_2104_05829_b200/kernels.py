@@ -65,6 +65,8 @@ def _bk5(u, mesh, lam0, lam1, ncomp, out=None, elements=None, mask=False, st=Non
     if u.numel() != nloc * ncomp:
         raise ContractError(f"contract error: field length {u.numel()} != {nloc * ncomp}")
     w = torch.empty_like(u) if out is None else out
+    if elements is not None and elements.numel() == 0:
+        return w            # empty subset (its data pointer is NULL = "all" in the ABI)
     D = mesh.basis.diff  # host array: baked into the launch parameters
     nl = 0 if elements is None else int(elements.numel())
     check(lib().nk_bk5(mesh.N, mesh.E, ptr(D), ptr(mesh.G), ptr(u), ptr(w), float(lam0),

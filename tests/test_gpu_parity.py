@@ -425,3 +425,55 @@ def test_fused_pcg_u8_multiplicity_weights():
     r2 = s2.solve(dev(b))
     assert r1.iterations == r2.iterations
     assert np.max(np.abs(x1 - r2.x.cpu().numpy())) < 1e-12 * np.max(np.abs(x1))
+
+
+# ---------------------------------------------------------------- edge cases
+def test_edge_empty_and_ragged():
+    N = 3
+    m, o = both_meshes((2, 2, 1), N)
+    u = dev(np.random.default_rng(0).standard_normal((m.E, 4, 4, 4)))
+    w = torch.full_like(u, 3.0)
+    nk.apply_stiffness_local(u, m, out=w, elements=torch.zeros(0, dtype=torch.int32,
+                                                                 device="cuda"))
+    assert torch.all(w == 3.0)                       # empty element list: no-op
+    h = nk.gs_setup(np.zeros(0, dtype=np.int64))
+    assert h.nseg == 0
+    nk.gs_op(h, torch.zeros(0, dtype=torch.float64, device="cuda"))
+    with pytest.raises(nk.UnsupportedOrderError):
+        from paper_2104_05829_b200._lib import check, lib, ptr
+        check(lib().nk_bk5(16, 1, ptr(np.zeros(289)), 1, 1, 1, 1.0, None, 0.0, 1, 1, None, None,
+                           0, None, None, 0, 0, None), "bk5")
+    with pytest.raises(nk.ContractError):
+        nk.apply_stiffness_local(u.float(), m)
+
+
+def test_edge_gs_large_multiplicities_and_many_classes():
+    """multiplicity up to 40 (> 32: CSR remainder path) and > 16 distinct
+    multiplicities (class table overflow) stay bit-exact."""
+    rng = np.random.default_rng(21)
+    ids = []
+    for g, mult in enumerate(list(range(1, 41)) + [2, 3, 5, 7] * 50, start=1):
+        ids += [g] * mult
+    ids = np.array(ids, dtype=np.int64)
+    rng.shuffle(ids)
+    w = rng.standard_normal(ids.size)
+    h = nk.gs_setup(ids)
+    assert h.plan.rest is not None
+    for op in ("+", "*", "min", "max"):
+        got = nk.gs_op(h, dev(w.copy()), op).cpu().numpy()
+        assert np.array_equal(got, ogs.gs_op(ids, w, op)), op
+
+
+def test_edge_fused_pcg_zero_rhs_and_all_dirichlet():
+    m, o = both_meshes((2, 2, 2), 7)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    r = nk.FusedPCG(op, jac, tol=1e-8).solve(torch.zeros(m.n_local, dtype=torch.float64,
+                                                        device="cuda"))
+    assert r.iterations == 0 and r.converged and float(r.x.abs().max()) == 0.0
+    # single element, all faces Dirichlet, N=1: every point is masked -> b = 0
+    m1 = nk.build_box_mesh((1, 1, 1), (1, 1, 1), 1, bc="dirichlet")
+    op1 = nk.PoissonOperator(m1)
+    r1 = nk.pcg(op1, nk.JacobiPreconditioner(op1),
+                torch.zeros(8, dtype=torch.float64, device="cuda"))
+    assert r1.iterations == 0
