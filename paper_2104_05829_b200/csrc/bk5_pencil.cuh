@@ -88,7 +88,7 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
            const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
            double lam0, const double* __restrict__ B, double lam1,
            const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
-           int64_t part_base, int64_t reduce_count, int pfG) {
+           int64_t part_base, int64_t reduce_count, int pfG, int64_t pf_ahead) {
   using L = PencilLayout<NQ>;
   constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, VOL = L::VOL;
   extern __shared__ double smem[];
@@ -110,6 +110,12 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   // Start this element's G (75% of its bytes) streaming into L2 now, so the
   // G-phase loads after F1-F3 hit L2 instead of waiting on HBM.
   if (pfG && active && tt == 0) prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
+  // optionally also the element one resident wave ahead (u and G)
+  if (pf_ahead > 0 && tt == 0 && slot + pf_ahead < nlist) {
+    const int64_t ea = elist ? (int64_t)elist[slot + pf_ahead] : slot + pf_ahead;
+    prefetch_l2(G + ea * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
+    prefetch_l2(u + ea * NQ3, NQ3 * (int64_t)sizeof(double));
+  }
 
   // ---- F1: i-pencils (j = a, k = b)
   if (active) {
@@ -246,6 +252,7 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
                          double* partials, int64_t part_base, int64_t reduce_count,
                          cudaStream_t s, int pfG) {
   using C = PencilCfg<NQ, EPB, MINB>;
+  static int64_t resident = -1;  // CTAs resident on the device (one wave)
   const size_t smem = C::smem_bytes();
   static bool configured = false;
   if (!configured) {
@@ -259,10 +266,21 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
   }
   const int64_t nblk = (nlist + EPB - 1) / EPB;
   if (nblk == 0) return NK_OK;
+  if (resident < 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil<NQ, EPB, MINB>, C::THREADS,
+                                                  smem);
+    resident = (int64_t)sms * (per > 0 ? per : 1);
+  }
   DParam<NQ> D;
   for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  // pfG: 0 off, 1 own G into L2, 2 own G + the element one wave ahead
+  const int64_t ahead = pfG >= 2 ? resident * EPB : 0;
   bk5_pencil<NQ, EPB, MINB><<<(unsigned)nblk, C::THREADS, smem, s>>>(
-      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG);
+      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG,
+      ahead);
   return check_launch("bk5_pencil");
 }
 

@@ -185,7 +185,7 @@ def main():
         for N in range(1, 16):
             ne = E_FOR_N[N]
             m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
-            for variant, pf in ((3, 1),):
+            for variant, pf in ((3, 1), (3, 2)):
                 L.nk_bk5_set_variant(variant)
                 L.nk_bk5_tune(0, pf)
                 med, best, _ = time_bk5(nk, L, m, args.reps, flush)
