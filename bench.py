@@ -388,8 +388,9 @@ def run_ours(args):
         op = nk.PoissonOperator(bmesh, comm=comm)
         jac = nk.JacobiPreconditioner(op)
         iters = 100
-        solver = nk.FusedPCG(op, jac, tol=1e-30, max_iter=iters, chunk=iters,
-                             use_graph=(ws == 1 or os.environ.get("NK_BENCH_GRAPH_MULTI") == "1"))
+        # FusedPCG captures the iteration in a CUDA graph whenever every
+        # exchange is on-stream (1 rank, or peer-memory halo + board dots)
+        solver = nk.FusedPCG(op, jac, tol=1e-30, max_iter=iters, chunk=iters, use_graph=True)
         b_rhs = torch.as_tensor(rng.standard_normal(bn), device="cuda")
         nk.gs_op(op.gs, b_rhs)
         b_rhs *= bmesh.mask.reshape(-1).to(torch.float64)
@@ -425,7 +426,10 @@ def run_ours(args):
                "kernels_per_iteration": solver.launches_per_iter,
                "unfused_model_frac": round((bn * 173 + 20 * op.gs.nperm) / (per_it * 1e-3) / 1e9 / peak, 3),
                "global_counts": list(weak_counts(ws)) if ws > 1 else list(COUNTS),
-               "halo_neighbors": op.gs.ngh, "graph": bool(solver.use_graph)}
+               "halo_neighbors": op.gs.ngh, "graph": bool(solver.use_graph),
+               "halo_transport": getattr(op.gs, "transport", None) if ws > 1 else None,
+               "dot_allreduce": ("ipc-board" if getattr(comm, "board", None) is not None
+                                 else "torch.distributed") if ws > 1 else None}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None

@@ -217,6 +217,46 @@ int nk_halo_combine(int64_t nh, const int32_t* src_start, const int32_t* src_idx
                     const double* buf, const int32_t* dst_start, const int32_t* dst_idx,
                     double* w, int op, const nk_cg_state* st, nk_stream_t stream);
 
+/* ------------------------------------------- NVLink peer-memory halo
+ * NCCL-free halo transport (gs_op_overlapped's exchange, SPEC.md:212-220;
+ * PAPER.md:130-141): library-owned receive buffers mapped into the
+ * neighbours through CUDA IPC; the push kernel stores boundary contributions
+ * straight into the neighbour's buffer over NVLink and publishes a per-pair
+ * epoch flag (system-scope release); the combine kernel acquire-waits on the
+ * flags, then folds in canonical order.  Buffers are double-buffered by epoch
+ * parity; epochs live in device memory (graph-replayable). */
+int nk_ipc_handle_size(void);
+/* cudaMalloc'ed, zeroed, IPC-exportable buffer; handle: nk_ipc_handle_size() bytes */
+int nk_ipc_alloc(int64_t bytes, void** ptr, void* handle);
+int nk_ipc_free(void* ptr);
+int nk_ipc_open(const void* handle, void** peer_ptr);
+int nk_ipc_close(void* peer_ptr);
+/* for neighbour q < nnb (<= 8): peer_recv[q][par*recv_len[q] + recv_off[q] + i]
+ * = w[send_idx[send_start[q] + i]]; par = (epoch[0]+1) & 1; then epoch[0]++
+ * and *peer_flag[q] = epoch[0] (release.sys).  epoch [dev, 2 x u64, zeroed]. */
+int nk_halo_push(int nnb, void* const* peer_recv, const int64_t* recv_off,
+                 const int64_t* recv_len, void* const* peer_flag, const int32_t* send_start,
+                 const int32_t* send_idx, const double* w, int64_t total, uint64_t* epoch,
+                 const nk_cg_state* st, nk_stream_t stream);
+/* wait flags[0..nflags) >= epoch[0] (acquire.sys), then as nk_halo_combine
+ * with buf index s < own_len read from buf[s] and s >= own_len from
+ * buf[par*buf_len + s]. */
+int nk_halo_combine_wait(int64_t nh, const int32_t* src_start, const int32_t* src_idx,
+                         const double* buf, int64_t buf_len, int64_t own_len,
+                         const int32_t* dst_start, const int32_t* dst_idx, double* w, int op,
+                         const uint64_t* flags, int nflags, const uint64_t* epoch,
+                         const nk_cg_state* st, nk_stream_t stream);
+
+/* Deterministic scalar all-reduce over peer memory (the PCG dots): vals[0..k)
+ * [dev, k <= 4] are written into slot [parity][rank] of every rank's board
+ * (boards[q] [host array of nranks mapped pointers, own included]) with a
+ * release of flags_for_me[q]; then this rank acquire-waits on my_flags
+ * [dev, nranks] and overwrites vals with the rank-ordered sum from my_board
+ * [dev, 2 x nranks x 4 doubles].  Identical bits on every rank. */
+int nk_board_allreduce(int nranks, int rank, double* vals, int k, void* const* boards,
+                       void* const* flags_for_me, const double* my_board,
+                       const uint64_t* my_flags, uint64_t* epoch, nk_stream_t stream);
+
 /* --------------------------------------------------------------- PCG
  * Jacobi-PCG vector kernels (pcg).  Weighted dots use
  * wt [dev] = 1/multiplicity (so <a,b>_w is the assembled l2 product).

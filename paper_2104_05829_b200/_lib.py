@@ -73,6 +73,15 @@ _SIGS = {
     "nk_gs_plan_build": ([_P, _I64, _P, _P, _P, _P], _I32),
     "nk_gather": ([_I64, _P, _P, _P, _P, _P], _I32),
     "nk_halo_combine": ([_I64, _P, _P, _P, _P, _P, _P, _I32, _P, _P], _I32),
+    "nk_ipc_handle_size": ([], _I32),
+    "nk_ipc_alloc": ([_I64, _P, _P], _I32),
+    "nk_ipc_free": ([_P], _I32),
+    "nk_ipc_open": ([_P, _P], _I32),
+    "nk_ipc_close": ([_P], _I32),
+    "nk_halo_push": ([_I32, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P], _I32),
+    "nk_halo_combine_wait": ([_I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _I32, _P, _I32, _P, _P,
+                              _P], _I32),
+    "nk_board_allreduce": ([_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "nk_cg_partials_len": ([_I64], _I64),
     "nk_cg_init": ([_I64, _P, _P, _P, _P, _P, _P, _P, _P, _D, _I32, _I32, _P], _I32),
     "nk_cg_init_finalize": ([_P, _P, _P], _I32),

@@ -36,7 +36,11 @@ class RankComm:
     them through host memory (the paper's host-staged variant; used with gloo
     when several ranks share one GPU in tests)."""
 
-    def __init__(self, group=None, staging=None):
+    def __init__(self, group=None, staging=None, transport="auto"):
+        """transport: 'ipc' -- halo values pushed by kernels straight into the
+        neighbours' receive buffers over NVLink peer memory (CUDA IPC);
+        'p2p' -- torch.distributed send/recv (NCCL or gloo); 'auto' -- 'ipc'
+        when every neighbour's buffer can be mapped, else 'p2p'."""
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -45,6 +49,9 @@ class RankComm:
         backend = dist.get_backend(group)
         self.backend = backend
         self.staging = staging or ("device" if backend == "nccl" else "host")
+        if transport not in ("auto", "ipc", "p2p"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
 
     # ------------------------------------------------------------ helpers
     def alltoallv_int64(self, parts):
@@ -67,7 +74,31 @@ class RankComm:
         offs = np.r_[0, np.cumsum(rc)]
         return [r[offs[q]:offs[q + 1]] for q in range(P)]
 
+    def enable_board(self, device="cuda"):
+        """Map every rank's scalar board (collective).  Afterwards
+        allreduce_sum_ on <= 4 CUDA doubles runs as nk_board_allreduce
+        (peer-memory, deterministic, graph-capturable).  Returns success."""
+        if getattr(self, "board", None) is not None:
+            return True
+        if self.transport == "p2p" or self.size > 8:
+            return False
+        try:
+            self.board = IpcBoard(self, device)
+        except Exception:
+            if self.transport == "ipc":
+                raise
+            self.board = None
+        ok = torch_all_ok(self, self.board is not None)
+        if not ok and self.board is not None:
+            self.board.close()
+            self.board = None
+        return self.board is not None
+
     def allreduce_sum_(self, t):
+        b = getattr(self, "board", None)
+        if b is not None and t.is_cuda and t.numel() <= 4 and t.dtype.itemsize == 8:
+            b.allreduce_(t)
+            return t
         if self.staging == "host" and t.is_cuda:
             h = t.detach().cpu()
             self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
@@ -78,6 +109,17 @@ class RankComm:
 
     def barrier(self):
         self.dist.barrier(group=self.group)
+
+    def exchange_bytes(self, sends):
+        """{peer: bytes} -> {peer: bytes} of equal length (setup metadata)."""
+        import torch
+        if not sends:
+            return {}
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        st = {q: torch.tensor(list(b), dtype=torch.uint8, device=dev) for q, b in sends.items()}
+        rv = {q: torch.zeros(len(b), dtype=torch.uint8, device=dev) for q, b in sends.items()}
+        self.exchange(st, rv)
+        return {q: bytes(t.cpu().numpy().tolist()) for q, t in rv.items()}
 
     def exchange(self, sends, recvs):
         """Pairwise exchange: sends/recvs are {peer: tensor}.  Blocking on the
@@ -231,3 +273,153 @@ def boundary_elements(plan, n_elem, nq3):
     if len(plan.dst_idx):
         flag[np.unique(plan.dst_idx // nq3)] = True
     return np.flatnonzero(flag), np.flatnonzero(~flag)
+
+
+class IpcHalo:
+    """Peer-memory halo transport for one gs handle (see nk_halo_push /
+    nk_halo_combine_wait).  Receive buffer layout (doubles), parity copy c at
+    c*buf_len: [own contributions | from neighbour 0 | from neighbour 1 ...]
+    exactly as the HaloPlan's buf, so the combine CSR is unchanged."""
+
+    def __init__(self, plan, comm, send_idx, send_slices, device):
+        import ctypes
+        import struct
+
+        import torch
+        from ._lib import check, lib, ptr
+        L = lib()
+        self.L = L
+        nb = plan.neighbors
+        if len(nb) > 8:
+            raise RuntimeError("IPC halo supports at most 8 neighbours")
+        hs = L.nk_ipc_handle_size()
+        self.buf_len = max(plan.buf_len, 1)
+        self.own_len = len(plan.dst_idx)
+        self.buf_ptr = ctypes.c_void_p()
+        self.flag_ptr = ctypes.c_void_p()
+        hb = (ctypes.c_char * hs)()
+        hf = (ctypes.c_char * hs)()
+        check(L.nk_ipc_alloc(2 * self.buf_len * 8, ctypes.byref(self.buf_ptr), hb), "ipc_alloc")
+        check(L.nk_ipc_alloc(max(len(nb), 1) * 8, ctypes.byref(self.flag_ptr), hf),
+              "ipc_alloc")
+        # tell each neighbour: my handles, where its contributions go in my buffer,
+        # my buffer length and its slot in my flag array
+        me = comm.rank
+        msgs = {}
+        for slot, q in enumerate(nb):
+            meta = struct.pack("<qqq", plan.recv_off[q], self.buf_len, slot)
+            msgs[q] = bytes(hb) + bytes(hf) + meta
+        got = comm.exchange_bytes(msgs)
+        self.peers = []
+        n = len(nb)
+        self.peer_recv = np.zeros(max(n, 1), dtype=np.uint64)
+        self.peer_flag = np.zeros(max(n, 1), dtype=np.uint64)
+        self.recv_off = np.zeros(max(n, 1), dtype=np.int64)
+        self.recv_len = np.zeros(max(n, 1), dtype=np.int64)
+        for i, q in enumerate(nb):
+            raw = got[q]
+            pb, pf = ctypes.c_void_p(), ctypes.c_void_p()
+            check(L.nk_ipc_open(raw[:hs], ctypes.byref(pb)), f"ipc_open(rank {q})")
+            check(L.nk_ipc_open(raw[hs:2 * hs], ctypes.byref(pf)), f"ipc_open(rank {q})")
+            off, blen, slot = struct.unpack("<qqq", raw[2 * hs:2 * hs + 24])
+            self.peers += [pb, pf]
+            self.peer_recv[i] = pb.value
+            self.peer_flag[i] = pf.value + 8 * slot
+            self.recv_off[i] = off
+            self.recv_len[i] = blen
+        del me
+        starts = [0]
+        for q in nb:
+            a, b = send_slices[q]
+            starts.append(b)
+        self.send_start = torch.as_tensor(np.asarray(starts, dtype=np.int32), device=device)
+        self.send_idx = send_idx
+        self.total = int(starts[-1])
+        self.nnb = n
+        self.epoch = torch.zeros(2, dtype=torch.int64, device=device)
+        comm.barrier()
+
+    def own_buffer(self):
+        return self.buf_ptr.value
+
+    def push(self, w, st, stream):
+        from ._lib import check, ptr
+        check(self.L.nk_halo_push(self.nnb, ptr(self.peer_recv), ptr(self.recv_off),
+                                  ptr(self.recv_len), ptr(self.peer_flag), ptr(self.send_start),
+                                  ptr(self.send_idx), ptr(w), self.total, ptr(self.epoch),
+                                  ptr(st), stream), "halo_push")
+
+    def combine(self, h, w, op_code, st, stream):
+        from ._lib import check, ptr
+        check(self.L.nk_halo_combine_wait(h.nh, ptr(h.src_start), ptr(h.src_idx),
+                                          self.buf_ptr.value, self.buf_len, self.own_len,
+                                          ptr(h.dst_start), ptr(h.dst_idx), ptr(w), op_code,
+                                          self.flag_ptr.value, self.nnb, ptr(self.epoch), ptr(st),
+                                          stream), "halo_combine_wait")
+
+    def close(self):
+        for p in self.peers:
+            self.L.nk_ipc_close(p.value)
+        self.peers = []
+        self.L.nk_ipc_free(self.buf_ptr.value)
+        self.L.nk_ipc_free(self.flag_ptr.value)
+
+
+def torch_all_ok(comm, ok):
+    """True on every rank iff ok on every rank."""
+    import torch
+    dev = "cuda" if comm.backend == "nccl" else "cpu"
+    t = torch.tensor([1 if ok else 0], dtype=torch.int64, device=dev)
+    comm.dist.all_reduce(t, op=comm.dist.ReduceOp.MIN, group=comm.group)
+    return bool(int(t.item()))
+
+
+class IpcBoard:
+    """Per-rank scalar board (2 parities x P ranks x 4 doubles) + P flags,
+    mapped into every rank (nk_board_allreduce)."""
+
+    def __init__(self, comm, device):
+        import ctypes
+
+        import torch
+        from ._lib import check, lib
+        L = lib()
+        self.L, self.comm = L, comm
+        P, me = comm.size, comm.rank
+        hs = L.nk_ipc_handle_size()
+        self.board_ptr, self.flag_ptr = ctypes.c_void_p(), ctypes.c_void_p()
+        hb, hf = (ctypes.c_char * hs)(), (ctypes.c_char * hs)()
+        check(L.nk_ipc_alloc(2 * P * 4 * 8, ctypes.byref(self.board_ptr), hb), "ipc_alloc")
+        check(L.nk_ipc_alloc(P * 8, ctypes.byref(self.flag_ptr), hf), "ipc_alloc")
+        got = comm.exchange_bytes({q: bytes(hb) + bytes(hf) for q in range(P) if q != me})
+        self.boards = np.zeros(P, dtype=np.uint64)
+        self.flags_for_me = np.zeros(P, dtype=np.uint64)
+        self.opened = []
+        for q in range(P):
+            if q == me:
+                self.boards[q] = self.board_ptr.value
+                self.flags_for_me[q] = self.flag_ptr.value + 8 * me
+                continue
+            raw = got[q]
+            pb, pf = ctypes.c_void_p(), ctypes.c_void_p()
+            check(L.nk_ipc_open(raw[:hs], ctypes.byref(pb)), f"ipc_open(rank {q})")
+            check(L.nk_ipc_open(raw[hs:2 * hs], ctypes.byref(pf)), f"ipc_open(rank {q})")
+            self.opened += [pb, pf]
+            self.boards[q] = pb.value
+            self.flags_for_me[q] = pf.value + 8 * me
+        self.epoch = torch.zeros(2, dtype=torch.int64, device=device)
+        comm.barrier()
+
+    def allreduce_(self, t):
+        from ._lib import check, ptr, stream_ptr
+        check(self.L.nk_board_allreduce(self.comm.size, self.comm.rank, ptr(t), t.numel(),
+                                        ptr(self.boards), ptr(self.flags_for_me),
+                                        self.board_ptr.value, self.flag_ptr.value,
+                                        ptr(self.epoch), stream_ptr()), "board_allreduce")
+
+    def close(self):
+        for p in self.opened:
+            self.L.nk_ipc_close(p.value)
+        self.opened = []
+        self.L.nk_ipc_free(self.board_ptr.value)
+        self.L.nk_ipc_free(self.flag_ptr.value)

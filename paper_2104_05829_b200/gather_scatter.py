@@ -152,6 +152,15 @@ def gs_setup(ids, comm=None, nq=None, device="cuda"):
             h.send_slices[q] = (o, o + k)
             h.recv_slices[q] = (plan.recv_off[q], plan.recv_off[q] + plan.recv_len[q])
             o += k
+        h.ipc = None
+        if getattr(comm, "transport", "p2p") in ("ipc", "auto"):
+            try:
+                h.ipc = _dist.IpcHalo(plan, comm, h.send_idx, h.send_slices, device)
+            except Exception:
+                if comm.transport == "ipc":
+                    raise
+                h.ipc = None        # auto: fall back to send/recv
+        h.transport = "ipc" if h.ipc is not None else "p2p"
         # local segments of halo ids are not folded locally (the combine folds
         # every contribution in canonical order); the rest run as usual
         seg_ids = ids_h[perm[seg[:-1]]] if h.nseg else np.zeros(0, np.int64)
@@ -196,8 +205,15 @@ def _local(h, w, op, ncomp, st=None, part=None):
 
 
 def _halo_start(h, w, st=None):
-    """Pack: own contributions of halo ids into buf[0:), send buffers."""
+    """Pack: own contributions of halo ids into buf[0:), send buffers.  With
+    the IPC transport the push kernel also delivers them to the neighbours."""
     L, s = lib(), stream_ptr()
+    if getattr(h, "ipc", None) is not None:
+        if h.nh:
+            check(L.nk_gather(h.own_idx.numel(), ptr(h.own_idx), ptr(w), h.ipc.own_buffer(),
+                              ptr(st), s), "gather")
+        h.ipc.push(w, st, s)
+        return
     if h.nh:
         check(L.nk_gather(h.own_idx.numel(), ptr(h.own_idx), ptr(w), ptr(h.buf), ptr(st), s),
               "gather")
@@ -207,12 +223,17 @@ def _halo_start(h, w, st=None):
 
 
 def _halo_exchange(h):
+    if getattr(h, "ipc", None) is not None:
+        return              # delivered by the push kernel
     sends = {q: h.send_buf[a:b] for q, (a, b) in h.send_slices.items()}
     recvs = {q: h.buf[a:b] for q, (a, b) in h.recv_slices.items()}
     h.comm.exchange(sends, recvs)
 
 
 def _halo_finish(h, w, op, st=None):
+    if getattr(h, "ipc", None) is not None:
+        h.ipc.combine(h, w, OP_CODES[op], st, stream_ptr())
+        return
     if h.nh:
         check(lib().nk_halo_combine(h.nh, ptr(h.src_start), ptr(h.src_idx), ptr(h.buf),
                                     ptr(h.dst_start), ptr(h.dst_idx), ptr(w), OP_CODES[op],

@@ -246,7 +246,12 @@ class FusedPCG:
         self.tol, self.max_iter, self.flexible = float(tol), int(max_iter), bool(flexible)
         self.chunk = max(1, int(chunk))
         comm = op.gs.comm
-        self.use_graph = use_graph and (comm is None or comm.size == 1 or
+        board = False
+        if comm is not None and comm.size > 1 and getattr(op.gs, "transport", "p2p") == "ipc":
+            board = comm.enable_board(op.mesh.device)     # NCCL-free scalar all-reduce
+        # graph capture needs every per-iteration exchange on the stream:
+        # peer-memory halo + board, or NCCL (device staging)
+        self.use_graph = use_graph and (comm is None or comm.size == 1 or board or
                                         comm.staging == "device")
         dev = op.mesh.device
         n = op.n * op.ncomp

@@ -25,7 +25,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, outdir, counts, N):
+def _worker(rank, world, port, outdir, counts, N, transport="auto"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -40,7 +40,7 @@ def _worker(rank, world, port, outdir, counts, N):
         nq3 = (N + 1) ** 3
         part = nk.rcb(g.xyz.reshape(3, g.E, -1).mean(axis=2).T, world)
         mine = np.flatnonzero(part == rank)
-        comm = RankComm()
+        comm = RankComm(transport=transport)
         m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05),
                               elements=mine)
         op = nk.PoissonOperator(m, comm=comm)
@@ -54,17 +54,22 @@ def _worker(rank, world, port, outdir, counts, N):
         bglob = g.mask.ravel() * ogs.gs_op(g.ids, g.B.ravel() * f)
         b = bglob.reshape(g.E, nq3)[mine].ravel()
         jac = nk.JacobiPreconditioner(op)
-        res = nk.FusedPCG(op, jac, tol=1e-8, max_iter=500, use_graph=False).solve(
-            torch.as_tensor(b, device="cuda"))
+        # ipc: halo + dots over peer memory -> the iteration is graph-captured
+        solver = nk.FusedPCG(op, jac, tol=1e-8, max_iter=500, use_graph=(transport == "ipc"))
+        res = solver.solve(torch.as_tensor(b, device="cuda"))
+        graph = bool(solver.use_graph)
         np.savez(os.path.join(outdir, f"r{rank}.npz"), mine=mine, ids=m.ids.cpu().numpy(),
+                 transport=op.gs.transport, graph=graph,
                  w=w, gsw=gsw, x=res.x.cpu().numpy(), it=res.iterations,
                  conv=res.converged, ngh=op.gs.ngh, nb=op.gs.boundary_elements.numel())
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("N", [5, 7])      # N=7 exercises the persistent TMA step
-def test_two_ranks_one_gpu_gs_and_pcg(N):
+@pytest.mark.parametrize("N,transport", [(5, "p2p"), (7, "p2p"), (5, "ipc"), (7, "ipc")])
+def test_two_ranks_one_gpu_gs_and_pcg(N, transport):
+    """N=7 exercises the persistent TMA step; transport 'ipc' the NVLink
+    peer-memory push/combine kernels (IPC mappings of the same device here)."""
     import torch.multiprocessing as mp
     from oracle import gs as ogs
     from oracle import mesh as om
@@ -72,10 +77,12 @@ def test_two_ranks_one_gpu_gs_and_pcg(N):
     from oracle import solvers as osol
     counts, world = (4, 4, 2), 2
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _port(), d, counts, N), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _port(), d, counts, N, transport), nprocs=world, join=True)
         res = [np.load(os.path.join(d, f"r{r}.npz")) for r in range(world)]
     ref = ogs.gs_op_multi([r["ids"] for r in res], [r["w"] for r in res])
     for r, ro in zip(res, ref):
+        assert str(r["transport"]) == transport
+        assert bool(r["graph"]) == (transport == "ipc")
         assert np.array_equal(r["gsw"], ro)            # CUDA halo path, bit-exact
         assert int(r["ngh"]) == 1 and int(r["nb"]) > 0
     g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05))
