@@ -1,0 +1,32 @@
+"""Small end-to-end exercise of every kernel family, for compute-sanitizer
+(memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2104_05829_b200 as nk
+from paper_2104_05829_b200 import _lib
+
+L = _lib.lib()
+for N, counts in ((7, (3, 2, 2)), (4, (2, 2, 2)), (9, (2, 1, 1))):
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    for v in (1, 3, 4):
+        L.nk_bk5_set_variant(v)
+        nk.apply_stiffness_local(u, m)
+        nk.apply_stiffness_local(u, m, elements=torch.tensor([0, 2], dtype=torch.int32,
+                                                             device="cuda"))
+    L.nk_bk5_set_variant(0)
+    u3 = torch.randn(3 * m.n_local, dtype=torch.float64, device="cuda")
+    nk.apply_helmholtz_local(u3, m, 0.5, 2.0, ncomp=3)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    b = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(torch.float64)
+    nk.FusedPCG(op, jac, tol=1e-6, max_iter=20, use_graph=False).solve(b)
+    nk.pcg(lambda v: op(v), lambda r: jac(r), b, tol=1e-6, max_iter=10)
+    uh = u.cpu().pin_memory()
+    nk.apply_stiffness_local(uh, m)
+torch.cuda.synchronize()
+print("sanitize run ok")
