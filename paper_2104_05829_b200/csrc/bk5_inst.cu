@@ -146,8 +146,8 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
 #undef NK_TARGS
     }
   }
-  if constexpr (NQ % 2 == 0 && NQ <= 10) {
-    // 3-component batch: G staged once per element (pencil3); k-slab otherwise
+  if constexpr (NQ >= 2 && NQ <= 12) {
+    // 3-component batch: G read once per element (pencil3); k-slab otherwise
     if (ncomp == 3 && variant != 1) {
       if (nblocks) {
         *nblocks = nlist;
@@ -157,7 +157,8 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
         set_error("bk5: the fused dot is not available for ncomp = 3");
         return NK_ERR_INVALID;
       }
-      constexpr int M3 = NQ <= 6 ? 6 : (NQ == 8 ? 4 : 2);
+      // smem 7 element buffers: NQ 8 -> 32 KB, 10 -> 57 KB, 12 -> 105 KB per CTA
+      constexpr int M3 = NQ <= 6 ? 4 : (NQ <= 8 ? 3 : (NQ <= 10 ? 2 : 1));
       return launch_pencil3<NQ, M3>(nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, s);
     }
   }
