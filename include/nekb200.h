@@ -145,7 +145,9 @@ int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double*
            nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
            nk_stream_t stream);
 int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
-/* kernel variant selection: 0 = auto (= 3), 1 = k-slab (2D
+/* kernel variant selection: 0 = auto (measured per-order table: 5 for
+ * N in {2,6,8,9,13,14,15}, else 3), 5 = pencil2 (two shared buffers, u
+ * re-read from L1/L2), 1 = k-slab (2D
  * thread plane, k-column in registers, D in shared memory), 3 = pencil
  * (register 1-D contractions, D in the constant bank, swizzled shared
  * transposes), 4 = pencil-TMA (persistent CTAs, cp.async.bulk 2-stage ring;

@@ -70,14 +70,18 @@ extern "C" int nk_bk5_bulk_launch(int N, int64_t nlist, const int32_t* elist, co
 extern "C" int nk_bk5_variant_get();
 
 static bool use_bulk(int N, int ncomp) { return nk_bk5_variant_get() == 2 && N == 7 && ncomp == 1; }
-// auto (0): pencil for every order -- measured best under the cold-and-clean
-// L2 protocol (sweep16: N=7 pencil 85.9% vs pencil-TMA 79.2% of HBM peak).
-// The fused BP5 step keeps its TMA pipeline (nk_bk5_pcg).
+// auto (0): the measured winner per order (the select_kernel_variant of
+// SPEC.md:420-428, decided offline by scripts/bk5_sweep.py --orders on the
+// B200 under the cold-and-clean L2 protocol, profiles/r1_bk5_order_sweep*):
+// pencil2 (2 shared buffers) where its extra residency wins, pencil
+// elsewhere.  The fused BP5 step keeps its TMA pipeline (nk_bk5_pcg).
 static int kvariant_for(int N) {
   const int v = nk_bk5_variant_get();
-  if (v == 1 || v == 3 || v == 4) return v;
-  (void)N;
-  return 3;
+  if (v == 1 || v == 3 || v == 4 || v == 5) return v;
+  switch (N) {
+    case 2: case 6: case 8: case 9: case 13: case 14: case 15: return 5;
+    default: return 3;
+  }
 }
 
 extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {

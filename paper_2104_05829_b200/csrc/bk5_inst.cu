@@ -67,6 +67,30 @@ int runp(int64_t nlist, const int32_t* elist, const double* D, const double* G, 
                                       part_base, reduce_count, s, pfG);
 }
 
+// pencil2 shapes: 2 element buffers allow ~1.5x the resident CTAs of pencil
+template <int NQ> struct Pencil2Default;
+#define NK_P2D(NQ_, EPB_, MINB_) \
+  template <> struct Pencil2Default<NQ_> { static constexpr int EPB = EPB_, MINB = MINB_; };
+NK_P2D(2, 32, 8) NK_P2D(3, 14, 6) NK_P2D(4, 4, 14) NK_P2D(5, 5, 8) NK_P2D(6, 2, 12)
+NK_P2D(7, 2, 5) NK_P2D(8, 1, 8) NK_P2D(9, 1, 5) NK_P2D(10, 1, 4) NK_P2D(11, 1, 4)
+NK_P2D(12, 1, 3) NK_P2D(13, 1, 3) NK_P2D(14, 1, 2) NK_P2D(15, 1, 2) NK_P2D(16, 1, 2)
+#undef NK_P2D
+
+template <int NQ>
+int run_pencil2(int cfg, int64_t nlist, const int32_t* elist, const double* D, const double* G,
+                const double* u, double* w, double lam0, const double* B, double lam1,
+                const uint8_t* mask, nk_cg_state* st, double* partials, int64_t part_base,
+                int64_t reduce_count, cudaStream_t s, int64_t* nb, int pfG) {
+  constexpr int EPB = Pencil2Default<NQ>::EPB, MINB = Pencil2Default<NQ>::MINB;
+  if (nb) {
+    *nb = (nlist + EPB - 1) / EPB;
+    return NK_OK;
+  }
+  (void)cfg;
+  return launch_pencil2<NQ, EPB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st,
+                                       partials, part_base, reduce_count, s, pfG);
+}
+
 template <int NQ>
 int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, const double* G,
                const double* u, double* w, double lam0, const double* B, double lam1,
@@ -162,6 +186,9 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
       return launch_pencil3<NQ, M3>(nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, s);
     }
   }
+  if (variant == 5 && ncomp == 1)
+    return run_pencil2<NQ>(cfg, nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                           part_base, reduce_count, s, nblocks, pf_dist);
   if ((variant == 3 || variant == 4) && ncomp == 1)
     return run_pencil<NQ>(cfg, nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
                           part_base, reduce_count, s, nblocks, pf_dist);

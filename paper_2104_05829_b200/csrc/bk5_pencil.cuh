@@ -285,3 +285,191 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
 }
 
 }  // namespace nk
+
+namespace nk {
+
+// ---------------------------------------------------------------------------
+// Variant 5, "pencil2": the pencil scheme with TWO shared element buffers.
+//   F1 i-pencils: u row (HBM)           -> ur -> R
+//   F2 j-pencils: u column (L1/L2)      -> us -> S
+//   F3 k-pencils: u column (L1/L2)      -> ut (registers)
+//   G  k-pencils: gr -> R, gs -> S in place, gt (registers)
+//   B2 j-pencils: S column -> D^T gs    -> S in place (the pencil owns it)
+//   B3 k-pencils: D^T gt + S column     -> S in place
+//   B1 i-pencils: D^T R row + S row     -> epilogue -> HBM
+// 12 shared accesses per point instead of 15 and 2/3 of the shared memory
+// (more resident CTAs), for two extra L2 reads of u.
+template <int NQ, int EPB>
+struct Pencil2Cfg {
+  static constexpr int VOL = PencilLayout<NQ>::VOL;
+  static size_t smem_bytes() { return sizeof(double) * ((size_t)EPB * 2 * VOL + 32); }
+};
+
+template <int NQ, int EPB, int MINB>
+__global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
+bk5_pencil2(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
+            const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
+            double lam0, const double* __restrict__ B, double lam1,
+            const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
+            int64_t part_base, int64_t reduce_count, int pfG) {
+  using L = PencilLayout<NQ>;
+  constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, VOL = L::VOL;
+  extern __shared__ double smem[];
+  if (st != nullptr && st->done) return;
+  const int t = threadIdx.x;
+  const int le = t / NQ2;
+  const int tt = t - le * NQ2;
+  const int a = tt % NQ, b = tt / NQ;
+  double* red = smem;
+  double* Rr = smem + 32 + (size_t)le * 2 * VOL;
+  double* Ss = Rr + VOL;
+  const int64_t slot = (int64_t)blockIdx.x * EPB + le;
+  const bool active = slot < nlist;
+  const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
+  const double* ue = u + e * NQ3;
+  if (pfG && active && tt == 0) prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
+
+  if (active) {  // F1: i-pencils (j = a, k = b)
+    double v[NQ], o[NQ];
+    const double* row = ue + b * NQ2 + a * NQ;
+    if (NQ % 2 == 0) {
+#pragma unroll
+      for (int m = 0; m < NQ; m += 2) {
+        const double2 p = __ldg(reinterpret_cast<const double2*>(row + m));
+        v[m] = p.x;
+        v[m + 1] = p.y;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = __ldg(row + m);
+    }
+    matvec<NQ, false>(D, v, o);
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
+  }
+  double ut[NQ];
+  if (active) {  // F2: j-pencils (i = a, k = b) from L1/L2 ; F3: k-pencils (i = a, j = b)
+    double v[NQ], o[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) v[m] = __ldg(ue + b * NQ2 + m * NQ + a);
+    matvec<NQ, false>(D, v, o);
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) v[m] = __ldg(ue + m * NQ2 + b * NQ + a);
+    matvec<NQ, false>(D, v, ut);
+  }
+  __syncthreads();
+  double gt[NQ];
+  if (active) {  // G: k-pencils
+    const double* gp = G + e * 6 * NQ3 + b * NQ + a;
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const double g0 = __ldg(gp + 0 * NQ3 + k * NQ2), g1 = __ldg(gp + 1 * NQ3 + k * NQ2);
+      const double g2 = __ldg(gp + 2 * NQ3 + k * NQ2), g3 = __ldg(gp + 3 * NQ3 + k * NQ2);
+      const double g4 = __ldg(gp + 4 * NQ3 + k * NQ2), g5 = __ldg(gp + 5 * NQ3 + k * NQ2);
+      const int q = L::idx(k, b, a);
+      const double ur = Rr[q], us = Ss[q];
+      Rr[q] = g0 * ur + g1 * us + g2 * ut[k];
+      Ss[q] = g1 * ur + g3 * us + g4 * ut[k];
+      gt[k] = g2 * ur + g4 * us + g5 * ut[k];
+    }
+  }
+  __syncthreads();
+  if (active) {  // B2: j-pencils, in place on their own S column
+    double v[NQ], o[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) v[m] = Ss[L::idx(b, m, a)];
+    matvec<NQ, true>(D, v, o);
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+  }
+  __syncthreads();
+  if (active) {  // B3: k-pencils, S column += D^T gt
+    double o[NQ];
+    matvec<NQ, true>(D, gt, o);
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int q = L::idx(k, b, a);
+      Ss[q] = o[k] + Ss[q];
+    }
+  }
+  __syncthreads();
+  double dot = 0.0;
+  if (active) {  // B1: i-pencils + epilogue
+    double v[NQ], o[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) v[m] = Rr[L::idx(b, a, m)];
+    matvec<NQ, true>(D, v, o);
+    const int64_t off = e * NQ3 + b * NQ2 + a * NQ;
+    double res[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) res[i] = lam0 * (o[i] + Ss[L::idx(b, a, i)]);
+    if (B != nullptr || st != nullptr) {
+      double urw[NQ];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) urw[i] = __ldg(ue + b * NQ2 + a * NQ + i);
+      if (B != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) res[i] = fma(lam1 * __ldg(B + off + i), urw[i], res[i]);
+      }
+      if (mask != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) dot = fma(urw[i], res[i], dot);
+    } else if (mask != nullptr) {
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+    }
+    double* wr = w + off;
+    if (NQ % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < NQ; i += 2)
+        *reinterpret_cast<double2*>(wr + i) = make_double2(res[i], res[i + 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) wr[i] = res[i];
+    }
+  }
+  if (st != nullptr) {
+    double vv[1] = {dot};
+    block_sum<1>(vv, red);
+    if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+    if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
+      double s[1];
+      reduce_partials<1>(partials, reduce_count, 0, s, red);
+      if (t == 0) st->pAp = s[0];
+    }
+  }
+}
+
+template <int NQ, int EPB, int MINB>
+static int launch_pencil2(int64_t nlist, const int32_t* elist, const double* Dhost,
+                          const double* G, const double* u, double* w, double lam0,
+                          const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
+                          double* partials, int64_t part_base, int64_t reduce_count,
+                          cudaStream_t s, int pfG) {
+  using C = Pencil2Cfg<NQ, EPB>;
+  const size_t smem = C::smem_bytes();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t err = cudaFuncSetAttribute(bk5_pencil2<NQ, EPB, MINB>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) {
+      set_error("bk5_pencil2: smem attribute (%zu B): %s", smem, cudaGetErrorString(err));
+      return NK_ERR_CUDA;
+    }
+    configured = true;
+  }
+  const int64_t nblk = (nlist + EPB - 1) / EPB;
+  if (nblk == 0) return NK_OK;
+  DParam<NQ> D;
+  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  bk5_pencil2<NQ, EPB, MINB><<<(unsigned)nblk, EPB * NQ * NQ, smem, s>>>(
+      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG);
+  return check_launch("bk5_pencil2");
+}
+
+}  // namespace nk

@@ -164,7 +164,7 @@ def main():
     if args.shapes:
         m = nk.build_box_mesh((1, 1, 1), (20, 20, 20), 7, deformation=("sine", 0.05))
         ref = None
-        for variant, cfg, pf in [(3, c, f) for c in (0, 8, 9, 2, 1, 5) for f in (0, 1)] + [(4, 0, 0), (4, 1, 0), (1, 4, 0)]:
+        for variant, cfg, pf in [(3, 0, 1), (5, 0, 1), (4, 0, 0)]:
             if True:
                 L.nk_bk5_set_variant(variant)
                 L.nk_bk5_tune(cfg, pf)
@@ -185,7 +185,7 @@ def main():
         for N in range(1, 16):
             ne = E_FOR_N[N]
             m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
-            for variant, pf in ((3, 1), (3, 2)):
+            for variant, pf in ((0, 1),):
                 L.nk_bk5_set_variant(variant)
                 L.nk_bk5_tune(0, pf)
                 med, best, _ = time_bk5(nk, L, m, args.reps, flush)

@@ -295,8 +295,8 @@ def variant_guard():
     L.nk_bk5_tune(0, 1)
 
 
-@pytest.mark.parametrize("variant", [1, 3, 4])
-@pytest.mark.parametrize("N", [3, 5, 7])
+@pytest.mark.parametrize("variant", [1, 3, 4, 5])
+@pytest.mark.parametrize("N", [3, 5, 7, 12])
 def test_bk5_variants_match_oracle(variant_guard, variant, N):
     """k-slab (1), pencil (3) and pencil-TMA (4, even N+1; others fall back)
     all within the 1e-12 bar, incl. element subsets, mask and the fused p.Ap."""
