@@ -83,14 +83,10 @@ class RankComm:
         if self.transport == "p2p" or self.size > 8:
             return False
         try:
-            self.board = IpcBoard(self, device)
+            self.board = IpcBoard(self, device)   # raises on every rank or none
         except Exception:
             if self.transport == "ipc":
                 raise
-            self.board = None
-        ok = torch_all_ok(self, self.board is not None)
-        if not ok and self.board is not None:
-            self.board.close()
             self.board = None
         return self.board is not None
 
@@ -299,9 +295,12 @@ class IpcHalo:
         self.flag_ptr = ctypes.c_void_p()
         hb = (ctypes.c_char * hs)()
         hf = (ctypes.c_char * hs)()
-        check(L.nk_ipc_alloc(2 * self.buf_len * 8, ctypes.byref(self.buf_ptr), hb), "ipc_alloc")
-        check(L.nk_ipc_alloc(max(len(nb), 1) * 8, ctypes.byref(self.flag_ptr), hf),
-              "ipc_alloc")
+        self.peers = []
+        ok = (L.nk_ipc_alloc(2 * self.buf_len * 8, ctypes.byref(self.buf_ptr), hb) == 0 and
+              L.nk_ipc_alloc(max(len(nb), 1) * 8, ctypes.byref(self.flag_ptr), hf) == 0)
+        if not torch_all_ok(comm, ok):      # every rank leaves together
+            self.close()
+            raise RuntimeError("IPC allocation failed on some rank")
         # tell each neighbour: my handles, where its contributions go in my buffer,
         # my buffer length and its slot in my flag array
         me = comm.rank
@@ -310,17 +309,19 @@ class IpcHalo:
             meta = struct.pack("<qqq", plan.recv_off[q], self.buf_len, slot)
             msgs[q] = bytes(hb) + bytes(hf) + meta
         got = comm.exchange_bytes(msgs)
-        self.peers = []
         n = len(nb)
         self.peer_recv = np.zeros(max(n, 1), dtype=np.uint64)
         self.peer_flag = np.zeros(max(n, 1), dtype=np.uint64)
         self.recv_off = np.zeros(max(n, 1), dtype=np.int64)
         self.recv_len = np.zeros(max(n, 1), dtype=np.int64)
+        ok = True
         for i, q in enumerate(nb):
             raw = got[q]
             pb, pf = ctypes.c_void_p(), ctypes.c_void_p()
-            check(L.nk_ipc_open(raw[:hs], ctypes.byref(pb)), f"ipc_open(rank {q})")
-            check(L.nk_ipc_open(raw[hs:2 * hs], ctypes.byref(pf)), f"ipc_open(rank {q})")
+            if L.nk_ipc_open(raw[:hs], ctypes.byref(pb)) != 0 or \
+                    L.nk_ipc_open(raw[hs:2 * hs], ctypes.byref(pf)) != 0:
+                ok = False
+                break
             off, blen, slot = struct.unpack("<qqq", raw[2 * hs:2 * hs + 24])
             self.peers += [pb, pf]
             self.peer_recv[i] = pb.value
@@ -328,6 +329,9 @@ class IpcHalo:
             self.recv_off[i] = off
             self.recv_len[i] = blen
         del me
+        if not torch_all_ok(comm, ok):
+            self.close()
+            raise RuntimeError("IPC peer mapping failed on some rank")
         starts = [0]
         for q in nb:
             a, b = send_slices[q]
@@ -337,7 +341,6 @@ class IpcHalo:
         self.total = int(starts[-1])
         self.nnb = n
         self.epoch = torch.zeros(2, dtype=torch.int64, device=device)
-        comm.barrier()
 
     def own_buffer(self):
         return self.buf_ptr.value
@@ -358,11 +361,14 @@ class IpcHalo:
                                           stream), "halo_combine_wait")
 
     def close(self):
-        for p in self.peers:
-            self.L.nk_ipc_close(p.value)
+        for p in getattr(self, "peers", []):
+            if p.value:
+                self.L.nk_ipc_close(p.value)
         self.peers = []
-        self.L.nk_ipc_free(self.buf_ptr.value)
-        self.L.nk_ipc_free(self.flag_ptr.value)
+        for p in (self.buf_ptr, self.flag_ptr):
+            if p.value:
+                self.L.nk_ipc_free(p.value)
+                p.value = None
 
 
 def torch_all_ok(comm, ok):
@@ -389,12 +395,16 @@ class IpcBoard:
         hs = L.nk_ipc_handle_size()
         self.board_ptr, self.flag_ptr = ctypes.c_void_p(), ctypes.c_void_p()
         hb, hf = (ctypes.c_char * hs)(), (ctypes.c_char * hs)()
-        check(L.nk_ipc_alloc(2 * P * 4 * 8, ctypes.byref(self.board_ptr), hb), "ipc_alloc")
-        check(L.nk_ipc_alloc(P * 8, ctypes.byref(self.flag_ptr), hf), "ipc_alloc")
+        self.opened = []
+        ok = (L.nk_ipc_alloc(2 * P * 4 * 8, ctypes.byref(self.board_ptr), hb) == 0 and
+              L.nk_ipc_alloc(P * 8, ctypes.byref(self.flag_ptr), hf) == 0)
+        if not torch_all_ok(comm, ok):
+            self.close()
+            raise RuntimeError("IPC allocation failed on some rank")
         got = comm.exchange_bytes({q: bytes(hb) + bytes(hf) for q in range(P) if q != me})
         self.boards = np.zeros(P, dtype=np.uint64)
         self.flags_for_me = np.zeros(P, dtype=np.uint64)
-        self.opened = []
+        ok = True
         for q in range(P):
             if q == me:
                 self.boards[q] = self.board_ptr.value
@@ -402,13 +412,17 @@ class IpcBoard:
                 continue
             raw = got[q]
             pb, pf = ctypes.c_void_p(), ctypes.c_void_p()
-            check(L.nk_ipc_open(raw[:hs], ctypes.byref(pb)), f"ipc_open(rank {q})")
-            check(L.nk_ipc_open(raw[hs:2 * hs], ctypes.byref(pf)), f"ipc_open(rank {q})")
+            if L.nk_ipc_open(raw[:hs], ctypes.byref(pb)) != 0 or \
+                    L.nk_ipc_open(raw[hs:2 * hs], ctypes.byref(pf)) != 0:
+                ok = False
+                break
             self.opened += [pb, pf]
             self.boards[q] = pb.value
             self.flags_for_me[q] = pf.value + 8 * me
+        if not torch_all_ok(comm, ok):
+            self.close()
+            raise RuntimeError("IPC peer mapping failed on some rank")
         self.epoch = torch.zeros(2, dtype=torch.int64, device=device)
-        comm.barrier()
 
     def allreduce_(self, t):
         from ._lib import check, ptr, stream_ptr
@@ -418,8 +432,11 @@ class IpcBoard:
                                         ptr(self.epoch), stream_ptr()), "board_allreduce")
 
     def close(self):
-        for p in self.opened:
-            self.L.nk_ipc_close(p.value)
+        for p in getattr(self, "opened", []):
+            if p.value:
+                self.L.nk_ipc_close(p.value)
         self.opened = []
-        self.L.nk_ipc_free(self.board_ptr.value)
-        self.L.nk_ipc_free(self.flag_ptr.value)
+        for p in (self.board_ptr, self.flag_ptr):
+            if p.value:
+                self.L.nk_ipc_free(p.value)
+                p.value = None

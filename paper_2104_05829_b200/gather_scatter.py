@@ -154,12 +154,18 @@ def gs_setup(ids, comm=None, nq=None, device="cuda"):
             o += k
         h.ipc = None
         if getattr(comm, "transport", "p2p") in ("ipc", "auto"):
+            err = None
             try:
                 h.ipc = _dist.IpcHalo(plan, comm, h.send_idx, h.send_slices, device)
-            except Exception:
+            except Exception as exc:          # e.g. no peer access / IPC disabled
+                err = exc
+            # the transport must be the same on every rank: decide collectively
+            if not _dist.torch_all_ok(comm, h.ipc is not None):
+                if h.ipc is not None:
+                    h.ipc.close()
+                    h.ipc = None
                 if comm.transport == "ipc":
-                    raise
-                h.ipc = None        # auto: fall back to send/recv
+                    raise RuntimeError(f"IPC halo transport unavailable: {err}")
         h.transport = "ipc" if h.ipc is not None else "p2p"
         # local segments of halo ids are not folded locally (the combine folds
         # every contribution in canonical order); the rest run as usual
