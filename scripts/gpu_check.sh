@@ -15,7 +15,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-ceiling > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:bk5_ -s 3 -c 1 \
   -o gpurun_out/bk5_full_$TAG python bench.py --steps 2 --warmup 3 --no-bp5 --no-cpu --no-ceiling > gpurun_out/ncu_full_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gs_classes|cg_update|cg_pupdate" -s 30 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pcg|gs_classes|cg_update" -s 30 -c 3 \
   -o gpurun_out/cg_full_$TAG python bench.py --steps 2 --warmup 3 --no-cpu --no-ceiling > gpurun_out/ncu_cg_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_full_$TAG.log gpurun_out/ncu_cg_$TAG.log
 ls gpurun_out
