@@ -289,6 +289,36 @@ int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double*
 int nk_cg_pupdate(int64_t n, const double* r, double* p, const double* invD, const double* z,
                   nk_cg_state* st, double* hist, nk_stream_t stream);
 
+/* ------------------------------------------------------ p-multigrid
+ * Building blocks of the Chebyshev-Jacobi p-multigrid preconditioner
+ * (V-cycle sequenced by the host, see
+ * paper_2104_05829_b200/multigrid.py).  st [nullable]: skip when st->done.
+ *
+ * Order-to-order transfer, per element (ni, no in [2, 16]):
+ *   v   = (in - sub) * wt                    sub, wt nullable
+ *   res = (M x M x M) v                      M: no x ni row-major, HOST
+ *   res = mask[q] ? res : 0                  mask (output side) nullable
+ *   out = accumulate ? out + res : res
+ * Restriction: M = J^T with in = r, sub = A e, wt = 1/mult (then gs);
+ * prolongation: M = J, accumulate = 1 (J = interp_matrix(coarse -> fine),
+ * basis.py:99-117). */
+int nk_interp3(int ni, int no, int64_t nelem, const double* M, const double* in,
+               const double* sub, const double* wt, const uint8_t* mask, double* out,
+               int accumulate, const nk_cg_state* st, nk_stream_t stream);
+
+/* One fused Chebyshev-Jacobi step:
+ *   rv = r - Aq (Aq nullable);  res_out = rv (nullable)
+ *   d  = a d + b invD rv       (a == 0: d is not read)
+ *   e  = (e_acc ? e : 0) + d */
+int nk_cheb_step(int64_t n, const double* r, const double* Aq, const double* invD,
+                 double* res_out, double* d, double* e, double a, double b, int e_acc,
+                 const nk_cg_state* st, nk_stream_t stream);
+
+/* y = A x for a dense row-major n x n A (the explicit inverse of the
+ * assembled coarse operator, coarse_solve SPEC.md:519-527). */
+int nk_dense_matvec(int64_t n, const double* A, const double* x, double* y,
+                    const nk_cg_state* st, nk_stream_t stream);
+
 /* out[0] = <a, b>_wt (wt nullable = unweighted), deterministic two-stage. */
 int nk_wdot(int64_t n, const double* a, const double* b, const double* wt, double* out,
             double* partials, nk_stream_t stream);

@@ -8,7 +8,8 @@ partition.  Compute runs in libnekb200.so (hand-written sm_100a CUDA, C ABI in
 include/nekb200.h); PyTorch only owns device buffers and streams.
 """
 
-from . import basis, distributed, gather_scatter, kernels, mesh, partition, solvers  # noqa: F401
+from . import (basis, distributed, gather_scatter, kernels, mesh, multigrid,  # noqa: F401
+               partition, solvers)
 from ._lib import (ContractError, NativeLibraryError, UnsupportedOrderError,  # noqa: F401
                    LIB_PATH)
 from .basis import InvalidOrderError, SpectralBasis, gll_rule, interp_matrix  # noqa: F401
@@ -17,6 +18,8 @@ from .kernels import (apply_helmholtz_local, apply_mass, apply_stiffness_local, 
                       extract_diagonal, inner_product)
 from .mesh import (Mesh, assign_global_ids, build_box_mesh, geometric_factors,  # noqa: F401
                    read_hexmesh, write_hexmesh)
+from .multigrid import (MultigridHierarchy, MultigridPCG, chebyshev_smooth,  # noqa: F401
+                        coarse_solve, pmg_preconditioner)
 from .partition import rcb  # noqa: F401
 from .solvers import (BreakdownError, FusedPCG, HelmholtzVectorSolver,  # noqa: F401
                       JacobiPreconditioner, PoissonOperator, pcg)

@@ -1,0 +1,184 @@
+// p-multigrid building blocks (SPEC.md:489-527,
+// PAPER.md:274-313): order-to-order tensor-product transfer, the fused
+// Chebyshev-Jacobi vector step and the dense coarse matvec.  The V-cycle is
+// sequenced on the host (paper_2104_05829_b200/multigrid.py) from these plus
+// nk_bk5 + gs at every level; every kernel takes the PCG state so a graph
+// replay after convergence does no work.
+//
+// All three are HBM-streaming kernels:
+//   nk_interp3   restriction reads in, sub, wt (24 B per fine point) and writes
+//                1/8-ish of that; prolongation reads the coarse field, reads +
+//                writes the fine one (17 B per fine point with the mask).
+//   nk_cheb_step 32-56 B per point.
+//   nk_dense_matvec  8 n^2 B (the explicit inverse of the coarse operator).
+#include "common.cuh"
+
+namespace nk {
+
+static unsigned grid_stride(int64_t n, int threads, int64_t cap) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+struct TransferM {
+  double m[16 * 16];  // row-major no x ni
+};
+
+// One element per CTA.  v (ni^3) -> t1 (ni^2 no) -> t2 (ni no^2) -> out (no^3):
+// contraction order i, j, k (oracle/pmg.py:_interp3).
+__global__ void __launch_bounds__(256)
+interp3_kernel(int ni, int no, const __grid_constant__ TransferM M, const double* __restrict__ in,
+               const double* __restrict__ sub, const double* __restrict__ wt,
+               const uint8_t* __restrict__ mask, double* __restrict__ out, int accumulate,
+               const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  extern __shared__ __align__(16) double sm[];
+  const int ni2 = ni * ni, ni3 = ni2 * ni, no2 = no * no, no3 = no2 * no;
+  double* v = sm;
+  double* t1 = v + ni3;
+  double* t2 = t1 + ni2 * no;
+  const int64_t e = blockIdx.x;
+  const int64_t ib = e * ni3, ob = e * no3;
+  for (int q = threadIdx.x; q < ni3; q += blockDim.x) {
+    double x = __ldg(in + ib + q);
+    if (sub) x -= __ldg(sub + ib + q);
+    if (wt) x *= __ldg(wt + ib + q);
+    v[q] = x;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < ni2 * no; q += blockDim.x) {  // t1[k][j][a]
+    const int a = q % no, kj = q / no;
+    const double* row = M.m + a * ni;
+    const double* src = v + kj * ni;
+    double s = 0.0;
+    for (int i = 0; i < ni; ++i) s = fma(row[i], src[i], s);
+    t1[q] = s;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < ni * no2; q += blockDim.x) {  // t2[k][b][a]
+    const int a = q % no, b = (q / no) % no, k = q / no2;
+    const double* row = M.m + b * ni;
+    const double* src = t1 + k * ni * no + a;
+    double s = 0.0;
+    for (int j = 0; j < ni; ++j) s = fma(row[j], src[j * no], s);
+    t2[q] = s;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < no3; q += blockDim.x) {  // out[c][b][a]
+    const int ba = q % no2, c = q / no2;
+    const double* row = M.m + c * ni;
+    const double* src = t2 + ba;
+    double s = 0.0;
+    for (int k = 0; k < ni; ++k) s = fma(row[k], src[k * no2], s);
+    if (mask && !mask[ob + q]) s = 0.0;
+    out[ob + q] = accumulate ? out[ob + q] + s : s;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+cheb_step_kernel(int64_t n, const double* __restrict__ r, const double* __restrict__ Aq,
+                 const double* __restrict__ invD, double* __restrict__ res_out,
+                 double* __restrict__ d, double* __restrict__ e, double a, double b, int e_acc,
+                 const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    double rv = r[q];
+    if (Aq) rv -= __ldg(Aq + q);
+    if (res_out) res_out[q] = rv;
+    const double z = __ldg(invD + q) * rv;
+    const double dv = a != 0.0 ? a * d[q] + b * z : b * z;
+    d[q] = dv;
+    e[q] = e_acc ? e[q] + dv : dv;
+  }
+}
+
+// y = A x, one warp per row, fixed lane-strided order (deterministic).
+__global__ void __launch_bounds__(256)
+dense_matvec_kernel(int64_t n, const double* __restrict__ A, const double* __restrict__ x,
+                    double* __restrict__ y, const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n;
+       row += warps) {
+    const double* a = A + row * n;
+    double s = 0.0;
+    if ((n & 1) == 0) {
+      const double2* a2 = reinterpret_cast<const double2*>(a);
+      const double2* x2 = reinterpret_cast<const double2*>(x);
+      for (int64_t c = lane; c < (n >> 1); c += 32) {
+        const double2 av = __ldcs(a2 + c);
+        const double2 xv = __ldg(x2 + c);
+        s = fma(av.x, xv.x, s);
+        s = fma(av.y, xv.y, s);
+      }
+    } else {
+      for (int64_t c = lane; c < n; c += 32) s = fma(__ldcs(a + c), __ldg(x + c), s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) y[row] = s;
+  }
+}
+
+}  // namespace nk
+
+using namespace nk;
+
+extern "C" int nk_interp3(int ni, int no, int64_t nelem, const double* M, const double* in,
+                          const double* sub, const double* wt, const uint8_t* mask, double* out,
+                          int accumulate, const nk_cg_state* st, nk_stream_t stream) {
+  if (ni < 2 || ni > 16 || no < 2 || no > 16 || nelem < 0 || !M ||
+      (nelem > 0 && (!in || !out))) {
+    set_error("interp3: invalid arguments (ni=%d no=%d nelem=%lld)", ni, no, (long long)nelem);
+    return NK_ERR_INVALID;
+  }
+  if (nelem == 0) return NK_OK;
+  if (nelem > 0x7fffffffLL) {
+    set_error("interp3: too many elements");
+    return NK_ERR_INVALID;
+  }
+  TransferM T;
+  for (int q = 0; q < no * ni; ++q) T.m[q] = M[q];
+  const size_t smem = sizeof(double) * (size_t)(ni * ni * ni + ni * ni * no + ni * no * no);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t err = cudaFuncSetAttribute(interp3_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(sizeof(double) * 3 * 4096));
+    if (err != cudaSuccess) {
+      set_error("interp3: smem attribute: %s", cudaGetErrorString(err));
+      return NK_ERR_CUDA;
+    }
+    configured = true;
+  }
+  interp3_kernel<<<(unsigned)nelem, 256, smem, S(stream)>>>(ni, no, T, in, sub, wt, mask, out,
+                                                            accumulate, st);
+  return check_launch("interp3");
+}
+
+extern "C" int nk_cheb_step(int64_t n, const double* r, const double* Aq, const double* invD,
+                            double* res_out, double* d, double* e, double a, double b, int e_acc,
+                            const nk_cg_state* st, nk_stream_t stream) {
+  if (n < 0 || (n > 0 && (!r || !invD || !d || !e))) {
+    set_error("cheb_step: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  if (n == 0) return NK_OK;
+  cheb_step_kernel<<<grid_stride(n, 256, 8 * 148), 256, 0, S(stream)>>>(n, r, Aq, invD, res_out, d,
+                                                                         e, a, b, e_acc, st);
+  return check_launch("cheb_step");
+}
+
+extern "C" int nk_dense_matvec(int64_t n, const double* A, const double* x, double* y,
+                               const nk_cg_state* st, nk_stream_t stream) {
+  if (n < 0 || (n > 0 && (!A || !x || !y))) {
+    set_error("dense_matvec: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  if (n == 0) return NK_OK;
+  dense_matvec_kernel<<<grid_stride(n, 8, 16 * 148), 256, 0, S(stream)>>>(n, A, x, y, st);
+  return check_launch("dense_matvec");
+}

@@ -401,6 +401,13 @@ def pcg(apply_A, apply_M, b, tol=1e-8, max_iter=1000, flexible=False, weights=No
         if host:
             res = res._replace(x=res.x.cpu().numpy().reshape(np.shape(b)))
         return res
+    from .multigrid import MultigridHierarchy, MultigridPCG
+    if (isinstance(apply_A, PoissonOperator) and isinstance(apply_M, MultigridHierarchy)
+            and apply_M.levels[0].op is apply_A and x0 is None and weights is None):
+        res = MultigridPCG(apply_A, apply_M, tol, max_iter, flexible).solve(bt)
+        if host:
+            res = res._replace(x=res.x.cpu().numpy().reshape(np.shape(b)))
+        return res
     return _pcg_generic(apply_A, apply_M, bt, tol, max_iter, flexible, weights, x0, host,
                         np.shape(b))
 

@@ -1,0 +1,152 @@
+"""CPU: the p-multigrid oracle (oracle/pmg.py) against SPEC.md's examples
+ and the product's host-side Chebyshev logic."""
+
+import numpy as np
+import pytest
+
+from oracle import gs as ogs
+from oracle import pmg
+from oracle import solvers as osol
+
+
+def _rhs(lv):
+    X = lv.mesh.xyz.reshape(3, -1)
+    f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+    return lv.mask * ogs.gs_op(lv.mesh.ids, lv.mesh.B.ravel() * f)
+
+
+def _assembled_random(lv, seed):
+    x = np.random.default_rng(seed).standard_normal(lv.mask.size)
+    return lv.mask * ogs.gs_op(lv.mesh.ids, lv.wt * x)
+
+
+@pytest.fixture(scope="module")
+def h7():
+    return pmg.build_hierarchy((1, 1, 1), (2, 2, 2), 7, deformation=("sine", 0.05))
+
+
+def test_orders():
+    assert pmg.orders_for(7) == [7, 3, 1]
+    assert pmg.orders_for(8) == [8, 4, 1]
+    assert pmg.orders_for(3) == [3, 1]
+    assert pmg.orders_for(2) == [2, 1]
+    assert pmg.orders_for(1) == [1]
+
+
+def test_product_orders_and_coefficients_match_oracle():
+    from paper_2104_05829_b200.multigrid import chebyshev_coefficients, pmg_orders
+    for N in range(1, 16):
+        assert pmg_orders(N) == pmg.orders_for(N)
+    # the coefficient recurrence reproduces the oracle smoother on a dense SPD
+    # matrix, and its error propagator equals T_k((theta - l)/delta) / T_k(theta/delta)
+    rng = np.random.default_rng(0)
+    Q, _ = np.linalg.qr(rng.standard_normal((10, 10)))
+    A = Q @ np.diag(np.linspace(1, 10, 10)) @ Q.T
+    Dinv = 1.0 / np.diag(A)
+    lam = np.linalg.eigvals(Dinv[:, None] * A).real
+    lmax = lam.max()
+    lo, hi = 0.1 * lmax, 1.1 * lmax
+    for deg in (1, 2, 3, 5):
+        coef = chebyshev_coefficients(deg, lo, hi)
+        S = np.zeros_like(A)
+        for c in range(10):
+            r = np.eye(10)[c]
+            res, d, e = r.copy(), np.zeros(10), np.zeros(10)
+            for i, (a, b) in enumerate(coef):
+                if i:
+                    res = res - A @ d
+                d = a * d + b * Dinv * res
+                e = e + d
+            S[:, c] = e
+        Eprop = np.eye(10) - S @ A
+        # similarity: D^-1 A = V diag(lam) V^-1, Eprop = p(D^-1 A)
+        w, V = np.linalg.eig(Dinv[:, None] * A)
+        theta, delta = 0.5 * (hi + lo), 0.5 * (hi - lo)
+        Tk = lambda x: np.cos(deg * np.arccos(x)) if abs(x) <= 1 else np.cosh(deg * np.arccosh(abs(x))) * np.sign(x) ** deg
+        pw = np.array([Tk((theta - l) / delta) / Tk(theta / delta) for l in w.real])
+        Eref = (V @ np.diag(pw) @ np.linalg.inv(V)).real
+        assert np.max(np.abs(Eprop - Eref)) < 1e-10
+    with pytest.raises(ValueError):
+        chebyshev_coefficients(0, lo, hi)
+    with pytest.raises(ValueError):
+        chebyshev_coefficients(2, hi, lo)
+
+
+def test_chebyshev_base_case_and_zero(h7):
+    lv = h7["levels"][0]
+    r = _assembled_random(lv, 1)
+    e1 = pmg.chebyshev_smooth(lv, r, 1, lv.lo, lv.hi)
+    assert np.allclose(e1, lv.invD * r / (0.5 * (lv.lo + lv.hi)), rtol=0, atol=1e-15)
+    assert not np.any(pmg.chebyshev_smooth(lv, 0 * r, 2, lv.lo, lv.hi))
+
+
+def test_lambda_max_estimate_brackets(h7):
+    """The power estimate is below the true lambda_max and the 1.1 bound
+    above it (the smoother must not amplify the top of the spectrum)."""
+    lv = h7["levels"][0]
+    x = _assembled_random(lv, 7)
+    for _ in range(150):
+        y = lv.invD * pmg._apply_op(lv, x)
+        x = y / np.sqrt(np.sum(lv.wt * y * y))
+    y = lv.invD * pmg._apply_op(lv, x)
+    true = np.sqrt(np.sum(lv.wt * y * y)) / np.sqrt(np.sum(lv.wt * x * x))
+    assert lv.lmax <= true * (1 + 1e-9)
+    assert 1.1 * lv.lmax >= true
+
+
+def test_vcycle_zero_and_symmetric(h7):
+    lv = h7["levels"][0]
+    assert not np.any(pmg.vcycle(h7, np.zeros(lv.mask.size)))
+    r1, r2 = _assembled_random(lv, 2), _assembled_random(lv, 3)
+    a = np.sum(lv.wt * pmg.vcycle(h7, r1) * r2)
+    b = np.sum(lv.wt * r1 * pmg.vcycle(h7, r2))
+    assert abs(a - b) < 1e-12 * max(abs(a), 1.0)
+
+
+def test_vcycle_is_contraction(h7):
+    """one V-cycle reduces the A-norm error of a random guess
+    by >= 1.5 (x* = 0, b = 0: e <- e - M^-1 A e)."""
+    lv = h7["levels"][0]
+    A = pmg.fine_operator(h7)
+    e = _assembled_random(lv, 4)
+    anorm = lambda v: np.sqrt(np.sum(lv.wt * v * A(v)))
+    e1 = e - pmg.vcycle(h7, A(e))
+    assert anorm(e) / anorm(e1) >= 1.5
+
+
+def test_coarse_solve_recovers_unit_vector():
+    h = pmg.build_hierarchy((1, 1, 1), (2, 2, 2), 1)
+    lv = h["levels"][0]
+    assert len(h["levels"]) == 1
+    # the single interior dof of a 2x2x2 N=1 Dirichlet box
+    A = pmg.fine_operator(h)
+    ek = np.zeros(lv.mask.size)
+    ek[lv.mesh.ids == lv.mesh.ids[lv.mask.astype(bool)][0]] = 1.0
+    z = pmg.vcycle(h, A(ek))           # one level: exact coarse solve
+    assert np.max(np.abs(z - ek)) < 1e-12
+
+
+def test_coarse_solve_neumann_mean_zero():
+    h = pmg.build_hierarchy((1, 1, 1), (2, 2, 2), 1, bc="neumann")
+    lv = h["levels"][0]
+    A = pmg.fine_operator(h)
+    x = _assembled_random(lv, 5)
+    z = pmg.vcycle(h, A(x))
+    Q = lv.coarse[0]
+    zu = Q.T @ (lv.wt * z)
+    xu = Q.T @ (lv.wt * x)
+    assert abs(zu.mean()) < 1e-12
+    assert np.max(np.abs(zu - (xu - xu.mean()))) < 1e-10
+
+
+def test_pmg_pcg_beats_jacobi(h7):
+    """on the N=7, E=8 box, p-MG-PCG needs strictly fewer
+    iterations than Jacobi-PCG; both reach the same solution."""
+    lv = h7["levels"][0]
+    b = _rhs(lv)
+    A = pmg.fine_operator(h7)
+    rm = osol.pcg(A, lambda r: pmg.vcycle(h7, r), b, tol=1e-8, max_iter=200, weights=lv.wt)
+    rj = osol.pcg(A, lambda r: lv.invD * r, b, tol=1e-8, max_iter=2000, weights=lv.wt)
+    assert rm.converged and rj.converged
+    assert rm.iterations < rj.iterations
+    assert np.max(np.abs(rm.x - rj.x)) < 1e-7 * np.max(np.abs(rj.x))
