@@ -323,6 +323,28 @@ int nk_dense_matvec(int64_t n, const double* A, const double* x, double* y,
 int nk_wdot(int64_t n, const double* a, const double* b, const double* wt, double* out,
             double* partials, nk_stream_t stream);
 
+/* ---- projection-based initial guesses ----
+ * The ProjectionSpace holds k <= NK_PROJ_MAX prior solutions X[q] and A X[q]
+ * (row q at X + q*ldx).  project_guess / update are sequenced on the host
+ * (paper_2104_05829_b200/projection.py) from these three primitives. */
+#define NK_PROJ_MAX 16
+
+/* partial-sum scratch (doubles) nk_multi_wdot needs */
+int64_t nk_multi_wdot_partials_len(void);
+
+/* out[q] = sum_i wt_i X[q]_i y_i for q < k (wt nullable), deterministic
+ * two-stage reduction; out is [dev] k doubles. */
+int nk_multi_wdot(int64_t n, int k, const double* X, int64_t ldx, const double* y,
+                  const double* wt, double* out, double* partials, nk_stream_t stream);
+
+/* yout = yin + scale * sum_{q<k} c[q] V[q]   (c [dev] k doubles; yin nullable
+ * = 0; yin may alias yout). */
+int nk_multi_axpy(int64_t n, int k, const double* c, double scale, const double* V, int64_t ldv,
+                  const double* yin, double* yout, nk_stream_t stream);
+
+/* y = x / sqrt(s[0])  (s [dev]); A-normalisation of a new basis vector. */
+int nk_vscale(int64_t n, const double* x, double* y, const double* s, nk_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif
