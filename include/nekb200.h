@@ -345,6 +345,32 @@ int nk_multi_axpy(int64_t n, int k, const double* c, double scale, const double*
 /* y = x / sqrt(s[0])  (s [dev]); A-normalisation of a new basis vector. */
 int nk_vscale(int64_t n, const double* x, double* y, const double* s, nk_stream_t stream);
 
+/* ---- overlapping Schwarz smoother with FDM local solves ----------------
+ * (SPEC.md:410-418 fdm_local_solve, 499-507 schwarz_smooth; PAPER.md:228-231,
+ * 298-313).  Extended element boxes have (N+3)^3 points [e][k'][j'][i'].
+ *   fmap [dev] int32 [E][6][(N+1)^2]: local index (into r) of the point one
+ *        layer inside the face neighbour, faces x- x+ y- y+ z- z+, tangential
+ *        (slow, fast) = (k,j) | (k,i) | (j,i); -1 = no neighbour.
+ *   S    [dev] FP64 [E][3][N+3][N+3]: per element and direction, S[p][mode]
+ *        with S^T M S = I (generalised eigenvectors of the 1-D surrogate).
+ *   lam  [dev] FP64 [E][3][N+3]: eigenvalues, +inf for dropped points. */
+
+/* out = FDM solve of the extended residual of (r - sub): (S3) diag(1/(lam0
+ * (Lx+Ly+Lz) + lam1)) (S3)^T r_ext per element.  out_ext != 0: out is the
+ * extended field [E][(N+3)^3] (ASM); else the own points [E][(N+1)^3] (RAS).
+ * sub, res_out nullable; res_out (own points) receives r - sub and must not
+ * alias r or sub.  Skipped once st->done (st nullable). */
+int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, double* res_out,
+           const int32_t* fmap, const double* S, const double* lam, double lam0, double lam1,
+           double* out, int out_ext, const nk_cg_state* st, nk_stream_t stream);
+
+/* z = mask * W * src (own points; src extended [E][(N+3)^3] if src_ext) fused
+ * with d = a d + b z (d nullable: d := b z not stored) and e = (e_acc ? e : 0)
+ * + d.  W, mask nullable. */
+int nk_schwarz_post(int N, int64_t nelem, const double* src, int src_ext, const double* W,
+                    const uint8_t* mask, double* d, double* e, double a, double b, int e_acc,
+                    const nk_cg_state* st, nk_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

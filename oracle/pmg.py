@@ -16,8 +16,12 @@ Frozen choices:
   * transfers: prolongation e_f = (J x J x J) e_c per element with
     J = interp_matrix(coarse nodes -> fine nodes) (basis.py:99-117);
     restriction r_c = mask_c * QQ^T_c (J^T x J^T x J^T)(r_f / mult_f);
-  * smoother: Chebyshev on D^-1 A with x0 = 0 (Saad's 3-term recurrence),
-    `degree` terms, degree - 1 operator applications;
+  * smoother: Chebyshev on S A with x0 = 0 (Saad's 3-term recurrence),
+    `degree` terms, degree - 1 operator applications, S the inner smoother:
+    D^-1 (cheby_jac; 'jacobi' = degree 1, the Chebyshev-optimal damped
+    Jacobi), or an overlapping Schwarz solve (cheby_asm / cheby_ras,
+    oracle/schwarz.py, PAPER.md:298-313 CHEBY-ASM); 'asm' / 'ras' apply the
+    Schwarz smoother once, undamped (SPEC.md:462-464);
   * V-cycle: pre-smooth, residual, restrict, recurse, prolong + correct,
     post-smooth on the updated residual; coarsest level: exact solve of the
     assembled masked operator (dense inverse on unique unmasked dofs).
@@ -28,7 +32,10 @@ import numpy as np
 from . import gs as ogs
 from . import mesh as om
 from . import operators as oop
+from . import schwarz as osz
 from .basis import Basis, interp_matrix
+
+SMOOTHERS = ("jacobi", "cheby_jac", "asm", "ras", "cheby_asm", "cheby_ras")
 
 
 class Level:
@@ -60,8 +67,15 @@ def _interp3(M, v, E):
     return t
 
 
+def inner(lv, r):
+    """The inner smoother S r of a level (D^-1, or Schwarz)."""
+    if lv.schwarz is None:
+        return lv.invD * r
+    return osz.schwarz_smooth(lv.fdm, lv.schwarz, r, lv.mesh.ids, lv.mask)
+
+
 def power_lambda_max(lv, iters=20, seed=2104):
-    """lambda_max of D^-1 A by power iteration.  Start vector: a fixed-seed
+    """lambda_max of S A by power iteration.  Start vector: a fixed-seed
     random, assembled, masked field -- SPEC.md:491's masked ones vector is
     nearly free of high-frequency content and underestimates lambda_max by
     ~30% at N = 7 (10 iterations: 1.62 vs 2.41), which makes the Chebyshev
@@ -70,32 +84,42 @@ def power_lambda_max(lv, iters=20, seed=2104):
     x = lv.mask * ogs.gs_op(lv.mesh.ids, lv.wt * x)
     lam = 0.0
     for _ in range(iters):
-        y = lv.invD * _apply_op(lv, x)
+        y = inner(lv, _apply_op(lv, x))
         lam = float(np.sqrt(np.sum(lv.wt * y * y)) / np.sqrt(np.sum(lv.wt * x * x)))
         x = y / np.sqrt(np.sum(lv.wt * y * y))
     return lam
 
 
 def chebyshev_smooth(lv, r, degree, lo, hi):
-    """Chebyshev-accelerated Jacobi on A e = r from e0 = 0."""
+    """Chebyshev-accelerated inner smoother on A e = r from e0 = 0
+    (SPEC.md:489-497)."""
     theta = 0.5 * (hi + lo)
     delta = 0.5 * (hi - lo)
     sigma = theta / delta
     rho = 1.0 / sigma
     res = r.copy()
-    d = (1.0 / theta) * lv.invD * res
+    d = (1.0 / theta) * inner(lv, res)
     x = d.copy()
     for _ in range(1, degree):
         res = res - _apply_op(lv, d)
         rho_new = 1.0 / (2.0 * sigma - rho)
-        d = (rho_new * rho) * d + (2.0 * rho_new / delta) * (lv.invD * res)
+        d = (rho_new * rho) * d + (2.0 * rho_new / delta) * inner(lv, res)
         rho = rho_new
         x = x + d
     return x
 
 
+def smooth(lv, r, degree):
+    """One smoothing of A e = r from e0 = 0 with the level's smoother kind."""
+    if lv.kind in ("asm", "ras"):
+        return inner(lv, r)
+    return chebyshev_smooth(lv, r, 1 if lv.kind == "jacobi" else degree, lv.lo, lv.hi)
+
+
 def build_hierarchy(extent, counts, N, bc="dirichlet", deformation=None, lam0=1.0, lam1=0.0,
-                    degree=2, bounds=(0.1, 1.1), power_iters=20):
+                    degree=2, bounds=(0.1, 1.1), power_iters=20, smoother="cheby_jac"):
+    if smoother not in SMOOTHERS:
+        raise ValueError(f"unknown smoother {smoother!r}")
     levels = []
     for n in orders_for(N):
         lv = Level()
@@ -107,6 +131,13 @@ def build_hierarchy(extent, counts, N, bc="dirichlet", deformation=None, lam0=1.
         diag = ogs.gs_op(lv.mesh.ids, oop.local_diagonal(lv.mesh.basis.diff, lv.mesh.G, lam0,
                                                          lv.mesh.B, lam1).ravel())
         lv.invD = lv.mask / diag
+        lv.kind = smoother
+        lv.schwarz = {"asm": "asm", "cheby_asm": "asm", "ras": "ras",
+                      "cheby_ras": "ras"}.get(smoother)
+        lv.fdm = None
+        if lv.schwarz is not None and n != orders_for(N)[-1]:
+            lv.fdm = osz.fdm_setup(lv.mesh.xyz, lv.mesh.ids, lv.mask, lv.mesh.E, n,
+                                   lv.mesh.basis.diff, lv.mesh.basis.weights, lam0, lam1)
         levels.append(lv)
     for lv in levels[:-1]:
         lv.lmax = power_lambda_max(lv, power_iters)
@@ -153,7 +184,7 @@ def vcycle(h, r, level=0):
         Q, Ainv = lv.coarse
         return lv.mask * (Q @ (Ainv @ (Q.T @ (lv.wt * r))))
     deg = h["degree"]
-    e = chebyshev_smooth(lv, r, deg, lv.lo, lv.hi)
+    e = smooth(lv, r, deg)
     res = r - _apply_op(lv, e)
     c = L[level + 1]
     Jt = lv.J.T
@@ -162,7 +193,7 @@ def vcycle(h, r, level=0):
     ec = vcycle(h, rc, level + 1)
     e = e + lv.mask * _interp3(lv.J, ec, lv.mesh.E).ravel()
     res = r - _apply_op(lv, e)
-    e = e + chebyshev_smooth(lv, res, deg, lv.lo, lv.hi)
+    e = e + smooth(lv, res, deg)
     return e
 
 

@@ -9,7 +9,7 @@ include/nekb200.h); PyTorch only owns device buffers and streams.
 """
 
 from . import (basis, distributed, gather_scatter, kernels, mesh, multigrid,  # noqa: F401
-               partition, projection, solvers)
+               partition, projection, schwarz, solvers)
 from ._lib import (ContractError, NativeLibraryError, UnsupportedOrderError,  # noqa: F401
                    LIB_PATH)
 from .basis import InvalidOrderError, SpectralBasis, gll_rule, interp_matrix  # noqa: F401
@@ -22,6 +22,7 @@ from .multigrid import (MultigridHierarchy, MultigridPCG, chebyshev_smooth,  # n
                         coarse_solve, pmg_preconditioner)
 from .partition import rcb  # noqa: F401
 from .projection import ProjectedSolver, ProjectionSpace, project_guess  # noqa: F401
+from .schwarz import SchwarzSmoother, fdm_local_solve, schwarz_smooth  # noqa: F401
 from .solvers import (BreakdownError, FusedPCG, HelmholtzVectorSolver,  # noqa: F401
                       JacobiPreconditioner, PoissonOperator, pcg)
 

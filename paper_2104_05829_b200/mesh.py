@@ -19,7 +19,7 @@ in (z, y, x) order; 'sine' deformation
 import numpy as np
 
 from . import _lib
-from ._lib import check, lib, ptr, stream_ptr
+from ._lib import ContractError, check, lib, ptr, stream_ptr
 from .basis import SpectralBasis
 
 FACES = ("x-", "x+", "y-", "y+", "z-", "z+")
@@ -183,6 +183,32 @@ def build_box_mesh(extent, counts, N, bc="dirichlet", deformation=None, origin=(
              origin=tuple(float(v) for v in origin), bc=bcn, deformation=deformation,
              elements=None if elements is None else np.asarray(elements, dtype=np.int64))
     return m
+
+
+def mesh_coordinates(m):
+    """GLL point coordinates (3, E, nq, nq, nq) of a mesh on its device: the
+    stored ones, or (box meshes built without keep_coords) regenerated by
+    nk_box_coords with the mesh's own counts / extent / deformation."""
+    import torch
+    if m.xyz is not None:
+        return m.xyz
+    if m.counts is None:
+        raise ContractError("mesh has neither coordinates nor a box description")
+    N, nq = m.N, m.nq
+    _, nodes, _ = m.basis.device_arrays(m.device)
+    eidx = None if m.elements is None else torch.as_tensor(m.elements, device=m.device)
+    callable_def = callable(m.deformation)
+    kind, amp = (0, 0.0) if callable_def else _deform_spec(m.deformation)
+    xyz = torch.empty((3, m.E, nq, nq, nq), dtype=torch.float64, device=m.device)
+    check(lib().nk_box_coords(N, m.E, ptr(eidx), ptr(np.array(m.counts, dtype=np.int32)),
+                              ptr(np.array(m.extent, dtype=np.float64)),
+                              ptr(np.array(m.origin, dtype=np.float64)), kind, amp, ptr(nodes),
+                              ptr(xyz), stream_ptr()), "box_coords")
+    if callable_def:
+        h = xyz.cpu().numpy()
+        x, y, z = m.deformation(h[0], h[1], h[2])
+        xyz = torch.as_tensor(np.stack([x, y, z]).astype(np.float64), device=m.device)
+    return xyz
 
 
 def geometric_factors(element_xyz, basis, device="cuda"):

@@ -20,11 +20,18 @@ Setup (meshes per order, gs plans, lambda_max by power iteration, the coarse
 inverse) runs once on the device through the same library plus torch
 linear algebra.
 
+Smoothers (SPEC.md:462-464 SmootherConfig kinds): 'cheby_jac' (default),
+'jacobi' (Chebyshev degree 1 = optimally damped Jacobi), 'asm' / 'ras' (one
+overlapping-Schwarz FDM application, paper_2104_05829_b200/schwarz.py) and
+'cheby_asm' / 'cheby_ras' (Chebyshev acceleration of the Schwarz smoother,
+PAPER.md:312-313 CHEBY-ASM).  Schwarz smoothing is not symmetric in the PCG
+inner product (the counting weight): use flexible PCG.
+
 Frozen choices (oracle/pmg.py states the same algorithm on the CPU):
-degree 2, bounds (0.1, 1.1) x lambda_max, lambda_max from 20 power
-iterations from a fixed-seed random start (SPEC's 10 iterations from the
-ones vector underestimate it by ~30% at N = 7 and make the smoother amplify
-the top of the spectrum -- DESIGN.md "p-multigrid").
+degree 2, bounds (0.1, 1.1) x lambda_max of S A (S the inner smoother),
+lambda_max from 20 power iterations from a fixed-seed random start (SPEC's
+10 iterations from the ones vector underestimate it by ~30% at N = 7 and make
+the smoother amplify the top of the spectrum -- DESIGN.md "p-multigrid").
 """
 
 import numpy as np
@@ -35,7 +42,10 @@ from .gather_scatter import _halo_exchange, _halo_finish, _halo_start, _local
 from .mesh import Mesh, assign_global_ids, build_box_mesh, mesh_from_coords
 
 __all__ = ["MultigridHierarchy", "MultigridPCG", "chebyshev_smooth", "pmg_preconditioner",
-           "coarse_solve", "chebyshev_coefficients", "pmg_orders"]
+           "coarse_solve", "chebyshev_coefficients", "pmg_orders", "SMOOTHERS"]
+
+SMOOTHERS = ("jacobi", "cheby_jac", "asm", "ras", "cheby_asm", "cheby_ras")
+_SCHWARZ = {"asm": "asm", "ras": "ras", "cheby_asm": "asm", "cheby_ras": "ras"}
 
 DENSE_COARSE_MAX = 16384     # unique unmasked coarse dofs (2 GiB FP64 inverse)
 
@@ -125,7 +135,7 @@ class MultigridHierarchy:
     coarse problem exceeds DENSE_COARSE_MAX unique dofs."""
 
     def __init__(self, op, degree=2, bounds=(0.1, 1.1), power_iters=20, seed=2104,
-                 coarse="dense"):
+                 coarse="dense", smoother="cheby_jac"):
         import torch
         from .solvers import JacobiPreconditioner, PoissonOperator
         if op.ncomp != 1:
@@ -140,6 +150,9 @@ class MultigridHierarchy:
         self.degree = int(degree)
         if self.degree < 1:
             raise ContractError("Chebyshev degree must be >= 1")
+        if smoother not in SMOOTHERS:
+            raise ContractError(f"unknown smoother {smoother!r} (built: {SMOOTHERS})")
+        self.smoother = smoother
         self.bounds = (float(bounds[0]), float(bounds[1]))
         self.orders = pmg_orders(op.mesh.N)
         dev = op.mesh.device
@@ -159,13 +172,21 @@ class MultigridHierarchy:
             f = lambda: torch.zeros(lv.n, dtype=torch.float64, device=dev)
             lv.e, lv.d, lv.res, lv.Aq = f(), f(), f(), f()
             lv.r = f() if self.levels else None
+            lv.kind = smoother
+            lv.sm = None
             self.levels.append(lv)
+        from .schwarz import SchwarzSmoother
+        for lv in self.levels[:-1]:
+            if smoother in _SCHWARZ:
+                lv.sm = SchwarzSmoother(lv.op, _SCHWARZ[smoother])
+                lv.res2 = torch.zeros_like(lv.res)
+            lv.deg = 1 if smoother in ("jacobi", "asm", "ras") else self.degree
         for lv in self.levels[:-1]:
             lv.lmax = self._power_lambda_max(lv, power_iters, seed)
             if not lv.lmax > 0.0:
                 raise ContractError(f"lambda_max estimate {lv.lmax} <= 0 (order {lv.order})")
             lv.lo, lv.hi = self.bounds[0] * lv.lmax, self.bounds[1] * lv.lmax
-            lv.coef = chebyshev_coefficients(self.degree, lv.lo, lv.hi)
+            lv.coef = chebyshev_coefficients(lv.deg, lv.lo, lv.hi)
         for f, c in zip(self.levels[:-1], self.levels[1:]):
             J = lagrange_interp_matrix(c.mesh.basis.nodes, f.mesh.basis.nodes)  # (nq_f, nq_c)
             f.P = np.ascontiguousarray(J)
@@ -185,7 +206,10 @@ class MultigridHierarchy:
         lam = 0.0
         for _ in range(int(iters)):
             lv.op.apply(x, y)
-            y = lv.invD * y
+            if lv.sm is not None:
+                y = lv.sm(y)
+            else:
+                y = lv.invD * y
             ny = float(torch.sqrt(torch.sum(lv.wt * y * y)))
             nx = float(torch.sqrt(torch.sum(lv.wt * x * x)))
             lam = ny / nx
@@ -259,11 +283,14 @@ class MultigridHierarchy:
         lv.op.apply(x, y)
 
     def _cheb(self, lv, r, st, post):
-        """Chebyshev-Jacobi smoothing of A e = r into lv.e.  Pre: e = S r.
-        Post (r = the level's right-hand side, lv.Aq = A e on entry):
-        e += S (r - A e).  (oracle/pmg.py:chebyshev_smooth)"""
+        """Smoothing of A e = r into lv.e.  Pre: e = S r.  Post (r = the
+        level's right-hand side, lv.Aq = A e on entry): e += S (r - A e).
+        (oracle/pmg.py:smooth / chebyshev_smooth)"""
+        if lv.sm is not None:
+            self._cheb_schwarz(lv, r, st, post)
+            return
         L, s = lib(), stream_ptr()
-        deg = self.degree
+        deg = lv.deg
         a0, b0 = lv.coef[0]
         keep_res = deg > 1
         check(L.nk_cheb_step(lv.n, ptr(r), ptr(lv.Aq) if post else None, ptr(lv.invD),
@@ -277,6 +304,30 @@ class MultigridHierarchy:
             check(L.nk_cheb_step(lv.n, ptr(src), ptr(lv.Aq), ptr(lv.invD), ptr(store),
                                  ptr(lv.d), ptr(lv.e), a, b, 1, ptr(st), s), "cheb_step")
             src = lv.res
+
+    def _cheb_schwarz(self, lv, r, st, post):
+        """Schwarz smoothing: 'asm'/'ras' one application; cheby_* the
+        Chebyshev recurrence with the Schwarz solve as inner smoother.  The
+        residual update r - A d is fused into the FDM gather (sub = A d);
+        residuals ping-pong between two buffers (the gather reads neighbour
+        points of the buffer the previous step wrote)."""
+        sm = lv.sm
+        if lv.kind in ("asm", "ras"):
+            sm.apply(r, lv.e, sub=lv.Aq if post else None, e_acc=post, st=st)
+            return
+        deg = lv.deg
+        bufs = (lv.res, lv.res2)
+        a0, b0 = lv.coef[0]
+        store = bufs[0] if (post and deg > 1) else None
+        sm.apply(r, lv.e, sub=lv.Aq if post else None, res_out=store, d=lv.d, a=a0, b=b0,
+                 e_acc=post, st=st)
+        src = store if post else r
+        for i in range(1, deg):
+            self._apply_A(lv, lv.d, lv.Aq)
+            a, b = lv.coef[i]
+            store = bufs[i % 2] if i < deg - 1 else None
+            sm.apply(src, lv.e, sub=lv.Aq, res_out=store, d=lv.d, a=a, b=b, e_acc=True, st=st)
+            src = store
 
     def _coarse(self, lv, r, st):
         L, s = lib(), stream_ptr()
@@ -323,28 +374,32 @@ class MultigridHierarchy:
         for lv in self.levels[:-1]:
             g = 1                                             # gs (single rank)
             A = 1 + g
-            n += 2 * self.degree                              # cheb steps (pre + post)
-            n += 2 * (self.degree - 1) * A                    # A d inside smoothing
+            per = 3 if lv.sm is not None else 1               # fdm + gs + post | cheb step
+            n += 2 * lv.deg * per                             # smoothing steps (pre + post)
+            n += 2 * (lv.deg - 1) * A                         # A d inside smoothing
             n += 2 * A                                        # A e before restrict / after prolong
             n += 2 + g                                        # interp x2, coarse gs
         return n + 3
 
 
 def chebyshev_smooth(hierarchy, level, r, degree=None):
-    """Correction e = S r of one Chebyshev-Jacobi smoothing (e0 = 0) at
-    `level` of a hierarchy.  Returns a new tensor."""
+    """Correction e = S r of one smoothing (e0 = 0) with the hierarchy's
+    smoother at `level` (degree overrides the Chebyshev
+    degree).  Returns a new tensor."""
     h = hierarchy
     lv = h.levels[level]
     if level == len(h.levels) - 1:
         raise ContractError("the coarsest level is solved directly, not smoothed")
-    old = h.degree, lv.coef
-    if degree is not None and int(degree) != h.degree:
-        h.degree = int(degree)
-        lv.coef = chebyshev_coefficients(h.degree, lv.lo, lv.hi)
+    old = lv.deg, lv.coef
+    if degree is not None and int(degree) != lv.deg:
+        if int(degree) < 1:
+            raise ContractError("Chebyshev degree must be >= 1")
+        lv.deg = int(degree)
+        lv.coef = chebyshev_coefficients(lv.deg, lv.lo, lv.hi)
     try:
         h._cheb(lv, r.reshape(-1).contiguous(), None, post=False)
     finally:
-        h.degree, lv.coef = old
+        lv.deg, lv.coef = old
     return lv.e.clone().view_as(r)
 
 

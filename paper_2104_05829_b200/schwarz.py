@@ -1,0 +1,252 @@
+"""Overlapping Schwarz smoothers with FDM local solves.
+
+Drop-in for nekmini's ``fdm_local_solve`` and ``schwarz_smooth`` (SPEC.md:
+410-418, 499-507) and the smoother kinds asm / ras / cheby_asm / cheby_ras of
+``SmootherConfig``:
+each spectral element is extended by one layer of points from its face
+neighbours ((N+3)^3 boxes), the residual there is solved exactly for an
+axis-aligned box surrogate by fast diagonalisation, and the results are
+combined by exchange-and-add with the counting weight (ASM) or kept per
+element (RAS).
+
+Per application (all libnekb200 launches on the current stream, CUDA-graph
+capturable, skipped once the PCG state says done):
+  nk_fdm            gather r (- A e) on the extended boxes, 6 tensor
+                    contractions + inverse spectrum, write the extended (ASM)
+                    or own-point (RAS) solution;
+  gs                ASM: the extended-id gs handle (SPEC.md:504's "dedicated gs
+                    handle"); RAS: the operator's own QQ^T;
+  nk_schwarz_post   z = mask * weight * (own points), fused with the
+                    Chebyshev update d = a d + b z, e (+)= d.
+Setup (face-neighbour map from global ids, element lengths, the batched 1-D
+generalised eigenproblems, extended ids and counting weights) runs once on the
+host/device.  oracle/schwarz.py states the same algorithm on the CPU.
+"""
+
+import numpy as np
+
+from ._lib import ContractError, check, lib, ptr, stream_ptr
+
+__all__ = ["SchwarzSmoother", "fdm_local_solve", "schwarz_smooth", "face_source_map",
+           "fdm_1d_batch", "KINDS"]
+
+KINDS = ("asm", "ras")
+_NBR, _NEU, _DIR = 0, 1, 2
+_FACE_AXES = ((0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (2, 1))
+
+
+def _face_slice(nq, axis, side, inward=False):
+    p = (1 if side == 0 else nq - 2) if inward else (0 if side == 0 else nq - 1)
+    s = [slice(None)] * 4
+    s[3 - axis] = p
+    return tuple(s)
+
+
+def face_source_map(ids, E, N):
+    """fmap[e, f, a, b]: local index of the point one layer inside the face
+    neighbour across face f (x- x+ y- y+ z- z+) at e's face point (a, b)
+    (tangential slow, fast); -1 without a neighbour.  Neighbours are the
+    faces holding the same (N+1)^2 global ids (HEXMESH and periodic meshes
+    work unchanged).  Vectorised host setup; int64 (E, 6, nq, nq)."""
+    nq = N + 1
+    ids = np.asarray(ids, dtype=np.int64).reshape(E, nq, nq, nq)
+    loc = np.arange(E * nq ** 3, dtype=np.int64).reshape(E, nq, nq, nq)
+    fid = np.stack([ids[_face_slice(nq, a, s)].reshape(E, nq * nq) for a, s in _FACE_AXES], 1)
+    finw = np.stack([loc[_face_slice(nq, a, s, True)].reshape(E, nq * nq)
+                     for a, s in _FACE_AXES], 1)
+    fid = fid.reshape(E * 6, nq * nq)
+    finw = finw.reshape(E * 6, nq * nq)
+    fmap = np.full((E * 6, nq * nq), -1, dtype=np.int64)
+    if E == 0:
+        return fmap.reshape(E, 6, nq, nq)
+    srt = np.sort(fid, axis=1)
+    _, grp, cnt = np.unique(srt, axis=0, return_inverse=True, return_counts=True)
+    if np.any(cnt > 2):
+        raise ContractError("a face id set is held by more than two element faces")
+    grp = grp.ravel()
+    order = np.argsort(grp, kind="stable")
+    g = grp[order]
+    same = g[1:] == g[:-1]
+    r0, r1 = order[:-1][same], order[1:][same]
+    A = np.concatenate([r0, r1])
+    B = np.concatenate([r1, r0])
+    if len(A):
+        ob = np.argsort(fid[B], axis=1, kind="stable")
+        oa = np.argsort(fid[A], axis=1, kind="stable")
+        rank = np.empty_like(oa)
+        np.put_along_axis(rank, oa, np.arange(nq * nq)[None, :].repeat(len(A), 0), axis=1)
+        pos = np.take_along_axis(ob, rank, axis=1)
+        fmap[A] = np.take_along_axis(finw[B], pos, axis=1)
+    return fmap.reshape(E, 6, nq, nq)
+
+
+def fdm_1d_batch(D, w, h, left, right):
+    """Batched extended 1-D generalised eigenproblems (oracle/schwarz.py:
+    fdm_1d): h (B,), left/right (B,) side kinds 0 nbr / 1 neu / 2 dir.
+    Returns S (B, N+3, N+3) with S^T M S = I and lam (B, N+3), +inf on the
+    modes of dropped points (decoupled with a -1 diagonal, so eigh isolates
+    them)."""
+    D = np.asarray(D, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    N = len(w) - 1
+    nb = len(h)
+    n3 = 3 * N + 1
+    K1 = D.T @ (w[:, None] * D)
+    use = np.stack([left == _NBR, np.ones(nb, bool), right == _NBR], 1).astype(np.float64)
+    K = np.zeros((nb, n3, n3))
+    M = np.zeros((nb, n3))
+    for el in range(3):
+        s = el * N
+        K[:, s:s + N + 1, s:s + N + 1] += (use[:, el] * 2.0 / h)[:, None, None] * K1
+        M[:, s:s + N + 1] += (use[:, el] * h / 2.0)[:, None] * w
+    sel = np.arange(N - 1, 2 * N + 2)
+    K = K[:, sel][:, :, sel]
+    M = M[:, sel]
+    keep = np.ones((nb, N + 3), dtype=bool)
+    keep[:, 0] = left == _NBR
+    keep[:, 1] = left != _DIR
+    keep[:, N + 2] = right == _NBR
+    keep[:, N + 1] = right != _DIR
+    drop = ~keep
+    K = np.where(drop[:, :, None] | drop[:, None, :], 0.0, K)
+    K[:, np.arange(N + 3), np.arange(N + 3)] = np.where(drop, -1.0,
+                                                        K[:, np.arange(N + 3), np.arange(N + 3)])
+    M = np.where(drop, 1.0, M)
+    Mh = 1.0 / np.sqrt(M)
+    lam, V = np.linalg.eigh(Mh[:, :, None] * K * Mh[:, None, :])
+    S = Mh[:, :, None] * V
+    lam = np.where(lam < -0.5, np.inf, lam)
+    return S, lam
+
+
+class SchwarzSmoother:
+    """z = S r for a PoissonOperator (single rank): kind 'asm' or 'ras'.
+
+    Buffers are preallocated; ``apply`` writes into caller buffers so the
+    smoother can sit inside a captured CUDA graph (MultigridHierarchy)."""
+
+    def __init__(self, op, kind="asm"):
+        import torch
+        from .gather_scatter import gs_setup
+        from .mesh import mesh_coordinates
+        if kind not in KINDS:
+            raise ContractError(f"unknown Schwarz kind {kind!r} (built: {KINDS})")
+        if op.ncomp != 1:
+            raise ContractError("Schwarz smoothing is built for scalar operators")
+        if op.gs.comm is not None and op.gs.comm.size > 1:
+            raise ContractError("multi-rank Schwarz smoothing is not built (the extended "
+                                "boxes would need a second halo)")
+        m = op.mesh
+        self.op, self.kind, self.mesh = op, kind, m
+        N, E, nq = m.N, m.E, m.nq
+        nqe = N + 3
+        self.N, self.E, self.nqe = N, E, nqe
+        dev = m.device
+        ids = m.ids.detach().cpu().numpy().astype(np.int64).ravel()
+        mask = m.mask.detach().cpu().numpy().reshape(E, nq, nq, nq)
+        fmap = face_source_map(ids, E, N)
+        # side kinds
+        kinds = np.empty((E, 6), dtype=np.int64)
+        for f, (axis, side) in enumerate(_FACE_AXES):
+            masked = np.all(mask[_face_slice(nq, axis, side)].reshape(E, -1) == 0, axis=1)
+            kinds[:, f] = np.where(fmap[:, f, 0, 0] >= 0, _NBR, np.where(masked, _DIR, _NEU))
+        self.kinds = kinds
+        # element lengths (mean distance between opposite faces)
+        X = mesh_coordinates(m)
+        h = torch.zeros((E, 3), dtype=torch.float64, device=dev)
+        for d in range(3):
+            lo, hi = _face_slice(nq, d, 0), _face_slice(nq, d, 1)
+            diff = torch.stack([X[c][hi] - X[c][lo] for c in range(3)])
+            h[:, d] = torch.sqrt((diff ** 2).sum(0)).reshape(E, -1).mean(1)
+        h = h.cpu().numpy()
+        self.h = h
+        b = m.basis
+        S, lam = fdm_1d_batch(b.diff, b.weights, h.reshape(-1), kinds[:, 0::2].reshape(-1),
+                              kinds[:, 1::2].reshape(-1))
+        S = S.reshape(E, 3, nqe, nqe)
+        lam = lam.reshape(E, 3, nqe)
+        lam1 = float(op.lam1)
+        if lam1 == 0.0:
+            neu = np.all(kinds == _NEU, axis=1)
+            if neu.any():   # pure-Neumann surrogate: shift by eps = 1e-8 max(Lambda)
+                fin = np.isfinite(lam[neu])
+                eps = 1e-8 * np.sum(np.max(np.where(fin, lam[neu], 0.0), axis=2), axis=1)
+                lam[neu] = np.where(fin, lam[neu] + eps[:, None, None] / 3.0, np.inf)
+        self.S = torch.as_tensor(np.ascontiguousarray(S), device=dev)
+        self.lam = torch.as_tensor(np.ascontiguousarray(lam), device=dev)
+        self.fmap = torch.as_tensor(fmap.astype(np.int32), device=dev).contiguous()
+        self.mask = m.mask.reshape(-1)
+        n = E * nq ** 3
+        self.n = n
+        if kind == "asm":
+            src = np.full((E, nqe, nqe, nqe), -1, dtype=np.int64)
+            src[:, 1:nq + 1, 1:nq + 1, 1:nq + 1] = np.arange(n).reshape(E, nq, nq, nq)
+            for fi, (axis, side) in enumerate(_FACE_AXES):
+                s = [slice(None), slice(1, nq + 1), slice(1, nq + 1), slice(1, nq + 1)]
+                s[3 - axis] = 0 if side == 0 else nqe - 1
+                src[tuple(s)] = fmap[:, fi]
+            src = src.reshape(-1)
+            ext_ids = np.where(src >= 0, ids[np.maximum(src, 0)], 0)
+            self.ext_gs = gs_setup(ext_ids, device=dev)
+            self.buf = torch.zeros(E * nqe ** 3, dtype=torch.float64, device=dev)
+            cnt = torch.as_tensor((src >= 0).astype(np.float64), device=dev)
+            self._gs(self.ext_gs, cnt)
+            own = cnt.view(E, nqe, nqe, nqe)[:, 1:nq + 1, 1:nq + 1, 1:nq + 1].reshape(-1)
+            self.W = (1.0 / own).contiguous()
+            self.ext_ids = ext_ids
+        else:
+            self.ext_gs = None
+            self.buf = torch.zeros(n, dtype=torch.float64, device=dev)
+            self.W = op.weights
+
+    @staticmethod
+    def _gs(h, w, st=None):
+        from .gather_scatter import _local
+        _local(h, w, "+", 1, st=st)
+
+    @property
+    def launches(self):
+        return 3
+
+    def fdm(self, r, out, sub=None, res_out=None, out_ext=True, st=None):
+        """FDM local solves of the extended residual of r - sub (nk_fdm)."""
+        check(lib().nk_fdm(self.N, self.E, ptr(r), ptr(sub), ptr(res_out), ptr(self.fmap),
+                           ptr(self.S), ptr(self.lam), float(self.op.lam0), float(self.op.lam1),
+                           ptr(out), int(out_ext), ptr(st), stream_ptr()), "fdm")
+
+    def apply(self, r, e, sub=None, res_out=None, d=None, a=0.0, b=1.0, e_acc=False, st=None):
+        """z = S (r - sub); d = a d + b z (d optional); e = [e +] d.
+        res_out receives r - sub (must not alias r or sub)."""
+        asm = self.kind == "asm"
+        self.fdm(r, self.buf, sub, res_out, out_ext=asm, st=st)
+        self._gs(self.ext_gs if asm else self.op.gs, self.buf, st)
+        check(lib().nk_schwarz_post(self.N, self.E, ptr(self.buf), int(asm), ptr(self.W),
+                                    ptr(self.mask), ptr(d), ptr(e), float(a), float(b),
+                                    int(bool(e_acc)), ptr(st), stream_ptr()), "schwarz_post")
+        return e
+
+    def __call__(self, r):
+        import torch
+        rf = r.reshape(-1).contiguous()
+        if rf.numel() != self.n:
+            raise ContractError(f"contract error: field length {rf.numel()} != {self.n}")
+        z = torch.empty_like(rf)
+        self.apply(rf, z)
+        return z.view_as(r)
+
+
+def fdm_local_solve(smoother, residual):
+    """Extended FDM solution u_ext [E][(N+3)^3] of an assembled residual
+    (SPEC.md:410-418), a new tensor."""
+    import torch
+    rf = residual.reshape(-1).contiguous()
+    if rf.numel() != smoother.n:
+        raise ContractError(f"contract error: field length {rf.numel()} != {smoother.n}")
+    out = torch.empty(smoother.E * smoother.nqe ** 3, dtype=torch.float64, device=rf.device)
+    smoother.fdm(rf, out, out_ext=True)
+    return out.view(smoother.E, smoother.nqe, smoother.nqe, smoother.nqe)
+
+
+def schwarz_smooth(smoother, r):
+    """z = S r; a new tensor."""
+    return smoother(r)

@@ -1,0 +1,153 @@
+"""GPU parity: FDM local solves and overlapping Schwarz smoothers
+(paper_2104_05829_b200.schwarz; libnekb200 nk_fdm / nk_schwarz_post + gs)
+and the p-multigrid hierarchy with every SmootherConfig kind, against
+oracle/schwarz.py and oracle/pmg.py.  Bars: FDM and Schwarz applications
+within 1e-12 relative L2 (FP64, different summation order), lambda_max and
+V-cycles within 1e-9, flexible-PCG iteration counts within +-1 of the
+oracle at the same tolerance."""
+
+import numpy as np
+import pytest
+
+from oracle import gs as ogs
+from oracle import mesh as om
+from oracle import pmg as opmg
+from oracle import schwarz as osz
+from oracle import solvers as osol
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2104_05829_b200 as nk  # noqa: E402
+
+
+def rel_l2(a, b):
+    a, b = np.ravel(a), np.ravel(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+
+
+def pair(counts, N, bc="dirichlet", deformation=("sine", 0.05), lam0=1.0, lam1=0.0):
+    m = nk.build_box_mesh((1, 1, 1), counts, N, bc=bc, deformation=deformation)
+    o = om.build_box_mesh((1, 1, 1), counts, N, bc=bc, deformation=deformation)
+    op = nk.PoissonOperator(m, lam0=lam0, lam1=lam1)
+    f = osz.fdm_setup(o.xyz, o.ids, o.mask, o.E, N, o.basis.diff, o.basis.weights, lam0, lam1)
+    return m, o, op, f
+
+
+def assembled_random(o, seed):
+    x = np.random.default_rng(seed).standard_normal(o.mask.size)
+    return o.mask.ravel() * ogs.gs_op(o.ids, x / ogs.multiplicity(o.ids))
+
+
+CASES = [((3, 2, 2), 1, "dirichlet"), ((2, 2, 2), 2, "dirichlet"), ((3, 2, 2), 3, "dirichlet"),
+         ((2, 3, 2), 5, "periodic"), ((2, 2, 2), 7, "dirichlet"), ((2, 1, 2), 7, "neumann"),
+         ((2, 2, 1), 9, "dirichlet"), ((1, 2, 1), 12, "dirichlet"), ((1, 1, 2), 15, "dirichlet")]
+
+
+@pytest.mark.parametrize("counts,N,bc", CASES)
+def test_fdm_local_solve_matches_oracle(counts, N, bc):
+    m, o, op, f = pair(counts, N, bc=bc, lam0=0.8, lam1=(0.0 if bc == "dirichlet" else 2.5))
+    sm = nk.SchwarzSmoother(op, "asm")
+    assert np.array_equal(sm.fmap.cpu().numpy(), f.fmap)
+    r = assembled_random(o, N)
+    u = nk.fdm_local_solve(sm, dev(r)).cpu().numpy()
+    uo = osz.fdm_solve(f, osz.extend(f, r))
+    # sampled (non-dropped) points only: outputs at never-sampled box points
+    # are discarded by both smoothers
+    used = f.ext_ids.reshape(u.shape) != 0
+    assert rel_l2(u[used], uo[used]) < 1e-12
+    assert not torch.any(nk.fdm_local_solve(sm, torch.zeros_like(dev(r))))
+
+
+@pytest.mark.parametrize("kind", ["asm", "ras"])
+@pytest.mark.parametrize("counts,N,bc", CASES)
+def test_schwarz_smooth_matches_oracle(kind, counts, N, bc):
+    m, o, op, f = pair(counts, N, bc=bc)
+    sm = nk.SchwarzSmoother(op, kind)
+    r = assembled_random(o, 100 + N)
+    z = nk.schwarz_smooth(sm, dev(r)).cpu().numpy()
+    zo = osz.schwarz_smooth(f, kind, r, o.ids, o.mask)
+    assert rel_l2(z, zo) < 1e-12
+    if kind == "asm":
+        assert rel_l2(sm.W.cpu().numpy(), f.Wext) < 1e-15
+    # z is continuous: every copy of a shared point holds the same value
+    zz = ogs.gs_op(o.ids, z) / ogs.multiplicity(o.ids)
+    assert np.max(np.abs(zz - z)) <= 1e-14 * np.max(np.abs(z))
+
+
+def test_single_element_asm_equals_ras_and_affine_exact_inverse():
+    m, o, op, f = pair((1, 1, 1), 4, deformation=None)
+    r = assembled_random(o, 1)
+    za = nk.SchwarzSmoother(op, "asm")(dev(r))
+    zr = nk.SchwarzSmoother(op, "ras")(dev(r))
+    assert rel_l2(za.cpu().numpy(), zr.cpu().numpy()) < 1e-14
+    # the surrogate of an affine element with Dirichlet faces is the element:
+    # A z = r on the unmasked points
+    Az = op(za).cpu().numpy()
+    keep = o.mask.ravel() > 0
+    assert rel_l2(Az[keep], r[keep]) < 1e-11
+
+
+SMOOTHERS = ["jacobi", "cheby_jac", "asm", "ras", "cheby_asm", "cheby_ras"]
+
+
+@pytest.mark.parametrize("smoother", SMOOTHERS)
+def test_hierarchy_smoothers_match_oracle(smoother):
+    N, counts = 7, (2, 2, 2)
+    kw = dict(bc="dirichlet", deformation=("sine", 0.05))
+    m = nk.build_box_mesh((1, 1, 1), counts, N, **kw)
+    op = nk.PoissonOperator(m)
+    h = nk.MultigridHierarchy(op, smoother=smoother)
+    o = opmg.build_hierarchy((1, 1, 1), counts, N, smoother=smoother, **kw)
+    for lg, lo in zip(h.levels[:-1], o["levels"][:-1]):
+        assert abs(lg.lmax - lo.lmax) < 1e-9 * lo.lmax
+    lv = o["levels"][0]
+    r = lv.mask * ogs.gs_op(lv.mesh.ids, lv.wt * np.random.default_rng(7).standard_normal(
+        lv.mask.size))
+    z = nk.pmg_preconditioner(h, dev(r)).cpu().numpy()
+    assert rel_l2(z, opmg.vcycle(o, r)) < 1e-9
+    for level in (0, 1):
+        lo = o["levels"][level]
+        rl = lo.mask * ogs.gs_op(lo.mesh.ids, lo.wt * np.random.default_rng(level).standard_normal(
+            lo.mask.size))
+        e = nk.chebyshev_smooth(h, level, dev(rl)).cpu().numpy()
+        assert rel_l2(e, opmg.smooth(lo, rl, o["degree"])) < 1e-10
+
+
+@pytest.mark.parametrize("smoother", SMOOTHERS)
+def test_flexible_pcg_iterations_match_oracle(smoother):
+    N, counts = 7, (3, 3, 3)
+    kw = dict(bc="dirichlet", deformation=("sine", 0.05))
+    m = nk.build_box_mesh((1, 1, 1), counts, N, **kw)
+    op = nk.PoissonOperator(m)
+    h = nk.MultigridHierarchy(op, smoother=smoother)
+    o = opmg.build_hierarchy((1, 1, 1), counts, N, smoother=smoother, **kw)
+    lv = o["levels"][0]
+    X = lv.mesh.xyz.reshape(3, -1)
+    f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+    b = lv.mask * ogs.gs_op(lv.mesh.ids, lv.mesh.B.ravel() * f)
+    ro = osol.pcg(opmg.fine_operator(o), lambda r: opmg.vcycle(o, r), b, tol=1e-8,
+                  max_iter=200, flexible=True, weights=lv.wt)
+    res = nk.MultigridPCG(op, h, tol=1e-8, max_iter=200, flexible=True).solve(dev(b))
+    assert res.converged and ro.converged
+    assert abs(res.iterations - ro.iterations) <= 1
+    assert np.max(np.abs(res.x.cpu().numpy() - ro.x)) < 1e-7 * np.max(np.abs(ro.x))
+
+
+def test_contract_errors():
+    m = nk.build_box_mesh((1, 1, 1), (2, 2, 2), 3)
+    op = nk.PoissonOperator(m)
+    with pytest.raises(nk.ContractError):
+        nk.SchwarzSmoother(op, "bogus")
+    with pytest.raises(nk.ContractError):
+        nk.MultigridHierarchy(op, smoother="bogus")
+    sm = nk.SchwarzSmoother(op, "ras")
+    with pytest.raises(nk.ContractError):
+        sm(torch.zeros(5, dtype=torch.float64, device="cuda"))
