@@ -4,8 +4,8 @@
 // elements, FDM cost ~12E(N+3)^4, ASM with the counting weight, RAS).
 // oracle/schwarz.py states the algorithm on the CPU.
 //
-//   nk_fdm           one element per CTA, (N+3)^2 threads, each owning one
-//                    1-D line of the extended box in shared memory:
+//   nk_fdm           one element per CTA, (N+3)^2 / 2 threads, each owning
+//                    two 1-D lines of the extended box in shared memory:
 //                    gather r (- sub) on the element and the face-neighbour
 //                    layers -> S_x^T, S_y^T along lines -> (S_z^T, 1/Lambda,
 //                    S_z) fused in one pass -> S_y, S_x -> extended (ASM) or
@@ -19,102 +19,182 @@
 
 namespace nk {
 
-// One thread's 1-D contraction of its line L[0..NQE) (stride ST) in place:
-// forward (FWD): L[a] = sum_i S[i][a] L[i]   (S^T), optionally scaled by
-//                1 / (lam0 (lab + lz[a]) + lam1), 0 when that sum is +inf;
-// backward:      L[i] = sum_a S[i][a] L[a].
-// S is read from shared memory with every thread of the warp on the same
-// address (broadcast); only the line lives in registers.
-template <int NQE, int ST, bool FWD>
-__device__ __forceinline__ void fdm_line(double* L, const double* __restrict__ Sm,
-                                         const double* lz, double lab, double lam0,
-                                         double lam1) {
-  double v[NQE];
+// One thread's 1-D contractions of TWO lines L0, L1 (stride ST) in place:
+//   L[a] = sum_i M[a][i] L[i]   (M rows of length SP in shared memory),
+// optionally scaled by 1 / (lam0 (lab + lz[a]) + lam1) (0 when that sum is
+// +inf: dropped points).  M is S^T for the forward and S for the backward
+// transform.  Every M element loaded (16-B broadcast loads, all lanes on one
+// address) feeds two FMAs (one per line): 1 shared load per 4 DFMA.
+template <int NQE, int ST>
+__device__ __forceinline__ void fdm_line2(double* L0, double* L1, const double* __restrict__ M,
+                                          const double* lz, double lab0, double lab1,
+                                          double lam0, double lam1) {
+  constexpr int SP = (NQE + 1) & ~1;
+  double v0[NQE], v1[NQE];
 #pragma unroll
-  for (int i = 0; i < NQE; ++i) v[i] = L[i * ST];
+  for (int i = 0; i < NQE; ++i) {
+    v0[i] = L0[i * ST];
+    v1[i] = L1[i * ST];
+  }
 #pragma unroll 2
   for (int a = 0; a < NQE; ++a) {
-    double s = 0.0;
+    const double* row = M + a * SP;
+    double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-    for (int i = 0; i < NQE; ++i) s = fma(FWD ? Sm[i * NQE + a] : Sm[a * NQE + i], v[i], s);
-    if (lz != nullptr) {
-      const double lsum = lab + lz[a];
-      s = isinf(lsum) ? 0.0 : s / fma(lam0, lsum, lam1);
+    for (int i = 0; i + 1 < NQE; i += 2) {
+      const double2 m = *reinterpret_cast<const double2*>(row + i);
+      s0 = fma(m.x, v0[i], s0);
+      s1 = fma(m.x, v1[i], s1);
+      s0 = fma(m.y, v0[i + 1], s0);
+      s1 = fma(m.y, v1[i + 1], s1);
     }
-    L[a * ST] = s;
+    if (NQE & 1) {
+      const double m = row[NQE - 1];
+      s0 = fma(m, v0[NQE - 1], s0);
+      s1 = fma(m, v1[NQE - 1], s1);
+    }
+    if (lz != nullptr) {
+      const double l0 = lab0 + lz[a], l1 = lab1 + lz[a];
+      s0 = isinf(l0) ? 0.0 : s0 * __drcp_rn(fma(lam0, l0, lam1));
+      s1 = isinf(l1) ? 0.0 : s1 * __drcp_rn(fma(lam0, l1, lam1));
+    }
+    L0[a * ST] = s0;
+    L1[a * ST] = s1;
   }
 }
 
 template <int NQE>
-__global__ void __launch_bounds__(NQE * NQE)
+struct FdmShape {
+  static constexpr int NQ = NQE - 2;                 // N + 1
+  static constexpr int LS = NQE + 1;                 // padded line stride
+  static constexpr int PS = NQE * LS;                // plane stride
+  static constexpr int SP = (NQE + 1) & ~1;          // matrix row stride (16-B rows)
+  static constexpr int NL = NQE * NQE;               // lines per orientation
+  static constexpr int NT = (NL + 1) / 2;            // threads: two lines each
+  static constexpr int A_SZ = NQE * PS;
+  static constexpr int M_SZ = 3 * NQE * SP;          // one of S^T / S, 3 directions
+  static constexpr size_t SMEM = sizeof(double) * (A_SZ + 2 * M_SZ + 3 * NQE);
+};
+
+// One element per CTA, (N+3)^2 / 2 threads, two 1-D lines per thread and
+// orientation, transposes through one padded shared box.
+template <int NQE>
+__global__ void __launch_bounds__(FdmShape<NQE>::NT)
 fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict__ sub,
            double* __restrict__ res_out, const int32_t* __restrict__ fmap,
            const double* __restrict__ Sg, const double* __restrict__ lamg, double lam0,
            double lam1, double* __restrict__ out, int out_ext, const nk_cg_state* st) {
   if (st != nullptr && st->done) return;
-  constexpr int NQ = NQE - 2;            // N + 1
+  using F = FdmShape<NQE>;
+  constexpr int NQ = F::NQ;
   constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
-  constexpr int LS = NQE + 1;            // padded line stride
-  constexpr int PS = NQE * LS;           // plane stride
-  constexpr int NT = NQE * NQE;
+  constexpr int LS = F::LS, PS = F::PS, SP = F::SP, NT = F::NT, NL = F::NL;
   extern __shared__ __align__(16) double fdm_smem[];
   double* A = fdm_smem;                  // [k][j][i], padded lines
-  double* Ss = A + NQE * PS;             // Ss[d][p][mode]
-  double* Ls = Ss + 3 * NQE * NQE;       // lambda[d][mode]
+  double* Sf = A + F::A_SZ;              // Sf[d][a][i] = S[d][i][a]  (forward)
+  double* Sb = Sf + F::M_SZ;             // Sb[d][i][a] = S[d][i][a]  (backward)
+  double* Ls = Sb + F::M_SZ;             // lambda[d][mode]
   const int64_t e = blockIdx.x;
   const int t = threadIdx.x;
   const double* Se = Sg + e * 3 * NQE * NQE;
-  for (int q = t; q < 3 * NQE * NQE; q += NT) Ss[q] = __ldg(Se + q);
-  if (t < 3 * NQE) Ls[t] = __ldg(lamg + e * 3 * NQE + t);
-  // own points (coalesced) + zero elsewhere
   const int64_t ob = e * NQ3;
+  const int32_t* fm = fmap + e * 6 * NQ2;
+  // Global loads are issued in batches of CH independent loads per thread
+  // (the gather is latency-bound: one element per CTA, few warps per SM).
+  constexpr int CH = 8;
+  constexpr int NS = 3 * NQE * NQE, NF = 6 * NQ2;
+  for (int q0 = 0; q0 < NS; q0 += CH * NT) {
+    double v[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      v[u] = q < NS ? __ldg(Se + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      if (q < NS) {
+        const int d = q / (NQE * NQE), ia = q % (NQE * NQE), i = ia / NQE, a = ia % NQE;
+        Sb[d * NQE * SP + i * SP + a] = v[u];
+        Sf[d * NQE * SP + a * SP + i] = v[u];
+      }
+    }
+  }
+  for (int q = t; q < 3 * NQE; q += NT) Ls[q] = __ldg(lamg + e * 3 * NQE + q);
   for (int q = t; q < NQE * NQE * NQE; q += NT) {
     const int i = q % NQE, j = (q / NQE) % NQE, k = q / (NQE * NQE);
     A[k * PS + j * LS + i] = 0.0;
   }
   __syncthreads();
-  for (int q = t; q < NQ3; q += NT) {
-    const int i = q % NQ, j = (q / NQ) % NQ, k = q / NQ2;
-    double v = __ldg(r + ob + q);
-    if (sub) v -= __ldg(sub + ob + q);
-    if (res_out) res_out[ob + q] = v;
-    A[(k + 1) * PS + (j + 1) * LS + (i + 1)] = v;
+  // own points (coalesced); res_out = r - sub on them
+  for (int q0 = 0; q0 < NQ3; q0 += CH * NT) {
+    double v[CH], w[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      v[u] = q < NQ3 ? __ldg(r + ob + q) : 0.0;
+      w[u] = (sub != nullptr && q < NQ3) ? __ldg(sub + ob + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      if (q < NQ3) {
+        const int i = q % NQ, j = (q / NQ) % NQ, k = q / NQ2;
+        const double x = v[u] - w[u];
+        if (res_out) res_out[ob + q] = x;
+        A[(k + 1) * PS + (j + 1) * LS + (i + 1)] = x;
+      }
+    }
   }
   // face-neighbour layers: face f, tangential (a, b) slow/fast
-  const int32_t* fm = fmap + e * 6 * NQ2;
-  for (int q = t; q < 6 * NQ2; q += NT) {
-    const int32_t src = __ldg(fm + q);
-    if (src < 0) continue;
-    const int f = q / NQ2, ab = q % NQ2, a = ab / NQ + 1, b = ab % NQ + 1;
-    const int pos = (f & 1) ? NQE - 1 : 0;
-    double v = __ldg(r + src);
-    if (sub) v -= __ldg(sub + src);
-    int idx;
-    if (f < 2) idx = a * PS + b * LS + pos;        // x faces: (k, j)
-    else if (f < 4) idx = a * PS + pos * LS + b;   // y faces: (k, i)
-    else idx = pos * PS + a * LS + b;              // z faces: (j, i)
-    A[idx] = v;
+  for (int q0 = 0; q0 < NF; q0 += CH * NT) {
+    int32_t src[CH];
+    double v[CH], w[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      src[u] = q < NF ? __ldg(fm + q) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      v[u] = src[u] >= 0 ? __ldg(r + src[u]) : 0.0;
+      w[u] = (sub != nullptr && src[u] >= 0) ? __ldg(sub + src[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      if (src[u] >= 0) {
+        const int f = q / NQ2, ab = q % NQ2, a = ab / NQ + 1, b = ab % NQ + 1;
+        const int pos = (f & 1) ? NQE - 1 : 0;
+        int idx;
+        if (f < 2) idx = a * PS + b * LS + pos;        // x faces: (k, j)
+        else if (f < 4) idx = a * PS + pos * LS + b;   // y faces: (k, i)
+        else idx = pos * PS + a * LS + b;              // z faces: (j, i)
+        A[idx] = v[u] - w[u];
+      }
+    }
   }
   __syncthreads();
-  const double* Sx = Ss;
-  const double* Sy = Ss + NQE * NQE;
-  const double* Sz = Ss + 2 * NQE * NQE;
-  const int t1 = t / NQE, t0 = t % NQE;
-  // forward x: line (k = t1, j = t0) along i
-  fdm_line<NQE, 1, true>(A + t1 * PS + t0 * LS, Sx, nullptr, 0.0, 0.0, 0.0);
+  // this thread's two lines (the second clamped onto the first when NL is odd)
+  const int l0 = t, l1 = (t + NT < NL) ? t + NT : t;
+  const int h0 = l0 / NQE, o0 = l0 % NQE, h1 = l1 / NQE, o1 = l1 % NQE;
+  constexpr int MD = NQE * SP;
+  // forward x: lines (k = h, j = o) along i
+  fdm_line2<NQE, 1>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sf, nullptr, 0, 0, 0, 0);
   __syncthreads();
-  // forward y: line (k = t1, i = t0) along j
-  fdm_line<NQE, LS, true>(A + t1 * PS + t0, Sy, nullptr, 0.0, 0.0, 0.0);
+  // forward y: lines (k = h, i = o) along j
+  fdm_line2<NQE, LS>(A + h0 * PS + o0, A + h1 * PS + o1, Sf + MD, nullptr, 0, 0, 0, 0);
   __syncthreads();
-  // z: forward + inverse Kronecker-sum spectrum, then backward, on one line
-  // (j = t1 -> mode b, i = t0 -> mode a); dropped points have lambda = +inf
-  fdm_line<NQE, PS, true>(A + t1 * LS + t0, Sz, Ls + 2 * NQE, Ls[t0] + Ls[NQE + t1], lam0, lam1);
-  fdm_line<NQE, PS, false>(A + t1 * LS + t0, Sz, nullptr, 0.0, 0.0, 0.0);
+  // z: forward + inverse Kronecker-sum spectrum, then backward
+  // (lines j = h -> mode b, i = o -> mode a, along k)
+  fdm_line2<NQE, PS>(A + h0 * LS + o0, A + h1 * LS + o1, Sf + 2 * MD, Ls + 2 * NQE,
+                     Ls[o0] + Ls[NQE + h0], Ls[o1] + Ls[NQE + h1], lam0, lam1);
+  fdm_line2<NQE, PS>(A + h0 * LS + o0, A + h1 * LS + o1, Sb + 2 * MD, nullptr, 0, 0, 0, 0);
   __syncthreads();
   // backward y, backward x
-  fdm_line<NQE, LS, false>(A + t1 * PS + t0, Sy, nullptr, 0.0, 0.0, 0.0);
+  fdm_line2<NQE, LS>(A + h0 * PS + o0, A + h1 * PS + o1, Sb + MD, nullptr, 0, 0, 0, 0);
   __syncthreads();
-  fdm_line<NQE, 1, false>(A + t1 * PS + t0 * LS, Sx, nullptr, 0.0, 0.0, 0.0);
+  fdm_line2<NQE, 1>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sb, nullptr, 0, 0, 0, 0);
   __syncthreads();
   if (out_ext) {
     double* o = out + e * NQE * NQE * NQE;
@@ -164,7 +244,7 @@ static int launch_fdm(int64_t E, const double* r, const double* sub, double* res
                       const int32_t* fmap, const double* S, const double* lam, double lam0,
                       double lam1, double* out, int out_ext, const nk_cg_state* st,
                       cudaStream_t s) {
-  constexpr size_t smem = sizeof(double) * (NQE * NQE * (NQE + 1) + 3 * NQE * NQE + 3 * NQE);
+  constexpr size_t smem = FdmShape<NQE>::SMEM;
   static bool configured = false;
   if (!configured) {
     cudaError_t err = cudaFuncSetAttribute(fdm_kernel<NQE>,
@@ -175,7 +255,7 @@ static int launch_fdm(int64_t E, const double* r, const double* sub, double* res
     }
     configured = true;
   }
-  fdm_kernel<NQE><<<(unsigned)E, NQE * NQE, smem, s>>>(E, r, sub, res_out, fmap, S, lam, lam0,
+  fdm_kernel<NQE><<<(unsigned)E, FdmShape<NQE>::NT, smem, s>>>(E, r, sub, res_out, fmap, S, lam, lam0,
                                                       lam1, out, out_ext, st);
   return check_launch("fdm");
 }

@@ -200,10 +200,12 @@ def mesh_coordinates(m):
     callable_def = callable(m.deformation)
     kind, amp = (0, 0.0) if callable_def else _deform_spec(m.deformation)
     xyz = torch.empty((3, m.E, nq, nq, nq), dtype=torch.float64, device=m.device)
-    check(lib().nk_box_coords(N, m.E, ptr(eidx), ptr(np.array(m.counts, dtype=np.int32)),
-                              ptr(np.array(m.extent, dtype=np.float64)),
-                              ptr(np.array(m.origin, dtype=np.float64)), kind, amp, ptr(nodes),
-                              ptr(xyz), stream_ptr()), "box_coords")
+    # host arrays bound to names: they must outlive the call
+    c32 = np.array(m.counts, dtype=np.int32)
+    ext = np.array(m.extent, dtype=np.float64)
+    org = np.array(m.origin, dtype=np.float64)
+    check(lib().nk_box_coords(N, m.E, ptr(eidx), ptr(c32), ptr(ext), ptr(org), kind, amp,
+                              ptr(nodes), ptr(xyz), stream_ptr()), "box_coords")
     if callable_def:
         h = xyz.cpu().numpy()
         x, y, z = m.deformation(h[0], h[1], h[2])

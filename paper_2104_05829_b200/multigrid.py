@@ -104,10 +104,10 @@ def _level_mesh(fine, n):
         raise ContractError("p-multigrid needs a box mesh or a mesh built with coordinates")
     import torch
     fb, cb = fine.basis, SpectralBasis.get(n)
-    M = lagrange_interp_matrix(fb.nodes, cb.nodes)          # (n+1, N+1)
+    M = np.ascontiguousarray(lagrange_interp_matrix(fb.nodes, cb.nodes))   # (n+1, N+1)
     xyz = torch.empty((3, fine.E, n + 1, n + 1, n + 1), dtype=torch.float64, device=fine.device)
     for c in range(3):
-        check(lib().nk_interp3(fine.nq, n + 1, fine.E, ptr(np.ascontiguousarray(M)),
+        check(lib().nk_interp3(fine.nq, n + 1, fine.E, ptr(M),
                                ptr(fine.xyz[c].contiguous()), None, None, None, ptr(xyz[c]), 0,
                                None, stream_ptr()), "interp3")
     near = np.argmin(np.abs(cb.nodes[:, None] - fb.nodes[None, :]), axis=1)
