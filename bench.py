@@ -17,6 +17,8 @@ e2e    : same metric through the public API (apply_stiffness_local) with
 roofline: algorithmic 64 B per local point (u 8 + G 48 + w 8) / kernel time
          vs MEASURED_PEAKS.json hbm_gbs.
 bp5    : fused Jacobi-PCG (Dirichlet box, same mesh) iterations x DOF / time.
+bp5_time_to_solution: wall time to tol 1e-8 on the same mesh for Jacobi-PCG
+         and the p-multigrid preconditioners (cheby_jac, ras, asm smoothers).
 --impl reference: the reference has no CPU Ax, so the
          reference arm times the CPU oracle port (numpy BK5, all host threads)
          on a bounded sample of the same workload.
@@ -431,6 +433,45 @@ def run_ours(args):
                "dot_allreduce": ("ipc-board" if getattr(comm, "board", None) is not None
                                  else "torch.distributed") if ws > 1 else None}
 
+    # ---- Time to solution at tol 1e-8 (N = 1 only, same mesh, random
+    # assembled rhs): Jacobi-PCG vs the p-multigrid preconditioners
+    # -- wall time of solve() after a warm solve, synchronised.
+    solvers = None
+    if ws == 1 and not args.no_bp5 and not args.no_solvers:
+        import time as _time
+        op = nk.PoissonOperator(mesh)
+        b_rhs = torch.as_tensor(rng.standard_normal(mesh.n_local), device="cuda")
+        nk.gs_op(op.gs, b_rhs)
+        b_rhs *= mesh.mask.reshape(-1).to(torch.float64)
+        solvers = {"tol": 1e-8, "rhs": "random, assembled, masked", "E": E, "N": N}
+        cases = [("jacobi_pcg", lambda: nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-8,
+                                                     max_iter=5000, chunk=32))]
+        for kind in ("cheby_jac", "ras", "asm"):
+            cases.append((f"pmg_{kind}", lambda kind=kind: nk.MultigridPCG(
+                op, nk.MultigridHierarchy(op, smoother=kind), tol=1e-8, max_iter=500,
+                flexible=kind not in ("jacobi", "cheby_jac"))))
+        for name, make in cases:
+            t0 = _time.perf_counter()
+            sv = make()
+            torch.cuda.synchronize()
+            setup_s = _time.perf_counter() - t0
+            sv.solve(b_rhs)
+            best, res = None, None
+            for _ in range(3):
+                torch.cuda.synchronize()
+                t0 = _time.perf_counter()
+                res = sv.solve(b_rhs)
+                torch.cuda.synchronize()
+                t = _time.perf_counter() - t0
+                best = t if best is None else min(best, t)
+            solvers[name] = {"iterations": res.iterations, "solve_ms": round(best * 1e3, 3),
+                             "ms_per_iteration": round(best * 1e3 / max(res.iterations, 1), 4),
+                             "setup_s": round(setup_s, 3), "converged": bool(res.converged)}
+            del sv
+        base = solvers["jacobi_pcg"]["solve_ms"]
+        for name, _ in cases[1:]:
+            solvers[name]["speedup_vs_jacobi_pcg"] = round(base / solvers[name]["solve_ms"], 2)
+
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if ws == 1 and not args.no_cpu:
@@ -466,6 +507,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline_context": ceiling,
             "bp5": bp5,
+            "bp5_time_to_solution": solvers,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "wall_s_timed_region": round(t_wall, 4),
@@ -486,6 +528,7 @@ def main():
     ap.add_argument("--no-bp5", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ceiling", action="store_true")
+    ap.add_argument("--no-solvers", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
