@@ -364,6 +364,13 @@ int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, double* res
            const int32_t* fmap, const double* S, const double* lam, double lam0, double lam1,
            double* out, int out_ext, const nk_cg_state* st, nk_stream_t stream);
 
+/* nk_fdm with the local solves in FP32 (the paper's 32-bit smoothing,
+ * PAPER.md:323-325): r, sub, res_out, out stay FP64; S and lam are FP32
+ * copies ([E][3][N+3][N+3], [E][3][N+3]). */
+int nk_fdm32(int N, int64_t nelem, const double* r, const double* sub, double* res_out,
+             const int32_t* fmap, const float* S, const float* lam, double lam0, double lam1,
+             double* out, int out_ext, const nk_cg_state* st, nk_stream_t stream);
+
 /* z = mask * W * src (own points; src extended [E][(N+3)^3] if src_ext) fused
  * with d = a d + b z (d nullable: d := b z not stored) and e = (e_acc ? e : 0)
  * + d.  W, mask nullable. */

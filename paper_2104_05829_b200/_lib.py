@@ -96,6 +96,7 @@ _SIGS = {
     "nk_multi_axpy": ([_I64, _I32, _P, _D, _P, _I64, _P, _P, _P], _I32),
     "nk_vscale": ([_I64, _P, _P, _P, _P], _I32),
     "nk_fdm": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
+    "nk_fdm32": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
     "nk_schwarz_post": ([_I32, _I64, _P, _I32, _P, _P, _P, _P, _D, _D, _I32, _P, _P], _I32),
 }
 

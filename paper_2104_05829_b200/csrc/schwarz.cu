@@ -25,12 +25,18 @@ namespace nk {
 // +inf: dropped points).  M is S^T for the forward and S for the backward
 // transform.  Every M element loaded (16-B broadcast loads, all lanes on one
 // address) feeds two FMAs (one per line): 1 shared load per 4 DFMA.
-template <int NQE, int ST>
-__device__ __forceinline__ void fdm_line2(double* L0, double* L1, const double* __restrict__ M,
-                                          const double* lz, double lab0, double lab1,
-                                          double lam0, double lam1) {
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+__device__ __forceinline__ double fdm_rcp(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ float fdm_rcp(float x) { return __frcp_rn(x); }
+
+template <int NQE, int ST, typename T>
+__device__ __forceinline__ void fdm_line2(T* L0, T* L1, const T* __restrict__ M, const T* lz,
+                                          T lab0, T lab1, T lam0, T lam1) {
+  using V2 = typename Vec2<T>::type;
   constexpr int SP = (NQE + 1) & ~1;
-  double v0[NQE], v1[NQE];
+  T v0[NQE], v1[NQE];
 #pragma unroll
   for (int i = 0; i < NQE; ++i) {
     v0[i] = L0[i * ST];
@@ -38,32 +44,32 @@ __device__ __forceinline__ void fdm_line2(double* L0, double* L1, const double* 
   }
 #pragma unroll 2
   for (int a = 0; a < NQE; ++a) {
-    const double* row = M + a * SP;
-    double s0 = 0.0, s1 = 0.0;
+    const T* row = M + a * SP;
+    T s0 = 0, s1 = 0;
 #pragma unroll
     for (int i = 0; i + 1 < NQE; i += 2) {
-      const double2 m = *reinterpret_cast<const double2*>(row + i);
+      const V2 m = *reinterpret_cast<const V2*>(row + i);
       s0 = fma(m.x, v0[i], s0);
       s1 = fma(m.x, v1[i], s1);
       s0 = fma(m.y, v0[i + 1], s0);
       s1 = fma(m.y, v1[i + 1], s1);
     }
     if (NQE & 1) {
-      const double m = row[NQE - 1];
+      const T m = row[NQE - 1];
       s0 = fma(m, v0[NQE - 1], s0);
       s1 = fma(m, v1[NQE - 1], s1);
     }
     if (lz != nullptr) {
-      const double l0 = lab0 + lz[a], l1 = lab1 + lz[a];
-      s0 = isinf(l0) ? 0.0 : s0 * __drcp_rn(fma(lam0, l0, lam1));
-      s1 = isinf(l1) ? 0.0 : s1 * __drcp_rn(fma(lam0, l1, lam1));
+      const T l0 = lab0 + lz[a], l1 = lab1 + lz[a];
+      s0 = isinf(l0) ? T(0) : s0 * fdm_rcp(fma(lam0, l0, lam1));
+      s1 = isinf(l1) ? T(0) : s1 * fdm_rcp(fma(lam0, l1, lam1));
     }
     L0[a * ST] = s0;
     L1[a * ST] = s1;
   }
 }
 
-template <int NQE>
+template <int NQE, typename T>
 struct FdmShape {
   static constexpr int NQ = NQE - 2;                 // N + 1
   static constexpr int LS = NQE + 1;                 // padded line stride
@@ -73,30 +79,34 @@ struct FdmShape {
   static constexpr int NT = (NL + 1) / 2;            // threads: two lines each
   static constexpr int A_SZ = NQE * PS;
   static constexpr int M_SZ = 3 * NQE * SP;          // one of S^T / S, 3 directions
-  static constexpr size_t SMEM = sizeof(double) * (A_SZ + 2 * M_SZ + 3 * NQE);
+  static constexpr size_t SMEM = sizeof(T) * (A_SZ + 2 * M_SZ + 3 * NQE);
 };
 
 // One element per CTA, (N+3)^2 / 2 threads, two 1-D lines per thread and
 // orientation, transposes through one padded shared box.
-template <int NQE>
-__global__ void __launch_bounds__(FdmShape<NQE>::NT)
+// T = double, or float for the 32-bit smoothing mode ("FP32
+// is used only for the smoothing steps"): fields stay FP64 in HBM, the
+// extended box, S and the spectrum are T in shared memory.
+template <int NQE, typename T>
+__global__ void __launch_bounds__(FdmShape<NQE, T>::NT)
 fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict__ sub,
            double* __restrict__ res_out, const int32_t* __restrict__ fmap,
-           const double* __restrict__ Sg, const double* __restrict__ lamg, double lam0,
-           double lam1, double* __restrict__ out, int out_ext, const nk_cg_state* st) {
+           const T* __restrict__ Sg, const T* __restrict__ lamg, double lam0_d,
+           double lam1_d, double* __restrict__ out, int out_ext, const nk_cg_state* st) {
   if (st != nullptr && st->done) return;
-  using F = FdmShape<NQE>;
+  using F = FdmShape<NQE, T>;
+  const T lam0 = (T)lam0_d, lam1 = (T)lam1_d;
   constexpr int NQ = F::NQ;
   constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
   constexpr int LS = F::LS, PS = F::PS, SP = F::SP, NT = F::NT, NL = F::NL;
-  extern __shared__ __align__(16) double fdm_smem[];
-  double* A = fdm_smem;                  // [k][j][i], padded lines
-  double* Sf = A + F::A_SZ;              // Sf[d][a][i] = S[d][i][a]  (forward)
-  double* Sb = Sf + F::M_SZ;             // Sb[d][i][a] = S[d][i][a]  (backward)
-  double* Ls = Sb + F::M_SZ;             // lambda[d][mode]
+  extern __shared__ __align__(16) unsigned char fdm_smem_raw[];
+  T* A = reinterpret_cast<T*>(fdm_smem_raw);   // [k][j][i], padded lines
+  T* Sf = A + F::A_SZ;                   // Sf[d][a][i] = S[d][i][a]  (forward)
+  T* Sb = Sf + F::M_SZ;                  // Sb[d][i][a] = S[d][i][a]  (backward)
+  T* Ls = Sb + F::M_SZ;                  // lambda[d][mode]
   const int64_t e = blockIdx.x;
   const int t = threadIdx.x;
-  const double* Se = Sg + e * 3 * NQE * NQE;
+  const T* Se = Sg + e * 3 * NQE * NQE;
   const int64_t ob = e * NQ3;
   const int32_t* fm = fmap + e * 6 * NQ2;
   // Global loads are issued in batches of CH independent loads per thread
@@ -104,11 +114,11 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
   constexpr int CH = 8;
   constexpr int NS = 3 * NQE * NQE, NF = 6 * NQ2;
   for (int q0 = 0; q0 < NS; q0 += CH * NT) {
-    double v[CH];
+    T v[CH];
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
       const int q = q0 + u * NT + t;
-      v[u] = q < NS ? __ldg(Se + q) : 0.0;
+      v[u] = q < NS ? __ldg(Se + q) : T(0);
     }
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
@@ -123,7 +133,7 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
   for (int q = t; q < 3 * NQE; q += NT) Ls[q] = __ldg(lamg + e * 3 * NQE + q);
   for (int q = t; q < NQE * NQE * NQE; q += NT) {
     const int i = q % NQE, j = (q / NQE) % NQE, k = q / (NQE * NQE);
-    A[k * PS + j * LS + i] = 0.0;
+    A[k * PS + j * LS + i] = T(0);
   }
   __syncthreads();
   // own points (coalesced); res_out = r - sub on them
@@ -142,7 +152,7 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
         const int i = q % NQ, j = (q / NQ) % NQ, k = q / NQ2;
         const double x = v[u] - w[u];
         if (res_out) res_out[ob + q] = x;
-        A[(k + 1) * PS + (j + 1) * LS + (i + 1)] = x;
+        A[(k + 1) * PS + (j + 1) * LS + (i + 1)] = (T)x;
       }
     }
   }
@@ -170,7 +180,7 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
         if (f < 2) idx = a * PS + b * LS + pos;        // x faces: (k, j)
         else if (f < 4) idx = a * PS + pos * LS + b;   // y faces: (k, i)
         else idx = pos * PS + a * LS + b;              // z faces: (j, i)
-        A[idx] = v[u] - w[u];
+        A[idx] = (T)(v[u] - w[u]);
       }
     }
   }
@@ -180,32 +190,32 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
   const int h0 = l0 / NQE, o0 = l0 % NQE, h1 = l1 / NQE, o1 = l1 % NQE;
   constexpr int MD = NQE * SP;
   // forward x: lines (k = h, j = o) along i
-  fdm_line2<NQE, 1>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sf, nullptr, 0, 0, 0, 0);
+  fdm_line2<NQE, 1, T>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sf, nullptr, 0, 0, 0, 0);
   __syncthreads();
   // forward y: lines (k = h, i = o) along j
-  fdm_line2<NQE, LS>(A + h0 * PS + o0, A + h1 * PS + o1, Sf + MD, nullptr, 0, 0, 0, 0);
+  fdm_line2<NQE, LS, T>(A + h0 * PS + o0, A + h1 * PS + o1, Sf + MD, nullptr, 0, 0, 0, 0);
   __syncthreads();
   // z: forward + inverse Kronecker-sum spectrum, then backward
   // (lines j = h -> mode b, i = o -> mode a, along k)
-  fdm_line2<NQE, PS>(A + h0 * LS + o0, A + h1 * LS + o1, Sf + 2 * MD, Ls + 2 * NQE,
+  fdm_line2<NQE, PS, T>(A + h0 * LS + o0, A + h1 * LS + o1, Sf + 2 * MD, Ls + 2 * NQE,
                      Ls[o0] + Ls[NQE + h0], Ls[o1] + Ls[NQE + h1], lam0, lam1);
-  fdm_line2<NQE, PS>(A + h0 * LS + o0, A + h1 * LS + o1, Sb + 2 * MD, nullptr, 0, 0, 0, 0);
+  fdm_line2<NQE, PS, T>(A + h0 * LS + o0, A + h1 * LS + o1, Sb + 2 * MD, nullptr, 0, 0, 0, 0);
   __syncthreads();
   // backward y, backward x
-  fdm_line2<NQE, LS>(A + h0 * PS + o0, A + h1 * PS + o1, Sb + MD, nullptr, 0, 0, 0, 0);
+  fdm_line2<NQE, LS, T>(A + h0 * PS + o0, A + h1 * PS + o1, Sb + MD, nullptr, 0, 0, 0, 0);
   __syncthreads();
-  fdm_line2<NQE, 1>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sb, nullptr, 0, 0, 0, 0);
+  fdm_line2<NQE, 1, T>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sb, nullptr, 0, 0, 0, 0);
   __syncthreads();
   if (out_ext) {
     double* o = out + e * NQE * NQE * NQE;
     for (int q = t; q < NQE * NQE * NQE; q += NT) {
       const int i = q % NQE, j = (q / NQE) % NQE, k = q / (NQE * NQE);
-      o[q] = A[k * PS + j * LS + i];
+      o[q] = (double)A[k * PS + j * LS + i];
     }
   } else {
     for (int q = t; q < NQ3; q += NT) {
       const int i = q % NQ, j = (q / NQ) % NQ, k = q / NQ2;
-      out[ob + q] = A[(k + 1) * PS + (j + 1) * LS + (i + 1)];
+      out[ob + q] = (double)A[(k + 1) * PS + (j + 1) * LS + (i + 1)];
     }
   }
 }
@@ -239,15 +249,15 @@ schwarz_post_kernel(int nq, int64_t n, const double* __restrict__ src, int src_e
   }
 }
 
-template <int NQE>
+template <int NQE, typename T>
 static int launch_fdm(int64_t E, const double* r, const double* sub, double* res_out,
-                      const int32_t* fmap, const double* S, const double* lam, double lam0,
+                      const int32_t* fmap, const T* S, const T* lam, double lam0,
                       double lam1, double* out, int out_ext, const nk_cg_state* st,
                       cudaStream_t s) {
-  constexpr size_t smem = FdmShape<NQE>::SMEM;
+  constexpr size_t smem = FdmShape<NQE, T>::SMEM;
   static bool configured = false;
   if (!configured) {
-    cudaError_t err = cudaFuncSetAttribute(fdm_kernel<NQE>,
+    cudaError_t err = cudaFuncSetAttribute(fdm_kernel<NQE, T>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) {
       set_error("fdm: smem attribute: %s", cudaGetErrorString(err));
@@ -255,19 +265,17 @@ static int launch_fdm(int64_t E, const double* r, const double* sub, double* res
     }
     configured = true;
   }
-  fdm_kernel<NQE><<<(unsigned)E, FdmShape<NQE>::NT, smem, s>>>(E, r, sub, res_out, fmap, S, lam, lam0,
-                                                      lam1, out, out_ext, st);
+  fdm_kernel<NQE, T><<<(unsigned)E, FdmShape<NQE, T>::NT, smem, s>>>(E, r, sub, res_out, fmap, S,
+                                                                    lam, lam0, lam1, out, out_ext,
+                                                                    st);
   return check_launch("fdm");
 }
 
-}  // namespace nk
-
-using namespace nk;
-
-extern "C" int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, double* res_out,
-                      const int32_t* fmap, const double* Smat, const double* lam, double lam0,
-                      double lam1, double* out, int out_ext, const nk_cg_state* st,
-                      nk_stream_t stream) {
+template <typename T>
+static int fdm_dispatch(int N, int64_t nelem, const double* r, const double* sub,
+                        double* res_out, const int32_t* fmap, const T* Smat, const T* lam,
+                        double lam0, double lam1, double* out, int out_ext,
+                        const nk_cg_state* st, nk_stream_t stream) {
   if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) {
     set_error("fdm: order %d outside [%d, %d]", N, NK_MIN_ORDER, NK_MAX_ORDER);
     return NK_ERR_UNSUPPORTED;
@@ -282,7 +290,7 @@ extern "C" int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, 
   switch (N + 3) {
 #define NK_FDM_CASE(Q) \
   case Q:              \
-    return launch_fdm<Q>(nelem, r, sub, res_out, fmap, Smat, lam, lam0, lam1, out, out_ext, st, s);
+    return launch_fdm<Q, T>(nelem, r, sub, res_out, fmap, Smat, lam, lam0, lam1, out, out_ext, st, s);
     NK_FDM_CASE(4) NK_FDM_CASE(5) NK_FDM_CASE(6) NK_FDM_CASE(7) NK_FDM_CASE(8) NK_FDM_CASE(9)
     NK_FDM_CASE(10) NK_FDM_CASE(11) NK_FDM_CASE(12) NK_FDM_CASE(13) NK_FDM_CASE(14)
     NK_FDM_CASE(15) NK_FDM_CASE(16) NK_FDM_CASE(17) NK_FDM_CASE(18)
@@ -291,6 +299,26 @@ extern "C" int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, 
   }
   set_error("fdm: order %d not instantiated", N);
   return NK_ERR_UNSUPPORTED;
+}
+
+}  // namespace nk
+
+using namespace nk;
+
+extern "C" int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, double* res_out,
+                      const int32_t* fmap, const double* Smat, const double* lam, double lam0,
+                      double lam1, double* out, int out_ext, const nk_cg_state* st,
+                      nk_stream_t stream) {
+  return fdm_dispatch<double>(N, nelem, r, sub, res_out, fmap, Smat, lam, lam0, lam1, out,
+                              out_ext, st, stream);
+}
+
+extern "C" int nk_fdm32(int N, int64_t nelem, const double* r, const double* sub,
+                        double* res_out, const int32_t* fmap, const float* Smat,
+                        const float* lam, double lam0, double lam1, double* out, int out_ext,
+                        const nk_cg_state* st, nk_stream_t stream) {
+  return fdm_dispatch<float>(N, nelem, r, sub, res_out, fmap, Smat, lam, lam0, lam1, out,
+                             out_ext, st, stream);
 }
 
 extern "C" int nk_schwarz_post(int N, int64_t nelem, const double* src, int src_ext,

@@ -131,17 +131,25 @@ class MultigridHierarchy:
     Calling the hierarchy applies one V-cycle (pmg_preconditioner).
 
     coarse: 'dense' (explicit inverse of the assembled, masked order-1
-    operator; exact) -- the only coarse solver built; setup raises when the
-    coarse problem exceeds DENSE_COARSE_MAX unique dofs."""
+    operator; exact; at most DENSE_COARSE_MAX unique dofs), 'pcg' (fused
+    Jacobi-PCG on the order-1 level to coarse_tol relative residual, at most
+    coarse_iters iterations -- a nonlinear preconditioner: use flexible PCG),
+    or 'auto' (dense when it fits, else pcg).  The paper uses AMG (Hypre /
+    parAlmond) here; the iterative coarse solve is the
+    scalable stand-in built on the same fused PCG kernels."""
 
     def __init__(self, op, degree=2, bounds=(0.1, 1.1), power_iters=20, seed=2104,
-                 coarse="dense", smoother="cheby_jac"):
+                 coarse="auto", smoother="cheby_jac", smoother_precision=64, coarse_tol=1e-3,
+                 coarse_iters=100):
         import torch
         from .solvers import JacobiPreconditioner, PoissonOperator
         if op.ncomp != 1:
             raise ContractError("p-multigrid preconditions scalar operators")
-        if coarse != "dense":
-            raise ContractError(f"unknown coarse solver {coarse!r} (built: 'dense')")
+        if coarse not in ("dense", "pcg", "auto"):
+            raise ContractError(f"unknown coarse solver {coarse!r} (built: 'dense', 'pcg', "
+                                f"'auto')")
+        self.coarse_kind = coarse
+        self.coarse_tol, self.coarse_iters = float(coarse_tol), int(coarse_iters)
         if op.comm is not None and op.comm.size > 1:
             raise ContractError("multi-rank p-multigrid is not built (coarse solve is "
                                 "single-rank); use Jacobi-PCG across ranks")
@@ -153,6 +161,11 @@ class MultigridHierarchy:
         if smoother not in SMOOTHERS:
             raise ContractError(f"unknown smoother {smoother!r} (built: {SMOOTHERS})")
         self.smoother = smoother
+        if smoother_precision not in (32, 64):
+            raise ContractError(f"smoother_precision must be 32 or 64, got {smoother_precision!r}")
+        if smoother_precision == 32 and smoother not in _SCHWARZ:
+            raise ContractError("32-bit smoothing is built for the Schwarz (FDM) smoothers")
+        self.smoother_precision = int(smoother_precision)
         self.bounds = (float(bounds[0]), float(bounds[1]))
         self.orders = pmg_orders(op.mesh.N)
         dev = op.mesh.device
@@ -178,7 +191,7 @@ class MultigridHierarchy:
         from .schwarz import SchwarzSmoother
         for lv in self.levels[:-1]:
             if smoother in _SCHWARZ:
-                lv.sm = SchwarzSmoother(lv.op, _SCHWARZ[smoother])
+                lv.sm = SchwarzSmoother(lv.op, _SCHWARZ[smoother], precision=smoother_precision)
                 lv.res2 = torch.zeros_like(lv.res)
             lv.deg = 1 if smoother in ("jacobi", "asm", "ras") else self.degree
         for lv in self.levels[:-1]:
@@ -235,9 +248,14 @@ class MultigridHierarchy:
         keep_u = torch.zeros(uniq.numel(), dtype=torch.bool, device=dev)
         keep_u[inv[mask]] = True
         nu = int(keep_u.sum())
+        lv.nu = nu
+        if self.coarse_kind == "pcg" or (self.coarse_kind == "auto" and nu > DENSE_COARSE_MAX):
+            self._coarse_setup_pcg(lv)
+            return
         if nu > DENSE_COARSE_MAX:
             raise ContractError(f"coarse problem has {nu} unique dofs > {DENSE_COARSE_MAX}: "
-                                f"the dense coarse solve is not built for it")
+                                f"use coarse='pcg' (or 'auto')")
+        lv.cpcg = None
         newid = torch.full((uniq.numel(),), -1, dtype=torch.int64, device=dev)
         newid[keep_u] = torch.arange(nu, device=dev)
         uid = newid[inv]                                  # per local point, -1 masked
@@ -329,8 +347,23 @@ class MultigridHierarchy:
             sm.apply(src, lv.e, sub=lv.Aq, res_out=store, d=lv.d, a=a, b=b, e_acc=True, st=st)
             src = store
 
+    def _coarse_setup_pcg(self, lv):
+        from .solvers import FusedPCG, JacobiPreconditioner
+        lv.cpcg = FusedPCG(lv.op, JacobiPreconditioner(lv.op), tol=self.coarse_tol,
+                           max_iter=self.coarse_iters, use_graph=False)
+        lv.e = lv.cpcg.x           # the coarse correction is the inner solution
+
     def _coarse(self, lv, r, st):
         L, s = lib(), stream_ptr()
+        if lv.cpcg is not None:
+            # fixed launch sequence (graph-capturable): init + max_iter + 1
+            # fused iterations; converged iterations are no-ops, the last one
+            # applies the deferred x update
+            c = lv.cpcg
+            c.init(r)
+            for _ in range(self.coarse_iters + 1):
+                c._iteration()
+            return
         check(L.nk_gather(lv.nu, ptr(lv.rep), ptr(r), ptr(lv.ru), ptr(st), s), "gather")
         check(L.nk_dense_matvec(lv.nu, ptr(lv.Ainv), ptr(lv.ru), ptr(lv.eu), ptr(st), s),
               "dense_matvec")
@@ -379,6 +412,9 @@ class MultigridHierarchy:
             n += 2 * (lv.deg - 1) * A                         # A d inside smoothing
             n += 2 * A                                        # A e before restrict / after prolong
             n += 2 + g                                        # interp x2, coarse gs
+        c = self.levels[-1]
+        if getattr(c, "cpcg", None) is not None:
+            return n + 2 + 3 * (self.coarse_iters + 1)
         return n + 3
 
 
@@ -428,12 +464,17 @@ class MultigridPCG:
     graph replay; once the device flag is set, every launch is a no-op except
     the V-cycle's BK5s (they carry no state pointer)."""
 
-    def __init__(self, op, hierarchy=None, tol=1e-8, max_iter=500, flexible=False, chunk=4,
+    def __init__(self, op, hierarchy=None, tol=1e-8, max_iter=500, flexible=None, chunk=4,
                  use_graph=True, **hier_kw):
         import torch
         from .solvers import _state_tensor
         self.op = op
         self.h = hierarchy if hierarchy is not None else MultigridHierarchy(op, **hier_kw)
+        if flexible is None:
+            # non-symmetric (Schwarz counting weight) or nonlinear (iterative
+            # coarse solve) preconditioners need the flexible beta
+            flexible = (self.h.smoother in _SCHWARZ or
+                        getattr(self.h.levels[-1], "cpcg", None) is not None)
         self.tol, self.max_iter, self.flexible = float(tol), int(max_iter), bool(flexible)
         self.chunk = max(1, int(chunk))
         self.use_graph = use_graph

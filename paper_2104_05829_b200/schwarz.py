@@ -120,12 +120,14 @@ def fdm_1d_batch(D, w, h, left, right):
 
 
 class SchwarzSmoother:
-    """z = S r for a PoissonOperator (single rank): kind 'asm' or 'ras'.
+    """z = S r for a PoissonOperator (single rank): kind 'asm' or 'ras';
+    precision 64, or 32 (local solves in FP32, fields FP64 -- the paper's
+    32-bit smoothing, SmootherConfig.precision SPEC.md:463).
 
     Buffers are preallocated; ``apply`` writes into caller buffers so the
     smoother can sit inside a captured CUDA graph (MultigridHierarchy)."""
 
-    def __init__(self, op, kind="asm"):
+    def __init__(self, op, kind="asm", precision=64):
         import torch
         from .gather_scatter import gs_setup
         from .mesh import mesh_coordinates
@@ -133,6 +135,9 @@ class SchwarzSmoother:
             raise ContractError(f"unknown Schwarz kind {kind!r} (built: {KINDS})")
         if op.ncomp != 1:
             raise ContractError("Schwarz smoothing is built for scalar operators")
+        if precision not in (32, 64):
+            raise ContractError(f"precision must be 32 or 64, got {precision!r}")
+        self.precision = int(precision)
         if op.gs.comm is not None and op.gs.comm.size > 1:
             raise ContractError("multi-rank Schwarz smoothing is not built (the extended "
                                 "boxes would need a second halo)")
@@ -174,6 +179,9 @@ class SchwarzSmoother:
                 lam[neu] = np.where(fin, lam[neu] + eps[:, None, None] / 3.0, np.inf)
         self.S = torch.as_tensor(np.ascontiguousarray(S), device=dev)
         self.lam = torch.as_tensor(np.ascontiguousarray(lam), device=dev)
+        if self.precision == 32:      # local solves in FP32 (+inf stays +inf)
+            self.S = self.S.float().contiguous()
+            self.lam = self.lam.float().contiguous()
         self.fmap = torch.as_tensor(fmap.astype(np.int32), device=dev).contiguous()
         self.mask = m.mask.reshape(-1)
         n = E * nq ** 3
@@ -209,8 +217,10 @@ class SchwarzSmoother:
         return 3
 
     def fdm(self, r, out, sub=None, res_out=None, out_ext=True, st=None):
-        """FDM local solves of the extended residual of r - sub (nk_fdm)."""
-        check(lib().nk_fdm(self.N, self.E, ptr(r), ptr(sub), ptr(res_out), ptr(self.fmap),
+        """FDM local solves of the extended residual of r - sub (nk_fdm, or
+        nk_fdm32 in the 32-bit smoothing mode)."""
+        fn = lib().nk_fdm32 if self.precision == 32 else lib().nk_fdm
+        check(fn(self.N, self.E, ptr(r), ptr(sub), ptr(res_out), ptr(self.fmap),
                            ptr(self.S), ptr(self.lam), float(self.op.lam0), float(self.op.lam1),
                            ptr(out), int(out_ext), ptr(st), stream_ptr()), "fdm")
 

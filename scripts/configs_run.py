@@ -22,6 +22,8 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+PMG = False
+
 
 def rhs_sine(mesh, gsh):
     import torch
@@ -103,6 +105,33 @@ def config2(out):
          "ms_per_iteration": round(1e3 * t / max(res.iterations, 1), 4),
          "gdof_iter_per_s": round(dof * res.iterations / t / 1e9, 3),
          "setup_s": round(setup, 2), "gpus": 1})
+    if not PMG:
+        return
+    # the same solve with the p-multigrid preconditioners:
+    # coarse level (65^3-ish N=1 problem) solved by the fused Jacobi-PCG to 1e-3
+    xj = res.x.clone()
+    for kind, prec in (("cheby_jac", 64), ("ras", 32), ("ras", 64)):
+        t0 = time.perf_counter()
+        h = nk.MultigridHierarchy(op, smoother=kind, smoother_precision=prec, coarse="auto")
+        torch.cuda.synchronize()
+        hs = time.perf_counter() - t0
+        sv = nk.MultigridPCG(op, h, tol=1e-8, max_iter=300)
+        sv.solve(b)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r2 = sv.solve(b)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter() - t0
+        out({"config": 2, "preconditioner": f"pmg_{kind}", "smoother_precision": prec,
+             "coarse": "pcg" if h.levels[-1].cpcg is not None else "dense",
+             "coarse_dofs": h.levels[-1].nu, "iterations": r2.iterations,
+             "converged": r2.converged, "solve_s": round(t2, 4),
+             "ms_per_iteration": round(1e3 * t2 / max(r2.iterations, 1), 3),
+             "setup_s": round(hs, 2), "speedup_vs_jacobi_pcg": round(t / t2, 2),
+             "max_rel_x_diff_vs_jacobi": float((r2.x - xj).abs().max() / xj.abs().max()),
+             "flexible": sv.flexible})
+        del sv, h
+        torch.cuda.empty_cache()
 
 
 def config4(out):
@@ -154,7 +183,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", nargs="*", type=int, default=[0, 2, 4])
     ap.add_argument("--out", default=None)
+    ap.add_argument("--pmg", action="store_true", help="config 2: also the p-multigrid solves")
     args = ap.parse_args()
+    global PMG
+    PMG = args.pmg
     import torch
     torch.cuda.set_device(0)
     f = open(args.out, "a") if args.out else None

@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=4)
     ap.add_argument("--out", default=None)
     ap.add_argument("--smoothers", nargs="*", default=["cheby_jac"])
+    ap.add_argument("--precision", type=int, default=64, help="Schwarz local-solve precision")
     args = ap.parse_args()
     import torch
     import paper_2104_05829_b200 as nk
@@ -69,7 +70,8 @@ def main():
         for sm_kind in args.smoothers:
             flex = sm_kind not in ("jacobi", "cheby_jac")
             t0 = time.perf_counter()
-            h = nk.MultigridHierarchy(op, smoother=sm_kind)
+            prec = args.precision if not sm_kind.endswith("jac") and sm_kind != "jacobi" else 64
+            h = nk.MultigridHierarchy(op, smoother=sm_kind, smoother_precision=prec)
             torch.cuda.synchronize()
             setup = time.perf_counter() - t0
             s = nk.MultigridPCG(op, h, tol=args.tol, max_iter=2000, chunk=args.chunk,
@@ -85,6 +87,7 @@ def main():
             ms_it = a.elapsed_time(z) / s.chunk
             dx = float((rm.x - rj.x).abs().max() / rj.x.abs().max())
             line = {"case": "pmg_vs_jacobi", "smoother": sm_kind, "flexible": flex,
+                    "smoother_precision": prec,
                     "counts": counts, "E": m.E, "N": N,
                     "dof": m.E * N ** 3, "tol": args.tol,
                     "jacobi_iters": rj.iterations, "jacobi_s": round(tj, 5),
@@ -105,7 +108,8 @@ def main():
                 t = a.elapsed_time(z) / reps * 1e-3
                 nqe = N + 3
                 flops = 12 * m.E * nqe ** 4
-                byts = m.E * (8 * (N + 1) ** 3 + 12 * 6 * (N + 1) ** 2 + 8 * 3 * nqe * (nqe + 1)
+                sb = 4 if prec == 32 else 8
+                byts = m.E * (8 * (N + 1) ** 3 + 12 * 6 * (N + 1) ** 2 + sb * 3 * nqe * (nqe + 1)
                               + 8 * (nqe ** 3 if sm0.kind == "asm" else (N + 1) ** 3))
                 line["fdm_us"] = round(t * 1e6, 2)
                 line["fdm_gflops"] = round(flops / t * 1e-9, 1)

@@ -20,13 +20,14 @@ def main():
     ap.add_argument("--order", type=int, default=7)
     ap.add_argument("--kind", default="asm")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--precision", type=int, default=64)
     args = ap.parse_args()
     import torch
     import paper_2104_05829_b200 as nk
     N = args.order
     m = nk.build_box_mesh((1, 1, 1), tuple(args.counts), N, deformation=("sine", 0.05))
     op = nk.PoissonOperator(m)
-    sm = nk.SchwarzSmoother(op, args.kind)
+    sm = nk.SchwarzSmoother(op, args.kind, precision=args.precision)
     r = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
     nk.gs_op(op.gs, r)
     z = torch.empty_like(r)
@@ -45,7 +46,8 @@ def main():
     t_fdm = ev[0].elapsed_time(ev[1]) / args.reps
     t_app = ev[1].elapsed_time(ev[2]) / args.reps
     nqe = N + 3
-    print(json.dumps({"E": m.E, "N": N, "kind": args.kind, "fdm_ms": round(t_fdm, 4),
+    print(json.dumps({"E": m.E, "N": N, "kind": args.kind, "precision": args.precision,
+                      "fdm_ms": round(t_fdm, 4),
                       "apply_ms": round(t_app, 4),
                       "fdm_gflops": round(12 * m.E * nqe ** 4 / t_fdm * 1e-6, 1)}))
 

@@ -188,3 +188,28 @@ def test_contract_errors():
     with pytest.raises(nk.ContractError):
         nk.chebyshev_smooth(h, len(h.levels) - 1, torch.zeros(8, dtype=torch.float64,
                                                                device="cuda"))
+
+
+def test_iterative_coarse_solve():
+    """coarse='pcg': fused Jacobi-PCG on the order-1 level to coarse_tol --
+    the scalable stand-in for the paper's AMG coarse solver.  Approximates the
+    dense coarse solve to the inner tolerance; the flexible outer PCG needs at
+    most a couple more iterations than with the exact coarse solve."""
+    op, hd, o = pair((4, 4, 3), 7)
+    hp = nk.MultigridHierarchy(op, coarse="pcg", coarse_tol=1e-6, coarse_iters=200)
+    assert hp.levels[-1].cpcg is not None and hd.levels[-1].cpcg is None
+    lo = o["levels"][-1]
+    r = rand_assembled(lo, 9)
+    ed = nk.coarse_solve(hd, dev(r)).cpu().numpy()
+    ep = nk.coarse_solve(hp, dev(r)).cpu().numpy()
+    assert rel_l2(ep, ed) < 1e-4
+    b = dev(rhs(o["levels"][0]))
+    rd = nk.MultigridPCG(op, hd, tol=1e-8, max_iter=200, flexible=True).solve(b)
+    xd = rd.x.clone()
+    sp = nk.MultigridPCG(op, nk.MultigridHierarchy(op, coarse="pcg"), tol=1e-8, max_iter=200)
+    assert sp.flexible                      # auto: nonlinear preconditioner
+    rp = sp.solve(b)
+    assert rp.converged and rp.iterations <= rd.iterations + 3
+    assert float((rp.x - xd).abs().max()) < 1e-6 * float(xd.abs().max())
+    with pytest.raises(nk.ContractError):
+        nk.MultigridHierarchy(op, coarse="amg")

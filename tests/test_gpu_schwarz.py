@@ -151,3 +151,48 @@ def test_contract_errors():
     sm = nk.SchwarzSmoother(op, "ras")
     with pytest.raises(nk.ContractError):
         sm(torch.zeros(5, dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("kind", ["asm", "ras"])
+@pytest.mark.parametrize("N", [3, 7, 15])
+def test_fp32_local_solves_close_to_fp64(kind, N):
+    """32-bit smoothing: FP32 local solves,
+    FP64 fields -- within single-precision accuracy of the FP64 smoother."""
+    counts = (2, 2, 2) if N < 15 else (1, 2, 1)
+    m, o, op, f = pair(counts, N)
+    r = dev(assembled_random(o, 5))
+    z64 = nk.SchwarzSmoother(op, kind)(r).cpu().numpy()
+    z32 = nk.SchwarzSmoother(op, kind, precision=32)(r).cpu().numpy()
+    assert rel_l2(z32, z64) < 2e-5
+
+
+@pytest.mark.parametrize("smoother", ["asm", "ras", "cheby_asm", "cheby_ras"])
+def test_fp32_smoothing_iterations_within_two(smoother):
+    """32-bit smoothing changes iteration counts by <= 2 and the
+    converged solution meets the tolerance."""
+    N, counts = 7, (3, 3, 3)
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    op = nk.PoissonOperator(m)
+    b = torch.randn(op.n, dtype=torch.float64, device="cuda")
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(b.dtype)
+    r64 = nk.MultigridPCG(op, nk.MultigridHierarchy(op, smoother=smoother), tol=1e-8,
+                          max_iter=200, flexible=True).solve(b)
+    x64 = r64.x.clone()
+    r32 = nk.MultigridPCG(op, nk.MultigridHierarchy(op, smoother=smoother, smoother_precision=32),
+                          tol=1e-8, max_iter=200, flexible=True).solve(b)
+    assert r32.converged and abs(r32.iterations - r64.iterations) <= 2
+    res = b - op(r32.x)
+    wt = op.weights
+    assert float(torch.sqrt(torch.sum(wt * res * res))) <= 1.01e-8 * float(
+        torch.sqrt(torch.sum(wt * b * b)))
+    assert float((r32.x - x64).abs().max()) < 1e-6 * float(x64.abs().max())
+
+
+def test_fp32_contract_errors():
+    m = nk.build_box_mesh((1, 1, 1), (2, 2, 2), 3)
+    op = nk.PoissonOperator(m)
+    with pytest.raises(nk.ContractError):
+        nk.SchwarzSmoother(op, "asm", precision=16)
+    with pytest.raises(nk.ContractError):
+        nk.MultigridHierarchy(op, smoother="cheby_jac", smoother_precision=32)
