@@ -139,8 +139,8 @@ class MultigridHierarchy:
     scalable stand-in built on the same fused PCG kernels."""
 
     def __init__(self, op, degree=2, bounds=(0.1, 1.1), power_iters=20, seed=2104,
-                 coarse="auto", smoother="cheby_jac", smoother_precision=64, coarse_tol=1e-3,
-                 coarse_iters=100):
+                 coarse="auto", smoother="cheby_jac", smoother_precision=64, coarse_tol=1e-2,
+                 coarse_iters=50):
         import torch
         from .solvers import JacobiPreconditioner, PoissonOperator
         if op.ncomp != 1:

@@ -42,6 +42,32 @@ def _face_slice(nq, axis, side, inward=False):
     return tuple(s)
 
 
+def _face_pairs(srt):
+    """Rows of srt (sorted face id sets) that are equal, as index pairs.
+    Groups by a 64-bit polynomial hash of the row (fast), then verifies the
+    candidate pairs exactly; any collision or a group of more than two falls
+    back to the exact (slow) row-unique path."""
+    with np.errstate(over="ignore"):
+        key = np.zeros(len(srt), dtype=np.uint64)
+        for q in range(srt.shape[1]):
+            key = key * np.uint64(0x9E3779B97F4A7C15) + srt[:, q].astype(np.uint64)
+    order = np.argsort(key, kind="stable")
+    k = key[order]
+    same = k[1:] == k[:-1]
+    triple = same[1:] & same[:-1]
+    r0, r1 = order[:-1][same], order[1:][same]
+    if not triple.any() and np.array_equal(srt[r0], srt[r1]):
+        return r0, r1
+    _, grp, cnt = np.unique(srt, axis=0, return_inverse=True, return_counts=True)
+    if np.any(cnt > 2):
+        raise ContractError("a face id set is held by more than two element faces")
+    grp = grp.ravel()
+    order = np.argsort(grp, kind="stable")
+    g = grp[order]
+    same = g[1:] == g[:-1]
+    return order[:-1][same], order[1:][same]
+
+
 def face_source_map(ids, E, N):
     """fmap[e, f, a, b]: local index of the point one layer inside the face
     neighbour across face f (x- x+ y- y+ z- z+) at e's face point (a, b)
@@ -60,14 +86,7 @@ def face_source_map(ids, E, N):
     if E == 0:
         return fmap.reshape(E, 6, nq, nq)
     srt = np.sort(fid, axis=1)
-    _, grp, cnt = np.unique(srt, axis=0, return_inverse=True, return_counts=True)
-    if np.any(cnt > 2):
-        raise ContractError("a face id set is held by more than two element faces")
-    grp = grp.ravel()
-    order = np.argsort(grp, kind="stable")
-    g = grp[order]
-    same = g[1:] == g[:-1]
-    r0, r1 = order[:-1][same], order[1:][same]
+    r0, r1 = _face_pairs(srt)
     A = np.concatenate([r0, r1])
     B = np.concatenate([r1, r0])
     if len(A):
@@ -80,42 +99,59 @@ def face_source_map(ids, E, N):
     return fmap.reshape(E, 6, nq, nq)
 
 
-def fdm_1d_batch(D, w, h, left, right):
+def fdm_1d_batch(D, w, h, left, right, device="cpu"):
     """Batched extended 1-D generalised eigenproblems (oracle/schwarz.py:
     fdm_1d): h (B,), left/right (B,) side kinds 0 nbr / 1 neu / 2 dir.
-    Returns S (B, N+3, N+3) with S^T M S = I and lam (B, N+3), +inf on the
-    modes of dropped points (decoupled with a -1 diagonal, so eigh isolates
-    them)."""
-    D = np.asarray(D, dtype=np.float64)
-    w = np.asarray(w, dtype=np.float64)
-    N = len(w) - 1
-    nb = len(h)
-    n3 = 3 * N + 1
+    Returns float64 torch tensors on `device`: S (B, N+3, N+3) with
+    S^T M S = I and lam (B, N+3), +inf on the modes of dropped points
+    (decoupled with a -1 diagonal, so eigh isolates them).  The restricted
+    matrices are built directly (own element on points 1..N+1, the left /
+    right neighbour's two points next to the shared face when present) and
+    solved by batched eigh on the device (cuSOLVER on a GPU)."""
+    import torch
+    f64 = torch.float64
+    def _t(x, dt=f64):
+        if isinstance(x, torch.Tensor):
+            return x.to(device=device, dtype=dt)
+        return torch.as_tensor(np.array(x), device=device, dtype=dt)
+    D, w, h = _t(D), _t(w), _t(h)
+    left, right = _t(left, torch.int64), _t(right, torch.int64)
+    N = w.numel() - 1
+    nb = h.numel()
     K1 = D.T @ (w[:, None] * D)
-    use = np.stack([left == _NBR, np.ones(nb, bool), right == _NBR], 1).astype(np.float64)
-    K = np.zeros((nb, n3, n3))
-    M = np.zeros((nb, n3))
-    for el in range(3):
-        s = el * N
-        K[:, s:s + N + 1, s:s + N + 1] += (use[:, el] * 2.0 / h)[:, None, None] * K1
-        M[:, s:s + N + 1] += (use[:, el] * h / 2.0)[:, None] * w
-    sel = np.arange(N - 1, 2 * N + 2)
-    K = K[:, sel][:, :, sel]
-    M = M[:, sel]
-    keep = np.ones((nb, N + 3), dtype=bool)
+    g = (2.0 / h)[:, None, None]
+    K = torch.zeros((nb, N + 3, N + 3), dtype=f64, device=device)
+    M = torch.zeros((nb, N + 3), dtype=f64, device=device)
+    K[:, 1:N + 2, 1:N + 2] = g * K1
+    M[:, 1:N + 2] = (h / 2.0)[:, None] * w
+    ln = (left == _NBR).to(f64)
+    rn = (right == _NBR).to(f64)
+    # left neighbour: its local points N-1, N -> restricted 0, 1
+    K[:, 0:2, 0:2] += (ln[:, None, None] * g) * K1[N - 1:N + 1, N - 1:N + 1]
+    M[:, 0:2] += (ln * h / 2.0)[:, None] * w[N - 1:N + 1]
+    # right neighbour: its local points 0, 1 -> restricted N+1, N+2
+    K[:, N + 1:N + 3, N + 1:N + 3] += (rn[:, None, None] * g) * K1[0:2, 0:2]
+    M[:, N + 1:N + 3] += (rn * h / 2.0)[:, None] * w[0:2]
+    keep = torch.ones((nb, N + 3), dtype=torch.bool, device=device)
     keep[:, 0] = left == _NBR
     keep[:, 1] = left != _DIR
     keep[:, N + 2] = right == _NBR
     keep[:, N + 1] = right != _DIR
     drop = ~keep
-    K = np.where(drop[:, :, None] | drop[:, None, :], 0.0, K)
-    K[:, np.arange(N + 3), np.arange(N + 3)] = np.where(drop, -1.0,
-                                                        K[:, np.arange(N + 3), np.arange(N + 3)])
-    M = np.where(drop, 1.0, M)
-    Mh = 1.0 / np.sqrt(M)
-    lam, V = np.linalg.eigh(Mh[:, :, None] * K * Mh[:, None, :])
+    K = torch.where(drop[:, :, None] | drop[:, None, :], torch.zeros((), dtype=f64, device=device), K)
+    idx = torch.arange(N + 3, device=device)
+    K[:, idx, idx] = torch.where(drop, torch.full((), -1.0, dtype=f64, device=device),
+                                 K[:, idx, idx])
+    M = torch.where(drop, torch.ones((), dtype=f64, device=device), M)
+    Mh = 1.0 / torch.sqrt(M)
+    Ks = Mh[:, :, None] * K * Mh[:, None, :]
+    lam = torch.empty((nb, N + 3), dtype=f64, device=device)
+    V = torch.empty_like(Ks)
+    CH = 1 << 14          # cuSOLVER batched syev rejects batches >= 32768
+    for c0 in range(0, nb, CH):
+        lam[c0:c0 + CH], V[c0:c0 + CH] = torch.linalg.eigh(Ks[c0:c0 + CH])
     S = Mh[:, :, None] * V
-    lam = np.where(lam < -0.5, np.inf, lam)
+    lam = torch.where(lam < -0.5, torch.full((), float("inf"), dtype=f64, device=device), lam)
     return S, lam
 
 
@@ -163,22 +199,22 @@ class SchwarzSmoother:
             lo, hi = _face_slice(nq, d, 0), _face_slice(nq, d, 1)
             diff = torch.stack([X[c][hi] - X[c][lo] for c in range(3)])
             h[:, d] = torch.sqrt((diff ** 2).sum(0)).reshape(E, -1).mean(1)
-        h = h.cpu().numpy()
         self.h = h
         b = m.basis
         S, lam = fdm_1d_batch(b.diff, b.weights, h.reshape(-1), kinds[:, 0::2].reshape(-1),
-                              kinds[:, 1::2].reshape(-1))
+                              kinds[:, 1::2].reshape(-1), device=dev)
         S = S.reshape(E, 3, nqe, nqe)
         lam = lam.reshape(E, 3, nqe)
         lam1 = float(op.lam1)
         if lam1 == 0.0:
-            neu = np.all(kinds == _NEU, axis=1)
-            if neu.any():   # pure-Neumann surrogate: shift by eps = 1e-8 max(Lambda)
-                fin = np.isfinite(lam[neu])
-                eps = 1e-8 * np.sum(np.max(np.where(fin, lam[neu], 0.0), axis=2), axis=1)
-                lam[neu] = np.where(fin, lam[neu] + eps[:, None, None] / 3.0, np.inf)
-        self.S = torch.as_tensor(np.ascontiguousarray(S), device=dev)
-        self.lam = torch.as_tensor(np.ascontiguousarray(lam), device=dev)
+            neu = torch.as_tensor(np.all(kinds == _NEU, axis=1), device=dev)
+            if bool(neu.any()):   # pure-Neumann surrogate: shift by eps = 1e-8 max(Lambda)
+                ln_ = lam[neu]
+                fin = torch.isfinite(ln_)
+                eps = 1e-8 * torch.where(fin, ln_, torch.zeros_like(ln_)).amax(dim=2).sum(dim=1)
+                lam[neu] = torch.where(fin, ln_ + eps[:, None, None] / 3.0, ln_)
+        self.S = S.contiguous()
+        self.lam = lam.contiguous()
         if self.precision == 32:      # local solves in FP32 (+inf stays +inf)
             self.S = self.S.float().contiguous()
             self.lam = self.lam.float().contiguous()

@@ -54,6 +54,9 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--smoothers", nargs="*", default=["cheby_jac"])
     ap.add_argument("--precision", type=int, default=64, help="Schwarz local-solve precision")
+    ap.add_argument("--coarse", default="auto")
+    ap.add_argument("--coarse-tol", nargs="*", type=float, default=[1e-2])
+    ap.add_argument("--coarse-iters", type=int, default=50)
     args = ap.parse_args()
     import torch
     import paper_2104_05829_b200 as nk
@@ -67,15 +70,17 @@ def main():
         jac = nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=args.tol, max_iter=20000,
                           chunk=32)
         rj, tj = timed(jac, b)
-        for sm_kind in args.smoothers:
+        for sm_kind, ctol in [(k, c) for k in args.smoothers for c in args.coarse_tol]:
             flex = sm_kind not in ("jacobi", "cheby_jac")
             t0 = time.perf_counter()
             prec = args.precision if not sm_kind.endswith("jac") and sm_kind != "jacobi" else 64
-            h = nk.MultigridHierarchy(op, smoother=sm_kind, smoother_precision=prec)
+            h = nk.MultigridHierarchy(op, smoother=sm_kind, smoother_precision=prec,
+                                      coarse=args.coarse, coarse_tol=ctol,
+                                      coarse_iters=args.coarse_iters)
             torch.cuda.synchronize()
             setup = time.perf_counter() - t0
             s = nk.MultigridPCG(op, h, tol=args.tol, max_iter=2000, chunk=args.chunk,
-                                flexible=flex)
+                                flexible=flex or h.levels[-1].cpcg is not None)
             rm, tm = timed(s, b)
             # per-iteration split: one graph replay of `chunk` iterations
             a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -88,6 +93,8 @@ def main():
             dx = float((rm.x - rj.x).abs().max() / rj.x.abs().max())
             line = {"case": "pmg_vs_jacobi", "smoother": sm_kind, "flexible": flex,
                     "smoother_precision": prec,
+                    "coarse": "pcg" if h.levels[-1].cpcg is not None else "dense",
+                    "coarse_tol": ctol, "coarse_iters": args.coarse_iters,
                     "counts": counts, "E": m.E, "N": N,
                     "dof": m.E * N ** 3, "tol": args.tol,
                     "jacobi_iters": rj.iterations, "jacobi_s": round(tj, 5),

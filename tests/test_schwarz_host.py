@@ -48,6 +48,7 @@ def test_fdm_1d_batch_matches_oracle(N):
     h = np.linspace(0.3, 1.7, len(pairs))
     S, lam = sz.fdm_1d_batch(b.diff, b.weights, h, np.array([CODES[l] for l, _ in pairs]),
                              np.array([CODES[r] for _, r in pairs]))
+    S, lam = S.numpy(), lam.numpy()
     for q, (l, r) in enumerate(pairs):
         So, lo, keep = osz.fdm_1d(b.diff, b.weights, h[q], l, r)
         f = lambda L: np.where(np.isfinite(L), 1.0 / (np.where(np.isfinite(L), L, 0) + 1.0), 0)
