@@ -319,6 +319,11 @@ int nk_cheb_step(int64_t n, const double* r, const double* Aq, const double* inv
 int nk_dense_matvec(int64_t n, const double* A, const double* x, double* y,
                     const nk_cg_state* st, nk_stream_t stream);
 
+/* inner->done = 1 when outer->done: a nested solve (the iterative coarse
+ * solve inside a p-multigrid preconditioner) becomes a no-op once the outer
+ * PCG has converged, so graph replays past convergence cost nothing. */
+int nk_cg_gate(nk_cg_state* inner, const nk_cg_state* outer, nk_stream_t stream);
+
 /* out[0] = <a, b>_wt (wt nullable = unweighted), deterministic two-stage. */
 int nk_wdot(int64_t n, const double* a, const double* b, const double* wt, double* out,
             double* partials, nk_stream_t stream);

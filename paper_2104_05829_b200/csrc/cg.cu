@@ -344,6 +344,19 @@ extern "C" int nk_cg_pupdate(int64_t n, const double* r, double* p, const double
   return check_launch("cg_pupdate");
 }
 
+__global__ void cg_gate_kernel(nk_cg_state* inner, const nk_cg_state* outer) {
+  if (outer->done) inner->done = 1;
+}
+
+extern "C" int nk_cg_gate(nk_cg_state* inner, const nk_cg_state* outer, nk_stream_t stream) {
+  if (!inner || !outer) {
+    set_error("cg_gate: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  cg_gate_kernel<<<1, 1, 0, S(stream)>>>(inner, outer);
+  return check_launch("cg_gate");
+}
+
 extern "C" int nk_wdot(int64_t n, const double* a, const double* b, const double* wt,
                        double* out, double* partials, nk_stream_t stream) {
   if (n < 0 || !a || !b || !out || !partials) {

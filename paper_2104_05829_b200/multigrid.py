@@ -187,6 +187,7 @@ class MultigridHierarchy:
             lv.r = f() if self.levels else None
             lv.kind = smoother
             lv.sm = None
+            lv.gate_partials = torch.zeros(lv.op.partials_len(), dtype=torch.float64, device=dev)
             self.levels.append(lv)
         from .schwarz import SchwarzSmoother
         for lv in self.levels[:-1]:
@@ -297,8 +298,13 @@ class MultigridHierarchy:
         lv.eu = torch.zeros(nu + 1, dtype=torch.float64, device=dev)
 
     # ---------------------------------------------------------------- apply
-    def _apply_A(self, lv, x, y):
-        lv.op.apply(x, y)
+    def _apply_A(self, lv, x, y, st=None):
+        """y = A x on a level; with the PCG state, the launches are skipped
+        once the outer solve is done (graph replays past convergence)."""
+        if st is None or lv.op.gs.comm is not None and lv.op.gs.comm.size > 1:
+            lv.op.apply(x, y)
+        else:
+            lv.op.apply(x, y, st=st, partials=lv.gate_partials, reduce=False)
 
     def _cheb(self, lv, r, st, post):
         """Smoothing of A e = r into lv.e.  Pre: e = S r.  Post (r = the
@@ -316,7 +322,7 @@ class MultigridHierarchy:
                              a0, b0, int(post), ptr(st), s), "cheb_step")
         src = lv.res if post else r
         for i in range(1, deg):
-            self._apply_A(lv, lv.d, lv.Aq)
+            self._apply_A(lv, lv.d, lv.Aq, st)
             a, b = lv.coef[i]
             store = lv.res if i < deg - 1 else None
             check(L.nk_cheb_step(lv.n, ptr(src), ptr(lv.Aq), ptr(lv.invD), ptr(store),
@@ -341,7 +347,7 @@ class MultigridHierarchy:
                  e_acc=post, st=st)
         src = store if post else r
         for i in range(1, deg):
-            self._apply_A(lv, lv.d, lv.Aq)
+            self._apply_A(lv, lv.d, lv.Aq, st)
             a, b = lv.coef[i]
             store = bufs[i % 2] if i < deg - 1 else None
             sm.apply(src, lv.e, sub=lv.Aq, res_out=store, d=lv.d, a=a, b=b, e_acc=True, st=st)
@@ -361,6 +367,8 @@ class MultigridHierarchy:
             # applies the deferred x update
             c = lv.cpcg
             c.init(r)
+            if st is not None:       # no-op once the outer PCG is done
+                check(L.nk_cg_gate(ptr(c.st), ptr(st), s), "cg_gate")
             for _ in range(self.coarse_iters + 1):
                 c._iteration()
             return
@@ -377,14 +385,14 @@ class MultigridHierarchy:
             return
         c = self.levels[k + 1]
         self._cheb(lv, r, st, post=False)                         # pre-smooth
-        self._apply_A(lv, lv.e, lv.Aq)
+        self._apply_A(lv, lv.e, lv.Aq, st)
         check(L.nk_interp3(lv.nq, c.nq, lv.mesh.E, ptr(lv.R), ptr(r), ptr(lv.Aq), ptr(lv.wt),
                            ptr(c.mask), ptr(c.r), 0, ptr(st), s), "interp3")   # restrict
         _gs(c.op.gs, c.r, st)
         self._vcycle(k + 1, c.r, st)
         check(L.nk_interp3(c.nq, lv.nq, lv.mesh.E, ptr(lv.P), ptr(c.e), None, None,
                            ptr(lv.mask), ptr(lv.e), 1, ptr(st), s), "interp3")  # prolong
-        self._apply_A(lv, lv.e, lv.Aq)
+        self._apply_A(lv, lv.e, lv.Aq, st)
         self._cheb(lv, r, st, post=True)                          # post-smooth
 
     def apply(self, r, st=None):
@@ -414,7 +422,7 @@ class MultigridHierarchy:
             n += 2 + g                                        # interp x2, coarse gs
         c = self.levels[-1]
         if getattr(c, "cpcg", None) is not None:
-            return n + 2 + 3 * (self.coarse_iters + 1)
+            return n + 3 + 3 * (self.coarse_iters + 1)
         return n + 3
 
 

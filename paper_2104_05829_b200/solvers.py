@@ -101,9 +101,11 @@ class PoissonOperator:
         self.apply(p, out)
         return out
 
-    def apply(self, p, w, st=None, partials=None):
+    def apply(self, p, w, st=None, partials=None, reduce=True):
         """w = A p (masked, assembled).  With st/partials the BK5 launch also
-        stores p^T A p (the rank-local part) in st->pAp."""
+        stores p^T A p (the rank-local part) in st->pAp; with reduce=False the
+        state only gates the launches (no-ops once st->done, e.g. inside a
+        preconditioner replayed after convergence) and st is not written."""
         m = self.mesh
         L, s = lib(), stream_ptr()
         D = m.basis.diff  # host: passed by value to the kernel
@@ -119,7 +121,7 @@ class PoissonOperator:
 
         if not multi:
             nb = int(L.nk_bk5_blocks(m.N, m.E, self.ncomp))
-            bk5(None, 0, nb if st is not None else 0)
+            bk5(None, 0, nb if (st is not None and reduce) else 0)
             if self.ncomp == 1:
                 _local(g, w, "+", 1, st=st)
             else:
