@@ -82,6 +82,12 @@ struct GsClasses {
   int64_t bstart[NK_GS_MAX_CLASSES + 1];
 };
 
+// U chunks of 256 lanes per block: each thread issues U independent index
+// loads, then U independent value gathers, before any shuffle -- U round
+// trips in flight per thread (the kernel is L2-latency-bound, w having just
+// been written by BK5).
+constexpr int kGsU = 4;
+
 template <int OP>
 __global__ void __launch_bounds__(256)
 gs_classes_kernel(const __grid_constant__ GsClasses C, double* __restrict__ w, int ncomp,
@@ -92,21 +98,31 @@ gs_classes_kernel(const __grid_constant__ GsClasses C, double* __restrict__ w, i
   while (c + 1 < C.n && b >= C.bstart[c + 1]) ++c;
   const int M = C.M[c], Mp = C.Mp[c];
   const int64_t lanes = C.nseg[c] * Mp;
-  const int64_t t = (b - C.bstart[c]) * blockDim.x + threadIdx.x;
+  const int64_t t0 = (b - C.bstart[c]) * (int64_t)(kGsU * blockDim.x) + threadIdx.x;
   // whole warps stay active for the shuffles; out-of-range lanes carry -1
-  const int idx = t < lanes ? __ldg(C.mem[c] + t) : -1;
+  int idx[kGsU];
+#pragma unroll
+  for (int u = 0; u < kGsU; ++u) {
+    const int64_t t = t0 + (int64_t)u * blockDim.x;
+    idx[u] = t < lanes ? __ldg(C.mem[c] + t) : -1;
+  }
   const int lane = threadIdx.x & 31;
   const int m = lane & (Mp - 1);
   for (int cc = 0; cc < ncomp; ++cc) {
     double* wc = w + cc * cs;
-    const double v = idx >= 0 ? wc[idx] : 0.0;
-    double acc = v;
-    for (int j = 1; j < M; ++j) {
-      const double o = __shfl_down_sync(0xffffffffu, v, j, Mp);
-      acc = fold<OP>(acc, o);
+    double v[kGsU];
+#pragma unroll
+    for (int u = 0; u < kGsU; ++u) v[u] = idx[u] >= 0 ? wc[idx[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < kGsU; ++u) {
+      double acc = v[u];
+      for (int j = 1; j < M; ++j) {
+        const double o = __shfl_down_sync(0xffffffffu, v[u], j, Mp);
+        acc = fold<OP>(acc, o);
+      }
+      const double res = __shfl_sync(0xffffffffu, acc, lane - m);
+      if (idx[u] >= 0) wc[idx[u]] = res;
     }
-    const double res = __shfl_sync(0xffffffffu, acc, lane - m);
-    if (idx >= 0) wc[idx] = res;
   }
 }
 
@@ -166,7 +182,7 @@ extern "C" int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t*
     C.nseg[k] = nsegs[c];
     C.mem[k] = members[c];
     C.bstart[k] = blocks;
-    blocks += (nsegs[c] * mp + 255) / 256;
+    blocks += (nsegs[c] * mp + 256 * kGsU - 1) / (256 * kGsU);
     ++k;
   }
   C.n = k;
