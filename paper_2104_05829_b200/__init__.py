@@ -15,7 +15,7 @@ from ._lib import (ContractError, NativeLibraryError, UnsupportedOrderError,  # 
 from .basis import InvalidOrderError, SpectralBasis, gll_rule, interp_matrix  # noqa: F401
 from .gather_scatter import gs_op, gs_op_overlapped, gs_setup  # noqa: F401
 from .kernels import (apply_helmholtz_local, apply_mass, apply_stiffness_local,  # noqa: F401
-                      extract_diagonal, inner_product)
+                      extract_diagonal, inner_product, select_kernel_variant)
 from .mesh import (Mesh, assign_global_ids, build_box_mesh, geometric_factors,  # noqa: F401
                    read_hexmesh, write_hexmesh)
 from .multigrid import (MultigridHierarchy, MultigridPCG, chebyshev_smooth,  # noqa: F401

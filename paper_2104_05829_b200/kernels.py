@@ -13,7 +13,8 @@ import numpy as np
 from ._lib import ContractError, check, lib, ptr, stream_ptr
 
 __all__ = ["apply_stiffness_local", "apply_helmholtz_local", "apply_mass", "inner_product",
-           "extract_diagonal", "KernelCounters", "COUNTERS", "bk5_bytes", "bk5_flops"]
+           "extract_diagonal", "KernelCounters", "COUNTERS", "bk5_bytes", "bk5_flops",
+           "select_kernel_variant", "reset_kernel_variant", "variant_report", "BK5_VARIANTS"]
 
 
 @dataclass
@@ -255,3 +256,80 @@ def extract_diagonal(mesh, basis=None, spec="stiffness", gs=None, assemble=True)
             gs = gs_setup(mesh.ids, nq=mesh.nq, device=mesh.device)
         gs_op(gs, d)
     return d
+
+
+# BK5 variants (nk_bk5_set_variant): declaration order = tie-break order
+BK5_VARIANTS = {"kslab": 1, "pencil": 3, "pencil_tma": 4, "pencil2": 5}
+_VARIANT_REPORT = []
+
+
+def bk5_variant_eligible(name, N, ncomp=1):
+    """Which BK5 variants serve an order (the analogue of SPEC.md:426's
+    "N_q=12 -> full3d not eligible"): pencil-TMA needs N+1 in {4, 6, 8};
+    3-component batches use the k-slab or the pencil kernels."""
+    if name not in BK5_VARIANTS:
+        return False
+    if name == "pencil_tma":
+        return ncomp == 1 and N + 1 in (4, 6, 8)
+    return True
+
+
+def select_kernel_variant(mesh, candidates=None, reps=20, force=None, ncomp=1):
+    """Measured BK5 variant choice on `mesh` (the runtime
+    analogue of the paper's "2D or 3D thread structure ... whichever is more
+    performant"): every eligible candidate runs `reps`
+    timed applies (CUDA events, after one warm-up); the lowest median wins,
+    ties broken by declaration order; `force` (a variant name) skips the
+    benchmark.  The choice is installed process-wide (nk_bk5_set_variant) and
+    recorded in variant_report().  Returns the chosen name."""
+    import statistics
+
+    import torch
+    names = list(BK5_VARIANTS) if candidates is None else list(candidates)
+    for nme in names:
+        if nme not in BK5_VARIANTS:
+            raise ContractError(f"unknown BK5 variant {nme!r} (built: {list(BK5_VARIANTS)})")
+    if force is not None:
+        if force not in BK5_VARIANTS:
+            raise ContractError(f"unknown BK5 variant {force!r}")
+        lib().nk_bk5_set_variant(BK5_VARIANTS[force])
+        _VARIANT_REPORT.append({"N": mesh.N, "E": mesh.E, "chosen": force, "forced": True})
+        return force
+    elig = [n for n in names if bk5_variant_eligible(n, mesh.N, ncomp)]
+    if not elig:
+        raise ContractError("no eligible BK5 variant among the candidates")
+    u = torch.randn(mesh.n_local * ncomp, dtype=torch.float64, device=mesh.device)
+    w = torch.empty_like(u)
+    old = lib().nk_bk5_set_variant(0)
+    times = {}
+    try:
+        for nme in elig:
+            lib().nk_bk5_set_variant(BK5_VARIANTS[nme])
+            _bk5(u, mesh, 1.0, 0.0, ncomp, out=w)
+            ts = []
+            for _ in range(max(1, int(reps))):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                _bk5(u, mesh, 1.0, 0.0, ncomp, out=w)
+                b.record()
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            times[nme] = statistics.median(ts)
+    finally:
+        lib().nk_bk5_set_variant(old)
+    best = min(elig, key=lambda n: (times[n], elig.index(n)))
+    lib().nk_bk5_set_variant(BK5_VARIANTS[best])
+    _VARIANT_REPORT.append({"N": mesh.N, "E": mesh.E, "chosen": best, "forced": False,
+                            "median_ms": {k: round(v, 5) for k, v in times.items()}})
+    return best
+
+
+def reset_kernel_variant():
+    """Back to the measured per-order table (nk_bk5_set_variant(0))."""
+    lib().nk_bk5_set_variant(0)
+
+
+def variant_report():
+    """Selections made by select_kernel_variant (the timing report entry of
+    SPEC.md:425)."""
+    return list(_VARIANT_REPORT)
