@@ -432,6 +432,35 @@ def run_ours(args):
                "halo_transport": getattr(op.gs, "transport", None) if ws > 1 else None,
                "dot_allreduce": ("ipc-board" if getattr(comm, "board", None) is not None
                                  else "torch.distributed") if ws > 1 else None}
+        if ws > 1 and not args.no_solvers:
+            # the distributed p-multigrid (Chebyshev-Jacobi, iterative coarse
+            # solve over the same halo + all-reduce) on the weak-scaling box:
+            # time to tol 1e-8 vs the distributed Jacobi-PCG, max over ranks
+            import time as _time
+            tts = {}
+            try:
+                for name, make in (
+                        ("jacobi_pcg", lambda: nk.FusedPCG(op, jac, tol=1e-8, max_iter=5000,
+                                                           chunk=32)),
+                        ("pmg_cheby_jac", lambda: nk.MultigridPCG(
+                            op, nk.MultigridHierarchy(op, coarse="pcg"), tol=1e-8,
+                            max_iter=500))):
+                    sv = make()
+                    sv.solve(b_rhs)
+                    barrier(ws)
+                    torch.cuda.synchronize()
+                    t0 = _time.perf_counter()
+                    res = sv.solve(b_rhs)
+                    torch.cuda.synchronize()
+                    tt = max_over_ranks(_time.perf_counter() - t0, ws)
+                    tts[name] = {"iterations": res.iterations, "solve_ms": round(tt * 1e3, 3),
+                                 "converged": bool(res.converged)}
+                    del sv
+                tts["pmg_speedup_vs_jacobi_pcg"] = round(
+                    tts["jacobi_pcg"]["solve_ms"] / tts["pmg_cheby_jac"]["solve_ms"], 2)
+            except Exception as exc:  # reported, never fatal for the headline
+                tts["error"] = f"{type(exc).__name__}: {exc}"[:200]
+            bp5["time_to_solution_tol1e-8"] = tts
 
     # ---- Time to solution at tol 1e-8 (N = 1 only, same mesh, random
     # assembled rhs): Jacobi-PCG vs the p-multigrid preconditioners

@@ -150,9 +150,18 @@ class MultigridHierarchy:
                                 f"'auto')")
         self.coarse_kind = coarse
         self.coarse_tol, self.coarse_iters = float(coarse_tol), int(coarse_iters)
-        if op.comm is not None and op.comm.size > 1:
-            raise ContractError("multi-rank p-multigrid is not built (coarse solve is "
-                                "single-rank); use Jacobi-PCG across ranks")
+        self.comm = op.comm if (op.comm is not None and op.comm.size > 1) else None
+        if self.comm is not None:
+            # across ranks: box meshes (each rank rebuilds its own elements at
+            # every order), Jacobi-family smoothing (the Schwarz boxes would
+            # need a second halo) and the iterative coarse solve (the fused
+            # PCG runs over the same halo + all-reduce path)
+            if op.mesh.counts is None:
+                raise ContractError("multi-rank p-multigrid needs a box mesh")
+            if smoother not in ("jacobi", "cheby_jac"):
+                raise ContractError("multi-rank p-multigrid smooths with jacobi / cheby_jac")
+            if coarse == "dense":
+                raise ContractError("the dense coarse solve is single-rank: use coarse='pcg'")
         if not (0.0 < bounds[0] < bounds[1]):
             raise ContractError(f"invalid eigenvalue bound fractions {bounds}")
         self.degree = int(degree)
@@ -218,14 +227,18 @@ class MultigridHierarchy:
         x = x * lv.mask.to(x.dtype)
         y = torch.empty_like(x)
         lam = 0.0
+        nrm = torch.zeros(2, dtype=torch.float64, device=x.device)
         for _ in range(int(iters)):
             lv.op.apply(x, y)
             if lv.sm is not None:
                 y = lv.sm(y)
             else:
                 y = lv.invD * y
-            ny = float(torch.sqrt(torch.sum(lv.wt * y * y)))
-            nx = float(torch.sqrt(torch.sum(lv.wt * x * x)))
+            nrm[0] = torch.sum(lv.wt * y * y)
+            nrm[1] = torch.sum(lv.wt * x * x)
+            if self.comm is not None:
+                self.comm.allreduce_sum_(nrm)
+            ny, nx = (float(v) for v in torch.sqrt(nrm).cpu())
             lam = ny / nx
             x = y / ny
             y = torch.empty_like(x)
@@ -240,6 +253,10 @@ class MultigridHierarchy:
         Ainv = (A + 1 1^T)^-1 - 1 1^T / n^2."""
         import torch
         from .kernels import _bk5
+        if self.comm is not None:
+            lv.nu = -1                 # distributed: no global unique numbering here
+            self._coarse_setup_pcg(lv)
+            return
         m, dev = lv.mesh, lv.mesh.device
         nq3 = lv.nq ** 3
         ids = m.ids.reshape(-1)
@@ -499,6 +516,18 @@ class MultigridPCG:
         self.hist = torch.zeros(self.max_iter + 2, dtype=torch.float64, device=dev)
         self.wt = op.weights
         self.graph = None
+        comm = op.gs.comm
+        self.comm = comm if (comm is not None and comm.size > 1) else None
+        if self.comm is not None:
+            board = False
+            if getattr(op.gs, "transport", "p2p") == "ipc":
+                board = self.comm.enable_board(dev)
+            # graph capture needs every exchange on the stream
+            self.use_graph = self.use_graph and (board or self.comm.staging == "device")
+
+    def _allreduce(self, a, b):
+        if self.comm is not None:
+            self.comm.allreduce_sum_(self.s64[a:b])
 
     @property
     def launches_per_iter(self):
@@ -508,15 +537,19 @@ class MultigridPCG:
         L, s = lib(), stream_ptr()
         n = self.n
         self.op.apply(self.p, self.w, st=self.st, partials=self.part_bk5)      # pAp
+        self._allreduce(1, 2)
         check(L.nk_cg_update(n, ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.w), None,
                              ptr(self.wt), None, ptr(self.st), ptr(self.part_cg), s),
               "cg_update")
+        self._allreduce(3, 4)                                                  # rr
         z = self.h.apply(self.r, self.st)
         check(L.nk_wdot(n, ptr(self.r), ptr(z), ptr(self.wt), ptr(self.s64[2:3]),
                         ptr(self.part_dot), s), "wdot")
+        self._allreduce(2, 3)                                                  # rz_new
         if self.flexible:
             check(L.nk_wdot(n, ptr(z), ptr(self.w), ptr(self.wt), ptr(self.s64[4:5]),
                             ptr(self.part_dot), s), "wdot")
+            self._allreduce(4, 5)                                              # zAp
         check(L.nk_cg_pupdate(n, ptr(self.r), ptr(self.p), None, ptr(z), ptr(self.st),
                               ptr(self.hist), s), "cg_pupdate")
 
@@ -533,10 +566,13 @@ class MultigridPCG:
                            self.max_iter, int(self.flexible), s), "cg_init")
         check(L.nk_wdot(n, ptr(self.b), ptr(self.b), ptr(self.wt), ptr(self.s64[5:6]),
                         ptr(self.part_dot), s), "wdot")
+        self._allreduce(3, 4)                                                  # rr
+        self._allreduce(5, 6)                                                  # bb
         z = self.h.apply(self.r)
         self.p.copy_(z)
         check(L.nk_wdot(n, ptr(self.r), ptr(z), ptr(self.wt), ptr(self.s64[0:1]),
                         ptr(self.part_dot), s), "wdot")
+        self._allreduce(0, 1)                                                  # rz
         check(L.nk_cg_init_finalize(ptr(self.st), ptr(self.hist), s), "cg_init_finalize")
 
     def _capture(self):

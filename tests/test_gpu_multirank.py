@@ -102,3 +102,80 @@ def test_two_ranks_one_gpu_gs_and_pcg(N, transport):
         xg[r["mine"]] = r["x"].reshape(-1, nq3)
     assert int(res[0]["it"]) == int(res[1]["it"])
     assert np.max(np.abs(xg.ravel() - o.x)) < 1e-7 * np.max(np.abs(o.x))
+
+
+def _pmg_worker(rank, world, port, outdir, counts, N, transport):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2104_05829_b200 as nk
+        from oracle import gs as ogs
+        from oracle import mesh as om
+        from paper_2104_05829_b200.distributed import RankComm
+        g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05))
+        nq3 = (N + 1) ** 3
+        part = nk.rcb(g.xyz.reshape(3, g.E, -1).mean(axis=2).T, world)
+        mine = np.flatnonzero(part == rank)
+        comm = RankComm(transport=transport)
+        m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05),
+                              elements=mine)
+        op = nk.PoissonOperator(m, comm=comm)
+        X = g.xyz.reshape(3, -1)
+        f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+        bglob = g.mask.ravel() * ogs.gs_op(g.ids, g.B.ravel() * f)
+        b = bglob.reshape(g.E, nq3)[mine].ravel()
+        h = nk.MultigridHierarchy(op, smoother="cheby_jac", coarse="auto")
+        s = nk.MultigridPCG(op, h, tol=1e-8, max_iter=200)
+        res = s.solve(torch.as_tensor(b, device="cuda"))
+        np.savez(os.path.join(outdir, f"p{rank}.npz"), mine=mine, x=res.x.cpu().numpy(),
+                 it=res.iterations, conv=res.converged, graph=bool(s.use_graph),
+                 lmax=np.array([lv.lmax for lv in h.levels[:-1]]),
+                 coarse_pcg=h.levels[-1].cpcg is not None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("transport", ["p2p", "ipc"])
+def test_two_ranks_pmg(transport):
+    """p-multigrid across ranks (Chebyshev-Jacobi smoothing, iterative coarse
+    solve, halo at every order, all-reduced scalars): same solution as the
+    single-rank oracle Jacobi-PCG, iteration count within 2 of the
+    single-process p-multigrid on the same global mesh."""
+    import torch.multiprocessing as mp
+    import paper_2104_05829_b200 as nk
+    from oracle import gs as ogs
+    from oracle import mesh as om
+    from oracle import operators as oop
+    from oracle import solvers as osol
+    counts, world, N = (4, 4, 2), 2, 5
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_pmg_worker, args=(world, _port(), d, counts, N, transport), nprocs=world,
+                 join=True)
+        res = [np.load(os.path.join(d, f"p{r}.npz")) for r in range(world)]
+    g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05))
+    X = g.xyz.reshape(3, -1)
+    f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+    mask = g.mask.ravel()
+    b = mask * ogs.gs_op(g.ids, g.B.ravel() * f)
+    sh = (g.E,) + g.G.shape[2:]
+    A = lambda v: mask * ogs.gs_op(g.ids, oop.bk5(g.basis.diff, g.G, v.reshape(sh)).ravel())
+    inv = mask / ogs.gs_op(g.ids, oop.local_diagonal(g.basis.diff, g.G).ravel())
+    o = osol.pcg(A, lambda r: inv * r, b, tol=1e-10, max_iter=2000,
+                 weights=1.0 / ogs.multiplicity(g.ids))
+    m1 = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05))
+    op1 = nk.PoissonOperator(m1)
+    r1 = nk.MultigridPCG(op1, nk.MultigridHierarchy(op1, coarse="pcg"), tol=1e-8,
+                         max_iter=200).solve(torch.as_tensor(b, device="cuda"))
+    nq3 = (N + 1) ** 3
+    xg = np.zeros((g.E, nq3))
+    for r in res:
+        assert bool(r["conv"]) and bool(r["coarse_pcg"])
+        assert bool(r["graph"]) == (transport == "ipc")
+        assert abs(int(r["it"]) - r1.iterations) <= 2
+        xg[r["mine"]] = r["x"].reshape(-1, nq3)
+    assert int(res[0]["it"]) == int(res[1]["it"])
+    assert np.allclose(res[0]["lmax"], res[1]["lmax"], rtol=0, atol=0)
+    assert np.max(np.abs(xg.ravel() - o.x)) < 1e-6 * np.max(np.abs(o.x))
