@@ -109,86 +109,86 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
   const T* Se = Sg + e * 3 * NQE * NQE;
   const int64_t ob = e * NQ3;
   const int32_t* fm = fmap + e * 6 * NQ2;
-  constexpr int MD = NQE * SP;
-  // Every gather / scatter below works on whole rows (one thread per row of
-  // contiguous points): one index computation per row instead of per point,
-  // and a row's loads are independent (in flight together).
-  // zero the box (edges / corners / missing neighbours stay 0)
-  for (int q = t; q < F::A_SZ; q += NT) A[q] = T(0);
-  // S rows (d, i): Sb row-major, Sf transposed
-  for (int rw = t; rw < 3 * NQE; rw += NT) {
-    const int d = rw / NQE, i = rw % NQE;
-    T v[NQE];
+  // Global loads are issued in batches of CH independent loads per thread
+  // (the gather is latency-bound: one element per CTA, few warps per SM).
+  constexpr int CH = 8;
+  constexpr int NS = 3 * NQE * NQE, NF = 6 * NQ2;
+  for (int q0 = 0; q0 < NS; q0 += CH * NT) {
+    T v[CH];
 #pragma unroll
-    for (int q = 0; q < NQE; ++q) v[q] = __ldg(Se + rw * NQE + q);
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      v[u] = q < NS ? __ldg(Se + q) : T(0);
+    }
 #pragma unroll
-    for (int q = 0; q < NQE; ++q) {
-      Sb[d * MD + i * SP + q] = v[q];
-      Sf[d * MD + q * SP + i] = v[q];
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      if (q < NS) {
+        const int d = q / (NQE * NQE), ia = q % (NQE * NQE), i = ia / NQE, a = ia % NQE;
+        Sb[d * NQE * SP + i * SP + a] = v[u];
+        Sf[d * NQE * SP + a * SP + i] = v[u];
+      }
     }
   }
   for (int q = t; q < 3 * NQE; q += NT) Ls[q] = __ldg(lamg + e * 3 * NQE + q);
+  for (int q = t; q < NQE * NQE * NQE; q += NT) {
+    const int i = q % NQE, j = (q / NQE) % NQE, k = q / (NQE * NQE);
+    A[k * PS + j * LS + i] = T(0);
+  }
   __syncthreads();
-  // own rows (k, j): NQ contiguous points of r (- sub); res_out = r - sub
-  constexpr int OWN_IT = (NQ2 + NT - 1) / NT;
+  // own points (coalesced); res_out = r - sub on them
+  for (int q0 = 0; q0 < NQ3; q0 += CH * NT) {
+    double v[CH], w[CH];
 #pragma unroll
-  for (int it = 0; it < OWN_IT; ++it) {
-    const int rho = t + it * NT;
-    if (rho < NQ2) {
-      const int k = rho / NQ, j = rho % NQ;
-      const double* src = r + ob + rho * NQ;
-      double v[NQ];
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      v[u] = q < NQ3 ? __ldg(r + ob + q) : 0.0;
+      w[u] = (sub != nullptr && q < NQ3) ? __ldg(sub + ob + q) : 0.0;
+    }
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) v[i] = __ldg(src + i);
-      if (sub) {
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) v[i] -= __ldg(sub + ob + rho * NQ + i);
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      if (q < NQ3) {
+        const int i = q % NQ, j = (q / NQ) % NQ, k = q / NQ2;
+        const double x = v[u] - w[u];
+        if (res_out) res_out[ob + q] = x;
+        A[(k + 1) * PS + (j + 1) * LS + (i + 1)] = (T)x;
       }
-      if (res_out) {
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) res_out[ob + rho * NQ + i] = v[i];
-      }
-      T* dst = A + (k + 1) * PS + (j + 1) * LS + 1;
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) dst[i] = (T)v[i];
     }
   }
-  // face-neighbour rows (f, a): NQ sources through the face map
-  constexpr int FACE_IT = (6 * NQ + NT - 1) / NT;
+  // face-neighbour layers: face f, tangential (a, b) slow/fast
+  for (int q0 = 0; q0 < NF; q0 += CH * NT) {
+    int32_t src[CH];
+    double v[CH], w[CH];
 #pragma unroll
-  for (int it = 0; it < FACE_IT; ++it) {
-    const int fr = t + it * NT;
-    if (fr < 6 * NQ) {
-      const int f = fr / NQ, a = fr % NQ + 1;
-      int32_t src[NQ];
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      src[u] = q < NF ? __ldg(fm + q) : -1;
+    }
 #pragma unroll
-      for (int b = 0; b < NQ; ++b) src[b] = __ldg(fm + fr * NQ + b);
-      double v[NQ];
+    for (int u = 0; u < CH; ++u) {
+      v[u] = src[u] >= 0 ? __ldg(r + src[u]) : 0.0;
+      w[u] = (sub != nullptr && src[u] >= 0) ? __ldg(sub + src[u]) : 0.0;
+    }
 #pragma unroll
-      for (int b = 0; b < NQ; ++b) {
-        double x = 0.0;
-        if (src[b] >= 0) {
-          x = __ldg(r + src[b]);
-          if (sub) x -= __ldg(sub + src[b]);
-        }
-        v[b] = x;
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      if (src[u] >= 0) {
+        const int f = q / NQ2, ab = q % NQ2, a = ab / NQ + 1, b = ab % NQ + 1;
+        const int pos = (f & 1) ? NQE - 1 : 0;
+        int idx;
+        if (f < 2) idx = a * PS + b * LS + pos;        // x faces: (k, j)
+        else if (f < 4) idx = a * PS + pos * LS + b;   // y faces: (k, i)
+        else idx = pos * PS + a * LS + b;              // z faces: (j, i)
+        A[idx] = (T)(v[u] - w[u]);
       }
-      const int pos = (f & 1) ? NQE - 1 : 0;
-      // x faces: (k, j) -> stride LS over b; y faces: (k, i); z faces: (j, i)
-      T* dst;
-      int bs;
-      if (f < 2) { dst = A + a * PS + LS + pos; bs = LS; }
-      else if (f < 4) { dst = A + a * PS + pos * LS + 1; bs = 1; }
-      else { dst = A + pos * PS + a * LS + 1; bs = 1; }
-#pragma unroll
-      for (int b = 0; b < NQ; ++b)
-        if (src[b] >= 0) dst[b * bs] = (T)v[b];
     }
   }
   __syncthreads();
   // this thread's two lines (the second clamped onto the first when NL is odd)
   const int l0 = t, l1 = (t + NT < NL) ? t + NT : t;
   const int h0 = l0 / NQE, o0 = l0 % NQE, h1 = l1 / NQE, o1 = l1 % NQE;
+  constexpr int MD = NQE * SP;
   // forward x: lines (k = h, j = o) along i
   fdm_line2<NQE, 1, T>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sf, nullptr, 0, 0, 0, 0);
   __syncthreads();
@@ -207,19 +207,15 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
   fdm_line2<NQE, 1, T>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sb, nullptr, 0, 0, 0, 0);
   __syncthreads();
   if (out_ext) {
-    // extended rows (k, j): NQE contiguous values
     double* o = out + e * NQE * NQE * NQE;
-    for (int rw = t; rw < NQE * NQE; rw += NT) {
-      const T* srow = A + (rw / NQE) * PS + (rw % NQE) * LS;
-#pragma unroll
-      for (int i = 0; i < NQE; ++i) o[rw * NQE + i] = (double)srow[i];
+    for (int q = t; q < NQE * NQE * NQE; q += NT) {
+      const int i = q % NQE, j = (q / NQE) % NQE, k = q / (NQE * NQE);
+      o[q] = (double)A[k * PS + j * LS + i];
     }
   } else {
-    // own rows (k, j): NQ contiguous values
-    for (int rho = t; rho < NQ2; rho += NT) {
-      const T* srow = A + (rho / NQ + 1) * PS + (rho % NQ + 1) * LS + 1;
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) out[ob + rho * NQ + i] = (double)srow[i];
+    for (int q = t; q < NQ3; q += NT) {
+      const int i = q % NQ, j = (q / NQ) % NQ, k = q / NQ2;
+      out[ob + q] = (double)A[(k + 1) * PS + (j + 1) * LS + (i + 1)];
     }
   }
 }
