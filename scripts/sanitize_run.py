@@ -30,3 +30,26 @@ for N, counts in ((7, (3, 2, 2)), (4, (2, 2, 2)), (9, (2, 1, 1))):
     nk.apply_stiffness_local(uh, m)
 torch.cuda.synchronize()
 print("sanitize run ok")
+
+# SURVEY.md §8f kernels: p-multigrid (interp3, cheb_step, dense matvec, the
+# nested coarse PCG + cg_gate), Schwarz (fdm FP64/FP32, schwarz_post, ext gs),
+# projection (multi_wdot, multi_axpy, vscale), the BK5 variant selection
+for N, counts in ((5, (2, 2, 2)), (4, (3, 2, 1))):
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    op = nk.PoissonOperator(m)
+    b = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(torch.float64)
+    for sm, prec, coarse in (("cheby_jac", 64, "dense"), ("ras", 32, "pcg"),
+                             ("cheby_asm", 64, "dense")):
+        h = nk.MultigridHierarchy(op, smoother=sm, smoother_precision=prec, coarse=coarse,
+                                  coarse_iters=5, power_iters=3)
+        nk.MultigridPCG(op, h, tol=1e-6, max_iter=4, use_graph=False).solve(b)
+    ps = nk.ProjectedSolver(nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-6,
+                                        max_iter=30, use_graph=False), capacity=3)
+    for s in range(4):
+        ps.solve(b * (1.0 + 0.1 * s))
+    nk.select_kernel_variant(m, reps=1)
+    nk.kernels.reset_kernel_variant()
+torch.cuda.synchronize()
+print("sanitize run (pMG / Schwarz / projection) ok")
