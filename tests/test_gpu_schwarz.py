@@ -219,3 +219,25 @@ def test_coordinate_mesh_schwarz_matches_box(tmp_path):
     hc = nk.MultigridHierarchy(nk.PoissonOperator(mc), smoother="ras")
     z = nk.pmg_preconditioner(hc, r)
     assert torch.isfinite(z).all() and float(z.abs().max()) > 0
+
+
+@pytest.mark.parametrize("smoother", ["asm", "ras", "cheby_ras"])
+@pytest.mark.parametrize("bc,lam1", [("periodic", 5.0), ("neumann", 3.0),
+                                     ({"x-": "dirichlet", "y+": "dirichlet"}, 0.0)])
+def test_hierarchy_schwarz_boundary_kinds_match_oracle(smoother, bc, lam1):
+    """Schwarz-smoothed V-cycles on periodic / Neumann (Helmholtz) / mixed
+    boundaries -- every side kind of the FDM surrogate ('nbr', 'neu', 'dir')
+    -- against the oracle hierarchy."""
+    N, counts = 5, (3, 2, 2)
+    kw = dict(bc=bc, deformation=("sine", 0.05) if bc != "periodic" else None)
+    m = nk.build_box_mesh((1, 1, 1), counts, N, **kw)
+    op = nk.PoissonOperator(m, lam0=1.0, lam1=lam1)
+    h = nk.MultigridHierarchy(op, smoother=smoother)
+    o = opmg.build_hierarchy((1, 1, 1), counts, N, smoother=smoother, lam0=1.0, lam1=lam1, **kw)
+    for lg, lo in zip(h.levels[:-1], o["levels"][:-1]):
+        assert abs(lg.lmax - lo.lmax) < 1e-9 * lo.lmax
+    lv = o["levels"][0]
+    r = lv.mask * ogs.gs_op(lv.mesh.ids, lv.wt * np.random.default_rng(3).standard_normal(
+        lv.mask.size))
+    z = nk.pmg_preconditioner(h, dev(r)).cpu().numpy()
+    assert rel_l2(z, opmg.vcycle(o, r)) < 1e-9
