@@ -364,17 +364,26 @@ int nk_vscale(int64_t n, const double* x, double* y, const double* s, nk_stream_
  * (Lx+Ly+Lz) + lam1)) (S3)^T r_ext per element.  out_ext != 0: out is the
  * extended field [E][(N+3)^3] (ASM); else the own points [E][(N+1)^3] (RAS).
  * sub, res_out nullable; res_out (own points) receives r - sub and must not
- * alias r or sub.  Skipped once st->done (st nullable). */
-int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, double* res_out,
-           const int32_t* fmap, const double* S, const double* lam, double lam0, double lam1,
-           double* out, int out_ext, const nk_cg_state* st, nk_stream_t stream);
+ * alias r or sub.  fmap entries <= -2 read rx[-src - 2] (values already
+ * r - sub received from the neighbour rank; rx nullable when there are
+ * none).  Skipped once st->done (st nullable). */
+int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, const double* rx,
+           double* res_out, const int32_t* fmap, const double* S, const double* lam,
+           double lam0, double lam1, double* out, int out_ext, const nk_cg_state* st,
+           nk_stream_t stream);
 
 /* nk_fdm with the local solves in FP32 (the paper's 32-bit smoothing,
  * PAPER.md:323-325): r, sub, res_out, out stay FP64; S and lam are FP32
  * copies ([E][3][N+3][N+3], [E][3][N+3]). */
-int nk_fdm32(int N, int64_t nelem, const double* r, const double* sub, double* res_out,
-             const int32_t* fmap, const float* S, const float* lam, double lam0, double lam1,
-             double* out, int out_ext, const nk_cg_state* st, nk_stream_t stream);
+int nk_fdm32(int N, int64_t nelem, const double* r, const double* sub, const double* rx,
+             double* res_out, const int32_t* fmap, const float* S, const float* lam,
+             double lam0, double lam1, double* out, int out_ext, const nk_cg_state* st,
+             nk_stream_t stream);
+
+/* out[i] = a[idx[i]] - b[idx[i]] (b nullable): packs the face-inward layer
+ * (r - A e) a neighbour rank's extended boxes need (multi-rank Schwarz). */
+int nk_gather_diff(int64_t n, const int32_t* idx, const double* a, const double* b,
+                   double* out, const nk_cg_state* st, nk_stream_t stream);
 
 /* z = mask * W * src (own points; src extended [E][(N+3)^3] if src_ext) fused
  * with d = a d + b z (d nullable: d := b z not stored) and e = (e_acc ? e : 0)

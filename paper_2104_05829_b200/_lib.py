@@ -96,8 +96,9 @@ _SIGS = {
     "nk_multi_wdot": ([_I64, _I32, _P, _I64, _P, _P, _P, _P, _P], _I32),
     "nk_multi_axpy": ([_I64, _I32, _P, _D, _P, _I64, _P, _P, _P], _I32),
     "nk_vscale": ([_I64, _P, _P, _P, _P], _I32),
-    "nk_fdm": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
-    "nk_fdm32": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
+    "nk_fdm": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
+    "nk_fdm32": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
+    "nk_gather_diff": ([_I64, _P, _P, _P, _P, _P, _P], _I32),
     "nk_schwarz_post": ([_I32, _I64, _P, _I32, _P, _P, _P, _P, _D, _D, _I32, _P, _P], _I32),
 }
 

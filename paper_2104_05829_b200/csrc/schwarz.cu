@@ -90,7 +90,8 @@ struct FdmShape {
 template <int NQE, typename T>
 __global__ void __launch_bounds__(FdmShape<NQE, T>::NT)
 fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict__ sub,
-           double* __restrict__ res_out, const int32_t* __restrict__ fmap,
+           const double* __restrict__ rx, double* __restrict__ res_out,
+           const int32_t* __restrict__ fmap,
            const T* __restrict__ Sg, const T* __restrict__ lamg, double lam0_d,
            double lam1_d, double* __restrict__ out, int out_ext, const nk_cg_state* st) {
   if (st != nullptr && st->done) return;
@@ -167,13 +168,15 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
     }
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
-      v[u] = src[u] >= 0 ? __ldg(r + src[u]) : 0.0;
+      // src >= 0: local point of r (- sub); src <= -2: a value received from
+      // the neighbour rank (already r - sub) at rx[-src - 2]; -1: none
+      v[u] = src[u] >= 0 ? __ldg(r + src[u]) : (src[u] <= -2 ? __ldg(rx - src[u] - 2) : 0.0);
       w[u] = (sub != nullptr && src[u] >= 0) ? __ldg(sub + src[u]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
       const int q = q0 + u * NT + t;
-      if (src[u] >= 0) {
+      if (src[u] != -1) {
         const int f = q / NQ2, ab = q % NQ2, a = ab / NQ + 1, b = ab % NQ + 1;
         const int pos = (f & 1) ? NQE - 1 : 0;
         int idx;
@@ -250,7 +253,8 @@ schwarz_post_kernel(int nq, int64_t n, const double* __restrict__ src, int src_e
 }
 
 template <int NQE, typename T>
-static int launch_fdm(int64_t E, const double* r, const double* sub, double* res_out,
+static int launch_fdm(int64_t E, const double* r, const double* sub, const double* rx,
+                      double* res_out,
                       const int32_t* fmap, const T* S, const T* lam, double lam0,
                       double lam1, double* out, int out_ext, const nk_cg_state* st,
                       cudaStream_t s) {
@@ -265,7 +269,7 @@ static int launch_fdm(int64_t E, const double* r, const double* sub, double* res
     }
     configured = true;
   }
-  fdm_kernel<NQE, T><<<(unsigned)E, FdmShape<NQE, T>::NT, smem, s>>>(E, r, sub, res_out, fmap, S,
+  fdm_kernel<NQE, T><<<(unsigned)E, FdmShape<NQE, T>::NT, smem, s>>>(E, r, sub, rx, res_out, fmap, S,
                                                                     lam, lam0, lam1, out, out_ext,
                                                                     st);
   return check_launch("fdm");
@@ -273,7 +277,7 @@ static int launch_fdm(int64_t E, const double* r, const double* sub, double* res
 
 template <typename T>
 static int fdm_dispatch(int N, int64_t nelem, const double* r, const double* sub,
-                        double* res_out, const int32_t* fmap, const T* Smat, const T* lam,
+                        const double* rx, double* res_out, const int32_t* fmap, const T* Smat, const T* lam,
                         double lam0, double lam1, double* out, int out_ext,
                         const nk_cg_state* st, nk_stream_t stream) {
   if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) {
@@ -290,7 +294,8 @@ static int fdm_dispatch(int N, int64_t nelem, const double* r, const double* sub
   switch (N + 3) {
 #define NK_FDM_CASE(Q) \
   case Q:              \
-    return launch_fdm<Q, T>(nelem, r, sub, res_out, fmap, Smat, lam, lam0, lam1, out, out_ext, st, s);
+    return launch_fdm<Q, T>(nelem, r, sub, rx, res_out, fmap, Smat, lam, lam0, lam1, out, out_ext, \
+                            st, s);
     NK_FDM_CASE(4) NK_FDM_CASE(5) NK_FDM_CASE(6) NK_FDM_CASE(7) NK_FDM_CASE(8) NK_FDM_CASE(9)
     NK_FDM_CASE(10) NK_FDM_CASE(11) NK_FDM_CASE(12) NK_FDM_CASE(13) NK_FDM_CASE(14)
     NK_FDM_CASE(15) NK_FDM_CASE(16) NK_FDM_CASE(17) NK_FDM_CASE(18)
@@ -305,20 +310,47 @@ static int fdm_dispatch(int N, int64_t nelem, const double* r, const double* sub
 
 using namespace nk;
 
-extern "C" int nk_fdm(int N, int64_t nelem, const double* r, const double* sub, double* res_out,
-                      const int32_t* fmap, const double* Smat, const double* lam, double lam0,
-                      double lam1, double* out, int out_ext, const nk_cg_state* st,
-                      nk_stream_t stream) {
-  return fdm_dispatch<double>(N, nelem, r, sub, res_out, fmap, Smat, lam, lam0, lam1, out,
+extern "C" int nk_fdm(int N, int64_t nelem, const double* r, const double* sub,
+                      const double* rx, double* res_out, const int32_t* fmap, const double* Smat,
+                      const double* lam, double lam0, double lam1, double* out, int out_ext,
+                      const nk_cg_state* st, nk_stream_t stream) {
+  return fdm_dispatch<double>(N, nelem, r, sub, rx, res_out, fmap, Smat, lam, lam0, lam1, out,
                               out_ext, st, stream);
 }
 
 extern "C" int nk_fdm32(int N, int64_t nelem, const double* r, const double* sub,
-                        double* res_out, const int32_t* fmap, const float* Smat,
-                        const float* lam, double lam0, double lam1, double* out, int out_ext,
-                        const nk_cg_state* st, nk_stream_t stream) {
-  return fdm_dispatch<float>(N, nelem, r, sub, res_out, fmap, Smat, lam, lam0, lam1, out,
+                        const double* rx, double* res_out, const int32_t* fmap,
+                        const float* Smat, const float* lam, double lam0, double lam1,
+                        double* out, int out_ext, const nk_cg_state* st, nk_stream_t stream) {
+  return fdm_dispatch<float>(N, nelem, r, sub, rx, res_out, fmap, Smat, lam, lam0, lam1, out,
                              out_ext, st, stream);
+}
+
+// out[i] = a[idx[i]] - b[idx[i]] (b nullable): packs the face-inward layer
+// values r - A e a neighbour rank's extended boxes need.
+__global__ void __launch_bounds__(256)
+gather_diff_kernel(int64_t n, const int32_t* __restrict__ idx, const double* __restrict__ a,
+                   const double* __restrict__ b, double* __restrict__ out,
+                   const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int32_t q = __ldg(idx + i);
+    out[i] = b ? __ldg(a + q) - __ldg(b + q) : __ldg(a + q);
+  }
+}
+
+extern "C" int nk_gather_diff(int64_t n, const int32_t* idx, const double* a, const double* b,
+                              double* out, const nk_cg_state* st, nk_stream_t stream) {
+  if (n < 0 || (n > 0 && (!idx || !a || !out))) {
+    set_error("gather_diff: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  if (n == 0) return NK_OK;
+  int64_t g = (n + 255) / 256;
+  if (g > 8 * 148) g = 8 * 148;
+  gather_diff_kernel<<<(unsigned)g, 256, 0, S(stream)>>>(n, idx, a, b, out, st);
+  return check_launch("gather_diff");
 }
 
 extern "C" int nk_schwarz_post(int N, int64_t nelem, const double* src, int src_ext,

@@ -153,13 +153,13 @@ class MultigridHierarchy:
         self.comm = op.comm if (op.comm is not None and op.comm.size > 1) else None
         if self.comm is not None:
             # across ranks: box meshes (each rank rebuilds its own elements at
-            # every order), Jacobi-family smoothing (the Schwarz boxes would
-            # need a second halo) and the iterative coarse solve (the fused
-            # PCG runs over the same halo + all-reduce path)
+            # every order), any smoother (the Schwarz boxes read the neighbour
+            # ranks' face layers from one exchange per smoothing; ASM's
+            # extended gs runs over the ranks) and the iterative coarse solve
+            # (the fused PCG runs over the same halo + all-reduce path)
             if op.mesh.counts is None:
                 raise ContractError("multi-rank p-multigrid needs a box mesh")
-            if smoother not in ("jacobi", "cheby_jac"):
-                raise ContractError("multi-rank p-multigrid smooths with jacobi / cheby_jac")
+
             if coarse == "dense":
                 raise ContractError("the dense coarse solve is single-rank: use coarse='pcg'")
         if not (0.0 < bounds[0] < bounds[1]):
@@ -522,8 +522,11 @@ class MultigridPCG:
             board = False
             if getattr(op.gs, "transport", "p2p") == "ipc":
                 board = self.comm.enable_board(dev)
-            # graph capture needs every exchange on the stream
-            self.use_graph = self.use_graph and (board or self.comm.staging == "device")
+            # graph capture needs every exchange on the stream; the Schwarz
+            # face-layer exchange goes through torch.distributed
+            schwarz = any(lv.sm is not None for lv in self.h.levels)
+            self.use_graph = self.use_graph and (
+                self.comm.staging == "device" or (board and not schwarz))
 
     def _allreduce(self, a, b):
         if self.comm is not None:

@@ -155,8 +155,91 @@ def fdm_1d_batch(D, w, h, left, right, device="cpu"):
     return S, lam
 
 
+def _face_hashes(srt):
+    """Two independent 64-bit polynomial hashes of sorted face id rows."""
+    with np.errstate(over="ignore"):
+        k1 = np.zeros(len(srt), dtype=np.uint64)
+        k2 = np.zeros(len(srt), dtype=np.uint64)
+        for q in range(srt.shape[1]):
+            v = srt[:, q].astype(np.uint64)
+            k1 = k1 * np.uint64(0x9E3779B97F4A7C15) + v
+            k2 = k2 * np.uint64(0xC2B2AE3D27D4EB4F) + (v ^ np.uint64(0x5851F42D4C957F2D))
+    return k1.view(np.int64), k2.view(np.int64)
+
+
+def remote_face_plan(ids, fmap, E, N, comm):
+    """Cross-rank face neighbours of the extended boxes (collective).
+
+    Faces without a local neighbour are matched across ranks by their global
+    id sets (two 64-bit hashes; owner rank = hash mod P, like the gs halo
+    discovery).  For every matched face both ranks list the face points in
+    the same order -- (face hashes, face point global id) -- so rank p's
+    i-th received value is the neighbour's point one layer inside the face at
+    p's i-th listed face point.  Returns (fmap with entries -(2 + slot) for
+    remote sources, {peer: local indices to send}, {peer: receive count},
+    total receive count)."""
+    nq = N + 1
+    P, rank = comm.size, comm.rank
+    ids = np.asarray(ids, dtype=np.int64).reshape(E, nq, nq, nq)
+    loc = np.arange(E * nq ** 3, dtype=np.int64).reshape(E, nq, nq, nq)
+    fmap = fmap.copy()
+    cand = np.argwhere(fmap[:, :, 0, 0] == -1)                      # (e, f)
+    rows_g, rows_in = [], []
+    for e, f in cand:
+        axis, side = _FACE_AXES[f]
+        rows_g.append(ids[e][_face_slice(nq, axis, side)[1:]].reshape(-1))
+        rows_in.append(loc[e][_face_slice(nq, axis, side, True)[1:]].reshape(-1))
+    nc = len(cand)
+    G = np.array(rows_g, dtype=np.int64).reshape(nc, nq * nq)
+    IN = np.array(rows_in, dtype=np.int64).reshape(nc, nq * nq)
+    k1, k2 = _face_hashes(np.sort(G, axis=1)) if nc else (np.zeros(0, np.int64),) * 2
+    owner = (k1.view(np.uint64) % np.uint64(P)).astype(np.int64)
+    parts = [np.stack([k1[owner == q], k2[owner == q], np.flatnonzero(owner == q)], 1).ravel()
+             for q in range(P)]
+    got = comm.alltoallv_int64(parts)
+    # owner side: pair equal keys held by two different ranks
+    recs = [(int(a), int(b), src, int(c)) for src in range(P)
+            for a, b, c in got[src].reshape(-1, 3)]
+    recs.sort()
+    replies = [[] for _ in range(P)]
+    i = 0
+    while i < len(recs):
+        j = i
+        while j < len(recs) and recs[j][:2] == recs[i][:2]:
+            j += 1
+        grp = recs[i:j]
+        if len(grp) == 2 and grp[0][2] != grp[1][2]:
+            (_, _, ra, ca), (_, _, rb, cb) = grp
+            replies[ra] += [ca, rb]
+            replies[rb] += [cb, ra]
+        elif len(grp) > 2:
+            raise ContractError("a face id set is held by more than two element faces")
+        i = j
+    back = comm.alltoallv_int64([np.array(r, dtype=np.int64) for r in replies])
+    matched = np.concatenate([b.reshape(-1, 2) for b in back]) if P else np.zeros((0, 2))
+    send_idx, recv_cnt, entries = {}, {}, {}
+    for c, peer in matched:
+        e, f = cand[c]
+        for a_b in range(nq * nq):
+            entries.setdefault(int(peer), []).append(
+                (int(k1[c]), int(k2[c]), int(G[c, a_b]), int(IN[c, a_b]), int(e), int(f), a_b))
+    off = 0
+    for peer in sorted(entries):
+        lst = sorted(entries[peer])
+        send_idx[peer] = np.array([t[3] for t in lst], dtype=np.int64)
+        recv_cnt[peer] = len(lst)
+        for slot, t in enumerate(lst):
+            e, f, a_b = t[4], t[5], t[6]
+            fmap[e, f, a_b // nq, a_b % nq] = -(2 + off + slot)
+        off += len(lst)
+    return fmap, send_idx, recv_cnt, off
+
+
 class SchwarzSmoother:
-    """z = S r for a PoissonOperator (single rank): kind 'asm' or 'ras';
+    """z = S r for a PoissonOperator: kind 'asm' or 'ras'.  Across ranks the
+    face-inward layers of neighbour ranks are exchanged before each solve, and
+    ASM's extended gs runs over the ranks (the remote sources' global ids are
+    exchanged once at setup);
     precision 64, or 32 (local solves in FP32, fields FP64 -- the paper's
     32-bit smoothing, SmootherConfig.precision SPEC.md:463).
 
@@ -174,9 +257,9 @@ class SchwarzSmoother:
         if precision not in (32, 64):
             raise ContractError(f"precision must be 32 or 64, got {precision!r}")
         self.precision = int(precision)
-        if op.gs.comm is not None and op.gs.comm.size > 1:
-            raise ContractError("multi-rank Schwarz smoothing is not built (the extended "
-                                "boxes would need a second halo)")
+        comm = op.gs.comm
+        self.comm = comm if (comm is not None and comm.size > 1) else None
+
         m = op.mesh
         self.op, self.kind, self.mesh = op, kind, m
         N, E, nq = m.N, m.E, m.nq
@@ -186,11 +269,37 @@ class SchwarzSmoother:
         ids = m.ids.detach().cpu().numpy().astype(np.int64).ravel()
         mask = m.mask.detach().cpu().numpy().reshape(E, nq, nq, nq)
         fmap = face_source_map(ids, E, N)
+        self.send_idx, self.recv_cnt = {}, {}
+        if self.comm is not None:
+            # faces whose neighbour lives on another rank read that rank's
+            # inward layer from a receive buffer (one exchange per smoothing)
+            fmap, sidx, self.recv_cnt, nrecv = remote_face_plan(ids, fmap, E, N, self.comm)
+            self.send_idx = {q: torch.as_tensor(v.astype(np.int32), device=dev)
+                             for q, v in sidx.items()}
+            self.send_buf = {q: torch.zeros(len(v), dtype=torch.float64, device=dev)
+                             for q, v in sidx.items()}
+            self.rx = torch.zeros(max(nrecv, 1), dtype=torch.float64, device=dev)
+            self.recv_slices = {}
+            o = 0
+            for q in sorted(self.recv_cnt):
+                self.recv_slices[q] = self.rx[o:o + self.recv_cnt[q]]
+                o += self.recv_cnt[q]
+            # the global ids of the remote sources (ASM's extended numbering)
+            xdev = dev if self.comm.backend == "nccl" else "cpu"
+            rid = torch.zeros(max(nrecv, 1), dtype=torch.int64, device=xdev)
+            sid = {q: torch.as_tensor(ids[v], device=xdev) for q, v in sidx.items()}
+            ridv, o = {}, 0
+            for q in sorted(self.recv_cnt):
+                ridv[q] = rid[o:o + self.recv_cnt[q]]
+                o += self.recv_cnt[q]
+            self.comm.exchange(sid, ridv)
+            rid = rid.cpu()
+            self.remote_ids = rid.numpy()[:nrecv]
         # side kinds
         kinds = np.empty((E, 6), dtype=np.int64)
         for f, (axis, side) in enumerate(_FACE_AXES):
             masked = np.all(mask[_face_slice(nq, axis, side)].reshape(E, -1) == 0, axis=1)
-            kinds[:, f] = np.where(fmap[:, f, 0, 0] >= 0, _NBR, np.where(masked, _DIR, _NEU))
+            kinds[:, f] = np.where(fmap[:, f, 0, 0] != -1, _NBR, np.where(masked, _DIR, _NEU))
         self.kinds = kinds
         # element lengths (mean distance between opposite faces)
         X = mesh_coordinates(m)
@@ -231,9 +340,12 @@ class SchwarzSmoother:
                 src[tuple(s)] = fmap[:, fi]
             src = src.reshape(-1)
             ext_ids = np.where(src >= 0, ids[np.maximum(src, 0)], 0)
-            self.ext_gs = gs_setup(ext_ids, device=dev)
+            if self.comm is not None:      # remote sources carry the neighbour's ids
+                rem = src <= -2
+                ext_ids[rem] = self.remote_ids[-src[rem] - 2]
+            self.ext_gs = gs_setup(ext_ids, comm=self.comm, device=dev)
             self.buf = torch.zeros(E * nqe ** 3, dtype=torch.float64, device=dev)
-            cnt = torch.as_tensor((src >= 0).astype(np.float64), device=dev)
+            cnt = torch.as_tensor((src != -1).astype(np.float64), device=dev)
             self._gs(self.ext_gs, cnt)
             own = cnt.view(E, nqe, nqe, nqe)[:, 1:nq + 1, 1:nq + 1, 1:nq + 1].reshape(-1)
             self.W = (1.0 / own).contiguous()
@@ -245,8 +357,14 @@ class SchwarzSmoother:
 
     @staticmethod
     def _gs(h, w, st=None):
-        from .gather_scatter import _local
-        _local(h, w, "+", 1, st=st)
+        from .gather_scatter import _halo_exchange, _halo_finish, _halo_start, _local
+        if h.comm is None or h.comm.size == 1:
+            _local(h, w, "+", 1, st=st)
+            return
+        _halo_start(h, w, st=st)
+        _halo_exchange(h)
+        _local(h, w, "+", 1, st=st, part=h.seg_rest)
+        _halo_finish(h, w, "+", st=st)
 
     @property
     def launches(self):
@@ -256,7 +374,15 @@ class SchwarzSmoother:
         """FDM local solves of the extended residual of r - sub (nk_fdm, or
         nk_fdm32 in the 32-bit smoothing mode)."""
         fn = lib().nk_fdm32 if self.precision == 32 else lib().nk_fdm
-        check(fn(self.N, self.E, ptr(r), ptr(sub), ptr(res_out), ptr(self.fmap),
+        rx = None
+        if self.comm is not None:
+            L, s = lib(), stream_ptr()
+            for q, idx in self.send_idx.items():
+                check(L.nk_gather_diff(idx.numel(), ptr(idx), ptr(r), ptr(sub),
+                                       ptr(self.send_buf[q]), ptr(st), s), "gather_diff")
+            self.comm.exchange(self.send_buf, self.recv_slices)
+            rx = self.rx
+        check(fn(self.N, self.E, ptr(r), ptr(sub), ptr(rx), ptr(res_out), ptr(self.fmap),
                            ptr(self.S), ptr(self.lam), float(self.op.lam0), float(self.op.lam1),
                            ptr(out), int(out_ext), ptr(st), stream_ptr()), "fdm")
 
