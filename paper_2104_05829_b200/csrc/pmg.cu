@@ -123,6 +123,129 @@ dense_matvec_kernel(int64_t n, const double* __restrict__ A, const double* __res
   }
 }
 
+// Specialised transfer for the order pairs the p-multigrid uses (pmg_orders:
+// N+1 <-> N/2+1 and N/2+1 <-> 2): one element per CTA, max(NI, NO)^2 threads,
+// each contraction a per-thread line in registers with the transfer matrix in
+// the constant bank (compile-time indices), odd-pitched shared rows.  The
+// generic kernel above runs every other pair.
+template <int NI, int NO>
+struct TransferMT {
+  double m[NO * NI];
+};
+
+template <int NI, int NO>
+__global__ void __launch_bounds__((NI > NO ? NI * NI : NO * NO))
+interp3_fast(const __grid_constant__ TransferMT<NI, NO> M, const double* __restrict__ in,
+             const double* __restrict__ sub, const double* __restrict__ wt,
+             const uint8_t* __restrict__ mask, double* __restrict__ out, int accumulate,
+             const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  constexpr int TH = NI > NO ? NI * NI : NO * NO;
+  constexpr int PI = NI | 1, PO = NO | 1;         // odd row pitches
+  constexpr int SA = NI * NI * PI > NI * NO * PO ? NI * NI * PI : NI * NO * PO;
+  extern __shared__ double ismem[];
+  double* v = ismem;                               // [k][j][i]
+  double* t2 = ismem;                              // [k][b][a]  (v is dead by then)
+  double* t1 = ismem + SA;                         // [k][j][a]
+  const int64_t e = blockIdx.x;
+  const int t = threadIdx.x;
+  const int64_t ib = e * NI * NI * NI, ob = e * NO * NO * NO;
+  for (int q = t; q < NI * NI * NI; q += TH) {
+    double x = __ldg(in + ib + q);
+    if (sub) x -= __ldg(sub + ib + q);
+    if (wt) x *= __ldg(wt + ib + q);
+    v[(q / NI) * PI + q % NI] = x;
+  }
+  __syncthreads();
+  if (t < NI * NI) {                               // i -> a on line (k, j) = t
+    double x[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) x[i] = v[t * PI + i];
+#pragma unroll
+    for (int a = 0; a < NO; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) acc = fma(M.m[a * NI + i], x[i], acc);
+      t1[t * PO + a] = acc;
+    }
+  }
+  __syncthreads();
+  if (t < NI * NO) {                               // j -> b on line (k, a)
+    const int k = t / NO, a = t % NO;
+    double x[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) x[j] = t1[(k * NI + j) * PO + a];
+#pragma unroll
+    for (int b = 0; b < NO; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NI; ++j) acc = fma(M.m[b * NI + j], x[j], acc);
+      t2[(k * NO + b) * PO + a] = acc;
+    }
+  }
+  __syncthreads();
+  if (t < NO * NO) {                               // k -> c on line (b, a)
+    const int b = t / NO, a = t % NO;
+    double x[NI];
+#pragma unroll
+    for (int k = 0; k < NI; ++k) x[k] = t2[(k * NO + b) * PO + a];
+#pragma unroll
+    for (int c = 0; c < NO; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < NI; ++k) acc = fma(M.m[c * NI + k], x[k], acc);
+      const int64_t o = ob + (c * NO + b) * NO + a;
+      if (mask && !mask[o]) acc = 0.0;
+      out[o] = accumulate ? out[o] + acc : acc;
+    }
+  }
+}
+
+template <int NI, int NO>
+static int launch_interp_fast(int64_t nelem, const double* Mh, const double* in,
+                              const double* sub, const double* wt, const uint8_t* mask,
+                              double* out, int accumulate, const nk_cg_state* st,
+                              cudaStream_t s) {
+  TransferMT<NI, NO> T;
+  for (int q = 0; q < NO * NI; ++q) T.m[q] = Mh[q];
+  constexpr int TH = NI > NO ? NI * NI : NO * NO;
+  constexpr int PI = NI | 1, PO = NO | 1;
+  constexpr int SA = NI * NI * PI > NI * NO * PO ? NI * NI * PI : NI * NO * PO;
+  constexpr size_t smem = sizeof(double) * (SA + NI * NI * PO);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t err = cudaFuncSetAttribute(interp3_fast<NI, NO>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) {
+      set_error("interp3: smem attribute: %s", cudaGetErrorString(err));
+      return NK_ERR_CUDA;
+    }
+    configured = true;
+  }
+  interp3_fast<NI, NO><<<(unsigned)nelem, TH, smem, s>>>(T, in, sub, wt, mask, out, accumulate,
+                                                         st);
+  return check_launch("interp3_fast");
+}
+
+// the pmg_orders pairs (N = 1..15): N+1 <-> N/2+1 and N/2+1 <-> 2
+#define NK_INTERP_PAIRS(X) \
+  X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8) X(3, 2) X(3, 5) X(3, 6) X(4, 2) X(4, 7) \
+  X(4, 8) X(5, 2) X(5, 3) X(5, 9) X(5, 10) X(6, 2) X(6, 3) X(6, 11) X(6, 12) X(7, 2) X(7, 4) \
+  X(7, 13) X(7, 14) X(8, 2) X(8, 4) X(8, 15) X(8, 16) X(9, 5) X(10, 5) X(11, 6) X(12, 6) \
+  X(13, 7) X(14, 7) X(15, 8) X(16, 8)
+
+static int interp_fast_dispatch(int ni, int no, int64_t nelem, const double* M, const double* in,
+                                const double* sub, const double* wt, const uint8_t* mask,
+                                double* out, int accumulate, const nk_cg_state* st,
+                                cudaStream_t s) {
+#define NK_IP_CASE(A, B)                                                                   \
+  if (ni == A && no == B)                                                                  \
+    return launch_interp_fast<A, B>(nelem, M, in, sub, wt, mask, out, accumulate, st, s);
+  NK_INTERP_PAIRS(NK_IP_CASE)
+#undef NK_IP_CASE
+  return -1;
+}
+
 }  // namespace nk
 
 using namespace nk;
@@ -139,6 +262,11 @@ extern "C" int nk_interp3(int ni, int no, int64_t nelem, const double* M, const 
   if (nelem > 0x7fffffffLL) {
     set_error("interp3: too many elements");
     return NK_ERR_INVALID;
+  }
+  {
+    const int rc = interp_fast_dispatch(ni, no, nelem, M, in, sub, wt, mask, out, accumulate, st,
+                                        S(stream));
+    if (rc >= 0) return rc;
   }
   TransferM T;
   for (int q = 0; q < no * ni; ++q) T.m[q] = M[q];
