@@ -11,6 +11,8 @@ element (RAS).
 
 Per application (all libnekb200 launches on the current stream, CUDA-graph
 capturable, skipped once the PCG state says done):
+  [multi-rank]      nk_gather_diff packs r (- A e) at the face-inward layers
+                    neighbour ranks need; one pairwise exchange;
   nk_fdm            gather r (- A e) on the extended boxes, 6 tensor
                     contractions + inverse spectrum, write the extended (ASM)
                     or own-point (RAS) solution;
@@ -259,7 +261,6 @@ class SchwarzSmoother:
         self.precision = int(precision)
         comm = op.gs.comm
         self.comm = comm if (comm is not None and comm.size > 1) else None
-
         m = op.mesh
         self.op, self.kind, self.mesh = op, kind, m
         N, E, nq = m.N, m.E, m.nq
