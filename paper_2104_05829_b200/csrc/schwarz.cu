@@ -132,10 +132,7 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
     }
   }
   for (int q = t; q < 3 * NQE; q += NT) Ls[q] = __ldg(lamg + e * 3 * NQE + q);
-  for (int q = t; q < NQE * NQE * NQE; q += NT) {
-    const int i = q % NQE, j = (q / NQE) % NQE, k = q / (NQE * NQE);
-    A[k * PS + j * LS + i] = T(0);
-  }
+  for (int q = t; q < F::A_SZ; q += NT) A[q] = T(0);   // whole padded box, no index math
   __syncthreads();
   // own points (coalesced); res_out = r - sub on them
   for (int q0 = 0; q0 < NQ3; q0 += CH * NT) {
@@ -210,10 +207,12 @@ fdm_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict
   fdm_line2<NQE, 1, T>(A + h0 * PS + o0 * LS, A + h1 * PS + o1 * LS, Sb, nullptr, 0, 0, 0, 0);
   __syncthreads();
   if (out_ext) {
+    // extended rows (k, j): NQE contiguous values each
     double* o = out + e * NQE * NQE * NQE;
-    for (int q = t; q < NQE * NQE * NQE; q += NT) {
-      const int i = q % NQE, j = (q / NQE) % NQE, k = q / (NQE * NQE);
-      o[q] = (double)A[k * PS + j * LS + i];
+    for (int rw = t; rw < NQE * NQE; rw += NT) {
+      const T* srow = A + (rw / NQE) * PS + (rw % NQE) * LS;
+#pragma unroll
+      for (int i = 0; i < NQE; ++i) o[rw * NQE + i] = (double)srow[i];
     }
   } else {
     for (int q = t; q < NQ3; q += NT) {
