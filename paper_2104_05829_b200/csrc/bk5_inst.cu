@@ -221,6 +221,20 @@ extern "C" int NK_CAT(nk_bk5_pcg_nq, NK_BK5_NQ)(int64_t nlist, const int32_t* el
   constexpr int NQ = NK_BK5_NQ;
   constexpr int EPB = PencilDefault<NQ>::EPB;
   constexpr int MINB = NQ == 8 ? 10 : PencilDefault<NQ>::MINB;  // ~100 regs at NQ = 8
+  if constexpr (NQ == 2) {   // element per thread (the order-1 coarse level)
+    const int64_t nb = (nlist + kN1Threads - 1) / kN1Threads;
+    if (nblocks) {
+      *nblocks = nb;
+      return NK_OK;
+    }
+    if (nb == 0) return NK_OK;
+    DParam<2> Dp;
+    for (int q = 0; q < 4; ++q) Dp.d[q] = D[q];
+    bk5_n1_pcg<2><<<(unsigned)nb, kN1Threads, 0, s>>>(nlist, elist, Dp, G, p, w, lam0, B, lam1,
+                                                   mask, x, r, invD, st, partials, part_base,
+                                                   reduce_count, hist);
+    return check_launch("bk5_n1_pcg");
+  }
   if constexpr (NQ == 8) {
     if (nk_bk5_variant_get() != 3) {  // auto / 4: TMA pipeline
       if (nblocks) {

@@ -239,4 +239,133 @@ static int launch_pencil_pcg(int64_t nlist, const int32_t* elist, const double* 
   return check_launch("bk5_pencil_pcg");
 }
 
+
+// N = 1 (NQ = 2, 8 points per element): the pencil machinery (shared
+// transposes, barriers) costs more than the element's arithmetic, so one
+// THREAD owns one element -- p, r, invD, x, w as four 16-B loads each and
+// G as 24 -- with the same prologue / epilogue semantics as bk5_pencil_pcg.
+// Used by the iterative coarse solve of the p-multigrid (order-1 level).
+constexpr int kN1Threads = 128;
+
+template <int NQ_ONE>   // = 2; a template so every translation unit may include it
+__global__ void __launch_bounds__(kN1Threads)
+bk5_n1_pcg(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<2> D,
+           const double* __restrict__ G, double* __restrict__ p, double* __restrict__ w,
+           double lam0, const double* __restrict__ B, double lam1,
+           const uint8_t* __restrict__ mask, double* __restrict__ x,
+           const double* __restrict__ r, const double* __restrict__ invD, nk_cg_state* st,
+           double* __restrict__ partials, int64_t part_base, int64_t reduce_count,
+           double* __restrict__ hist) {
+  __shared__ double red[32];
+  if (st->done) return;
+  const int it = st->iter;
+  const bool conv = it > 0 && st->rr <= st->thresh2;
+  const bool stop = it > 0 && (conv || it >= st->max_iter);
+  const double alpha_prev = st->alpha;
+  const double rz = st->rz;
+  const double beta = it == 0 ? 0.0 : (st->flexible ? (-alpha_prev * st->zap) / rz
+                                                    : st->rz_new / rz);
+  const int t = threadIdx.x;
+  const int64_t slot = (int64_t)blockIdx.x * kN1Threads + t;
+  const bool active = slot < nlist;
+  const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
+  const int64_t off = e * 8;
+  double dot = 0.0;
+  if (active) {
+    double pv[8];
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(p + off + q);
+      pv[q] = v.x;
+      pv[q + 1] = v.y;
+    }
+    if (it > 0) {
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        double2 xv = *reinterpret_cast<const double2*>(x + off + q);
+        xv.x = fma(alpha_prev, pv[q], xv.x);
+        xv.y = fma(alpha_prev, pv[q + 1], xv.y);
+        *reinterpret_cast<double2*>(x + off + q) = xv;
+      }
+      if (!stop) {
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          const double2 rv = __ldg(reinterpret_cast<const double2*>(r + off + q));
+          const double2 dv = __ldg(reinterpret_cast<const double2*>(invD + off + q));
+          pv[q] = fma(beta, pv[q], dv.x * rv.x);
+          pv[q + 1] = fma(beta, pv[q + 1], dv.y * rv.y);
+          *reinterpret_cast<double2*>(p + off + q) = make_double2(pv[q], pv[q + 1]);
+        }
+      }
+    }
+    if (!stop) {
+      // point q = k*4 + j*2 + i;  d/dr along i, d/ds along j, d/dt along k
+      double ur[8], us[8], ut[8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int q = k * 4 + j * 2 + i;
+            ur[q] = D.d[i * 2 + 0] * pv[k * 4 + j * 2 + 0] + D.d[i * 2 + 1] * pv[k * 4 + j * 2 + 1];
+            us[q] = D.d[j * 2 + 0] * pv[k * 4 + 0 * 2 + i] + D.d[j * 2 + 1] * pv[k * 4 + 1 * 2 + i];
+            ut[q] = D.d[k * 2 + 0] * pv[0 * 4 + j * 2 + i] + D.d[k * 2 + 1] * pv[1 * 4 + j * 2 + i];
+          }
+      const double* ge = G + e * 48;
+      double g[48];
+#pragma unroll
+      for (int q = 0; q < 48; q += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(ge + q));
+        g[q] = v.x;
+        g[q + 1] = v.y;
+      }
+      double gr[8], gs[8], gt[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        gr[q] = g[q] * ur[q] + g[8 + q] * us[q] + g[16 + q] * ut[q];
+        gs[q] = g[8 + q] * ur[q] + g[24 + q] * us[q] + g[32 + q] * ut[q];
+        gt[q] = g[16 + q] * ur[q] + g[32 + q] * us[q] + g[40 + q] * ut[q];
+      }
+      double res[8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int q = k * 4 + j * 2 + i;
+            double v = D.d[0 * 2 + i] * gr[k * 4 + j * 2 + 0] + D.d[1 * 2 + i] * gr[k * 4 + j * 2 + 1];
+            v += D.d[0 * 2 + j] * gs[k * 4 + 0 * 2 + i] + D.d[1 * 2 + j] * gs[k * 4 + 1 * 2 + i];
+            v += D.d[0 * 2 + k] * gt[0 * 4 + j * 2 + i] + D.d[1 * 2 + k] * gt[1 * 4 + j * 2 + i];
+            v *= lam0;
+            if (B != nullptr) v = fma(lam1 * __ldg(B + off + q), pv[q], v);
+            if (mask != nullptr) v = mask[off + q] ? v : 0.0;
+            res[q] = v;
+            dot = fma(pv[q], v, dot);
+          }
+#pragma unroll
+      for (int q = 0; q < 8; q += 2)
+        *reinterpret_cast<double2*>(w + off + q) = make_double2(res[q], res[q + 1]);
+    }
+  }
+  double vv[1] = {dot};
+  block_sum<1>(vv, red);
+  if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+  if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
+    double sres[1];
+    reduce_partials<1>(partials, reduce_count, 0, sres, red);
+    if (t == 0) {
+      if (it > 0 && hist) hist[it] = sqrt(st->rr);
+      if (stop) {
+        st->converged = conv ? 1 : 0;
+        st->done = 1;
+      } else {
+        st->pAp = sres[0];
+        if (it > 0) st->rz = st->rz_new;
+      }
+    }
+  }
+}
+
 }  // namespace nk

@@ -477,3 +477,24 @@ def test_edge_fused_pcg_zero_rhs_and_all_dirichlet():
     r1 = nk.pcg(op1, nk.JacobiPreconditioner(op1),
                 torch.zeros(8, dtype=torch.float64, device="cuda"))
     assert r1.iterations == 0
+
+
+@pytest.mark.parametrize("bc,lam1", [("dirichlet", 0.0), ("periodic", 2.0)])
+def test_fused_pcg_order_one_element_per_thread(bc, lam1):
+    """N = 1 runs the element-per-thread fused step (bk5_n1_pcg, the
+    iterative coarse solve's kernel): iterations within +-1 of the oracle,
+    same solution."""
+    m, o = both_meshes((6, 5, 4), 1, bc=bc)
+    op = nk.PoissonOperator(m, lam1=lam1)
+    D, G = o.basis.diff, o.G
+    mask = o.mask.ravel()
+    sh = (o.G.shape[0],) + o.G.shape[2:]
+    A = lambda v: mask * ogs.gs_op(o.ids, oop.bk5(D, G, v.reshape(sh), 1.0, o.B, lam1).ravel())
+    inv = mask / ogs.gs_op(o.ids, oop.local_diagonal(D, G, 1.0, o.B, lam1).ravel())
+    rng = np.random.default_rng(11)
+    b = mask * ogs.gs_op(o.ids, rng.standard_normal(o.ids.size))
+    ref = osol.pcg(A, lambda r: inv * r, b, tol=1e-9, max_iter=2000,
+                   weights=1.0 / ogs.multiplicity(o.ids))
+    res = nk.pcg(op, nk.JacobiPreconditioner(op), dev(b), tol=1e-9, max_iter=2000)
+    assert res.converged and abs(res.iterations - ref.iterations) <= 1
+    assert np.max(np.abs(res.x.cpu().numpy() - ref.x)) < 1e-7 * np.max(np.abs(ref.x))
