@@ -100,3 +100,65 @@ def test_distributed_gs_equals_global_oracle(world, counts, N, bc):
         for p in nb[q]:
             assert q in nb[p]
         assert res[q]["nb"] + res[q]["ni"] == len(res[q]["mine"])
+
+
+def _face_worker(rank, world, port, outdir, counts, N, bc):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import mesh as om
+        from paper_2104_05829_b200.distributed import RankComm
+        from paper_2104_05829_b200.partition import rcb
+        from paper_2104_05829_b200.schwarz import face_source_map, remote_face_plan
+        g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, bc=bc)
+        nq3 = (N + 1) ** 3
+        part = rcb(g.xyz.reshape(3, g.E, -1).mean(axis=2).T, world)
+        mine = np.flatnonzero(part == rank)
+        ids = g.ids.reshape(g.E, nq3)[mine].ravel()
+        comm = RankComm(transport="p2p")
+        fm = face_source_map(ids, len(mine), N)
+        fm, sidx, rcnt, nrecv = remote_face_plan(ids, fm, len(mine), N, comm)
+        # exchange the GLOBAL index of every sent point, as the runtime
+        # exchange does with values: the receiver can resolve remote slots
+        gidx = (mine[:, None] * nq3 + np.arange(nq3)[None, :]).ravel()
+        sends = {q: torch.as_tensor(gidx[v]) for q, v in sidx.items()}
+        recv = torch.zeros(max(nrecv, 1), dtype=torch.int64)
+        rv, o = {}, 0
+        for q in sorted(rcnt):
+            rv[q] = recv[o:o + rcnt[q]]
+            o += rcnt[q]
+        comm.exchange(sends, rv)
+        np.savez(os.path.join(outdir, f"f{rank}.npz"), mine=mine, fm=fm,
+                 recv=recv.numpy()[:nrecv])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,counts,bc", [(2, (4, 3, 2), "dirichlet"),
+                                             (4, (4, 4, 2), "periodic")])
+def test_remote_face_plan_matches_single_process(world, counts, bc):
+    """Multi-rank Schwarz setup (schwarz.remote_face_plan): after matching
+    faces across ranks, every extended-box source -- local or received --
+    is the same global point the single-process face map names."""
+    import torch.multiprocessing as mp
+    from oracle import mesh as om
+    from paper_2104_05829_b200.schwarz import face_source_map
+    N = 3
+    nq3 = (N + 1) ** 3
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_face_worker, args=(world, _free_port(), d, counts, N, bc), nprocs=world,
+                 join=True)
+        res = [np.load(os.path.join(d, f"f{r}.npz")) for r in range(world)]
+    g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, bc=bc)
+    ref = face_source_map(g.ids, g.E, N)               # global local-index map
+    n_remote = 0
+    for r in res:
+        mine, fm, recv = r["mine"], r["fm"], r["recv"]
+        loc2glob = (mine[:, None] * nq3 + np.arange(nq3)[None, :]).ravel()
+        got = np.where(fm >= 0, loc2glob[np.maximum(fm, 0)],
+                       np.where(fm <= -2, recv[np.maximum(-fm - 2, 0)], -1))
+        assert np.array_equal(got, ref[mine])
+        n_remote += int((fm <= -2).sum())
+    assert n_remote > 0
