@@ -129,6 +129,20 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
     return NK_ERR_INVALID;
   }
   cudaStream_t s = S(stream);
+  // 3-component batches: the batched pencil3 kernel (G read once) is
+  // issue-bound; three scalar launches (G read three times) measured faster
+  // at every order but N = 7 (scripts/helm3_compare.py: N = 5 / 9 batched
+  // 1.06x / 1.08-1.16x slower, N = 7 0.96x), so auto runs the scalar kernel
+  // per component there.
+  if (ncomp == 3 && nk_bk5_variant_get() == 0 && N != 7 && st == nullptr) {
+    for (int c = 0; c < 3; ++c) {
+      int rc = kslab_table[N](1, n, elem_list, D, G, u + c * comp_stride, w + c * comp_stride,
+                              lam0, B, lam1, comp_stride, mask, nullptr, nullptr, 0, 0, s,
+                              nullptr, g_cfg, g_pf, kvariant_for(N));
+      if (rc != NK_OK) return rc;
+    }
+    return NK_OK;
+  }
   if (use_bulk(N, ncomp))
     return nk_bk5_bulk_launch(N, n, elem_list, D, G, u, w, lam0, B, lam1, mask, st, partials,
                               part_base, reduce_count, s, nullptr, 0);

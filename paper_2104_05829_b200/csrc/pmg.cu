@@ -107,14 +107,30 @@ dense_matvec_kernel(int64_t n, const double* __restrict__ A, const double* __res
     const double* a = A + row * n;
     double s = 0.0;
     if ((n & 1) == 0) {
+      // four independent 16-B row loads in flight per lane (the matrix is
+      // streamed once per V-cycle: memory-level parallelism is the limiter);
+      // fixed association (s0 + s1) + (s2 + s3) keeps the sum deterministic
       const double2* a2 = reinterpret_cast<const double2*>(a);
       const double2* x2 = reinterpret_cast<const double2*>(x);
-      for (int64_t c = lane; c < (n >> 1); c += 32) {
+      const int64_t n2 = n >> 1;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int64_t c = lane;
+      for (; c + 96 < n2; c += 128) {
+        const double2 a0 = __ldcs(a2 + c), a1 = __ldcs(a2 + c + 32);
+        const double2 a2v = __ldcs(a2 + c + 64), a3 = __ldcs(a2 + c + 96);
+        const double2 x0 = __ldg(x2 + c), x1 = __ldg(x2 + c + 32);
+        const double2 x2v = __ldg(x2 + c + 64), x3 = __ldg(x2 + c + 96);
+        s0 = fma(a0.y, x0.y, fma(a0.x, x0.x, s0));
+        s1 = fma(a1.y, x1.y, fma(a1.x, x1.x, s1));
+        s2 = fma(a2v.y, x2v.y, fma(a2v.x, x2v.x, s2));
+        s3 = fma(a3.y, x3.y, fma(a3.x, x3.x, s3));
+      }
+      for (; c < n2; c += 32) {
         const double2 av = __ldcs(a2 + c);
         const double2 xv = __ldg(x2 + c);
-        s = fma(av.x, xv.x, s);
-        s = fma(av.y, xv.y, s);
+        s0 = fma(av.y, xv.y, fma(av.x, xv.x, s0));
       }
+      s = (s0 + s1) + (s2 + s3);
     } else {
       for (int64_t c = lane; c < n; c += 32) s = fma(__ldcs(a + c), __ldg(x + c), s);
     }
