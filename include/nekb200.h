@@ -208,6 +208,19 @@ int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t* nsegs,
 int nk_gs_plan_build(const int64_t* ids, int64_t n, int32_t* perm, int32_t* seg_start,
                      int64_t* nseg, int64_t* nperm);
 
+/* Library-owned gs handle (SPEC.md:184-200 GatherScatterHandle, one rank):
+ * built from the canonical CSR of nk_gs_plan_build [host perm, seg_start],
+ * re-packed by multiplicity class on the device.  nk_gs_apply runs the
+ * same bit-exact canonical fold as nk_gs_op / nk_gs_op_classes (the SURVEY
+ * sketch's nk_gs_op(handle, ...)); handles are not thread-safe and must be
+ * destroyed with nk_gs_destroy. */
+typedef struct nk_gs nk_gs;
+int nk_gs_create(const int32_t* perm, const int32_t* seg_start, int64_t nseg, int64_t nperm,
+                 nk_gs** out);
+int nk_gs_apply(nk_gs* h, double* w, int op, int ncomp, int64_t comp_stride,
+                const nk_cg_state* st, nk_stream_t stream);
+int nk_gs_destroy(nk_gs* h);
+
 /* dst[i] = src[idx[i]] for i < n  (halo pack) */
 int nk_gather(int64_t n, const int32_t* idx, const double* src, double* dst,
               const nk_cg_state* st, nk_stream_t stream);

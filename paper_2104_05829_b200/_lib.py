@@ -72,6 +72,9 @@ _SIGS = {
     "nk_gs_op_classes": ([_I32, _P, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
     "nk_gs_plan_build": ([_P, _I64, _P, _P, _P, _P], _I32),
     "nk_gather": ([_I64, _P, _P, _P, _P, _P], _I32),
+    "nk_gs_create": ([_P, _P, _I64, _I64, _P], _I32),
+    "nk_gs_apply": ([_P, _P, _I32, _I32, _I64, _P, _P], _I32),
+    "nk_gs_destroy": ([_P], _I32),
     "nk_halo_combine": ([_I64, _P, _P, _P, _P, _P, _P, _I32, _P, _P], _I32),
     "nk_ipc_handle_size": ([], _I32),
     "nk_ipc_alloc": ([_I64, _P, _P], _I32),

@@ -270,3 +270,117 @@ extern "C" int nk_gs_plan_build(const int64_t* ids, int64_t n, int32_t* perm, in
   *nperm = np;
   return NK_OK;
 }
+
+// ------------------------------------------------------------ gs handle
+// Library-owned plan (SPEC.md:184-200's GatherScatterHandle for one rank):
+// the canonical CSR re-packed by multiplicity class on the device, so a C
+// caller needs no host-side re-packing -- nk_gs_create / nk_gs_apply /
+// nk_gs_destroy.
+struct nk_gs {
+  int nclass = 0;
+  int32_t sizes[NK_GS_MAX_CLASSES];
+  int64_t nsegs[NK_GS_MAX_CLASSES];
+  int32_t* mem[NK_GS_MAX_CLASSES];
+  int64_t nrest = 0;
+  int32_t* rest_seg = nullptr;
+  int32_t* rest_idx = nullptr;
+  int64_t nseg = 0, nperm = 0;
+};
+
+static void gs_free(nk_gs* h) {
+  if (!h) return;
+  for (int c = 0; c < h->nclass; ++c) cudaFree(h->mem[c]);
+  cudaFree(h->rest_seg);
+  cudaFree(h->rest_idx);
+  delete h;
+}
+
+extern "C" int nk_gs_create(const int32_t* perm, const int32_t* seg_start, int64_t nseg,
+                            int64_t nperm, nk_gs** out) {
+  if (!out || nseg < 0 || nperm < 0 || (nseg > 0 && (!perm || !seg_start))) {
+    set_error("gs_create: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  *out = nullptr;
+  nk_gs* h = new nk_gs();
+  h->nseg = nseg;
+  h->nperm = nperm;
+  // classes: distinct segment sizes <= 32, ascending, at most 16; the rest CSR
+  std::vector<int> sizes_present;
+  for (int64_t s = 0; s < nseg; ++s) {
+    const int M = seg_start[s + 1] - seg_start[s];
+    if (M >= 1 && M <= 32 &&
+        std::find(sizes_present.begin(), sizes_present.end(), M) == sizes_present.end())
+      sizes_present.push_back(M);
+  }
+  std::sort(sizes_present.begin(), sizes_present.end());
+  if ((int)sizes_present.size() > NK_GS_MAX_CLASSES) sizes_present.resize(NK_GS_MAX_CLASSES);
+  std::vector<int32_t> rest_seg{0}, rest_idx;
+  std::vector<std::vector<int32_t>> mems(sizes_present.size());
+  for (int64_t s = 0; s < nseg; ++s) {
+    const int a = seg_start[s], M = seg_start[s + 1] - a;
+    auto it = std::find(sizes_present.begin(), sizes_present.end(), M);
+    if (it == sizes_present.end()) {
+      for (int m = 0; m < M; ++m) rest_idx.push_back(perm[a + m]);
+      rest_seg.push_back((int32_t)rest_idx.size());
+      continue;
+    }
+    const int c = (int)(it - sizes_present.begin());
+    int Mp = 1;
+    while (Mp < M) Mp <<= 1;
+    for (int m = 0; m < Mp; ++m) mems[c].push_back(m < M ? perm[a + m] : -1);
+  }
+  int rc = NK_OK;
+  for (size_t c = 0; c < sizes_present.size() && rc == NK_OK; ++c) {
+    int Mp = 1;
+    while (Mp < sizes_present[c]) Mp <<= 1;
+    h->sizes[c] = sizes_present[c];
+    h->nsegs[c] = (int64_t)mems[c].size() / Mp;
+    h->mem[c] = nullptr;
+    if (cudaMalloc(&h->mem[c], mems[c].size() * sizeof(int32_t)) != cudaSuccess ||
+        cudaMemcpy(h->mem[c], mems[c].data(), mems[c].size() * sizeof(int32_t),
+                   cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = NK_ERR_CUDA;
+    h->nclass = (int)c + 1;
+  }
+  h->nrest = (int64_t)rest_seg.size() - 1;
+  if (rc == NK_OK && h->nrest > 0) {
+    if (cudaMalloc(&h->rest_seg, rest_seg.size() * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->rest_idx, rest_idx.size() * sizeof(int32_t)) != cudaSuccess ||
+        cudaMemcpy(h->rest_seg, rest_seg.data(), rest_seg.size() * sizeof(int32_t),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(h->rest_idx, rest_idx.data(), rest_idx.size() * sizeof(int32_t),
+                   cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = NK_ERR_CUDA;
+  }
+  if (rc != NK_OK) {
+    set_error("gs_create: device allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
+    gs_free(h);
+    return rc;
+  }
+  *out = h;
+  return NK_OK;
+}
+
+extern "C" int nk_gs_apply(nk_gs* h, double* w, int op, int ncomp, int64_t comp_stride,
+                           const nk_cg_state* st, nk_stream_t stream) {
+  if (!h) {
+    set_error("gs_apply: null handle");
+    return NK_ERR_INVALID;
+  }
+  if (h->nclass > 0) {
+    const int32_t* ptrs[NK_GS_MAX_CLASSES];
+    for (int c = 0; c < h->nclass; ++c) ptrs[c] = h->mem[c];
+    int rc = nk_gs_op_classes(h->nclass, h->sizes, h->nsegs, ptrs, w, op, ncomp, comp_stride,
+                              st, stream);
+    if (rc != NK_OK) return rc;
+  }
+  if (h->nrest > 0)
+    return nk_gs_op(h->nrest, h->rest_seg, h->rest_idx, w, op, ncomp, comp_stride, st, stream);
+  return NK_OK;
+}
+
+extern "C" int nk_gs_destroy(nk_gs* h) {
+  gs_free(h);
+  return NK_OK;
+}

@@ -498,3 +498,37 @@ def test_fused_pcg_order_one_element_per_thread(bc, lam1):
     res = nk.pcg(op, nk.JacobiPreconditioner(op), dev(b), tol=1e-9, max_iter=2000)
     assert res.converged and abs(res.iterations - ref.iterations) <= 1
     assert np.max(np.abs(res.x.cpu().numpy() - ref.x)) < 1e-7 * np.max(np.abs(ref.x))
+
+
+def test_gs_handle_c_api_bit_exact():
+    """nk_gs_create / nk_gs_apply / nk_gs_destroy (the library-owned handle a
+    C caller uses): bit-exact against the oracle's canonical fold, including
+    multiplicities > 32 (the CSR remainder) and more than 16 size classes."""
+    import ctypes
+    from paper_2104_05829_b200._lib import check, lib
+    L = lib()
+    rng = np.random.default_rng(7)
+    ids = np.concatenate([np.repeat(np.arange(1, 200), 2), np.repeat(np.arange(200, 260), 3),
+                          np.repeat([300], 40), np.repeat([301], 33),
+                          np.concatenate([np.repeat(400 + k, k) for k in range(2, 26)]),
+                          np.zeros(50, np.int64), np.arange(1000, 1100)]).astype(np.int64)
+    ids = ids[rng.permutation(len(ids))]
+    n = len(ids)
+    perm = np.zeros(n, np.int32)
+    seg = np.zeros(n // 2 + 2, np.int32)
+    ns, npm = ctypes.c_int64(), ctypes.c_int64()
+    check(L.nk_gs_plan_build(ids.ctypes.data, n, perm.ctypes.data, seg.ctypes.data,
+                             ctypes.byref(ns), ctypes.byref(npm)), "plan")
+    h = ctypes.c_void_p()
+    check(L.nk_gs_create(perm.ctypes.data, seg.ctypes.data, ns.value, npm.value,
+                         ctypes.byref(h)), "gs_create")
+    try:
+        for op in ("+", "min", "max", "*"):
+            w = rng.standard_normal(n)
+            wd = torch.as_tensor(w.copy(), device="cuda")
+            from paper_2104_05829_b200._lib import OP_CODES
+            check(L.nk_gs_apply(h, wd.data_ptr(), OP_CODES[op], 1, n, None,
+                                torch.cuda.current_stream().cuda_stream), "gs_apply")
+            assert np.array_equal(wd.cpu().numpy(), ogs.gs_op(ids, w, op)), op
+    finally:
+        check(L.nk_gs_destroy(h), "gs_destroy")
