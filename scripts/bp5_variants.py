@@ -25,3 +25,16 @@ for v in (0, 3):
     print(json.dumps({"variant": v, "ms_per_iter": round(min(ts), 4),
                       "breakdown": {k: round(x, 4) for k, x in s.profile_iteration().items()}}))
 L.nk_bk5_set_variant(0)
+# parity across variants: one converged solve each, same iterations / answer
+xs = {}
+for v in (0, 3):
+    L.nk_bk5_set_variant(v)
+    op = nk.PoissonOperator(m)
+    s = nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-8, max_iter=2000, chunk=16)
+    b = torch.ones(m.n_local, dtype=torch.float64, device="cuda") * m.mask.reshape(-1).to(torch.float64)
+    r = s.solve(b)
+    xs[v] = (r.iterations, r.x.clone())
+L.nk_bk5_set_variant(0)
+it0, x0 = xs[0]
+print(json.dumps({"iterations": {k: v[0] for k, v in xs.items()},
+                  "max_rel_dx": {k: float((v[1] - x0).abs().max() / x0.abs().max()) for k, v in xs.items()}}))
