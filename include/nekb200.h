@@ -201,6 +201,14 @@ int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t* nsegs,
                      const int32_t* const* members, double* w, int op, int ncomp,
                      int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream);
 
+/* 32-bit gs_op (SPEC.md:202's precision = 32-bit): the same plans and the
+ * same canonical fold order on float fields (folded in FP32). */
+int nk_gs_op_f32(int64_t nseg, const int32_t* seg_start, const int32_t* perm, float* w, int op,
+                 int ncomp, int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream);
+int nk_gs_op_classes_f32(int nclass, const int32_t* sizes, const int64_t* nsegs,
+                         const int32_t* const* members, float* w, int op, int ncomp,
+                         int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream);
+
 /* Host-side plan construction (gs_setup for one rank):
  * stable counting sort of ids [host, n] by id; ids with multiplicity >= 2
  * become segments.  perm [host, capacity n], seg_start [host, capacity

@@ -46,9 +46,10 @@ def local_plan(ids):
     return perm.astype(np.int64), seg_start
 
 
-def gs_op_plan(perm, seg_start, w, op="+"):
-    """Apply a local plan: sequential fold in plan order; writes back."""
-    w = np.array(w, dtype=np.float64, copy=True)
+def gs_op_plan(perm, seg_start, w, op="+", precision=64):
+    """Apply a local plan: sequential fold in plan order; writes back.
+    precision 32 folds in float32 (SPEC.md:202's 32-bit gs)."""
+    w = np.array(w, dtype=np.float32 if precision == 32 else np.float64, copy=True)
     flat = w.reshape(-1)
     if len(seg_start) <= 1:
         return w
@@ -62,13 +63,13 @@ def gs_op_plan(perm, seg_start, w, op="+"):
     return w
 
 
-def gs_op(ids, w, op="+"):
+def gs_op(ids, w, op="+", precision=64):
     """Single-rank QQ^T."""
     ids = np.asarray(ids).ravel()
     if np.asarray(w).size != ids.size:
         raise ValueError("contract error: field length mismatch")
     perm, seg = local_plan(ids)
-    return gs_op_plan(perm, seg, w, op)
+    return gs_op_plan(perm, seg, w, op, precision)
 
 
 def gs_op_multi(ids_per_rank, w_per_rank, op="+"):

@@ -70,6 +70,8 @@ _SIGS = {
     "nk_local_diag": ([_I32, _I64, _P, _P, _D, _P, _D, _P, _P], _I32),
     "nk_gs_op": ([_I64, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
     "nk_gs_op_classes": ([_I32, _P, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
+    "nk_gs_op_f32": ([_I64, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
+    "nk_gs_op_classes_f32": ([_I32, _P, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
     "nk_gs_plan_build": ([_P, _I64, _P, _P, _P, _P], _I32),
     "nk_gather": ([_I64, _P, _P, _P, _P, _P], _I32),
     "nk_gs_create": ([_P, _P, _I64, _I64, _P], _I32),

@@ -21,18 +21,25 @@ __device__ __forceinline__ double fold(double a, double b) {
   if (OP == NK_OP_MIN) return fmin(a, b);
   return fmax(a, b);
 }
-
 template <int OP>
+__device__ __forceinline__ float fold(float a, float b) {   // 32-bit gs
+  if (OP == NK_OP_ADD) return a + b;
+  if (OP == NK_OP_MUL) return a * b;
+  if (OP == NK_OP_MIN) return fminf(a, b);
+  return fmaxf(a, b);
+}
+
+template <int OP, typename V = double>
 __global__ void __launch_bounds__(256)
 gs_segments(int64_t nseg, const int32_t* __restrict__ seg_start, const int32_t* __restrict__ perm,
-            double* __restrict__ w, int ncomp, int64_t cstride, const nk_cg_state* st) {
+            V* __restrict__ w, int ncomp, int64_t cstride, const nk_cg_state* st) {
   if (st != nullptr && st->done) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += stride) {
     const int a = __ldg(seg_start + s), b = __ldg(seg_start + s + 1);
     for (int c = 0; c < ncomp; ++c) {
-      double* wc = w + c * cstride;
-      double acc = wc[__ldg(perm + a)];
+      V* wc = w + c * cstride;
+      V acc = wc[__ldg(perm + a)];
       for (int q = a + 1; q < b; ++q) acc = fold<OP>(acc, wc[__ldg(perm + q)]);
       for (int q = a; q < b; ++q) wc[__ldg(perm + q)] = acc;
     }
@@ -88,9 +95,9 @@ struct GsClasses {
 // been written by BK5).
 constexpr int kGsU = 4;
 
-template <int OP>
+template <int OP, typename V = double>
 __global__ void __launch_bounds__(256)
-gs_classes_kernel(const __grid_constant__ GsClasses C, double* __restrict__ w, int ncomp,
+gs_classes_kernel(const __grid_constant__ GsClasses C, V* __restrict__ w, int ncomp,
                   int64_t cs, const nk_cg_state* st) {
   if (st != nullptr && st->done) return;
   const int64_t b = blockIdx.x;
@@ -109,18 +116,18 @@ gs_classes_kernel(const __grid_constant__ GsClasses C, double* __restrict__ w, i
   const int lane = threadIdx.x & 31;
   const int m = lane & (Mp - 1);
   for (int cc = 0; cc < ncomp; ++cc) {
-    double* wc = w + cc * cs;
-    double v[kGsU];
+    V* wc = w + cc * cs;
+    V v[kGsU];
 #pragma unroll
-    for (int u = 0; u < kGsU; ++u) v[u] = idx[u] >= 0 ? wc[idx[u]] : 0.0;
+    for (int u = 0; u < kGsU; ++u) v[u] = idx[u] >= 0 ? wc[idx[u]] : V(0);
 #pragma unroll
     for (int u = 0; u < kGsU; ++u) {
-      double acc = v[u];
+      V acc = v[u];
       for (int j = 1; j < M; ++j) {
-        const double o = __shfl_down_sync(0xffffffffu, v[u], j, Mp);
+        const V o = __shfl_down_sync(0xffffffffu, v[u], j, Mp);
         acc = fold<OP>(acc, o);
       }
-      const double res = __shfl_sync(0xffffffffu, acc, lane - m);
+      const V res = __shfl_sync(0xffffffffu, acc, lane - m);
       if (idx[u] >= 0) wc[idx[u]] = res;
     }
   }
@@ -135,9 +142,9 @@ static unsigned grid_for(int64_t n, int threads) {
 
 using namespace nk;
 
-extern "C" int nk_gs_op(int64_t nseg, const int32_t* seg_start, const int32_t* perm, double* w,
-                        int op, int ncomp, int64_t comp_stride, const nk_cg_state* st,
-                        nk_stream_t stream) {
+template <typename V>
+static int gs_op_t(int64_t nseg, const int32_t* seg_start, const int32_t* perm, V* w, int op,
+                   int ncomp, int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream) {
   if (nseg < 0 || (nseg > 0 && (!seg_start || !perm || !w))) {
     set_error("gs_op: invalid plan");
     return NK_ERR_INVALID;
@@ -150,18 +157,31 @@ extern "C" int nk_gs_op(int64_t nseg, const int32_t* seg_start, const int32_t* p
   cudaStream_t s = S(stream);
   const unsigned g = grid_for(nseg, 256);
   switch (op) {
-    case NK_OP_ADD: gs_segments<NK_OP_ADD><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
-    case NK_OP_MUL: gs_segments<NK_OP_MUL><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
-    case NK_OP_MIN: gs_segments<NK_OP_MIN><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
-    case NK_OP_MAX: gs_segments<NK_OP_MAX><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
+    case NK_OP_ADD: gs_segments<NK_OP_ADD, V><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
+    case NK_OP_MUL: gs_segments<NK_OP_MUL, V><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
+    case NK_OP_MIN: gs_segments<NK_OP_MIN, V><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
+    case NK_OP_MAX: gs_segments<NK_OP_MAX, V><<<g, 256, 0, s>>>(nseg, seg_start, perm, w, ncomp, comp_stride, st); break;
     default: set_error("gs_op: unknown op %d", op); return NK_ERR_INVALID;
   }
   return check_launch("gs_segments");
 }
 
-extern "C" int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t* nsegs,
-                                const int32_t* const* members, double* w, int op, int ncomp,
-                                int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream) {
+extern "C" int nk_gs_op(int64_t nseg, const int32_t* seg_start, const int32_t* perm, double* w,
+                        int op, int ncomp, int64_t comp_stride, const nk_cg_state* st,
+                        nk_stream_t stream) {
+  return gs_op_t<double>(nseg, seg_start, perm, w, op, ncomp, comp_stride, st, stream);
+}
+
+extern "C" int nk_gs_op_f32(int64_t nseg, const int32_t* seg_start, const int32_t* perm, float* w,
+                            int op, int ncomp, int64_t comp_stride, const nk_cg_state* st,
+                            nk_stream_t stream) {
+  return gs_op_t<float>(nseg, seg_start, perm, w, op, ncomp, comp_stride, st, stream);
+}
+
+template <typename V>
+static int gs_op_classes_t(int nclass, const int32_t* sizes, const int64_t* nsegs,
+                           const int32_t* const* members, V* w, int op, int ncomp,
+                           int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream) {
   if (nclass < 0 || nclass > NK_GS_MAX_CLASSES || (nclass > 0 && (!sizes || !nsegs || !members))) {
     set_error("gs_op_classes: invalid class table (max %d classes)", NK_GS_MAX_CLASSES);
     return NK_ERR_INVALID;
@@ -194,13 +214,28 @@ extern "C" int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t*
   }
   cudaStream_t s = S(stream);
   switch (op) {
-    case NK_OP_ADD: gs_classes_kernel<NK_OP_ADD><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
-    case NK_OP_MUL: gs_classes_kernel<NK_OP_MUL><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
-    case NK_OP_MIN: gs_classes_kernel<NK_OP_MIN><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
-    case NK_OP_MAX: gs_classes_kernel<NK_OP_MAX><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    case NK_OP_ADD: gs_classes_kernel<NK_OP_ADD, V><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MUL: gs_classes_kernel<NK_OP_MUL, V><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MIN: gs_classes_kernel<NK_OP_MIN, V><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MAX: gs_classes_kernel<NK_OP_MAX, V><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
     default: set_error("gs_op_classes: unknown op %d", op); return NK_ERR_INVALID;
   }
   return check_launch("gs_classes");
+}
+
+extern "C" int nk_gs_op_classes(int nclass, const int32_t* sizes, const int64_t* nsegs,
+                                const int32_t* const* members, double* w, int op, int ncomp,
+                                int64_t comp_stride, const nk_cg_state* st, nk_stream_t stream) {
+  return gs_op_classes_t<double>(nclass, sizes, nsegs, members, w, op, ncomp, comp_stride, st,
+                                 stream);
+}
+
+extern "C" int nk_gs_op_classes_f32(int nclass, const int32_t* sizes, const int64_t* nsegs,
+                                    const int32_t* const* members, float* w, int op, int ncomp,
+                                    int64_t comp_stride, const nk_cg_state* st,
+                                    nk_stream_t stream) {
+  return gs_op_classes_t<float>(nclass, sizes, nsegs, members, w, op, ncomp, comp_stride, st,
+                                stream);
 }
 
 extern "C" int nk_gather(int64_t n, const int32_t* idx, const double* src, double* dst,

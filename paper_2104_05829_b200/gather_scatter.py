@@ -80,14 +80,17 @@ class _Plan:
             self.rest = None
 
     def run(self, w, op, ncomp, stride, st=None):
+        import torch
         L, s = lib(), stream_ptr()
+        f32 = w.dtype == torch.float32          # 32-bit gs (SPEC.md:202 precision)
         if self.nclass:
-            check(L.nk_gs_op_classes(self.nclass, ptr(self.sizes), ptr(self.nsegs), ptr(self.ptrs),
-                                     ptr(w), OP_CODES[op], ncomp, stride, ptr(st), s),
-                  "gs_op_classes")
+            fn = L.nk_gs_op_classes_f32 if f32 else L.nk_gs_op_classes
+            check(fn(self.nclass, ptr(self.sizes), ptr(self.nsegs), ptr(self.ptrs),
+                     ptr(w), OP_CODES[op], ncomp, stride, ptr(st), s), "gs_op_classes")
         if self.rest is not None:
             n, seg, idx = self.rest
-            check(L.nk_gs_op(n, ptr(seg), ptr(idx), ptr(w), OP_CODES[op], ncomp, stride, ptr(st), s),
+            fn = L.nk_gs_op_f32 if f32 else L.nk_gs_op
+            check(fn(n, ptr(seg), ptr(idx), ptr(w), OP_CODES[op], ncomp, stride, ptr(st), s),
                   "gs_op")
 
 
@@ -200,8 +203,8 @@ def _check_field(h, w, ncomp):
     import torch
     if not isinstance(w, torch.Tensor) or not w.is_cuda:
         raise ContractError("field must be a CUDA tensor")
-    if w.dtype != torch.float64 or not w.is_contiguous():
-        raise ContractError("field must be contiguous float64")
+    if w.dtype not in (torch.float64, torch.float32) or not w.is_contiguous():
+        raise ContractError("field must be contiguous float64 (or float32 for precision=32)")
     if w.numel() != h.n * ncomp:
         raise ContractError(f"contract error: field length {w.numel()} != {h.n * ncomp}")
 
@@ -247,19 +250,33 @@ def _halo_finish(h, w, op, st=None):
 
 
 def gs_op(handle, w, op="+", precision=64, ncomp=1):
-    """w <- QQ^T w in place.  Accepts a CUDA float64 tensor
-    (in place) or a numpy array (copied to the device and back; returned)."""
+    """w <- QQ^T w in place.  Accepts a CUDA tensor (in
+    place) or a numpy array (copied to the device and back; returned).
+    precision 64: float64 fields.  precision 32: float32 fields folded in
+    FP32 in the same canonical order (bit-exact against an FP32 sequential
+    fold on one rank); across ranks the halo path accumulates in FP64 and
+    rounds the result to FP32."""
     import torch
     if op not in OP_CODES:
         raise ContractError(f"unknown op {op!r}")
-    if precision != 64:
-        raise NotImplementedError("only the 64-bit path is built (32-bit is out of scope)")
+    if precision not in (32, 64):
+        raise ContractError(f"precision must be 32 or 64, got {precision!r}")
+    want = torch.float32 if precision == 32 else torch.float64
     if isinstance(w, np.ndarray):
         if w.size != handle.n * ncomp:
             raise ContractError(f"contract error: field length {w.size} != {handle.n * ncomp}")
-        t = torch.as_tensor(np.ascontiguousarray(w, dtype=np.float64), device=handle.device)
+        t = torch.as_tensor(np.ascontiguousarray(w, dtype=np.float32 if precision == 32
+                                                 else np.float64), device=handle.device)
         gs_op(handle, t, op, precision, ncomp)
         return t.cpu().numpy().reshape(w.shape)
+    if w.dtype != want:
+        raise ContractError(f"contract error: precision {precision} needs a {want} field, "
+                            f"got {w.dtype}")
+    if precision == 32 and handle.comm is not None and handle.comm.size > 1:
+        t = w.to(torch.float64)
+        gs_op(handle, t, op, 64, ncomp)
+        w.copy_(t)
+        return w
     _check_field(handle, w, ncomp)
     if handle.comm is None or handle.comm.size == 1 or ncomp != 1:
         if handle.comm is not None and handle.comm.size > 1 and ncomp != 1:

@@ -532,3 +532,21 @@ def test_gs_handle_c_api_bit_exact():
             assert np.array_equal(wd.cpu().numpy(), ogs.gs_op(ids, w, op)), op
     finally:
         check(L.nk_gs_destroy(h), "gs_destroy")
+
+
+@pytest.mark.parametrize("op", ["+", "*", "min", "max"])
+def test_gs_32bit_bit_exact(op):
+    """SPEC.md:202 precision = 32-bit: float32 fields folded in FP32 in the
+    canonical order -- bit-exact against the oracle's FP32 sequential fold."""
+    m, o = both_meshes((3, 2, 2), 5, bc="periodic")
+    h = nk.gs_setup(m.ids, nq=m.nq)
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal(o.ids.size).astype(np.float32)
+    if op == "*":
+        w = (1.0 + 0.01 * w).astype(np.float32)
+    got = nk.gs_op(h, torch.as_tensor(w, device="cuda"), op, precision=32).cpu().numpy()
+    ref = ogs.gs_op(o.ids, w, op, precision=32)
+    assert got.dtype == np.float32 and np.array_equal(got, ref)
+    assert np.array_equal(nk.gs_op(h, w.copy(), op, precision=32), ref)     # numpy path
+    with pytest.raises(nk.ContractError):
+        nk.gs_op(h, torch.as_tensor(w, device="cuda"), op, precision=64)
