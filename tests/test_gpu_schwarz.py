@@ -241,3 +241,24 @@ def test_hierarchy_schwarz_boundary_kinds_match_oracle(smoother, bc, lam1):
         lv.mask.size))
     z = nk.pmg_preconditioner(h, dev(r)).cpu().numpy()
     assert rel_l2(z, opmg.vcycle(o, r)) < 1e-9
+
+
+@pytest.mark.parametrize("N", [2, 3, 4, 6, 9, 10, 15])
+def test_ras_hierarchy_all_orders_match_oracle(N):
+    """p-multigrid with RAS smoothing at low and high orders (every
+    specialised transfer pair N+1 <-> N/2+1 <-> 2): λmax and the V-cycle vs
+    the oracle."""
+    counts = (2, 2, 1) if N < 10 else (1, 2, 1)
+    kw = dict(bc="dirichlet", deformation=("sine", 0.05))
+    m = nk.build_box_mesh((1, 1, 1), counts, N, **kw)
+    op = nk.PoissonOperator(m)
+    h = nk.MultigridHierarchy(op, smoother="ras")
+    o = opmg.build_hierarchy((1, 1, 1), counts, N, smoother="ras", **kw)
+    assert h.orders == opmg.orders_for(N)
+    for lg, lo in zip(h.levels[:-1], o["levels"][:-1]):
+        assert abs(lg.lmax - lo.lmax) < 1e-9 * lo.lmax
+    lv = o["levels"][0]
+    r = lv.mask * ogs.gs_op(lv.mesh.ids, lv.wt * np.random.default_rng(N).standard_normal(
+        lv.mask.size))
+    z = nk.pmg_preconditioner(h, dev(r)).cpu().numpy()
+    assert rel_l2(z, opmg.vcycle(o, r)) < 1e-9
