@@ -328,9 +328,64 @@ def gs_op_overlapped(handle, local_work, field, op="+"):
     return field
 
 
-def autotune(handle, trials=1, callback=None):
-    """SPEC.md:222-230.  On one NVSwitch node every peer is one hop at full
-    bandwidth, so pairwise is the only strategy built; autotune records it
-    (the tie-break order of SPEC.md:225 also selects pairwise)."""
+def _set_transport(handle, kind):
+    if kind == "p2p":
+        if handle.ipc is not None:
+            handle._ipc_saved = handle.ipc
+            handle.ipc = None
+    elif kind == "ipc":
+        if handle.ipc is None and getattr(handle, "_ipc_saved", None) is not None:
+            handle.ipc = handle._ipc_saved
+    handle.transport = "ipc" if handle.ipc is not None else "p2p"
+
+
+def autotune(handle, trials=3, callback=None):
+    """pick the exchange that yields the lowest maximum (over
+    ranks) median time over `trials` (§3.2).  The strategy is
+    pairwise (on one NVSwitch node every peer is one hop at full bandwidth,
+    so crystal-router / all-reduce exchanges only add hops -- not built); the
+    choice is between the transports the handle can run: peer-memory pushes
+    ('ipc', when every neighbour's buffer is mapped on every rank) and
+    torch.distributed send/recv ('p2p').  `callback(handle)` replaces the
+    plain gs_op as the trial workload (tested in tandem with the caller's
+    setup).  Collective; every rank adopts the same choice.  Returns the
+    handle with `strategy`, `transport` and `autotune_times` set."""
+    import statistics
+    import time
+
+    import torch
+    if int(trials) < 1:
+        raise ContractError("autotune needs trials >= 1")
     handle.strategy = "pairwise"
+    comm = handle.comm
+    if comm is None or comm.size == 1:
+        handle.autotune_times = {}
+        return handle
+    dist, dev = comm.dist, ("cuda" if comm.backend == "nccl" else "cpu")
+    has_ipc = torch.tensor([1.0 if (handle.ipc is not None or
+                                    getattr(handle, "_ipc_saved", None) is not None) else 0.0],
+                           dtype=torch.float64, device=dev)
+    dist.all_reduce(has_ipc, op=dist.ReduceOp.MIN, group=comm.group)
+    cands = (["ipc"] if float(has_ipc) > 0 else []) + ["p2p"]
+    w = torch.randn(handle.n, dtype=torch.float64, device=handle.device)
+    times = {}
+    for kind in cands:
+        _set_transport(handle, kind)
+        ts = []
+        for _ in range(int(trials) + 1):            # first run: warm-up
+            torch.cuda.synchronize()
+            comm.barrier()
+            t0 = time.perf_counter()
+            if callback is not None:
+                callback(handle)
+            else:
+                gs_op(handle, w)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        t = torch.tensor([statistics.median(ts[1:])], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=comm.group)
+        times[kind] = float(t)
+    best = min(cands, key=lambda k: (times[k], cands.index(k)))
+    _set_transport(handle, best)
+    handle.autotune_times = times
     return handle

@@ -282,3 +282,48 @@ def test_two_ranks_schwarz_and_pmg(transport):
         xa[r["mine"]] = r["xa"].reshape(-1, nq3)
     assert int(res[0]["ita"]) == int(res[1]["ita"])
     assert np.max(np.abs(xa.ravel() - o.x)) < 1e-6 * np.max(np.abs(o.x))
+
+
+def _autotune_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2104_05829_b200 as nk
+        from paper_2104_05829_b200 import gather_scatter as gsm
+        from paper_2104_05829_b200.distributed import RankComm
+        from oracle import mesh as om
+        counts, N = (4, 2, 2), 3
+        g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N)
+        part = nk.rcb(g.xyz.reshape(3, g.E, -1).mean(axis=2).T, world)
+        mine = np.flatnonzero(part == rank)
+        m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, elements=mine)
+        op = nk.PoissonOperator(m, comm=RankComm(transport="auto"))
+        w = np.random.default_rng(5 + rank).standard_normal(m.n_local)
+        before = nk.gs_op(op.gs, torch.as_tensor(w, device="cuda")).cpu().numpy()
+        gsm.autotune(op.gs, trials=2)
+        chosen = op.gs.transport
+        after = nk.gs_op(op.gs, torch.as_tensor(w, device="cuda")).cpu().numpy()
+        calls = []
+        gsm.autotune(op.gs, trials=1, callback=lambda h: calls.append(1) or nk.gs_op(
+            h, torch.as_tensor(w, device="cuda")))
+        np.savez(os.path.join(outdir, f"a{rank}.npz"), chosen=chosen, same=np.array_equal(
+            before, after), cands=sorted(op.gs.autotune_times), ncalls=len(calls))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_autotune_agrees_across_ranks():
+    """every rank adopts the same exchange; results stay
+    bit-identical; the callback runs as the trial workload."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_autotune_worker, args=(2, _port(), d), nprocs=2, join=True)
+        res = [np.load(os.path.join(d, f"a{r}.npz")) for r in range(2)]
+    assert str(res[0]["chosen"]) == str(res[1]["chosen"])
+    assert str(res[0]["chosen"]) in ("ipc", "p2p")
+    for r in res:
+        assert bool(r["same"]) and set(r["cands"]) == {"ipc", "p2p"}
+        assert int(r["ncalls"]) == 2 * 2            # (1 trial + warm-up) x 2 candidates
