@@ -327,3 +327,94 @@ def test_autotune_agrees_across_ranks():
     for r in res:
         assert bool(r["same"]) and set(r["cands"]) == {"ipc", "p2p"}
         assert int(r["ncalls"]) == 2 * 2            # (1 trial + warm-up) x 2 candidates
+
+
+def _four_worker(rank, world, port, outdir, counts, N, transport):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2104_05829_b200 as nk
+        from oracle import gs as ogs
+        from oracle import mesh as om
+        from paper_2104_05829_b200.distributed import RankComm
+        kw = dict(deformation=("sine", 0.05))
+        g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, **kw)
+        nq3 = (N + 1) ** 3
+        part = nk.rcb(g.xyz.reshape(3, g.E, -1).mean(axis=2).T, world)
+        mine = np.flatnonzero(part == rank)
+        comm = RankComm(transport=transport)
+        m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, elements=mine, **kw)
+        op = nk.PoissonOperator(m, comm=comm)
+        w = np.random.default_rng(50 + rank).standard_normal(m.n_local)
+        gsw = nk.gs_op(op.gs, torch.as_tensor(w, device="cuda")).cpu().numpy()
+        x = np.random.default_rng(9).standard_normal(g.mask.size)
+        rg = g.mask.ravel() * ogs.gs_op(g.ids, x / ogs.multiplicity(g.ids))
+        r = torch.as_tensor(rg.reshape(g.E, nq3)[mine].ravel(), device="cuda")
+        zr = nk.SchwarzSmoother(op, "ras")(r).cpu().numpy()
+        X = g.xyz.reshape(3, -1)
+        f = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+        b = (g.mask.ravel() * ogs.gs_op(g.ids, g.B.ravel() * f)).reshape(g.E, nq3)[mine].ravel()
+        bt = torch.as_tensor(b, device="cuda")
+        rj = nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-8, max_iter=800,
+                         use_graph=(transport == "ipc")).solve(bt)
+        xj = rj.x.cpu().numpy().copy()
+        rp = nk.MultigridPCG(op, nk.MultigridHierarchy(op, smoother="ras", coarse="pcg"),
+                             tol=1e-8, max_iter=200).solve(bt)
+        np.savez(os.path.join(outdir, f"q{rank}.npz"), mine=mine, ids=m.ids.cpu().numpy(), w=w,
+                 gsw=gsw, zr=zr, xj=xj, itj=rj.iterations, xp=rp.x.cpu().numpy(),
+                 itp=rp.iterations, ngh=op.gs.ngh)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("transport", ["p2p", "ipc"])
+def test_four_ranks_gs_schwarz_pcg_pmg(transport):
+    """Four ranks sharing one B200 (RCB 2x2 blocks: edge- and corner-sharing
+    neighbours): gs bit-exact vs the oracle's multi-rank canonical fold, RAS
+    = the single-process oracle to 1e-12, Jacobi-PCG iterations within 1 of
+    the oracle, pMG-RAS converging to the same solution."""
+    import torch.multiprocessing as mp
+    from oracle import gs as ogs
+    from oracle import mesh as om
+    from oracle import operators as oop
+    from oracle import schwarz as osz
+    from oracle import solvers as osol
+    counts, world, N = (4, 4, 2), 4, 3
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_four_worker, args=(world, _port(), d, counts, N, transport), nprocs=world,
+                 join=True)
+        res = [np.load(os.path.join(d, f"q{r}.npz")) for r in range(world)]
+    ref = ogs.gs_op_multi([r["ids"] for r in res], [r["w"] for r in res])
+    for r, ro in zip(res, ref):
+        assert np.array_equal(r["gsw"], ro)
+    assert max(int(r["ngh"]) for r in res) >= 2
+    g = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05))
+    nq3 = (N + 1) ** 3
+    f = osz.fdm_setup(g.xyz, g.ids, g.mask, g.E, N, g.basis.diff, g.basis.weights)
+    x = np.random.default_rng(9).standard_normal(g.mask.size)
+    rg = g.mask.ravel() * ogs.gs_op(g.ids, x / ogs.multiplicity(g.ids))
+    zo = osz.schwarz_smooth(f, "ras", rg, g.ids, g.mask).reshape(g.E, nq3)
+    zg = np.zeros((g.E, nq3))
+    for r in res:
+        zg[r["mine"]] = r["zr"].reshape(-1, nq3)
+    assert np.linalg.norm(zg - zo) / np.linalg.norm(zo) < 1e-12
+    X = g.xyz.reshape(3, -1)
+    fs = 3 * np.pi ** 2 * np.prod(np.sin(np.pi * X), axis=0)
+    mask = g.mask.ravel()
+    b = mask * ogs.gs_op(g.ids, g.B.ravel() * fs)
+    sh = (g.E,) + g.G.shape[2:]
+    A = lambda v: mask * ogs.gs_op(g.ids, oop.bk5(g.basis.diff, g.G, v.reshape(sh)).ravel())
+    inv = mask / ogs.gs_op(g.ids, oop.local_diagonal(g.basis.diff, g.G).ravel())
+    o = osol.pcg(A, lambda r: inv * r, b, tol=1e-8, max_iter=800,
+                 weights=1.0 / ogs.multiplicity(g.ids))
+    xj, xp = np.zeros((g.E, nq3)), np.zeros((g.E, nq3))
+    for r in res:
+        assert abs(int(r["itj"]) - o.iterations) <= 1
+        xj[r["mine"]] = r["xj"].reshape(-1, nq3)
+        xp[r["mine"]] = r["xp"].reshape(-1, nq3)
+    assert len({int(r["itp"]) for r in res}) == 1
+    assert np.max(np.abs(xj.ravel() - o.x)) < 1e-7 * np.max(np.abs(o.x))
+    assert np.max(np.abs(xp.ravel() - o.x)) < 1e-6 * np.max(np.abs(o.x))
