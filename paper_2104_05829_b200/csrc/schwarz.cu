@@ -25,17 +25,21 @@ namespace nk {
 // +inf: dropped points).  M is S^T for the forward and S for the backward
 // transform.  Every M element loaded (16-B broadcast loads, all lanes on one
 // address) feeds two FMAs (one per line): 1 shared load per 4 DFMA.
-template <typename T> struct Vec2;
-template <> struct Vec2<double> { using type = double2; };
-template <> struct Vec2<float> { using type = float2; };
+// 16-byte row chunks: 2 doubles or 4 floats per shared load
+template <typename T> struct RowVec;
+template <> struct RowVec<double> { static constexpr int W = 2; };
+template <> struct RowVec<float> { static constexpr int W = 4; };
+template <typename T> struct alignas(16) Chunk { T v[RowVec<T>::W]; };
+template <int NQE, typename T>
+struct RowPitch { static constexpr int SP = (NQE + RowVec<T>::W - 1) / RowVec<T>::W * RowVec<T>::W; };
 __device__ __forceinline__ double fdm_rcp(double x) { return __drcp_rn(x); }
 __device__ __forceinline__ float fdm_rcp(float x) { return __frcp_rn(x); }
 
 template <int NQE, int ST, typename T>
 __device__ __forceinline__ void fdm_line2(T* L0, T* L1, const T* __restrict__ M, const T* lz,
                                           T lab0, T lab1, T lam0, T lam1) {
-  using V2 = typename Vec2<T>::type;
-  constexpr int SP = (NQE + 1) & ~1;
+  constexpr int W = RowVec<T>::W;
+  constexpr int SP = RowPitch<NQE, T>::SP;
   T v0[NQE], v1[NQE];
 #pragma unroll
   for (int i = 0; i < NQE; ++i) {
@@ -47,17 +51,19 @@ __device__ __forceinline__ void fdm_line2(T* L0, T* L1, const T* __restrict__ M,
     const T* row = M + a * SP;
     T s0 = 0, s1 = 0;
 #pragma unroll
-    for (int i = 0; i + 1 < NQE; i += 2) {
-      const V2 m = *reinterpret_cast<const V2*>(row + i);
-      s0 = fma(m.x, v0[i], s0);
-      s1 = fma(m.x, v1[i], s1);
-      s0 = fma(m.y, v0[i + 1], s0);
-      s1 = fma(m.y, v1[i + 1], s1);
+    for (int i = 0; i + W <= NQE; i += W) {
+      const Chunk<T> m = *reinterpret_cast<const Chunk<T>*>(row + i);
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        s0 = fma(m.v[c], v0[i + c], s0);
+        s1 = fma(m.v[c], v1[i + c], s1);
+      }
     }
-    if (NQE & 1) {
-      const T m = row[NQE - 1];
-      s0 = fma(m, v0[NQE - 1], s0);
-      s1 = fma(m, v1[NQE - 1], s1);
+#pragma unroll
+    for (int i = NQE - NQE % W; i < NQE; ++i) {
+      const T m = row[i];
+      s0 = fma(m, v0[i], s0);
+      s1 = fma(m, v1[i], s1);
     }
     if (lz != nullptr) {
       const T l0 = lab0 + lz[a], l1 = lab1 + lz[a];
@@ -74,10 +80,10 @@ struct FdmShape {
   static constexpr int NQ = NQE - 2;                 // N + 1
   static constexpr int LS = NQE + 1;                 // padded line stride
   static constexpr int PS = NQE * LS;                // plane stride
-  static constexpr int SP = (NQE + 1) & ~1;          // matrix row stride (16-B rows)
+  static constexpr int SP = RowPitch<NQE, T>::SP;    // matrix row stride (16-B rows)
   static constexpr int NL = NQE * NQE;               // lines per orientation
   static constexpr int NT = (NL + 1) / 2;            // threads: two lines each
-  static constexpr int A_SZ = NQE * PS;
+  static constexpr int A_SZ = (NQE * PS + RowVec<T>::W - 1) / RowVec<T>::W * RowVec<T>::W;  // 16-B aligned end
   static constexpr int M_SZ = 3 * NQE * SP;          // one of S^T / S, 3 directions
   static constexpr size_t SMEM = sizeof(T) * (A_SZ + 2 * M_SZ + 3 * NQE);
 };
