@@ -161,6 +161,21 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
                                                  cudaStream_t s, int64_t* nblocks, int cfg,
                                                  int pf_dist, int variant) {
   constexpr int NQ = NK_BK5_NQ;
+  if constexpr (NQ == 2) {   // N = 1: element per thread unless k-slab is forced
+    if (ncomp == 1 && variant != 1) {
+      const int64_t nb = (nlist * 8 + kN1PtThreads - 1) / kN1PtThreads;
+      if (nblocks) {
+        *nblocks = nb;
+        return NK_OK;
+      }
+      if (nb == 0) return NK_OK;
+      DParam<2> Dp;
+      for (int q = 0; q < 4; ++q) Dp.d[q] = D[q];
+      bk5_n1<2><<<(unsigned)nb, kN1PtThreads, 0, s>>>(nlist, elist, Dp, G, u, w, lam0, B, lam1,
+                                                    mask, st, partials, part_base, reduce_count);
+      return check_launch("bk5_n1");
+    }
+  }
   if constexpr (NQ == 4 || NQ == 6 || NQ == 8) {
     if (variant == 4 && ncomp == 1) {
 #define NK_TARGS nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, \
@@ -221,8 +236,8 @@ extern "C" int NK_CAT(nk_bk5_pcg_nq, NK_BK5_NQ)(int64_t nlist, const int32_t* el
   constexpr int NQ = NK_BK5_NQ;
   constexpr int EPB = PencilDefault<NQ>::EPB;
   constexpr int MINB = NQ == 8 ? 10 : PencilDefault<NQ>::MINB;  // ~100 regs at NQ = 8
-  if constexpr (NQ == 2) {   // element per thread (the order-1 coarse level)
-    const int64_t nb = (nlist + kN1Threads - 1) / kN1Threads;
+  if constexpr (NQ == 2) {   // point per thread (the order-1 coarse level)
+    const int64_t nb = (nlist * 8 + kN1PtThreads - 1) / kN1PtThreads;
     if (nblocks) {
       *nblocks = nb;
       return NK_OK;
@@ -230,7 +245,7 @@ extern "C" int NK_CAT(nk_bk5_pcg_nq, NK_BK5_NQ)(int64_t nlist, const int32_t* el
     if (nb == 0) return NK_OK;
     DParam<2> Dp;
     for (int q = 0; q < 4; ++q) Dp.d[q] = D[q];
-    bk5_n1_pcg<2><<<(unsigned)nb, kN1Threads, 0, s>>>(nlist, elist, Dp, G, p, w, lam0, B, lam1,
+    bk5_n1_pcg<2><<<(unsigned)nb, kN1PtThreads, 0, s>>>(nlist, elist, Dp, G, p, w, lam0, B, lam1,
                                                    mask, x, r, invD, st, partials, part_base,
                                                    reduce_count, hist);
     return check_launch("bk5_n1_pcg");

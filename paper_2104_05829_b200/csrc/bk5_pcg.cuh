@@ -241,14 +241,42 @@ static int launch_pencil_pcg(int64_t nlist, const int32_t* elist, const double* 
 
 
 // N = 1 (NQ = 2, 8 points per element): the pencil machinery (shared
-// transposes, barriers) costs more than the element's arithmetic, so one
-// THREAD owns one element -- p, r, invD, x, w as four 16-B loads each and
-// G as 24 -- with the same prologue / epilogue semantics as bk5_pencil_pcg.
-// Used by the iterative coarse solve of the p-multigrid (order-1 level).
-constexpr int kN1Threads = 128;
+// transposes, barriers) costs more than the element's arithmetic, so each
+// element is owned by 8 consecutive lanes, one point per lane: every load
+// (p, r, invD, x, G's six components) is warp-coalesced, and the three
+// 2-point derivatives and their transposes swap partner values with xor
+// shuffles (lane bit 0 = i, 1 = j, 2 = k).  Both kernels below share it:
+// the plain apply (nk_bk5 at N = 1) and the fused PCG step (the
+// p-multigrid's iterative order-1 coarse solve).
+constexpr int kN1PtThreads = 256;
+
+// (G grad p)ᵀ grad at point q = k*4 + j*2 + i of the lane's element; all
+// 32 lanes must call it (shuffles).  g = the point's six G components.
+__device__ __forceinline__ double n1_point_stiffness(double pv, const double (&g)[6],
+                                                     const DParam<2>& D, int q) {
+  const int i = q & 1, j = (q >> 1) & 1, k = q >> 2;
+  const double pi = __shfl_xor_sync(0xffffffffu, pv, 1);
+  const double pj = __shfl_xor_sync(0xffffffffu, pv, 2);
+  const double pk = __shfl_xor_sync(0xffffffffu, pv, 4);
+  // d/dr at (i,j,k) = D[i][0] u(0,j,k) + D[i][1] u(1,j,k)
+  const double ur = i ? D.d[2] * pi + D.d[3] * pv : D.d[0] * pv + D.d[1] * pi;
+  const double us = j ? D.d[2] * pj + D.d[3] * pv : D.d[0] * pv + D.d[1] * pj;
+  const double ut = k ? D.d[2] * pk + D.d[3] * pv : D.d[0] * pv + D.d[1] * pk;
+  const double gr = g[0] * ur + g[1] * us + g[2] * ut;
+  const double gs = g[1] * ur + g[3] * us + g[4] * ut;
+  const double gt = g[2] * ur + g[4] * us + g[5] * ut;
+  const double ri = __shfl_xor_sync(0xffffffffu, gr, 1);
+  const double sj = __shfl_xor_sync(0xffffffffu, gs, 2);
+  const double tk = __shfl_xor_sync(0xffffffffu, gt, 4);
+  // transpose: sum_a D[a][i] gr(a,j,k) (+ s, t)
+  double v = i ? D.d[1] * ri + D.d[3] * gr : D.d[0] * gr + D.d[2] * ri;
+  v += j ? D.d[1] * sj + D.d[3] * gs : D.d[0] * gs + D.d[2] * sj;
+  v += k ? D.d[1] * tk + D.d[3] * gt : D.d[0] * gt + D.d[2] * tk;
+  return v;
+}
 
 template <int NQ_ONE>   // = 2; a template so every translation unit may include it
-__global__ void __launch_bounds__(kN1Threads)
+__global__ void __launch_bounds__(kN1PtThreads)
 bk5_n1_pcg(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<2> D,
            const double* __restrict__ G, double* __restrict__ p, double* __restrict__ w,
            double lam0, const double* __restrict__ B, double lam1,
@@ -266,87 +294,40 @@ bk5_n1_pcg(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   const double beta = it == 0 ? 0.0 : (st->flexible ? (-alpha_prev * st->zap) / rz
                                                     : st->rz_new / rz);
   const int t = threadIdx.x;
-  const int64_t slot = (int64_t)blockIdx.x * kN1Threads + t;
+  const int64_t slot = ((int64_t)blockIdx.x * kN1PtThreads + t) >> 3;
+  const int q = t & 7;
   const bool active = slot < nlist;
   const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
-  const int64_t off = e * 8;
+  const int64_t pt = e * 8 + q;
   double dot = 0.0;
+  // every load issued in one batch (one memory round trip per lane)
+  double pv = 0.0, xv = 0.0, rv = 0.0, dv = 0.0, g[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (active) {
-    double pv[8];
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(p + off + q);
-      pv[q] = v.x;
-      pv[q + 1] = v.y;
-    }
-    if (it > 0) {
-#pragma unroll
-      for (int q = 0; q < 8; q += 2) {
-        double2 xv = *reinterpret_cast<const double2*>(x + off + q);
-        xv.x = fma(alpha_prev, pv[q], xv.x);
-        xv.y = fma(alpha_prev, pv[q + 1], xv.y);
-        *reinterpret_cast<double2*>(x + off + q) = xv;
-      }
-      if (!stop) {
-#pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-          const double2 rv = __ldg(reinterpret_cast<const double2*>(r + off + q));
-          const double2 dv = __ldg(reinterpret_cast<const double2*>(invD + off + q));
-          pv[q] = fma(beta, pv[q], dv.x * rv.x);
-          pv[q + 1] = fma(beta, pv[q + 1], dv.y * rv.y);
-          *reinterpret_cast<double2*>(p + off + q) = make_double2(pv[q], pv[q + 1]);
-        }
-      }
-    }
+    pv = p[pt];
+    if (it > 0) xv = x[pt];
     if (!stop) {
-      // point q = k*4 + j*2 + i;  d/dr along i, d/ds along j, d/dt along k
-      double ur[8], us[8], ut[8];
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int q = k * 4 + j * 2 + i;
-            ur[q] = D.d[i * 2 + 0] * pv[k * 4 + j * 2 + 0] + D.d[i * 2 + 1] * pv[k * 4 + j * 2 + 1];
-            us[q] = D.d[j * 2 + 0] * pv[k * 4 + 0 * 2 + i] + D.d[j * 2 + 1] * pv[k * 4 + 1 * 2 + i];
-            ut[q] = D.d[k * 2 + 0] * pv[0 * 4 + j * 2 + i] + D.d[k * 2 + 1] * pv[1 * 4 + j * 2 + i];
-          }
-      const double* ge = G + e * 48;
-      double g[48];
-#pragma unroll
-      for (int q = 0; q < 48; q += 2) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(ge + q));
-        g[q] = v.x;
-        g[q + 1] = v.y;
+      if (it > 0) {
+        rv = __ldg(r + pt);
+        dv = __ldg(invD + pt);
       }
-      double gr[8], gs[8], gt[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        gr[q] = g[q] * ur[q] + g[8 + q] * us[q] + g[16 + q] * ut[q];
-        gs[q] = g[8 + q] * ur[q] + g[24 + q] * us[q] + g[32 + q] * ut[q];
-        gt[q] = g[16 + q] * ur[q] + g[32 + q] * us[q] + g[40 + q] * ut[q];
-      }
-      double res[8];
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int q = k * 4 + j * 2 + i;
-            double v = D.d[0 * 2 + i] * gr[k * 4 + j * 2 + 0] + D.d[1 * 2 + i] * gr[k * 4 + j * 2 + 1];
-            v += D.d[0 * 2 + j] * gs[k * 4 + 0 * 2 + i] + D.d[1 * 2 + j] * gs[k * 4 + 1 * 2 + i];
-            v += D.d[0 * 2 + k] * gt[0 * 4 + j * 2 + i] + D.d[1 * 2 + k] * gt[1 * 4 + j * 2 + i];
-            v *= lam0;
-            if (B != nullptr) v = fma(lam1 * __ldg(B + off + q), pv[q], v);
-            if (mask != nullptr) v = mask[off + q] ? v : 0.0;
-            res[q] = v;
-            dot = fma(pv[q], v, dot);
-          }
-#pragma unroll
-      for (int q = 0; q < 8; q += 2)
-        *reinterpret_cast<double2*>(w + off + q) = make_double2(res[q], res[q + 1]);
+      for (int c = 0; c < 6; ++c) g[c] = __ldg(G + e * 48 + c * 8 + q);
+    }
+  }
+  if (it > 0 && active) {
+    x[pt] = fma(alpha_prev, pv, xv);
+    if (!stop) {
+      pv = fma(beta, pv, dv * rv);
+      p[pt] = pv;
+    }
+  }
+  if (!stop) {   // grid-uniform
+    double v = lam0 * n1_point_stiffness(pv, g, D, q);
+    if (active) {
+      if (B != nullptr) v = fma(lam1 * __ldg(B + pt), pv, v);
+      if (mask != nullptr) v = mask[pt] ? v : 0.0;
+      w[pt] = v;
+      dot = pv * v;
     }
   }
   double vv[1] = {dot};
@@ -364,6 +345,44 @@ bk5_n1_pcg(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
         st->pAp = sres[0];
         if (it > 0) st->rz = st->rz_new;
       }
+    }
+  }
+}
+
+template <int NQ_ONE>   // = 2
+__global__ void __launch_bounds__(kN1PtThreads)
+bk5_n1(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<2> D,
+       const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
+       double lam0, const double* __restrict__ B, double lam1, const uint8_t* __restrict__ mask,
+       nk_cg_state* st, double* __restrict__ partials, int64_t part_base, int64_t reduce_count) {
+  __shared__ double red[32];
+  if (st != nullptr && st->done) return;
+  const int t = threadIdx.x;
+  const int64_t slot = ((int64_t)blockIdx.x * kN1PtThreads + t) >> 3;
+  const int q = t & 7;
+  const bool active = slot < nlist;
+  const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
+  const int64_t pt = e * 8 + q;
+  const double pv = active ? __ldg(u + pt) : 0.0;
+  double g[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) g[c] = active ? __ldg(G + e * 48 + c * 8 + q) : 0.0;
+  double v = lam0 * n1_point_stiffness(pv, g, D, q);
+  double dot = 0.0;
+  if (active) {
+    if (B != nullptr) v = fma(lam1 * __ldg(B + pt), pv, v);
+    if (mask != nullptr) v = mask[pt] ? v : 0.0;
+    w[pt] = v;
+    dot = pv * v;
+  }
+  if (st != nullptr) {
+    double vv[1] = {dot};
+    block_sum<1>(vv, red);
+    if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+    if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
+      double sres[1];
+      reduce_partials<1>(partials, reduce_count, 0, sres, red);
+      if (t == 0) st->pAp = sres[0];
     }
   }
 }
