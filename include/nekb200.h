@@ -151,8 +151,9 @@ int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
  * thread plane, k-column in registers, D in shared memory), 3 = pencil
  * (register 1-D contractions, D in the constant bank, swizzled shared
  * transposes), 4 = pencil-TMA (persistent CTAs, cp.async.bulk 2-stage ring;
- * N+1 in {4, 6, 8}, else pencil).  Variants 3/4 serve ncomp = 1; ncomp = 3
- * uses k-slab.  Returns the previous value. */
+ * N+1 in {4, 6, 8}, else pencil).  N = 1 always runs its point-per-lane
+ * kernel unless 1 is set.  Variants 3/4/5 serve ncomp = 1;
+ * ncomp = 3 uses k-slab or pencil3.  Returns the previous value. */
 int nk_bk5_set_variant(int variant);
 /* k-slab tuning: cfg selects the (elements per CTA, CTAs per SM) shape for
  * N = 7 (0 = default 4x2, 1 = 4x3, 2 = 2x4, 3 = 2x6, 4 = 1x8, 5 = 1x12,

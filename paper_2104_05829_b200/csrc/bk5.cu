@@ -1,5 +1,5 @@
 // BK5 dispatch by order (the kernels are in bk5_kernels.cuh, instantiated
-// per order in bk5_inst.cu; the bulk-copy variant in bk5_bulk.cu).
+// per order in bk5_inst.cu).
 #include "common.cuh"
 
 typedef int (*kslab_fn)(int, int64_t, const int32_t*, const double*, const double*, const double*,
@@ -61,15 +61,8 @@ extern "C" int nk_bk5_tune(int cfg, int pf_dist) {
   g_pf = pf_dist;
   return NK_OK;
 }
-extern "C" int nk_bk5_bulk_launch(int N, int64_t nlist, const int32_t* elist, const double* D,
-                                  const double* G, const double* u, double* w, double lam0,
-                                  const double* B, double lam1, const uint8_t* mask,
-                                  nk_cg_state* st, double* partials, int64_t part_base,
-                                  int64_t reduce_count, cudaStream_t s, int64_t* nblocks_out,
-                                  int query_only);
 extern "C" int nk_bk5_variant_get();
 
-static bool use_bulk(int N, int ncomp) { return nk_bk5_variant_get() == 2 && N == 7 && ncomp == 1; }
 // auto (0): the measured winner per order (the select_kernel_variant of
 // SPEC.md:420-428, decided offline by scripts/bk5_sweep.py --orders on the
 // B200 under the cold-and-clean L2 protocol, profiles/r1_bk5_order_sweep*):
@@ -85,12 +78,6 @@ static int kvariant_for(int N) {
 }
 
 extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {
-  if (use_bulk(N, ncomp)) {
-    int64_t nb = 0;
-    nk_bk5_bulk_launch(N, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0,
-                       nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, 1);
-    return nb;
-  }
   if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) return -1;
   int64_t nb = -1;
   kslab_table[N](ncomp, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0, 0,
@@ -143,9 +130,6 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
     }
     return NK_OK;
   }
-  if (use_bulk(N, ncomp))
-    return nk_bk5_bulk_launch(N, n, elem_list, D, G, u, w, lam0, B, lam1, mask, st, partials,
-                              part_base, reduce_count, s, nullptr, 0);
   return kslab_table[N](ncomp, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, st,
                         partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf,
                         kvariant_for(N));

@@ -15,7 +15,6 @@
 // element (consecutive threads -> consecutive points).  HBM traffic per
 // point: u 8 B + G 48 B + w 8 B (+ B 8 B, + mask 1 B).
 //
-// Variant 2 lives in bk5_bulk.cu (persistent CTAs, cp.async.bulk pipeline).
 #pragma once
 #include "common.cuh"
 

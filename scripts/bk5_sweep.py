@@ -63,6 +63,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", action="store_true")
     ap.add_argument("--orders", action="store_true")
+    ap.add_argument("--low", action="store_true", help="N = 1, 2 variant comparison")
     ap.add_argument("--probe", action="store_true")
     ap.add_argument("--helm3", action="store_true")
     ap.add_argument("--reps", type=int, default=50)
@@ -181,11 +182,12 @@ def main():
                       "gdofs": round(m.E * 343 / med / 1e6, 3), "bitwise_same": same})
         L.nk_bk5_tune(0, 0)
         L.nk_bk5_set_variant(0)
-    if args.orders:
-        for N in range(1, 16):
+    if args.orders or args.low:
+        low = {1: (0, 1), 2: (0, 3, 5)}
+        for N in (range(1, 16) if args.orders else (1, 2)):
             ne = E_FOR_N[N]
             m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
-            for variant, pf in ((0, 1),):
+            for variant, pf in (((v, 1) for v in low[N]) if args.low else ((0, 1),)):
                 L.nk_bk5_set_variant(variant)
                 L.nk_bk5_tune(0, pf)
                 med, best, _ = time_bk5(nk, L, m, args.reps, flush)

@@ -296,10 +296,10 @@ def variant_guard():
 
 
 @pytest.mark.parametrize("variant", [1, 3, 4, 5])
-@pytest.mark.parametrize("N", [3, 5, 7, 12])
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 12])
 def test_bk5_variants_match_oracle(variant_guard, variant, N):
-    """k-slab (1), pencil (3) and pencil-TMA (4, even N+1; others fall back)
-    all within the 1e-12 bar, incl. element subsets, mask and the fused p.Ap."""
+    """k-slab (1), pencil (3), pencil-TMA (4, even N+1; others fall back),
+    pencil2 (5; N = 1 has its own point-per-lane kernel) all within the 1e-12 bar, incl. element subsets, mask and the fused p.Ap."""
     L = variant_guard
     L.nk_bk5_set_variant(variant)
     m, o = both_meshes((5, 4, 3), N)

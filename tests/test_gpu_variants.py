@@ -18,7 +18,7 @@ import paper_2104_05829_b200 as nk  # noqa: E402
 from paper_2104_05829_b200 import kernels as K  # noqa: E402
 
 
-@pytest.mark.parametrize("N", [3, 7, 12])
+@pytest.mark.parametrize("N", [2, 3, 7, 12])
 def test_select_variant_and_parity(N):
     counts = (3, 2, 2)
     m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
