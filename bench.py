@@ -417,8 +417,15 @@ def run_ours(args):
         for _ in range(2):                 # profile a steady-state iteration (iter > 0)
             solver._iteration()
         brk = solver.profile_iteration() if ws == 1 else None
-        # fused schedule: nk_bk5_pcg 105 B + cg_update 40 B per point + gs
-        bp_bytes = bn * (105 + 40) + 20 * op.gs.nperm + 4 * op.gs.nseg
+        if solver.codes is not None:
+            # one rank: nk_bk5_pcg 105 B + nk_cg_update_gs 36 B per point (r in/out,
+            # w, invD, int32 gs code) + the edge/vertex gs (20 B per member)
+            sub = solver.codes[1]
+            nsub = int(sum(int(a) * int(b) for a, b in zip(sub.sizes, sub.nsegs)))
+            bp_bytes = bn * (105 + 36) + 20 * nsub
+        else:
+            # fused schedule: nk_bk5_pcg 105 B + cg_update 40 B per point + gs
+            bp_bytes = bn * (105 + 40) + 20 * op.gs.nperm + 4 * op.gs.nseg
         bdof = bmesh.E * N ** 3
         bp5 = {"gdof_per_s": round(ws * bdof * it / (bp_ms * 1e-3) / 1e9, 3),
                "breakdown_ms_in_situ": None if brk is None else {k: round(v, 4) for k, v in brk.items()},

@@ -305,6 +305,19 @@ int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double*
                  const double* invD, const double* wt, const uint8_t* mult, nk_cg_state* st,
                  double* partials, nk_stream_t stream);
 
+/* Single-rank fused-BP5 update with the face part of the gather-scatter
+ * folded in: w is A p written by nk_bk5_pcg after a gs over the NON-PAIR
+ * segments only (edges, vertices: nk_gs_op_classes on that sub-plan); each
+ * point's assembled value and 1/mult dot weight come from its gs code
+ * [dev, int32, n]: -1 unshared (w, 1); >= 0 the partner of a 2-member
+ * segment (w + w[code], 1/2); <= -2 already assembled (w, 1/M with
+ * M = -code).  Same sums as gs + nk_cg_update's fused form, bit for bit;
+ * face pairs (most shared points) cost one L2 read instead of a gs pass.
+ * Replaces the gs_op + cg_update pair of one PCG iteration
+ * (SPEC.md:479-487). */
+int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
+                    const int32_t* code, nk_cg_state* st, double* partials, nk_stream_t stream);
+
 /* convergence test on st->rr; else beta (Fletcher-Reeves, or Polak-Ribiere
  * -alpha*zap/rz when flexible) and p = z + beta p with z = invD r (or the
  * explicit z [dev, nullable]).  Records hist[iter] = sqrt(rr). */

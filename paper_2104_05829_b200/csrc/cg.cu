@@ -94,22 +94,38 @@ __device__ __forceinline__ void upd_point(double alpha, double& x, double& r, do
   }
 }
 
+// Assembled value of a point of w and its 1/mult dot weight from the
+// per-point gs code (single-rank fused BP5 path, nk_cg_update_gs):
+//   code == -1: unshared                        -> Ap = w[q],          wt = 1
+//   code >= 0 : 2-member segment, partner index -> Ap = w[q] + w[code], wt = 1/2
+//               (a + b == b + a: the bits of the canonical 2-term fold)
+//   code <= -2: member of an M = -code segment already assembled in place
+//               by the gs over the non-pair segments -> Ap = w[q], wt = 1/M
+// rcp: exact 1/m for m < 256 (shared table); larger m divide.
+__device__ __forceinline__ void gs_point(int32_t c, double own, double partner, double& ap,
+                                         double& wq, const double* rcp) {
+  ap = c >= 0 ? own + partner : own;
+  wq = c == -1 ? 1.0 : (c >= 0 ? 0.5 : (c > -256 ? rcp[-c] : 1.0 / (double)(-c)));
+}
+
 // VEC: 16-byte loads of two consecutive points (all vectors 16-B aligned),
 // two pairs in flight per thread per trip for memory-level parallelism.
 // FUSED (BP5 fused path): x and p are not touched -- the deferred x update
 // and the p update live in bk5_pencil_pcg -- and the iteration counter is
 // advanced here.
-template <bool VEC, bool FUSED>
+// GS (implies FUSED): Ap is the pair-unassembled w, assembled per point
+// from the gs code (gs_point) -- generic fallback of nk_cg_update_gs.
+template <bool VEC, bool FUSED, bool GS = false>
 __global__ void __launch_bounds__(kVecThreads)
 cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                  const double* __restrict__ p, const double* __restrict__ Ap,
                  const double* __restrict__ invD, const double* __restrict__ wt,
                  const uint8_t* __restrict__ mult, nk_cg_state* st,
-                 double* __restrict__ partials) {
+                 double* __restrict__ partials, const int32_t* __restrict__ code = nullptr) {
   __shared__ double red[3 * 32];
   __shared__ double rcp_tab[256];  // exact 1/m for the u8 multiplicity weights
   if (st->done) return;
-  if (mult != nullptr) {
+  if (mult != nullptr || GS) {
     for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
     __syncthreads();
   }
@@ -130,10 +146,14 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
     double2 xv = FUSED ? make_double2(0, 0) : reinterpret_cast<const double2*>(x)[q];
     double2 rv = reinterpret_cast<const double2*>(r)[q];
     const double2 pv = FUSED ? make_double2(0, 0) : __ldg(reinterpret_cast<const double2*>(p) + q);
-    const double2 av = __ldg(reinterpret_cast<const double2*>(Ap) + q);
+    double2 av = __ldg(reinterpret_cast<const double2*>(Ap) + q);
     const double2 dv = hz ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
     double2 wv;
-    if (wt) {
+    if (GS) {
+      const int2 cv = __ldg(reinterpret_cast<const int2*>(code) + q);
+      gs_point(cv.x, av.x, cv.x >= 0 ? Ap[cv.x] : 0.0, av.x, wv.x, rcp_tab);
+      gs_point(cv.y, av.y, cv.y >= 0 ? Ap[cv.y] : 0.0, av.y, wv.y, rcp_tab);
+    } else if (wt) {
       wv = __ldg(reinterpret_cast<const double2*>(wt) + q);
     } else if (mult) {  // 1-byte multiplicity: the l2 weight is 1/mult
       const uchar2 mv = __ldg(reinterpret_cast<const uchar2*>(mult) + q);
@@ -158,15 +178,19 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
     for (; q < np; q += nthr) pair(q);
     if ((n & 1) && gtid == 0) {
       const int64_t t = n - 1;
-      double xd = 0.0;
-      upd_point<FUSED>(alpha, FUSED ? xd : x[t], r[t], FUSED ? 0.0 : p[t], Ap[t],
-                       hz ? invD[t] : 0.0, wt ? wt[t] : (mult ? rcp_tab[mult[t]] : 1.0), hz, acc);
+      double xd = 0.0, at = Ap[t], wq = 0.0;
+      if (GS) gs_point(code[t], at, code[t] >= 0 ? Ap[code[t]] : 0.0, at, wq, rcp_tab);
+      else wq = wt ? wt[t] : (mult ? rcp_tab[mult[t]] : 1.0);
+      upd_point<FUSED>(alpha, FUSED ? xd : x[t], r[t], FUSED ? 0.0 : p[t], at,
+                       hz ? invD[t] : 0.0, wq, hz, acc);
     }
   } else {
     for (int64_t q = gtid; q < n; q += nthr) {
-      double xd = 0.0;
-      upd_point<FUSED>(alpha, FUSED ? xd : x[q], r[q], FUSED ? 0.0 : p[q], Ap[q],
-                       hz ? invD[q] : 0.0, wt ? wt[q] : (mult ? rcp_tab[mult[q]] : 1.0), hz, acc);
+      double xd = 0.0, aq = Ap[q], wq = 0.0;
+      if (GS) gs_point(code[q], aq, code[q] >= 0 ? Ap[code[q]] : 0.0, aq, wq, rcp_tab);
+      else wq = wt ? wt[q] : (mult ? rcp_tab[mult[q]] : 1.0);
+      upd_point<FUSED>(alpha, FUSED ? xd : x[q], r[q], FUSED ? 0.0 : p[q], aq,
+                       hz ? invD[q] : 0.0, wq, hz, acc);
     }
   }
   double v[3] = {acc.rr, acc.rz, acc.zap};
@@ -186,6 +210,90 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
       st->zap = s[2];
       st->alpha = alpha;
       if (FUSED) st->iter = st->iter + 1;
+    }
+  }
+}
+
+// nk_cg_update_gs, 16-B path: the cg_update_kernel<true, true, true> loop
+// restructured so that every load of a trip is issued before any is used
+// -- codes, r, w, invD of U pairs, then the pair partners -- instead of a
+// dependent chain per point; same per-thread point order and accumulation
+// as the generic form (bit-identical sums).  80 registers -> 3 CTAs/SM.
+__global__ void __launch_bounds__(kVecThreads, 4)
+cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restrict__ w,
+                        const double* __restrict__ invD, const int32_t* __restrict__ code,
+                        nk_cg_state* st, double* __restrict__ partials) {
+  __shared__ double red[3 * 32];
+  __shared__ double rcp_tab[256];
+  if (st->done) return;
+  for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
+  __syncthreads();
+  const double pAp = st->pAp;
+  if (!(pAp > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->breakdown = 1;
+      st->done = 1;
+    }
+    return;
+  }
+  const double alpha = st->rz / pAp;
+  const bool hz = invD != nullptr;
+  UpdAcc acc;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t np = n >> 1;
+  constexpr int U = 1;
+  for (int64_t q0 = gtid; q0 < np; q0 += U * nthr) {
+    int2 cv[U];
+    double2 rv[U], av[U], dv[U], pv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * nthr;
+      const bool ok = q < np;
+      cv[u] = ok ? __ldg(reinterpret_cast<const int2*>(code) + q) : make_int2(-1, -1);
+      rv[u] = ok ? reinterpret_cast<const double2*>(r)[q] : make_double2(0, 0);
+      av[u] = ok ? __ldg(reinterpret_cast<const double2*>(w) + q) : make_double2(0, 0);
+      dv[u] = (ok && hz) ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      pv[u] = make_double2(cv[u].x >= 0 ? w[cv[u].x] : 0.0, cv[u].y >= 0 ? w[cv[u].y] : 0.0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * nthr;
+      if (q >= np) break;
+      double2 wv;
+      gs_point(cv[u].x, av[u].x, pv[u].x, av[u].x, wv.x, rcp_tab);
+      gs_point(cv[u].y, av[u].y, pv[u].y, av[u].y, wv.y, rcp_tab);
+      double xd = 0.0;
+      upd_point<true>(alpha, xd, rv[u].x, 0.0, av[u].x, dv[u].x, wv.x, hz, acc);
+      upd_point<true>(alpha, xd, rv[u].y, 0.0, av[u].y, dv[u].y, wv.y, hz, acc);
+      reinterpret_cast<double2*>(r)[q] = rv[u];
+    }
+  }
+  if ((n & 1) && gtid == 0) {
+    const int64_t t = n - 1;
+    double xd = 0.0, at = 0.0, wq = 0.0;
+    gs_point(code[t], w[t], code[t] >= 0 ? w[code[t]] : 0.0, at, wq, rcp_tab);
+    upd_point<true>(alpha, xd, r[t], 0.0, at, hz ? invD[t] : 0.0, wq, hz, acc);
+  }
+  double v[3] = {acc.rr, acc.rz, acc.zap};
+  block_sum<3>(v, red);
+  const int nb = gridDim.x;
+  if (threadIdx.x == 0) {
+    partials[0 * kVecMaxBlocks + blockIdx.x] = v[0];
+    partials[1 * kVecMaxBlocks + blockIdx.x] = v[1];
+    partials[2 * kVecMaxBlocks + blockIdx.x] = v[2];
+  }
+  if (last_block(&st->ticket[1], nb)) {
+    double sres[3];
+    reduce_partials<3>(partials, nb, kVecMaxBlocks, sres, red);
+    if (threadIdx.x == 0) {
+      st->rr = sres[0];
+      if (hz) st->rz_new = sres[1];
+      st->zap = sres[2];
+      st->alpha = alpha;
+      st->iter = st->iter + 1;
     }
   }
 }
@@ -327,6 +435,23 @@ extern "C" int nk_cg_update(int64_t n, double* x, double* r, const double* p, co
     cg_update_kernel<false, false><<<g, kVecThreads, 0, s>>>(n, x, r, p, Ap, invD, wt, mult, st, partials);
   }
   return check_launch("cg_update");
+}
+
+extern "C" int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
+                               const int32_t* code, nk_cg_state* st, double* partials,
+                               nk_stream_t stream) {
+  if (n < 0 || !r || !w || !code || !st || !partials) {
+    set_error("cg_update_gs: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  const unsigned g = (unsigned)vec_grid(n);
+  cudaStream_t s = S(stream);
+  if (aligned16(r, w, invD) && ((uintptr_t)code & 7) == 0)
+    cg_update_gs_vec_kernel<<<g, kVecThreads, 0, s>>>(n, r, w, invD, code, st, partials);
+  else
+    cg_update_kernel<false, true, true><<<g, kVecThreads, 0, s>>>(
+        n, nullptr, r, nullptr, w, invD, nullptr, nullptr, st, partials, code);
+  return check_launch("cg_update_gs");
 }
 
 extern "C" int nk_cg_pupdate(int64_t n, const double* r, double* p, const double* invD,

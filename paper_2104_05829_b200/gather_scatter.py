@@ -116,6 +116,36 @@ class GatherScatterHandle:
         return self.perm_h.astype(np.int64), self.seg_h.astype(np.int64)
 
 
+def point_codes(h):
+    """Per-point gs codes for the fused single-rank CG update
+    (nk_cg_update_gs, include/nekb200.h) and the gs sub-plan of the non-pair
+    segments it relies on: returns (code, plan) -- code an int32 device
+    tensor (-1 unshared, the partner's index for a 2-member segment, -M for
+    a member of an M >= 3 segment), plan a _Plan over the segments of 3 or
+    more members (run it before the update).  None with several ranks or
+    n >= 2^31.  Cached on the handle."""
+    import torch
+    if getattr(h, "_codes", False) is not False:
+        return h._codes
+    res = None
+    if (h.comm is None or h.comm.size == 1) and h.n < 2 ** 31:
+        perm = h.perm_h.astype(np.int64)
+        seg = h.seg_h.astype(np.int64)
+        sizes = np.diff(seg)
+        code = np.full(h.n, -1, dtype=np.int32)
+        two = seg[:-1][sizes == 2]
+        a, b = perm[two], perm[two + 1]
+        code[a], code[b] = b, a
+        sel = np.flatnonzero(sizes > 2)
+        cnt = sizes[sel]
+        mem = perm[_dist._ranges(seg[sel], cnt)] if len(sel) else np.zeros(0, np.int64)
+        code[mem] = -np.repeat(cnt, cnt)
+        sub_seg = np.r_[0, np.cumsum(cnt)].astype(np.int64)
+        res = (torch.as_tensor(code, device=h.device), _Plan(mem, sub_seg, h.device))
+    h._codes = res
+    return res
+
+
 def gs_setup(ids, comm=None, nq=None, device="cuda"):
     """Build the gs plan from global ids of this rank's local points
     (SPEC.md:192-200).  ids <= 0 and ids held once (over all ranks) are

@@ -153,10 +153,11 @@ class PoissonOperator:
         COUNTERS.add("stiffness", bk5_flops(m.N, m.E, self.ncomp), 7 * self.n * self.ncomp)
         return w
 
-    def apply_pcg(self, p, w, x, r, invD, st, partials, hist):
+    def apply_pcg(self, p, w, x, r, invD, st, partials, hist, gs=True):
         """Fused BP5 operator step (nk_bk5_pcg): convergence test, deferred
         x += alpha p, Jacobi p = invD r + beta p, then w = A p with p^T A p
-        into st->pAp -- followed by gs (and the halo on several ranks)."""
+        into st->pAp -- followed by gs (and the halo on several ranks).
+        gs=False (one rank) leaves w unassembled for nk_cg_update_gs."""
         m = self.mesh
         L, s = lib(), stream_ptr()
         D = m.basis.diff
@@ -174,7 +175,8 @@ class PoissonOperator:
         if not multi:
             nb = int(L.nk_bk5_pcg_blocks(m.N, m.E))
             k1(None, 0, nb)
-            _local(g, w, "+", 1, st=st)
+            if gs:
+                _local(g, w, "+", 1, st=st)
         else:
             import torch
             be, ie = g.boundary_elements, g.interior_elements
@@ -239,10 +241,13 @@ class FusedPCG:
     all-reduce), then replays a CUDA graph of ``chunk`` iterations until the
     device flag ``done`` is set.  Per iteration: nk_bk5_pcg (convergence
     test, deferred x update, Jacobi p update, BK5, p.Ap), gs, [halo],
-    nk_cg_update (r, rr, rz, zAp) -- 3 kernels on one rank."""
+    nk_cg_update (r, rr, rz, zAp).  On one rank the face pairs of the gs fold
+    into the update (nk_cg_update_gs: a point of a 2-member segment adds its
+    partner's w on the fly; the gs pass only covers edge / vertex segments)
+    -- bit-identical; fuse_gs=False keeps the full gs pass."""
 
     def __init__(self, op, prec, tol=1e-8, max_iter=1000, flexible=False, chunk=16,
-                 use_graph=True):
+                 use_graph=True, fuse_gs=True):
         import torch
         self.op, self.prec = op, prec
         self.tol, self.max_iter, self.flexible = float(tol), int(max_iter), bool(flexible)
@@ -276,7 +281,11 @@ class FusedPCG:
         self.comm = op.gs.comm if (op.gs.comm is not None and op.gs.comm.size > 1) else None
         self.s64 = self.st.view(torch.float64)   # rz pAp rz_new rr zap bb thresh2 alpha
         self.graph = None
-        self.launches_per_iter = 3
+        self.codes = None
+        if fuse_gs and self.comm is None:
+            from .gather_scatter import point_codes
+            self.codes = point_codes(op.gs)
+        self.launches_per_iter = 3    # bk5_pcg, gs (all | non-pair segments), update
 
     def _allreduce(self, a, b):
         if self.comm is not None:
@@ -286,6 +295,14 @@ class FusedPCG:
         """One PCG iteration = 3 kernels on one rank: nk_bk5_pcg (test,
         x/p updates, BK5, p.Ap), gs, nk_cg_update (r, rr, rz, zAp)."""
         L, s = lib(), stream_ptr()
+        if self.codes is not None:
+            self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
+                              self.part_bk5, self.hist, gs=False)
+            self.codes[1].run(self.w, "+", 1, self.n, self.st)          # edges, vertices
+            check(L.nk_cg_update_gs(self.n, ptr(self.r), ptr(self.w), ptr(self.invD),
+                                    ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
+                  "cg_update_gs")
+            return
         self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st, self.part_bk5,
                           self.hist)
         self._allreduce(1, 2)                                            # pAp
@@ -309,7 +326,8 @@ class FusedPCG:
         import torch
         L, s = lib(), stream_ptr()
         op, g = self.op, self.op.gs
-        names = ("bk5_pcg", "gs", "cg_update")
+        fused = self.codes is not None
+        names = ("bk5_pcg", "gs_nonpair", "cg_update_gs") if fused else ("bk5_pcg", "gs", "cg_update")
         acc = dict.fromkeys(names, 0.0)
         st_save = self.st.clone()
         m = op.mesh
@@ -323,12 +341,20 @@ class FusedPCG:
                                None, 0, ptr(self.x), ptr(self.r), ptr(self.invD), ptr(self.st),
                                ptr(self.part_bk5), 0, nb, ptr(self.hist), s), "bk5_pcg")
             ev[1].record()
-            _local(g, self.w, "+", 1, st=self.st)
-            ev[2].record()
-            check(L.nk_cg_update(self.n, None, ptr(self.r), None, ptr(self.w), ptr(self.invD),
-                                 ptr(self.wt), ptr(self.mult), ptr(self.st), ptr(self.part_cg),
-                                 s), "cg_update")
-            ev[3].record()
+            if fused:
+                self.codes[1].run(self.w, "+", 1, self.n, self.st)
+                ev[2].record()
+                check(L.nk_cg_update_gs(self.n, ptr(self.r), ptr(self.w), ptr(self.invD),
+                                        ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
+                      "cg_update_gs")
+                ev[3].record()
+            else:
+                _local(g, self.w, "+", 1, st=self.st)
+                ev[2].record()
+                check(L.nk_cg_update(self.n, None, ptr(self.r), None, ptr(self.w),
+                                     ptr(self.invD), ptr(self.wt), ptr(self.mult), ptr(self.st),
+                                     ptr(self.part_cg), s), "cg_update")
+                ev[3].record()
             torch.cuda.synchronize()
             for q, nm in enumerate(names):
                 acc[nm] += ev[q].elapsed_time(ev[q + 1])

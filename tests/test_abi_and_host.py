@@ -77,6 +77,39 @@ def test_native_plan_builder_random_ids(L):
         assert np.array_equal(perm, operm) and np.array_equal(seg, oseg)
 
 
+@pytest.mark.parametrize("counts,N,bc", [((3, 2, 2), 3, "dirichlet"), ((3, 3, 3), 2, "periodic"),
+                                         ((2, 1, 1), 1, "neumann")])
+def test_point_codes_assemble_like_gs(L, counts, N, bc):
+    """The per-point gs codes of the fused CG update (nk_cg_update_gs): the
+    non-pair sub-plan covers exactly the segments of 3+ members in canonical
+    order; pair folding (w + w[partner]) on top of the oracle's gs over those
+    segments reproduces the full QQ^T bit for bit; weights are 1/mult."""
+    import types
+    from paper_2104_05829_b200.gather_scatter import _local_plan, point_codes
+    ids = om.build_box_mesh((1, 1, 1), counts, N, bc=bc).ids
+    perm, seg = _local_plan(ids)
+    h = types.SimpleNamespace(perm_h=perm, seg_h=seg, n=len(ids), comm=None, device="cpu")
+    code_t, sub = point_codes(h)
+    code = code_t.numpy()
+    w = np.random.default_rng(5).standard_normal(len(ids))
+    # host replay of the sub-plan: fold each 3+ segment in canonical order
+    wg = w.copy()
+    sizes = np.diff(seg)
+    for s0, M in zip(seg[:-1], sizes):
+        if M > 2:
+            mem = perm[s0:s0 + M]
+            acc = w[mem[0]]
+            for j in range(1, M):
+                acc = acc + w[mem[j]]
+            wg[mem] = acc
+    ap = np.where(code >= 0, wg + wg[np.maximum(code, 0)], wg)
+    wt = np.where(code == -1, 1.0, np.where(code >= 0, 0.5, 1.0 / np.abs(code)))
+    assert np.array_equal(ap, ogs.gs_op(ids, w))
+    assert np.array_equal(wt, 1.0 / ogs.multiplicity(ids))
+    assert int(sub.nseg) == int(np.sum(sizes > 2))
+    assert point_codes(h) is h._codes                          # cached
+
+
 def test_product_basis_bitwise_reference(golden_basis):
     from paper_2104_05829_b200 import basis as pb
     for N in range(1, 17):

@@ -273,6 +273,37 @@ def test_fused_pcg_deterministic_and_graph_equivalent():
     assert r3.iterations == r1.iterations and np.array_equal(x1, r3.x.cpu().numpy())
 
 
+@pytest.mark.parametrize("counts,N,bc,lam1", [((4, 4, 4), 7, "dirichlet", 0.0),
+                                              ((3, 4, 2), 3, "periodic", 1.0),
+                                              ((6, 5, 4), 1, "dirichlet", 0.0),
+                                              ((3, 3, 3), 2, "neumann", 0.5),
+                                              ((2, 2, 3), 12, "dirichlet", 0.0)])
+def test_fused_gs_update_bit_identical(counts, N, bc, lam1):
+    """nk_cg_update_gs (face pairs folded into the CG update, gs pass over
+    edge/vertex segments only) against the full-gs schedule (bk5_pcg, gs,
+    cg_update): same iterations, residual history and solution bit for bit;
+    and the answer solves the system."""
+    m, o = both_meshes(counts, N, bc=bc)
+    op = nk.PoissonOperator(m, lam1=lam1)
+    jac = nk.JacobiPreconditioner(op)
+    rng = np.random.default_rng(N)
+    b = torch.as_tensor(o.mask.ravel() * ogs.gs_op(o.ids, rng.standard_normal(m.n_local)),
+                        device="cuda")
+    s2 = nk.FusedPCG(op, jac, tol=1e-9, max_iter=2000)
+    assert s2.codes is not None and s2.launches_per_iter == 3
+    s3 = nk.FusedPCG(op, jac, tol=1e-9, max_iter=2000, fuse_gs=False)
+    assert s3.codes is None
+    r2, r3 = s2.solve(b), s3.solve(b)
+    assert r2.converged and r2.iterations == r3.iterations
+    assert r2.residual_history == r3.residual_history
+    assert torch.equal(r2.x, r3.x)
+    Ax = torch.empty_like(b)
+    op(r2.x.reshape(-1), out=Ax)
+    assert float(torch.linalg.norm(Ax - b)) <= 2e-9 * float(torch.linalg.norm(b))
+    prof = s2.profile_iteration(reps=2)
+    assert set(prof) == {"bk5_pcg", "gs_nonpair", "cg_update_gs"}
+
+
 def test_native_library_loaded():
     import os
     assert os.path.exists(_lib.LIB_PATH)
@@ -417,10 +448,10 @@ def test_fused_pcg_u8_multiplicity_weights():
     b, _, _, _ = _oracle_problem(o)
     op = nk.PoissonOperator(m)
     jac = nk.JacobiPreconditioner(op)
-    s1 = nk.FusedPCG(op, jac, tol=1e-8)
+    s1 = nk.FusedPCG(op, jac, tol=1e-8, fuse_gs=False)
     r1 = s1.solve(dev(b))
     x1 = r1.x.cpu().numpy().copy()
-    s2 = nk.FusedPCG(op, jac, tol=1e-8)
+    s2 = nk.FusedPCG(op, jac, tol=1e-8, fuse_gs=False)
     s2.wt, s2.mult = None, op.multiplicity_u8
     r2 = s2.solve(dev(b))
     assert r1.iterations == r2.iterations
