@@ -72,7 +72,7 @@ static int kvariant_for(int N) {
   const int v = nk_bk5_variant_get();
   if (v == 1 || v == 3 || v == 4 || v == 5) return v;
   switch (N) {
-    case 2: case 6: case 8: case 9: case 13: case 14: case 15: return 5;
+    case 2: case 6: case 8: case 14: case 15: return 5;
     default: return 3;
   }
 }

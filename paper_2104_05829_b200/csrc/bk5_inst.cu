@@ -44,14 +44,16 @@ int run(int64_t nlist, const int32_t* elist, const double* D, const double* G, c
                                          st, partials, part_base, reduce_count, s, pf_dist);
 }
 
-// Default shapes: small CTAs (64-128 threads), as many resident as the
-// register cap (~80-128 regs) and shared memory allow.
+// Default shapes: one element per CTA; MINB from the order sweep
+// (profiles/r1k_high_shapes.jsonl): at NQ >= 10 a lower MINB (higher register
+// cap, no spills) beats the extra resident CTAs -- multi-element CTAs, which
+// would pack NQ^2 threads into whole warps, spill and lose at every order.
 template <int NQ> struct PencilDefault;
 #define NK_PD(NQ_, EPB_, MINB_) \
   template <> struct PencilDefault<NQ_> { static constexpr int EPB = EPB_, MINB = MINB_; };
 NK_PD(2, 32, 8) NK_PD(3, 14, 6) NK_PD(4, 4, 12) NK_PD(5, 5, 6) NK_PD(6, 2, 10) NK_PD(7, 2, 8)
-NK_PD(8, 1, 10) NK_PD(9, 1, 8) NK_PD(10, 1, 6) NK_PD(11, 1, 5) NK_PD(12, 1, 4) NK_PD(13, 1, 3)
-NK_PD(14, 1, 3) NK_PD(15, 1, 2) NK_PD(16, 1, 2)
+NK_PD(8, 1, 10) NK_PD(9, 1, 8) NK_PD(10, 1, 5) NK_PD(11, 1, 4) NK_PD(12, 1, 3) NK_PD(13, 1, 2)
+NK_PD(14, 1, 2) NK_PD(15, 1, 2) NK_PD(16, 1, 2)
 #undef NK_PD
 
 template <int NQ, int EPB, int MINB>
@@ -76,17 +78,50 @@ NK_P2D(7, 2, 5) NK_P2D(8, 1, 8) NK_P2D(9, 1, 5) NK_P2D(10, 1, 4) NK_P2D(11, 1, 4
 NK_P2D(12, 1, 3) NK_P2D(13, 1, 3) NK_P2D(14, 1, 2) NK_P2D(15, 1, 2) NK_P2D(16, 1, 2)
 #undef NK_P2D
 
+
+// Alternative (EPB, MINB) shapes for NQ >= 9, selected by nk_bk5_tune(cfg = 11..14)
+// for the order sweep (scripts/bk5_sweep.py --high-shapes): several elements per
+// CTA pack NQ^2-thread elements into whole warps (e.g. NQ = 13: 169 -> 192
+// threads, 2 x 169 -> 352).
+template <int NQ> struct PencilAlt {
+  static constexpr int E[4] = {1, 1, 1, 1}, M[4] = {1, 1, 1, 1};
+};
+#define NK_ALT(NQ_, e0, m0, e1, m1, e2, m2, e3, m3)                 \
+  template <> struct PencilAlt<NQ_> {                               \
+    static constexpr int E[4] = {e0, e1, e2, e3}, M[4] = {m0, m1, m2, m3}; \
+  };
+NK_ALT(9, 1, 6, 1, 5, 1, 4, 1, 3) NK_ALT(10, 1, 5, 1, 4, 1, 3, 1, 2)
+NK_ALT(11, 1, 4, 1, 3, 1, 2, 1, 1) NK_ALT(12, 1, 3, 1, 2, 1, 1, 2, 1)
+NK_ALT(13, 1, 2, 1, 1, 2, 1, 1, 4) NK_ALT(14, 1, 2, 1, 1, 2, 1, 1, 4)
+NK_ALT(15, 1, 1, 1, 3, 2, 1, 1, 4) NK_ALT(16, 1, 1, 2, 1, 1, 3, 1, 4)
+#undef NK_ALT
+
 template <int NQ>
 int run_pencil2(int cfg, int64_t nlist, const int32_t* elist, const double* D, const double* G,
                 const double* u, double* w, double lam0, const double* B, double lam1,
                 const uint8_t* mask, nk_cg_state* st, double* partials, int64_t part_base,
                 int64_t reduce_count, cudaStream_t s, int64_t* nb, int pfG) {
+  if constexpr (NQ >= 9) {
+    if (cfg >= 11 && cfg <= 14) {
+      using A = PencilAlt<NQ>;
+#define NK_P2ALT(K)                                                                           \
+  if (cfg == 11 + K) {                                                                        \
+    if (nb) {                                                                                 \
+      *nb = (nlist + A::E[K] - 1) / A::E[K];                                                  \
+      return NK_OK;                                                                           \
+    }                                                                                         \
+    return launch_pencil2<NQ, A::E[K], A::M[K]>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, \
+                                                st, partials, part_base, reduce_count, s, pfG); \
+  }
+      NK_P2ALT(0) NK_P2ALT(1) NK_P2ALT(2) NK_P2ALT(3)
+#undef NK_P2ALT
+    }
+  }
   constexpr int EPB = Pencil2Default<NQ>::EPB, MINB = Pencil2Default<NQ>::MINB;
   if (nb) {
     *nb = (nlist + EPB - 1) / EPB;
     return NK_OK;
   }
-  (void)cfg;
   return launch_pencil2<NQ, EPB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st,
                                        partials, part_base, reduce_count, s, pfG);
 }
@@ -111,6 +146,16 @@ int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, co
       default: return runp<8, 1, 10>(NK_PARGS);   // measured best (sweep16)
     }
   } else {
+    if constexpr (NQ >= 9) {
+      using A = PencilAlt<NQ>;
+      switch (cfg) {
+        case 11: return runp<NQ, A::E[0], A::M[0]>(NK_PARGS);
+        case 12: return runp<NQ, A::E[1], A::M[1]>(NK_PARGS);
+        case 13: return runp<NQ, A::E[2], A::M[2]>(NK_PARGS);
+        case 14: return runp<NQ, A::E[3], A::M[3]>(NK_PARGS);
+        default: break;
+      }
+    }
     return runp<NQ, PencilDefault<NQ>::EPB, PencilDefault<NQ>::MINB>(NK_PARGS);
   }
 #undef NK_PARGS

@@ -65,6 +65,8 @@ def main():
     ap.add_argument("--orders", action="store_true")
     ap.add_argument("--low", action="store_true", help="N = 1, 2 variant comparison")
     ap.add_argument("--probe", action="store_true")
+    ap.add_argument("--high-shapes", default=None,
+                    help="comma list of orders: pencil / pencil2 x CTA shapes (cfg 0, 11..14)")
     ap.add_argument("--helm3", action="store_true")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--out", default=None)
@@ -180,6 +182,26 @@ def main():
                       "ms_best": round(best, 5), "GBs": round(bytes_ / med / 1e6, 1),
                       "frac": round(bytes_ / med / 1e6 / pk, 4),
                       "gdofs": round(m.E * 343 / med / 1e6, 3), "bitwise_same": same})
+        L.nk_bk5_tune(0, 0)
+        L.nk_bk5_set_variant(0)
+    if args.high_shapes:
+        for N in [int(x) for x in args.high_shapes.split(",")]:
+            ne = E_FOR_N[N]
+            m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
+            ref = None
+            for variant in (3, 5):
+                for cfg in (0, 11, 12, 13, 14):
+                    L.nk_bk5_set_variant(variant)
+                    L.nk_bk5_tune(cfg, 1)
+                    med, best, w = time_bk5(nk, L, m, args.reps, flush)
+                    if ref is None:
+                        ref = w.clone()
+                    same = bool(torch.equal(ref, w))
+                    bytes_ = 64 * m.n_local
+                    emit({"sweep": "high_shape", "N": N, "E": m.E, "variant": variant, "cfg": cfg,
+                          "ms_med": round(med, 5), "frac": round(bytes_ / med / 1e6 / pk, 4),
+                          "gdofs": round(m.E * N ** 3 / med / 1e6, 3), "bitwise_same": same})
+            del m
         L.nk_bk5_tune(0, 0)
         L.nk_bk5_set_variant(0)
     if args.orders or args.low:
