@@ -116,19 +116,36 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
     return NK_ERR_INVALID;
   }
   cudaStream_t s = S(stream);
-  // 3-component batches: the batched pencil3 kernel (G read once) is
-  // issue-bound; three scalar launches (G read three times) measured faster
-  // at every order but N = 7 (scripts/helm3_compare.py: N = 5 / 9 batched
-  // 1.06x / 1.08-1.16x slower, N = 7 0.96x), so auto runs the scalar kernel
-  // per component there.
-  if (ncomp == 3 && nk_bk5_variant_get() == 0 && N != 7 && st == nullptr) {
-    for (int c = 0; c < 3; ++c) {
-      int rc = kslab_table[N](1, n, elem_list, D, G, u + c * comp_stride, w + c * comp_stride,
-                              lam0, B, lam1, comp_stride, mask, nullptr, nullptr, 0, 0, s,
-                              nullptr, g_cfg, g_pf, kvariant_for(N));
-      if (rc != NK_OK) return rc;
+  // 3-component batches (vector Helmholtz), measured per order on the B200
+  // (scripts/bk5_sweep.py --helm3, profiles/r1k_helm3.jsonl):
+  //   seq3    -- bk5_pencil<NC = 3>: the three components back to back in one
+  //              CTA, G from HBM once and re-read from L2 (N = 3, 5, 7, 10, 11);
+  //   pencil3 -- the three components interleaved, G in registers once
+  //              (N = 4, 6);
+  //   scalar  -- three scalar launches, G read three times (N = 1, 2, 8, 9,
+  //              12..15, where both batched forms spill or lose occupancy).
+  // A forced variant (nk_bk5_set_variant) keeps its own kernel: 6 = seq3,
+  // any other = pencil3 / k-slab as before.
+  if (ncomp == 3 && st == nullptr) {
+    int v = nk_bk5_variant_get();
+    if (v == 0) {
+      switch (N) {
+        case 3: case 5: case 7: case 10: case 11: v = 6; break;
+        case 4: case 6: v = 3; break;
+        default: v = -1; break;
+      }
+      if (v == -1) {
+        for (int c = 0; c < 3; ++c) {
+          int rc = kslab_table[N](1, n, elem_list, D, G, u + c * comp_stride,
+                                  w + c * comp_stride, lam0, B, lam1, comp_stride, mask, nullptr,
+                                  nullptr, 0, 0, s, nullptr, g_cfg, g_pf, kvariant_for(N));
+          if (rc != NK_OK) return rc;
+        }
+        return NK_OK;
+      }
     }
-    return NK_OK;
+    return kslab_table[N](3, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, nullptr,
+                          nullptr, 0, 0, s, nullptr, g_cfg, g_pf, v);
   }
   return kslab_table[N](ncomp, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, st,
                         partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf,

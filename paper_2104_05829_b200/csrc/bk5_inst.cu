@@ -230,6 +230,16 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
 #undef NK_TARGS
     }
   }
+  if (ncomp == 3 && st == nullptr && variant == 6) {
+    // 3 components back to back per CTA, G from HBM once (bk5_pencil NC = 3)
+    constexpr int EPB = PencilDefault<NQ>::EPB, MINB = PencilDefault<NQ>::MINB;
+    if (nblocks) {
+      *nblocks = (nlist + EPB - 1) / EPB;
+      return NK_OK;
+    }
+    return launch_pencil<NQ, EPB, MINB, 3>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, nullptr,
+                                           nullptr, 0, 0, s, pf_dist, cstride);
+  }
   if constexpr (NQ >= 2 && NQ <= 12) {
     // 3-component batch: G read once per element (pencil3); k-slab otherwise
     if (ncomp == 3 && variant != 1) {

@@ -82,13 +82,20 @@ __device__ __forceinline__ void matvec(const DParam<NQ>& D, const double (&v)[NQ
   }
 }
 
-template <int NQ, int EPB, int MINB>
+// NC = 3: the three velocity components of one element run back to back in
+// the same CTA (vector Helmholtz): G is fetched from HBM once
+// (L2 prefetch at CTA start) and re-read from L2 by components 1 and 2, so HBM
+// moves 104 B per point for three components instead of 3 x 72, while the
+// register and shared footprint stays that of the scalar kernel.
+template <int NQ, int EPB, int MINB, int NC = 1>
 __global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
 bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
-           const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
+           const double* __restrict__ G, const double* __restrict__ u_, double* __restrict__ w_,
            double lam0, const double* __restrict__ B, double lam1,
            const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
-           int64_t part_base, int64_t reduce_count, int pfG, int64_t pf_ahead) {
+           int64_t part_base, int64_t reduce_count, int pfG, int64_t pf_ahead,
+           int64_t cstride = 0) {
+  static_assert(NC == 1 || NC == 3, "NC");
   using L = PencilLayout<NQ>;
   constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, VOL = L::VOL;
   extern __shared__ double smem[];
@@ -106,7 +113,11 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   const int64_t slot = (int64_t)blockIdx.x * EPB + le;
   const bool active = slot < nlist;
   const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
-  const double* ue = u + e * NQ3;
+  if (NC > 1 && active && tt == 0) {
+#pragma unroll
+    for (int c = 1; c < NC; ++c)
+      prefetch_l2(u_ + c * cstride + e * NQ3, NQ3 * (int64_t)sizeof(double));
+  }
   // Start this element's G (75% of its bytes) streaming into L2 now, so the
   // G-phase loads after F1-F3 hit L2 instead of waiting on HBM.
   if (pfG && active && tt == 0) prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
@@ -114,8 +125,16 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   if (pf_ahead > 0 && tt == 0 && slot + pf_ahead < nlist) {
     const int64_t ea = elist ? (int64_t)elist[slot + pf_ahead] : slot + pf_ahead;
     prefetch_l2(G + ea * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
-    prefetch_l2(u + ea * NQ3, NQ3 * (int64_t)sizeof(double));
+    prefetch_l2(u_ + ea * NQ3, NQ3 * (int64_t)sizeof(double));
   }
+
+  double dot = 0.0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+  const double* u = u_ + c * cstride;
+  double* w = w_ + c * cstride;
+  const double* ue = u + e * NQ3;
+  if (NC > 1 && c > 0) __syncthreads();  // previous component's B1 reads of R / U
 
   // ---- F1: i-pencils (j = a, k = b)
   if (active) {
@@ -193,7 +212,6 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   }
   __syncthreads();
   // ---- B1: i-pencils (j = a, k = b): w = D^T gr + (ws + wt), epilogue
-  double dot = 0.0;
   if (active) {
     double v[NQ], o[NQ];
 #pragma unroll
@@ -233,6 +251,7 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
     }
   }
 
+  }  // components
   if (st != nullptr) {
     double vv[1] = {dot};
     block_sum<1>(vv, red);
@@ -245,18 +264,18 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   }
 }
 
-template <int NQ, int EPB, int MINB>
+template <int NQ, int EPB, int MINB, int NC = 1>
 static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhost,
                          const double* G, const double* u, double* w, double lam0,
                          const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
                          double* partials, int64_t part_base, int64_t reduce_count,
-                         cudaStream_t s, int pfG) {
+                         cudaStream_t s, int pfG, int64_t cstride = 0) {
   using C = PencilCfg<NQ, EPB, MINB>;
   static int64_t resident = -1;  // CTAs resident on the device (one wave)
   const size_t smem = C::smem_bytes();
   static bool configured = false;
   if (!configured) {
-    cudaError_t err = cudaFuncSetAttribute(bk5_pencil<NQ, EPB, MINB>,
+    cudaError_t err = cudaFuncSetAttribute(bk5_pencil<NQ, EPB, MINB, NC>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) {
       set_error("bk5_pencil: smem attribute (%zu B): %s", smem, cudaGetErrorString(err));
@@ -270,7 +289,7 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil<NQ, EPB, MINB>, C::THREADS,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil<NQ, EPB, MINB, NC>, C::THREADS,
                                                   smem);
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
@@ -278,9 +297,9 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
   for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
   // pfG: 0 off, 1 own G into L2, 2 own G + the element one wave ahead
   const int64_t ahead = pfG >= 2 ? resident * EPB : 0;
-  bk5_pencil<NQ, EPB, MINB><<<(unsigned)nblk, C::THREADS, smem, s>>>(
+  bk5_pencil<NQ, EPB, MINB, NC><<<(unsigned)nblk, C::THREADS, smem, s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG,
-      ahead);
+      ahead, cstride);
   return check_launch("bk5_pencil");
 }
 

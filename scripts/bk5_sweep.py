@@ -134,7 +134,8 @@ def main():
     if args.helm3:
         from paper_2104_05829_b200._lib import ptr
         s = torch.cuda.current_stream()
-        for N, ne in ((9, 16), (7, 20), (5, 29)):
+        for N in range(1, 16):
+            ne = E_FOR_N[N]
             m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
             n = m.n_local
             u3 = torch.randn(3 * n, dtype=torch.float64, device="cuda")
@@ -148,7 +149,19 @@ def main():
                     L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), u3.data_ptr() + 8 * c * n,
                              w3.data_ptr() + 8 * c * n, lam0, ptr(m.B), lam1, 1, n, None, None,
                              0, None, None, 0, 0, s.cuda_stream)
-            for name, fn, bpp in (("batched3", batched, 104), ("3x scalar", separate, 216)):
+            def pencil3():
+                L.nk_bk5_set_variant(3)
+                batched()
+                L.nk_bk5_set_variant(0)
+            def seq3():
+                L.nk_bk5_set_variant(6)
+                batched()
+                L.nk_bk5_set_variant(0)
+            outs = {}
+            cands = [("3x scalar", separate, 216), ("seq3", seq3, 104), ("auto", batched, 104)]
+            if N <= 11:
+                cands.append(("pencil3", pencil3, 104))
+            for name, fn, bpp in cands:
                 ts = []
                 for rep in range(args.reps + 5):
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -159,7 +172,9 @@ def main():
                     ts.append((a, b))
                 torch.cuda.synchronize()
                 ms = statistics.median([a.elapsed_time(b) for a, b in ts[5:]])
+                outs[name] = w3.clone()
                 emit({"sweep": "helm3", "N": N, "E": m.E, "kernel": name, "ms_med": round(ms, 5),
+                      "bitwise_same_as_scalar": bool(torch.equal(outs["3x scalar"], w3)),
                       "alg_bytes_per_pt": bpp,
                       "frac_of_own_bytes": round(bpp * n / ms / 1e6 / pk, 4),
                       "gdofs_3comp": round(3 * m.E * N ** 3 / ms / 1e6, 3)})

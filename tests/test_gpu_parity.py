@@ -102,6 +102,35 @@ def test_bk5_helmholtz_and_batched(N):
     assert rel_l2(w1, oop.bk5(o.basis.diff, o.G, u[1], lam0=lam0, B=o.B, lam1=lam1)) < BK5_TOL
 
 
+@pytest.mark.parametrize("N", list(range(1, 16)))
+def test_bk5_helmholtz3_auto_and_seq3(N):
+    """3-component batches at every order: the auto table (seq3 / pencil3 /
+    three scalar launches, bk5.cu) vs the oracle, and the seq3 kernel
+    (bk5_pencil NC = 3) bitwise equal to three scalar pencil launches."""
+    from paper_2104_05829_b200 import kernels as K
+    from paper_2104_05829_b200._lib import lib
+    counts = (3, 2, 2) if N <= 9 else (2, 2, 1)
+    m, o = both_meshes(counts, N)
+    rng = np.random.default_rng(50 + N)
+    u = rng.standard_normal((3, m.E, N + 1, N + 1, N + 1))
+    lam0, lam1 = 0.7, 2.5
+    w = nk.apply_helmholtz_local(dev(u), m, lam0, lam1, ncomp=3).cpu().numpy()
+    for c in range(3):
+        ref = oop.bk5(o.basis.diff, o.G, u[c], lam0=lam0, B=o.B, lam1=lam1)
+        assert rel_l2(w[c], ref) < BK5_TOL
+    try:
+        lib().nk_bk5_set_variant(K.BK5_VARIANTS["seq3"])
+        ws = nk.apply_helmholtz_local(dev(u), m, lam0, lam1, ncomp=3).cpu().numpy()
+        lib().nk_bk5_set_variant(K.BK5_VARIANTS["pencil"])
+        w1 = [nk.apply_helmholtz_local(dev(u[c]), m, lam0, lam1).cpu().numpy() for c in range(3)]
+    finally:
+        lib().nk_bk5_set_variant(0)
+    for c in range(3):
+        assert rel_l2(ws[c], oop.bk5(o.basis.diff, o.G, u[c], lam0=lam0, B=o.B, lam1=lam1)) < BK5_TOL
+        if N > 1:   # N = 1 scalar calls run bk5_n1, not the pencil kernel
+            assert np.array_equal(ws[c], w1[c])
+
+
 def test_bk5_element_subset():
     N = 7
     m, o = both_meshes((3, 3, 2), N)
