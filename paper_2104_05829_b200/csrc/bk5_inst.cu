@@ -79,7 +79,7 @@ NK_P2D(12, 1, 3) NK_P2D(13, 1, 3) NK_P2D(14, 1, 2) NK_P2D(15, 1, 2) NK_P2D(16, 1
 #undef NK_P2D
 
 
-// Alternative (EPB, MINB) shapes for NQ >= 9, selected by nk_bk5_tune(cfg = 11..14)
+// Alternative (EPB, MINB) shapes for NQ >= 3 (not 8: own table), selected by nk_bk5_tune(cfg = 11..14)
 // for the order sweep (scripts/bk5_sweep.py --high-shapes): several elements per
 // CTA pack NQ^2-thread elements into whole warps (e.g. NQ = 13: 169 -> 192
 // threads, 2 x 169 -> 352).
@@ -90,6 +90,9 @@ template <int NQ> struct PencilAlt {
   template <> struct PencilAlt<NQ_> {                               \
     static constexpr int E[4] = {e0, e1, e2, e3}, M[4] = {m0, m1, m2, m3}; \
   };
+NK_ALT(3, 32, 6, 28, 4, 14, 8, 7, 12) NK_ALT(4, 8, 6, 4, 16, 2, 16, 8, 8)
+NK_ALT(5, 5, 8, 5, 4, 10, 3, 10, 4) NK_ALT(6, 8, 3, 8, 4, 4, 6, 7, 4)
+NK_ALT(7, 1, 16, 2, 10, 5, 4, 4, 4)
 NK_ALT(9, 1, 6, 1, 5, 1, 4, 1, 3) NK_ALT(10, 1, 5, 1, 4, 1, 3, 1, 2)
 NK_ALT(11, 1, 4, 1, 3, 1, 2, 1, 1) NK_ALT(12, 1, 3, 1, 2, 1, 1, 2, 1)
 NK_ALT(13, 1, 2, 1, 1, 2, 1, 1, 4) NK_ALT(14, 1, 2, 1, 1, 2, 1, 1, 4)
@@ -101,7 +104,7 @@ int run_pencil2(int cfg, int64_t nlist, const int32_t* elist, const double* D, c
                 const double* u, double* w, double lam0, const double* B, double lam1,
                 const uint8_t* mask, nk_cg_state* st, double* partials, int64_t part_base,
                 int64_t reduce_count, cudaStream_t s, int64_t* nb, int pfG) {
-  if constexpr (NQ >= 9) {
+  if constexpr (NQ >= 3 && NQ != 8) {
     if (cfg >= 11 && cfg <= 14) {
       using A = PencilAlt<NQ>;
 #define NK_P2ALT(K)                                                                           \
@@ -146,7 +149,7 @@ int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, co
       default: return runp<8, 1, 10>(NK_PARGS);   // measured best (sweep16)
     }
   } else {
-    if constexpr (NQ >= 9) {
+    if constexpr (NQ >= 3) {
       using A = PencilAlt<NQ>;
       switch (cfg) {
         case 11: return runp<NQ, A::E[0], A::M[0]>(NK_PARGS);

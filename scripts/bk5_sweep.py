@@ -204,8 +204,11 @@ def main():
             ne = E_FOR_N[N]
             m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
             ref = None
-            for variant in (3, 5):
-                for cfg in (0, 11, 12, 13, 14):
+            combos = [(v, c) for v in (3, 5) for c in (0, 11, 12, 13, 14)]
+            if N + 1 in (4, 6, 8):
+                combos.append((4, 0))
+            for variant, cfg in combos:
+                if True:
                     L.nk_bk5_set_variant(variant)
                     L.nk_bk5_tune(cfg, 1)
                     med, best, w = time_bk5(nk, L, m, args.reps, flush)
