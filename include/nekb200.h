@@ -146,18 +146,24 @@ int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double*
            nk_stream_t stream);
 int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
 /* kernel variant selection: 0 = auto (measured per-order table: 5 for
- * N in {2,6,8,9,13,14,15}, else 3), 5 = pencil2 (two shared buffers, u
- * re-read from L1/L2), 1 = k-slab (2D
+ * N in {2,6,8,14,15}, else 3; 3-component batches: 6 at N in {3,5,7,10,11},
+ * pencil3 at N in {4,6}, three scalar launches elsewhere), 5 = pencil2 (two
+ * shared buffers, u re-read from L1/L2), 1 = k-slab (2D
  * thread plane, k-column in registers, D in shared memory), 3 = pencil
  * (register 1-D contractions, D in the constant bank, swizzled shared
  * transposes), 4 = pencil-TMA (persistent CTAs, cp.async.bulk 2-stage ring;
- * N+1 in {4, 6, 8}, else pencil).  N = 1 always runs its point-per-lane
- * kernel unless 1 is set.  Variants 3/4/5 serve ncomp = 1;
- * ncomp = 3 uses k-slab or pencil3.  Returns the previous value. */
+ * N+1 in {4, 6, 8}, else pencil), 6 = seq3 (ncomp = 3: the pencil kernel
+ * running the three components back to back per CTA, G from HBM once;
+ * ncomp = 1 calls use the auto table).  N = 1 always runs its
+ * point-per-lane kernel unless 1 is set.  Variants 3/4/5 serve ncomp = 1;
+ * with them forced, ncomp = 3 uses pencil3 (k-slab for 1).  Returns the
+ * previous value. */
 int nk_bk5_set_variant(int variant);
-/* k-slab tuning: cfg selects the (elements per CTA, CTAs per SM) shape for
- * N = 7 (0 = default 4x2, 1 = 4x3, 2 = 2x4, 3 = 2x6, 4 = 1x8, 5 = 1x12,
- * 6 = 8x1); pf_dist = L2 bulk-prefetch distance in CTAs (-1 = one wave of
+/* shape tuning: cfg selects the (elements per CTA, CTAs per SM) shape --
+ * k-slab at N = 7 (0 = default 4x2, 1 = 4x3, 2 = 2x4, 3 = 2x6, 4 = 1x8,
+ * 5 = 1x12, 6 = 8x1), pencil at N = 7 (1..9, bk5_inst.cu), and pencil /
+ * pencil2 at N = 2..6, 8..15 (11..14: the PencilAlt table in bk5_inst.cu,
+ * swept by scripts/bk5_sweep.py --high-shapes); pf_dist = L2 bulk-prefetch distance in CTAs (-1 = one wave of
  * resident CTAs ahead, 0 = off). */
 int nk_bk5_tune(int cfg, int pf_dist);
 
