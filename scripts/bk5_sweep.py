@@ -65,6 +65,8 @@ def main():
     ap.add_argument("--orders", action="store_true")
     ap.add_argument("--low", action="store_true", help="N = 1, 2 variant comparison")
     ap.add_argument("--probe", action="store_true")
+    ap.add_argument("--pf-orders", default=None,
+                    help="comma list of orders: auto variant x L2 prefetch mode 0/1/2")
     ap.add_argument("--high-shapes", default=None,
                     help="comma list of orders: pencil / pencil2 x CTA shapes (cfg 0, 11..14)")
     ap.add_argument("--helm3", action="store_true")
@@ -199,6 +201,17 @@ def main():
                       "gdofs": round(m.E * 343 / med / 1e6, 3), "bitwise_same": same})
         L.nk_bk5_tune(0, 0)
         L.nk_bk5_set_variant(0)
+    if args.pf_orders:
+        for N in [int(x) for x in args.pf_orders.split(",")]:
+            ne = E_FOR_N[N]
+            m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
+            for pf in (0, 1, 2):
+                L.nk_bk5_tune(0, pf)
+                med, best, w = time_bk5(nk, L, m, args.reps, flush)
+                emit({"sweep": "pf", "N": N, "E": m.E, "pf": pf, "ms_med": round(med, 5),
+                      "frac": round(64 * m.n_local / med / 1e6 / pk, 4)})
+            del m
+        L.nk_bk5_tune(0, 0)
     if args.high_shapes:
         for N in [int(x) for x in args.high_shapes.split(",")]:
             ne = E_FOR_N[N]
