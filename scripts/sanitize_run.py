@@ -8,7 +8,7 @@ import paper_2104_05829_b200 as nk
 from paper_2104_05829_b200 import _lib
 
 L = _lib.lib()
-for N, counts in ((7, (3, 2, 2)), (4, (2, 2, 2)), (9, (2, 1, 1))):
+for N, counts in ((7, (3, 2, 2)), (4, (2, 2, 2)), (9, (2, 1, 1)), (12, (2, 1, 1))):
     m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
     u = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
     for v in (1, 3, 4):
@@ -19,6 +19,9 @@ for N, counts in ((7, (3, 2, 2)), (4, (2, 2, 2)), (9, (2, 1, 1))):
     L.nk_bk5_set_variant(0)
     u3 = torch.randn(3 * m.n_local, dtype=torch.float64, device="cuda")
     nk.apply_helmholtz_local(u3, m, 0.5, 2.0, ncomp=3)
+    L.nk_bk5_set_variant(6)   # seq3: bk5_pencil<NC = 3>
+    nk.apply_helmholtz_local(u3, m, 0.5, 2.0, ncomp=3)
+    L.nk_bk5_set_variant(0)
     op = nk.PoissonOperator(m)
     jac = nk.JacobiPreconditioner(op)
     b = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
