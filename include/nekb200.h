@@ -146,7 +146,7 @@ int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double*
            nk_stream_t stream);
 int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
 /* kernel variant selection: 0 = auto (measured per-order table: 5 for
- * N in {2,6,8,14,15}, else 3; 3-component batches: 6 at N in {3,5,7,10,11},
+ * N in {2,6,8,14,15}, else 3; 3-component batches: 6 at N in {3,5,7,9,10,11},
  * pencil3 at N in {4,6}, three scalar launches elsewhere), 5 = pencil2 (two
  * shared buffers, u re-read from L1/L2), 1 = k-slab (2D
  * thread plane, k-column in registers, D in shared memory), 3 = pencil

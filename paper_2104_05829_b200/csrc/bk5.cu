@@ -119,10 +119,11 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
   // 3-component batches (vector Helmholtz), measured per order on the B200
   // (scripts/bk5_sweep.py --helm3, profiles/r1k_helm3.jsonl):
   //   seq3    -- bk5_pencil<NC = 3>: the three components back to back in one
-  //              CTA, G from HBM once and re-read from L2 (N = 3, 5, 7, 10, 11);
+  //              CTA, G from HBM once and re-read from L2 (N = 3, 5, 7, 9, 10,
+  //              11);
   //   pencil3 -- the three components interleaved, G in registers once
   //              (N = 4, 6);
-  //   scalar  -- three scalar launches, G read three times (N = 1, 2, 8, 9,
+  //   scalar  -- three scalar launches, G read three times (N = 1, 2, 8,
   //              12..15, where both batched forms spill or lose occupancy).
   // A forced variant (nk_bk5_set_variant) keeps its own kernel: 6 = seq3,
   // any other = pencil3 / k-slab as before.
@@ -130,7 +131,7 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
     int v = nk_bk5_variant_get();
     if (v == 0) {
       switch (N) {
-        case 3: case 5: case 7: case 10: case 11: v = 6; break;
+        case 3: case 5: case 7: case 9: case 10: case 11: v = 6; break;
         case 4: case 6: v = 3; break;
         default: v = -1; break;
       }

@@ -235,7 +235,24 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
   }
   if (ncomp == 3 && st == nullptr && variant == 6) {
     // 3 components back to back per CTA, G from HBM once (bk5_pencil NC = 3)
-    constexpr int EPB = PencilDefault<NQ>::EPB, MINB = PencilDefault<NQ>::MINB;
+    if constexpr (NQ >= 3 && NQ != 8) {
+      using A = PencilAlt<NQ>;
+#define NK_S3ALT(K)                                                                             \
+  if (cfg == 11 + K) {                                                                          \
+    if (nblocks) {                                                                              \
+      *nblocks = (nlist + A::E[K] - 1) / A::E[K];                                               \
+      return NK_OK;                                                                             \
+    }                                                                                           \
+    return launch_pencil<NQ, A::E[K], A::M[K], 3>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, \
+                                                  nullptr, nullptr, 0, 0, s, pf_dist, cstride);  \
+  }
+      NK_S3ALT(0) NK_S3ALT(1) NK_S3ALT(2) NK_S3ALT(3)
+#undef NK_S3ALT
+    }
+    // seq3 keeps the scalar shape except N = 9: one MINB lower (4, not 5)
+    // drops its 96 B spill (profiles/r1l_seq3_shapes.jsonl)
+    constexpr int EPB = PencilDefault<NQ>::EPB;
+    constexpr int MINB = NQ == 10 ? 4 : PencilDefault<NQ>::MINB;
     if (nblocks) {
       *nblocks = (nlist + EPB - 1) / EPB;
       return NK_OK;

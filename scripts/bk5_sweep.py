@@ -65,6 +65,8 @@ def main():
     ap.add_argument("--orders", action="store_true")
     ap.add_argument("--low", action="store_true", help="N = 1, 2 variant comparison")
     ap.add_argument("--probe", action="store_true")
+    ap.add_argument("--seq3-shapes", default=None,
+                    help="comma list of orders: seq3 (3-component) x CTA shapes vs 3 x scalar")
     ap.add_argument("--pf-orders", default=None,
                     help="comma list of orders: auto variant x L2 prefetch mode 0/1/2")
     ap.add_argument("--high-shapes", default=None,
@@ -201,6 +203,44 @@ def main():
                       "gdofs": round(m.E * 343 / med / 1e6, 3), "bitwise_same": same})
         L.nk_bk5_tune(0, 0)
         L.nk_bk5_set_variant(0)
+    if args.seq3_shapes:
+        from paper_2104_05829_b200._lib import ptr
+        s = torch.cuda.current_stream()
+        for N in [int(x) for x in args.seq3_shapes.split(",")]:
+            ne = E_FOR_N[N]
+            m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
+            n = m.n_local
+            u3 = torch.randn(3 * n, dtype=torch.float64, device="cuda")
+            w3 = torch.empty_like(u3)
+            ref = None
+            for kind, cfg in [("3x scalar", 0)] + [("seq3", c) for c in (0, 11, 12, 13, 14)]:
+                ts = []
+                for rep in range(args.reps + 5):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    L.nk_l2_flush(ptr(flush), flush.numel(), s.cuda_stream)
+                    a.record(s)
+                    if kind == "seq3":
+                        L.nk_bk5_set_variant(6)
+                        L.nk_bk5_tune(cfg, 1)
+                        L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(u3), ptr(w3), 1e-3,
+                                 ptr(m.B), 1833.3, 3, n, None, None, 0, None, None, 0, 0,
+                                 s.cuda_stream)
+                        L.nk_bk5_tune(0, 1)
+                        L.nk_bk5_set_variant(0)
+                    else:
+                        for c in range(3):
+                            L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), u3.data_ptr() + 8 * c * n,
+                                     w3.data_ptr() + 8 * c * n, 1e-3, ptr(m.B), 1833.3, 1, n,
+                                     None, None, 0, None, None, 0, 0, s.cuda_stream)
+                    b.record(s)
+                    ts.append((a, b))
+                torch.cuda.synchronize()
+                ms = statistics.median([a.elapsed_time(b) for a, b in ts[5:]])
+                if ref is None:
+                    ref = w3.clone()
+                emit({"sweep": "seq3_shape", "N": N, "E": m.E, "kind": kind, "cfg": cfg,
+                      "ms_med": round(ms, 5), "close_to_scalar": bool(torch.allclose(ref, w3, rtol=1e-12, atol=1e-9))})
+            del m, u3, w3
     if args.pf_orders:
         for N in [int(x) for x in args.pf_orders.split(",")]:
             ne = E_FOR_N[N]
