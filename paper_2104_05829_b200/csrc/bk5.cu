@@ -57,6 +57,12 @@ static int g_cfg = 0;
 static int g_pf = 1;
 
 extern "C" int nk_bk5_tune(int cfg, int pf_dist) {
+#ifndef NK_BK5_SHAPE_SWEEP
+  if (cfg >= 11 && cfg <= 14) {
+    set_error("bk5_tune: CTA-shape sweep configs 11..14 need a sweep build (make SWEEP=1)");
+    return NK_ERR_UNSUPPORTED;
+  }
+#endif
   g_cfg = cfg;
   g_pf = pf_dist;
   return NK_OK;

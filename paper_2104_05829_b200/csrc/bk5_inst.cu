@@ -80,6 +80,8 @@ NK_P2D(12, 1, 3) NK_P2D(13, 1, 3) NK_P2D(14, 1, 2) NK_P2D(15, 1, 2) NK_P2D(16, 1
 
 
 // Alternative (EPB, MINB) shapes for NQ >= 3 (not 8: own table), selected by nk_bk5_tune(cfg = 11..14)
+// in a sweep build (make SWEEP=1 -> -DNK_BK5_SHAPE_SWEEP; the product build
+// does not instantiate them)
 // for the order sweep (scripts/bk5_sweep.py --high-shapes): several elements per
 // CTA pack NQ^2-thread elements into whole warps (e.g. NQ = 13: 169 -> 192
 // threads, 2 x 169 -> 352).
@@ -104,6 +106,7 @@ int run_pencil2(int cfg, int64_t nlist, const int32_t* elist, const double* D, c
                 const double* u, double* w, double lam0, const double* B, double lam1,
                 const uint8_t* mask, nk_cg_state* st, double* partials, int64_t part_base,
                 int64_t reduce_count, cudaStream_t s, int64_t* nb, int pfG) {
+#ifdef NK_BK5_SHAPE_SWEEP
   if constexpr (NQ >= 3 && NQ != 8) {
     if (cfg >= 11 && cfg <= 14) {
       using A = PencilAlt<NQ>;
@@ -120,6 +123,7 @@ int run_pencil2(int cfg, int64_t nlist, const int32_t* elist, const double* D, c
 #undef NK_P2ALT
     }
   }
+#endif
   constexpr int EPB = Pencil2Default<NQ>::EPB, MINB = Pencil2Default<NQ>::MINB;
   if (nb) {
     *nb = (nlist + EPB - 1) / EPB;
@@ -149,6 +153,7 @@ int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, co
       default: return runp<8, 1, 10>(NK_PARGS);   // measured best (sweep16)
     }
   } else {
+#ifdef NK_BK5_SHAPE_SWEEP
     if constexpr (NQ >= 3) {
       using A = PencilAlt<NQ>;
       switch (cfg) {
@@ -159,6 +164,7 @@ int run_pencil(int cfg, int64_t nlist, const int32_t* elist, const double* D, co
         default: break;
       }
     }
+#endif
     return runp<NQ, PencilDefault<NQ>::EPB, PencilDefault<NQ>::MINB>(NK_PARGS);
   }
 #undef NK_PARGS
@@ -235,6 +241,7 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
   }
   if (ncomp == 3 && st == nullptr && variant == 6) {
     // 3 components back to back per CTA, G from HBM once (bk5_pencil NC = 3)
+#ifdef NK_BK5_SHAPE_SWEEP
     if constexpr (NQ >= 3 && NQ != 8) {
       using A = PencilAlt<NQ>;
 #define NK_S3ALT(K)                                                                             \
@@ -249,6 +256,7 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
       NK_S3ALT(0) NK_S3ALT(1) NK_S3ALT(2) NK_S3ALT(3)
 #undef NK_S3ALT
     }
+#endif
     // seq3 keeps the scalar shape except N = 9: one MINB lower (4, not 5)
     // drops its 96 B spill (profiles/r1l_seq3_shapes.jsonl)
     constexpr int EPB = PencilDefault<NQ>::EPB;

@@ -3,6 +3,9 @@
 sweep of BASELINE configs[1]).  Prints one JSON line per measurement.
 
     python scripts/bk5_sweep.py [--shapes] [--orders] [--reps 50]
+
+--high-shapes / --seq3-shapes need the sweep build of the library
+(cd paper_2104_05829_b200/csrc && make clean && make SWEEP=1).
 """
 
 import argparse
@@ -221,7 +224,8 @@ def main():
                     a.record(s)
                     if kind == "seq3":
                         L.nk_bk5_set_variant(6)
-                        L.nk_bk5_tune(cfg, 1)
+                        if L.nk_bk5_tune(cfg, 1) != 0:
+                            raise SystemExit(L.nk_last_error().decode())
                         L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(u3), ptr(w3), 1e-3,
                                  ptr(m.B), 1833.3, 3, n, None, None, 0, None, None, 0, 0,
                                  s.cuda_stream)
@@ -263,7 +267,8 @@ def main():
             for variant, cfg in combos:
                 if True:
                     L.nk_bk5_set_variant(variant)
-                    L.nk_bk5_tune(cfg, 1)
+                    if L.nk_bk5_tune(cfg, 1) != 0:
+                        raise SystemExit(L.nk_last_error().decode())
                     med, best, w = time_bk5(nk, L, m, args.reps, flush)
                     if ref is None:
                         ref = w.clone()
