@@ -324,6 +324,16 @@ int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double*
 int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
                     const int32_t* code, nk_cg_state* st, double* partials, nk_stream_t stream);
 
+/* The vector head of nk_bk5_pcg as its own coalesced pass (iteration
+ * k = st->iter): k > 0: stop test on st->rr, x += alpha_{k-1} p,
+ * p = invD r + beta p (Fletcher-Reeves or flexible beta); hist[k], stop and
+ * rz bookkeeping as nk_bk5_pcg.  Follow with nk_bk5(..., st, partials) for
+ * w = mask A p and st->pAp, then gs + nk_cg_update_gs as in the fused
+ * schedule.  Used by FusedPCG at orders where it beats the
+ * fused kernel (paper_2104_05829_b200/solvers.py). */
+int nk_cg_xpstep(int64_t n, double* x, const double* r, double* p, const double* invD,
+                 nk_cg_state* st, double* hist, nk_stream_t stream);
+
 /* convergence test on st->rr; else beta (Fletcher-Reeves, or Polak-Ribiere
  * -alpha*zap/rz when flexible) and p = z + beta p with z = invD r (or the
  * explicit z [dev, nullable]).  Records hist[iter] = sqrt(rr). */

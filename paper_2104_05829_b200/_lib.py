@@ -93,6 +93,7 @@ _SIGS = {
     "nk_cg_update": ([_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "nk_cg_update_gs": ([_I64, _P, _P, _P, _P, _P, _P, _P], _I32),
     "nk_cg_pupdate": ([_I64, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "nk_cg_xpstep": ([_I64, _P, _P, _P, _P, _P, _P, _P], _I32),
     "nk_wdot": ([_I64, _P, _P, _P, _P, _P, _P], _I32),
     "nk_cg_gate": ([_P, _P, _P], _I32),
     "nk_interp3": ([_I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _I32, _P, _P], _I32),

@@ -469,6 +469,87 @@ extern "C" int nk_cg_pupdate(int64_t n, const double* r, double* p, const double
   return check_launch("cg_pupdate");
 }
 
+// The vector head of the fused BP5 step (bk5_pcg.cuh, nk_bk5_pcg) as its own
+// coalesced pass: at iteration k = st->iter, k > 0: test ||r_k||, x += alpha_{k-1}
+// p_{k-1}, p_k = invD r_k + beta_k p_{k-1}; the last block records hist[k] and
+// the stop / rz bookkeeping exactly as nk_bk5_pcg's last block does.  Followed
+// by nk_bk5 with st (w = mask A p, st->pAp) it replaces nk_bk5_pcg at orders
+// where the fused kernel's row-wise prologue is latency-bound (N != 7).
+template <bool VEC>
+__global__ void __launch_bounds__(kVecThreads)
+cg_xpstep_kernel(int64_t n, double* __restrict__ x, const double* __restrict__ r,
+                 double* __restrict__ p, const double* __restrict__ invD, nk_cg_state* st,
+                 double* __restrict__ hist) {
+  if (st->done) return;
+  const int it = st->iter;
+  const bool conv = it > 0 && st->rr <= st->thresh2;
+  const bool stop = it > 0 && (conv || it >= st->max_iter);
+  const double alpha_prev = st->alpha;
+  const double rz = st->rz;
+  const double beta =
+      it == 0 ? 0.0 : (st->flexible ? (-alpha_prev * st->zap) / rz : st->rz_new / rz);
+  if (it > 0) {
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    if (VEC) {
+      const int64_t np = n >> 1;
+#pragma unroll 2
+      for (int64_t q = gtid; q < np; q += nthr) {
+        const double2 pv = reinterpret_cast<const double2*>(p)[q];
+        double2 xv = reinterpret_cast<const double2*>(x)[q];
+        xv.x = fma(alpha_prev, pv.x, xv.x);
+        xv.y = fma(alpha_prev, pv.y, xv.y);
+        reinterpret_cast<double2*>(x)[q] = xv;
+        if (!stop) {
+          const double2 rv = __ldg(reinterpret_cast<const double2*>(r) + q);
+          const double2 dv = __ldg(reinterpret_cast<const double2*>(invD) + q);
+          reinterpret_cast<double2*>(p)[q] =
+              make_double2(fma(beta, pv.x, dv.x * rv.x), fma(beta, pv.y, dv.y * rv.y));
+        }
+      }
+      if ((n & 1) && gtid == 0) {
+        const int64_t q = n - 1;
+        const double pv = p[q];
+        x[q] = fma(alpha_prev, pv, x[q]);
+        if (!stop) p[q] = fma(beta, pv, invD[q] * r[q]);
+      }
+    } else {
+      for (int64_t q = gtid; q < n; q += nthr) {
+        const double pv = p[q];
+        x[q] = fma(alpha_prev, pv, x[q]);
+        if (!stop) p[q] = fma(beta, pv, invD[q] * r[q]);
+      }
+    }
+  }
+  if (last_block(&st->ticket[2], gridDim.x)) {
+    if (threadIdx.x == 0) {
+      if (it > 0 && hist) hist[it] = sqrt(st->rr);
+      if (stop) {
+        st->converged = conv ? 1 : 0;
+        st->done = 1;
+      } else if (it > 0) {
+        st->rz = st->rz_new;
+      }
+    }
+  }
+}
+
+extern "C" int nk_cg_xpstep(int64_t n, double* x, const double* r, double* p,
+                            const double* invD, nk_cg_state* st, double* hist,
+                            nk_stream_t stream) {
+  if (n < 0 || !x || !r || !p || !invD || !st) {
+    set_error("cg_xpstep: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  if (aligned16(x, r, p, invD))
+    cg_xpstep_kernel<true><<<(unsigned)vec_grid(n), kVecThreads, 0, S(stream)>>>(n, x, r, p, invD,
+                                                                               st, hist);
+  else
+    cg_xpstep_kernel<false><<<(unsigned)vec_grid(n), kVecThreads, 0, S(stream)>>>(n, x, r, p,
+                                                                                invD, st, hist);
+  return check_launch("cg_xpstep");
+}
+
 __global__ void cg_gate_kernel(nk_cg_state* inner, const nk_cg_state* outer) {
   if (outer->done) inner->done = 1;
 }

@@ -234,6 +234,11 @@ class JacobiPreconditioner:
         return self.invD.view_as(r) * r
 
 
+# orders whose fused BP5 step stays one kernel (N = 1: point-per-lane,
+# N = 7: the TMA pipeline); elsewhere FusedPCG splits it (split_step)
+SPLIT_STEP_OFF = (1, 7)
+
+
 class FusedPCG:
     """Graph-captured Jacobi-PCG on a PoissonOperator (BP5).
 
@@ -244,10 +249,17 @@ class FusedPCG:
     nk_cg_update (r, rr, rz, zAp).  On one rank the face pairs of the gs fold
     into the update (nk_cg_update_gs: a point of a 2-member segment adds its
     partner's w on the fly; the gs pass only covers edge / vertex segments)
-    -- bit-identical; fuse_gs=False keeps the full gs pass."""
+    -- bit-identical; fuse_gs=False keeps the full gs pass.
+
+    split_step (one rank, fused gs): run nk_bk5_pcg's vector head as its own
+    coalesced pass (nk_cg_xpstep) followed by nk_bk5 with the fused p.Ap --
+    4 kernels per iteration.  None = auto: on at the orders where it measured
+    faster than the fused kernel (every N except 1 and 7, whose fused steps
+    are the point-per-lane and TMA kernels; profiles/r1m_bp5_split.jsonl:
+    1.02-1.15x at N = 2, 4..6, 8..15, a tie at N = 3)."""
 
     def __init__(self, op, prec, tol=1e-8, max_iter=1000, flexible=False, chunk=16,
-                 use_graph=True, fuse_gs=True):
+                 use_graph=True, fuse_gs=True, split_step=None):
         import torch
         self.op, self.prec = op, prec
         self.tol, self.max_iter, self.flexible = float(tol), int(max_iter), bool(flexible)
@@ -286,6 +298,11 @@ class FusedPCG:
             from .gather_scatter import point_codes
             self.codes = point_codes(op.gs)
         self.launches_per_iter = 3    # bk5_pcg, gs (all | non-pair segments), update
+        if split_step is None:
+            split_step = op.mesh.N not in SPLIT_STEP_OFF
+        self.split = bool(split_step) and self.codes is not None
+        if self.split:
+            self.launches_per_iter = 4    # xpstep, bk5 (+p.Ap), gs non-pair, update
 
     def _allreduce(self, a, b):
         if self.comm is not None:
@@ -296,8 +313,11 @@ class FusedPCG:
         x/p updates, BK5, p.Ap), gs, nk_cg_update (r, rr, rz, zAp)."""
         L, s = lib(), stream_ptr()
         if self.codes is not None:
-            self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
-                              self.part_bk5, self.hist, gs=False)
+            if self.split:
+                self._split_head(L, s)
+            else:
+                self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
+                                  self.part_bk5, self.hist, gs=False)
             self.codes[1].run(self.w, "+", 1, self.n, self.st)          # edges, vertices
             check(L.nk_cg_update_gs(self.n, ptr(self.r), ptr(self.w), ptr(self.invD),
                                     ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
@@ -310,6 +330,18 @@ class FusedPCG:
                              ptr(self.wt), ptr(self.mult), ptr(self.st), ptr(self.part_cg), s),
               "cg_update")
         self._allreduce(2, 5)                                            # rz_new rr zap
+
+    def _split_head(self, L, s):
+        """nk_cg_xpstep (test, x and p updates) + nk_bk5 with the fused p.Ap:
+        the same iterates as nk_bk5_pcg up to the rounding of the BK5
+        variant the order's table picks."""
+        op, m = self.op, self.op.mesh
+        check(L.nk_cg_xpstep(self.n, ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.invD),
+                             ptr(self.st), ptr(self.hist), s), "cg_xpstep")
+        nb = int(L.nk_bk5_blocks(m.N, m.E, 1))
+        check(L.nk_bk5(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p), ptr(self.w),
+                       op.lam0, ptr(m.B) if op.lam1 else None, op.lam1, 1, self.n, ptr(m.mask),
+                       None, 0, ptr(self.st), ptr(self.part_bk5), 0, nb, s), "bk5")
 
     def _capture(self):
         import torch
@@ -335,11 +367,15 @@ class FusedPCG:
             self.st.copy_(st_save)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
-            nb = int(L.nk_bk5_pcg_blocks(m.N, m.E))
-            check(L.nk_bk5_pcg(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p), ptr(self.w),
-                               op.lam0, ptr(m.B) if op.lam1 else None, op.lam1, ptr(m.mask),
-                               None, 0, ptr(self.x), ptr(self.r), ptr(self.invD), ptr(self.st),
-                               ptr(self.part_bk5), 0, nb, ptr(self.hist), s), "bk5_pcg")
+            if fused and self.split:
+                self._split_head(L, s)
+            else:
+                nb = int(L.nk_bk5_pcg_blocks(m.N, m.E))
+                check(L.nk_bk5_pcg(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p),
+                                   ptr(self.w), op.lam0, ptr(m.B) if op.lam1 else None, op.lam1,
+                                   ptr(m.mask), None, 0, ptr(self.x), ptr(self.r),
+                                   ptr(self.invD), ptr(self.st), ptr(self.part_bk5), 0, nb,
+                                   ptr(self.hist), s), "bk5_pcg")
             ev[1].record()
             if fused:
                 self.codes[1].run(self.w, "+", 1, self.n, self.st)

@@ -287,6 +287,43 @@ def test_pcg_spec_examples():
         nk.pcg(lambda v: -v, lambda v: v, torch.ones(3, dtype=torch.float64, device="cuda"))
 
 
+@pytest.mark.parametrize("counts,N,lam1", [((3, 3, 2), 2, 0.0), ((3, 2, 3), 3, 0.5),
+                                           ((4, 4, 4), 7, 0.0), ((2, 3, 2), 8, 0.0),
+                                           ((2, 2, 2), 12, 0.3)])
+def test_fused_pcg_split_step(counts, N, lam1):
+    """split_step (nk_cg_xpstep + nk_bk5 with the fused p.Ap) against the
+    one-kernel fused step: with the pencil kernel forced on both paths the
+    solves are bit-identical (same iterations, residual history, x); in auto
+    mode the split is the default at N != 1, 7 and solves the system."""
+    from paper_2104_05829_b200 import kernels as K
+    from paper_2104_05829_b200._lib import lib
+    m, o = both_meshes(counts, N)
+    op = nk.PoissonOperator(m, lam1=lam1)
+    jac = nk.JacobiPreconditioner(op)
+    rng = np.random.default_rng(40 + N)
+    b = torch.as_tensor(o.mask.ravel() * ogs.gs_op(o.ids, rng.standard_normal(m.n_local)),
+                        device="cuda")
+    try:
+        lib().nk_bk5_set_variant(K.BK5_VARIANTS["pencil"])
+        sa = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000, split_step=True)
+        sb = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000, split_step=False)
+        assert sa.split and sa.launches_per_iter == 4 and not sb.split
+        ra, rb = sa.solve(b), sb.solve(b)
+    finally:
+        lib().nk_bk5_set_variant(0)
+    assert ra.converged and ra.iterations == rb.iterations
+    assert ra.residual_history == rb.residual_history
+    assert torch.equal(ra.x, rb.x)
+    sc = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000)
+    assert sc.split == (N not in (1, 7))
+    rc = sc.solve(b)
+    assert rc.converged and abs(rc.iterations - rb.iterations) <= 1
+    Ax = torch.empty_like(b)
+    op(rc.x.reshape(-1), out=Ax)
+    assert float(torch.linalg.norm(Ax - b)) <= 2e-9 * float(torch.linalg.norm(b))
+    assert set(sc.profile_iteration(reps=2)) == {"bk5_pcg", "gs_nonpair", "cg_update_gs"}
+
+
 def test_fused_pcg_deterministic_and_graph_equivalent():
     m, o = both_meshes((4, 4, 4), 7)
     b, _, _, _ = _oracle_problem(o)
@@ -318,7 +355,7 @@ def test_fused_gs_update_bit_identical(counts, N, bc, lam1):
     rng = np.random.default_rng(N)
     b = torch.as_tensor(o.mask.ravel() * ogs.gs_op(o.ids, rng.standard_normal(m.n_local)),
                         device="cuda")
-    s2 = nk.FusedPCG(op, jac, tol=1e-9, max_iter=2000)
+    s2 = nk.FusedPCG(op, jac, tol=1e-9, max_iter=2000, split_step=False)
     assert s2.codes is not None and s2.launches_per_iter == 3
     s3 = nk.FusedPCG(op, jac, tol=1e-9, max_iter=2000, fuse_gs=False)
     assert s3.codes is None
