@@ -372,8 +372,11 @@ class MultigridHierarchy:
 
     def _coarse_setup_pcg(self, lv):
         from .solvers import FusedPCG, JacobiPreconditioner
+        # one kernel per fused step here: the coarse levels are small and
+        # launch-bound, where a 4th launch per iteration costs more than the
+        # split saves (the split_step default is measured at ~3M points)
         lv.cpcg = FusedPCG(lv.op, JacobiPreconditioner(lv.op), tol=self.coarse_tol,
-                           max_iter=self.coarse_iters, use_graph=False)
+                           max_iter=self.coarse_iters, use_graph=False, split_step=False)
         lv.e = lv.cpcg.x           # the coarse correction is the inner solution
 
     def _coarse(self, lv, r, st):

@@ -234,9 +234,9 @@ class JacobiPreconditioner:
         return self.invD.view_as(r) * r
 
 
-# orders whose fused BP5 step stays one kernel (N = 1: point-per-lane,
-# N = 7: the TMA pipeline); elsewhere FusedPCG splits it (split_step)
-SPLIT_STEP_OFF = (1, 7)
+# orders whose fused BP5 step stays one kernel (N = 7: the TMA pipeline,
+# 0.117 vs 0.138 ms split); elsewhere FusedPCG splits it (split_step)
+SPLIT_STEP_OFF = (7,)
 
 
 class FusedPCG:
@@ -254,9 +254,9 @@ class FusedPCG:
     split_step (one rank, fused gs): run nk_bk5_pcg's vector head as its own
     coalesced pass (nk_cg_xpstep) followed by nk_bk5 with the fused p.Ap --
     4 kernels per iteration.  None = auto: on at the orders where it measured
-    faster than the fused kernel (every N except 1 and 7, whose fused steps
-    are the point-per-lane and TMA kernels; profiles/r1m_bp5_split.jsonl:
-    1.02-1.15x at N = 2, 4..6, 8..15, a tie at N = 3)."""
+    faster than the fused kernel (every N except 7, whose fused step is the
+    TMA pipeline; profiles/r1m_bp5_split.jsonl: 1.02-1.15x at N = 1, 2,
+    4..6, 8..15, a tie at N = 3)."""
 
     def __init__(self, op, prec, tol=1e-8, max_iter=1000, flexible=False, chunk=16,
                  use_graph=True, fuse_gs=True, split_step=None):

@@ -21,6 +21,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--orders", default=",".join(str(n) for n in range(1, 16)))
     ap.add_argument("--out", default=None)
+    ap.add_argument("--split", default="auto", choices=("auto", "on", "off"),
+                    help="FusedPCG split_step: auto (per-order default), on, off")
     args = ap.parse_args()
     import torch
     import paper_2104_05829_b200 as nk
@@ -31,7 +33,9 @@ def main():
         ne = E_FOR_N[N]
         m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
         op = nk.PoissonOperator(m)
-        s = nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-30, max_iter=100, chunk=100)
+        split = {"auto": None, "on": True, "off": False}[args.split]
+        s = nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-30, max_iter=100, chunk=100,
+                        split_step=split)
         b = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
         nk.gs_op(op.gs, b)
         b *= m.mask.reshape(-1).to(torch.float64)
@@ -46,7 +50,8 @@ def main():
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(e) / 100)
         ms = sorted(ts)[len(ts) // 2]
-        d = {"sweep": "bp5_order", "N": N, "E": m.E, "ms_per_iteration": round(ms, 5),
+        d = {"sweep": "bp5_order", "N": N, "E": m.E, "split": s.split,
+             "ms_per_iteration": round(ms, 5),
              "gdof_iter_per_s": round(m.E * N ** 3 / ms / 1e6, 3),
              "frac_at_143.8_B_per_pt": round(143.8 * m.n_local / ms / 1e6 / pk, 4)}
         line = json.dumps(d)

@@ -287,14 +287,15 @@ def test_pcg_spec_examples():
         nk.pcg(lambda v: -v, lambda v: v, torch.ones(3, dtype=torch.float64, device="cuda"))
 
 
-@pytest.mark.parametrize("counts,N,lam1", [((3, 3, 2), 2, 0.0), ((3, 2, 3), 3, 0.5),
+@pytest.mark.parametrize("counts,N,lam1", [((5, 4, 4), 1, 0.0), ((3, 3, 2), 2, 0.0),
+                                           ((3, 2, 3), 3, 0.5),
                                            ((4, 4, 4), 7, 0.0), ((2, 3, 2), 8, 0.0),
                                            ((2, 2, 2), 12, 0.3)])
 def test_fused_pcg_split_step(counts, N, lam1):
     """split_step (nk_cg_xpstep + nk_bk5 with the fused p.Ap) against the
     one-kernel fused step: with the pencil kernel forced on both paths the
     solves are bit-identical (same iterations, residual history, x); in auto
-    mode the split is the default at N != 1, 7 and solves the system."""
+    mode the split is the default at N != 7 and solves the system."""
     from paper_2104_05829_b200 import kernels as K
     from paper_2104_05829_b200._lib import lib
     m, o = both_meshes(counts, N)
@@ -311,11 +312,12 @@ def test_fused_pcg_split_step(counts, N, lam1):
         ra, rb = sa.solve(b), sb.solve(b)
     finally:
         lib().nk_bk5_set_variant(0)
-    assert ra.converged and ra.iterations == rb.iterations
-    assert ra.residual_history == rb.residual_history
-    assert torch.equal(ra.x, rb.x)
+    assert ra.converged and abs(ra.iterations - rb.iterations) <= (1 if N == 1 else 0)
+    if N > 1:   # N = 1 runs the point-per-lane kernels (bk5_n1 vs bk5_n1_pcg)
+        assert ra.residual_history == rb.residual_history
+        assert torch.equal(ra.x, rb.x)
     sc = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000)
-    assert sc.split == (N not in (1, 7))
+    assert sc.split == (N != 7)
     rc = sc.solve(b)
     assert rc.converged and abs(rc.iterations - rb.iterations) <= 1
     Ax = torch.empty_like(b)
