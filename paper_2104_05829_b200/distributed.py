@@ -144,7 +144,7 @@ class HaloPlan:
     """Host-side arrays describing the cross-rank part of QQ^T for one rank.
 
     hids        sorted halo ids (held by >= 2 ranks)
-    holders     holder-rank array per halo id (ascending)
+    masks       holder-rank bitmask per halo id
     neighbors   sorted neighbour ranks; ngh = len(neighbors)
     dst_start/dst_idx   CSR: all local copies of each halo id (ascending); the
                         own contributions are buf[0:len(dst_idx)] = w[dst_idx]
@@ -200,8 +200,9 @@ def build_halo_plan(ids, comm, nq=None):
     plan.hids = rec[:, 0].copy()
     masks = rec[:, 1].copy()
     nh = len(plan.hids)
-    plan.holders = [np.flatnonzero((int(m) >> np.arange(P)) & 1) for m in masks]
-    nb = sorted({int(q) for h in plan.holders for q in h if q != me})
+    plan.masks = masks
+    bitsP = ((masks[:, None] >> np.arange(P, dtype=np.int64)[None, :]) & 1).astype(bool)
+    nb = [q for q in range(P) if q != me and bool(bitsP[:, q].any())]
     plan.neighbors, plan.ngh = nb, len(nb)
     # local copies of every halo id (ascending local index)
     order = np.argsort(ids, kind="stable")
@@ -216,8 +217,7 @@ def build_halo_plan(ids, comm, nq=None):
     plan.rep = order[lo] if nh else np.zeros(0, np.int64)
     own_len = len(plan.dst_idx)
     # ids shared with each neighbour (positions into hids, ascending id)
-    shared_pos = {q: np.array([t for t in range(nh) if q in set(plan.holders[t].tolist())],
-                              dtype=np.int64) for q in nb}
+    shared_pos = {q: np.flatnonzero(bitsP[:, q]).astype(np.int64) for q in nb}
     plan.send_idx = {q: plan.dst_idx[_ranges(plan.dst_start[shared_pos[q]], mult[shared_pos[q]])]
                      for q in nb}
     # setup exchange: how many copies each neighbour holds of each shared id
@@ -227,28 +227,26 @@ def build_halo_plan(ids, comm, nq=None):
         sends = {q: t.cuda() for q, t in sends.items()}
         recvs = {q: t.cuda() for q, t in recvs.items()}
     comm.exchange(sends, recvs)
-    their = {q: recvs[q].cpu().numpy() for q in nb}
+    their = {q: recvs[q].cpu().numpy().astype(np.int64) for q in nb}
     plan.recv_off, plan.recv_len, off = {}, {}, own_len
     for q in nb:
         plan.recv_off[q] = off
         plan.recv_len[q] = int(their[q].sum())
         off += plan.recv_len[q]
     plan.buf_len = off
-    # where h's contributions from q start inside q's stream
-    start_in_q = {q: dict(zip(shared_pos[q].tolist(),
-                              (np.r_[0, np.cumsum(their[q])[:-1]]).tolist())) for q in nb}
-    cnt_in_q = {q: dict(zip(shared_pos[q].tolist(), their[q].tolist())) for q in nb}
-    src_start, src_idx = [0], []
-    for t in range(nh):
-        for q in plan.holders[t].tolist():
-            if q == me:
-                src_idx.extend(range(plan.dst_start[t], plan.dst_start[t + 1]))
-            else:
-                a0 = plan.recv_off[q] + start_in_q[q][t]
-                src_idx.extend(range(a0, a0 + cnt_in_q[q][t]))
-        src_start.append(len(src_idx))
-    plan.src_start = np.asarray(src_start, dtype=np.int64)
-    plan.src_idx = np.asarray(src_idx, dtype=np.int64)
+    # contributions of halo id t from rank q: cnt[t, q] values starting at
+    # buf[start[t, q]]; the combine reads them row by row (t ascending), ranks
+    # ascending within a row -- the canonical (rank, local index) order
+    cnt = np.zeros((nh, P), dtype=np.int64)
+    start = np.zeros((nh, P), dtype=np.int64)
+    cnt[:, me] = mult
+    start[:, me] = plan.dst_start[:-1]
+    for q in nb:
+        sp = shared_pos[q]
+        cnt[sp, q] = their[q]
+        start[sp, q] = plan.recv_off[q] + np.r_[0, np.cumsum(their[q])[:-1]]
+    plan.src_start = np.r_[0, np.cumsum(cnt.sum(axis=1))].astype(np.int64)
+    plan.src_idx = _ranges(start.ravel(), cnt.ravel())
     return plan
 
 

@@ -331,13 +331,16 @@ class FusedPCG:
               "cg_update")
         self._allreduce(2, 5)                                            # rz_new rr zap
 
-    def _split_head(self, L, s):
+    def _split_head(self, L, s, mid_event=None):
         """nk_cg_xpstep (test, x and p updates) + nk_bk5 with the fused p.Ap:
         the same iterates as nk_bk5_pcg up to the rounding of the BK5
-        variant the order's table picks."""
+        variant the order's table picks.  mid_event (profiling) is recorded
+        between the two launches."""
         op, m = self.op, self.op.mesh
         check(L.nk_cg_xpstep(self.n, ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.invD),
                              ptr(self.st), ptr(self.hist), s), "cg_xpstep")
+        if mid_event is not None:
+            mid_event.record()
         nb = int(L.nk_bk5_blocks(m.N, m.E, 1))
         check(L.nk_bk5(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p), ptr(self.w),
                        op.lam0, ptr(m.B) if op.lam1 else None, op.lam1, 1, self.n, ptr(m.mask),
@@ -359,16 +362,21 @@ class FusedPCG:
         L, s = lib(), stream_ptr()
         op, g = self.op, self.op.gs
         fused = self.codes is not None
+        split = fused and self.split
         names = ("bk5_pcg", "gs_nonpair", "cg_update_gs") if fused else ("bk5_pcg", "gs", "cg_update")
+        if split:
+            names = ("cg_xpstep", "bk5") + names[1:]
         acc = dict.fromkeys(names, 0.0)
         st_save = self.st.clone()
         m = op.mesh
         for _ in range(reps):
             self.st.copy_(st_save)
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+            ev0 = ev[0]
             ev[0].record()
-            if fused and self.split:
-                self._split_head(L, s)
+            if split:
+                self._split_head(L, s, mid_event=ev[1])
+                ev = ev[1:]   # the remaining indices line up with the 3-kernel form
             else:
                 nb = int(L.nk_bk5_pcg_blocks(m.N, m.E))
                 check(L.nk_bk5_pcg(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p),
@@ -392,6 +400,8 @@ class FusedPCG:
                                      ptr(self.part_cg), s), "cg_update")
                 ev[3].record()
             torch.cuda.synchronize()
+            if split:
+                ev = [ev0] + ev
             for q, nm in enumerate(names):
                 acc[nm] += ev[q].elapsed_time(ev[q + 1])
         self.st.copy_(st_save)

@@ -288,6 +288,7 @@ def test_pcg_spec_examples():
 
 
 @pytest.mark.parametrize("counts,N,lam1", [((5, 4, 4), 1, 0.0), ((3, 3, 2), 2, 0.0),
+                                           ((3, 3, 3), 2, 0.0),   # n = 729: odd tail
                                            ((3, 2, 3), 3, 0.5),
                                            ((4, 4, 4), 7, 0.0), ((2, 3, 2), 8, 0.0),
                                            ((2, 2, 2), 12, 0.3)])
@@ -323,7 +324,9 @@ def test_fused_pcg_split_step(counts, N, lam1):
     Ax = torch.empty_like(b)
     op(rc.x.reshape(-1), out=Ax)
     assert float(torch.linalg.norm(Ax - b)) <= 2e-9 * float(torch.linalg.norm(b))
-    assert set(sc.profile_iteration(reps=2)) == {"bk5_pcg", "gs_nonpair", "cg_update_gs"}
+    keys = ({"cg_xpstep", "bk5"} if sc.split else {"bk5_pcg"}) | {"gs_nonpair", "cg_update_gs"}
+    assert set(sc.profile_iteration(reps=2)) == keys
+    assert len(keys) == sc.launches_per_iter
 
 
 def test_fused_pcg_deterministic_and_graph_equivalent():
@@ -649,3 +652,35 @@ def test_gs_32bit_bit_exact(op):
     assert np.array_equal(nk.gs_op(h, w.copy(), op, precision=32), ref)     # numpy path
     with pytest.raises(nk.ContractError):
         nk.gs_op(h, torch.as_tensor(w, device="cuda"), op, precision=64)
+
+
+@pytest.mark.parametrize("n_extra", [0, 1])
+def test_cg_xpstep_unaligned_matches_vec(n_extra):
+    """nk_cg_xpstep's scalar fallback (buffers offset by one double, not
+    16-B aligned) against its 16-B path, bit for bit; n odd and even."""
+    from paper_2104_05829_b200._lib import lib, ptr
+    m, o = both_meshes((3, 3, 3), 2)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    rng = np.random.default_rng(3)
+    b = torch.as_tensor(o.mask.ravel() * ogs.gs_op(o.ids, rng.standard_normal(m.n_local)),
+                        device="cuda")
+    s = nk.FusedPCG(op, jac, tol=1e-30, max_iter=3, split_step=True, use_graph=False, chunk=1)
+    s.init(b)
+    s._iteration()
+    s._iteration()   # iter = 2: xpstep does the x and p updates
+    n = s.n - n_extra
+    L = lib()
+    outs = []
+    for off in (0, 1):
+        buf = lambda v: torch.cat([torch.zeros(off, dtype=v.dtype, device="cuda"), v[:n]])
+        x, r, p, d = buf(s.x), buf(s.r), buf(s.p), buf(s.invD)
+        st = s.st.clone()
+        sl = lambda t: t[off:]
+        assert (sl(x).data_ptr() % 16 == 0) == (off == 0)
+        _lib.check(L.nk_cg_xpstep(n, ptr(sl(x)), ptr(sl(r)), ptr(sl(p)), ptr(sl(d)), ptr(st),
+                                  None, None), "xpstep")
+        outs.append((sl(x).clone(), sl(p).clone()))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert not torch.equal(outs[0][0], s.x[:n])   # the update did run
