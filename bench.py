@@ -2,26 +2,35 @@
 """Benchmark: BK5 (and BP5) GDOF/s FP64 on B200 -- BASELINE.json metric.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--strong]
 
 Workload (BASELINE.json configs[1], the 1-GPU headline): BK5 Ax at N=7 on a
 deformed 20^3-element box per GPU (E = 8000, 4.096M local points, 2.744M DOF),
-FP64.  A "step" is one BK5 apply over the whole mesh.  For N > 1 (torchrun,
-one rank per GPU) every rank owns an independent 20^3 box: BK5 has no
-collective, so scaling is weak and value = all ranks' DOF / max-rank time.
+FP64.  A "step" is one BK5 apply over the whole mesh.  BK5 is element-local
+(no collective), so for N GPUs every rank applies BK5 to its own 20^3 box:
+scaling is weak and value = all ranks' DOF / max-rank time.
 
+--gpus N without torchrun: bench.py re-launches itself under
+         torch.distributed.run with N ranks (127.0.0.1).  With fewer visible
+         GPUs than ranks the ranks share devices over gloo (the multi-rank
+         code path, not a scaling measurement: `ranks_per_gpu` > 1).
 value  : GDOF/s = E*N^3 / t (the paper's n = E N^3), inputs
          resident in HBM, CUDA events on the launching stream per step, L2
-         flushed (256 MiB write) between steps, max over ranks.
+         flushed (256 MiB write + read) between steps, max over ranks.
 e2e    : same metric through the public API (apply_stiffness_local) with
          pinned HOST u in and HOST w out, H2D + kernel + D2H inside the events.
 roofline: algorithmic 64 B per local point (u 8 + G 48 + w 8) / kernel time
          vs MEASURED_PEAKS.json hbm_gbs.
-bp5    : fused Jacobi-PCG (Dirichlet box, same mesh) iterations x DOF / time.
-bp5_time_to_solution: wall time to tol 1e-8 on the same mesh for Jacobi-PCG
-         and the p-multigrid preconditioners (cheby_jac, ras, asm smoothers).
---impl reference: the reference has no CPU Ax, so the
-         reference arm times the CPU oracle port (numpy BK5, all host threads)
-         on a bounded sample of the same workload.
+bp5    : fused Jacobi-PCG, 100 graph-replayed iterations; N = 1 on the same
+         box; N > 1 the configs[3] weak-scaling box (20^3 elements per GPU,
+         RCB, halo over NVLink peer memory overlapped with the interior BK5,
+         dots over the peer-memory board) with t_iter(1) measured in the same
+         run on each rank's own 20^3 box -> efficiency = t_iter(1)/t_iter(N).
+         --strong: configs[2] instead (E = 64^3 split over the N ranks).
+cpu_baseline / --impl reference: the reference ships no CPU Ax (SURVEY.md
+         §0), so both time the oracle's compiled C + OpenMP BK5
+         (oracle/c/bk5_cpu.c, pinned to the numpy oracle) on the full E=8000
+         mesh on the host cores (all threads, plus a 1-thread figure).
 """
 
 import argparse
@@ -148,11 +157,13 @@ def dist_setup(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = max(1, torch.cuda.device_count())
     if ws > 1:
-        # NK_BENCH_BACKEND=gloo lets several ranks share one GPU (host-staged
-        # halo) to exercise the multi-rank path; the real run uses NCCL.
-        backend = os.environ.get("NK_BENCH_BACKEND", "nccl")
-        dev = local % max(1, torch.cuda.device_count())
+        # one rank per GPU over NCCL; with fewer GPUs than ranks (NCCL refuses
+        # two ranks on one device) the ranks share devices over gloo -- the
+        # multi-rank code path with host-staged setup collectives
+        backend = os.environ.get("NK_BENCH_BACKEND", "nccl" if ndev >= ws else "gloo")
+        dev = local % ndev
         torch.cuda.set_device(dev)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
@@ -161,6 +172,11 @@ def dist_setup(args):
     else:
         torch.cuda.set_device(0)
     return ws, rank, local
+
+
+def ranks_per_gpu(ws):
+    import torch
+    return max(1, -(-ws // max(1, torch.cuda.device_count())))
 
 
 def max_over_ranks(x, ws):
@@ -182,76 +198,291 @@ def barrier(ws):
     torch.cuda.synchronize()
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 _CPU_CACHE = {}
 
 
-def cpu_oracle_bk5(E_sample, reps_target_s=10.0, threads=None):
-    """Oracle numpy BK5 on E_sample elements, all host threads; returns
-    (local pts/s, threads, seconds, elements).  Mesh/inputs/pool are built once."""
+def cpu_oracle_setup(N=N_ORDER, counts=COUNTS):
+    """Oracle mesh (numpy, deformed) + seeded input for the CPU legs; built
+    once per process (not timed)."""
     import numpy as np
-    from concurrent.futures import ThreadPoolExecutor
     from oracle import mesh as om
-    from oracle import operators as oop
-    threads = threads or (os.cpu_count() or 1)
-    key = (E_sample, threads)
+    key = (N, counts)
     if key not in _CPU_CACHE:
-        nx = max(1, round(E_sample ** (1 / 3)))
-        counts = (nx, nx, max(1, E_sample // (nx * nx)))
-        o = om.build_box_mesh((1.0, 1.0, 1.0), counts, N_ORDER, deformation=("sine", 0.05))
-        rng = np.random.default_rng(1000 + N_ORDER)
+        o = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, deformation=("sine", 0.05))
+        rng = np.random.default_rng(1000 + N)
         u = rng.standard_normal((o.G.shape[0],) + o.G.shape[2:])
-        chunks = np.array_split(np.arange(u.shape[0]), threads)
-        pool = ThreadPoolExecutor(threads)
-        D, G = o.basis.diff, o.G
-        work = lambda idx: oop.bk5(D, G[idx], u[idx])
-        list(pool.map(work, chunks))  # warm
-        _CPU_CACHE[key] = (pool, work, chunks, u)
-    pool, work, chunks, u = _CPU_CACHE[key]
-    t0 = time.perf_counter()
-    reps = 0
+        _CPU_CACHE[key] = (o.basis.diff, np.ascontiguousarray(o.G), u, np.empty_like(u))
+    return _CPU_CACHE[key]
+
+
+def cpu_oracle_bk5(target_s, threads=0, N=N_ORDER, counts=COUNTS):
+    """Full-mesh BK5 applies with the compiled CPU oracle (oracle/c, C +
+    OpenMP over elements) until target_s elapsed.  Returns (median seconds
+    per apply, threads used, applies, E)."""
+    from oracle import cpu_bk5
+    D, G, u, w = cpu_oracle_setup(N, counts)
+    _, used = cpu_bk5.bk5(D, G, u, out=w, threads=threads)       # warm (page-in)
+    per = []
+    t_end = time.perf_counter() + target_s
     while True:
-        list(pool.map(work, chunks))
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= reps_target_s or reps >= 100000:
+        t0 = time.perf_counter()
+        cpu_bk5.bk5(D, G, u, out=w, threads=threads)
+        per.append(time.perf_counter() - t0)
+        if time.perf_counter() >= t_end or len(per) >= 100000:
             break
-    return reps * u.size / el, threads, el, u.shape[0]
+    return statistics.median(per), used, len(per), u.shape[0]
+
+
+def cpu_baseline_block(N, E, target_all=8.0, target_one=3.0):
+    t_all, used, reps, _ = cpu_oracle_bk5(target_all)
+    t_one, _, reps1, _ = cpu_oracle_bk5(target_one, threads=1)
+    g = lambda t: E * N ** 3 / t / 1e9
+    return {"value": round(g(t_all), 5), "unit": "GDOF/s", "cores": used, "kind": "port",
+            "single_thread_value": round(g(t_one), 5),
+            "ms_per_apply": round(t_all * 1e3, 3), "ms_per_apply_1thread": round(t_one * 1e3, 3),
+            "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count(),
+            "sample": f"oracle/c/bk5_cpu.c (C, OpenMP over elements, -O3 -march=x86-64-v3) on "
+                      f"the FULL E={E} deformed mesh, N={N}: median of {reps} applies over "
+                      f"{target_all:.0f} s on {used} threads, and of {reps1} applies over "
+                      f"{target_one:.0f} s on 1 thread"}
+
+
+def bench_config(N, E, n, dof, ws):
+    """The `config` both arms print (identical dicts: same workload)."""
+    return {"workload": f"configs[1]: BK5 Ax sweep point N={N}, E={E} per GPU, "
+                        "deformed box (sine 0.05)",
+            "N": N, "elements_per_gpu": E, "local_points_per_gpu": n, "dof_per_gpu": dof,
+            "parallelism": f"element-partitioned x{ws}",
+            "l2": "flushed between steps: 256 MiB write + 256 MiB read (cold, clean L2 at every "
+                  "launch); inputs 262 MB > L2"}
+
+
+METRIC = "BK5 GDOF/s FP64 (N=7, E=20^3 deformed box per GPU)"
 
 
 def run_reference(args):
+    """The reference arm: the reference ships no CPU Ax, so it
+    times the oracle's compiled CPU BK5 on the SAME workload as our arm (full
+    E = 8000 mesh, N = 7, same config dict), all host threads; rank 0 only."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    E_sample = 1000
-    per_step = []
-    cores = os.cpu_count() or 1
-    # bounded: the whole --steps K --warmup W run stays within ~150 s
-    step_s = max(0.05, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        cpu_oracle_bk5(E_sample, reps_target_s=step_s)
-    for _ in range(args.steps):
-        pts_s, cores, el, Es = cpu_oracle_bk5(E_sample, reps_target_s=step_s)
-        per_step.append(pts_s)
-    pts_s = statistics.median(per_step)
-    gdof = pts_s * (N_ORDER ** 3) / ((N_ORDER + 1) ** 3) / 1e9
+    N = args.order
     E = COUNTS[0] * COUNTS[1] * COUNTS[2]
-    ms = E * N_ORDER ** 3 / (gdof * 1e9) * 1e3
+    n, dof = E * (N + 1) ** 3, E * N ** 3
+    from oracle import cpu_bk5
+    D, G, u, w = cpu_oracle_setup(N)
+    used = 0
+    for _ in range(max(1, args.warmup)):
+        _, used = cpu_bk5.bk5(D, G, u, out=w)
+    per = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_bk5.bk5(D, G, u, out=w)
+        per.append(time.perf_counter() - t0)
+    ms = statistics.mean(per) * 1e3
+    gdof = ws * dof / (ms * 1e-3) / 1e9
     line = {
-        "impl": "reference", "metric": "BK5 GDOF/s FP64 (N=7, E=20^3 deformed box per GPU)",
+        "impl": "reference", "metric": METRIC,
         "value": round(gdof, 5), "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "configs[1]: BK5 Ax sweep point N=7, E=8000, deformed (sine 0.05)",
-                   "N": N_ORDER, "elements_per_gpu": E},
-        "cpu_baseline": {"value": round(gdof, 5), "unit": "GDOF/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle numpy BK5 over {E_sample} of the 8000 elements "
-                                   f"(N=7, deformed), ThreadPool x{cores}, ~{step_s:.2f} s "
-                                   f"per step"},
+        "config": bench_config(N, E, n, dof, ws),
+        "same_config_as_ours": True,
+        "cpu_baseline": {"value": round(gdof, 5), "unit": "GDOF/s", "cores": used,
+                         "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"oracle/c/bk5_cpu.c (C + OpenMP) on the full E={E} mesh, "
+                                   f"N={N}: one full apply per step, {args.steps} steps on "
+                                   f"{used} threads"},
         "e2e": {"value": round(gdof, 5), "unit": "GDOF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def bp5_bytes(solver, op, bn):
+    """Algorithmic bytes of one BP5 iteration for the schedule that runs
+    (DESIGN.md §5 PCG table): one rank with the face-pair gs fused into the
+    update -- nk_bk5_pcg 105 B/pt (or, split, nk_cg_xpstep 48 + nk_bk5 65
+    B/pt) + nk_cg_update_gs 36 B/pt + 20 B per edge/vertex gs member; the
+    full-gs schedule -- 105 + cg_update 40 B/pt + 20 B per gs member + 4 B
+    per segment."""
+    if solver.codes is not None:
+        sub = solver.codes[1]
+        nsub = int(sum(int(a) * int(b) for a, b in zip(sub.sizes, sub.nsegs)))
+        head = (48 + 65) if solver.split else 105
+        return bn * (head + 36) + 20 * nsub
+    return bn * (105 + 40) + 20 * op.gs.nperm + 4 * op.gs.nseg
+
+
+def time_bp5(nk, op, jac, b_rhs, ws, iters=100):
+    """100 graph-replayed fused Jacobi-PCG iterations (tol 1e-30: no early
+    stop), CUDA events on the current stream, max over ranks.  Returns
+    (solver, ms per iteration, iterations)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    solver = nk.FusedPCG(op, jac, tol=1e-30, max_iter=iters, chunk=iters, use_graph=True)
+    solver.solve(b_rhs)  # warm (+ graph capture)
+    barrier(ws)
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    solver.init(b_rhs)
+    barrier(ws)
+    a_ev.record(stream)
+    if solver.use_graph:
+        solver.graph.replay()
+    else:
+        for _ in range(iters):
+            solver._iteration()
+    b_ev.record(stream)
+    barrier(ws)
+    st = nk.solvers.read_state(solver.st)
+    it = int(st.iter)
+    bp_ms = max_over_ranks(a_ev.elapsed_time(b_ev), ws)
+    return solver, bp_ms / max(it, 1), it
+
+
+def bp5_rhs(nk, op, mesh, seed):
+    import numpy as np
+    import torch
+    rng = np.random.default_rng(seed)
+    b = torch.as_tensor(rng.standard_normal(mesh.n_local), device="cuda")
+    nk.gs_op(op.gs, b)
+    b *= mesh.mask.reshape(-1).to(torch.float64)
+    return b
+
+
+def partitioned_box(nk, gcounts, N, ws, rank):
+    """This rank's RCB share (contiguous blocks) of a global box whose
+    elements keep the 1/20 edge of the per-GPU 20^3 box."""
+    import numpy as np
+    nx, ny, nz = gcounts
+    el = np.arange(nx * ny * nz)
+    cent = np.stack([el % nx, (el // nx) % ny, el // (nx * ny)], axis=1) + 0.5
+    part = nk.rcb(cent, ws)
+    mine = np.flatnonzero(part == rank)
+    return nk.build_box_mesh((nx / 20.0, ny / 20.0, nz / 20.0), gcounts, N, bc="dirichlet",
+                             deformation=("sine", 0.05), elements=mine)
+
+
+def bp5_block(nk, args, ws, rank, mesh, N, peak):
+    """BP5 (fused Jacobi-PCG) at N ranks; see the module docstring."""
+    import torch
+    t1 = None
+    strong = bool(args.strong)
+    if ws == 1 and not strong:
+        bmesh, comm = mesh, None
+    else:
+        from paper_2104_05829_b200.distributed import RankComm
+        gcounts = (64, 64, 64) if strong else weak_counts(ws)
+        if ws > 1 and not strong:
+            # t_iter(1) in the same run: this rank alone on its own 20^3 box
+            # (same element count and kernels, no halo, no collectives);
+            # ranks sharing a GPU take turns so each sees the whole device
+            rpg = ranks_per_gpu(ws)
+            for turn in range(rpg):
+                barrier(ws)
+                if rank % rpg == turn:
+                    op1 = nk.PoissonOperator(mesh)
+                    s1, t1, _ = time_bp5(nk, op1, nk.JacobiPreconditioner(op1),
+                                         bp5_rhs(nk, op1, mesh, 7 + rank), 1)
+                    del s1, op1
+                torch.cuda.synchronize()
+            barrier(ws)
+            t1 = max_over_ranks(t1, ws)
+        comm = RankComm() if ws > 1 else None
+        bmesh = partitioned_box(nk, gcounts, N, ws, rank) if ws > 1 else \
+            nk.build_box_mesh((gcounts[0] / 20.0,) * 3, gcounts, N, bc="dirichlet",
+                              deformation=("sine", 0.05))
+    bn = bmesh.n_local
+    op = nk.PoissonOperator(bmesh, comm=comm)
+    jac = nk.JacobiPreconditioner(op)
+    b_rhs = bp5_rhs(nk, op, bmesh, 11 + rank)
+    solver, per_it, it = time_bp5(nk, op, jac, b_rhs, ws)
+    if ws == 1:
+        solver.init(b_rhs)
+        for _ in range(2):                 # profile a steady-state iteration (iter > 0)
+            solver._iteration()
+        brk = solver.profile_iteration()
+    else:
+        brk = None
+    bp_bytes = bp5_bytes(solver, op, bn)
+    dof_all = bmesh.E * N ** 3
+    if ws > 1:
+        t = torch.tensor([float(dof_all)], dtype=torch.float64,
+                         device="cuda" if torch.distributed.get_backend() == "nccl" else "cpu")
+        torch.distributed.all_reduce(t)
+        dof_all = float(t.item())
+    gcounts = list((64, 64, 64) if strong else (weak_counts(ws) if ws > 1 else COUNTS))
+    out = {"mode": "strong (configs[2])" if strong else "weak (configs[3])",
+           "gdof_per_s": round(dof_all / (per_it * 1e-3) / 1e9, 3),
+           "ms_per_iteration": round(per_it, 4), "iterations": it,
+           "breakdown_ms_in_situ": None if brk is None else {k: round(v, 4) for k, v in brk.items()},
+           "roofline_frac": round(bp_bytes / (per_it * 1e-3) / 1e9 / peak, 3),
+           "model_bytes_per_local_point": round(bp_bytes / bn, 1),
+           "split_step": bool(solver.split),
+           "kernels_per_iteration": solver.launches_per_iter,
+           "global_counts": gcounts, "local_points_per_rank": bn,
+           "halo_neighbors": op.gs.ngh, "graph": bool(solver.use_graph),
+           "halo_transport": getattr(op.gs, "transport", None) if ws > 1 else None,
+           "dot_allreduce": ("ipc-board" if getattr(comm, "board", None) is not None
+                             else "torch.distributed") if ws > 1 else None}
+    if t1 is not None:
+        rpg = ranks_per_gpu(ws)
+        out["t_iter_1_ms"] = round(t1, 4)
+        out["efficiency"] = round(t1 / per_it, 4)
+        out["ranks_per_gpu"] = rpg
+        if rpg > 1:
+            # ranks share a device: ideal t_iter(N) = rpg * t_iter(1)
+            out["efficiency_per_device_share"] = round(rpg * t1 / per_it, 4)
+            out["note"] = ("ranks share GPUs (fewer visible devices than ranks): multi-rank code "
+                           "path check, not an NVLink scaling measurement")
+    elif ws == 1:
+        out["t_iter_1_ms"] = round(per_it, 4)
+        out["efficiency"] = 1.0
+    if ws > 1 and args.pmg_scaling:
+        out["time_to_solution_tol1e-8"] = pmg_scaling(nk, op, jac, b_rhs, ws)
+    del solver
+    return out
+
+
+def pmg_scaling(nk, op, jac, b_rhs, ws):
+    """opt-in (--pmg-scaling): the distributed p-multigrid (Chebyshev-Jacobi,
+    iterative coarse solve over the same halo + all-reduce) on the BP5 box:
+    time to tol 1e-8 vs the distributed Jacobi-PCG, max over ranks."""
+    import torch
+    tts = {}
+    try:
+        for name, make in (
+                ("jacobi_pcg", lambda: nk.FusedPCG(op, jac, tol=1e-8, max_iter=5000, chunk=32)),
+                ("pmg_cheby_jac", lambda: nk.MultigridPCG(
+                    op, nk.MultigridHierarchy(op, coarse="pcg"), tol=1e-8, max_iter=500))):
+            sv = make()
+            sv.solve(b_rhs)
+            barrier(ws)
+            t0 = time.perf_counter()
+            res = sv.solve(b_rhs)
+            torch.cuda.synchronize()
+            tt = max_over_ranks(time.perf_counter() - t0, ws)
+            tts[name] = {"iterations": res.iterations, "solve_ms": round(tt * 1e3, 3),
+                         "converged": bool(res.converged)}
+            del sv
+        tts["pmg_speedup_vs_jacobi_pcg"] = round(
+            tts["jacobi_pcg"]["solve_ms"] / tts["pmg_cheby_jac"]["solve_ms"], 2)
+    except Exception as exc:  # reported, never fatal for the headline
+        tts["error"] = f"{type(exc).__name__}: {exc}"[:200]
+    return tts
 
 
 def run_ours(args):
@@ -367,109 +598,8 @@ def run_ours(args):
                    "bk5_E40cubed_gdofs": round(big.E * N ** 3 / (bms * 1e-3) / 1e9, 2)}
         del big, ub, wb
 
-    # ---- BP5: fused Jacobi-PCG, fixed 100 iterations.  N = 1: the same mesh.
-    # N > 1: weak scaling (configs[3]): a global box of 20^3 elements per GPU
-    # (20^3, 40x20^2, 40^2x20, 40^3), RCB-partitioned, halo over NCCL
-    # (pairwise P2P, boundary-first overlap) and all-reduced PCG scalars.
-    bp5 = None
-    if not args.no_bp5:
-        if ws == 1:
-            bmesh, comm = mesh, None
-        else:
-            from paper_2104_05829_b200.distributed import RankComm
-            gcounts = weak_counts(ws)
-            nx, ny, nz = gcounts
-            el = np.arange(nx * ny * nz)
-            cent = np.stack([el % nx, (el // nx) % ny, el // (nx * ny)], axis=1) + 0.5
-            part = nk.rcb(cent, ws)
-            mine = np.flatnonzero(part == rank)
-            comm = RankComm()
-            bmesh = nk.build_box_mesh((nx / 20.0, ny / 20.0, nz / 20.0), gcounts, N,
-                                      bc="dirichlet", deformation=("sine", 0.05), elements=mine)
-        bn = bmesh.n_local
-        op = nk.PoissonOperator(bmesh, comm=comm)
-        jac = nk.JacobiPreconditioner(op)
-        iters = 100
-        # FusedPCG captures the iteration in a CUDA graph whenever every
-        # exchange is on-stream (1 rank, or peer-memory halo + board dots)
-        solver = nk.FusedPCG(op, jac, tol=1e-30, max_iter=iters, chunk=iters, use_graph=True)
-        b_rhs = torch.as_tensor(rng.standard_normal(bn), device="cuda")
-        nk.gs_op(op.gs, b_rhs)
-        b_rhs *= bmesh.mask.reshape(-1).to(torch.float64)
-        solver.solve(b_rhs)  # warm (+ graph capture)
-        barrier(ws)
-        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        solver.init(b_rhs)
-        barrier(ws)
-        a_ev.record(stream)
-        if solver.use_graph:
-            solver.graph.replay()
-        else:
-            for _ in range(iters):
-                solver._iteration()
-        b_ev.record(stream)
-        barrier(ws)
-        st = nk.solvers.read_state(solver.st)
-        bp_ms = max_over_ranks(a_ev.elapsed_time(b_ev), ws)
-        it = int(st.iter)
-        per_it = bp_ms / max(it, 1)
-        solver.init(b_rhs)
-        for _ in range(2):                 # profile a steady-state iteration (iter > 0)
-            solver._iteration()
-        brk = solver.profile_iteration() if ws == 1 else None
-        if solver.codes is not None:
-            # one rank: nk_bk5_pcg 105 B + nk_cg_update_gs 36 B per point (r in/out,
-            # w, invD, int32 gs code) + the edge/vertex gs (20 B per member)
-            sub = solver.codes[1]
-            nsub = int(sum(int(a) * int(b) for a, b in zip(sub.sizes, sub.nsegs)))
-            bp_bytes = bn * (105 + 36) + 20 * nsub
-        else:
-            # fused schedule: nk_bk5_pcg 105 B + cg_update 40 B per point + gs
-            bp_bytes = bn * (105 + 40) + 20 * op.gs.nperm + 4 * op.gs.nseg
-        bdof = bmesh.E * N ** 3
-        bp5 = {"gdof_per_s": round(ws * bdof * it / (bp_ms * 1e-3) / 1e9, 3),
-               "breakdown_ms_in_situ": None if brk is None else {k: round(v, 4) for k, v in brk.items()},
-               "iterations": it, "ms_per_iteration": round(per_it, 4),
-               "roofline_frac": round(bp_bytes / (per_it * 1e-3) / 1e9 / peak, 3),
-               "model_bytes_per_local_point": round(bp_bytes / bn, 1),
-               "kernels_per_iteration": solver.launches_per_iter,
-               "unfused_model_frac": round((bn * 173 + 20 * op.gs.nperm) / (per_it * 1e-3) / 1e9 / peak, 3),
-               "global_counts": list(weak_counts(ws)) if ws > 1 else list(COUNTS),
-               "halo_neighbors": op.gs.ngh, "graph": bool(solver.use_graph),
-               "halo_transport": getattr(op.gs, "transport", None) if ws > 1 else None,
-               "dot_allreduce": ("ipc-board" if getattr(comm, "board", None) is not None
-                                 else "torch.distributed") if ws > 1 else None}
-        if ws > 1 and args.pmg_scaling:
-            # opt-in (--pmg-scaling): the distributed p-multigrid (Chebyshev-
-            # Jacobi, iterative coarse solve over the same halo + all-reduce)
-            # on the weak-scaling box: time to tol 1e-8 vs the distributed
-            # Jacobi-PCG, max over ranks.  Off by default so the headline
-            # scaling run never waits on the extra collectives.
-            import time as _time
-            tts = {}
-            try:
-                for name, make in (
-                        ("jacobi_pcg", lambda: nk.FusedPCG(op, jac, tol=1e-8, max_iter=5000,
-                                                           chunk=32)),
-                        ("pmg_cheby_jac", lambda: nk.MultigridPCG(
-                            op, nk.MultigridHierarchy(op, coarse="pcg"), tol=1e-8,
-                            max_iter=500))):
-                    sv = make()
-                    sv.solve(b_rhs)
-                    barrier(ws)
-                    torch.cuda.synchronize()
-                    t0 = _time.perf_counter()
-                    res = sv.solve(b_rhs)
-                    torch.cuda.synchronize()
-                    tt = max_over_ranks(_time.perf_counter() - t0, ws)
-                    tts[name] = {"iterations": res.iterations, "solve_ms": round(tt * 1e3, 3),
-                                 "converged": bool(res.converged)}
-                    del sv
-                tts["pmg_speedup_vs_jacobi_pcg"] = round(
-                    tts["jacobi_pcg"]["solve_ms"] / tts["pmg_cheby_jac"]["solve_ms"], 2)
-            except Exception as exc:  # reported, never fatal for the headline
-                tts["error"] = f"{type(exc).__name__}: {exc}"[:200]
-            bp5["time_to_solution_tol1e-8"] = tts
+    # ---- BP5 (fused Jacobi-PCG), weak scaling with same-run t_iter(1)
+    bp5 = None if args.no_bp5 else bp5_block(nk, args, ws, rank, mesh, N, peak)
 
     # ---- Time to solution at tol 1e-8 (N = 1 only, same mesh, random
     # assembled rhs): Jacobi-PCG vs the p-multigrid preconditioners
@@ -510,27 +640,20 @@ def run_ours(args):
         for name, _ in cases[1:]:
             solvers[name]["speedup_vs_jacobi_pcg"] = round(base / solvers[name]["solve_ms"], 2)
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, N=1 only): compiled oracle, full mesh
     cpu = None
     if ws == 1 and not args.no_cpu:
-        pts_s, cores, el, Es = cpu_oracle_bk5(1000, reps_target_s=10.0)
-        cpu = {"value": round(pts_s * N ** 3 / nq ** 3 / 1e9, 5), "unit": "GDOF/s",
-               "cores": cores, "kind": "port",
-               "sample": f"oracle numpy BK5 on {Es} elements (N=7, deformed), "
-                         f"{el:.1f} s, ThreadPool x{cores}"}
+        cpu = cpu_baseline_block(N, E)
 
     if rank == 0:
         traffic = ncu_traffic()
         line = {
-            "metric": "BK5 GDOF/s FP64 (N=7, E=20^3 deformed box per GPU)",
+            "metric": METRIC,
             "value": round(value, 3), "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1]: BK5 Ax sweep point N=7, E=8000 per GPU, "
-                                   "deformed box (sine 0.05)",
-                       "N": N, "elements_per_gpu": E, "local_points_per_gpu": n,
-                       "dof_per_gpu": dof, "parallelism": f"element-partitioned x{ws}",
-                       "l2": "flushed between steps: 256 MiB write + 256 MiB read (cold, clean L2 at every launch); inputs 262 MB > L2"},
+            "config": bench_config(N, E, n, dof, ws),
+            "ranks_per_gpu": ranks_per_gpu(ws),
             "local_points_per_s": round(ws * n / (ms * 1e-3) / 1e9, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -545,6 +668,8 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline_context": ceiling,
             "bp5": bp5,
+            "bp5_efficiency": None if bp5 is None else bp5.get("efficiency"),
+            "bp5_ms_per_iteration": None if bp5 is None else bp5["ms_per_iteration"],
             "bp5_time_to_solution": solvers,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
@@ -554,6 +679,22 @@ def run_ours(args):
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on 127.0.0.1 and pass rank 0's line
+    through.  Returns the launcher's exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main():
@@ -569,7 +710,12 @@ def main():
     ap.add_argument("--no-solvers", action="store_true")
     ap.add_argument("--pmg-scaling", action="store_true",
                     help="N > 1: also time the distributed p-multigrid solve")
+    ap.add_argument("--strong", action="store_true",
+                    help="BP5 on configs[2] (E = 64^3 split over the ranks) instead of the "
+                         "configs[3] weak-scaling box")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -117,29 +117,43 @@ class GatherScatterHandle:
 
 
 def point_codes(h):
-    """Per-point gs codes for the fused single-rank CG update
-    (nk_cg_update_gs, include/nekb200.h) and the gs sub-plan of the non-pair
-    segments it relies on: returns (code, plan) -- code an int32 device
-    tensor (-1 unshared, the partner's index for a 2-member segment, -M for
-    a member of an M >= 3 segment), plan a _Plan over the segments of 3 or
-    more members (run it before the update).  None with several ranks or
-    n >= 2^31.  Cached on the handle."""
+    """Per-point gs codes for the fused CG update (nk_cg_update_gs,
+    include/nekb200.h) and the gs sub-plan it relies on: returns (code,
+    plan) -- code an int32 device tensor, plan a _Plan over the rank-private
+    segments of 3 or more members (run it before the update).  Codes:
+      -1   unshared point;
+      i>=0 member of a rank-private 2-member segment, i = the partner's
+           local index (the update adds w[i]: a + b == b + a, the bits of
+           the canonical fold);
+      -M   member of an M-member segment assembled in place before the
+           update: a rank-private segment of >= 3 members (by `plan`) or,
+           on several ranks, a halo id (by the halo combine; M = its global
+           multiplicity, the number of contributions over all ranks).
+    None when n >= 2^31.  Cached on the handle."""
     import torch
     if getattr(h, "_codes", False) is not False:
         return h._codes
     res = None
-    if (h.comm is None or h.comm.size == 1) and h.n < 2 ** 31:
+    if h.n < 2 ** 31:
         perm = h.perm_h.astype(np.int64)
         seg = h.seg_h.astype(np.int64)
         sizes = np.diff(seg)
+        multi = h.comm is not None and h.comm.size > 1
+        keep = getattr(h, "private_seg", None) if multi else None
+        if keep is None:
+            keep = np.ones(len(sizes), dtype=bool)
         code = np.full(h.n, -1, dtype=np.int32)
-        two = seg[:-1][sizes == 2]
+        two = seg[:-1][(sizes == 2) & keep]
         a, b = perm[two], perm[two + 1]
         code[a], code[b] = b, a
-        sel = np.flatnonzero(sizes > 2)
+        sel = np.flatnonzero((sizes > 2) & keep)
         cnt = sizes[sel]
         mem = perm[_dist._ranges(seg[sel], cnt)] if len(sel) else np.zeros(0, np.int64)
         code[mem] = -np.repeat(cnt, cnt)
+        if multi and h.nh:
+            hp = h.halo
+            gm = np.diff(hp.src_start)            # global multiplicity per halo id
+            code[hp.dst_idx] = -np.repeat(gm, np.diff(hp.dst_start))
         sub_seg = np.r_[0, np.cumsum(cnt)].astype(np.int64)
         res = (torch.as_tensor(code, device=h.device), _Plan(mem, sub_seg, h.device))
     h._codes = res
@@ -204,6 +218,7 @@ def gs_setup(ids, comm=None, nq=None, device="cuda"):
         # every contribution in canonical order); the rest run as usual
         seg_ids = ids_h[perm[seg[:-1]]] if h.nseg else np.zeros(0, np.int64)
         is_h = np.isin(seg_ids, plan.hids)
+        h.private_seg = ~is_h
         h.seg_rest = _sub_plan(perm, seg, ~is_h, device)
         if nq is not None:
             nq3 = nq ** 3

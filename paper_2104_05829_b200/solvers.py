@@ -101,11 +101,14 @@ class PoissonOperator:
         self.apply(p, out)
         return out
 
-    def apply(self, p, w, st=None, partials=None, reduce=True):
+    def apply(self, p, w, st=None, partials=None, reduce=True, local=None):
         """w = A p (masked, assembled).  With st/partials the BK5 launch also
         stores p^T A p (the rank-local part) in st->pAp; with reduce=False the
         state only gates the launches (no-ops once st->done, e.g. inside a
-        preconditioner replayed after convergence) and st is not written."""
+        preconditioner replayed after convergence) and st is not written.
+        local: a gs sub-plan to run instead of the rank-private segments
+        (the fused CG update's >= 3-member segments, point_codes); w is then
+        assembled only at those segments and the halo ids."""
         m = self.mesh
         L, s = lib(), stream_ptr()
         D = m.basis.diff  # host: passed by value to the kernel
@@ -147,17 +150,19 @@ class PoissonOperator:
                 done.record(side)
             if ie.numel():
                 bk5(ie, nbb, (nbb + nbi) if st is not None else 0)
-            _local(g, w, "+", 1, st=st, part=g.seg_rest)
+            _local(g, w, "+", 1, st=st, part=g.seg_rest if local is None else local)
             main.wait_event(done)
             _halo_finish(g, w, "+", st=st)
         COUNTERS.add("stiffness", bk5_flops(m.N, m.E, self.ncomp), 7 * self.n * self.ncomp)
         return w
 
-    def apply_pcg(self, p, w, x, r, invD, st, partials, hist, gs=True):
+    def apply_pcg(self, p, w, x, r, invD, st, partials, hist, gs=True, local=None):
         """Fused BP5 operator step (nk_bk5_pcg): convergence test, deferred
         x += alpha p, Jacobi p = invD r + beta p, then w = A p with p^T A p
         into st->pAp -- followed by gs (and the halo on several ranks).
-        gs=False (one rank) leaves w unassembled for nk_cg_update_gs."""
+        gs=False (one rank) leaves w unassembled for nk_cg_update_gs; on
+        several ranks `local` replaces the rank-private gs segments as in
+        apply()."""
         m = self.mesh
         L, s = lib(), stream_ptr()
         D = m.basis.diff
@@ -198,7 +203,7 @@ class PoissonOperator:
                 done.record(side)
             if ie.numel():
                 k1(ie, nbb, nbb + nbi)
-            _local(g, w, "+", 1, st=st, part=g.seg_rest)
+            _local(g, w, "+", 1, st=st, part=g.seg_rest if local is None else local)
             main.wait_event(done)
             _halo_finish(g, w, "+", st=st)
         COUNTERS.add("stiffness", bk5_flops(m.N, m.E, 1), 7 * self.n)
@@ -294,7 +299,7 @@ class FusedPCG:
         self.s64 = self.st.view(torch.float64)   # rz pAp rz_new rr zap bb thresh2 alpha
         self.graph = None
         self.codes = None
-        if fuse_gs and self.comm is None:
+        if fuse_gs:
             from .gather_scatter import point_codes
             self.codes = point_codes(op.gs)
         self.launches_per_iter = 3    # bk5_pcg, gs (all | non-pair segments), update
@@ -310,18 +315,34 @@ class FusedPCG:
 
     def _iteration(self):
         """One PCG iteration = 3 kernels on one rank: nk_bk5_pcg (test,
-        x/p updates, BK5, p.Ap), gs, nk_cg_update (r, rr, rz, zAp)."""
+        x/p updates, BK5, p.Ap), gs, nk_cg_update (r, rr, rz, zAp).  On
+        several ranks the same with the boundary / interior BK5 split around
+        the halo push, the combine, and the dot all-reduces."""
         L, s = lib(), stream_ptr()
         if self.codes is not None:
-            if self.split:
+            if self.comm is not None:
+                # private face pairs fold into the update; the >= 3-member
+                # private segments run between the interior BK5 and the combine
+                if self.split:
+                    check(L.nk_cg_xpstep(self.n, ptr(self.x), ptr(self.r), ptr(self.p),
+                                         ptr(self.invD), ptr(self.st), ptr(self.hist), s),
+                          "cg_xpstep")
+                    self.op.apply(self.p, self.w, self.st, self.part_bk5, local=self.codes[1])
+                else:
+                    self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
+                                      self.part_bk5, self.hist, local=self.codes[1])
+                self._allreduce(1, 2)                                    # pAp
+            elif self.split:
                 self._split_head(L, s)
+                self.codes[1].run(self.w, "+", 1, self.n, self.st)      # edges, vertices
             else:
                 self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
                                   self.part_bk5, self.hist, gs=False)
-            self.codes[1].run(self.w, "+", 1, self.n, self.st)          # edges, vertices
+                self.codes[1].run(self.w, "+", 1, self.n, self.st)      # edges, vertices
             check(L.nk_cg_update_gs(self.n, ptr(self.r), ptr(self.w), ptr(self.invD),
                                     ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
                   "cg_update_gs")
+            self._allreduce(2, 5)                                        # rz_new rr zap
             return
         self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st, self.part_bk5,
                           self.hist)

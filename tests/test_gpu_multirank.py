@@ -58,9 +58,23 @@ def _worker(rank, world, port, outdir, counts, N, transport="auto"):
         solver = nk.FusedPCG(op, jac, tol=1e-8, max_iter=500, use_graph=(transport == "ipc"))
         res = solver.solve(torch.as_tensor(b, device="cuda"))
         graph = bool(solver.use_graph)
+        fused = solver.codes is not None
+        x = res.x.cpu().numpy().copy()
+        hist = np.array(res.residual_history)
+        # the full-gs schedule (fuse_gs=False): bit-identical solve
+        full = nk.FusedPCG(op, jac, tol=1e-8, max_iter=500, use_graph=(transport == "ipc"),
+                           fuse_gs=False)
+        rf = full.solve(torch.as_tensor(b, device="cuda"))
+        # the split head (cg_xpstep + boundary/interior BK5) converges too
+        sp = nk.FusedPCG(op, jac, tol=1e-8, max_iter=500, use_graph=(transport == "ipc"),
+                         split_step=True)
+        rs = sp.solve(torch.as_tensor(b, device="cuda"))
         np.savez(os.path.join(outdir, f"r{rank}.npz"), mine=mine, ids=m.ids.cpu().numpy(),
-                 transport=op.gs.transport, graph=graph,
-                 w=w, gsw=gsw, x=res.x.cpu().numpy(), it=res.iterations,
+                 transport=op.gs.transport, graph=graph, fused=fused,
+                 w=w, gsw=gsw, x=x, it=res.iterations, hist=hist,
+                 x_full=rf.x.cpu().numpy(), it_full=rf.iterations,
+                 hist_full=np.array(rf.residual_history), split=sp.split,
+                 x_split=rs.x.cpu().numpy(), it_split=rs.iterations,
                  conv=res.converged, ngh=op.gs.ngh, nb=op.gs.boundary_elements.numel())
     finally:
         dist.destroy_process_group()
@@ -97,11 +111,20 @@ def test_two_ranks_one_gpu_gs_and_pcg(N, transport):
                  weights=1.0 / ogs.multiplicity(g.ids))
     nq3 = (N + 1) ** 3
     xg = np.zeros((g.E, nq3))
+    xs = np.zeros((g.E, nq3))
     for r in res:
         assert bool(r["conv"]) and abs(int(r["it"]) - o.iterations) <= 1
         xg[r["mine"]] = r["x"].reshape(-1, nq3)
+        xs[r["mine"]] = r["x_split"].reshape(-1, nq3)
+        # fused face-pair update across ranks == full gs schedule, bit for bit
+        assert bool(r["fused"]) and bool(r["split"])
+        assert int(r["it_full"]) == int(r["it"])
+        assert np.array_equal(r["hist_full"], r["hist"])
+        assert np.array_equal(r["x_full"], r["x"])
+        assert abs(int(r["it_split"]) - o.iterations) <= 1
     assert int(res[0]["it"]) == int(res[1]["it"])
     assert np.max(np.abs(xg.ravel() - o.x)) < 1e-7 * np.max(np.abs(o.x))
+    assert np.max(np.abs(xs.ravel() - o.x)) < 1e-7 * np.max(np.abs(o.x))
 
 
 def _pmg_worker(rank, world, port, outdir, counts, N, transport):
