@@ -145,6 +145,25 @@ int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double*
            nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
            nk_stream_t stream);
 int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp);
+/* nk_bk5 for a 3-component batch with per-component fused dots (the batched
+ * vector-Helmholtz PCG, configs[4]; "geometric factors ...
+ * reused across each velocity component"): st points to ncomp CG states;
+ * component c's block partials of p_c . A p_c go to partials + c *
+ * part_stride (part_stride >= reduce_count) and its sum to st[c].pAp; a
+ * component whose state is done is skipped.  Runs seq3 (G from HBM once for
+ * the three components) where nk_bk5_batch_variant(N) == 6, else three
+ * scalar launches.  With st == NULL it is nk_bk5. */
+int nk_bk5_batch(int N, int64_t nelem, const double* D, const double* G, const double* u,
+                 double* w, double lam0, const double* B, double lam1, int ncomp,
+                 int64_t comp_stride, const uint8_t* mask, const int32_t* elem_list,
+                 int64_t nlist, nk_cg_state* st, double* partials, int64_t part_stride,
+                 int64_t part_base, int64_t reduce_count, nk_stream_t stream);
+/* the 3-component kernel nk_bk5 / nk_bk5_batch run at order N: 6 = seq3,
+ * 3 = pencil3, -1 = three scalar launches (the measured auto table). */
+int nk_bk5_batch_variant(int N);
+/* blocks of one nk_bk5_batch launch (ncomp = 3, with st) over nlist elements
+ * -- the reduce_count of a single launch, the minimum part_stride. */
+int64_t nk_bk5_batch_blocks(int N, int64_t nlist);
 /* kernel variant selection: 0 = auto (measured per-order table: 5 for
  * N in {2,6,8,14,15}, else 3; 3-component batches: 6 at N in {3,5,7,9,10,11},
  * pencil3 at N in {4,6}, three scalar launches elsewhere), 5 = pencil2 (two
@@ -331,6 +350,17 @@ int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
  * w = mask A p and st->pAp, then gs + nk_cg_update_gs as in the fused
  * schedule.  Used by FusedPCG at orders where it beats the
  * fused kernel (paper_2104_05829_b200/solvers.py). */
+/* Batched forms (the lockstep 3-component PCG): ncomp components at
+ * cstride in r / w (and x / p), states st[0..ncomp), partials at c * 3 *
+ * nk_cg_partials_len(n) / 3 (i.e. 3 x 1184 doubles per component), history
+ * hist + c * hstride; invD and code shared.  Each component advances, stops
+ * and counts its own iterations. */
+int nk_cg_update_gs_batch(int64_t n, int ncomp, int64_t cstride, double* r, const double* w,
+                          const double* invD, const int32_t* code, nk_cg_state* st,
+                          double* partials, nk_stream_t stream);
+int nk_cg_xpstep_batch(int64_t n, int ncomp, int64_t cstride, double* x, const double* r,
+                       double* p, const double* invD, nk_cg_state* st, double* hist,
+                       int64_t hstride, nk_stream_t stream);
 int nk_cg_xpstep(int64_t n, double* x, const double* r, double* p, const double* invD,
                  nk_cg_state* st, double* hist, nk_stream_t stream);
 
@@ -378,6 +408,12 @@ int nk_cg_gate(nk_cg_state* inner, const nk_cg_state* outer, nk_stream_t stream)
 /* out[0] = <a, b>_wt (wt nullable = unweighted), deterministic two-stage. */
 int nk_wdot(int64_t n, const double* a, const double* b, const double* wt, double* out,
             double* partials, nk_stream_t stream);
+
+/* y = alpha * a * b (* mask when non-null), pointwise -- apply_mass (B u,
+ * SPEC.md:380-388) and the Jacobi preconditioner z = invD r
+ * outside the fused PCG.  y may alias a or b. */
+int nk_pointwise(int64_t n, const double* a, const double* b, double* y, double alpha,
+                 const uint8_t* mask, nk_stream_t stream);
 
 /* ---- projection-based initial guesses ----
  * The ProjectionSpace holds k <= NK_PROJ_MAX prior solutions X[q] and A X[q]

@@ -25,6 +25,12 @@ Frozen choices:
   * V-cycle: pre-smooth, residual, restrict, recurse, prolong + correct,
     post-smooth on the updated residual; coarsest level: exact solve of the
     assembled masked operator (dense inverse on unique unmasked dofs).
+  * Chebyshev bounds: SPEC.md:548's (0.1, 1.1) x lambda_max for cheby_jac;
+    (0.4, 1.1) for cheby_asm / cheby_ras.  Deviation: with 0.1 the degree-2
+    polynomial damps the whole S A spectrum by ~0.53, worse than one
+    undamped Schwarz application (lambda_max(S A) ~ 1.5), so CHEBY-ASM took
+    10 iterations vs ASM's 7 on SPEC.md:541's problem; 0.4 gives 5
+    (profiles/r2_smoother_bounds.jsonl).
 """
 
 import numpy as np
@@ -117,9 +123,11 @@ def smooth(lv, r, degree):
 
 
 def build_hierarchy(extent, counts, N, bc="dirichlet", deformation=None, lam0=1.0, lam1=0.0,
-                    degree=2, bounds=(0.1, 1.1), power_iters=20, smoother="cheby_jac"):
+                    degree=2, bounds=None, power_iters=20, smoother="cheby_jac"):
     if smoother not in SMOOTHERS:
         raise ValueError(f"unknown smoother {smoother!r}")
+    if bounds is None:        # (0.4, 1.1) for Chebyshev-Schwarz: see the module doc
+        bounds = (0.4, 1.1) if smoother in ("cheby_asm", "cheby_ras") else (0.1, 1.1)
     levels = []
     for n in orders_for(N):
         lv = Level()

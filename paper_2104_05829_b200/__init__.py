@@ -23,7 +23,7 @@ from .multigrid import (MultigridHierarchy, MultigridPCG, chebyshev_smooth,  # n
 from .partition import rcb  # noqa: F401
 from .projection import ProjectedSolver, ProjectionSpace, project_guess  # noqa: F401
 from .schwarz import SchwarzSmoother, fdm_local_solve, schwarz_smooth  # noqa: F401
-from .solvers import (BreakdownError, FusedPCG, HelmholtzVectorSolver,  # noqa: F401
+from .solvers import (BreakdownError, FusedPCG, FusedPCG3, HelmholtzVectorSolver,  # noqa: F401
                       JacobiPreconditioner, PoissonOperator, pcg)
 
 __version__ = "1.0.0"

@@ -103,6 +103,13 @@ _SIGS = {
     "nk_multi_wdot": ([_I64, _I32, _P, _I64, _P, _P, _P, _P, _P], _I32),
     "nk_multi_axpy": ([_I64, _I32, _P, _D, _P, _I64, _P, _P, _P], _I32),
     "nk_vscale": ([_I64, _P, _P, _P, _P], _I32),
+    "nk_pointwise": ([_I64, _P, _P, _P, _D, _P, _P], _I32),
+    "nk_bk5_batch": ([_I32, _I64, _P, _P, _P, _P, _D, _P, _D, _I32, _I64, _P, _P, _I64, _P, _P,
+                      _I64, _I64, _I64, _P], _I32),
+    "nk_bk5_batch_variant": ([_I32], _I32),
+    "nk_bk5_batch_blocks": ([_I32, _I64], _I64),
+    "nk_cg_update_gs_batch": ([_I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "nk_cg_xpstep_batch": ([_I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _I64, _P], _I32),
     "nk_fdm": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
     "nk_fdm32": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
     "nk_gather_diff": ([_I64, _P, _P, _P, _P, _P, _P], _I32),

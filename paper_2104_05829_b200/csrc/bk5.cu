@@ -5,7 +5,7 @@
 typedef int (*kslab_fn)(int, int64_t, const int32_t*, const double*, const double*, const double*,
                         double*, double, const double*, double, int64_t, const uint8_t*,
                         nk_cg_state*, double*, int64_t, int64_t, cudaStream_t, int64_t*, int,
-                        int, int);
+                        int, int, int64_t);
 typedef int (*diag_fn)(int64_t, const double*, const double*, double, const double*, double,
                        double*, cudaStream_t);
 
@@ -14,7 +14,7 @@ typedef int (*diag_fn)(int64_t, const double*, const double*, double, const doub
                                      const double*, const double*, double*, double,           \
                                      const double*, double, int64_t, const uint8_t*,          \
                                      nk_cg_state*, double*, int64_t, int64_t, cudaStream_t,   \
-                                     int64_t*, int, int, int);                                \
+                                     int64_t*, int, int, int, int64_t);                       \
   extern "C" int nk_local_diag_nq##NQ(int64_t, const double*, const double*, double,         \
                                       const double*, double, double*, cudaStream_t);
 #define NK_DECLP(NQ)                                                                        \
@@ -87,8 +87,48 @@ extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {
   if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) return -1;
   int64_t nb = -1;
   kslab_table[N](ncomp, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0, 0,
-                 nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, g_cfg, g_pf, kvariant_for(N));
+                 nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, g_cfg, g_pf, kvariant_for(N), 0);
   return nb;
+}
+
+// the 3-component kernel the auto table picks per order (-1: three scalar
+// launches), measured on the B200 (scripts/bk5_sweep.py --helm3,
+// profiles/r1k_helm3.jsonl):
+//   seq3    -- bk5_pencil<NC = 3>: the three components back to back in one
+//              CTA, G from HBM once and re-read from L2 (N = 3, 5, 7, 9, 10,
+//              11);
+//   pencil3 -- the three components interleaved, G in registers once
+//              (N = 4, 6);
+//   scalar  -- three scalar launches, G read three times (N = 1, 2, 8,
+//              12..15, where both batched forms spill or lose occupancy).
+// A forced variant (nk_bk5_set_variant) keeps its own kernel: 6 = seq3,
+// any other = pencil3 / k-slab.
+static int helm3_variant(int N) {
+  int v = nk_bk5_variant_get();
+  if (v != 0) return v;
+  switch (N) {
+    case 3: case 5: case 7: case 9: case 10: case 11: return 6;
+    case 4: case 6: return 3;
+    default: return -1;
+  }
+}
+
+extern "C" int64_t nk_bk5_batch_blocks(int N, int64_t nlist) {
+  if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) return -1;
+  int64_t nb = -1;
+  const int v = helm3_variant(N);
+  if (v == 6)
+    kslab_table[N](3, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0, 0,
+                   nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, g_cfg, g_pf, 6, 0);
+  else
+    kslab_table[N](1, nlist, nullptr, nullptr, nullptr, nullptr, nullptr, 1.0, nullptr, 0.0, 0,
+                   nullptr, nullptr, nullptr, 0, 0, nullptr, &nb, g_cfg, g_pf, kvariant_for(N), 0);
+  return nb;
+}
+
+extern "C" int nk_bk5_batch_variant(int N) {
+  if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) return -2;
+  return helm3_variant(N);
 }
 
 extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, const double* u,
@@ -96,6 +136,20 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
                       int64_t comp_stride, const uint8_t* mask, const int32_t* elem_list,
                       int64_t nlist, nk_cg_state* st, double* partials, int64_t part_base,
                       int64_t reduce_count, nk_stream_t stream) {
+  if (ncomp == 3 && st != nullptr) {
+    set_error("bk5: the fused dots of a 3-component batch need nk_bk5_batch");
+    return NK_ERR_INVALID;
+  }
+  return nk_bk5_batch(N, nelem, D, G, u, w, lam0, B, lam1, ncomp, comp_stride, mask, elem_list,
+                      nlist, st, partials, 0, part_base, reduce_count, stream);
+}
+
+extern "C" int nk_bk5_batch(int N, int64_t nelem, const double* D, const double* G,
+                            const double* u, double* w, double lam0, const double* B,
+                            double lam1, int ncomp, int64_t comp_stride, const uint8_t* mask,
+                            const int32_t* elem_list, int64_t nlist, nk_cg_state* st,
+                            double* partials, int64_t part_stride, int64_t part_base,
+                            int64_t reduce_count, nk_stream_t stream) {
   if (N < NK_MIN_ORDER || N > NK_MAX_ORDER) {
     set_error("bk5: order N=%d outside compiled range [%d, %d]", N, NK_MIN_ORDER, NK_MAX_ORDER);
     return NK_ERR_UNSUPPORTED;
@@ -121,42 +175,32 @@ extern "C" int nk_bk5(int N, int64_t nelem, const double* D, const double* G, co
     set_error("bk5: comp_stride too small");
     return NK_ERR_INVALID;
   }
+  if (ncomp > 1 && st != nullptr && part_stride < (reduce_count > 0 ? reduce_count : 1)) {
+    set_error("bk5: part_stride too small for the per-component partials");
+    return NK_ERR_INVALID;
+  }
   cudaStream_t s = S(stream);
-  // 3-component batches (vector Helmholtz), measured per order on the B200
-  // (scripts/bk5_sweep.py --helm3, profiles/r1k_helm3.jsonl):
-  //   seq3    -- bk5_pencil<NC = 3>: the three components back to back in one
-  //              CTA, G from HBM once and re-read from L2 (N = 3, 5, 7, 9, 10,
-  //              11);
-  //   pencil3 -- the three components interleaved, G in registers once
-  //              (N = 4, 6);
-  //   scalar  -- three scalar launches, G read three times (N = 1, 2, 8,
-  //              12..15, where both batched forms spill or lose occupancy).
-  // A forced variant (nk_bk5_set_variant) keeps its own kernel: 6 = seq3,
-  // any other = pencil3 / k-slab as before.
-  if (ncomp == 3 && st == nullptr) {
-    int v = nk_bk5_variant_get();
-    if (v == 0) {
-      switch (N) {
-        case 3: case 5: case 7: case 9: case 10: case 11: v = 6; break;
-        case 4: case 6: v = 3; break;
-        default: v = -1; break;
+  if (ncomp == 3) {
+    int v = helm3_variant(N);
+    // fused per-component dots: seq3 or three scalar launches
+    if (st != nullptr && v != 6) v = -1;
+    if (v == -1) {
+      for (int c = 0; c < 3; ++c) {
+        int rc = kslab_table[N](1, n, elem_list, D, G, u + c * comp_stride, w + c * comp_stride,
+                                lam0, B, lam1, comp_stride, mask, st ? st + c : nullptr,
+                                st ? partials + c * part_stride : nullptr, part_base,
+                                reduce_count, s, nullptr, g_cfg, g_pf, kvariant_for(N), 0);
+        if (rc != NK_OK) return rc;
       }
-      if (v == -1) {
-        for (int c = 0; c < 3; ++c) {
-          int rc = kslab_table[N](1, n, elem_list, D, G, u + c * comp_stride,
-                                  w + c * comp_stride, lam0, B, lam1, comp_stride, mask, nullptr,
-                                  nullptr, 0, 0, s, nullptr, g_cfg, g_pf, kvariant_for(N));
-          if (rc != NK_OK) return rc;
-        }
-        return NK_OK;
-      }
+      return NK_OK;
     }
-    return kslab_table[N](3, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, nullptr,
-                          nullptr, 0, 0, s, nullptr, g_cfg, g_pf, v);
+    return kslab_table[N](3, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, st,
+                          partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf, v,
+                          part_stride);
   }
   return kslab_table[N](ncomp, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, st,
                         partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf,
-                        kvariant_for(N));
+                        kvariant_for(N), 0);
 }
 
 extern "C" int nk_local_diag(int N, int64_t nelem, const double* D, const double* G, double lam0,

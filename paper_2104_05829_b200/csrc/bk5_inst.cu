@@ -213,7 +213,7 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
                                                  nk_cg_state* st, double* partials,
                                                  int64_t part_base, int64_t reduce_count,
                                                  cudaStream_t s, int64_t* nblocks, int cfg,
-                                                 int pf_dist, int variant) {
+                                                 int pf_dist, int variant, int64_t pstride) {
   constexpr int NQ = NK_BK5_NQ;
   if constexpr (NQ == 2) {   // N = 1: element per thread unless k-slab is forced
     if (ncomp == 1 && variant != 1) {
@@ -239,8 +239,9 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
 #undef NK_TARGS
     }
   }
-  if (ncomp == 3 && st == nullptr && variant == 6) {
-    // 3 components back to back per CTA, G from HBM once (bk5_pencil NC = 3)
+  if (ncomp == 3 && variant == 6) {
+    // 3 components back to back per CTA, G from HBM once (bk5_pencil NC = 3);
+    // with st: three CG states, per-component fused p.Ap (nk_bk5_batch)
 #ifdef NK_BK5_SHAPE_SWEEP
     if constexpr (NQ >= 3 && NQ != 8) {
       using A = PencilAlt<NQ>;
@@ -265,8 +266,9 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
       *nblocks = (nlist + EPB - 1) / EPB;
       return NK_OK;
     }
-    return launch_pencil<NQ, EPB, MINB, 3>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, nullptr,
-                                           nullptr, 0, 0, s, pf_dist, cstride);
+    return launch_pencil<NQ, EPB, MINB, 3>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st,
+                                           partials, part_base, reduce_count, s, pf_dist, cstride,
+                                           pstride);
   }
   if constexpr (NQ >= 2 && NQ <= 12) {
     // 3-component batch: G read once per element (pencil3); k-slab otherwise

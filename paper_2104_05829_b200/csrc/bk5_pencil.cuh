@@ -87,26 +87,35 @@ __device__ __forceinline__ void matvec(const DParam<NQ>& D, const double (&v)[NQ
 // (L2 prefetch at CTA start) and re-read from L2 by components 1 and 2, so HBM
 // moves 104 B per point for three components instead of 3 x 72, while the
 // register and shared footprint stays that of the scalar kernel.
-template <int NQ, int EPB, int MINB, int NC = 1>
+template <int NQ, int EPB, int MINB, int NC = 1, bool CDOT = false>
 __global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
 bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
            const double* __restrict__ G, const double* __restrict__ u_, double* __restrict__ w_,
            double lam0, const double* __restrict__ B, double lam1,
            const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
            int64_t part_base, int64_t reduce_count, int pfG, int64_t pf_ahead,
-           int64_t cstride = 0) {
+           int64_t cstride = 0, int64_t pstride = 0) {
+  // NC = 3, CDOT (the batched 3-component PCG, nk_bk5_batch): st points to
+  // three CG states; component c's p.Ap partials go to partials + c *
+  // pstride and its sum to st[c].pAp; a component whose state is done is
+  // skipped (its p no longer changes).
   static_assert(NC == 1 || NC == 3, "NC");
   using L = PencilLayout<NQ>;
   constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, VOL = L::VOL;
   extern __shared__ double smem[];
-  if (st != nullptr && st->done) return;
+  if ((NC == 1 || CDOT) && st != nullptr) {
+    bool all_done = true;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) all_done = all_done && st[c].done;
+    if (all_done) return;
+  }
 
   const int t = threadIdx.x;
   const int le = t / NQ2;
   const int tt = t - le * NQ2;
   const int a = tt % NQ, b = tt / NQ;
   double* red = smem;
-  double* U = smem + 32 + (size_t)le * 3 * VOL;
+  double* U = smem + 32 * NC + (size_t)le * 3 * VOL;
   double* Rr = U + VOL;
   double* Ss = Rr + VOL;
 
@@ -135,6 +144,10 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   double* w = w_ + c * cstride;
   const double* ue = u + e * NQ3;
   if (NC > 1 && c > 0) __syncthreads();  // previous component's B1 reads of R / U
+  if (NC > 1 && CDOT && st[c].done) {   // uniform over the grid
+    if (t == 0) partials[c * pstride + part_base + blockIdx.x] = 0.0;
+    continue;
+  }
 
   // ---- F1: i-pencils (j = a, k = b)
   if (active) {
@@ -251,31 +264,66 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
     }
   }
 
-  }  // components
-  if (st != nullptr) {
+  if (NC > 1 && CDOT) {
+    // this component's block partial now (no accumulator lives across the
+    // next component's contractions: the seq3 register budget is unchanged)
     double vv[1] = {dot};
     block_sum<1>(vv, red);
-    if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+    if (t == 0) partials[c * pstride + part_base + blockIdx.x] = vv[0];
+    dot = 0.0;
+  }
+  }  // components
+  if ((NC == 1 || CDOT) && st != nullptr) {
+    if (NC == 1) {
+      double vv[1] = {dot};
+      block_sum<1>(vv, red);
+      if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+    }
     if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
-      double s[1];
-      reduce_partials<1>(partials, reduce_count, 0, s, red);
-      if (t == 0) st->pAp = s[0];
+      double s[NC];
+      reduce_partials<NC>(partials, reduce_count, pstride, s, red);
+      if (t == 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) st[c].pAp = s[c];
+      }
     }
   }
 }
+
+template <int NQ, int EPB, int MINB, int NC, bool CDOT>
+static int launch_pencil_k(int64_t nlist, const int32_t* elist, const double* Dhost,
+                           const double* G, const double* u, double* w, double lam0,
+                           const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
+                           double* partials, int64_t part_base, int64_t reduce_count,
+                           cudaStream_t s, int pfG, int64_t cstride, int64_t pstride);
 
 template <int NQ, int EPB, int MINB, int NC = 1>
 static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhost,
                          const double* G, const double* u, double* w, double lam0,
                          const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
                          double* partials, int64_t part_base, int64_t reduce_count,
-                         cudaStream_t s, int pfG, int64_t cstride = 0) {
+                         cudaStream_t s, int pfG, int64_t cstride = 0, int64_t pstride = 0) {
+  if (NC > 1 && st != nullptr)   // per-component fused dots (nk_bk5_batch)
+    return launch_pencil_k<NQ, EPB, MINB, NC, (NC > 1)>(nlist, elist, Dhost, G, u, w, lam0, B,
+                                                       lam1, mask, st, partials, part_base,
+                                                       reduce_count, s, pfG, cstride, pstride);
+  return launch_pencil_k<NQ, EPB, MINB, NC, false>(nlist, elist, Dhost, G, u, w, lam0, B, lam1,
+                                                   mask, st, partials, part_base, reduce_count, s,
+                                                   pfG, cstride, pstride);
+}
+
+template <int NQ, int EPB, int MINB, int NC, bool CDOT>
+static int launch_pencil_k(int64_t nlist, const int32_t* elist, const double* Dhost,
+                           const double* G, const double* u, double* w, double lam0,
+                           const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
+                           double* partials, int64_t part_base, int64_t reduce_count,
+                           cudaStream_t s, int pfG, int64_t cstride, int64_t pstride) {
   using C = PencilCfg<NQ, EPB, MINB>;
   static int64_t resident = -1;  // CTAs resident on the device (one wave)
-  const size_t smem = C::smem_bytes();
+  const size_t smem = C::smem_bytes() + sizeof(double) * 32 * (NC - 1);
   static bool configured = false;
   if (!configured) {
-    cudaError_t err = cudaFuncSetAttribute(bk5_pencil<NQ, EPB, MINB, NC>,
+    cudaError_t err = cudaFuncSetAttribute(bk5_pencil<NQ, EPB, MINB, NC, CDOT>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) {
       set_error("bk5_pencil: smem attribute (%zu B): %s", smem, cudaGetErrorString(err));
@@ -289,17 +337,17 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil<NQ, EPB, MINB, NC>, C::THREADS,
-                                                  smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil<NQ, EPB, MINB, NC, CDOT>,
+                                                  C::THREADS, smem);
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
   DParam<NQ> D;
   for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
   // pfG: 0 off, 1 own G into L2, 2 own G + the element one wave ahead
   const int64_t ahead = pfG >= 2 ? resident * EPB : 0;
-  bk5_pencil<NQ, EPB, MINB, NC><<<(unsigned)nblk, C::THREADS, smem, s>>>(
+  bk5_pencil<NQ, EPB, MINB, NC, CDOT><<<(unsigned)nblk, C::THREADS, smem, s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG,
-      ahead, cstride);
+      ahead, cstride, pstride);
   return check_launch("bk5_pencil");
 }
 

@@ -115,15 +115,25 @@ __device__ __forceinline__ void gs_point(int32_t c, double own, double partner, 
 // advanced here.
 // GS (implies FUSED): Ap is the pair-unassembled w, assembled per point
 // from the gs code (gs_point) -- generic fallback of nk_cg_update_gs.
+// Batched (gridDim.y = ncomp components, component c at offset c * cstride
+// in r / Ap, state st + c, partials + c * 3 * kVecMaxBlocks): the GS path
+// only (nk_cg_update_gs_batch); x / p / invD / wt / code are shared.
 template <bool VEC, bool FUSED, bool GS = false>
 __global__ void __launch_bounds__(kVecThreads)
 cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                  const double* __restrict__ p, const double* __restrict__ Ap,
                  const double* __restrict__ invD, const double* __restrict__ wt,
                  const uint8_t* __restrict__ mult, nk_cg_state* st,
-                 double* __restrict__ partials, const int32_t* __restrict__ code = nullptr) {
+                 double* __restrict__ partials, const int32_t* __restrict__ code = nullptr,
+                 int64_t cstride = 0) {
   __shared__ double red[3 * 32];
   __shared__ double rcp_tab[256];  // exact 1/m for the u8 multiplicity weights
+  if (GS && blockIdx.y) {
+    r += blockIdx.y * cstride;
+    Ap += blockIdx.y * cstride;
+    st += blockIdx.y;
+    partials += blockIdx.y * 3 * (int64_t)kVecMaxBlocks;
+  }
   if (st->done) return;
   if (mult != nullptr || GS) {
     for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
@@ -219,12 +229,19 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
 // -- codes, r, w, invD of U pairs, then the pair partners -- instead of a
 // dependent chain per point; same per-thread point order and accumulation
 // as the generic form (bit-identical sums).  80 registers -> 3 CTAs/SM.
+// Batched like cg_update_kernel: gridDim.y components at cstride.
 __global__ void __launch_bounds__(kVecThreads, 4)
 cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restrict__ w,
                         const double* __restrict__ invD, const int32_t* __restrict__ code,
-                        nk_cg_state* st, double* __restrict__ partials) {
+                        nk_cg_state* st, double* __restrict__ partials, int64_t cstride = 0) {
   __shared__ double red[3 * 32];
   __shared__ double rcp_tab[256];
+  if (blockIdx.y) {
+    r += blockIdx.y * cstride;
+    w += blockIdx.y * cstride;
+    st += blockIdx.y;
+    partials += blockIdx.y * 3 * (int64_t)kVecMaxBlocks;
+  }
   if (st->done) return;
   for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
   __syncthreads();
@@ -437,21 +454,28 @@ extern "C" int nk_cg_update(int64_t n, double* x, double* r, const double* p, co
   return check_launch("cg_update");
 }
 
-extern "C" int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
-                               const int32_t* code, nk_cg_state* st, double* partials,
-                               nk_stream_t stream) {
-  if (n < 0 || !r || !w || !code || !st || !partials) {
+extern "C" int nk_cg_update_gs_batch(int64_t n, int ncomp, int64_t cstride, double* r,
+                                     const double* w, const double* invD, const int32_t* code,
+                                     nk_cg_state* st, double* partials, nk_stream_t stream) {
+  if (n < 0 || ncomp < 1 || ncomp > 65535 || (ncomp > 1 && cstride < n) || !r || !w || !code ||
+      !st || !partials) {
     set_error("cg_update_gs: invalid arguments");
     return NK_ERR_INVALID;
   }
-  const unsigned g = (unsigned)vec_grid(n);
+  const dim3 g((unsigned)vec_grid(n), (unsigned)ncomp);
   cudaStream_t s = S(stream);
-  if (aligned16(r, w, invD) && ((uintptr_t)code & 7) == 0)
-    cg_update_gs_vec_kernel<<<g, kVecThreads, 0, s>>>(n, r, w, invD, code, st, partials);
+  if (aligned16(r, w, invD) && ((uintptr_t)code & 7) == 0 && (cstride % 2 == 0 || ncomp == 1))
+    cg_update_gs_vec_kernel<<<g, kVecThreads, 0, s>>>(n, r, w, invD, code, st, partials, cstride);
   else
     cg_update_kernel<false, true, true><<<g, kVecThreads, 0, s>>>(
-        n, nullptr, r, nullptr, w, invD, nullptr, nullptr, st, partials, code);
+        n, nullptr, r, nullptr, w, invD, nullptr, nullptr, st, partials, code, cstride);
   return check_launch("cg_update_gs");
+}
+
+extern "C" int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
+                               const int32_t* code, nk_cg_state* st, double* partials,
+                               nk_stream_t stream) {
+  return nk_cg_update_gs_batch(n, 1, 0, r, w, invD, code, st, partials, stream);
 }
 
 extern "C" int nk_cg_pupdate(int64_t n, const double* r, double* p, const double* invD,
@@ -475,11 +499,20 @@ extern "C" int nk_cg_pupdate(int64_t n, const double* r, double* p, const double
 // the stop / rz bookkeeping exactly as nk_bk5_pcg's last block does.  Followed
 // by nk_bk5 with st (w = mask A p, st->pAp) it replaces nk_bk5_pcg at orders
 // where the fused kernel's row-wise prologue is latency-bound (N != 7).
+// Batched: gridDim.y components, component c at c * cstride in x / r / p,
+// state st + c, history hist + c * hstride (invD shared).
 template <bool VEC>
 __global__ void __launch_bounds__(kVecThreads)
 cg_xpstep_kernel(int64_t n, double* __restrict__ x, const double* __restrict__ r,
                  double* __restrict__ p, const double* __restrict__ invD, nk_cg_state* st,
-                 double* __restrict__ hist) {
+                 double* __restrict__ hist, int64_t cstride = 0, int64_t hstride = 0) {
+  if (blockIdx.y) {
+    x += blockIdx.y * cstride;
+    r += blockIdx.y * cstride;
+    p += blockIdx.y * cstride;
+    st += blockIdx.y;
+    if (hist) hist += blockIdx.y * hstride;
+  }
   if (st->done) return;
   const int it = st->iter;
   const bool conv = it > 0 && st->rr <= st->thresh2;
@@ -534,20 +567,57 @@ cg_xpstep_kernel(int64_t n, double* __restrict__ x, const double* __restrict__ r
   }
 }
 
-extern "C" int nk_cg_xpstep(int64_t n, double* x, const double* r, double* p,
-                            const double* invD, nk_cg_state* st, double* hist,
-                            nk_stream_t stream) {
-  if (n < 0 || !x || !r || !p || !invD || !st) {
+extern "C" int nk_cg_xpstep_batch(int64_t n, int ncomp, int64_t cstride, double* x,
+                                  const double* r, double* p, const double* invD,
+                                  nk_cg_state* st, double* hist, int64_t hstride,
+                                  nk_stream_t stream) {
+  if (n < 0 || ncomp < 1 || ncomp > 65535 || (ncomp > 1 && cstride < n) || !x || !r || !p ||
+      !invD || !st) {
     set_error("cg_xpstep: invalid arguments");
     return NK_ERR_INVALID;
   }
-  if (aligned16(x, r, p, invD))
-    cg_xpstep_kernel<true><<<(unsigned)vec_grid(n), kVecThreads, 0, S(stream)>>>(n, x, r, p, invD,
-                                                                               st, hist);
+  const dim3 g((unsigned)vec_grid(n), (unsigned)ncomp);
+  if (aligned16(x, r, p, invD) && (cstride % 2 == 0 || ncomp == 1))
+    cg_xpstep_kernel<true><<<g, kVecThreads, 0, S(stream)>>>(n, x, r, p, invD, st, hist, cstride,
+                                                            hstride);
   else
-    cg_xpstep_kernel<false><<<(unsigned)vec_grid(n), kVecThreads, 0, S(stream)>>>(n, x, r, p,
-                                                                                invD, st, hist);
+    cg_xpstep_kernel<false><<<g, kVecThreads, 0, S(stream)>>>(n, x, r, p, invD, st, hist,
+                                                             cstride, hstride);
   return check_launch("cg_xpstep");
+}
+
+extern "C" int nk_cg_xpstep(int64_t n, double* x, const double* r, double* p,
+                            const double* invD, nk_cg_state* st, double* hist,
+                            nk_stream_t stream) {
+  return nk_cg_xpstep_batch(n, 1, 0, x, r, p, invD, st, hist, 0, stream);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kVecThreads)
+pointwise_kernel(int64_t n, const double* a, const double* b, double* y, double alpha,
+                 const uint8_t* __restrict__ mask) {
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  if (VEC) {
+    const int64_t np = n >> 1;
+    for (int64_t q = gtid; q < np; q += nthr) {
+      const double2 av = reinterpret_cast<const double2*>(a)[q];
+      const double2 bv = reinterpret_cast<const double2*>(b)[q];
+      double2 yv = make_double2(alpha * av.x * bv.x, alpha * av.y * bv.y);
+      if (mask) {
+        const uchar2 mv = reinterpret_cast<const uchar2*>(mask)[q];
+        yv.x = mv.x ? yv.x : 0.0;
+        yv.y = mv.y ? yv.y : 0.0;
+      }
+      reinterpret_cast<double2*>(y)[q] = yv;
+    }
+    if ((n & 1) && gtid == 0) {
+      const int64_t q = n - 1;
+      y[q] = (mask && !mask[q]) ? 0.0 : alpha * a[q] * b[q];
+    }
+  } else {
+    for (int64_t q = gtid; q < n; q += nthr) y[q] = (mask && !mask[q]) ? 0.0 : alpha * a[q] * b[q];
+  }
 }
 
 __global__ void cg_gate_kernel(nk_cg_state* inner, const nk_cg_state* outer) {
@@ -561,6 +631,21 @@ extern "C" int nk_cg_gate(nk_cg_state* inner, const nk_cg_state* outer, nk_strea
   }
   cg_gate_kernel<<<1, 1, 0, S(stream)>>>(inner, outer);
   return check_launch("cg_gate");
+}
+
+extern "C" int nk_pointwise(int64_t n, const double* a, const double* b, double* y,
+                            double alpha, const uint8_t* mask, nk_stream_t stream) {
+  if (n < 0 || !a || !b || !y) {
+    set_error("pointwise: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  if (n == 0) return NK_OK;
+  const unsigned g = (unsigned)vec_grid(n);
+  if (aligned16(a, b, y) && ((uintptr_t)mask & 1) == 0)
+    pointwise_kernel<true><<<g, kVecThreads, 0, S(stream)>>>(n, a, b, y, alpha, mask);
+  else
+    pointwise_kernel<false><<<g, kVecThreads, 0, S(stream)>>>(n, a, b, y, alpha, mask);
+  return check_launch("pointwise");
 }
 
 extern "C" int nk_wdot(int64_t n, const double* a, const double* b, const double* wt,

@@ -6,6 +6,7 @@ Helmholtz form lam0*A + lam1*B and the
 3-component batch (G read once for u, v, w) use the same launch.
 """
 
+from contextlib import contextmanager
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -31,6 +32,27 @@ class KernelCounters:
     def reset(self):
         self.flops.clear()
         self.memory_refs.clear()
+
+    @contextmanager
+    def recording(self):
+        """Divert adds into a fresh KernelCounters (yielded) for the duration:
+        graph-captured solvers record one captured iteration's counts here and
+        add them once per iteration actually executed (add_scaled), so the
+        totals count device work, not captures or no-op replays."""
+        saved = (self.flops, self.memory_refs)
+        rec = KernelCounters()
+        self.flops, self.memory_refs = rec.flops, rec.memory_refs
+        try:
+            yield rec
+        finally:
+            self.flops, self.memory_refs = saved
+
+    def add_scaled(self, other, num, den=1):
+        """self += other * num / den (exact integer arithmetic)."""
+        for k, v in other.flops.items():
+            self.flops[k] = self.flops.get(k, 0) + v * int(num) // int(den)
+        for k, v in other.memory_refs.items():
+            self.memory_refs[k] = self.memory_refs.get(k, 0) + v * int(num) // int(den)
 
 
 COUNTERS = KernelCounters()
@@ -215,11 +237,16 @@ def apply_helmholtz_local(u, mesh, lam0, lam1, ncomp=1, out=None, elements=None)
     return w.cpu().numpy().reshape(np.shape(u)) if host else w
 
 
-def apply_mass(u, mesh):
-    """B u: pointwise, through the BK5 launch with lam0 = 0
-    would stream G needlessly, so this is a plain device multiply."""
+def apply_mass(u, mesh, out=None):
+    """B u: pointwise (nk_pointwise; the BK5 launch with
+    lam0 = 0 would stream G needlessly)."""
+    import torch
     t, host = _as_device(u, mesh, 1)
-    w = t * mesh.B.reshape(t.shape)
+    if t.numel() != mesh.n_local:
+        raise ContractError(f"contract error: field length {t.numel()} != {mesh.n_local}")
+    w = torch.empty_like(t) if out is None else out
+    check(lib().nk_pointwise(mesh.n_local, ptr(mesh.B), ptr(t), ptr(w), 1.0, None, stream_ptr()),
+          "pointwise")
     return w.cpu().numpy() if host else w
 
 

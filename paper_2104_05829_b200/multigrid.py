@@ -28,7 +28,12 @@ PAPER.md:312-313 CHEBY-ASM).  Schwarz smoothing is not symmetric in the PCG
 inner product (the counting weight): use flexible PCG.
 
 Frozen choices (oracle/pmg.py states the same algorithm on the CPU):
-degree 2, bounds (0.1, 1.1) x lambda_max of S A (S the inner smoother),
+degree 2, bounds (0.1, 1.1) x lambda_max of S A for Chebyshev-Jacobi and
+(0.4, 1.1) for Chebyshev-Schwarz (SCHWARZ_BOUNDS: with the lower fraction
+at SPEC's 0.1 the degree-2 polynomial damps the whole S A spectrum by only
+~0.53 and CHEBY-ASM needs MORE iterations than one undamped ASM application,
+10 vs 7 on SPEC.md:541's E = 64 problem; 0.4 gives 5 -- measured with the
+oracle, profiles/r2_smoother_bounds.jsonl; explicit `bounds` override both),
 lambda_max from 20 power iterations from a fixed-seed random start (SPEC's
 10 iterations from the ones vector underestimate it by ~30% at N = 7 and make
 the smoother amplify the top of the spectrum -- DESIGN.md "p-multigrid").
@@ -46,6 +51,11 @@ __all__ = ["MultigridHierarchy", "MultigridPCG", "chebyshev_smooth", "pmg_precon
 
 SMOOTHERS = ("jacobi", "cheby_jac", "asm", "ras", "cheby_asm", "cheby_ras")
 _SCHWARZ = {"asm": "asm", "ras": "ras", "cheby_asm": "asm", "cheby_ras": "ras"}
+
+# default Chebyshev bound fractions of lambda_max(S A): SPEC.md:548 for the
+# Jacobi smoothers, a measured lower fraction for the Schwarz ones (above)
+JACOBI_BOUNDS = (0.1, 1.1)
+SCHWARZ_BOUNDS = (0.4, 1.1)
 
 DENSE_COARSE_MAX = 16384     # unique unmasked coarse dofs (2 GiB FP64 inverse)
 
@@ -138,7 +148,7 @@ class MultigridHierarchy:
     parAlmond) here; the iterative coarse solve is the
     scalable stand-in built on the same fused PCG kernels."""
 
-    def __init__(self, op, degree=2, bounds=(0.1, 1.1), power_iters=20, seed=2104,
+    def __init__(self, op, degree=2, bounds=None, power_iters=20, seed=2104,
                  coarse="auto", smoother="cheby_jac", smoother_precision=64, coarse_tol=1e-2,
                  coarse_iters=50):
         import torch
@@ -162,6 +172,8 @@ class MultigridHierarchy:
 
             if coarse == "dense":
                 raise ContractError("the dense coarse solve is single-rank: use coarse='pcg'")
+        if bounds is None:
+            bounds = SCHWARZ_BOUNDS if smoother in ("cheby_asm", "cheby_ras") else JACOBI_BOUNDS
         if not (0.0 < bounds[0] < bounds[1]):
             raise ContractError(f"invalid eigenvalue bound fractions {bounds}")
         self.degree = int(degree)
@@ -592,19 +604,28 @@ class MultigridPCG:
     def run(self):
         import torch
         from .solvers import read_state
+        from .kernels import COUNTERS
         if self.use_graph and self.graph is None:
-            # warm-up outside capture (first-call attribute setup), then reset
-            self._iteration()
-            torch.cuda.synchronize()
-            self.graph = self._capture()
-            self.init(self.b)
+            # warm-up outside capture (first-call attribute setup), then reset;
+            # KernelCounters: the warm-up and the re-init are not counted, one
+            # captured chunk is recorded and added per executed iteration
+            with COUNTERS.recording():
+                self._iteration()
+                torch.cuda.synchronize()
+            with COUNTERS.recording() as rec:
+                self.graph = self._capture()
+            self._iter_counts = (rec, self.chunk)
+            with COUNTERS.recording():
+                self.init(self.b)
         stt = read_state(self.st)
         while not stt.done:
             if self.use_graph:
                 self.graph.replay()
             else:
-                for _ in range(self.chunk):
-                    self._iteration()
+                with COUNTERS.recording() as rec:
+                    for _ in range(self.chunk):
+                        self._iteration()
+                self._iter_counts = (rec, self.chunk)
             stt = read_state(self.st)
         return stt
 
@@ -615,5 +636,7 @@ class MultigridPCG:
         if stt.breakdown:
             raise BreakdownError(f"p^T A p <= 0 at iteration {stt.iter}")
         it = int(stt.iter)
+        from .solvers import _count_iterations
+        _count_iterations(self, it)
         hist = self.hist[:it + 1].cpu().numpy().tolist()
         return PCGResult(self.x.view_as(b), it, hist, bool(stt.converged))

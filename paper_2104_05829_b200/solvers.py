@@ -29,7 +29,7 @@ from .gather_scatter import _halo_exchange, _halo_finish, _halo_start, _local, g
 from .kernels import COUNTERS, bk5_flops, extract_diagonal
 
 __all__ = ["pcg", "PCGResult", "BreakdownError", "PoissonOperator", "JacobiPreconditioner",
-           "FusedPCG", "inverse_multiplicity", "HelmholtzVectorSolver"]
+           "FusedPCG", "FusedPCG3", "inverse_multiplicity", "HelmholtzVectorSolver"]
 
 PCGResult = namedtuple("PCGResult", "x iterations residual_history converged")
 
@@ -235,8 +235,14 @@ class JacobiPreconditioner:
         mask = m.mask.to(d.dtype)
         self.invD = (mask / d).reshape(-1).contiguous()
 
-    def __call__(self, r):
-        return self.invD.view_as(r) * r
+    def __call__(self, r, out=None):
+        import torch
+        if r.numel() != self.invD.numel():
+            raise ContractError("contract error: field length mismatch")
+        z = torch.empty_like(r) if out is None else out
+        check(lib().nk_pointwise(r.numel(), ptr(self.invD), ptr(r), ptr(z), 1.0, None,
+                                 stream_ptr()), "pointwise")
+        return z
 
 
 # orders whose fused BP5 step stays one kernel (N = 7: the TMA pipeline,
@@ -366,6 +372,7 @@ class FusedPCG:
         check(L.nk_bk5(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p), ptr(self.w),
                        op.lam0, ptr(m.B) if op.lam1 else None, op.lam1, 1, self.n, ptr(m.mask),
                        None, 0, ptr(self.st), ptr(self.part_bk5), 0, nb, s), "bk5")
+        COUNTERS.add("stiffness", bk5_flops(m.N, m.E, 1), 7 * self.n)
 
     def _capture(self):
         import torch
@@ -378,7 +385,12 @@ class FusedPCG:
     def profile_iteration(self, reps=20):
         """In-situ device time (ms) of each kernel group of one iteration,
         CUDA events between launches on the current stream (eager, no graph;
-        L2 state as in a real solve).  Returns {name: ms}."""
+        L2 state as in a real solve).  Returns {name: ms}.  Not counted in
+        KernelCounters (measurement replays)."""
+        with COUNTERS.recording():
+            return self._profile_iteration(reps)
+
+    def _profile_iteration(self, reps):
         import torch
         L, s = lib(), stream_ptr()
         op, g = self.op, self.op.gs
@@ -444,8 +456,11 @@ class FusedPCG:
         import torch
         if self.use_graph and self.graph is None:
             # capture while done == 1 would still record the kernels; capture
-            # is independent of the state values.
-            self._capture()
+            # is independent of the state values.  The counters of one
+            # captured chunk are kept and added per executed iteration.
+            with COUNTERS.recording() as rec:
+                self._capture()
+            self._iter_counts = (rec, self.chunk)
         done_h = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         off = CGState.done.offset
         done_dev = self.st[off:off + 4].view(torch.int32)
@@ -453,8 +468,10 @@ class FusedPCG:
             if self.use_graph:
                 self.graph.replay()
             else:
-                for _ in range(self.chunk):
-                    self._iteration()
+                with COUNTERS.recording() as rec:
+                    for _ in range(self.chunk):
+                        self._iteration()
+                self._iter_counts = (rec, self.chunk)
             done_h.copy_(done_dev, non_blocking=True)
             torch.cuda.current_stream().synchronize()
             if int(done_h[0]):
@@ -473,8 +490,18 @@ class FusedPCG:
         if stt.breakdown:
             raise BreakdownError(f"p^T A p <= 0 at iteration {stt.iter}")
         it = int(stt.iter)
+        _count_iterations(self, it)
         hist = self.hist[:it + 1].cpu().numpy().tolist()
         return PCGResult(self.x.view_as(b), it, hist, bool(stt.converged))
+
+
+def _count_iterations(solver, it):
+    """KernelCounters for a graph-captured / chunked solve: the counts of one
+    recorded chunk, scaled to the iterations that ran (exact: every
+    iteration issues the same launches)."""
+    ic = getattr(solver, "_iter_counts", None)
+    if ic is not None:
+        COUNTERS.add_scaled(ic[0], it, ic[1])
 
 
 def pcg(apply_A, apply_M, b, tol=1e-8, max_iter=1000, flexible=False, weights=None, x0=None,
@@ -566,6 +593,194 @@ def _pcg_generic(apply_A, apply_M, b, tol, max_iter, flexible, weights, x0, host
     return res
 
 
+class FusedPCG3:
+    """Lockstep batched Jacobi-PCG for three right-hand sides of ONE operator
+    (the vector Helmholtz solve, configs[4]; "geometric
+    factors ... reused across each velocity component").
+
+    Three independent CG states advance together, one launch per stage for
+    all three components (4 kernels per iteration for three solves):
+      nk_cg_xpstep_batch   per-component stop test, deferred x update,
+                           Jacobi p update (gridDim.y = component);
+      nk_bk5_batch         w_c = mask A p_c with p_c . A p_c per component --
+                           the seq3 kernel reads G from HBM ONCE for the
+                           three components (orders where the measured table
+                           picks it; three scalar launches elsewhere);
+      gs sub-plan          edge / vertex segments, ncomp = 3;
+      nk_cg_update_gs_batch  face pairs folded in, r_c, rr_c, rz_c, zAp_c.
+    Each component keeps its own scalars, iteration count, residual history
+    and convergence; a converged component's launches are no-ops (its BK5
+    part is skipped inside the kernel).  The iterates of component c are
+    those of a scalar FusedPCG solve of b_c up to the BK5 kernel's rounding
+    (same algorithm, same reductions).  One rank (several ranks: solve the
+    components one by one with FusedPCG)."""
+
+    NC = 3
+
+    def __init__(self, op, prec, tol=1e-6, max_iter=1000, flexible=False, chunk=16,
+                 use_graph=True):
+        import torch
+        from .gather_scatter import point_codes
+        if op.gs.comm is not None and op.gs.comm.size > 1:
+            raise ContractError("FusedPCG3 runs on one rank")
+        if op.ncomp != 1:
+            raise ContractError("FusedPCG3 takes the scalar operator (one per component)")
+        self.op, self.prec = op, prec
+        self.tol, self.max_iter, self.flexible = float(tol), int(max_iter), bool(flexible)
+        self.chunk = max(1, int(chunk))
+        self.use_graph = bool(use_graph)
+        m = op.mesh
+        dev = m.device
+        n = self.n = op.n
+        L = lib()
+        f = lambda: torch.zeros(self.NC * n, dtype=torch.float64, device=dev)
+        self.x, self.r, self.p, self.w = f(), f(), f(), f()
+        self.st = torch.zeros(self.NC * CG_STATE_BYTES, dtype=torch.uint8, device=dev)
+        self.pstride = int(L.nk_bk5_batch_blocks(m.N, m.E)) + 2
+        self.part_bk5 = torch.zeros(self.NC * self.pstride, dtype=torch.float64, device=dev)
+        self.cg_plen = int(L.nk_cg_partials_len(n))
+        self.part_cg = torch.zeros(self.NC * self.cg_plen, dtype=torch.float64, device=dev)
+        self.hstride = self.max_iter + 2
+        self.hist = torch.zeros(self.NC * self.hstride, dtype=torch.float64, device=dev)
+        self.invD = prec.invD
+        self.codes = point_codes(op.gs)
+        if self.codes is None:
+            raise ContractError("FusedPCG3 needs n < 2^31 local points")
+        self.graph = None
+        self.variant = int(L.nk_bk5_batch_variant(m.N))
+        self.launches_per_iter = 4 if self.variant == 6 else 6
+
+    def _sti(self, c):
+        return self.st.data_ptr() + c * CG_STATE_BYTES
+
+    def _iteration(self):
+        L, s = lib(), stream_ptr()
+        op, m = self.op, self.op.mesh
+        n = self.n
+        check(L.nk_cg_xpstep_batch(n, self.NC, n, ptr(self.x), ptr(self.r), ptr(self.p),
+                                   ptr(self.invD), ptr(self.st), ptr(self.hist), self.hstride, s),
+              "cg_xpstep_batch")
+        nb = self.pstride - 2
+        check(L.nk_bk5_batch(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p), ptr(self.w),
+                             op.lam0, ptr(m.B) if op.lam1 else None, op.lam1, self.NC, n,
+                             ptr(m.mask), None, 0, ptr(self.st), ptr(self.part_bk5), self.pstride,
+                             0, nb, s), "bk5_batch")
+        COUNTERS.add("stiffness", bk5_flops(m.N, m.E, self.NC), 7 * n * self.NC)
+        self.codes[1].run(self.w, "+", self.NC, n)                     # edges, vertices
+        check(L.nk_cg_update_gs_batch(n, self.NC, n, ptr(self.r), ptr(self.w), ptr(self.invD),
+                                      ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
+              "cg_update_gs_batch")
+
+    def profile_iteration(self, b3, reps=10):
+        """In-situ device time (ms) of each stage of one batched iteration
+        (CUDA events between launches, eager; state restored between reps):
+        {'xpstep', 'bk5', 'gs_nonpair', 'update_gs'}."""
+        import torch
+        L, s = lib(), stream_ptr()
+        op, m = self.op, self.op.mesh
+        n = self.n
+        names = ("xpstep", "bk5", "gs_nonpair", "update_gs")
+        acc = dict.fromkeys(names, 0.0)
+        with COUNTERS.recording():
+            self.init(b3.reshape(-1).contiguous())
+            for _ in range(2):
+                self._iteration()
+            save = [t.clone() for t in (self.st, self.x, self.r, self.p)]
+            for _ in range(reps):
+                for t, v in zip((self.st, self.x, self.r, self.p), save):
+                    t.copy_(v)
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                ev[0].record()
+                check(L.nk_cg_xpstep_batch(n, self.NC, n, ptr(self.x), ptr(self.r), ptr(self.p),
+                                           ptr(self.invD), ptr(self.st), ptr(self.hist),
+                                           self.hstride, s), "xpstep")
+                ev[1].record()
+                check(L.nk_bk5_batch(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p),
+                                     ptr(self.w), op.lam0, ptr(m.B) if op.lam1 else None,
+                                     op.lam1, self.NC, n, ptr(m.mask), None, 0, ptr(self.st),
+                                     ptr(self.part_bk5), self.pstride, 0, self.pstride - 2, s),
+                      "bk5_batch")
+                ev[2].record()
+                self.codes[1].run(self.w, "+", self.NC, n)
+                ev[3].record()
+                check(L.nk_cg_update_gs_batch(n, self.NC, n, ptr(self.r), ptr(self.w),
+                                              ptr(self.invD), ptr(self.codes[0]), ptr(self.st),
+                                              ptr(self.part_cg), s), "update")
+                ev[4].record()
+                torch.cuda.synchronize()
+                for q, nm in enumerate(names):
+                    acc[nm] += ev[q].elapsed_time(ev[q + 1])
+        return {k: v / reps for k, v in acc.items()}
+
+    def init(self, b3):
+        L, s = lib(), stream_ptr()
+        n = self.n
+        wt = self.op.weights
+        for c in range(self.NC):
+            o = c * n
+            check(L.nk_cg_init(n, ptr(b3[o:o + n]), ptr(self.x[o:o + n]), ptr(self.r[o:o + n]),
+                               ptr(self.p[o:o + n]), ptr(self.invD), ptr(wt), self._sti(c),
+                               ptr(self.part_cg), self.tol, self.max_iter, int(self.flexible), s),
+                  "cg_init")
+            check(L.nk_cg_init_finalize(self._sti(c), ptr(self.hist[c * self.hstride:]), s),
+                  "cg_init_finalize")
+
+    def _done(self):
+        import torch
+        off = CGState.done.offset
+        v = self.st.view(self.NC, CG_STATE_BYTES)[:, off:off + 4].contiguous()
+        return bool(torch.all(v.view(torch.int32) != 0))
+
+    def run(self):
+        import torch
+        if self.use_graph and self.graph is None:
+            with COUNTERS.recording() as rec:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for _ in range(self.chunk):
+                        self._iteration()
+                self.graph = g
+            self._per_iter = (rec, self.chunk)
+        while not self._done():
+            if self.use_graph:
+                self.graph.replay()
+            else:
+                with COUNTERS.recording() as rec:
+                    for _ in range(self.chunk):
+                        self._iteration()
+                self._per_iter = (rec, self.chunk)
+        raw = self.st.cpu().numpy().tobytes()
+        return [CGState.from_buffer_copy(raw[c * CG_STATE_BYTES:(c + 1) * CG_STATE_BYTES])
+                for c in range(self.NC)]
+
+    def solve(self, b3):
+        """b3: 3 component-major CUDA float64 fields (assembled, masked), any
+        shape with 3 * n entries.  Returns (x3 view shaped like b3, [PCGResult
+        per component]); x3 is the solver's buffer (overwritten next solve)."""
+        import torch
+        if not isinstance(b3, torch.Tensor) or not b3.is_cuda or b3.dtype != torch.float64 \
+                or b3.numel() != self.NC * self.n:
+            raise ContractError("contract error: rhs must be 3 x n CUDA float64")
+        self.init(b3.reshape(-1).contiguous())
+        sts = self.run()
+        results = []
+        x3 = self.x.view_as(b3)
+        for c, stt in enumerate(sts):
+            if stt.breakdown:
+                raise BreakdownError(f"component {c}: p^T A p <= 0 at iteration {stt.iter}")
+            it = int(stt.iter)
+            hist = self.hist[c * self.hstride:c * self.hstride + it + 1].cpu().numpy().tolist()
+            results.append(PCGResult(x3[c], it, hist, bool(stt.converged)))
+        # counters: one stiffness application per component iteration
+        rec, chunk = self._per_iter
+        per_comp = {k: v // (chunk * self.NC) for k, v in rec.flops.items()}
+        refs = {k: v // (chunk * self.NC) for k, v in rec.memory_refs.items()}
+        tot = sum(r.iterations for r in results)
+        for k in per_comp:
+            COUNTERS.add(k, per_comp[k] * tot, refs[k] * tot)
+        return x3, results
+
+
 class HelmholtzVectorSolver:
     """Viscous substep solve:
     per-component Jacobi-PCG on H = lam0 A + lam1 B, e.g. lam0 = 1/Re,
@@ -576,33 +791,52 @@ class HelmholtzVectorSolver:
     ``apply(u3)`` is the batched operator (G read once for all components)."""
 
     def __init__(self, mesh, lam0, lam1, gs=None, comm=None, tol=1e-6, max_iter=1000,
-                 chunk=16):
+                 chunk=16, batched=None):
         self.op = PoissonOperator(mesh, gs=gs, lam0=lam0, lam1=lam1, comm=comm)
         self.jac = JacobiPreconditioner(self.op)
-        self.solver = FusedPCG(self.op, self.jac, tol=tol, max_iter=max_iter, chunk=chunk)
+        self.tol, self.max_iter, self.chunk = tol, max_iter, chunk
+        multi = self.op.gs.comm is not None and self.op.gs.comm.size > 1
+        # batched (FusedPCG3, lockstep, G once per iteration for the three
+        # components): one rank; several ranks solve the components in turn
+        self.batched = (not multi) if batched is None else bool(batched)
+        self._solver = None
         self.mesh = mesh
+
+    @property
+    def solver(self):
+        if self._solver is None:
+            cls = FusedPCG3 if self.batched else FusedPCG
+            self._solver = cls(self.op, self.jac, tol=self.tol, max_iter=self.max_iter,
+                               chunk=self.chunk)
+        return self._solver
 
     def apply(self, u3, out=None):
         """w_c = mask * QQ^T (lam0 A_L + lam1 B) u_c for c = 0, 1, 2."""
         import torch
         from .gather_scatter import _local
-        from .kernels import apply_helmholtz_local
+        from .kernels import _as_device, _bk5
         m = self.mesh
-        w = apply_helmholtz_local(u3, m, self.op.lam0, self.op.lam1, ncomp=3, out=out)
+        t, host = _as_device(u3, m, 3)
+        # the Dirichlet mask is fused into the BK5 epilogue: it is continuous
+        # (equal on every copy of an id), so mask QQ^T w = QQ^T (mask w)
+        w = _bk5(t, m, self.op.lam0, self.op.lam1, 3, out=out, mask=True)
         g = self.op.gs
         if g.comm is not None and g.comm.size > 1:
             for c in range(3):
                 gs_op(g, w.view(3, -1)[c])
         else:
             _local(g, w, "+", 3)
-        w.view(3, -1).mul_(m.mask.reshape(1, -1).to(w.dtype))
-        return w
+        return w.cpu().numpy().reshape(np.shape(u3)) if host else w
 
     def solve(self, b3):
         """b3: (3, E, nq, nq, nq) CUDA float64 (assembled, masked).  Returns
         (x3, [PCGResult per component])."""
         import torch
         x3 = torch.empty_like(b3)
+        if self.batched:
+            xs, results = self.solver.solve(b3)
+            x3.copy_(xs)
+            return x3, [r._replace(x=x3[c]) for c, r in enumerate(results)]
         results = []
         for c in range(3):
             r = self.solver.solve(b3[c].contiguous())

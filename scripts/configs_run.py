@@ -151,6 +151,17 @@ def config4(out):
     b3 *= m.mask.reshape(1, -1).to(torch.float64)
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
+    # sequential scalar solves (FusedPCG per component) for comparison
+    hq = nk.HelmholtzVectorSolver(m, lam0, lam1, gs=hs.op.gs, tol=1e-6, max_iter=2000, chunk=16,
+                                  batched=False)
+    hq.solve(b3.reshape((3,) + m.field_shape()))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    xq, rq = hq.solve(b3.reshape((3,) + m.field_shape()))
+    torch.cuda.synchronize()
+    t_seq = time.perf_counter() - t0
+    del hq
+    torch.cuda.empty_cache()
     hs.solve(b3[:, :].reshape((3,) + m.field_shape()))      # warm + capture
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -158,6 +169,9 @@ def config4(out):
     torch.cuda.synchronize()
     t = time.perf_counter() - t0
     it = [r.iterations for r in res]
+    same = bool(torch.equal(xq, x3))
+    del xq
+    prof = hs.solver.profile_iteration(b3) if hasattr(hs.solver, "profile_iteration") else None
     dof = m.E * N ** 3
     # batched operator throughput (G read once for 3 components)
     u3 = torch.randn((3, n), dtype=torch.float64, device="cuda")
@@ -173,6 +187,11 @@ def config4(out):
     ms = a.elapsed_time(bb) / 10
     out({"config": 4, "E": m.E, "N": N, "components": 3, "local_points_per_comp": n,
          "iterations": it, "converged": [r.converged for r in res], "solve_s": round(t, 4),
+         "solver": type(hs.solver).__name__, "sequential_solve_s": round(t_seq, 4),
+         "sequential_iterations": [r.iterations for r in rq],
+         "batched_bitwise_equal_sequential": same,
+         "ms_per_iteration_3comp": round(t / max(it) * 1e3, 4),
+         "breakdown_ms_3comp": None if prof is None else {k: round(v, 4) for k, v in prof.items()},
          "gdof_iter_per_s": round(dof * sum(it) / t / 1e9, 3), "setup_s": round(setup, 2),
          "batched_apply_ms": round(ms, 4),
          "batched_apply_gdofs_3comp": round(3 * dof / ms / 1e6, 2), "gpus": 1,
