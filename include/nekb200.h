@@ -186,6 +186,18 @@ int nk_bk5_set_variant(int variant);
  * resident CTAs ahead, 0 = off). */
 int nk_bk5_tune(int cfg, int pf_dist);
 
+/* process-wide knobs; returns the previous value, or -1 for an unknown knob.
+ *   NK_KNOB_PDL: 1 = launch the PCG-iteration kernels (fused / split BK5
+ *     step, gs classes, CG updates) with programmatic dependent launch: each
+ *     kernel is scheduled while its predecessor drains, runs its static-
+ *     operand prologue (G bulk copies, plan indices, gs codes), then waits
+ *     for the predecessor's results (griddepcontrol.wait); 0 = plain launches.
+ *   NK_KNOB_CG_UPDATE: nk_cg_update_gs 16-B kernel -- k > 0 = each block
+ *     bulk-prefetches (cp.async.bulk.prefetch.L2) its r / w / invD / code
+ *     segment k grid-stride trips ahead; 0 = no prefetch.  Bit-identical. */
+enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_COUNT = 2 };
+int nk_set_knob(int knob, int value);
+
 /* Fused BP5 operator step (pcg iteration k = st->iter):
  *   k > 0: stop if st->rr <= st->thresh2 or k >= max_iter (sets done,
  *          converged, hist[k]); x += alpha_{k-1} p (deferred x update);
@@ -358,6 +370,19 @@ int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
 int nk_cg_update_gs_batch(int64_t n, int ncomp, int64_t cstride, double* r, const double* w,
                           const double* invD, const int32_t* code, nk_cg_state* st,
                           double* partials, nk_stream_t stream);
+/* nk_cg_update_gs_batch with gathered segments: a code <= -NK_GS_SEG_BASE
+ * marks a point of a rank-private segment of M >= 3 members listed at
+ * segtab[k] = M, segtab[k+1..k+M] = its members in canonical (ascending
+ * local index) order, k = -code - NK_GS_SEG_BASE; the point's assembled
+ * value is the canonical fold of the members' w, computed in place -- so no
+ * gs pass over edges / vertices precedes the update (bit-identical to one).
+ * Codes -2 .. -(NK_GS_SEG_BASE-1) keep their meaning (-M: assembled before
+ * the update, e.g. halo ids).  segtab NULL = nk_cg_update_gs_batch.  Needs
+ * 16-byte aligned r / w / invD and 8-byte aligned code when segtab != NULL. */
+#define NK_GS_SEG_BASE 65536
+int nk_cg_update_gs_seg(int64_t n, int ncomp, int64_t cstride, double* r, const double* w,
+                        const double* invD, const int32_t* code, const int32_t* segtab,
+                        nk_cg_state* st, double* partials, nk_stream_t stream);
 int nk_cg_xpstep_batch(int64_t n, int ncomp, int64_t cstride, double* x, const double* r,
                        double* p, const double* invD, nk_cg_state* st, double* hist,
                        int64_t hstride, nk_stream_t stream);

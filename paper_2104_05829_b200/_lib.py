@@ -67,6 +67,7 @@ _SIGS = {
     "nk_bk5_pcg_blocks": ([_I32, _I64], _I64),
     "nk_bk5_set_variant": ([_I32], _I32),
     "nk_bk5_tune": ([_I32, _I32], _I32),
+    "nk_set_knob": ([_I32, _I32], _I32),
     "nk_local_diag": ([_I32, _I64, _P, _P, _D, _P, _D, _P, _P], _I32),
     "nk_gs_op": ([_I64, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
     "nk_gs_op_classes": ([_I32, _P, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),
@@ -109,6 +110,7 @@ _SIGS = {
     "nk_bk5_batch_variant": ([_I32], _I32),
     "nk_bk5_batch_blocks": ([_I32, _I64], _I64),
     "nk_cg_update_gs_batch": ([_I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "nk_cg_update_gs_seg": ([_I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "nk_cg_xpstep_batch": ([_I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _I64, _P], _I32),
     "nk_fdm": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),
     "nk_fdm32": ([_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _I32, _P, _P], _I32),

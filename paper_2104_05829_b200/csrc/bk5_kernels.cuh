@@ -43,20 +43,6 @@ struct Bk5Cfg {
   }
 };
 
-// Fire-and-forget bulk prefetch of [p, p+bytes) into L2 (TMA engine; SASS
-// UBLKPF).  Start rounded up and end rounded down to 16 B so the request never
-// leaves the allocation.
-__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
-  uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  uintptr_t lo = (a + 15) & ~uintptr_t(15);
-  uintptr_t hi = (a + bytes) & ~uintptr_t(15);
-  while (lo < hi) {
-    const uint32_t n = (uint32_t)((hi - lo) > (1u << 20) ? (1u << 20) : (hi - lo));
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(n) : "memory");
-    lo += n;
-  }
-}
-
 template <int NQ, int NC, int EPB, int MINB>
 __global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
 bk5_kslab(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> Dg,

@@ -103,13 +103,6 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   using L = PencilLayout<NQ>;
   constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, VOL = L::VOL;
   extern __shared__ double smem[];
-  if ((NC == 1 || CDOT) && st != nullptr) {
-    bool all_done = true;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) all_done = all_done && st[c].done;
-    if (all_done) return;
-  }
-
   const int t = threadIdx.x;
   const int le = t / NQ2;
   const int tt = t - le * NQ2;
@@ -122,19 +115,41 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   const int64_t slot = (int64_t)blockIdx.x * EPB + le;
   const bool active = slot < nlist;
   const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
+  // PDL prologue (static operands only; L2 prefetches cannot go stale):
+  // start this element's G (75% of its bytes) streaming into L2 now, so the
+  // G-phase loads after F1-F3 hit L2 instead of waiting on HBM.  The done
+  // read is a racy hint that skips it for the no-op iterations after
+  // convergence.
+  bool live = true;
+  if ((NC == 1 || CDOT) && st != nullptr) {
+    live = false;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      live = live || *reinterpret_cast<volatile const int*>(&st[c].done) == 0;
+  }
+  if (live && pfG && active && tt == 0)
+    prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
+  // optionally also the element one resident wave ahead
+  if (live && pf_ahead > 0 && tt == 0 && slot + pf_ahead < nlist) {
+    const int64_t ea = elist ? (int64_t)elist[slot + pf_ahead] : slot + pf_ahead;
+    prefetch_l2(G + ea * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
+  }
+  pdl_wait();
+  pdl_trigger();
+  if ((NC == 1 || CDOT) && st != nullptr) {
+    bool all_done = true;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) all_done = all_done && st[c].done;
+    if (all_done) return;
+  }
+  if (pf_ahead > 0 && tt == 0 && slot + pf_ahead < nlist) {
+    const int64_t ea = elist ? (int64_t)elist[slot + pf_ahead] : slot + pf_ahead;
+    prefetch_l2(u_ + ea * NQ3, NQ3 * (int64_t)sizeof(double));
+  }
   if (NC > 1 && active && tt == 0) {
 #pragma unroll
     for (int c = 1; c < NC; ++c)
       prefetch_l2(u_ + c * cstride + e * NQ3, NQ3 * (int64_t)sizeof(double));
-  }
-  // Start this element's G (75% of its bytes) streaming into L2 now, so the
-  // G-phase loads after F1-F3 hit L2 instead of waiting on HBM.
-  if (pfG && active && tt == 0) prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
-  // optionally also the element one resident wave ahead (u and G)
-  if (pf_ahead > 0 && tt == 0 && slot + pf_ahead < nlist) {
-    const int64_t ea = elist ? (int64_t)elist[slot + pf_ahead] : slot + pf_ahead;
-    prefetch_l2(G + ea * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
-    prefetch_l2(u_ + ea * NQ3, NQ3 * (int64_t)sizeof(double));
   }
 
   double dot = 0.0;
@@ -345,9 +360,9 @@ static int launch_pencil_k(int64_t nlist, const int32_t* elist, const double* Dh
   for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
   // pfG: 0 off, 1 own G into L2, 2 own G + the element one wave ahead
   const int64_t ahead = pfG >= 2 ? resident * EPB : 0;
-  bk5_pencil<NQ, EPB, MINB, NC, CDOT><<<(unsigned)nblk, C::THREADS, smem, s>>>(
-      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG,
-      ahead, cstride, pstride);
+  launch_ex(st != nullptr ? kPdlStep : 0, bk5_pencil<NQ, EPB, MINB, NC, CDOT>,
+            dim3((unsigned)nblk), dim3(C::THREADS), smem, s, nlist, elist, D, G, u, w, lam0, B,
+            lam1, mask, st, partials, part_base, reduce_count, pfG, ahead, cstride, pstride);
   return check_launch("bk5_pencil");
 }
 

@@ -33,6 +33,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// expected-transaction bytes without an arrival (the arrival comes later)
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n"
@@ -291,21 +302,12 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
                    double* __restrict__ x, const double* __restrict__ r,
                    const double* __restrict__ invD, nk_cg_state* st,
                    double* __restrict__ partials, int64_t part_base, int64_t reduce_count,
-                   double* __restrict__ hist) {
+                   double* __restrict__ hist, int pdl_flags) {
   static_assert(NQ % 2 == 0, "bulk copies need 16-byte multiples");
   using L = PencilLayout<NQ>;
   using C = TmaPcgCfg<NQ, MINB>;
   constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL, STAGE = C::STAGE;
   extern __shared__ __align__(128) double smem[];
-  if (st->done) return;
-  const int it = st->iter;
-  const bool conv = it > 0 && st->rr <= st->thresh2;
-  const bool stop = it > 0 && (conv || it >= st->max_iter);
-  const double alpha_prev = st->alpha;
-  const double rz = st->rz;
-  const double beta =
-      it == 0 ? 0.0 : (st->flexible ? (-alpha_prev * st->zap) / rz : st->rz_new / rz);
-
   double* stage0 = smem;
   double* U = smem + 2 * STAGE;
   double* Rr = U + VOL;
@@ -318,6 +320,51 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
   const int64_t stride = gridDim.x;
   constexpr uint32_t UB = NQ3 * sizeof(double), GB = 6 * NQ3 * sizeof(double);
   auto elem_of = [&](int64_t slot) -> int64_t { return elist ? (int64_t)elist[slot] : slot; };
+
+  // PDL prologue: G (static) of this CTA's first two elements starts moving
+  // while the predecessor kernel drains.  The stage's mbarrier gets the G
+  // bytes as expected transactions but no arrival, so its phase cannot
+  // complete before the p copy (or the drain below) arrives.  The done read
+  // is a racy hint only (done is monotonic within a graph-replayed chunk).
+  __shared__ int s_pre;
+  if (t == 0) {
+    s_pre = !(pdl_flags & kPdlNoPrologue) &&
+            *reinterpret_cast<volatile const int*>(&st->done) == 0;
+    const bool pre = s_pre;
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (pre) {
+      for (int s = 0; s < 2; ++s) {
+        const int64_t slot = blockIdx.x + s * stride;
+        if (slot < nlist) {
+          mbar_expect_tx_only(&bar[s], GB);
+          tma_load_1d(stage0 + s * STAGE + NQ3, G + elem_of(slot) * 6 * NQ3, GB, &bar[s]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const bool pre = s_pre;
+  pdl_wait();
+  if (!(pdl_flags & kPdlLateTrigger)) pdl_trigger();
+  const bool done = st->done != 0;
+  const int it = st->iter;
+  const bool conv = it > 0 && st->rr <= st->thresh2;
+  const bool stop = it > 0 && (conv || it >= st->max_iter);
+  if (pre && (done || stop)) {  // drain the prologue copies before smem is released
+    for (int s = 0; s < 2; ++s) {
+      if (blockIdx.x + s * stride < nlist) {
+        if (t == 0) mbar_arrive(&bar[s]);
+        mbar_wait(&bar[s], 0);
+      }
+    }
+  }
+  if (done) return;
+  const double alpha_prev = st->alpha;
+  const double rz = st->rz;
+  const double beta =
+      it == 0 ? 0.0 : (st->flexible ? (-alpha_prev * st->zap) / rz : st->rz_new / rz);
   double dot = 0.0;
 
   if (stop) {  // final deferred x update only
@@ -330,12 +377,13 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
       }
     }
   } else {
-    auto issue = [&](int64_t slot, int s) {
+    // g: whether the stage's G copy is already in flight (the prologue)
+    auto issue = [&](int64_t slot, int s, bool g) {
       const int64_t e = elem_of(slot);
       double* dst = stage0 + s * STAGE;
-      mbar_expect_tx(&bar[s], UB + GB);
+      mbar_expect_tx(&bar[s], g ? UB : UB + GB);
       tma_load_1d(dst, p + e * NQ3, UB, &bar[s]);
-      tma_load_1d(dst + NQ3, G + e * 6 * NQ3, GB, &bar[s]);
+      if (!g) tma_load_1d(dst + NQ3, G + e * 6 * NQ3, GB, &bar[s]);
       // r, invD, x and mask of the same element are read with plain
       // (coalesced) loads: start them towards L2 now, two elements ahead
       if (it > 0) {
@@ -346,14 +394,8 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
       if (mask != nullptr) prefetch_l2(mask + e * NQ3, NQ3);
     };
     if (t == 0) {
-      mbar_init(&bar[0], 1);
-      mbar_init(&bar[1], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (t == 0) {
-      if ((int64_t)blockIdx.x < nlist) issue(blockIdx.x, 0);
-      if ((int64_t)blockIdx.x + stride < nlist) issue(blockIdx.x + stride, 1);
+      if ((int64_t)blockIdx.x < nlist) issue(blockIdx.x, 0, pre);
+      if ((int64_t)blockIdx.x + stride < nlist) issue(blockIdx.x + stride, 1, pre);
     }
     int itl = 0;
     for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++itl) {
@@ -466,11 +508,12 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
         // the stage was written through the generic proxy (p_k); order those
         // writes before the async-proxy (TMA) refill of the same bytes
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(slot + 2 * stride, s);
+        issue(slot + 2 * stride, s, false);
       }
     }
   }
 
+  if (pdl_flags & kPdlLateTrigger) pdl_trigger();
   double vv[1] = {dot};
   block_sum<1>(vv, red);
   if (t == 0) partials[part_base + blockIdx.x] = vv[0];
@@ -523,9 +566,9 @@ static int launch_pencil_tma_pcg(int64_t nlist, const int32_t* elist, const doub
   }
   DParam<NQ> D;
   for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
-  bk5_pencil_tma_pcg<NQ, MINB><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
-      nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base,
-      reduce_count, hist);
+  launch_ex(kPdlStep, bk5_pencil_tma_pcg<NQ, MINB>, dim3((unsigned)grid), dim3(C::THREADS),
+            C::smem_bytes(), s, nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st,
+            partials, part_base, reduce_count, hist, knob(NK_KNOB_PDL));
   return check_launch("bk5_pencil_tma_pcg");
 }
 

@@ -224,18 +224,80 @@ cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
   }
 }
 
+// Gathered segment (code <= -NK_GS_SEG_BASE, nk_cg_update_gs_seg): the point
+// belongs to a rank-private segment of M >= 3 members listed at
+// tab[k] = M, tab[k+1 .. k+M] = members in canonical order, k = -code -
+// NK_GS_SEG_BASE.  Every member folds the whole segment itself, in member
+// order -- the canonical fold of gs_classes / gs_segments, so bit-identical
+// -- which removes the separate gs pass over edges and vertices.
+__device__ __forceinline__ double seg_fold(int32_t c, const double* __restrict__ w,
+                                           const int32_t* __restrict__ tab, int& M) {
+  const int64_t k = -(int64_t)c - NK_GS_SEG_BASE;
+  M = __ldg(tab + k);
+  double acc = w[__ldg(tab + k + 1)];
+  for (int j = 2; j <= M; ++j) acc += w[__ldg(tab + k + j)];
+  return acc;
+}
+
+// gs_point plus the gathered-segment code: pv = the partner value or the
+// segment fold, m = M for a gathered segment.
+__device__ __forceinline__ void gs_point_seg(int32_t c, double own, double pv, int m, double& ap,
+                                             double& wq, const double* rcp) {
+  if (c <= -NK_GS_SEG_BASE) {
+    ap = pv;
+    wq = m < 256 ? rcp[m] : 1.0 / (double)m;
+  } else {
+    gs_point(c, own, pv, ap, wq, rcp);
+  }
+}
+
 // nk_cg_update_gs, 16-B path: the cg_update_kernel<true, true, true> loop
 // restructured so that every load of a trip is issued before any is used
-// -- codes, r, w, invD of U pairs, then the pair partners -- instead of a
-// dependent chain per point; same per-thread point order and accumulation
-// as the generic form (bit-identical sums).  80 registers -> 3 CTAs/SM.
+// -- codes, r, w, invD of a pair, then the pair partners (or, SEG, the
+// gathered segments) -- instead of a dependent chain per point; same
+// per-thread point order and accumulation as the generic form
+// (bit-identical sums).
+// PDL prologue: the reciprocal table and the first trip's code / invD
+// (static operands) are loaded before pdl_wait().
+// pf > 0 (NK_KNOB_CG_UPDATE): the block's contiguous 256-pair segment of
+// trip k + pf (r, w, invD, code) is bulk-prefetched into L2 by thread 0
+// during trip k, so each trip's loads are L2 hits and HBM streams
+// continuously.
 // Batched like cg_update_kernel: gridDim.y components at cstride.
+template <bool SEG>
 __global__ void __launch_bounds__(kVecThreads, 4)
 cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restrict__ w,
                         const double* __restrict__ invD, const int32_t* __restrict__ code,
-                        nk_cg_state* st, double* __restrict__ partials, int64_t cstride = 0) {
+                        const int32_t* __restrict__ tab, nk_cg_state* st,
+                        double* __restrict__ partials, int64_t cstride, int pf) {
   __shared__ double red[3 * 32];
   __shared__ double rcp_tab[256];
+  for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
+  const bool hz = invD != nullptr;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t np = n >> 1;
+  // bulk L2 prefetch of trip k's block segment: static arrays, or r / w
+  auto pf_trip = [&](int64_t k, bool stat, bool dyn) {
+    const int64_t q0 = k * nthr + (int64_t)blockIdx.x * blockDim.x;
+    if (q0 >= np) return;
+    const int64_t cnt = np - q0 < (int64_t)blockDim.x ? np - q0 : (int64_t)blockDim.x;
+    if (stat) {
+      prefetch_l2(code + 2 * q0, cnt * 8);
+      if (hz) prefetch_l2(invD + 2 * q0, cnt * 16);
+    }
+    if (dyn) {
+      prefetch_l2(r + 2 * q0, cnt * 16);  // r, w: already offset to component blockIdx.y
+      prefetch_l2(w + 2 * q0, cnt * 16);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int k = 1; k <= pf; ++k) pf_trip(k, true, false);
+  int2 cv = gtid < np ? __ldg(reinterpret_cast<const int2*>(code) + gtid) : make_int2(-1, -1);
+  double2 dv = (gtid < np && hz) ? __ldg(reinterpret_cast<const double2*>(invD) + gtid)
+                                 : make_double2(0, 0);
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.y) {
     r += blockIdx.y * cstride;
     w += blockIdx.y * cstride;
@@ -243,7 +305,6 @@ cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restr
     partials += blockIdx.y * 3 * (int64_t)kVecMaxBlocks;
   }
   if (st->done) return;
-  for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
   __syncthreads();
   const double pAp = st->pAp;
   if (!(pAp > 0.0)) {
@@ -254,44 +315,40 @@ cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restr
     return;
   }
   const double alpha = st->rz / pAp;
-  const bool hz = invD != nullptr;
   UpdAcc acc;
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  const int64_t np = n >> 1;
-  constexpr int U = 1;
-  for (int64_t q0 = gtid; q0 < np; q0 += U * nthr) {
-    int2 cv[U];
-    double2 rv[U], av[U], dv[U], pv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t q = q0 + u * nthr;
-      const bool ok = q < np;
-      cv[u] = ok ? __ldg(reinterpret_cast<const int2*>(code) + q) : make_int2(-1, -1);
-      rv[u] = ok ? reinterpret_cast<const double2*>(r)[q] : make_double2(0, 0);
-      av[u] = ok ? __ldg(reinterpret_cast<const double2*>(w) + q) : make_double2(0, 0);
-      dv[u] = (ok && hz) ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
+  auto gather = [&](int32_t c, int& m) -> double {
+    m = 0;
+    if (c >= 0) return w[c];
+    if (SEG && c <= -NK_GS_SEG_BASE) return seg_fold(c, w, tab, m);
+    return 0.0;
+  };
+  if (threadIdx.x == 0)
+    for (int k = 1; k <= pf; ++k) pf_trip(k, false, true);
+  int64_t k = 0;
+  for (int64_t q = gtid; q < np; q += nthr, ++k) {
+    if (pf > 0 && threadIdx.x == 0) pf_trip(k + 1 + pf, true, true);
+    if (q != gtid) {
+      cv = __ldg(reinterpret_cast<const int2*>(code) + q);
+      dv = hz ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      pv[u] = make_double2(cv[u].x >= 0 ? w[cv[u].x] : 0.0, cv[u].y >= 0 ? w[cv[u].y] : 0.0);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t q = q0 + u * nthr;
-      if (q >= np) break;
-      double2 wv;
-      gs_point(cv[u].x, av[u].x, pv[u].x, av[u].x, wv.x, rcp_tab);
-      gs_point(cv[u].y, av[u].y, pv[u].y, av[u].y, wv.y, rcp_tab);
-      double xd = 0.0;
-      upd_point<true>(alpha, xd, rv[u].x, 0.0, av[u].x, dv[u].x, wv.x, hz, acc);
-      upd_point<true>(alpha, xd, rv[u].y, 0.0, av[u].y, dv[u].y, wv.y, hz, acc);
-      reinterpret_cast<double2*>(r)[q] = rv[u];
-    }
+    double2 rv = reinterpret_cast<const double2*>(r)[q];
+    double2 av = __ldg(reinterpret_cast<const double2*>(w) + q);
+    int mx, my;
+    const double px = gather(cv.x, mx), py = gather(cv.y, my);
+    double2 wv;
+    gs_point_seg(cv.x, av.x, px, mx, av.x, wv.x, rcp_tab);
+    gs_point_seg(cv.y, av.y, py, my, av.y, wv.y, rcp_tab);
+    double xd = 0.0;
+    upd_point<true>(alpha, xd, rv.x, 0.0, av.x, dv.x, wv.x, hz, acc);
+    upd_point<true>(alpha, xd, rv.y, 0.0, av.y, dv.y, wv.y, hz, acc);
+    reinterpret_cast<double2*>(r)[q] = rv;
   }
   if ((n & 1) && gtid == 0) {
     const int64_t t = n - 1;
     double xd = 0.0, at = 0.0, wq = 0.0;
-    gs_point(code[t], w[t], code[t] >= 0 ? w[code[t]] : 0.0, at, wq, rcp_tab);
+    int m;
+    const double pt = gather(code[t], m);
+    gs_point_seg(code[t], w[t], pt, m, at, wq, rcp_tab);
     upd_point<true>(alpha, xd, r[t], 0.0, at, hz ? invD[t] : 0.0, wq, hz, acc);
   }
   double v[3] = {acc.rr, acc.rz, acc.zap};
@@ -454,9 +511,10 @@ extern "C" int nk_cg_update(int64_t n, double* x, double* r, const double* p, co
   return check_launch("cg_update");
 }
 
-extern "C" int nk_cg_update_gs_batch(int64_t n, int ncomp, int64_t cstride, double* r,
-                                     const double* w, const double* invD, const int32_t* code,
-                                     nk_cg_state* st, double* partials, nk_stream_t stream) {
+extern "C" int nk_cg_update_gs_seg(int64_t n, int ncomp, int64_t cstride, double* r,
+                                   const double* w, const double* invD, const int32_t* code,
+                                   const int32_t* segtab, nk_cg_state* st, double* partials,
+                                   nk_stream_t stream) {
   if (n < 0 || ncomp < 1 || ncomp > 65535 || (ncomp > 1 && cstride < n) || !r || !w || !code ||
       !st || !partials) {
     set_error("cg_update_gs: invalid arguments");
@@ -464,12 +522,29 @@ extern "C" int nk_cg_update_gs_batch(int64_t n, int ncomp, int64_t cstride, doub
   }
   const dim3 g((unsigned)vec_grid(n), (unsigned)ncomp);
   cudaStream_t s = S(stream);
-  if (aligned16(r, w, invD) && ((uintptr_t)code & 7) == 0 && (cstride % 2 == 0 || ncomp == 1))
-    cg_update_gs_vec_kernel<<<g, kVecThreads, 0, s>>>(n, r, w, invD, code, st, partials, cstride);
-  else
+  if (aligned16(r, w, invD) && ((uintptr_t)code & 7) == 0 && (cstride % 2 == 0 || ncomp == 1)) {
+    const int pf = knob(NK_KNOB_CG_UPDATE);
+    if (segtab)
+      launch_ex(kPdlVec, cg_update_gs_vec_kernel<true>, g, dim3(kVecThreads), 0, s, n, r, w,
+                invD, code, segtab, st, partials, cstride, pf);
+    else
+      launch_ex(kPdlVec, cg_update_gs_vec_kernel<false>, g, dim3(kVecThreads), 0, s, n, r, w,
+                invD, code, segtab, st, partials, cstride, pf);
+  } else {
+    if (segtab) {
+      set_error("cg_update_gs_seg: gathered segments need 16-byte aligned r / w / invD");
+      return NK_ERR_INVALID;
+    }
     cg_update_kernel<false, true, true><<<g, kVecThreads, 0, s>>>(
         n, nullptr, r, nullptr, w, invD, nullptr, nullptr, st, partials, code, cstride);
+  }
   return check_launch("cg_update_gs");
+}
+
+extern "C" int nk_cg_update_gs_batch(int64_t n, int ncomp, int64_t cstride, double* r,
+                                     const double* w, const double* invD, const int32_t* code,
+                                     nk_cg_state* st, double* partials, nk_stream_t stream) {
+  return nk_cg_update_gs_seg(n, ncomp, cstride, r, w, invD, code, nullptr, st, partials, stream);
 }
 
 extern "C" int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
@@ -506,6 +581,8 @@ __global__ void __launch_bounds__(kVecThreads)
 cg_xpstep_kernel(int64_t n, double* __restrict__ x, const double* __restrict__ r,
                  double* __restrict__ p, const double* __restrict__ invD, nk_cg_state* st,
                  double* __restrict__ hist, int64_t cstride = 0, int64_t hstride = 0) {
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.y) {
     x += blockIdx.y * cstride;
     r += blockIdx.y * cstride;
@@ -578,11 +655,11 @@ extern "C" int nk_cg_xpstep_batch(int64_t n, int ncomp, int64_t cstride, double*
   }
   const dim3 g((unsigned)vec_grid(n), (unsigned)ncomp);
   if (aligned16(x, r, p, invD) && (cstride % 2 == 0 || ncomp == 1))
-    cg_xpstep_kernel<true><<<g, kVecThreads, 0, S(stream)>>>(n, x, r, p, invD, st, hist, cstride,
-                                                            hstride);
+    launch_ex(kPdlVec, cg_xpstep_kernel<true>, g, dim3(kVecThreads), 0, S(stream), n, x, r, p,
+              invD, st, hist, cstride, hstride);
   else
-    cg_xpstep_kernel<false><<<g, kVecThreads, 0, S(stream)>>>(n, x, r, p, invD, st, hist,
-                                                             cstride, hstride);
+    launch_ex(kPdlVec, cg_xpstep_kernel<false>, g, dim3(kVecThreads), 0, S(stream), n, x, r, p,
+              invD, st, hist, cstride, hstride);
   return check_launch("cg_xpstep");
 }
 

@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <string>
+#include <utility>
 
 #include "../../include/nekb200.h"
 
@@ -29,6 +30,138 @@ inline int check_launch(const char* what) {
   }
   return NK_OK;
 }
+
+// Process-wide tuning knobs (nk_set_knob, include/nekb200.h): NK_KNOB_*.
+int knob(int k);
+
+// Programmatic dependent launch (PDL).  A kernel launched by launch_ex with
+// the knob on may be scheduled while its predecessor in the stream is still
+// running; it executes its static-operand prologue (plan indices, G tiles,
+// gs codes -- data no kernel writes), then pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible.  Every kernel
+// launched through launch_ex calls pdl_wait() on every path before it reads
+// or writes anything a predecessor produces, so the relaxation is safe after
+// any predecessor (PDL-aware or not).  pdl_trigger() lets the successor
+// launch once every CTA of this grid has started.  Both are no-ops for a
+// normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// NK_KNOB_PDL bits: which kernel families launch with PDL, and where the
+// BP5 step kernel triggers its dependents.
+enum {
+  kPdlStep = 1,        // fused / split BK5 step (bk5_pencil_tma_pcg, ...)
+  kPdlGs = 2,          // gs_classes_kernel
+  kPdlVec = 4,         // CG vector kernels (cg_update_gs, cg_xpstep)
+  kPdlLateTrigger = 8, // step kernel: trigger after its element loop, not at entry
+  kPdlNoPrologue = 16  // step kernel: no G bulk copies before pdl_wait()
+};
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(int family, void (*kern)(KArgs...), dim3 grid, dim3 block,
+                             size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (knob(NK_KNOB_PDL) & family) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// Fire-and-forget bulk prefetch of [p, p+bytes) into L2 (TMA engine; SASS
+// UBLKPF).  Start rounded up and end rounded down to 16 B so the request never
+// leaves the allocation.
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  uintptr_t lo = (a + 15) & ~uintptr_t(15);
+  uintptr_t hi = (a + bytes) & ~uintptr_t(15);
+  while (lo < hi) {
+    const uint32_t n = (uint32_t)((hi - lo) > (1u << 20) ? (1u << 20) : (hi - lo));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(n) : "memory");
+    lo += n;
+  }
+}
+
+// L2 eviction-priority policies (createpolicy; PTX ISA 7.4+) and the
+// loads / stores / bulk copies that carry them (.L2::cache_hint).  The BP5
+// kernels mark data they stream once per iteration (G, p, x, codes, mask)
+// evict_first and the vectors reused across the iteration's kernels (r, w,
+// invD) evict_last, so the L2 keeps the reused set while G streams through
+// (NK_KNOB_L2).
+__device__ __forceinline__ uint64_t l2_policy(int prio) {  // 0 normal, 1 first, 2 last
+  uint64_t p;
+  if (prio == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (prio == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_hint(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld2_hint(const double* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ldg2_hint(const double* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int2 ldg2i_hint(const int32_t* a, uint64_t pol) {
+  int2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint8_t ldg_u8_hint(const uint8_t* a, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
+  return (uint8_t)v;
+}
+__device__ __forceinline__ void st_hint(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st2_hint(double* a, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x),
+               "d"(v.y), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_hint(const void* p, int64_t bytes, uint64_t pol) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  uintptr_t lo = (a + 15) & ~uintptr_t(15);
+  uintptr_t hi = (a + bytes) & ~uintptr_t(15);
+  while (lo < hi) {
+    const uint32_t n = (uint32_t)((hi - lo) > (1u << 20) ? (1u << 20) : (hi - lo));
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(lo),
+                 "r"(n), "l"(pol)
+                 : "memory");
+    lo += n;
+  }
+}
+// NK_KNOB_L2 bits
+enum { kL2StreamFirst = 1, kL2ReuseLast = 2, kL2InvDLast = 4 };
 
 // Threads per block for the streaming PCG kernels and the fixed number of
 // partial sums they produce.  The partial count does not depend on the GPU so

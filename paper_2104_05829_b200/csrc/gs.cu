@@ -99,20 +99,23 @@ template <int OP, typename V = double>
 __global__ void __launch_bounds__(256)
 gs_classes_kernel(const __grid_constant__ GsClasses C, V* __restrict__ w, int ncomp,
                   int64_t cs, const nk_cg_state* st) {
-  if (st != nullptr && st->done) return;
   const int64_t b = blockIdx.x;
   int c = 0;
   while (c + 1 < C.n && b >= C.bstart[c + 1]) ++c;
   const int M = C.M[c], Mp = C.Mp[c];
   const int64_t lanes = C.nseg[c] * Mp;
   const int64_t t0 = (b - C.bstart[c]) * (int64_t)(kGsU * blockDim.x) + threadIdx.x;
-  // whole warps stay active for the shuffles; out-of-range lanes carry -1
+  // whole warps stay active for the shuffles; out-of-range lanes carry -1.
+  // The member indices are plan data (static): loaded before pdl_wait().
   int idx[kGsU];
 #pragma unroll
   for (int u = 0; u < kGsU; ++u) {
     const int64_t t = t0 + (int64_t)u * blockDim.x;
     idx[u] = t < lanes ? __ldg(C.mem[c] + t) : -1;
   }
+  pdl_wait();
+  pdl_trigger();
+  if (st != nullptr && st->done) return;
   const int lane = threadIdx.x & 31;
   const int m = lane & (Mp - 1);
   for (int cc = 0; cc < ncomp; ++cc) {
@@ -213,11 +216,12 @@ static int gs_op_classes_t(int nclass, const int32_t* sizes, const int64_t* nseg
     return NK_ERR_INVALID;
   }
   cudaStream_t s = S(stream);
+  const dim3 g((unsigned)blocks), blk(256);
   switch (op) {
-    case NK_OP_ADD: gs_classes_kernel<NK_OP_ADD, V><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
-    case NK_OP_MUL: gs_classes_kernel<NK_OP_MUL, V><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
-    case NK_OP_MIN: gs_classes_kernel<NK_OP_MIN, V><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
-    case NK_OP_MAX: gs_classes_kernel<NK_OP_MAX, V><<<(unsigned)blocks, 256, 0, s>>>(C, w, ncomp, comp_stride, st); break;
+    case NK_OP_ADD: launch_ex(kPdlGs, gs_classes_kernel<NK_OP_ADD, V>, g, blk, 0, s, C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MUL: launch_ex(kPdlGs, gs_classes_kernel<NK_OP_MUL, V>, g, blk, 0, s, C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MIN: launch_ex(kPdlGs, gs_classes_kernel<NK_OP_MIN, V>, g, blk, 0, s, C, w, ncomp, comp_stride, st); break;
+    case NK_OP_MAX: launch_ex(kPdlGs, gs_classes_kernel<NK_OP_MAX, V>, g, blk, 0, s, C, w, ncomp, comp_stride, st); break;
     default: set_error("gs_op_classes: unknown op %d", op); return NK_ERR_INVALID;
   }
   return check_launch("gs_classes");

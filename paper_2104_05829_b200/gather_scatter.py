@@ -160,6 +160,47 @@ def point_codes(h):
     return res
 
 
+GS_SEG_BASE = 65536     # NK_GS_SEG_BASE (include/nekb200.h)
+
+
+def point_codes_gathered(h):
+    """Single-rank point codes with gathered segments (nk_cg_update_gs_seg):
+    as point_codes, except that a member of a segment of M >= 3 members
+    carries -(GS_SEG_BASE + k), k = the segment's offset in segtab =
+    concat over those segments of [M, members in canonical order], so the
+    update folds edges and vertices itself and no gs pass precedes it.
+    Returns (code, segtab) int32 device tensors; None on several ranks or
+    when n >= 2^31 or the table would overflow int32.  Cached on the
+    handle."""
+    import torch
+    if getattr(h, "_codes_g", False) is not False:
+        return h._codes_g
+    res = None
+    multi = h.comm is not None and h.comm.size > 1
+    if not multi and h.n < 2 ** 31:
+        perm = h.perm_h.astype(np.int64)
+        seg = h.seg_h.astype(np.int64)
+        sizes = np.diff(seg)
+        code = np.full(h.n, -1, dtype=np.int64)
+        two = seg[:-1][sizes == 2]
+        a, b = perm[two], perm[two + 1]
+        code[a], code[b] = b, a
+        sel = np.flatnonzero(sizes > 2)
+        cnt = sizes[sel]
+        off = np.r_[0, np.cumsum(cnt + 1)].astype(np.int64)   # entry of each segment
+        if off[-1] + GS_SEG_BASE < 2 ** 31:
+            tab = np.empty(off[-1], dtype=np.int64)
+            tab[off[:-1]] = cnt
+            pos = _dist._ranges(off[:-1] + 1, cnt)
+            mem = perm[_dist._ranges(seg[sel], cnt)] if len(sel) else np.zeros(0, np.int64)
+            tab[pos] = mem
+            code[mem] = -(GS_SEG_BASE + np.repeat(off[:-1], cnt))
+            res = (torch.as_tensor(code.astype(np.int32), device=h.device),
+                   torch.as_tensor(tab.astype(np.int32), device=h.device))
+    h._codes_g = res
+    return res
+
+
 def gs_setup(ids, comm=None, nq=None, device="cuda"):
     """Build the gs plan from global ids of this rank's local points
     (SPEC.md:192-200).  ids <= 0 and ids held once (over all ranks) are

@@ -38,6 +38,10 @@ class BreakdownError(RuntimeError):
     """p^T A p <= 0."""
 
 
+def _aligned16(*ts):
+    return all(t is None or t.data_ptr() % 16 == 0 for t in ts)
+
+
 def _state_tensor(device):
     import torch
     return torch.zeros(CG_STATE_BYTES, dtype=torch.uint8, device=device)
@@ -267,10 +271,18 @@ class FusedPCG:
     4 kernels per iteration.  None = auto: on at the orders where it measured
     faster than the fused kernel (every N except 7, whose fused step is the
     TMA pipeline; profiles/r1m_bp5_split.jsonl: 1.02-1.15x at N = 1, 2,
-    4..6, 8..15, a tie at N = 3)."""
+    4..6, 8..15, a tie at N = 3).
+
+    gather_segments (one rank, fused gs; off by default): the update also
+    folds the edge / vertex segments itself (nk_cg_update_gs_seg: every
+    member of an M >= 3 segment gathers the segment in canonical order) --
+    no gs pass, 2 kernels per iteration (3 split), bit-identical -- but
+    measured SLOWER: 0.151 vs 0.115 ms per iteration at N = 7, E = 20^3
+    (three dependent L2 round trips per warp trip for the ~16% edge /
+    vertex points; profiles/r2j_bp5_knobs.jsonl)."""
 
     def __init__(self, op, prec, tol=1e-8, max_iter=1000, flexible=False, chunk=16,
-                 use_graph=True, fuse_gs=True, split_step=None):
+                 use_graph=True, fuse_gs=True, split_step=None, gather_segments=False):
         import torch
         self.op, self.prec = op, prec
         self.tol, self.max_iter, self.flexible = float(tol), int(max_iter), bool(flexible)
@@ -308,12 +320,20 @@ class FusedPCG:
         if fuse_gs:
             from .gather_scatter import point_codes
             self.codes = point_codes(op.gs)
+        self.gcodes = None
+        if fuse_gs and self.comm is None and gather_segments:
+            from .gather_scatter import point_codes_gathered
+            self.gcodes = point_codes_gathered(op.gs)
+            if self.gcodes is not None and not _aligned16(self.r, self.w, self.invD):
+                self.gcodes = None
         self.launches_per_iter = 3    # bk5_pcg, gs (all | non-pair segments), update
         if split_step is None:
             split_step = op.mesh.N not in SPLIT_STEP_OFF
         self.split = bool(split_step) and self.codes is not None
         if self.split:
             self.launches_per_iter = 4    # xpstep, bk5 (+p.Ap), gs non-pair, update
+        if self.gcodes is not None:
+            self.launches_per_iter -= 1   # no gs pass
 
     def _allreduce(self, a, b):
         if self.comm is not None:
@@ -340,14 +360,12 @@ class FusedPCG:
                 self._allreduce(1, 2)                                    # pAp
             elif self.split:
                 self._split_head(L, s)
-                self.codes[1].run(self.w, "+", 1, self.n, self.st)      # edges, vertices
+                self._edge_vertex_gs()
             else:
                 self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
                                   self.part_bk5, self.hist, gs=False)
-                self.codes[1].run(self.w, "+", 1, self.n, self.st)      # edges, vertices
-            check(L.nk_cg_update_gs(self.n, ptr(self.r), ptr(self.w), ptr(self.invD),
-                                    ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
-                  "cg_update_gs")
+                self._edge_vertex_gs()
+            self._update_gs(L, s)
             self._allreduce(2, 5)                                        # rz_new rr zap
             return
         self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st, self.part_bk5,
@@ -357,6 +375,24 @@ class FusedPCG:
                              ptr(self.wt), ptr(self.mult), ptr(self.st), ptr(self.part_cg), s),
               "cg_update")
         self._allreduce(2, 5)                                            # rz_new rr zap
+
+    def _edge_vertex_gs(self):
+        """The gs pass over the >= 3-member segments, unless the update
+        gathers them itself."""
+        if self.gcodes is None:
+            self.codes[1].run(self.w, "+", 1, self.n, self.st)
+
+    def _update_gs(self, L, s):
+        """nk_cg_update_gs (face pairs folded in) or, with gathered segments,
+        nk_cg_update_gs_seg (every shared point assembled in the update)."""
+        if self.gcodes is not None:
+            check(L.nk_cg_update_gs_seg(self.n, 1, 0, ptr(self.r), ptr(self.w), ptr(self.invD),
+                                        ptr(self.gcodes[0]), ptr(self.gcodes[1]), ptr(self.st),
+                                        ptr(self.part_cg), s), "cg_update_gs_seg")
+        else:
+            check(L.nk_cg_update_gs(self.n, ptr(self.r), ptr(self.w), ptr(self.invD),
+                                    ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
+                  "cg_update_gs")
 
     def _split_head(self, L, s, mid_event=None):
         """nk_cg_xpstep (test, x and p updates) + nk_bk5 with the fused p.Ap:
@@ -419,11 +455,9 @@ class FusedPCG:
                                    ptr(self.hist), s), "bk5_pcg")
             ev[1].record()
             if fused:
-                self.codes[1].run(self.w, "+", 1, self.n, self.st)
+                self._edge_vertex_gs()
                 ev[2].record()
-                check(L.nk_cg_update_gs(self.n, ptr(self.r), ptr(self.w), ptr(self.invD),
-                                        ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
-                      "cg_update_gs")
+                self._update_gs(L, s)
                 ev[3].record()
             else:
                 _local(g, self.w, "+", 1, st=self.st)
@@ -438,6 +472,8 @@ class FusedPCG:
             for q, nm in enumerate(names):
                 acc[nm] += ev[q].elapsed_time(ev[q + 1])
         self.st.copy_(st_save)
+        if self.gcodes is not None:
+            acc.pop("gs_nonpair")    # folded into the update (gathered segments)
         return {k: v / reps for k, v in acc.items()}
 
     def init(self, b):
@@ -618,9 +654,9 @@ class FusedPCG3:
     NC = 3
 
     def __init__(self, op, prec, tol=1e-6, max_iter=1000, flexible=False, chunk=16,
-                 use_graph=True):
+                 use_graph=True, gather_segments=False):
         import torch
-        from .gather_scatter import point_codes
+        from .gather_scatter import point_codes, point_codes_gathered
         if op.gs.comm is not None and op.gs.comm.size > 1:
             raise ContractError("FusedPCG3 runs on one rank")
         if op.ncomp != 1:
@@ -646,9 +682,23 @@ class FusedPCG3:
         self.codes = point_codes(op.gs)
         if self.codes is None:
             raise ContractError("FusedPCG3 needs n < 2^31 local points")
+        # gathered segments: the update folds edges / vertices itself (no gs pass)
+        self.gcodes = point_codes_gathered(op.gs) if gather_segments else None
         self.graph = None
         self.variant = int(L.nk_bk5_batch_variant(m.N))
-        self.launches_per_iter = 4 if self.variant == 6 else 6
+        self.launches_per_iter = (4 if self.variant == 6 else 6) - (self.gcodes is not None)
+
+    def _update(self, L, s):
+        n = self.n
+        if self.gcodes is not None:
+            check(L.nk_cg_update_gs_seg(n, self.NC, n, ptr(self.r), ptr(self.w), ptr(self.invD),
+                                        ptr(self.gcodes[0]), ptr(self.gcodes[1]), ptr(self.st),
+                                        ptr(self.part_cg), s), "cg_update_gs_seg")
+            return
+        self.codes[1].run(self.w, "+", self.NC, n)                     # edges, vertices
+        check(L.nk_cg_update_gs_batch(n, self.NC, n, ptr(self.r), ptr(self.w), ptr(self.invD),
+                                      ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
+              "cg_update_gs_batch")
 
     def _sti(self, c):
         return self.st.data_ptr() + c * CG_STATE_BYTES
@@ -666,10 +716,7 @@ class FusedPCG3:
                              ptr(m.mask), None, 0, ptr(self.st), ptr(self.part_bk5), self.pstride,
                              0, nb, s), "bk5_batch")
         COUNTERS.add("stiffness", bk5_flops(m.N, m.E, self.NC), 7 * n * self.NC)
-        self.codes[1].run(self.w, "+", self.NC, n)                     # edges, vertices
-        check(L.nk_cg_update_gs_batch(n, self.NC, n, ptr(self.r), ptr(self.w), ptr(self.invD),
-                                      ptr(self.codes[0]), ptr(self.st), ptr(self.part_cg), s),
-              "cg_update_gs_batch")
+        self._update(L, s)
 
     def profile_iteration(self, b3, reps=10):
         """In-situ device time (ms) of each stage of one batched iteration
@@ -701,11 +748,15 @@ class FusedPCG3:
                                      ptr(self.part_bk5), self.pstride, 0, self.pstride - 2, s),
                       "bk5_batch")
                 ev[2].record()
-                self.codes[1].run(self.w, "+", self.NC, n)
+                if self.gcodes is None:
+                    self.codes[1].run(self.w, "+", self.NC, n)
                 ev[3].record()
-                check(L.nk_cg_update_gs_batch(n, self.NC, n, ptr(self.r), ptr(self.w),
-                                              ptr(self.invD), ptr(self.codes[0]), ptr(self.st),
-                                              ptr(self.part_cg), s), "update")
+                if self.gcodes is not None:
+                    self._update(L, s)
+                else:
+                    check(L.nk_cg_update_gs_batch(n, self.NC, n, ptr(self.r), ptr(self.w),
+                                                  ptr(self.invD), ptr(self.codes[0]),
+                                                  ptr(self.st), ptr(self.part_cg), s), "update")
                 ev[4].record()
                 torch.cuda.synchronize()
                 for q, nm in enumerate(names):

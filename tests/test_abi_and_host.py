@@ -56,6 +56,16 @@ def test_version_error_and_state_layout(L):
     assert _lib.CGState.done.offset == 68
 
 
+def test_knobs(L):
+    """nk_set_knob: returns the previous value, -1 for an unknown knob; the
+    defaults are the measured best (PDL on the BK5 step + CG vector
+    kernels = 5, one-trip L2 prefetch in the update = 1)."""
+    assert L.nk_set_knob(0, 5) == 5 and L.nk_set_knob(1, 1) == 1
+    old = L.nk_set_knob(0, 0)
+    assert L.nk_set_knob(0, old) == 0
+    assert L.nk_set_knob(2, 1) == -1 and L.nk_set_knob(-1, 0) == -1
+
+
 @pytest.mark.parametrize("counts,N,bc", [((3, 2, 2), 3, "dirichlet"), ((4, 4, 4), 7, "periodic"),
                                          ((2, 1, 1), 1, "neumann"), ((5, 3, 2), 2, "periodic")])
 def test_native_plan_builder_bit_exact(L, counts, N, bc):
@@ -108,6 +118,48 @@ def test_point_codes_assemble_like_gs(L, counts, N, bc):
     assert np.array_equal(wt, 1.0 / ogs.multiplicity(ids))
     assert int(sub.nseg) == int(np.sum(sizes > 2))
     assert point_codes(h) is h._codes                          # cached
+
+
+@pytest.mark.parametrize("counts,N,bc", [((3, 2, 2), 3, "dirichlet"), ((2, 3, 2), 2, "periodic"),
+                                          ((4, 1, 3), 4, "mixed")])
+def test_point_codes_gathered_assemble_like_gs(L, counts, N, bc):
+    """Gathered-segment codes (nk_cg_update_gs_seg): a host replay of the
+    kernel's decode -- pair partner, or the canonical fold of the segment
+    listed in segtab -- reproduces the oracle's full QQ^T bit for bit with
+    no gs pass, and the weights are 1/mult."""
+    import types
+    from paper_2104_05829_b200.gather_scatter import (GS_SEG_BASE, _local_plan,
+                                                      point_codes_gathered)
+    ids = om.build_box_mesh((1, 1, 1), counts, N, bc=bc).ids
+    perm, seg = _local_plan(ids)
+    h = types.SimpleNamespace(perm_h=perm, seg_h=seg, n=len(ids), comm=None, device="cpu")
+    code_t, tab_t = point_codes_gathered(h)
+    code, tab = code_t.numpy().astype(np.int64), tab_t.numpy()
+    w = np.random.default_rng(6).standard_normal(len(ids))
+    ap = np.empty_like(w)
+    wt = np.empty_like(w)
+    for q in range(len(w)):
+        c = code[q]
+        if c >= 0:
+            ap[q], wt[q] = w[q] + w[c], 0.5
+        elif c == -1:
+            ap[q], wt[q] = w[q], 1.0
+        else:
+            assert c <= -GS_SEG_BASE
+            k = -c - GS_SEG_BASE
+            M = tab[k]
+            mem = tab[k + 1:k + 1 + M]
+            assert q in mem and np.all(np.diff(mem) > 0)     # canonical member order
+            acc = w[mem[0]]
+            for j in range(1, M):
+                acc = acc + w[mem[j]]
+            ap[q], wt[q] = acc, 1.0 / M
+    assert np.array_equal(ap, ogs.gs_op(ids, w))
+    assert np.array_equal(wt, 1.0 / ogs.multiplicity(ids))
+    assert point_codes_gathered(h) is h._codes_g                  # cached
+    h2 = types.SimpleNamespace(perm_h=perm, seg_h=seg, n=len(ids),
+                               comm=types.SimpleNamespace(size=2), device="cpu")
+    assert point_codes_gathered(h2) is None                       # one rank only
 
 
 def test_product_basis_bitwise_reference(golden_basis):

@@ -287,6 +287,69 @@ def test_pcg_spec_examples():
         nk.pcg(lambda v: -v, lambda v: v, torch.ones(3, dtype=torch.float64, device="cuda"))
 
 
+@pytest.mark.parametrize("counts,N", [((4, 4, 4), 7), ((10, 10, 10), 7), ((3, 3, 3), 5),
+                                      ((3, 2, 3), 3)])
+def test_launch_knobs_bit_identical(counts, N):
+    """PDL (programmatic dependent launch with static-operand prologues) and
+    the update's L2 prefetch change scheduling only: solves with every knob
+    off and at the defaults are bit-identical, graph-captured included."""
+    from paper_2104_05829_b200._lib import lib
+    L = lib()
+    m, o = both_meshes(counts, N)
+    op = nk.PoissonOperator(m)
+    jac = nk.JacobiPreconditioner(op)
+    rng = np.random.default_rng(90 + N)
+    b = torch.as_tensor(o.mask.ravel() * ogs.gs_op(o.ids, rng.standard_normal(m.n_local)),
+                        device="cuda")
+    ra = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000).solve(b)
+    old = (L.nk_set_knob(0, 0), L.nk_set_knob(1, 0))
+    try:
+        rb = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000).solve(b)
+        L.nk_set_knob(0, 31)      # every PDL family, late trigger, no prologue
+        rc = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000).solve(b)
+    finally:
+        L.nk_set_knob(0, old[0])
+        L.nk_set_knob(1, old[1])
+    for r in (rb, rc):
+        assert r.iterations == ra.iterations and r.residual_history == ra.residual_history
+        assert torch.equal(r.x, ra.x)
+
+
+@pytest.mark.parametrize("counts,N,lam1,split", [((5, 4, 4), 1, 0.0, None),
+                                                 ((3, 3, 3), 2, 0.0, None),  # odd n
+                                                 ((3, 2, 3), 3, 0.5, None),
+                                                 ((4, 4, 4), 7, 0.0, False),
+                                                 ((4, 4, 4), 7, 0.0, True),
+                                                 ((10, 10, 10), 7, 0.0, False),  # ring reuse
+                                                 ((2, 3, 2), 8, 0.0, None),
+                                                 ((2, 2, 2), 12, 0.3, None)])
+def test_fused_pcg_gathered_segments(counts, N, lam1, split):
+    """gather_segments (nk_cg_update_gs_seg: every member of an edge /
+    vertex segment folds the segment in canonical order inside the update,
+    no gs pass) against the gs sub-plan + nk_cg_update_gs: bit-identical
+    solves (iterations, residual history, x), one launch fewer."""
+    m, o = both_meshes(counts, N)
+    op = nk.PoissonOperator(m, lam1=lam1)
+    jac = nk.JacobiPreconditioner(op)
+    rng = np.random.default_rng(70 + N)
+    b = torch.as_tensor(o.mask.ravel() * ogs.gs_op(o.ids, rng.standard_normal(m.n_local)),
+                        device="cuda")
+    sa = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000, split_step=split, gather_segments=True)
+    sb = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000, split_step=split)
+    assert sa.gcodes is not None and sb.gcodes is None
+    assert sa.launches_per_iter == sb.launches_per_iter - 1
+    ra, rb = sa.solve(b), sb.solve(b)
+    assert ra.converged and ra.iterations == rb.iterations
+    assert ra.residual_history == rb.residual_history
+    assert torch.equal(ra.x, rb.x)
+    if m.E <= 64 and lam1 == 0.0:
+        _, A, inv, wt = _oracle_problem(o)
+        ref = osol.pcg(A, lambda r: inv * r, b.cpu().numpy(), tol=1e-9, max_iter=3000,
+                       weights=wt)
+        assert abs(ra.iterations - ref.iterations) <= 1
+        assert np.max(np.abs(ra.x.cpu().numpy() - ref.x)) < 1e-7 * np.max(np.abs(ref.x))
+
+
 @pytest.mark.parametrize("counts,N,lam1", [((5, 4, 4), 1, 0.0), ((3, 3, 2), 2, 0.0),
                                            ((3, 3, 3), 2, 0.0),   # n = 729: odd tail
                                            ((3, 2, 3), 3, 0.5),
@@ -324,7 +387,9 @@ def test_fused_pcg_split_step(counts, N, lam1):
     Ax = torch.empty_like(b)
     op(rc.x.reshape(-1), out=Ax)
     assert float(torch.linalg.norm(Ax - b)) <= 2e-9 * float(torch.linalg.norm(b))
-    keys = ({"cg_xpstep", "bk5"} if sc.split else {"bk5_pcg"}) | {"gs_nonpair", "cg_update_gs"}
+    keys = ({"cg_xpstep", "bk5"} if sc.split else {"bk5_pcg"}) | {"cg_update_gs"}
+    if sc.gcodes is None:
+        keys |= {"gs_nonpair"}
     assert set(sc.profile_iteration(reps=2)) == keys
     assert len(keys) == sc.launches_per_iter
 
