@@ -194,9 +194,18 @@ int nk_bk5_tune(int cfg, int pf_dist);
  *     for the predecessor's results (griddepcontrol.wait); 0 = plain launches.
  *   NK_KNOB_CG_UPDATE: nk_cg_update_gs 16-B kernel -- k > 0 = each block
  *     bulk-prefetches (cp.async.bulk.prefetch.L2) its r / w / invD / code
- *     segment k grid-stride trips ahead; 0 = no prefetch.  Bit-identical. */
-enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_COUNT = 2 };
+ *     segment k grid-stride trips ahead; 0 = no prefetch.  Bit-identical.
+ *   NK_KNOB_L2: L2 eviction-priority hints in the BP5 step and update
+ *     kernels -- bit 1: data streamed once per iteration (G, p, x, codes,
+ *     mask) evict_first; bit 2: r and w (reused by the next kernel) evict_last;
+ *     bit 4: invD (read twice per iteration) evict_last; bit 8: reserve the
+ *     device's maximum persisting-L2 set-aside for the evict_last lines
+ *     (cudaLimitPersistingL2CacheSize; released when the bit is cleared).
+ *     Bit-identical. */
+enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_COUNT = 3 };
 int nk_set_knob(int knob, int value);
+/* the device's maximum persisting-L2 set-aside in bytes (-1: no device). */
+int64_t nk_l2_set_aside_max(void);
 
 /* Fused BP5 operator step (pcg iteration k = st->iter):
  *   k > 0: stop if st->rr <= st->thresh2 or k >= max_iter (sets done,

@@ -65,6 +65,15 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 template <int NQ, int MINB>
 struct TmaCfg {
   static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
@@ -302,7 +311,7 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
                    double* __restrict__ x, const double* __restrict__ r,
                    const double* __restrict__ invD, nk_cg_state* st,
                    double* __restrict__ partials, int64_t part_base, int64_t reduce_count,
-                   double* __restrict__ hist, int pdl_flags) {
+                   double* __restrict__ hist, int pdl_flags, int l2_flags) {
   static_assert(NQ % 2 == 0, "bulk copies need 16-byte multiples");
   using L = PencilLayout<NQ>;
   using C = TmaPcgCfg<NQ, MINB>;
@@ -320,6 +329,11 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
   const int64_t stride = gridDim.x;
   constexpr uint32_t UB = NQ3 * sizeof(double), GB = 6 * NQ3 * sizeof(double);
   auto elem_of = [&](int64_t slot) -> int64_t { return elist ? (int64_t)elist[slot] : slot; };
+  // L2 policies (NK_KNOB_L2): streamed once per iteration (G, p, x, mask)
+  // vs reused by the iteration's update kernel (r, w) and invD
+  const uint64_t pol_s = l2_policy(l2_flags & kL2StreamFirst ? 1 : 0);
+  const uint64_t pol_r = l2_policy(l2_flags & kL2ReuseLast ? 2 : 0);
+  const uint64_t pol_d = l2_policy(l2_flags & kL2InvDLast ? 2 : 0);
 
   // PDL prologue: G (static) of this CTA's first two elements starts moving
   // while the predecessor kernel drains.  The stage's mbarrier gets the G
@@ -339,7 +353,8 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
         const int64_t slot = blockIdx.x + s * stride;
         if (slot < nlist) {
           mbar_expect_tx_only(&bar[s], GB);
-          tma_load_1d(stage0 + s * STAGE + NQ3, G + elem_of(slot) * 6 * NQ3, GB, &bar[s]);
+          tma_load_1d_hint(stage0 + s * STAGE + NQ3, G + elem_of(slot) * 6 * NQ3, GB, &bar[s],
+                           pol_s);
         }
       }
     }
@@ -373,7 +388,7 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
 #pragma unroll
       for (int k = 0; k < NQ; ++k) {
         const int64_t q = e * NQ3 + k * NQ2 + t;
-        x[q] = fma(alpha_prev, p[q], x[q]);
+        st_hint(x + q, fma(alpha_prev, ld_hint(p + q, pol_s), ld_hint(x + q, pol_s)), pol_s);
       }
     }
   } else {
@@ -382,16 +397,16 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
       const int64_t e = elem_of(slot);
       double* dst = stage0 + s * STAGE;
       mbar_expect_tx(&bar[s], g ? UB : UB + GB);
-      tma_load_1d(dst, p + e * NQ3, UB, &bar[s]);
-      if (!g) tma_load_1d(dst + NQ3, G + e * 6 * NQ3, GB, &bar[s]);
+      tma_load_1d_hint(dst, p + e * NQ3, UB, &bar[s], pol_s);
+      if (!g) tma_load_1d_hint(dst + NQ3, G + e * 6 * NQ3, GB, &bar[s], pol_s);
       // r, invD, x and mask of the same element are read with plain
       // (coalesced) loads: start them towards L2 now, two elements ahead
       if (it > 0) {
-        prefetch_l2(r + e * NQ3, UB);
-        prefetch_l2(invD + e * NQ3, UB);
-        prefetch_l2(x + e * NQ3, UB);
+        prefetch_l2_hint(r + e * NQ3, UB, pol_r);
+        prefetch_l2_hint(invD + e * NQ3, UB, pol_d);
+        prefetch_l2_hint(x + e * NQ3, UB, pol_s);
       }
-      if (mask != nullptr) prefetch_l2(mask + e * NQ3, NQ3);
+      if (mask != nullptr) prefetch_l2_hint(mask + e * NQ3, NQ3, pol_s);
     };
     if (t == 0) {
       if ((int64_t)blockIdx.x < nlist) issue(blockIdx.x, 0, pre);
@@ -410,9 +425,9 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
 #pragma unroll
         for (int k = 0; k < NQ; ++k) {
           const int64_t q = e * NQ3 + k * NQ2 + t;
-          xv[k] = x[q];
-          rv[k] = __ldg(r + q);
-          dv[k] = __ldg(invD + q);
+          xv[k] = ld_hint(x + q, pol_s);
+          rv[k] = ldg_hint(r + q, pol_r);
+          dv[k] = ldg_hint(invD + q, pol_d);
         }
       }
       mbar_wait(&bar[s], (itl >> 1) & 1);
@@ -426,9 +441,9 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
           const int pp = k * NQ2 + t;
           double pv = su[pp];
           if (it > 0) {
-            x[e * NQ3 + pp] = fma(alpha_prev, pv, xv[k]);
+            st_hint(x + e * NQ3 + pp, fma(alpha_prev, pv, xv[k]), pol_s);
             pv = fma(beta, pv, dv[k] * rv[k]);
-            p[e * NQ3 + pp] = pv;
+            st_hint(p + e * NQ3 + pp, pv, pol_s);
             su[pp] = pv;
           }
           v[k] = pv;
@@ -494,14 +509,14 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
         for (int i = 0; i < NQ; ++i) {
           double vv = lam0 * (o[i] + U[L::idx(b, a, i)]);
           if (B != nullptr) vv = fma(lam1 * __ldg(B + off + i), prow[i], vv);
-          if (mask != nullptr) vv = mask[off + i] ? vv : 0.0;
+          if (mask != nullptr) vv = ldg_u8_hint(mask + off + i, pol_s) ? vv : 0.0;
           res[i] = vv;
           dot = fma(prow[i], vv, dot);
         }
         double* wr = w + off;
 #pragma unroll
         for (int i = 0; i < NQ; i += 2)
-          *reinterpret_cast<double2*>(wr + i) = make_double2(res[i], res[i + 1]);
+          st2_hint(wr + i, make_double2(res[i], res[i + 1]), pol_r);
       }
       __syncthreads();
       if (t == 0 && slot + 2 * stride < nlist) {
@@ -568,7 +583,7 @@ static int launch_pencil_tma_pcg(int64_t nlist, const int32_t* elist, const doub
   for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
   launch_ex(kPdlStep, bk5_pencil_tma_pcg<NQ, MINB>, dim3((unsigned)grid), dim3(C::THREADS),
             C::smem_bytes(), s, nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st,
-            partials, part_base, reduce_count, hist, knob(NK_KNOB_PDL));
+            partials, part_base, reduce_count, hist, knob(NK_KNOB_PDL), knob(NK_KNOB_L2));
   return check_launch("bk5_pencil_tma_pcg");
 }
 

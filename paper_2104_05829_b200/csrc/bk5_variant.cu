@@ -18,12 +18,35 @@ extern "C" int nk_bk5_set_variant(int v) {
 // BP5 N = 7, E = 20^3: 0.1175 -> 0.1152 ms per iteration; N = 3: 0.0378 ->
 // 0.0360): PDL for the BK5 step and the CG vector kernels, not for the gs
 // classes kernel (whose early-resident CTAs slow the step kernel they
-// follow, 0.117 -> 0.127 ms), and a one-trip-ahead L2 prefetch in the update.
-static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1};
+// follow, 0.117 -> 0.127 ms), and a one-trip-ahead L2 prefetch in the update;
+// L2 hints: streamed data evict_first + r / w evict_last (0.1136 -> 0.1101 ms,
+// profiles/r2l_bp5_knobs.jsonl; the persisting set-aside did not help, r2m).
+static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1,
+                                     nk::kL2StreamFirst | nk::kL2ReuseLast};
 
 namespace nk {
 int knob(int k) { return (k >= 0 && k < NK_KNOB_COUNT) ? g_knobs[k] : 0; }
+
+void l2_apply_set_aside() {
+  static int applied = 0;   // the device default: no set-aside
+  const int want = (g_knobs[NK_KNOB_L2] & kL2SetAside) ? 1 : 0;
+  if (want == applied) return;
+  int dev = 0, maxp = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want ? (size_t)maxp : 0);
+  cudaGetLastError();
+  applied = want;
+}
 }  // namespace nk
+
+extern "C" int64_t nk_l2_set_aside_max() {
+  int dev = 0, maxp = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess)
+    return -1;
+  return maxp;
+}
 
 extern "C" int nk_set_knob(int k, int value) {
   if (k < 0 || k >= NK_KNOB_COUNT) {
@@ -32,5 +55,6 @@ extern "C" int nk_set_knob(int k, int value) {
   }
   const int old = g_knobs[k];
   g_knobs[k] = value;
+  if (k == NK_KNOB_L2) nk::l2_apply_set_aside();   // a host call: never inside a capture
   return old;
 }

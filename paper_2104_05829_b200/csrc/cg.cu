@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(kVecThreads, 4)
 cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restrict__ w,
                         const double* __restrict__ invD, const int32_t* __restrict__ code,
                         const int32_t* __restrict__ tab, nk_cg_state* st,
-                        double* __restrict__ partials, int64_t cstride, int pf) {
+                        double* __restrict__ partials, int64_t cstride, int pf,
+                        int l2_flags) {
   __shared__ double red[3 * 32];
   __shared__ double rcp_tab[256];
   for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
@@ -277,25 +278,27 @@ cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restr
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t np = n >> 1;
+  const uint64_t pol_s = l2_policy(l2_flags & kL2StreamFirst ? 1 : 0);   // code
+  const uint64_t pol_r = l2_policy(l2_flags & kL2ReuseLast ? 2 : 0);     // r, w
+  const uint64_t pol_d = l2_policy(l2_flags & kL2InvDLast ? 2 : 0);      // invD
   // bulk L2 prefetch of trip k's block segment: static arrays, or r / w
   auto pf_trip = [&](int64_t k, bool stat, bool dyn) {
     const int64_t q0 = k * nthr + (int64_t)blockIdx.x * blockDim.x;
     if (q0 >= np) return;
     const int64_t cnt = np - q0 < (int64_t)blockDim.x ? np - q0 : (int64_t)blockDim.x;
     if (stat) {
-      prefetch_l2(code + 2 * q0, cnt * 8);
-      if (hz) prefetch_l2(invD + 2 * q0, cnt * 16);
+      prefetch_l2_hint(code + 2 * q0, cnt * 8, pol_s);
+      if (hz) prefetch_l2_hint(invD + 2 * q0, cnt * 16, pol_d);
     }
     if (dyn) {
-      prefetch_l2(r + 2 * q0, cnt * 16);  // r, w: already offset to component blockIdx.y
-      prefetch_l2(w + 2 * q0, cnt * 16);
+      prefetch_l2_hint(r + 2 * q0, cnt * 16, pol_r);  // r, w: offset to component blockIdx.y
+      prefetch_l2_hint(w + 2 * q0, cnt * 16, pol_r);
     }
   };
   if (threadIdx.x == 0)
     for (int k = 1; k <= pf; ++k) pf_trip(k, true, false);
-  int2 cv = gtid < np ? __ldg(reinterpret_cast<const int2*>(code) + gtid) : make_int2(-1, -1);
-  double2 dv = (gtid < np && hz) ? __ldg(reinterpret_cast<const double2*>(invD) + gtid)
-                                 : make_double2(0, 0);
+  int2 cv = gtid < np ? ldg2i_hint(code + 2 * gtid, pol_s) : make_int2(-1, -1);
+  double2 dv = (gtid < np && hz) ? ldg2_hint(invD + 2 * gtid, pol_d) : make_double2(0, 0);
   pdl_wait();
   pdl_trigger();
   if (blockIdx.y) {
@@ -328,11 +331,11 @@ cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restr
   for (int64_t q = gtid; q < np; q += nthr, ++k) {
     if (pf > 0 && threadIdx.x == 0) pf_trip(k + 1 + pf, true, true);
     if (q != gtid) {
-      cv = __ldg(reinterpret_cast<const int2*>(code) + q);
-      dv = hz ? __ldg(reinterpret_cast<const double2*>(invD) + q) : make_double2(0, 0);
+      cv = ldg2i_hint(code + 2 * q, pol_s);
+      dv = hz ? ldg2_hint(invD + 2 * q, pol_d) : make_double2(0, 0);
     }
-    double2 rv = reinterpret_cast<const double2*>(r)[q];
-    double2 av = __ldg(reinterpret_cast<const double2*>(w) + q);
+    double2 rv = ld2_hint(r + 2 * q, pol_r);
+    double2 av = ldg2_hint(w + 2 * q, pol_r);
     int mx, my;
     const double px = gather(cv.x, mx), py = gather(cv.y, my);
     double2 wv;
@@ -341,7 +344,7 @@ cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restr
     double xd = 0.0;
     upd_point<true>(alpha, xd, rv.x, 0.0, av.x, dv.x, wv.x, hz, acc);
     upd_point<true>(alpha, xd, rv.y, 0.0, av.y, dv.y, wv.y, hz, acc);
-    reinterpret_cast<double2*>(r)[q] = rv;
+    st2_hint(r + 2 * q, rv, pol_r);
   }
   if ((n & 1) && gtid == 0) {
     const int64_t t = n - 1;
@@ -526,10 +529,10 @@ extern "C" int nk_cg_update_gs_seg(int64_t n, int ncomp, int64_t cstride, double
     const int pf = knob(NK_KNOB_CG_UPDATE);
     if (segtab)
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<true>, g, dim3(kVecThreads), 0, s, n, r, w,
-                invD, code, segtab, st, partials, cstride, pf);
+                invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
     else
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<false>, g, dim3(kVecThreads), 0, s, n, r, w,
-                invD, code, segtab, st, partials, cstride, pf);
+                invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
   } else {
     if (segtab) {
       set_error("cg_update_gs_seg: gathered segments need 16-byte aligned r / w / invD");

@@ -161,7 +161,11 @@ __device__ __forceinline__ void prefetch_l2_hint(const void* p, int64_t bytes, u
   }
 }
 // NK_KNOB_L2 bits
-enum { kL2StreamFirst = 1, kL2ReuseLast = 2, kL2InvDLast = 4 };
+enum { kL2StreamFirst = 1, kL2ReuseLast = 2, kL2InvDLast = 4, kL2SetAside = 8 };
+// Host (nk_set_knob(NK_KNOB_L2, ..)): with kL2SetAside, reserve the device's
+// maximum persisting-L2 set-aside (cudaLimitPersistingL2CacheSize) for
+// evict_last lines; without, release it.
+void l2_apply_set_aside();
 
 // Threads per block for the streaming PCG kernels and the fixed number of
 // partial sums they produce.  The partial count does not depend on the GPU so

@@ -290,9 +290,10 @@ def test_pcg_spec_examples():
 @pytest.mark.parametrize("counts,N", [((4, 4, 4), 7), ((10, 10, 10), 7), ((3, 3, 3), 5),
                                       ((3, 2, 3), 3)])
 def test_launch_knobs_bit_identical(counts, N):
-    """PDL (programmatic dependent launch with static-operand prologues) and
-    the update's L2 prefetch change scheduling only: solves with every knob
-    off and at the defaults are bit-identical, graph-captured included."""
+    """PDL (programmatic dependent launch with static-operand prologues), the
+    update's L2 prefetch and the L2 eviction hints change scheduling / cache
+    policy only: solves with every knob off, at the defaults and with every
+    option on are bit-identical, graph-captured included."""
     from paper_2104_05829_b200._lib import lib
     L = lib()
     m, o = both_meshes(counts, N)
@@ -302,14 +303,15 @@ def test_launch_knobs_bit_identical(counts, N):
     b = torch.as_tensor(o.mask.ravel() * ogs.gs_op(o.ids, rng.standard_normal(m.n_local)),
                         device="cuda")
     ra = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000).solve(b)
-    old = (L.nk_set_knob(0, 0), L.nk_set_knob(1, 0))
+    old = (L.nk_set_knob(0, 0), L.nk_set_knob(1, 0), L.nk_set_knob(2, 0))
     try:
         rb = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000).solve(b)
         L.nk_set_knob(0, 31)      # every PDL family, late trigger, no prologue
+        L.nk_set_knob(2, 7)       # every L2 hint
         rc = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000).solve(b)
     finally:
-        L.nk_set_knob(0, old[0])
-        L.nk_set_knob(1, old[1])
+        for k, v in enumerate(old):
+            L.nk_set_knob(k, v)
     for r in (rb, rc):
         assert r.iterations == ra.iterations and r.residual_history == ra.residual_history
         assert torch.equal(r.x, ra.x)
