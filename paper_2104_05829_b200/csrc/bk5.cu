@@ -77,6 +77,7 @@ extern "C" int nk_bk5_variant_get();
 static int kvariant_for(int N) {
   const int v = nk_bk5_variant_get();
   if (v == 1 || v == 3 || v == 4 || v == 5) return v;
+  if (v == 7) return N >= 8 ? 7 : 3;   // dmma: N + 1 >= 9
   switch (N) {
     case 2: case 6: case 8: case 14: case 15: return 5;
     default: return 3;

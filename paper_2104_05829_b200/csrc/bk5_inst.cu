@@ -3,6 +3,7 @@
 #include "bk5_tma.cuh"
 #include "bk5_pcg.cuh"
 #include "bk5_pencil3.cuh"
+#include "bk5_dmma.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -284,6 +285,17 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
       // smem 7 element buffers: NQ 8 -> 32 KB, 10 -> 57 KB, 12 -> 105 KB per CTA
       constexpr int M3 = NQ <= 6 ? 4 : (NQ <= 8 ? 3 : (NQ <= 10 ? 2 : 1));
       return launch_pencil3<NQ, M3>(nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, s);
+    }
+  }
+  if constexpr (NQ >= 9) {
+    if (variant == 7 && ncomp == 1) {   // FP64 tensor-core contractions (bk5_dmma.cuh)
+      constexpr int MINB = NQ <= 14 ? 2 : 1;   // shared memory fits two CTAs up to NQ = 14
+      if (nblocks) {
+        *nblocks = dmma_grid<NQ, MINB>(nlist);
+        return NK_OK;
+      }
+      return launch_dmma<NQ, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                                   part_base, reduce_count, s);
     }
   }
   if (variant == 5 && ncomp == 1)

@@ -18,7 +18,7 @@ import paper_2104_05829_b200 as nk  # noqa: E402
 from paper_2104_05829_b200 import kernels as K  # noqa: E402
 
 
-@pytest.mark.parametrize("N", [2, 3, 7, 12])
+@pytest.mark.parametrize("N", [2, 3, 7, 8, 12, 15])
 def test_select_variant_and_parity(N):
     counts = (3, 2, 2)
     m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
@@ -41,6 +41,43 @@ def test_select_variant_and_parity(N):
         assert K.variant_report()[-1]["forced"]
     finally:
         K.reset_kernel_variant()
+
+
+@pytest.mark.parametrize("N,counts", [(8, (3, 2, 2)), (9, (2, 2, 3)), (12, (3, 2, 2)),
+                                      (13, (2, 3, 1)), (14, (2, 2, 2)), (15, (3, 2, 2))])
+def test_dmma_variant_parity_fused(N, counts):
+    """Variant 7 (FP64 tensor-core contractions, bk5_dmma.cuh; persistent
+    CTAs that each take several elements, padded 16 x 16 fragments): w vs
+    the oracle with the Helmholtz mass term and the Dirichlet mask, and the
+    fused p.Ap (nk_bk5 with a CG state) vs the host dot, at every order it
+    serves."""
+    from paper_2104_05829_b200._lib import check, lib, ptr
+    from oracle import gs as ogs  # noqa: F401
+    L = lib()
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    o = om.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = np.random.default_rng(100 + N).standard_normal((m.E,) + (N + 1,) * 3)
+    lam0, lam1 = 0.7, 2.5
+    ref = lam0 * oop.bk5(o.basis.diff, o.G, u) + lam1 * o.B * u
+    ref = ref * o.mask
+    old = L.nk_bk5_set_variant(7)
+    try:
+        ut = torch.as_tensor(u, device="cuda").reshape(-1)
+        w = torch.empty_like(ut)
+        st = torch.zeros(256, dtype=torch.uint8, device="cuda")
+        nb = int(L.nk_bk5_blocks(N, m.E, 1))
+        assert 1 <= nb <= m.E
+        part = torch.zeros(nb, dtype=torch.float64, device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+        check(L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(ut), ptr(w), lam0, ptr(m.B),
+                       lam1, 1, m.n_local, ptr(m.mask), None, 0, ptr(st), ptr(part), 0, nb, s),
+              "bk5")
+        wh = w.cpu().numpy().reshape(ref.shape)
+        assert np.linalg.norm(wh - ref) / np.linalg.norm(ref) < 1e-12
+        pap = float(st[8:16].view(torch.float64).item())
+        assert abs(pap - float(np.sum(u * ref))) <= 1e-11 * abs(float(np.sum(u * ref)))
+    finally:
+        L.nk_bk5_set_variant(old)
 
 
 def test_variant_errors():
