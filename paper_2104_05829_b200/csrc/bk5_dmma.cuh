@@ -262,7 +262,7 @@ static int launch_dmma(int64_t nlist, const int32_t* elist, const double* Dhost,
   const int64_t grid = dmma_grid<NQ, MINB>(nlist);
   if (grid == 0) return NK_OK;
   DParam<NQ> D;
-  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  D.set(Dhost);
   launch_ex(st != nullptr ? kPdlStep : 0, bk5_dmma<NQ, MINB>, dim3((unsigned)grid),
             dim3(C::THREADS), C::smem_bytes(), s, nlist, elist, D, G, u, w, lam0, B, lam1, mask,
             st, partials, part_base, reduce_count);

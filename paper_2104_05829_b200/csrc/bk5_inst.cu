@@ -225,7 +225,7 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
       }
       if (nb == 0) return NK_OK;
       DParam<2> Dp;
-      for (int q = 0; q < 4; ++q) Dp.d[q] = D[q];
+      Dp.set(D);
       bk5_n1<2><<<(unsigned)nb, kN1PtThreads, 0, s>>>(nlist, elist, Dp, G, u, w, lam0, B, lam1,
                                                     mask, st, partials, part_base, reduce_count);
       return check_launch("bk5_n1");
@@ -341,7 +341,7 @@ extern "C" int NK_CAT(nk_bk5_pcg_nq, NK_BK5_NQ)(int64_t nlist, const int32_t* el
     }
     if (nb == 0) return NK_OK;
     DParam<2> Dp;
-    for (int q = 0; q < 4; ++q) Dp.d[q] = D[q];
+    Dp.set(D);
     bk5_n1_pcg<2><<<(unsigned)nb, kN1PtThreads, 0, s>>>(nlist, elist, Dp, G, p, w, lam0, B, lam1,
                                                    mask, x, r, invD, st, partials, part_base,
                                                    reduce_count, hist);

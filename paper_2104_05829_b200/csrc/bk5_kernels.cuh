@@ -20,9 +20,38 @@
 
 namespace nk {
 
+// D-hat as a kernel parameter (constant bank), plus its even-odd split.
+// D-hat is centro-antisymmetric (D[N-q][N-m] = -D[q][m]: GLL nodes are
+// symmetric), and so is its transpose; with s_m = v_m + v_{N-m},
+// d_m = v_m - v_{N-m} (m < H = NQ/2) a 1-D derivative is
+//   out_q = O_q + E_q,  out_{N-q} = O_q - E_q  (q < H),  out_mid = M . d  (NQ odd)
+//   E_q = sum_m Ev[q][m] s_m (+ Ev[q][H] v_mid),  O_q = sum_m Od[q][m] d_m
+// with Ev = (D[q][m] + D[q][N-m]) / 2 (Ev[q][H] = D[q][mid]), Od = (D[q][m] -
+// D[q][N-m]) / 2, M[m] = D[mid][m]: about half the multiply-adds and half the
+// D-hat operand fetches of the direct product (the rounding differs from it
+// at the 1e-16 level).  eo holds the forward tables, then the transposed ones.
 template <int NQ>
 struct DParam {
-  double d[NQ * NQ];  // row-major D[a][m] = h_m'(xi_a), passed by value
+  static constexpr int H = NQ / 2, ODD = NQ & 1;
+  static constexpr int EOF_ = H * (H + ODD) + H * H + ODD * H;   // one direction
+  double d[NQ * NQ];   // row-major D[a][m] = h_m'(xi_a)
+  double eo[2 * EOF_ > 0 ? 2 * EOF_ : 1];
+  void set(const double* Dh) {   // host
+    for (int q = 0; q < NQ * NQ; ++q) d[q] = Dh[q];
+    for (int tr = 0; tr < 2; ++tr) {
+      double* T = eo + tr * EOF_;
+      auto A = [&](int q, int m) { return tr ? Dh[m * NQ + q] : Dh[q * NQ + m]; };
+      for (int q = 0; q < H; ++q) {
+        for (int m = 0; m < H; ++m) {
+          T[q * (H + ODD) + m] = 0.5 * (A(q, m) + A(q, NQ - 1 - m));
+          T[H * (H + ODD) + q * H + m] = 0.5 * (A(q, m) - A(q, NQ - 1 - m));
+        }
+        if (ODD) T[q * (H + ODD) + H] = A(q, H);
+      }
+      if (ODD)
+        for (int m = 0; m < H; ++m) T[H * (H + ODD) + H * H + m] = A(H, m);
+    }
+  }
 };
 
 // Tunable shape: EPB elements per CTA (EPB*NQ^2 threads), MINB CTAs per SM
@@ -201,7 +230,7 @@ static int launch_kslab(int64_t nlist, const int32_t* elist, const double* Dhost
   const int64_t nblk = (nlist + C::EPB - 1) / C::EPB;
   if (nblk == 0) return NK_OK;
   DParam<NQ> D;
-  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  D.set(Dhost);
   bk5_kslab<NQ, NC, EPB, MINB><<<(unsigned)nblk, C::THREADS, smem, s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, cstride, mask, st, partials, part_base,
       reduce_count, pf_dist);

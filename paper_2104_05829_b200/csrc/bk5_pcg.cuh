@@ -232,7 +232,7 @@ static int launch_pencil_pcg(int64_t nlist, const int32_t* elist, const double* 
   const int64_t nblk = (nlist + EPB - 1) / EPB;
   if (nblk == 0) return NK_OK;
   DParam<NQ> D;
-  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  D.set(Dhost);
   bk5_pencil_pcg<NQ, EPB, MINB><<<(unsigned)nblk, C::THREADS, smem, s>>>(
       nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base,
       reduce_count, hist);

@@ -69,16 +69,36 @@ struct PencilCfg {
   static size_t smem_bytes() { return sizeof(double) * ((size_t)EPB * 3 * VOL + 32); }
 };
 
-// out[q] = sum_m D[q][m] v[m]   (TRANS: sum_m D[m][q] v[m])
+// out[q] = sum_m D[q][m] v[m]   (TRANS: sum_m D[m][q] v[m]), by the
+// even-odd split of D-hat (DParam): ~NQ^2/2 multiply-adds instead of NQ^2.
 template <int NQ, bool TRANS>
 __device__ __forceinline__ void matvec(const DParam<NQ>& D, const double (&v)[NQ],
                                        double (&out)[NQ]) {
+  constexpr int H = NQ / 2, ODD = NQ & 1, HE = H + ODD;
+  constexpr int OFF = TRANS ? DParam<NQ>::EOF_ : 0;
+  double s[H > 0 ? H : 1], d[H > 0 ? H : 1];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    double acc = 0.0;
+  for (int m = 0; m < H; ++m) {
+    s[m] = v[m] + v[NQ - 1 - m];
+    d[m] = v[m] - v[NQ - 1 - m];
+  }
 #pragma unroll
-    for (int m = 0; m < NQ; ++m) acc = fma(TRANS ? D.d[m * NQ + q] : D.d[q * NQ + m], v[m], acc);
-    out[q] = acc;
+  for (int q = 0; q < H; ++q) {
+    double e = 0.0, o = 0.0;
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      e = fma(D.eo[OFF + q * HE + m], s[m], e);
+      o = fma(D.eo[OFF + H * HE + q * H + m], d[m], o);
+    }
+    if (ODD) e = fma(D.eo[OFF + q * HE + H], v[H], e);
+    out[q] = o + e;
+    out[NQ - 1 - q] = o - e;
+  }
+  if (ODD) {
+    double mm = 0.0;
+#pragma unroll
+    for (int m = 0; m < H; ++m) mm = fma(D.eo[OFF + H * HE + H * H + m], d[m], mm);
+    out[H] = mm;
   }
 }
 
@@ -357,7 +377,7 @@ static int launch_pencil_k(int64_t nlist, const int32_t* elist, const double* Dh
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
   DParam<NQ> D;
-  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  D.set(Dhost);
   // pfG: 0 off, 1 own G into L2, 2 own G + the element one wave ahead
   const int64_t ahead = pfG >= 2 ? resident * EPB : 0;
   launch_ex(st != nullptr ? kPdlStep : 0, bk5_pencil<NQ, EPB, MINB, NC, CDOT>,
@@ -548,7 +568,7 @@ static int launch_pencil2(int64_t nlist, const int32_t* elist, const double* Dho
   const int64_t nblk = (nlist + EPB - 1) / EPB;
   if (nblk == 0) return NK_OK;
   DParam<NQ> D;
-  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  D.set(Dhost);
   bk5_pencil2<NQ, EPB, MINB><<<(unsigned)nblk, EPB * NQ * NQ, smem, s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG);
   return check_launch("bk5_pencil2");

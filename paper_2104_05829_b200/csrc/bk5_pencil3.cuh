@@ -171,7 +171,7 @@ static int launch_pencil3(int64_t nlist, const int32_t* elist, const double* Dho
   }
   if (nlist == 0) return NK_OK;
   DParam<NQ> D;
-  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  D.set(Dhost);
   bk5_pencil3<NQ, MINB><<<(unsigned)nlist, NQ * NQ, smem, s>>>(nlist, elist, D, G, u, w, lam0, B,
                                                               lam1, cstride, mask);
   return check_launch("bk5_pencil3");

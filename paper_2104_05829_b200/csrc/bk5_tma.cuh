@@ -276,7 +276,7 @@ static int launch_pencil_tma(int64_t nlist, const int32_t* elist, const double* 
     return NK_ERR_INVALID;
   }
   DParam<NQ> D;
-  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  D.set(Dhost);
   bk5_pencil_tma<NQ, MINB><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count);
   return check_launch("bk5_pencil_tma");
@@ -580,7 +580,7 @@ static int launch_pencil_tma_pcg(int64_t nlist, const int32_t* elist, const doub
     return NK_ERR_INVALID;
   }
   DParam<NQ> D;
-  for (int q = 0; q < NQ * NQ; ++q) D.d[q] = Dhost[q];
+  D.set(Dhost);
   launch_ex(kPdlStep, bk5_pencil_tma_pcg<NQ, MINB>, dim3((unsigned)grid), dim3(C::THREADS),
             C::smem_bytes(), s, nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st,
             partials, part_base, reduce_count, hist, knob(NK_KNOB_PDL), knob(NK_KNOB_L2));
