@@ -78,8 +78,8 @@ static int kvariant_for(int N) {
   const int v = nk_bk5_variant_get();
   if (v == 1 || v == 3 || v == 4 || v == 5) return v;
   if (v == 7) return N >= 8 ? 7 : 3;   // dmma: N + 1 >= 9
-  switch (N) {
-    case 2: case 6: case 8: case 14: case 15: return 5;
+  switch (N) {   // re-measured with the even-odd contractions (profiles/r2s_bk5_variants.jsonl)
+    case 2: case 6: case 8: case 9: case 10: case 15: return 5;
     default: return 3;
   }
 }
