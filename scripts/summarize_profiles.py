@@ -3,7 +3,7 @@
 
     python scripts/summarize_profiles.py --tag r1 --full gpurun_out/x.ncu-rep [...]
                                          [--launches gpurun_out/launches.csv]
-                                         [--traffic-kernel bk5_pencil_tma]
+                                         [--traffic-kernel 'bk5_pencil<8']
 
 Writes profiles/<tag>_ncu_<kernel>.json (key metrics + stall shares),
 profiles/<tag>_launches.json (per-kernel launch counts / mean / share of a
@@ -109,7 +109,10 @@ def main():
             p = os.path.join(PROF, f"{args.tag}_ncu_{short}.json")
             json.dump(d, open(p, "w"), indent=1)
             print("wrote", p)
-            if args.traffic_kernel and args.traffic_kernel in d["kernel"]:
+            # prefix match on the demangled name ("bk5_pencil<8" must not pick
+            # up bk5_pencil_tma_pcg<8, 3>, the fused BP5 step)
+            name = d["kernel"].split("(")[0].replace("void ", "").strip()
+            if args.traffic_kernel and name.startswith(args.traffic_kernel):
                 rd = d["dram__bytes_read.sum"]
                 wr = d["dram__bytes_write.sum"]
                 tr = scale(rd["value"], rd["unit"]) + scale(wr["value"], wr["unit"])
