@@ -164,19 +164,23 @@ int nk_bk5_batch_variant(int N);
 /* blocks of one nk_bk5_batch launch (ncomp = 3, with st) over nlist elements
  * -- the reduce_count of a single launch, the minimum part_stride. */
 int64_t nk_bk5_batch_blocks(int N, int64_t nlist);
-/* kernel variant selection: 0 = auto (measured per-order table: 5 for
- * N in {2,6,8,14,15}, else 3; 3-component batches: 6 at N in {3,5,7,9,10,11},
- * pencil3 at N in {4,6}, three scalar launches elsewhere), 5 = pencil2 (two
- * shared buffers, u re-read from L1/L2), 1 = k-slab (2D
- * thread plane, k-column in registers, D in shared memory), 3 = pencil
- * (register 1-D contractions, D in the constant bank, swizzled shared
+/* kernel variant selection: 0 = auto (measured per-order table: 8 for
+ * N in {9,10,12,13,14}, 5 for N in {2,6,8,15}, else 3; 3-component batches:
+ * 6 at N in {3,5,7,9,10,11}, pencil3 at N in {4,6}, three scalar launches
+ * elsewhere), 5 = pencil2 (two shared buffers, u re-read from L1/L2), 1 =
+ * k-slab (2D thread plane, k-column in registers, D in shared memory), 3 =
+ * pencil (register 1-D contractions, D in the constant bank, swizzled shared
  * transposes), 4 = pencil-TMA (persistent CTAs, cp.async.bulk 2-stage ring;
  * N+1 in {4, 6, 8}, else pencil), 6 = seq3 (ncomp = 3: the pencil kernel
  * running the three components back to back per CTA, G from HBM once;
- * ncomp = 1 calls use the auto table).  N = 1 always runs its
- * point-per-lane kernel unless 1 is set.  Variants 3/4/5 serve ncomp = 1;
- * with them forced, ncomp = 3 uses pencil3 (k-slab for 1).  Returns the
- * previous value. */
+ * ncomp = 1 calls use the auto table), 7 = dmma (FP64 tensor-core
+ * contractions, N+1 in 9..16), 8 = stage (persistent CTAs; the next
+ * element's u and G moved into shared memory by cp.async.bulk while the
+ * current one computes, w assembled in shared memory and bulk-stored;
+ * N+1 in 10..15, else pencil).  N = 1 always runs its point-per-lane kernel
+ * unless 1 is set.  Variants 3/4/5/7/8 serve ncomp = 1; with them forced,
+ * ncomp = 3 uses pencil3 (k-slab for 1) or three scalar launches.  Returns
+ * the previous value. */
 int nk_bk5_set_variant(int variant);
 /* shape tuning: cfg selects the (elements per CTA, CTAs per SM) shape --
  * k-slab at N = 7 (0 = default 4x2, 1 = 4x3, 2 = 2x4, 3 = 2x6, 4 = 1x8,

@@ -78,9 +78,11 @@ static int kvariant_for(int N) {
   const int v = nk_bk5_variant_get();
   if (v == 1 || v == 3 || v == 4 || v == 5) return v;
   if (v == 7) return N >= 8 ? 7 : 3;   // dmma: N + 1 >= 9
-  switch (N) {   // re-measured with the even-odd contractions (profiles/r2s_bk5_variants.jsonl)
-    case 2: case 6: case 8: case 9: case 10: case 15: return 5;
-    default: return 3;
+  if (v == 8) return (N >= 9 && N <= 14) ? 8 : 3;   // stage: N + 1 in 10..15
+  switch (N) {   // measured: profiles/r2s_bk5_order_sweep_evenodd.jsonl, r2x_stage_sweep.jsonl
+    case 2: case 6: case 8: case 15: return 5;            // pencil2
+    case 9: case 10: case 12: case 13: case 14: return 8; // stage (TMA-staged u, G)
+    default: return 3;                                      // pencil
   }
 }
 
@@ -181,6 +183,7 @@ extern "C" int nk_bk5_batch(int N, int64_t nelem, const double* D, const double*
     return NK_ERR_INVALID;
   }
   cudaStream_t s = S(stream);
+  const int64_t nq3 = (int64_t)(N + 1) * (N + 1) * (N + 1);
   if (ncomp == 3) {
     int v = helm3_variant(N);
     // fused per-component dots: seq3 or three scalar launches
@@ -188,7 +191,7 @@ extern "C" int nk_bk5_batch(int N, int64_t nelem, const double* D, const double*
     if (v == -1) {
       for (int c = 0; c < 3; ++c) {
         int rc = kslab_table[N](1, n, elem_list, D, G, u + c * comp_stride, w + c * comp_stride,
-                                lam0, B, lam1, comp_stride, mask, st ? st + c : nullptr,
+                                lam0, B, lam1, nelem * nq3, mask, st ? st + c : nullptr,
                                 st ? partials + c * part_stride : nullptr, part_base,
                                 reduce_count, s, nullptr, g_cfg, g_pf, kvariant_for(N), 0);
         if (rc != NK_OK) return rc;
@@ -199,7 +202,9 @@ extern "C" int nk_bk5_batch(int N, int64_t nelem, const double* D, const double*
                           partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf, v,
                           part_stride);
   }
-  return kslab_table[N](ncomp, n, elem_list, D, G, u, w, lam0, B, lam1, comp_stride, mask, st,
+  // ncomp = 1: the stride slot carries the u array length (nelem NQ^3
+  // doubles), which bounds the 16-byte rounded bulk copies of bk5_stage
+  return kslab_table[N](ncomp, n, elem_list, D, G, u, w, lam0, B, lam1, nelem * nq3, mask, st,
                         partials, part_base, reduce_count, s, nullptr, g_cfg, g_pf,
                         kvariant_for(N), 0);
 }

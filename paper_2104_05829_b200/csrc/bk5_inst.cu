@@ -4,6 +4,7 @@
 #include "bk5_pcg.cuh"
 #include "bk5_pencil3.cuh"
 #include "bk5_dmma.cuh"
+#include "bk5_stage.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -184,6 +185,35 @@ int runt(int64_t nlist, const int32_t* elist, const double* D, const double* G, 
                                      part_base, reduce_count, s);
 }
 
+// bk5_stage (variant 8) shapes per order: NGS of the six G components staged
+// in shared memory, NUB u buffers (2: u(next) issued an element ahead and w
+// bulk-stored), MINB CTAs per SM.  cfg 0 is the default; nk_bk5_tune cfg 21 /
+// 22 select two alternatives for the sweep (scripts/bk5_hot.py --sweep).
+template <int NQ> struct StageShapes {
+  static constexpr int G[3] = {6, 6, 6}, U[3] = {2, 1, 2}, M[3] = {1, 1, 1};
+};
+#define NK_SD(NQ_, g0, u0, m0, g1, u1, m1, g2, u2, m2)                      \
+  template <> struct StageShapes<NQ_> {                                     \
+    static constexpr int G[3] = {g0, g1, g2}, U[3] = {u0, u1, u2}, M[3] = {m0, m1, m2}; \
+  };
+NK_SD(10, 6, 2, 2, 6, 1, 3, 4, 2, 3) NK_SD(11, 6, 2, 2, 4, 1, 3, 6, 2, 1)
+NK_SD(12, 6, 2, 1, 4, 1, 3, 6, 2, 2) NK_SD(13, 6, 2, 1, 3, 2, 2, 6, 1, 1)
+NK_SD(14, 6, 2, 1, 2, 2, 2, 6, 1, 1) NK_SD(15, 4, 2, 1, 5, 1, 1, 3, 2, 1)
+#undef NK_SD
+
+template <int NQ, int NGS, int NUB, int MINB>
+int runs(int64_t nlist, const int32_t* elist, const double* D, const double* G, const double* u,
+         double* w, double lam0, const double* B, double lam1, const uint8_t* mask,
+         nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
+         int64_t u_len, cudaStream_t s, int64_t* nblocks) {
+  if (nblocks) {
+    *nblocks = stage_grid<NQ, NGS, NUB, MINB>(nlist);
+    return NK_OK;
+  }
+  return launch_stage<NQ, NGS, NUB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                                     part_base, reduce_count, u_len, s);
+}
+
 template <int NQ, int NC>
 int run_cfg(int cfg, int64_t nlist, const int32_t* elist, const double* D, const double* G,
             const double* u, double* w, double lam0, const double* B, double lam1,
@@ -296,6 +326,18 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
       }
       return launch_dmma<NQ, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
                                    part_base, reduce_count, s);
+    }
+  }
+  if constexpr (NQ >= 10 && NQ <= 15) {
+    if (variant == 8 && ncomp == 1) {   // TMA-staged operands (bk5_stage.cuh)
+      // cstride carries the length of the u array for ncomp = 1 (nk_bk5_batch)
+      using SD = StageShapes<NQ>;
+#define NK_SARGS nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, \
+                 reduce_count, cstride, s, nblocks
+      if (cfg == 21) return runs<NQ, SD::G[1], SD::U[1], SD::M[1]>(NK_SARGS);
+      if (cfg == 22) return runs<NQ, SD::G[2], SD::U[2], SD::M[2]>(NK_SARGS);
+      return runs<NQ, SD::G[0], SD::U[0], SD::M[0]>(NK_SARGS);
+#undef NK_SARGS
     }
   }
   if (variant == 5 && ncomp == 1)

@@ -1,0 +1,340 @@
+// BK5 variant 8, "stage": persistent CTAs whose element operands are staged
+// in shared memory by the TMA engine, for the high orders (N + 1 = NQ >= 10).
+//
+// Why: ncu source-level stall sampling of the register-pencil kernels at
+// N = 12 (bk5_pencil<13>) and N = 15 (bk5_pencil2<16>) puts 48-56% of the
+// warp stalls on two phases that wait for L2: the u rows of F1 (long
+// scoreboard 62%) and the 6 x NQ G loads per thread of the G phase (long
+// scoreboard 35-52%, LSU throttle) -- with only 2 CTAs (12-16 warps) per SM
+// nothing covers them, and a hot-L2 run (profiles/r2u_bk5_hot.jsonl) is no
+// faster than a cold one: the limiter is L2 -> SM latency, not HBM.  Here a
+// single thread moves the NEXT element's u and G into shared memory with
+// cp.async.bulk (SASS UBLKCP, mbarrier transaction counts) while the CTA
+// computes the current one, so every phase reads shared memory:
+//
+//   wait u_bar   F1 i-pencils  u row (shared)     -> ur -> R
+//                F2 j-pencils  u column (shared)  -> us -> S
+//                F3 k-pencils  u column (shared)  -> ut (registers)
+//   sync (A)     u buffer free: issue u(next)
+//   wait g_bar   G  k-pencils  G (shared; components >= NGS from L2) -> gr, gs
+//                   in place in R, S; gt (registers)
+//   sync (B)     G buffer free: issue G(next)
+//   B2 j-pencils S column  -> D^T gs in place      ; sync
+//   B3 k-pencils S column += D^T gt                 ; sync
+//   B1 i-pencils w = lam0 (D^T R row + S row) [+ lam1 B u, mask, u.w] -> HBM
+//   sync (C)
+//
+// The contractions are the register pencils of bk5_pencil.cuh (even-odd D-hat
+// in the constant bank, 12 shared accesses per point as in pencil2).  The
+// u buffer is the element's dense HBM image (i fastest): conflict-free for
+// the column passes and, for F1's rows, with 8-byte reads at odd NQ (row
+// stride NQ odd) and 16-byte reads at even NQ (row stride NQ/2 chunks: 5 and
+// 7 are conflict-free, 6 two-way).  At odd NQ an element starts 8 bytes off
+// a 16-byte boundary every other element: the copy then starts one double
+// early (the buffer pointer shifts by one); the array's very last double,
+// when a copy would run past the allocation, is stored by a plain load.
+// NGS of the six G components are staged (all six when the CTA fits); the
+// rest are read from global memory after a bulk L2 prefetch issued one
+// element ahead.  HBM per point: u 8 + G 48 + w 8 B (the BK5 roofline).
+#pragma once
+#include "bk5_tma.cuh"
+
+namespace nk {
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// NUB = 2: two u buffers -- u(next) is issued at the START of the current
+// element (one whole element of lead time), and the current element's w is
+// assembled in its own u buffer after B1 and written back by one bulk store
+// (cp.async.bulk.global.shared, SASS UBLKCP) instead of 13-16 strided 8-byte
+// stores per thread.  NUB = 1: one u buffer, refilled after F3.
+template <int NQ, int NGS, int NUB>
+struct StageCfg {
+  static_assert(NGS >= 1 && NGS <= 6, "NGS");
+  static_assert(NUB == 1 || NUB == 2, "NUB");
+  static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
+  static constexpr int VOL = PencilLayout<NQ>::VOL;
+  static constexpr int UB = (NQ3 + 2 + 1) & ~1;         // doubles, even: 16-B aligned next
+  static constexpr int GBUF = (NGS * NQ3 + 1 + 1) & ~1;
+  static constexpr int THREADS = NQ2;
+  // layout (doubles): U[NUB] | G | R | S | red[32] ; mbarriers u[NUB], g
+  static size_t smem_bytes() {
+    return sizeof(double) * ((size_t)NUB * UB + GBUF + 2 * VOL + 32) +
+           (NUB + 1) * sizeof(uint64_t);
+  }
+};
+
+template <int NQ, int NGS, int NUB, int MINB>
+__global__ void __launch_bounds__(NQ * NQ, MINB)
+bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
+          const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
+          double lam0, const double* __restrict__ B, double lam1,
+          const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
+          int64_t part_base, int64_t reduce_count, int64_t u_len) {
+  using L = PencilLayout<NQ>;
+  using C = StageCfg<NQ, NGS, NUB>;
+  constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL;
+  extern __shared__ __align__(128) double smem[];
+  if (st != nullptr && st->done) return;
+  double* Ub0 = smem;
+  double* Gb = Ub0 + NUB * C::UB;
+  double* Rr = Gb + C::GBUF;
+  double* Ss = Rr + VOL;
+  double* red = Ss + VOL;
+  uint64_t* ubar = reinterpret_cast<uint64_t*>(red + 32);   // [NUB]
+  uint64_t* gbar = ubar + NUB;
+
+  const int t = threadIdx.x;
+  const int a = t % NQ, b = t / NQ;
+  const int64_t stride = gridDim.x;
+  // w assembled in shared memory and bulk-stored: needs u and w at the same
+  // 16-byte phase (then the staged u row and the w row align alike)
+  const bool bulkw = NUB == 2 &&
+      ((reinterpret_cast<uintptr_t>(u) ^ reinterpret_cast<uintptr_t>(w)) & 15) == 0;
+  auto elem_of = [&](int64_t slot) -> int64_t { return elist ? (int64_t)elist[slot] : slot; };
+  auto phase_of = [&](int64_t e) -> int {   // 1: the element starts 8 B off 16 B
+    return (int)((reinterpret_cast<uintptr_t>(u + e * NQ3) >> 3) & 1);
+  };
+
+  // thread 0 only
+  auto issue_u = [&](int64_t slot, int bi) {
+    const int64_t s0 = elem_of(slot) * NQ3;
+    const int sh = phase_of(s0 / NQ3);
+    int64_t cnt = (NQ3 + sh + 1) & ~int64_t(1);          // whole 16-B chunks
+    const bool tail = s0 - sh + cnt > u_len;             // would pass the array end
+    if (tail) cnt -= 2;
+    double* dst = Ub0 + bi * C::UB;
+    mbar_expect_tx(&ubar[bi], (uint32_t)(cnt * sizeof(double)));
+    tma_load_1d(dst, u + s0 - sh, (uint32_t)(cnt * sizeof(double)), &ubar[bi]);
+    if (tail) {                                          // the one uncovered double
+      dst[cnt] = u[s0 - sh + cnt];
+      fence_proxy_async();                               // before later bulk writes
+    }
+  };
+  auto issue_g = [&](int64_t slot) {
+    const double* src = G + elem_of(slot) * 6 * NQ3;    // 48 NQ^3 B: always 16-B aligned
+    constexpr uint32_t GBYTES = (uint32_t)(((NGS * NQ3 + 1) & ~1) * sizeof(double));
+    mbar_expect_tx(gbar, GBYTES);
+    tma_load_1d(Gb, src, GBYTES, gbar);
+    if (NGS < 6) prefetch_l2(src + NGS * NQ3, (int64_t)(6 - NGS) * NQ3 * sizeof(double));
+  };
+
+  if (t == 0) {
+    for (int i = 0; i < NUB; ++i) mbar_init(&ubar[i], 1);
+    mbar_init(gbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0 && (int64_t)blockIdx.x < nlist) {
+    issue_u(blockIdx.x, 0);
+    issue_g(blockIdx.x);
+  }
+  __syncthreads();   // the tail store (if any) before the first F1
+
+  double dot = 0.0;
+  int it = 0;
+  for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++it) {
+    const int64_t e = elem_of(slot);
+    const int sh = phase_of(e);
+    const int bi = NUB == 2 ? (it & 1) : 0;
+    double* uS = Ub0 + bi * C::UB + sh;
+    if (NUB == 2 && t == 0 && slot + stride < nlist) {
+      bulk_wait_read0();             // the other buffer's w (previous element) has left
+      issue_u(slot + stride, bi ^ 1);
+    }
+    mbar_wait(&ubar[bi], NUB == 2 ? ((it >> 1) & 1) : (it & 1));
+    double ut[NQ];
+    {  // ---- F1: i-pencils (j = a, k = b) -> R
+      double v[NQ], o[NQ];
+      const double* row = uS + b * NQ2 + a * NQ;
+      if (NQ % 2 == 0 && sh == 0) {   // 16-byte rows (sh = 1 only for a misaligned u slice)
+#pragma unroll
+        for (int m = 0; m < NQ; m += 2) {
+          const double2 p = *reinterpret_cast<const double2*>(row + m);
+          v[m] = p.x;
+          v[m + 1] = p.y;
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) v[m] = row[m];
+      }
+      matvec<NQ, false>(D, v, o);
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
+      // ---- F2: j-pencils (i = a, k = b) -> S
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = uS[b * NQ2 + m * NQ + a];
+      matvec<NQ, false>(D, v, o);
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+      // ---- F3: k-pencils (i = a, j = b) -> ut
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = uS[m * NQ2 + b * NQ + a];
+      matvec<NQ, false>(D, v, ut);
+    }
+    __syncthreads();   // (A)
+    if (NUB == 1 && t == 0 && slot + stride < nlist) issue_u(slot + stride, 0);
+    mbar_wait(gbar, it & 1);
+    double gt[NQ];
+    {  // ---- G: k-pencils, pointwise symmetric 3x3
+      const double* gp = G + e * 6 * NQ3 + b * NQ + a;
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const int p = k * NQ2 + b * NQ + a;
+        double g[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          g[c] = c < NGS ? Gb[c * NQ3 + p] : __ldg(gp + c * NQ3 + k * NQ2);
+        const int q = L::idx(k, b, a);
+        const double ur = Rr[q], us = Ss[q];
+        Rr[q] = g[0] * ur + g[1] * us + g[2] * ut[k];
+        Ss[q] = g[1] * ur + g[3] * us + g[4] * ut[k];
+        gt[k] = g[2] * ur + g[4] * us + g[5] * ut[k];
+      }
+    }
+    __syncthreads();   // (B) G buffer read for the last time
+    if (t == 0 && slot + stride < nlist) issue_g(slot + stride);
+    {  // ---- B2: j-pencils, in place on their own S column
+      double v[NQ], o[NQ];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = Ss[L::idx(b, m, a)];
+      matvec<NQ, true>(D, v, o);
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+    }
+    __syncthreads();
+    {  // ---- B3: k-pencils, S column += D^T gt
+      double o[NQ];
+      matvec<NQ, true>(D, gt, o);
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const int q = L::idx(k, b, a);
+        Ss[q] = o[k] + Ss[q];
+      }
+    }
+    __syncthreads();
+    {  // ---- B1: i-pencils + epilogue
+      double v[NQ], o[NQ];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = Rr[L::idx(b, a, m)];
+      matvec<NQ, true>(D, v, o);
+      const int64_t off = e * NQ3 + b * NQ2 + a * NQ;
+      double res[NQ];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) res[i] = lam0 * (o[i] + Ss[L::idx(b, a, i)]);
+      double* urow = uS + b * NQ2 + a * NQ;   // NUB = 2: still this element's u
+      if (B != nullptr || st != nullptr) {
+        double urw[NQ];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) urw[i] = NUB == 2 ? urow[i] : __ldg(u + off + i);
+        if (B != nullptr) {
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) res[i] = fma(lam1 * __ldg(B + off + i), urw[i], res[i]);
+        }
+        if (mask != nullptr) {
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) dot = fma(urw[i], res[i], dot);
+      } else if (mask != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+      }
+      if (bulkw) {
+        // w row into the u row (this thread's own row); the element's two
+        // edge doubles that fall outside the 16-byte bulk range go direct
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) urow[i] = res[i];
+        fence_proxy_async();
+        if (t == 0 && sh) w[e * NQ3] = res[0];
+        if (t == NQ2 - 1 && ((NQ3 - sh) & 1)) w[e * NQ3 + NQ3 - 1] = res[NQ - 1];
+      } else {
+        double* wr = w + off;
+        if (NQ % 2 == 0 && sh == 0 &&
+            ((reinterpret_cast<uintptr_t>(wr) & 15) == 0)) {
+#pragma unroll
+          for (int i = 0; i < NQ; i += 2)
+            *reinterpret_cast<double2*>(wr + i) = make_double2(res[i], res[i + 1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) wr[i] = res[i];
+        }
+      }
+    }
+    __syncthreads();   // (C) R, S free for the next element; w rows in shared
+    if (bulkw && t == 0) {
+      const int64_t cnt = (NQ3 - sh) & ~int64_t(1);
+      bulk_store(w + e * NQ3 + sh, uS + sh, (uint32_t)(cnt * sizeof(double)));
+      bulk_commit();
+    }
+  }
+  if (NUB == 2 && t == 0) bulk_wait0();   // shared source read and global writes done
+
+  if (st != nullptr) {
+    double vv[1] = {dot};
+    block_sum<1>(vv, red);
+    if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+    if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
+      double sres[1];
+      reduce_partials<1>(partials, reduce_count, 0, sres, red);
+      if (t == 0) st->pAp = sres[0];
+    }
+  }
+}
+
+// Grid: persistent, min(nlist, SMs x resident CTAs per SM).
+template <int NQ, int NGS, int NUB, int MINB>
+static int64_t stage_grid(int64_t nlist) {
+  static int64_t resident = -1;
+  if (resident < 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    using C = StageCfg<NQ, NGS, NUB>;
+    cudaFuncSetAttribute(bk5_stage<NQ, NGS, NUB, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_stage<NQ, NGS, NUB, MINB>, C::THREADS,
+                                                  C::smem_bytes());
+    resident = (int64_t)sms * (per > 0 ? per : 1);
+  }
+  return nlist < resident ? nlist : resident;
+}
+
+// u_len: doubles in the u array (bounds the 16-byte rounded copies)
+template <int NQ, int NGS, int NUB, int MINB>
+static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost, const double* G,
+                        const double* u, double* w, double lam0, const double* B, double lam1,
+                        const uint8_t* mask, nk_cg_state* st, double* partials,
+                        int64_t part_base, int64_t reduce_count, int64_t u_len, cudaStream_t s) {
+  using C = StageCfg<NQ, NGS, NUB>;
+  const int64_t grid = stage_grid<NQ, NGS, NUB, MINB>(nlist);
+  if (grid == 0) return NK_OK;
+  if ((reinterpret_cast<uintptr_t>(u) & 7) || (reinterpret_cast<uintptr_t>(G) & 15)) {
+    set_error("bk5_stage: u must be 8-byte and G 16-byte aligned");
+    return NK_ERR_INVALID;
+  }
+  DParam<NQ> D;
+  D.set(Dhost);
+  bk5_stage<NQ, NGS, NUB, MINB><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
+      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, u_len);
+  return check_launch("bk5_stage");
+}
+
+}  // namespace nk

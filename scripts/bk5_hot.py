@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--waves", default="1,2,4")
     ap.add_argument("--variants", default="0")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--cfgs", default="0", help="nk_bk5_tune shape configs (21: stage alt)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="configs[1] sizes (~3M points, E_FOR_N) instead of whole waves")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import torch
@@ -39,21 +42,31 @@ def main():
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6551.7
     out = open(args.out, "a") if args.out else None
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from bk5_sweep import E_FOR_N
     for N in [int(x) for x in args.orders.split(",")]:
-        for k in [int(x) for x in args.waves.split(",")]:
-            m = nk.build_box_mesh((1, 1, 1), (148, k, 1), N, deformation=("sine", 0.05))
+        shapes = ([(E_FOR_N[N],) * 3] if args.sweep else
+                  [(148, int(k), 1) for k in args.waves.split(",")])
+        for counts in shapes:
+            k = counts[1] if not args.sweep else None
+            m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
             n = m.n_local
             u = torch.randn(n, dtype=torch.float64, device="cuda")
             w = torch.empty_like(u)
-            for v in [int(x) for x in args.variants.split(",")]:
+            first = None
+            for v, cfg in [(int(x), int(c)) for x in args.variants.split(",")
+                           for c in args.cfgs.split(",")]:
+                if cfg != 0 and v != 8:
+                    continue
                 L.nk_bk5_set_variant(v)
+                L.nk_bk5_tune(cfg, 1)
 
                 def run():
                     check(L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(u), ptr(w), 1.0, None,
                                    0.0, 1, n, None, None, 0, None, None, 0, 0, sp), "bk5")
 
                 res = {}
-                for mode in ("cold", "hot"):
+                for mode in (("cold",) if args.sweep else ("cold", "hot")):
                     ts = []
                     for rep in range(args.reps + 5):
                         a = torch.cuda.Event(enable_timing=True)
@@ -67,15 +80,22 @@ def main():
                     torch.cuda.synchronize()
                     res[mode] = statistics.median([a.elapsed_time(b) for a, b in ts[5:]])
                 bytes_ = 64 * n
-                d = {"N": N, "E": m.E, "ctas_per_sm_waves": k, "variant": v,
-                     "cold_us": round(1e3 * res["cold"], 2), "hot_us": round(1e3 * res["hot"], 2),
+                if first is None:
+                    first = w.clone()
+                d = {"N": N, "E": m.E, "ctas_per_sm_waves": k, "variant": v, "cfg": cfg,
+                     "cold_us": round(1e3 * res["cold"], 2),
                      "cold_frac": round(bytes_ / res["cold"] / 1e6 / pk, 4),
-                     "hot_equiv_frac": round(bytes_ / res["hot"] / 1e6 / pk, 4)}
+                     "gdofs": round(m.E * N ** 3 / res["cold"] / 1e6, 2),
+                     "bitwise_same_as_first": bool(torch.equal(first, w))}
+                if "hot" in res:
+                    d["hot_us"] = round(1e3 * res["hot"], 2)
+                    d["hot_equiv_frac"] = round(bytes_ / res["hot"] / 1e6 / pk, 4)
                 print(json.dumps(d), flush=True)
                 if out:
                     out.write(json.dumps(d) + "\n")
                     out.flush()
             L.nk_bk5_set_variant(0)
+            L.nk_bk5_tune(0, 1)
             del m, u, w
 
 

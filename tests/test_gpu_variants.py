@@ -43,14 +43,18 @@ def test_select_variant_and_parity(N):
         K.reset_kernel_variant()
 
 
-@pytest.mark.parametrize("N,counts", [(8, (3, 2, 2)), (9, (2, 2, 3)), (12, (3, 2, 2)),
-                                      (13, (2, 3, 1)), (14, (2, 2, 2)), (15, (3, 2, 2))])
-def test_dmma_variant_parity_fused(N, counts):
-    """Variant 7 (FP64 tensor-core contractions, bk5_dmma.cuh; persistent
-    CTAs that each take several elements, padded 16 x 16 fragments): w vs
-    the oracle with the Helmholtz mass term and the Dirichlet mask, and the
-    fused p.Ap (nk_bk5 with a CG state) vs the host dot, at every order it
-    serves."""
+@pytest.mark.parametrize("variant,N,counts", [
+    (7, 8, (3, 2, 2)), (7, 9, (2, 2, 3)), (7, 12, (3, 2, 2)), (7, 13, (2, 3, 1)),
+    (7, 14, (2, 2, 2)), (7, 15, (3, 2, 2)),
+    (8, 9, (3, 2, 2)), (8, 10, (2, 2, 3)), (8, 11, (3, 3, 3)), (8, 12, (3, 3, 3)),
+    (8, 13, (2, 3, 1)), (8, 14, (3, 3, 1))])
+def test_dmma_variant_parity_fused(variant, N, counts):
+    """Variant 7 (FP64 tensor-core contractions, bk5_dmma.cuh) and variant 8
+    (TMA-staged operands, bk5_stage.cuh): persistent CTAs that each take
+    several elements.  w vs the oracle with the Helmholtz mass term and the
+    Dirichlet mask, and the fused p.Ap (nk_bk5 with a CG state) vs the host
+    dot, at every order they serve; odd E at odd N + 1 (27 elements at
+    N = 12) exercises the stage kernel's last-double tail copy."""
     from paper_2104_05829_b200._lib import check, lib, ptr
     from oracle import gs as ogs  # noqa: F401
     L = lib()
@@ -60,7 +64,7 @@ def test_dmma_variant_parity_fused(N, counts):
     lam0, lam1 = 0.7, 2.5
     ref = lam0 * oop.bk5(o.basis.diff, o.G, u) + lam1 * o.B * u
     ref = ref * o.mask
-    old = L.nk_bk5_set_variant(7)
+    old = L.nk_bk5_set_variant(variant)
     try:
         ut = torch.as_tensor(u, device="cuda").reshape(-1)
         w = torch.empty_like(ut)
@@ -78,6 +82,58 @@ def test_dmma_variant_parity_fused(N, counts):
         assert abs(pap - float(np.sum(u * ref))) <= 1e-11 * abs(float(np.sum(u * ref)))
     finally:
         L.nk_bk5_set_variant(old)
+
+
+@pytest.mark.parametrize("N,counts", [(9, (10, 10, 10)), (12, (10, 10, 10)), (13, (9, 9, 9)),
+                                      (14, (8, 8, 8))])
+def test_stage_variant_ring_reuse(N, counts):
+    """Variant 8 at sizes where every persistent CTA takes several elements
+    (E >> 148 x CTAs per SM): the u / G buffers and both mbarrier phases are
+    reused many times.  The contractions and their order are pencil2's, so
+    w is bit-identical to variant 5, and within 1e-12 of the oracle."""
+    from paper_2104_05829_b200._lib import lib
+    L = lib()
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    o = om.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = np.random.default_rng(7 + N).standard_normal((m.E,) + (N + 1,) * 3)
+    ref = oop.bk5(o.basis.diff, o.G, u)
+    ut = torch.as_tensor(u, device="cuda")
+    old = L.nk_bk5_set_variant(8)
+    try:
+        w8 = nk.apply_stiffness_local(ut, m)
+        L.nk_bk5_set_variant(5)
+        w5 = nk.apply_stiffness_local(ut, m)
+    finally:
+        L.nk_bk5_set_variant(old)
+    assert torch.equal(w8, w5)
+    wh = w8.cpu().numpy()
+    assert np.linalg.norm(wh - ref) / np.linalg.norm(ref) < 1e-12
+
+
+@pytest.mark.parametrize("N", [12, 13])
+def test_stage_variant_misaligned_slice(N):
+    """u as an 8-byte-offset slice: the bulk copies start one double early
+    (odd N + 1: every other element; even N + 1: every element, with the
+    16-byte row reads falling back to 8-byte ones)."""
+    from paper_2104_05829_b200._lib import check, lib, ptr
+    L = lib()
+    counts = (3, 2, 3)
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    o = om.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = np.random.default_rng(3 + N).standard_normal((m.E,) + (N + 1,) * 3)
+    ref = oop.bk5(o.basis.diff, o.G, u)
+    buf = torch.zeros(m.n_local + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.as_tensor(u.reshape(-1), device="cuda")
+    w = torch.empty(m.n_local, dtype=torch.float64, device="cuda")
+    old = L.nk_bk5_set_variant(8)
+    try:
+        check(L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), buf.data_ptr() + 8, ptr(w), 1.0,
+                       None, 0.0, 1, m.n_local, None, None, 0, None, None, 0, 0,
+                       torch.cuda.current_stream().cuda_stream), "bk5")
+    finally:
+        L.nk_bk5_set_variant(old)
+    wh = w.cpu().numpy().reshape(ref.shape)
+    assert np.linalg.norm(wh - ref) / np.linalg.norm(ref) < 1e-12
 
 
 def test_variant_errors():
