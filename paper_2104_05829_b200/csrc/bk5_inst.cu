@@ -196,6 +196,7 @@ template <int NQ> struct StageShapes {
   template <> struct StageShapes<NQ_> {                                     \
     static constexpr int G[3] = {g0, g1, g2}, U[3] = {u0, u1, u2}, M[3] = {m0, m1, m2}; \
   };
+NK_SD(8, 6, 2, 5, 6, 2, 4, 6, 2, 3) NK_SD(9, 6, 2, 3, 6, 2, 2, 6, 1, 3)
 NK_SD(10, 6, 2, 2, 6, 1, 3, 4, 2, 3) NK_SD(11, 6, 2, 2, 4, 1, 3, 6, 2, 1)
 NK_SD(12, 6, 2, 1, 4, 1, 3, 6, 2, 2) NK_SD(13, 6, 2, 1, 3, 2, 2, 6, 1, 1)
 NK_SD(14, 6, 2, 1, 2, 2, 2, 6, 1, 1) NK_SD(15, 4, 2, 1, 5, 1, 1, 3, 2, 1)
@@ -328,7 +329,7 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
                                    part_base, reduce_count, s);
     }
   }
-  if constexpr (NQ >= 10 && NQ <= 15) {
+  if constexpr (NQ >= 8 && NQ <= 15) {
     if (variant == 8 && ncomp == 1) {   // TMA-staged operands (bk5_stage.cuh)
       // cstride carries the length of the u array for ncomp = 1 (nk_bk5_batch)
       using SD = StageShapes<NQ>;

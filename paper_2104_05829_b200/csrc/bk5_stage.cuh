@@ -1,5 +1,5 @@
 // BK5 variant 8, "stage": persistent CTAs whose element operands are staged
-// in shared memory by the TMA engine, for the high orders (N + 1 = NQ >= 10).
+// in shared memory by the TMA engine, for the high orders (N + 1 = NQ in 8..15).
 //
 // Why: ncu source-level stall sampling of the register-pencil kernels at
 // N = 12 (bk5_pencil<13>) and N = 15 (bk5_pencil2<16>) puts 48-56% of the
@@ -260,8 +260,14 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       if (bulkw) {
         // w row into the u row (this thread's own row); the element's two
         // edge doubles that fall outside the 16-byte bulk range go direct
+        if (NQ % 2 == 0 && sh == 0) {   // 16-byte stores: even row strides conflict at 8 B
 #pragma unroll
-        for (int i = 0; i < NQ; ++i) urow[i] = res[i];
+          for (int i = 0; i < NQ; i += 2)
+            *reinterpret_cast<double2*>(urow + i) = make_double2(res[i], res[i + 1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) urow[i] = res[i];
+        }
         fence_proxy_async();
         if (t == 0 && sh) w[e * NQ3] = res[0];
         if (t == NQ2 - 1 && ((NQ3 - sh) & 1)) w[e * NQ3 + NQ3 - 1] = res[NQ - 1];

@@ -1,7 +1,7 @@
 // Process-wide BK5 variant selection (nk_bk5_set_variant, include/nekb200.h):
 // 0 auto (the measured per-order table in bk5.cu), 1 k-slab, 3 pencil,
 // 4 pencil-TMA, 5 pencil2, 6 seq3 (3-component batches; scalar calls use
-// the auto table), 7 dmma, 8 stage (TMA-staged operands, N + 1 in 10..15).
+// the auto table), 7 dmma, 8 stage (TMA-staged operands, N + 1 in 8..15).
 #include "common.cuh"
 
 static int g_variant = 0;

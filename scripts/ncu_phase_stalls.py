@@ -34,6 +34,8 @@ hdr = rows[1]; data = [r for r in rows[2:] if len(r) > 5]
 iA=hdr.index("Address"); iS=hdr.index("Warp Stall Sampling (All Samples)"); iI=hdr.index("Instructions Executed")
 stalls=[c for c in hdr if c.startswith("stall_") and "Not Issued" not in c]
 base = int(data[0][iA],16)
+iX = hdr.index("L1 Wavefronts Shared Excessive") if "L1 Wavefronts Shared Excessive" in hdr else None
+iW = hdr.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in hdr else None
 agg = collections.defaultdict(lambda: collections.Counter())
 for r in data:
     off = int(r[iA],16)-base
@@ -43,8 +45,10 @@ for r in data:
         for a,b,n in phases:
             if a <= ln <= b: ph = n
     agg[ph]["samples"] += int(r[iS] or 0); agg[ph]["inst"] += int(r[iI] or 0)
+    if iX is not None:
+        agg[ph]["xwf"] += int(float(r[iX] or 0)); agg[ph]["wf"] += int(float(r[iW] or 0))
     for c in stalls: agg[ph][c] += int(r[hdr.index(c)] or 0)
 tot = sum(a["samples"] for a in agg.values())
 for ph, a in sorted(agg.items(), key=lambda x:-x[1]["samples"]):
     top = sorted(((c.replace("stall_",""), a[c]) for c in stalls), key=lambda x:-x[1])[:5]
-    print(f"{ph:6s} {100*a['samples']/tot:5.1f}% inst {a['inst']:>9d}  " + " ".join(f"{c}:{100*v/max(1,a['samples']):.0f}%" for c,v in top))
+    print(f"{ph:6s} {100*a['samples']/tot:5.1f}% inst {a['inst']:>9d} smem wf {a['wf']:>8d} excess {a['xwf']:>8d}  " + " ".join(f"{c}:{100*v/max(1,a['samples']):.0f}%" for c,v in top))

@@ -46,7 +46,7 @@ def test_select_variant_and_parity(N):
 @pytest.mark.parametrize("variant,N,counts", [
     (7, 8, (3, 2, 2)), (7, 9, (2, 2, 3)), (7, 12, (3, 2, 2)), (7, 13, (2, 3, 1)),
     (7, 14, (2, 2, 2)), (7, 15, (3, 2, 2)),
-    (8, 9, (3, 2, 2)), (8, 10, (2, 2, 3)), (8, 11, (3, 3, 3)), (8, 12, (3, 3, 3)),
+    (8, 7, (3, 2, 2)), (8, 8, (3, 3, 3)), (8, 9, (3, 2, 2)), (8, 10, (2, 2, 3)), (8, 11, (3, 3, 3)), (8, 12, (3, 3, 3)),
     (8, 13, (2, 3, 1)), (8, 14, (3, 3, 1))])
 def test_dmma_variant_parity_fused(variant, N, counts):
     """Variant 7 (FP64 tensor-core contractions, bk5_dmma.cuh) and variant 8
@@ -84,7 +84,8 @@ def test_dmma_variant_parity_fused(variant, N, counts):
         L.nk_bk5_set_variant(old)
 
 
-@pytest.mark.parametrize("N,counts", [(9, (10, 10, 10)), (12, (10, 10, 10)), (13, (9, 9, 9)),
+@pytest.mark.parametrize("N,counts", [(8, (12, 12, 12)), (9, (10, 10, 10)), (12, (10, 10, 10)),
+                                      (13, (9, 9, 9)),
                                       (14, (8, 8, 8))])
 def test_stage_variant_ring_reuse(N, counts):
     """Variant 8 at sizes where every persistent CTA takes several elements
