@@ -329,6 +329,20 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
                                    part_base, reduce_count, s);
     }
   }
+#if NK_BK5_NQ == 16
+  if constexpr (NQ == 16) {
+    if (variant == 8 && ncomp == 1) {   // tensor-map (swizzled) staging (bk5_stage.cuh)
+      if (nblocks) {
+        *nblocks = stage16_grid(nlist);
+        return NK_OK;
+      }
+      // needs 16-byte aligned u, w, G (tensor maps); errors otherwise (the
+      // pencil kernels' 16-byte row loads need the same at even NQ)
+      return launch_stage16(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                            part_base, reduce_count, cstride, s);
+    }
+  }
+#endif
   if constexpr (NQ >= 8 && NQ <= 15) {
     if (variant == 8 && ncomp == 1) {   // TMA-staged operands (bk5_stage.cuh)
       // cstride carries the length of the u array for ncomp = 1 (nk_bk5_batch)

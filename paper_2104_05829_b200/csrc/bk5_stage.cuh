@@ -37,6 +37,9 @@
 // rest are read from global memory after a bulk L2 prefetch issued one
 // element ahead.  HBM per point: u 8 + G 48 + w 8 B (the BK5 roofline).
 #pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "bk5_tma.cuh"
 
 namespace nk {
@@ -342,5 +345,309 @@ static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, u_len);
   return check_launch("bk5_stage");
 }
+
+#if defined(NK_BK5_NQ) && NK_BK5_NQ == 16   // one translation unit owns the N = 15 kernel
+// ---------------------------------------------------------------------------
+// N = 15 (NQ = 16): one u row is 128 B, so in the dense image every i-row
+// starts on bank 0 and F1's row reads would conflict 8-way.  u is therefore
+// moved by a 2-D tensor copy (cp.async.bulk.tensor, tensor map of rows of 16
+// doubles, box 16 x 256 = one element) with the 128-byte swizzle: 16-byte
+// chunk c of row r lands at chunk c ^ (r mod 8), which makes i-rows (16-byte
+// accesses), j- and k-columns (8-byte accesses) all conflict-free.  Shared
+// memory (227 KB) holds two u buffers (64 KB), S (32 KB) and four of the six
+// G components (128 KB): R lives in the current u buffer (u is dead after
+// F1-F3, so ur is written there after one extra barrier), and w is assembled
+// there too and leaves by a tensor store with the same swizzle.  G
+// components 4 and 5 come from global memory after an L2 prefetch one
+// element ahead.
+struct Stage16 {
+  static constexpr int NQ = 16, NQ2 = 256, NQ3 = 4096, NGS = 4;
+  static constexpr int THREADS = NQ2;
+  // (bytes) align slack | U0 | U1 | G[NGS] | S | red[32] | 3 mbarriers
+  static size_t smem_bytes() {
+    return 1024 + sizeof(double) * ((size_t)2 * NQ3 + NGS * NQ3 + NQ3 + 32) + 3 * sizeof(uint64_t);
+  }
+  // swizzled element (row r = k*16 + j, column i) of a u / R / w buffer
+  __device__ __forceinline__ static int sw(int r, int i) {
+    return r * 16 + ((((i >> 1) ^ (r & 7))) << 1) + (i & 1);
+  }
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y,
+                                             const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256, 1)
+bk5_stage16(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<16> D,
+            const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmw,
+            const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
+            double lam0, const double* __restrict__ B, double lam1,
+            const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
+            int64_t part_base, int64_t reduce_count) {
+  using C = Stage16;
+  using L = PencilLayout<16>;
+  constexpr int NQ = 16, NQ2 = C::NQ2, NQ3 = C::NQ3, NGS = C::NGS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (st != nullptr && st->done) return;
+  double* Ub0 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                          ~uintptr_t(1023));
+  double* Gb = Ub0 + 2 * NQ3;
+  double* Ss = Gb + NGS * NQ3;
+  double* red = Ss + NQ3;
+  uint64_t* ubar = reinterpret_cast<uint64_t*>(red + 32);   // [2]
+  uint64_t* gbar = ubar + 2;
+
+  const int t = threadIdx.x;
+  const int a = t & 15, b = t >> 4;
+  const int64_t stride = gridDim.x;
+  auto elem_of = [&](int64_t slot) -> int64_t { return elist ? (int64_t)elist[slot] : slot; };
+  auto issue_u = [&](int64_t slot, int bi) {
+    mbar_expect_tx(&ubar[bi], NQ3 * sizeof(double));
+    tma_load_2d(Ub0 + bi * NQ3, &tmu, 0, (int)(elem_of(slot) * NQ2), &ubar[bi]);
+  };
+  auto issue_g = [&](int64_t slot) {
+    const double* src = G + elem_of(slot) * 6 * NQ3;
+    mbar_expect_tx(gbar, NGS * NQ3 * sizeof(double));
+    tma_load_1d(Gb, src, NGS * NQ3 * sizeof(double), gbar);
+    prefetch_l2(src + NGS * NQ3, (int64_t)(6 - NGS) * NQ3 * sizeof(double));
+  };
+  if (t == 0) {
+    mbar_init(&ubar[0], 1);
+    mbar_init(&ubar[1], 1);
+    mbar_init(gbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0 && (int64_t)blockIdx.x < nlist) {
+    issue_u(blockIdx.x, 0);
+    issue_g(blockIdx.x);
+  }
+
+  double dot = 0.0;
+  int it = 0;
+  for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++it) {
+    const int64_t e = elem_of(slot);
+    const int bi = it & 1;
+    double* Uc = Ub0 + bi * NQ3;
+    if (t == 0 && slot + stride < nlist) {
+      bulk_wait_read0();   // the other buffer's w (previous element) has left
+      issue_u(slot + stride, bi ^ 1);
+    }
+    mbar_wait(&ubar[bi], (it >> 1) & 1);
+    double ut[NQ], o1[NQ];
+    {
+      double v[NQ], o[NQ];
+      // ---- F2: j-pencils (i = a, k = b) -> S
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = Uc[C::sw(b * 16 + m, a)];
+      matvec<NQ, false>(D, v, o);
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+      // ---- F3: k-pencils (i = a, j = b) -> ut
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = Uc[C::sw(m * 16 + b, a)];
+      matvec<NQ, false>(D, v, ut);
+      // ---- F1: i-pencils (j = a, k = b) -> o1 (to R = this u buffer after the barrier)
+      const int r = b * 16 + a;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double2 p = *reinterpret_cast<const double2*>(Uc + r * 16 + ((c ^ (r & 7)) << 1));
+        v[2 * c] = p.x;
+        v[2 * c + 1] = p.y;
+      }
+      matvec<NQ, false>(D, v, o1);
+    }
+    __syncthreads();   // (A) every u read done: the buffer becomes R
+    {
+      const int r = b * 16 + a;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<double2*>(Uc + r * 16 + ((c ^ (r & 7)) << 1)) =
+            make_double2(o1[2 * c], o1[2 * c + 1]);
+    }
+    __syncthreads();   // (A2)
+    mbar_wait(gbar, it & 1);
+    double gt[NQ];
+    {  // ---- G: k-pencils (i = a, j = b)
+      const double* gp = G + e * 6 * NQ3 + b * NQ + a;
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const int p = k * NQ2 + b * NQ + a;
+        double g[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          g[c] = c < NGS ? Gb[c * NQ3 + p] : __ldg(gp + c * NQ3 + k * NQ2);
+        const int qr = C::sw(k * 16 + b, a), qs = L::idx(k, b, a);
+        const double ur = Uc[qr], us = Ss[qs];
+        Uc[qr] = g[0] * ur + g[1] * us + g[2] * ut[k];
+        Ss[qs] = g[1] * ur + g[3] * us + g[4] * ut[k];
+        gt[k] = g[2] * ur + g[4] * us + g[5] * ut[k];
+      }
+    }
+    __syncthreads();   // (B) G buffer read for the last time
+    if (t == 0 && slot + stride < nlist) issue_g(slot + stride);
+    {  // ---- B2: j-pencils, in place on their own S column
+      double v[NQ], o[NQ];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) v[m] = Ss[L::idx(b, m, a)];
+      matvec<NQ, true>(D, v, o);
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
+    }
+    __syncthreads();
+    {  // ---- B3: k-pencils, S column += D^T gt
+      double o[NQ];
+      matvec<NQ, true>(D, gt, o);
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const int q = L::idx(k, b, a);
+        Ss[q] = o[k] + Ss[q];
+      }
+    }
+    __syncthreads();
+    {  // ---- B1: i-pencils (j = a, k = b) + epilogue; w row back into R's row
+      const int r = b * 16 + a;
+      double v[NQ], o[NQ];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double2 p = *reinterpret_cast<const double2*>(Uc + r * 16 + ((c ^ (r & 7)) << 1));
+        v[2 * c] = p.x;
+        v[2 * c + 1] = p.y;
+      }
+      matvec<NQ, true>(D, v, o);
+      const int64_t off = e * NQ3 + b * NQ2 + a * NQ;
+      double res[NQ];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) res[i] = lam0 * (o[i] + Ss[L::idx(b, a, i)]);
+      if (B != nullptr || st != nullptr) {
+        double urw[NQ];   // u row from L2 (its buffer now holds R)
+#pragma unroll
+        for (int i = 0; i < NQ; i += 2) {
+          const double2 p = __ldg(reinterpret_cast<const double2*>(u + off + i));
+          urw[i] = p.x;
+          urw[i + 1] = p.y;
+        }
+        if (B != nullptr) {
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) res[i] = fma(lam1 * __ldg(B + off + i), urw[i], res[i]);
+        }
+        if (mask != nullptr) {
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) dot = fma(urw[i], res[i], dot);
+      } else if (mask != nullptr) {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) res[i] = mask[off + i] ? res[i] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<double2*>(Uc + r * 16 + ((c ^ (r & 7)) << 1)) =
+            make_double2(res[2 * c], res[2 * c + 1]);
+      fence_proxy_async();
+    }
+    __syncthreads();   // (C) S free for the next element; w rows in shared
+    if (t == 0) {
+      tma_store_2d(&tmw, 0, (int)(e * NQ2), Uc);
+      bulk_commit();
+    }
+  }
+  if (t == 0) bulk_wait0();
+
+  if (st != nullptr) {
+    double vv[1] = {dot};
+    block_sum<1>(vv, red);
+    if (t == 0) partials[part_base + blockIdx.x] = vv[0];
+    if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
+      double sres[1];
+      reduce_partials<1>(partials, reduce_count, 0, sres, red);
+      if (t == 0) st->pAp = sres[0];
+    }
+  }
+}
+
+// 2-D tensor map over an array of rows of 16 doubles (128 B), box 16 x 256
+// (one N = 15 element), 128-byte swizzle.  cuTensorMapEncodeTiled is fetched
+// through the runtime's driver entry point (no link against libcuda).
+inline int encode_rows16(CUtensorMap* map, const double* base, int64_t ndoubles) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (enc == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || enc == nullptr) {
+      enc = nullptr;
+      set_error("bk5_stage16: cuTensorMapEncodeTiled unavailable");
+      return NK_ERR_CUDA;
+    }
+  }
+  cuuint64_t dims[2] = {16, (cuuint64_t)(ndoubles / 16)};
+  cuuint64_t strides[1] = {16 * sizeof(double)};
+  cuuint32_t box[2] = {16, 256};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("bk5_stage16: tensor map encode failed (%d)", (int)r);
+    return NK_ERR_CUDA;
+  }
+  return NK_OK;
+}
+
+inline int64_t stage16_grid(int64_t nlist) {
+  static int64_t resident = -1;
+  if (resident < 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(bk5_stage16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Stage16::smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_stage16, Stage16::THREADS,
+                                                  Stage16::smem_bytes());
+    resident = (int64_t)sms * (per > 0 ? per : 1);
+  }
+  return nlist < resident ? nlist : resident;
+}
+
+// u and w must be 16-byte aligned (tensor maps); u_len doubles in u and w.
+inline int launch_stage16(int64_t nlist, const int32_t* elist, const double* Dhost,
+                          const double* G, const double* u, double* w, double lam0,
+                          const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
+                          double* partials, int64_t part_base, int64_t reduce_count,
+                          int64_t u_len, cudaStream_t s) {
+  const int64_t grid = stage16_grid(nlist);
+  if (grid == 0) return NK_OK;
+  if (((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(w) |
+        reinterpret_cast<uintptr_t>(G)) & 15) || (u_len % 16) != 0) {
+    set_error("bk5_stage (N = 15): u, w and G must be 16-byte aligned");
+    return NK_ERR_INVALID;
+  }
+  CUtensorMap tmu, tmw;
+  int rc = encode_rows16(&tmu, u, u_len);
+  if (rc == NK_OK) rc = encode_rows16(&tmw, w, u_len);
+  if (rc != NK_OK) return rc;
+  DParam<16> D;
+  D.set(Dhost);
+  bk5_stage16<<<(unsigned)grid, Stage16::THREADS, Stage16::smem_bytes(), s>>>(
+      nlist, elist, D, tmu, tmw, G, u, w, lam0, B, lam1, mask, st, partials, part_base,
+      reduce_count);
+  return check_launch("bk5_stage16");
+}
+
+#endif  // NK_BK5_NQ == 16
 
 }  // namespace nk
