@@ -34,6 +34,27 @@ for N, counts in ((7, (3, 2, 2)), (4, (2, 2, 2)), (9, (2, 1, 1)), (12, (2, 1, 1)
 torch.cuda.synchronize()
 print("sanitize run ok")
 
+# stage kernel (variant 8, bk5_stage.cuh): persistent CTAs that loop over
+# several elements (u double buffer, G buffer, bulk w stores, the odd-NQ
+# 8-byte phase shift and tail copy, the N = 15 tensor-map path), plain,
+# Helmholtz + mask, the fused p.Ap of the split PCG step
+for N, counts in ((8, (20, 20, 1)), (12, (15, 20, 1)), (12, (3, 3, 3)), (13, (10, 15, 2)),
+                  (15, (10, 16, 2))):
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    L.nk_bk5_set_variant(8)
+    nk.apply_stiffness_local(u, m)
+    nk.apply_helmholtz_local(u, m, 0.5, 2.0)
+    op = nk.PoissonOperator(m)
+    b = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(torch.float64)
+    nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-6, max_iter=3, use_graph=False,
+                split_step=True).solve(b)
+    L.nk_bk5_set_variant(0)
+torch.cuda.synchronize()
+print("sanitize run (stage) ok")
+
 # SURVEY.md §8f kernels: p-multigrid (interp3, cheb_step, dense matvec, the
 # nested coarse PCG + cg_gate), Schwarz (fdm FP64/FP32, schwarz_post, ext gs),
 # projection (multi_wdot, multi_axpy, vscale), the BK5 variant selection
