@@ -5,6 +5,7 @@
 #include "bk5_pencil3.cuh"
 #include "bk5_dmma.cuh"
 #include "bk5_stage.cuh"
+#include "bk5_stage2.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -189,6 +190,7 @@ int runt(int64_t nlist, const int32_t* elist, const double* D, const double* G, 
 // in shared memory, NUB u buffers (2: u(next) issued an element ahead and w
 // bulk-stored), MINB CTAs per SM.  cfg 0 is the default; nk_bk5_tune cfg 21 /
 // 22 select two alternatives for the sweep (scripts/bk5_hot.py --sweep).
+// U = 3: two u buffers with R in the current one (RINU, odd NQ).
 template <int NQ> struct StageShapes {
   static constexpr int G[3] = {6, 6, 6}, U[3] = {2, 1, 2}, M[3] = {1, 1, 1};
 };
@@ -199,19 +201,29 @@ template <int NQ> struct StageShapes {
 NK_SD(8, 6, 2, 5, 6, 2, 4, 6, 2, 3) NK_SD(9, 6, 2, 3, 6, 2, 2, 6, 1, 3)
 NK_SD(10, 6, 2, 2, 6, 1, 3, 4, 2, 3) NK_SD(11, 6, 2, 2, 4, 1, 3, 6, 2, 1)
 NK_SD(12, 6, 2, 1, 4, 1, 3, 6, 2, 2) NK_SD(13, 6, 2, 1, 3, 2, 2, 6, 1, 1)
-NK_SD(14, 6, 2, 1, 2, 2, 2, 6, 1, 1) NK_SD(15, 4, 2, 1, 5, 1, 1, 3, 2, 1)
+NK_SD(14, 6, 2, 1, 2, 2, 2, 6, 1, 1) NK_SD(15, 4, 2, 1, 5, 3, 1, 5, 1, 1)
 #undef NK_SD
+
+// bk5_stage2 (variant 9, two threads per pencil): (NGS, MINB) per order
+template <int NQ> struct Stage2Shape { static constexpr int G = 6, M = 1; };
+#define NK_S2(NQ_, g, m) \
+  template <> struct Stage2Shape<NQ_> { static constexpr int G = g, M = m; };
+NK_S2(9, 6, 2) NK_S2(10, 6, 2) NK_S2(11, 6, 2) NK_S2(12, 6, 1) NK_S2(13, 6, 1) NK_S2(14, 6, 1)
+NK_S2(15, 4, 1)
+#undef NK_S2
 
 template <int NQ, int NGS, int NUB, int MINB>
 int runs(int64_t nlist, const int32_t* elist, const double* D, const double* G, const double* u,
          double* w, double lam0, const double* B, double lam1, const uint8_t* mask,
          nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
          int64_t u_len, cudaStream_t s, int64_t* nblocks) {
+  constexpr int NB = NUB == 3 ? 2 : NUB;
+  constexpr bool RINU = NUB == 3;
   if (nblocks) {
-    *nblocks = stage_grid<NQ, NGS, NUB, MINB>(nlist);
+    *nblocks = stage_grid<NQ, NGS, NB, MINB, RINU>(nlist);
     return NK_OK;
   }
-  return launch_stage<NQ, NGS, NUB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+  return launch_stage<NQ, NGS, NB, MINB, RINU>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
                                      part_base, reduce_count, u_len, s);
 }
 
@@ -343,6 +355,17 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
     }
   }
 #endif
+  if constexpr (NQ >= 9 && NQ <= 15) {
+    if (variant == 9 && ncomp == 1) {   // stage with two threads per pencil (bk5_stage2.cuh)
+      using S2 = Stage2Shape<NQ>;
+      if (nblocks) {
+        *nblocks = stage2_grid<NQ, S2::G, S2::M>(nlist);
+        return NK_OK;
+      }
+      return launch_stage2<NQ, S2::G, S2::M>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st,
+                                             partials, part_base, reduce_count, cstride, s);
+    }
+  }
   if constexpr (NQ >= 8 && NQ <= 15) {
     if (variant == 8 && ncomp == 1) {   // TMA-staged operands (bk5_stage.cuh)
       // cstride carries the length of the u array for ncomp = 1 (nk_bk5_batch)

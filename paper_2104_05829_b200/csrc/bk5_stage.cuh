@@ -67,10 +67,15 @@ __device__ __forceinline__ void fence_proxy_async() {
 // assembled in its own u buffer after B1 and written back by one bulk store
 // (cp.async.bulk.global.shared, SASS UBLKCP) instead of 13-16 strided 8-byte
 // stores per thread.  NUB = 1: one u buffer, refilled after F3.
-template <int NQ, int NGS, int NUB>
+// RINU (odd NQ, NUB = 2): R lives in the current u buffer -- u is dead once
+// F1..F3 have read it, so ur is written there after one extra barrier (the
+// dense odd-NQ u image IS the pencil layout).  Saves one element buffer,
+// which buys a fifth staged G component at NQ = 15.
+template <int NQ, int NGS, int NUB, bool RINU = false>
 struct StageCfg {
   static_assert(NGS >= 1 && NGS <= 6, "NGS");
   static_assert(NUB == 1 || NUB == 2, "NUB");
+  static_assert(!RINU || (NQ % 2 == 1 && NUB == 2), "R in the u buffer: odd NQ, two u buffers");
   static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
   static constexpr int VOL = PencilLayout<NQ>::VOL;
   static constexpr int UB = (NQ3 + 2 + 1) & ~1;         // doubles, even: 16-B aligned next
@@ -78,12 +83,12 @@ struct StageCfg {
   static constexpr int THREADS = NQ2;
   // layout (doubles): U[NUB] | G | R | S | red[32] ; mbarriers u[NUB], g
   static size_t smem_bytes() {
-    return sizeof(double) * ((size_t)NUB * UB + GBUF + 2 * VOL + 32) +
+    return sizeof(double) * ((size_t)NUB * UB + GBUF + (RINU ? 1 : 2) * VOL + 32) +
            (NUB + 1) * sizeof(uint64_t);
   }
 };
 
-template <int NQ, int NGS, int NUB, int MINB>
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false>
 __global__ void __launch_bounds__(NQ * NQ, MINB)
 bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
           const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
@@ -91,14 +96,14 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
           const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
           int64_t part_base, int64_t reduce_count, int64_t u_len) {
   using L = PencilLayout<NQ>;
-  using C = StageCfg<NQ, NGS, NUB>;
+  using C = StageCfg<NQ, NGS, NUB, RINU>;
   constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL;
   extern __shared__ __align__(128) double smem[];
   if (st != nullptr && st->done) return;
   double* Ub0 = smem;
   double* Gb = Ub0 + NUB * C::UB;
-  double* Rr = Gb + C::GBUF;
-  double* Ss = Rr + VOL;
+  double* Rfix = Gb + C::GBUF;                 // (RINU: unused)
+  double* Ss = RINU ? Rfix : Rfix + VOL;
   double* red = Ss + VOL;
   uint64_t* ubar = reinterpret_cast<uint64_t*>(red + 32);   // [NUB]
   uint64_t* gbar = ubar + NUB;
@@ -157,13 +162,14 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     const int sh = phase_of(e);
     const int bi = NUB == 2 ? (it & 1) : 0;
     double* uS = Ub0 + bi * C::UB + sh;
+    double* Rr = RINU ? uS : Rfix;
     if (NUB == 2 && t == 0 && slot + stride < nlist) {
       bulk_wait_read0();             // the other buffer's w (previous element) has left
       issue_u(slot + stride, bi ^ 1);
     }
     mbar_wait(&ubar[bi], NUB == 2 ? ((it >> 1) & 1) : (it & 1));
-    double ut[NQ];
-    {  // ---- F1: i-pencils (j = a, k = b) -> R
+    double ut[NQ], o1[NQ];
+    {  // ---- F1: i-pencils (j = a, k = b) -> R (RINU: o1, written after (A))
       double v[NQ], o[NQ];
       const double* row = uS + b * NQ2 + a * NQ;
       if (NQ % 2 == 0 && sh == 0) {   // 16-byte rows (sh = 1 only for a misaligned u slice)
@@ -177,9 +183,13 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
 #pragma unroll
         for (int m = 0; m < NQ; ++m) v[m] = row[m];
       }
-      matvec<NQ, false>(D, v, o);
+      if (RINU) {
+        matvec<NQ, false>(D, v, o1);
+      } else {
+        matvec<NQ, false>(D, v, o);
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
+        for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
+      }
       // ---- F2: j-pencils (i = a, k = b) -> S
 #pragma unroll
       for (int m = 0; m < NQ; ++m) v[m] = uS[b * NQ2 + m * NQ + a];
@@ -193,6 +203,11 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     }
     __syncthreads();   // (A)
     if (NUB == 1 && t == 0 && slot + stride < nlist) issue_u(slot + stride, 0);
+    if (RINU) {   // every u read is done: the buffer becomes R
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o1[i];
+      __syncthreads();   // (A2)
+    }
     mbar_wait(gbar, it & 1);
     double gt[NQ];
     {  // ---- G: k-pencils, pointwise symmetric 3x3
@@ -245,7 +260,7 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       if (B != nullptr || st != nullptr) {
         double urw[NQ];
 #pragma unroll
-        for (int i = 0; i < NQ; ++i) urw[i] = NUB == 2 ? urow[i] : __ldg(u + off + i);
+        for (int i = 0; i < NQ; ++i) urw[i] = (NUB == 2 && !RINU) ? urow[i] : __ldg(u + off + i);
         if (B != nullptr) {
 #pragma unroll
           for (int i = 0; i < NQ; ++i) res[i] = fma(lam1 * __ldg(B + off + i), urw[i], res[i]);
@@ -309,31 +324,31 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
 }
 
 // Grid: persistent, min(nlist, SMs x resident CTAs per SM).
-template <int NQ, int NGS, int NUB, int MINB>
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false>
 static int64_t stage_grid(int64_t nlist) {
   static int64_t resident = -1;
   if (resident < 0) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    using C = StageCfg<NQ, NGS, NUB>;
-    cudaFuncSetAttribute(bk5_stage<NQ, NGS, NUB, MINB>,
+    using C = StageCfg<NQ, NGS, NUB, RINU>;
+    cudaFuncSetAttribute(bk5_stage<NQ, NGS, NUB, MINB, RINU>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_stage<NQ, NGS, NUB, MINB>, C::THREADS,
-                                                  C::smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_stage<NQ, NGS, NUB, MINB, RINU>,
+                                                  C::THREADS, C::smem_bytes());
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
   return nlist < resident ? nlist : resident;
 }
 
 // u_len: doubles in the u array (bounds the 16-byte rounded copies)
-template <int NQ, int NGS, int NUB, int MINB>
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false>
 static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost, const double* G,
                         const double* u, double* w, double lam0, const double* B, double lam1,
                         const uint8_t* mask, nk_cg_state* st, double* partials,
                         int64_t part_base, int64_t reduce_count, int64_t u_len, cudaStream_t s) {
-  using C = StageCfg<NQ, NGS, NUB>;
-  const int64_t grid = stage_grid<NQ, NGS, NUB, MINB>(nlist);
+  using C = StageCfg<NQ, NGS, NUB, RINU>;
+  const int64_t grid = stage_grid<NQ, NGS, NUB, MINB, RINU>(nlist);
   if (grid == 0) return NK_OK;
   if ((reinterpret_cast<uintptr_t>(u) & 7) || (reinterpret_cast<uintptr_t>(G) & 15)) {
     set_error("bk5_stage: u must be 8-byte and G 16-byte aligned");
@@ -341,7 +356,7 @@ static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost
   }
   DParam<NQ> D;
   D.set(Dhost);
-  bk5_stage<NQ, NGS, NUB, MINB><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
+  bk5_stage<NQ, NGS, NUB, MINB, RINU><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, u_len);
   return check_launch("bk5_stage");
 }

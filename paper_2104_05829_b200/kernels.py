@@ -295,7 +295,7 @@ def extract_diagonal(mesh, basis=None, spec="stiffness", gs=None, assemble=True)
 
 # BK5 variants (nk_bk5_set_variant): declaration order = tie-break order
 BK5_VARIANTS = {"kslab": 1, "pencil": 3, "pencil_tma": 4, "pencil2": 5, "seq3": 6, "dmma": 7,
-                "stage": 8}
+                "stage": 8, "stage2": 9}
 _VARIANT_REPORT = []
 
 
@@ -303,7 +303,7 @@ def bk5_variant_eligible(name, N, ncomp=1):
     """Which BK5 variants serve an order (the analogue of SPEC.md:426's
     "N_q=12 -> full3d not eligible"): pencil-TMA needs N+1 in {4, 6, 8};
     dmma (FP64 tensor cores, two 8-row tiles) N+1 in 9..16; stage (TMA-staged
-    operands) N+1 in 8..16; seq3 serves
+    operands) N+1 in 8..16, stage2 N+1 in 9..15; seq3 serves
     3-component batches only."""
     if name not in BK5_VARIANTS:
         return False
@@ -313,6 +313,8 @@ def bk5_variant_eligible(name, N, ncomp=1):
         return ncomp == 1 and 9 <= N + 1 <= 16
     if name == "stage":   # TMA-staged u and G in shared memory (bk5_stage.cuh)
         return ncomp == 1 and 8 <= N + 1 <= 16
+    if name == "stage2":  # stage with two threads per pencil (bk5_stage2.cuh)
+        return ncomp == 1 and 9 <= N + 1 <= 15
     if name == "seq3":   # 3 components back to back per CTA (bk5_pencil NC = 3)
         return ncomp == 3
     return True
