@@ -412,24 +412,37 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
       if ((int64_t)blockIdx.x < nlist) issue(blockIdx.x, 0, pre);
       if ((int64_t)blockIdx.x + stride < nlist) issue(blockIdx.x + stride, 1, pre);
     }
+    // x, r, invD columns (k-pencil, coalesced planes) and the mask row of
+    // an element are loaded into registers one element AHEAD (software
+    // pipelined across the persistent loop), so their L2 latency overlaps
+    // a whole element's contractions instead of the F3 prologue (ncu phase
+    // attribution, profiles/r2zc_*: F3 long-scoreboard 56%).
+    double xv[NQ], rv[NQ], dv[NQ];
+    uint64_t mk = ~0ull;
+    const bool mask8 = NQ == 8 && mask != nullptr && (reinterpret_cast<uintptr_t>(mask) & 7) == 0;
+    auto load_vec = [&](int64_t slot, double (&xo)[NQ], double (&ro)[NQ], double (&dvo)[NQ],
+                        uint64_t& mo) {
+      const int64_t e = elem_of(slot);
+      if (it > 0) {
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          const int64_t q = e * NQ3 + k * NQ2 + t;
+          xo[k] = ld_hint(x + q, pol_s);
+          ro[k] = ldg_hint(r + q, pol_r);
+          dvo[k] = ldg_hint(invD + q, pol_d);
+        }
+      }
+      if (mask8)   // the B1 row (j = a, k = b): 8 bytes
+        mo = __ldg(reinterpret_cast<const unsigned long long*>(mask + e * NQ3 + b * NQ2 +
+                                                               a * NQ));
+    };
+    if ((int64_t)blockIdx.x < nlist) load_vec(blockIdx.x, xv, rv, dv, mk);
     int itl = 0;
     for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++itl) {
       const int s = itl & 1;
       double* su = stage0 + s * STAGE;
       const double* sg = su + NQ3;
       const int64_t e = elem_of(slot);
-      // x, r, invD columns (k-pencil, coalesced planes): issued before the
-      // barrier wait so their latency overlaps the TMA completion
-      double xv[NQ], rv[NQ], dv[NQ];
-      if (it > 0) {
-#pragma unroll
-        for (int k = 0; k < NQ; ++k) {
-          const int64_t q = e * NQ3 + k * NQ2 + t;
-          xv[k] = ld_hint(x + q, pol_s);
-          rv[k] = ldg_hint(r + q, pol_r);
-          dv[k] = ldg_hint(invD + q, pol_d);
-        }
-      }
       mbar_wait(&bar[s], (itl >> 1) & 1);
 
       // ---- F3 + prologue: k-pencils (i = a, j = b)
@@ -444,19 +457,22 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
             st_hint(x + e * NQ3 + pp, fma(alpha_prev, pv, xv[k]), pol_s);
             pv = fma(beta, pv, dv[k] * rv[k]);
             st_hint(p + e * NQ3 + pp, pv, pol_s);
-            su[pp] = pv;
           }
           v[k] = pv;
           U[L::idx(k, b, a)] = pv;
         }
         matvec<NQ, false>(D, v, ut);
       }
+      // the next element's vectors: in flight for the rest of this element
+      uint64_t mk_next = ~0ull;
+      if (slot + stride < nlist) load_vec(slot + stride, xv, rv, dv, mk_next);
       __syncthreads();
+      double prow[NQ];   // p row (j = a, k = b): F1's input, B1's dot and mass term
       {  // F1 (i-pencils) -> R ; F2 (j-pencils) -> S
         double v[NQ], o[NQ];
 #pragma unroll
-        for (int m = 0; m < NQ; ++m) v[m] = U[L::idx(b, a, m)];
-        matvec<NQ, false>(D, v, o);
+        for (int m = 0; m < NQ; ++m) prow[m] = U[L::idx(b, a, m)];
+        matvec<NQ, false>(D, prow, o);
 #pragma unroll
         for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
 #pragma unroll
@@ -503,13 +519,16 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
         for (int m = 0; m < NQ; ++m) v[m] = Rr[L::idx(b, a, m)];
         matvec<NQ, true>(D, v, o);
         const int64_t off = e * NQ3 + b * NQ2 + a * NQ;
-        const double* prow = su + b * NQ2 + a * NQ;
         double res[NQ];
 #pragma unroll
         for (int i = 0; i < NQ; ++i) {
           double vv = lam0 * (o[i] + U[L::idx(b, a, i)]);
           if (B != nullptr) vv = fma(lam1 * __ldg(B + off + i), prow[i], vv);
-          if (mask != nullptr) vv = ldg_u8_hint(mask + off + i, pol_s) ? vv : 0.0;
+          if (mask != nullptr) {
+            const bool keep = mask8 ? ((mk >> (8 * i)) & 0xff) != 0
+                                    : ldg_u8_hint(mask + off + i, pol_s) != 0;
+            vv = keep ? vv : 0.0;
+          }
           res[i] = vv;
           dot = fma(prow[i], vv, dot);
         }
@@ -519,12 +538,8 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
           st2_hint(wr + i, make_double2(res[i], res[i + 1]), pol_r);
       }
       __syncthreads();
-      if (t == 0 && slot + 2 * stride < nlist) {
-        // the stage was written through the generic proxy (p_k); order those
-        // writes before the async-proxy (TMA) refill of the same bytes
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(slot + 2 * stride, s, false);
-      }
+      mk = mk_next;
+      if (t == 0 && slot + 2 * stride < nlist) issue(slot + 2 * stride, s, false);
     }
   }
 

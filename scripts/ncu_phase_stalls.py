@@ -10,6 +10,7 @@ call site).  Phases are line ranges of the kernel source.
         [start:end:NAME,...]
 
 kernel.sass: nvdisasm -gi -c of the cubin (cuobjdump -xelf all build/obj/bk5_nqXX.o).
+NCU_KERNEL=<regex> selects one kernel of a multi-kernel report.
 """
 import csv, io, re, subprocess, sys, collections
 rep, sassf, fname = sys.argv[1], sys.argv[2], sys.argv[3]
@@ -28,7 +29,9 @@ for l in lines[start+1:]:
     if m: cur = int(m.group(1)); continue
     m = re.search(r'/\*([0-9a-f]{4,})\*/', l)
     if m: off2line[int(m.group(1),16)] = cur
-out = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","sass"],capture_output=True,text=True).stdout
+import os
+flt = ["--kernel-name", "regex:" + os.environ["NCU_KERNEL"]] if os.environ.get("NCU_KERNEL") else []
+out = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","sass"] + flt,capture_output=True,text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]; data = [r for r in rows[2:] if len(r) > 5]
 iA=hdr.index("Address"); iS=hdr.index("Warp Stall Sampling (All Samples)"); iI=hdr.index("Instructions Executed")
