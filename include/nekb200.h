@@ -205,8 +205,14 @@ int nk_bk5_tune(int cfg, int pf_dist);
  *     bit 4: invD (read twice per iteration) evict_last; bit 8: reserve the
  *     device's maximum persisting-L2 set-aside for the evict_last lines
  *     (cudaLimitPersistingL2CacheSize; released when the bit is cleared).
- *     Bit-identical. */
-enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_COUNT = 3 };
+ *     Bit-identical.
+ *   NK_KNOB_FDM: nk_fdm (FP64) contractions -- 1 = FP64 tensor cores
+ *     (mma.sync m8n8k4, N + 3 <= 16), 0 = the CUDA-core line kernel, 2 =
+ *     (default) the measured winner per order (tensor cores at N = 4, 5,
+ *     9..13).  Same algorithm, sums in a different order (rounding-level
+ *     differences). */
+enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_FDM = 3,
+       NK_KNOB_COUNT = 4 };
 int nk_set_knob(int knob, int value);
 /* the device's maximum persisting-L2 set-aside in bytes (-1: no device). */
 int64_t nk_l2_set_aside_max(void);

@@ -22,7 +22,7 @@ extern "C" int nk_bk5_set_variant(int v) {
 // L2 hints: streamed data evict_first + r / w evict_last (0.1136 -> 0.1101 ms,
 // profiles/r2l_bp5_knobs.jsonl; the persisting set-aside did not help, r2m).
 static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1,
-                                     nk::kL2StreamFirst | nk::kL2ReuseLast};
+                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2};
 
 namespace nk {
 int knob(int k) { return (k >= 0 && k < NK_KNOB_COUNT) ? g_knobs[k] : 0; }

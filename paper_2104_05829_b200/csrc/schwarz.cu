@@ -15,9 +15,17 @@
 //   nk_schwarz_post  z = mask * W * (own points of the extended / own
 //                    output) fused with the Chebyshev vector update
 //                    d = a d + b z, e (+)= d.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace nk {
+
+__device__ __forceinline__ void fdm_dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 
 // One thread's 1-D contractions of TWO lines L0, L1 (stride ST) in place:
 //   L[a] = sum_i M[a][i] L[i]   (M rows of length SP in shared memory),
@@ -257,12 +265,240 @@ schwarz_post_kernel(int nq, int64_t n, const double* __restrict__ src, int src_e
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// nk_fdm on the FP64 tensor cores (NK_KNOB_FDM = 1, N + 3 <= 16).
+//
+// Why: the line kernel above is issue/latency-bound at ~24% of the FP64 rate
+// (ncu r2o: short-scoreboard 31%, FP64 pipe 35%, ~0.45 shared-memory
+// instructions per DFMA).  Each direction pass is the small GEMM
+//   C[a][l] = sum_i M[a][i] B[i][l]   (M = S^T forward, S backward; B = the
+//   box's (N+3)^2 lines along that direction)
+// so a warp issues mma.sync.m8n8k4.f64 (SASS DMMA, 256 FMA per instruction)
+// over 8-line tiles: A fragments (M, zero-padded to 16 x 4 KS) stay in
+// registers for the pass, B fragments are one 8-byte shared load per lane
+// and k-step, C goes back in place (the warp owns its tiles' lines for the
+// pass; __syncwarp orders its reads before its writes).  The z pass applies
+// the inverse Kronecker-sum spectrum to the C fragments and runs the backward
+// z product on the same tile.  Padding (rows a >= N+3, k >= N+3, lines past
+// (N+3)^2) is zero in A and predicated off in B / C.  Box layout: line stride
+// LS and plane stride PS = 4 (mod 16) doubles, so one B-fragment load (4
+// consecutive k of 8 lines) hits every bank exactly twice in the x and y
+// passes.  4 warps per element (CTA).
+template <int NQE>
+struct FdmDmmaShape {
+  static constexpr int NQ = NQE - 2;
+  static constexpr int LS = NQE <= 4 ? 4 : 20;
+  static constexpr int PS0 = NQE * LS;
+  static constexpr int PS = PS0 + ((4 - PS0 % 16) + 16) % 16;
+  static constexpr int KS = (NQE + 3) / 4, MT = (NQE + 7) / 8;
+  static constexpr int NL = NQE * NQE, NTILE = (NL + 7) / 8;
+  static constexpr int NW = 4, THREADS = 32 * NW;
+  static constexpr int A_SZ = NQE * PS;
+  // A | S | lambda | lab[NL] (x + y eigenvalue sum of each z line) | base[3][NL] (ints)
+  static constexpr size_t SMEM =
+      sizeof(double) * (A_SZ + 3 * NQE * NQE + 3 * NQE + NL) + sizeof(int) * 3 * NL;
+};
+
+template <int NQE>
+__global__ void __launch_bounds__(FdmDmmaShape<NQE>::THREADS)
+fdm_dmma_kernel(int64_t nelem, const double* __restrict__ r, const double* __restrict__ sub,
+                const double* __restrict__ rx, double* __restrict__ res_out,
+                const int32_t* __restrict__ fmap, const double* __restrict__ Sg,
+                const double* __restrict__ lamg, double lam0, double lam1,
+                double* __restrict__ out, int out_ext, const nk_cg_state* st) {
+  static_assert(NQE <= 16, "two 8-row m tiles");
+  if (st != nullptr && st->done) return;
+  using F = FdmDmmaShape<NQE>;
+  constexpr int NQ = F::NQ, NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
+  constexpr int LS = F::LS, PS = F::PS, KS = F::KS, MT = F::MT, NL = F::NL, NT = F::THREADS;
+  extern __shared__ __align__(16) double fdm_dsmem[];
+  double* A = fdm_dsmem;              // [k][j][i] at k*PS + j*LS + i
+  double* Sm = A + F::A_SZ;           // S[d][i][a] as stored
+  double* Ls = Sm + 3 * NQE * NQE;    // lambda[d][mode]
+  double* lab = Ls + 3 * NQE;         // z line l = (j, i): lambda_x[i] + lambda_y[j]
+  int* lbase = reinterpret_cast<int*>(lab + NL);   // [dir][line] -> A offset of k = 0
+  const int64_t e = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wq = t >> 5;
+  const double* Se = Sg + e * 3 * NQE * NQE;
+  const int64_t ob = e * NQ3;
+  const int32_t* fm = fmap + e * 6 * NQ2;
+  for (int q = t; q < 3 * NQE * NQE; q += NT) Sm[q] = __ldg(Se + q);
+  for (int q = t; q < 3 * NQE; q += NT) Ls[q] = __ldg(lamg + e * 3 * NQE + q);
+  for (int q = t; q < F::A_SZ; q += NT) A[q] = 0.0;
+  for (int l = t; l < NL; l += NT) {
+    const int h = l / NQE, o = l - h * NQE;
+    lbase[l] = h * PS + o * LS;            // x lines (k = h, j = o) along i
+    lbase[NL + l] = h * PS + o;            // y lines (k = h, i = o) along j
+    lbase[2 * NL + l] = h * LS + o;        // z lines (j = h, i = o) along k
+  }
+  __syncthreads();
+  for (int l = t; l < NL; l += NT) {
+    const int h = l / NQE, o = l - h * NQE;
+    lab[l] = Ls[o] + Ls[NQE + h];
+  }
+  constexpr int CH = 8;
+  for (int q0 = 0; q0 < NQ3; q0 += CH * NT) {   // own points, res_out = r - sub
+    double v[CH], w[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      v[u] = q < NQ3 ? __ldg(r + ob + q) : 0.0;
+      w[u] = (sub != nullptr && q < NQ3) ? __ldg(sub + ob + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      if (q < NQ3) {
+        const int i = q % NQ, j = (q / NQ) % NQ, k = q / NQ2;
+        const double x = v[u] - w[u];
+        if (res_out) res_out[ob + q] = x;
+        A[(k + 1) * PS + (j + 1) * LS + (i + 1)] = x;
+      }
+    }
+  }
+  constexpr int NF = 6 * NQ2;
+  for (int q0 = 0; q0 < NF; q0 += CH * NT) {    // face-neighbour layers (as fdm_kernel)
+    int32_t src[CH];
+    double v[CH], w[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      src[u] = q < NF ? __ldg(fm + q) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      v[u] = src[u] >= 0 ? __ldg(r + src[u]) : (src[u] <= -2 ? __ldg(rx - src[u] - 2) : 0.0);
+      w[u] = (sub != nullptr && src[u] >= 0) ? __ldg(sub + src[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int q = q0 + u * NT + t;
+      if (src[u] != -1) {
+        const int f = q / NQ2, ab = q % NQ2, a = ab / NQ + 1, b = ab % NQ + 1;
+        const int pos = (f & 1) ? NQE - 1 : 0;
+        int idx;
+        if (f < 2) idx = a * PS + b * LS + pos;
+        else if (f < 4) idx = a * PS + pos * LS + b;
+        else idx = pos * PS + a * LS + b;
+        A[idx] = v[u] - w[u];
+      }
+    }
+  }
+  __syncthreads();
+
+  auto base_of = [&](int dir, int l) -> int { return lbase[dir * NL + l]; };
+  auto frags = [&](int dir, bool fwd, double (&af)[MT][KS]) {
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int a = mt * 8 + (lane >> 2), i = ks * 4 + (lane & 3);
+        const double* S = Sm + dir * NQE * NQE;
+        af[mt][ks] = (a < NQE && i < NQE) ? (fwd ? S[i * NQE + a] : S[a * NQE + i]) : 0.0;
+      }
+  };
+  // one tile: C = M B over the tile's 8 lines (B read from A), optional
+  // spectrum scaling, written back in place
+  auto tile = [&](int dir, int st_, int nt, const double (&af)[MT][KS], bool scale) {
+    const int lb = nt * 8 + (lane >> 2);
+    const int bb = lb < NL ? base_of(dir, lb) : 0;
+    double c[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int i = ks * 4 + (lane & 3);
+      const double bv = (lb < NL && i < NQE) ? A[bb + i * st_] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) fdm_dmma884(c[mt][0], c[mt][1], af[mt][ks], bv);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int a = mt * 8 + (lane >> 2), l = nt * 8 + 2 * (lane & 3) + hh;
+        if (a < NQE && l < NL) {
+          double val = c[mt][hh];
+          if (scale) {
+            const double l0 = lab[l] + Ls[2 * NQE + a];
+            val = isinf(l0) ? 0.0 : val * fdm_rcp(fma(lam0, l0, lam1));
+          }
+          A[base_of(dir, l) + a * st_] = val;
+        }
+      }
+    __syncwarp();
+  };
+  {
+    double af[MT][KS];
+    frags(0, true, af);   // forward x (along i)
+    for (int nt = wq; nt < F::NTILE; nt += F::NW) tile(0, 1, nt, af, false);
+    __syncthreads();
+    frags(1, true, af);   // forward y (along j)
+    for (int nt = wq; nt < F::NTILE; nt += F::NW) tile(1, LS, nt, af, false);
+    __syncthreads();
+    double ab[MT][KS];    // z: forward, spectrum, backward on the same tile
+    frags(2, true, af);
+    frags(2, false, ab);
+    for (int nt = wq; nt < F::NTILE; nt += F::NW) {
+      tile(2, PS, nt, af, true);
+      tile(2, PS, nt, ab, false);
+    }
+    __syncthreads();
+    frags(1, false, af);  // backward y, backward x
+    for (int nt = wq; nt < F::NTILE; nt += F::NW) tile(1, LS, nt, af, false);
+    __syncthreads();
+    frags(0, false, af);
+    for (int nt = wq; nt < F::NTILE; nt += F::NW) tile(0, 1, nt, af, false);
+    __syncthreads();
+  }
+  if (out_ext) {
+    double* o = out + e * NQE * NQE * NQE;
+    for (int rw = t; rw < NQE * NQE; rw += NT) {
+      const double* srow = A + (rw / NQE) * PS + (rw % NQE) * LS;
+#pragma unroll
+      for (int i = 0; i < NQE; ++i) o[rw * NQE + i] = srow[i];
+    }
+  } else {
+    for (int q = t; q < NQ3; q += NT) {
+      const int i = q % NQ, j = (q / NQ) % NQ, k = q / NQ2;
+      out[ob + q] = A[(k + 1) * PS + (j + 1) * LS + (i + 1)];
+    }
+  }
+}
+
 template <int NQE, typename T>
 static int launch_fdm(int64_t E, const double* r, const double* sub, const double* rx,
                       double* res_out,
                       const int32_t* fmap, const T* S, const T* lam, double lam0,
                       double lam1, double* out, int out_ext, const nk_cg_state* st,
                       cudaStream_t s) {
+  if constexpr (std::is_same<T, double>::value && NQE <= 16) {
+    // 2 = auto: the tensor-core path where it measured faster (scripts/prof_fdm.py
+    // --fdm-knob, E = 16^3, profiles/r2zd_fdm_knob_sweep.jsonl): N + 3 a multiple
+    // of 4 or >= 13 (1.05-1.62x); the 16 x 12 padding of the 10 x 10 operator
+    // makes it lose at N = 7 (0.86x), and N <= 3 / 6 / 8 tie or lose
+    const int kn = knob(NK_KNOB_FDM);
+    const bool tc = kn == 1 || (kn == 2 && (NQE == 7 || NQE == 8 || NQE >= 12));
+    if (tc) {
+      constexpr size_t dsmem = FdmDmmaShape<NQE>::SMEM;
+      static bool dconf = false;
+      if (!dconf) {
+        cudaError_t err = cudaFuncSetAttribute(fdm_dmma_kernel<NQE>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)dsmem);
+        if (err != cudaSuccess) {
+          set_error("fdm_dmma: smem attribute: %s", cudaGetErrorString(err));
+          return NK_ERR_CUDA;
+        }
+        dconf = true;
+      }
+      fdm_dmma_kernel<NQE><<<(unsigned)E, FdmDmmaShape<NQE>::THREADS, dsmem, s>>>(
+          E, r, sub, rx, res_out, fmap, S, lam, lam0, lam1, out, out_ext, st);
+      return check_launch("fdm_dmma");
+    }
+  }
   constexpr size_t smem = FdmShape<NQE, T>::SMEM;
   static bool configured = false;
   if (!configured) {

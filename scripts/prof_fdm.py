@@ -21,9 +21,14 @@ def main():
     ap.add_argument("--kind", default="asm")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--precision", type=int, default=64)
+    ap.add_argument("--fdm-knob", type=int, default=None,
+                    help="NK_KNOB_FDM: 1 FP64 tensor cores, 0 CUDA-core line kernel")
     args = ap.parse_args()
     import torch
     import paper_2104_05829_b200 as nk
+    if args.fdm_knob is not None:
+        from paper_2104_05829_b200._lib import lib
+        lib().nk_set_knob(3, args.fdm_knob)
     N = args.order
     m = nk.build_box_mesh((1, 1, 1), tuple(args.counts), N, deformation=("sine", 0.05))
     op = nk.PoissonOperator(m)
@@ -47,6 +52,7 @@ def main():
     t_app = ev[1].elapsed_time(ev[2]) / args.reps
     nqe = N + 3
     print(json.dumps({"E": m.E, "N": N, "kind": args.kind, "precision": args.precision,
+                      "fdm_knob": args.fdm_knob,
                       "fdm_ms": round(t_fdm, 4),
                       "apply_ms": round(t_app, 4),
                       "fdm_gflops": round(12 * m.E * nqe ** 4 / t_fdm * 1e-6, 1)}))

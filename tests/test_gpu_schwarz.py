@@ -66,6 +66,35 @@ def test_fdm_local_solve_matches_oracle(counts, N, bc):
     assert not torch.any(nk.fdm_local_solve(sm, torch.zeros_like(dev(r))))
 
 
+@pytest.mark.parametrize("counts,N,bc", [((3, 2, 2), 1, "dirichlet"), ((2, 3, 2), 5, "periodic"),
+                                         ((3, 3, 3), 7, "dirichlet"), ((2, 1, 2), 7, "neumann"),
+                                         ((2, 2, 1), 12, "dirichlet"), ((1, 2, 2), 13, "dirichlet")])
+def test_fdm_tensor_core_path_matches_line_kernel(counts, N, bc):
+    """NK_KNOB_FDM: the FP64 tensor-core FDM (mma.sync m8n8k4, N + 3 <= 16)
+    against the CUDA-core line kernel on the same extended boxes -- the same
+    algorithm with sums in a different order (1e-13), ASM and RAS outputs."""
+    from paper_2104_05829_b200._lib import lib
+    L = lib()
+    m, o, op, f = pair(counts, N, bc=bc, lam0=0.8, lam1=(0.0 if bc == "dirichlet" else 2.5))
+    r = dev(assembled_random(o, 7 + N))
+    outs = {}
+    try:
+        for kn in (0, 1):
+            L.nk_set_knob(3, kn)
+            for kind in ("asm", "ras"):
+                sm = nk.SchwarzSmoother(op, kind)
+                outs[(kn, kind, "fdm")] = nk.fdm_local_solve(sm, r).cpu().numpy()
+                z = torch.empty_like(r)
+                sm.apply(r, z)
+                outs[(kn, kind, "apply")] = z.cpu().numpy()
+    finally:
+        L.nk_set_knob(3, 2)
+    for kind in ("asm", "ras"):
+        for what in ("fdm", "apply"):
+            a, b = outs[(1, kind, what)], outs[(0, kind, what)]
+            assert rel_l2(a, b) < 1e-13, (kind, what)
+
+
 @pytest.mark.parametrize("kind", ["asm", "ras"])
 @pytest.mark.parametrize("counts,N,bc", CASES)
 def test_schwarz_smooth_matches_oracle(kind, counts, N, bc):
