@@ -65,7 +65,7 @@ int runp(int64_t nlist, const int32_t* elist, const double* D, const double* G, 
          nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
          cudaStream_t s, int64_t* nblocks, int pfG) {
   if (nblocks) {
-    *nblocks = (nlist + EPB - 1) / EPB;
+    *nblocks = pencil_dot_blocks<NQ, EPB, MINB>(nlist);
     return NK_OK;
   }
   return launch_pencil<NQ, EPB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
@@ -116,7 +116,7 @@ int run_pencil2(int cfg, int64_t nlist, const int32_t* elist, const double* D, c
 #define NK_P2ALT(K)                                                                           \
   if (cfg == 11 + K) {                                                                        \
     if (nb) {                                                                                 \
-      *nb = (nlist + A::E[K] - 1) / A::E[K];                                                  \
+      *nb = pencil2_dot_blocks<NQ, A::E[K], A::M[K]>(nlist);                                   \
       return NK_OK;                                                                           \
     }                                                                                         \
     return launch_pencil2<NQ, A::E[K], A::M[K]>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, \
@@ -129,7 +129,7 @@ int run_pencil2(int cfg, int64_t nlist, const int32_t* elist, const double* D, c
 #endif
   constexpr int EPB = Pencil2Default<NQ>::EPB, MINB = Pencil2Default<NQ>::MINB;
   if (nb) {
-    *nb = (nlist + EPB - 1) / EPB;
+    *nb = pencil2_dot_blocks<NQ, EPB, MINB>(nlist);
     return NK_OK;
   }
   return launch_pencil2<NQ, EPB, MINB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st,
@@ -190,19 +190,26 @@ int runt(int64_t nlist, const int32_t* elist, const double* D, const double* G, 
 // in shared memory, NUB u buffers (2: u(next) issued an element ahead and w
 // bulk-stored), MINB CTAs per SM.  cfg 0 is the default; nk_bk5_tune cfg 21 /
 // 22 select two alternatives for the sweep (scripts/bk5_hot.py --sweep).
-// U = 3: two u buffers with R in the current one (RINU, odd NQ).
+// U = 3: two u buffers with R in the current one (RINU, odd NQ).  E:
+// elements per CTA (the low orders run several small elements side by side).
 template <int NQ> struct StageShapes {
-  static constexpr int G[3] = {6, 6, 6}, U[3] = {2, 1, 2}, M[3] = {1, 1, 1};
+  static constexpr int G[3] = {6, 6, 6}, U[3] = {2, 1, 2}, M[3] = {1, 1, 1}, E[3] = {1, 1, 1};
 };
-#define NK_SD(NQ_, g0, u0, m0, g1, u1, m1, g2, u2, m2)                      \
-  template <> struct StageShapes<NQ_> {                                     \
-    static constexpr int G[3] = {g0, g1, g2}, U[3] = {u0, u1, u2}, M[3] = {m0, m1, m2}; \
+#define NK_SDE(NQ_, g0, u0, m0, e0, g1, u1, m1, e1, g2, u2, m2, e2)                        \
+  template <> struct StageShapes<NQ_> {                                                   \
+    static constexpr int G[3] = {g0, g1, g2}, U[3] = {u0, u1, u2}, M[3] = {m0, m1, m2},   \
+                         E[3] = {e0, e1, e2};                                             \
   };
+#define NK_SD(NQ_, g0, u0, m0, g1, u1, m1, g2, u2, m2) \
+  NK_SDE(NQ_, g0, u0, m0, 1, g1, u1, m1, 1, g2, u2, m2, 1)
+NK_SDE(3, 6, 2, 4, 16, 6, 2, 2, 32, 6, 2, 8, 8) NK_SDE(5, 6, 2, 4, 5, 6, 2, 5, 4, 6, 2, 2, 8)
+NK_SDE(6, 6, 2, 6, 2, 6, 2, 3, 4, 6, 2, 8, 1) NK_SDE(7, 6, 2, 4, 2, 6, 2, 2, 4, 6, 2, 6, 1)
 NK_SD(8, 6, 2, 5, 6, 2, 4, 6, 2, 3) NK_SD(9, 6, 2, 3, 6, 2, 2, 6, 1, 3)
 NK_SD(10, 6, 2, 2, 6, 1, 3, 4, 2, 3) NK_SD(11, 6, 2, 2, 4, 1, 3, 6, 2, 1)
 NK_SD(12, 6, 2, 1, 4, 1, 3, 6, 2, 2) NK_SD(13, 6, 2, 1, 3, 2, 2, 6, 1, 1)
 NK_SD(14, 6, 2, 1, 2, 2, 2, 6, 1, 1) NK_SD(15, 4, 2, 1, 5, 3, 1, 5, 1, 1)
 #undef NK_SD
+#undef NK_SDE
 
 // bk5_stage2 (variant 9, two threads per pencil): (NGS, MINB) per order
 template <int NQ> struct Stage2Shape { static constexpr int G = 6, M = 1; };
@@ -212,7 +219,7 @@ NK_S2(9, 6, 2) NK_S2(10, 6, 2) NK_S2(11, 6, 2) NK_S2(12, 6, 1) NK_S2(13, 6, 1) N
 NK_S2(15, 4, 1)
 #undef NK_S2
 
-template <int NQ, int NGS, int NUB, int MINB>
+template <int NQ, int NGS, int NUB, int MINB, int EPB>
 int runs(int64_t nlist, const int32_t* elist, const double* D, const double* G, const double* u,
          double* w, double lam0, const double* B, double lam1, const uint8_t* mask,
          nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
@@ -220,10 +227,10 @@ int runs(int64_t nlist, const int32_t* elist, const double* D, const double* G, 
   constexpr int NB = NUB == 3 ? 2 : NUB;
   constexpr bool RINU = NUB == 3;
   if (nblocks) {
-    *nblocks = stage_grid<NQ, NGS, NB, MINB, RINU>(nlist);
+    *nblocks = stage_grid<NQ, NGS, NB, MINB, RINU, EPB>(nlist);
     return NK_OK;
   }
-  return launch_stage<NQ, NGS, NB, MINB, RINU>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+  return launch_stage<NQ, NGS, NB, MINB, RINU, EPB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
                                      part_base, reduce_count, u_len, s);
 }
 
@@ -262,15 +269,20 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
   if constexpr (NQ == 2) {   // N = 1: element per thread unless k-slab is forced
     if (ncomp == 1 && variant != 1) {
       const int64_t nb = (nlist * 8 + kN1PtThreads - 1) / kN1PtThreads;
+      const int64_t nbd = nb < kN1DotBlocks ? nb : kN1DotBlocks;   // fused dot: capped, looped
       if (nblocks) {
-        *nblocks = nb;
+        *nblocks = nbd;
         return NK_OK;
       }
       if (nb == 0) return NK_OK;
       DParam<2> Dp;
       Dp.set(D);
-      bk5_n1<2><<<(unsigned)nb, kN1PtThreads, 0, s>>>(nlist, elist, Dp, G, u, w, lam0, B, lam1,
-                                                    mask, st, partials, part_base, reduce_count);
+      if (st != nullptr)
+        bk5_n1<2, true><<<(unsigned)nbd, kN1PtThreads, 0, s>>>(
+            nlist, elist, Dp, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count);
+      else
+        bk5_n1<2><<<(unsigned)nb, kN1PtThreads, 0, s>>>(nlist, elist, Dp, G, u, w, lam0, B, lam1,
+                                                      mask, st, partials, part_base, reduce_count);
       return check_launch("bk5_n1");
     }
   }
@@ -366,15 +378,15 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
                                              partials, part_base, reduce_count, cstride, s);
     }
   }
-  if constexpr (NQ >= 8 && NQ <= 15) {
+  if constexpr (NQ >= 3 && NQ <= 15 && NQ != 4) {
     if (variant == 8 && ncomp == 1) {   // TMA-staged operands (bk5_stage.cuh)
       // cstride carries the length of the u array for ncomp = 1 (nk_bk5_batch)
       using SD = StageShapes<NQ>;
 #define NK_SARGS nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, \
                  reduce_count, cstride, s, nblocks
-      if (cfg == 21) return runs<NQ, SD::G[1], SD::U[1], SD::M[1]>(NK_SARGS);
-      if (cfg == 22) return runs<NQ, SD::G[2], SD::U[2], SD::M[2]>(NK_SARGS);
-      return runs<NQ, SD::G[0], SD::U[0], SD::M[0]>(NK_SARGS);
+      if (cfg == 21) return runs<NQ, SD::G[1], SD::U[1], SD::M[1], SD::E[1]>(NK_SARGS);
+      if (cfg == 22) return runs<NQ, SD::G[2], SD::U[2], SD::M[2], SD::E[2]>(NK_SARGS);
+      return runs<NQ, SD::G[0], SD::U[0], SD::M[0], SD::E[0]>(NK_SARGS);
 #undef NK_SARGS
     }
   }

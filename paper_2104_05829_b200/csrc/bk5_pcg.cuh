@@ -349,31 +349,40 @@ bk5_n1_pcg(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   }
 }
 
-template <int NQ_ONE>   // = 2
+constexpr int64_t kN1DotBlocks = 1184;   // 8 x 148: one resident wave of 256-thread CTAs
+
+template <int NQ_ONE, bool LOOP = false>   // NQ_ONE = 2
 __global__ void __launch_bounds__(kN1PtThreads)
 bk5_n1(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<2> D,
        const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
        double lam0, const double* __restrict__ B, double lam1, const uint8_t* __restrict__ mask,
        nk_cg_state* st, double* __restrict__ partials, int64_t part_base, int64_t reduce_count) {
+  // LOOP (fused-dot launches): grid-stride over a grid capped at kN1DotBlocks,
+  // so the partials / last-block ticket stay short (an uncapped launch at
+  // E = 96^3 had 27648 partials, ~50 us of same-address atomics).
   __shared__ double red[32];
   if (st != nullptr && st->done) return;
   const int t = threadIdx.x;
-  const int64_t slot = ((int64_t)blockIdx.x * kN1PtThreads + t) >> 3;
   const int q = t & 7;
-  const bool active = slot < nlist;
-  const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
-  const int64_t pt = e * 8 + q;
-  const double pv = active ? __ldg(u + pt) : 0.0;
-  double g[6];
-#pragma unroll
-  for (int c = 0; c < 6; ++c) g[c] = active ? __ldg(G + e * 48 + c * 8 + q) : 0.0;
-  double v = lam0 * n1_point_stiffness(pv, g, D, q);
+  const int64_t nblk = (nlist * 8 + kN1PtThreads - 1) / kN1PtThreads;
   double dot = 0.0;
-  if (active) {
-    if (B != nullptr) v = fma(lam1 * __ldg(B + pt), pv, v);
-    if (mask != nullptr) v = mask[pt] ? v : 0.0;
-    w[pt] = v;
-    dot = pv * v;
+  int once = 0;
+  for (int64_t blk = blockIdx.x; LOOP ? blk < nblk : once < 1; blk += gridDim.x, ++once) {
+    const int64_t slot = (blk * kN1PtThreads + t) >> 3;
+    const bool active = slot < nlist;
+    const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
+    const int64_t pt = e * 8 + q;
+    const double pv = active ? __ldg(u + pt) : 0.0;
+    double g[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) g[c] = active ? __ldg(G + e * 48 + c * 8 + q) : 0.0;
+    double v = lam0 * n1_point_stiffness(pv, g, D, q);
+    if (active) {
+      if (B != nullptr) v = fma(lam1 * __ldg(B + pt), pv, v);
+      if (mask != nullptr) v = mask[pt] ? v : 0.0;
+      w[pt] = v;
+      dot = fma(pv, v, dot);
+    }
   }
   if (st != nullptr) {
     double vv[1] = {dot};

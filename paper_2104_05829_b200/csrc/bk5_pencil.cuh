@@ -107,7 +107,7 @@ __device__ __forceinline__ void matvec(const DParam<NQ>& D, const double (&v)[NQ
 // (L2 prefetch at CTA start) and re-read from L2 by components 1 and 2, so HBM
 // moves 104 B per point for three components instead of 3 x 72, while the
 // register and shared footprint stays that of the scalar kernel.
-template <int NQ, int EPB, int MINB, int NC = 1, bool CDOT = false>
+template <int NQ, int EPB, int MINB, int NC = 1, bool CDOT = false, bool LOOP = false>
 __global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
 bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
            const double* __restrict__ G, const double* __restrict__ u_, double* __restrict__ w_,
@@ -132,9 +132,17 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   double* Rr = U + VOL;
   double* Ss = Rr + VOL;
 
-  const int64_t slot = (int64_t)blockIdx.x * EPB + le;
-  const bool active = slot < nlist;
-  const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
+  // LOOP (fused-dot launches at NQ <= 8, launcher): a capped, grid-stride
+  // grid -- one partial per resident CTA instead of one per element group,
+  // so the last-block ticket and the partial list stay short (thousands of
+  // same-address atomics cost ~3 ns each, profiles/r2zf_bk5_dot_cost.jsonl).
+  // Without LOOP the loop below runs exactly once (and compiles away: a
+  // real loop lets ptxas hoist D-hat's constant-bank operands out of it and
+  // spill at NQ >= 12).
+  const int64_t nblk = (nlist + EPB - 1) / EPB;
+  const int64_t slot0 = (int64_t)blockIdx.x * EPB + le;
+  const bool active0 = slot0 < nlist;
+  const int64_t e0 = active0 ? (elist ? (int64_t)elist[slot0] : slot0) : 0;
   // PDL prologue (static operands only; L2 prefetches cannot go stale):
   // start this element's G (75% of its bytes) streaming into L2 now, so the
   // G-phase loads after F1-F3 hit L2 instead of waiting on HBM.  The done
@@ -147,11 +155,11 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
     for (int c = 0; c < NC; ++c)
       live = live || *reinterpret_cast<volatile const int*>(&st[c].done) == 0;
   }
-  if (live && pfG && active && tt == 0)
-    prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
+  if (live && pfG && active0 && tt == 0)
+    prefetch_l2(G + e0 * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
   // optionally also the element one resident wave ahead
-  if (live && pf_ahead > 0 && tt == 0 && slot + pf_ahead < nlist) {
-    const int64_t ea = elist ? (int64_t)elist[slot + pf_ahead] : slot + pf_ahead;
+  if (live && pf_ahead > 0 && tt == 0 && slot0 + pf_ahead < nlist) {
+    const int64_t ea = elist ? (int64_t)elist[slot0 + pf_ahead] : slot0 + pf_ahead;
     prefetch_l2(G + ea * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
   }
   pdl_wait();
@@ -161,6 +169,18 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
 #pragma unroll
     for (int c = 0; c < NC; ++c) all_done = all_done && st[c].done;
     if (all_done) return;
+  }
+
+  double dot = 0.0;
+  int once = 0;   // LOOP = false: exactly one trip, provable at compile time
+  for (int64_t blk = blockIdx.x; LOOP ? blk < nblk : once < 1; blk += gridDim.x, ++once) {
+  const int64_t slot = blk * EPB + le;
+  const bool active = slot < nlist;
+  const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
+  if (LOOP && blk != blockIdx.x) {
+    __syncthreads();   // the previous group's B1 reads of R / U
+    if (live && pfG && active && tt == 0)
+      prefetch_l2(G + e * 6 * NQ3, 6 * NQ3 * (int64_t)sizeof(double));
   }
   if (pf_ahead > 0 && tt == 0 && slot + pf_ahead < nlist) {
     const int64_t ea = elist ? (int64_t)elist[slot + pf_ahead] : slot + pf_ahead;
@@ -172,7 +192,6 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
       prefetch_l2(u_ + c * cstride + e * NQ3, NQ3 * (int64_t)sizeof(double));
   }
 
-  double dot = 0.0;
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
   const double* u = u_ + c * cstride;
@@ -308,6 +327,7 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
     dot = 0.0;
   }
   }  // components
+  }  // element groups
   if ((NC == 1 || CDOT) && st != nullptr) {
     if (NC == 1) {
       double vv[1] = {dot};
@@ -325,7 +345,37 @@ bk5_pencil(int64_t nlist, const int32_t* __restrict__ elist, const __grid_consta
   }
 }
 
-template <int NQ, int EPB, int MINB, int NC, bool CDOT>
+// Fused-dot (NC = 1) launches at NQ <= 8 run the LOOP instantiation on a
+// grid capped at the resident CTAs; above, the loop would spill (see the
+// kernel) and the element counts are small anyway.
+template <int NQ> struct PencilDotLoop { static constexpr bool value = NQ <= 8; };
+
+// Partials of a fused-dot (NC = 1) pencil launch.
+template <int NQ, int EPB, int MINB>
+static int64_t pencil_dot_blocks(int64_t nlist) {
+  using C = PencilCfg<NQ, EPB, MINB>;
+  constexpr bool LP = PencilDotLoop<NQ>::value;
+  const int64_t nblk = (nlist + EPB - 1) / EPB;
+  if constexpr (!LP) {
+    return nblk;
+  } else {
+  static int64_t resident = -1;
+  if (resident < 0) {
+    const size_t smem = C::smem_bytes();
+    cudaFuncSetAttribute(bk5_pencil<NQ, EPB, MINB, 1, false, LP>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil<NQ, EPB, MINB, 1, false, LP>,
+                                                  C::THREADS, smem);
+    resident = (int64_t)sms * (per > 0 ? per : 1);
+  }
+  return nblk < resident ? nblk : resident;
+  }
+}
+
+template <int NQ, int EPB, int MINB, int NC, bool CDOT, bool LOOP = false>
 static int launch_pencil_k(int64_t nlist, const int32_t* elist, const double* Dhost,
                            const double* G, const double* u, double* w, double lam0,
                            const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
@@ -342,12 +392,18 @@ static int launch_pencil(int64_t nlist, const int32_t* elist, const double* Dhos
     return launch_pencil_k<NQ, EPB, MINB, NC, (NC > 1)>(nlist, elist, Dhost, G, u, w, lam0, B,
                                                        lam1, mask, st, partials, part_base,
                                                        reduce_count, s, pfG, cstride, pstride);
+  if constexpr (NC == 1 && PencilDotLoop<NQ>::value) {
+    if (st != nullptr)
+      return launch_pencil_k<NQ, EPB, MINB, 1, false, true>(nlist, elist, Dhost, G, u, w, lam0, B,
+                                                           lam1, mask, st, partials, part_base,
+                                                           reduce_count, s, pfG, cstride, pstride);
+  }
   return launch_pencil_k<NQ, EPB, MINB, NC, false>(nlist, elist, Dhost, G, u, w, lam0, B, lam1,
                                                    mask, st, partials, part_base, reduce_count, s,
                                                    pfG, cstride, pstride);
 }
 
-template <int NQ, int EPB, int MINB, int NC, bool CDOT>
+template <int NQ, int EPB, int MINB, int NC, bool CDOT, bool LOOP>
 static int launch_pencil_k(int64_t nlist, const int32_t* elist, const double* Dhost,
                            const double* G, const double* u, double* w, double lam0,
                            const double* B, double lam1, const uint8_t* mask, nk_cg_state* st,
@@ -358,7 +414,7 @@ static int launch_pencil_k(int64_t nlist, const int32_t* elist, const double* Dh
   const size_t smem = C::smem_bytes() + sizeof(double) * 32 * (NC - 1);
   static bool configured = false;
   if (!configured) {
-    cudaError_t err = cudaFuncSetAttribute(bk5_pencil<NQ, EPB, MINB, NC, CDOT>,
+    cudaError_t err = cudaFuncSetAttribute(bk5_pencil<NQ, EPB, MINB, NC, CDOT, LOOP>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) {
       set_error("bk5_pencil: smem attribute (%zu B): %s", smem, cudaGetErrorString(err));
@@ -366,21 +422,22 @@ static int launch_pencil_k(int64_t nlist, const int32_t* elist, const double* Dh
     }
     configured = true;
   }
-  const int64_t nblk = (nlist + EPB - 1) / EPB;
+  int64_t nblk = (nlist + EPB - 1) / EPB;
   if (nblk == 0) return NK_OK;
   if (resident < 0) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil<NQ, EPB, MINB, NC, CDOT>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil<NQ, EPB, MINB, NC, CDOT, LOOP>,
                                                   C::THREADS, smem);
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
+  if (LOOP && nblk > resident) nblk = resident;   // = pencil_dot_blocks
   DParam<NQ> D;
   D.set(Dhost);
   // pfG: 0 off, 1 own G into L2, 2 own G + the element one wave ahead
   const int64_t ahead = pfG >= 2 ? resident * EPB : 0;
-  launch_ex(st != nullptr ? kPdlStep : 0, bk5_pencil<NQ, EPB, MINB, NC, CDOT>,
+  launch_ex(st != nullptr ? kPdlStep : 0, bk5_pencil<NQ, EPB, MINB, NC, CDOT, LOOP>,
             dim3((unsigned)nblk), dim3(C::THREADS), smem, s, nlist, elist, D, G, u, w, lam0, B,
             lam1, mask, st, partials, part_base, reduce_count, pfG, ahead, cstride, pstride);
   return check_launch("bk5_pencil");
@@ -407,7 +464,7 @@ struct Pencil2Cfg {
   static size_t smem_bytes() { return sizeof(double) * ((size_t)EPB * 2 * VOL + 32); }
 };
 
-template <int NQ, int EPB, int MINB>
+template <int NQ, int EPB, int MINB, bool LOOP = false>
 __global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
 bk5_pencil2(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
             const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
@@ -425,7 +482,13 @@ bk5_pencil2(int64_t nlist, const int32_t* __restrict__ elist, const __grid_const
   double* red = smem;
   double* Rr = smem + 32 + (size_t)le * 2 * VOL;
   double* Ss = Rr + VOL;
-  const int64_t slot = (int64_t)blockIdx.x * EPB + le;
+  // LOOP: capped grid-stride grid for fused-dot launches (see bk5_pencil)
+  const int64_t nblk = (nlist + EPB - 1) / EPB;
+  double dot = 0.0;
+  int once = 0;   // LOOP = false: exactly one trip, provable at compile time
+  for (int64_t blk = blockIdx.x; LOOP ? blk < nblk : once < 1; blk += gridDim.x, ++once) {
+  if (LOOP && blk != blockIdx.x) __syncthreads();   // the previous group's B1 reads of R / S
+  const int64_t slot = blk * EPB + le;
   const bool active = slot < nlist;
   const int64_t e = active ? (elist ? (int64_t)elist[slot] : slot) : 0;
   const double* ue = u + e * NQ3;
@@ -497,7 +560,6 @@ bk5_pencil2(int64_t nlist, const int32_t* __restrict__ elist, const __grid_const
     }
   }
   __syncthreads();
-  double dot = 0.0;
   if (active) {  // B1: i-pencils + epilogue
     double v[NQ], o[NQ];
 #pragma unroll
@@ -535,6 +597,7 @@ bk5_pencil2(int64_t nlist, const int32_t* __restrict__ elist, const __grid_const
       for (int i = 0; i < NQ; ++i) wr[i] = res[i];
     }
   }
+  }  // element groups
   if (st != nullptr) {
     double vv[1] = {dot};
     block_sum<1>(vv, red);
@@ -544,6 +607,30 @@ bk5_pencil2(int64_t nlist, const int32_t* __restrict__ elist, const __grid_const
       reduce_partials<1>(partials, reduce_count, 0, s, red);
       if (t == 0) st->pAp = s[0];
     }
+  }
+}
+
+// Partials of a fused-dot pencil2 launch (capped, LOOP, at NQ <= 8).
+template <int NQ, int EPB, int MINB>
+static int64_t pencil2_dot_blocks(int64_t nlist) {
+  using C = Pencil2Cfg<NQ, EPB>;
+  const int64_t nb = (nlist + EPB - 1) / EPB;
+  if constexpr (!PencilDotLoop<NQ>::value) {
+    return nb;
+  } else {
+  static int64_t resident = -1;
+  if (resident < 0) {
+    const size_t smem = C::smem_bytes();
+    cudaFuncSetAttribute(bk5_pencil2<NQ, EPB, MINB, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil2<NQ, EPB, MINB, true>,
+                                                  EPB * NQ * NQ, smem);
+    resident = (int64_t)sms * (per > 0 ? per : 1);
+  }
+  return nb < resident ? nb : resident;
   }
 }
 
@@ -569,6 +656,21 @@ static int launch_pencil2(int64_t nlist, const int32_t* elist, const double* Dho
   if (nblk == 0) return NK_OK;
   DParam<NQ> D;
   D.set(Dhost);
+  if constexpr (PencilDotLoop<NQ>::value) {
+    if (st != nullptr) {
+      static bool lconf = false;
+      if (!lconf) {
+        cudaFuncSetAttribute(bk5_pencil2<NQ, EPB, MINB, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        lconf = true;
+      }
+      const int64_t g = pencil2_dot_blocks<NQ, EPB, MINB>(nlist);
+      bk5_pencil2<NQ, EPB, MINB, true><<<(unsigned)g, EPB * NQ * NQ, smem, s>>>(
+          nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count,
+          pfG);
+      return check_launch("bk5_pencil2");
+    }
+  }
   bk5_pencil2<NQ, EPB, MINB><<<(unsigned)nblk, EPB * NQ * NQ, smem, s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, pfG);
   return check_launch("bk5_pencil2");

@@ -71,7 +71,9 @@ __device__ __forceinline__ void fence_proxy_async() {
 // F1..F3 have read it, so ur is written there after one extra barrier (the
 // dense odd-NQ u image IS the pencil layout).  Saves one element buffer,
 // which buys a fifth staged G component at NQ = 15.
-template <int NQ, int NGS, int NUB, bool RINU = false>
+// EPB: elements per CTA (low orders: EPB small elements side by side, each
+// with its own buffers and NQ^2 threads; one barrier sequence per group).
+template <int NQ, int NGS, int NUB, bool RINU = false, int EPB = 1>
 struct StageCfg {
   static_assert(NGS >= 1 && NGS <= 6, "NGS");
   static_assert(NUB == 1 || NUB == 2, "NUB");
@@ -80,37 +82,40 @@ struct StageCfg {
   static constexpr int VOL = PencilLayout<NQ>::VOL;
   static constexpr int UB = (NQ3 + 2 + 1) & ~1;         // doubles, even: 16-B aligned next
   static constexpr int GBUF = (NGS * NQ3 + 1 + 1) & ~1;
-  static constexpr int THREADS = NQ2;
-  // layout (doubles): U[NUB] | G | R | S | red[32] ; mbarriers u[NUB], g
+  static constexpr int THREADS = EPB * NQ2;
+  // layout (doubles): U[NUB][EPB] | G[EPB] | R[EPB] | S[EPB] | red[32] ; mbarriers u[NUB], g
   static size_t smem_bytes() {
-    return sizeof(double) * ((size_t)NUB * UB + GBUF + (RINU ? 1 : 2) * VOL + 32) +
+    return sizeof(double) * ((size_t)EPB * (NUB * UB + GBUF + (RINU ? 1 : 2) * VOL) + 32) +
            (NUB + 1) * sizeof(uint64_t);
   }
 };
 
-template <int NQ, int NGS, int NUB, int MINB, bool RINU = false>
-__global__ void __launch_bounds__(NQ * NQ, MINB)
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1>
+__global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
 bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
           const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
           double lam0, const double* __restrict__ B, double lam1,
           const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
           int64_t part_base, int64_t reduce_count, int64_t u_len) {
   using L = PencilLayout<NQ>;
-  using C = StageCfg<NQ, NGS, NUB, RINU>;
+  using C = StageCfg<NQ, NGS, NUB, RINU, EPB>;
   constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL;
   extern __shared__ __align__(128) double smem[];
   if (st != nullptr && st->done) return;
-  double* Ub0 = smem;
-  double* Gb = Ub0 + NUB * C::UB;
-  double* Rfix = Gb + C::GBUF;                 // (RINU: unused)
-  double* Ss = RINU ? Rfix : Rfix + VOL;
-  double* red = Ss + VOL;
+  const int t = threadIdx.x;
+  const int le = EPB == 1 ? 0 : t / NQ2;       // this thread's element of the group
+  const int tt = t - le * NQ2;
+  const int a = tt % NQ, b = tt / NQ;
+  double* Ub0 = smem;                          // [NUB][EPB][UB]
+  double* Gb0 = Ub0 + NUB * EPB * C::UB;       // [EPB][GBUF]
+  double* Gb = Gb0 + le * C::GBUF;
+  double* Rfix = Gb0 + EPB * C::GBUF + le * VOL;        // (RINU: unused)
+  double* Ss = Gb0 + EPB * C::GBUF + (RINU ? 0 : EPB * VOL) + le * VOL;
+  double* red = Gb0 + EPB * C::GBUF + (RINU ? 1 : 2) * EPB * VOL;
   uint64_t* ubar = reinterpret_cast<uint64_t*>(red + 32);   // [NUB]
   uint64_t* gbar = ubar + NUB;
-
-  const int t = threadIdx.x;
-  const int a = t % NQ, b = t / NQ;
   const int64_t stride = gridDim.x;
+  const int64_t ngroups = (nlist + EPB - 1) / EPB;
   // w assembled in shared memory and bulk-stored: needs u and w at the same
   // 16-byte phase (then the staged u row and the w row align alike)
   const bool bulkw = NUB == 2 &&
@@ -120,27 +125,48 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     return (int)((reinterpret_cast<uintptr_t>(u + e * NQ3) >> 3) & 1);
   };
 
-  // thread 0 only
-  auto issue_u = [&](int64_t slot, int bi) {
-    const int64_t s0 = elem_of(slot) * NQ3;
-    const int sh = phase_of(s0 / NQ3);
-    int64_t cnt = (NQ3 + sh + 1) & ~int64_t(1);          // whole 16-B chunks
-    const bool tail = s0 - sh + cnt > u_len;             // would pass the array end
+  // thread 0 only: one mbarrier transaction for the group's EPB copies
+  auto u_copy = [&](int64_t s0, int64_t& cnt, int& sh) -> bool {   // -> tail
+    sh = phase_of(s0 / NQ3);                              // 8 B off a 16-B boundary
+    cnt = (NQ3 + sh + 1) & ~int64_t(1);                   // whole 16-B chunks
+    const bool tail = s0 - sh + cnt > u_len;              // would pass the array end
     if (tail) cnt -= 2;
-    double* dst = Ub0 + bi * C::UB;
-    mbar_expect_tx(&ubar[bi], (uint32_t)(cnt * sizeof(double)));
-    tma_load_1d(dst, u + s0 - sh, (uint32_t)(cnt * sizeof(double)), &ubar[bi]);
-    if (tail) {                                          // the one uncovered double
-      dst[cnt] = u[s0 - sh + cnt];
-      fence_proxy_async();                               // before later bulk writes
+    return tail;
+  };
+  auto issue_u = [&](int64_t grp, int bi) {
+    int64_t tot = 0;
+    for (int l = 0; l < EPB; ++l) {
+      if (grp * EPB + l >= nlist) break;
+      int64_t cnt;
+      int sh;
+      u_copy(elem_of(grp * EPB + l) * NQ3, cnt, sh);
+      tot += cnt;
+    }
+    mbar_expect_tx(&ubar[bi], (uint32_t)(tot * sizeof(double)));
+    for (int l = 0; l < EPB; ++l) {
+      if (grp * EPB + l >= nlist) break;
+      const int64_t s0 = elem_of(grp * EPB + l) * NQ3;
+      int64_t cnt;
+      int sh;
+      const bool tail = u_copy(s0, cnt, sh);
+      double* dst = Ub0 + (bi * EPB + l) * C::UB;
+      tma_load_1d(dst, u + s0 - sh, (uint32_t)(cnt * sizeof(double)), &ubar[bi]);
+      if (tail) {                                         // the one uncovered double
+        dst[cnt] = u[s0 - sh + cnt];
+        fence_proxy_async();                              // before later bulk writes
+      }
     }
   };
-  auto issue_g = [&](int64_t slot) {
-    const double* src = G + elem_of(slot) * 6 * NQ3;    // 48 NQ^3 B: always 16-B aligned
+  auto issue_g = [&](int64_t grp) {
     constexpr uint32_t GBYTES = (uint32_t)(((NGS * NQ3 + 1) & ~1) * sizeof(double));
-    mbar_expect_tx(gbar, GBYTES);
-    tma_load_1d(Gb, src, GBYTES, gbar);
-    if (NGS < 6) prefetch_l2(src + NGS * NQ3, (int64_t)(6 - NGS) * NQ3 * sizeof(double));
+    int nv = 0;
+    for (int l = 0; l < EPB; ++l) nv += grp * EPB + l < nlist ? 1 : 0;
+    mbar_expect_tx(gbar, nv * GBYTES);
+    for (int l = 0; l < nv; ++l) {
+      const double* src = G + elem_of(grp * EPB + l) * 6 * NQ3;   // always 16-B aligned
+      tma_load_1d(Gb0 + l * C::GBUF, src, GBYTES, gbar);
+      if (NGS < 6) prefetch_l2(src + NGS * NQ3, (int64_t)(6 - NGS) * NQ3 * sizeof(double));
+    }
   };
 
   if (t == 0) {
@@ -149,7 +175,7 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (t == 0 && (int64_t)blockIdx.x < nlist) {
+  if (t == 0 && (int64_t)blockIdx.x < ngroups) {
     issue_u(blockIdx.x, 0);
     issue_g(blockIdx.x);
   }
@@ -157,19 +183,20 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
 
   double dot = 0.0;
   int it = 0;
-  for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++it) {
-    const int64_t e = elem_of(slot);
+  for (int64_t slot = blockIdx.x; slot < ngroups; slot += stride, ++it) {
+    const bool act = EPB == 1 || slot * EPB + le < nlist;
+    const int64_t e = act ? elem_of(slot * EPB + le) : 0;
     const int sh = phase_of(e);
     const int bi = NUB == 2 ? (it & 1) : 0;
-    double* uS = Ub0 + bi * C::UB + sh;
+    double* uS = Ub0 + (bi * EPB + le) * C::UB + sh;
     double* Rr = RINU ? uS : Rfix;
-    if (NUB == 2 && t == 0 && slot + stride < nlist) {
-      bulk_wait_read0();             // the other buffer's w (previous element) has left
+    if (NUB == 2 && t == 0 && slot + stride < ngroups) {
+      bulk_wait_read0();             // the other buffer's w (previous group) has left
       issue_u(slot + stride, bi ^ 1);
     }
     mbar_wait(&ubar[bi], NUB == 2 ? ((it >> 1) & 1) : (it & 1));
     double ut[NQ], o1[NQ];
-    {  // ---- F1: i-pencils (j = a, k = b) -> R (RINU: o1, written after (A))
+    if (act) {  // ---- F1: i-pencils (j = a, k = b) -> R (RINU: o1, written after (A))
       double v[NQ], o[NQ];
       const double* row = uS + b * NQ2 + a * NQ;
       if (NQ % 2 == 0 && sh == 0) {   // 16-byte rows (sh = 1 only for a misaligned u slice)
@@ -202,15 +229,17 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       matvec<NQ, false>(D, v, ut);
     }
     __syncthreads();   // (A)
-    if (NUB == 1 && t == 0 && slot + stride < nlist) issue_u(slot + stride, 0);
+    if (NUB == 1 && t == 0 && slot + stride < ngroups) issue_u(slot + stride, 0);
     if (RINU) {   // every u read is done: the buffer becomes R
+      if (act) {
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o1[i];
+        for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o1[i];
+      }
       __syncthreads();   // (A2)
     }
     mbar_wait(gbar, it & 1);
     double gt[NQ];
-    {  // ---- G: k-pencils, pointwise symmetric 3x3
+    if (act) {  // ---- G: k-pencils, pointwise symmetric 3x3
       const double* gp = G + e * 6 * NQ3 + b * NQ + a;
 #pragma unroll
       for (int k = 0; k < NQ; ++k) {
@@ -227,8 +256,8 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       }
     }
     __syncthreads();   // (B) G buffer read for the last time
-    if (t == 0 && slot + stride < nlist) issue_g(slot + stride);
-    {  // ---- B2: j-pencils, in place on their own S column
+    if (t == 0 && slot + stride < ngroups) issue_g(slot + stride);
+    if (act) {  // ---- B2: j-pencils, in place on their own S column
       double v[NQ], o[NQ];
 #pragma unroll
       for (int m = 0; m < NQ; ++m) v[m] = Ss[L::idx(b, m, a)];
@@ -237,7 +266,7 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
     }
     __syncthreads();
-    {  // ---- B3: k-pencils, S column += D^T gt
+    if (act) {  // ---- B3: k-pencils, S column += D^T gt
       double o[NQ];
       matvec<NQ, true>(D, gt, o);
 #pragma unroll
@@ -247,7 +276,7 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       }
     }
     __syncthreads();
-    {  // ---- B1: i-pencils + epilogue
+    if (act) {  // ---- B1: i-pencils + epilogue
       double v[NQ], o[NQ];
 #pragma unroll
       for (int m = 0; m < NQ; ++m) v[m] = Rr[L::idx(b, a, m)];
@@ -287,8 +316,8 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
           for (int i = 0; i < NQ; ++i) urow[i] = res[i];
         }
         fence_proxy_async();
-        if (t == 0 && sh) w[e * NQ3] = res[0];
-        if (t == NQ2 - 1 && ((NQ3 - sh) & 1)) w[e * NQ3 + NQ3 - 1] = res[NQ - 1];
+        if (tt == 0 && sh) w[e * NQ3] = res[0];
+        if (tt == NQ2 - 1 && ((NQ3 - sh) & 1)) w[e * NQ3 + NQ3 - 1] = res[NQ - 1];
       } else {
         double* wr = w + off;
         if (NQ % 2 == 0 && sh == 0 &&
@@ -304,8 +333,14 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     }
     __syncthreads();   // (C) R, S free for the next element; w rows in shared
     if (bulkw && t == 0) {
-      const int64_t cnt = (NQ3 - sh) & ~int64_t(1);
-      bulk_store(w + e * NQ3 + sh, uS + sh, (uint32_t)(cnt * sizeof(double)));
+      for (int l = 0; l < EPB; ++l) {
+        if (slot * EPB + l >= nlist) break;
+        const int64_t el = elem_of(slot * EPB + l);
+        const int shl = phase_of(el);
+        const int64_t cnt = (NQ3 - shl) & ~int64_t(1);
+        bulk_store(w + el * NQ3 + shl, Ub0 + (bi * EPB + l) * C::UB + 2 * shl,
+                   (uint32_t)(cnt * sizeof(double)));
+      }
       bulk_commit();
     }
   }
@@ -323,32 +358,33 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
   }
 }
 
-// Grid: persistent, min(nlist, SMs x resident CTAs per SM).
-template <int NQ, int NGS, int NUB, int MINB, bool RINU = false>
+// Grid: persistent, min(groups, SMs x resident CTAs per SM).
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1>
 static int64_t stage_grid(int64_t nlist) {
   static int64_t resident = -1;
   if (resident < 0) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    using C = StageCfg<NQ, NGS, NUB, RINU>;
-    cudaFuncSetAttribute(bk5_stage<NQ, NGS, NUB, MINB, RINU>,
+    using C = StageCfg<NQ, NGS, NUB, RINU, EPB>;
+    cudaFuncSetAttribute(bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_stage<NQ, NGS, NUB, MINB, RINU>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB>,
                                                   C::THREADS, C::smem_bytes());
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
-  return nlist < resident ? nlist : resident;
+  const int64_t groups = (nlist + EPB - 1) / EPB;
+  return groups < resident ? groups : resident;
 }
 
 // u_len: doubles in the u array (bounds the 16-byte rounded copies)
-template <int NQ, int NGS, int NUB, int MINB, bool RINU = false>
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1>
 static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost, const double* G,
                         const double* u, double* w, double lam0, const double* B, double lam1,
                         const uint8_t* mask, nk_cg_state* st, double* partials,
                         int64_t part_base, int64_t reduce_count, int64_t u_len, cudaStream_t s) {
-  using C = StageCfg<NQ, NGS, NUB, RINU>;
-  const int64_t grid = stage_grid<NQ, NGS, NUB, MINB, RINU>(nlist);
+  using C = StageCfg<NQ, NGS, NUB, RINU, EPB>;
+  const int64_t grid = stage_grid<NQ, NGS, NUB, MINB, RINU, EPB>(nlist);
   if (grid == 0) return NK_OK;
   if ((reinterpret_cast<uintptr_t>(u) & 7) || (reinterpret_cast<uintptr_t>(G) & 15)) {
     set_error("bk5_stage: u must be 8-byte and G 16-byte aligned");
@@ -356,7 +392,7 @@ static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost
   }
   DParam<NQ> D;
   D.set(Dhost);
-  bk5_stage<NQ, NGS, NUB, MINB, RINU><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
+  bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, u_len);
   return check_launch("bk5_stage");
 }

@@ -303,7 +303,7 @@ def bk5_variant_eligible(name, N, ncomp=1):
     """Which BK5 variants serve an order (the analogue of SPEC.md:426's
     "N_q=12 -> full3d not eligible"): pencil-TMA needs N+1 in {4, 6, 8};
     dmma (FP64 tensor cores, two 8-row tiles) N+1 in 9..16; stage (TMA-staged
-    operands) N+1 in 8..16, stage2 N+1 in 9..15; seq3 serves
+    operands) N+1 in 3, 5..16, stage2 N+1 in 9..15; seq3 serves
     3-component batches only."""
     if name not in BK5_VARIANTS:
         return False
@@ -312,7 +312,7 @@ def bk5_variant_eligible(name, N, ncomp=1):
     if name == "dmma":
         return ncomp == 1 and 9 <= N + 1 <= 16
     if name == "stage":   # TMA-staged u and G in shared memory (bk5_stage.cuh)
-        return ncomp == 1 and 8 <= N + 1 <= 16
+        return ncomp == 1 and N + 1 >= 3 and N + 1 != 4
     if name == "stage2":  # stage with two threads per pencil (bk5_stage2.cuh)
         return ncomp == 1 and 9 <= N + 1 <= 15
     if name == "seq3":   # 3 components back to back per CTA (bk5_pencil NC = 3)

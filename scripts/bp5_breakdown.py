@@ -1,9 +1,12 @@
+"""In-situ per-kernel breakdown of one BP5 iteration (FusedPCG.profile_iteration)
+at the configs[1] sweep sizes:  python scripts/bp5_breakdown.py [orders]"""
 import json, os, sys
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "scripts"))
 import torch
 import paper_2104_05829_b200 as nk
 from bk5_sweep import E_FOR_N
-for N in (5, 7, 8, 11, 14):
+orders = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else (5, 7, 8, 11, 14)
+for N in orders:
     ne = E_FOR_N[N]
     m = nk.build_box_mesh((1, 1, 1), (ne, ne, ne), N, deformation=("sine", 0.05))
     op = nk.PoissonOperator(m)

@@ -46,6 +46,7 @@ def test_select_variant_and_parity(N):
 @pytest.mark.parametrize("variant,N,counts", [
     (7, 8, (3, 2, 2)), (7, 9, (2, 2, 3)), (7, 12, (3, 2, 2)), (7, 13, (2, 3, 1)),
     (7, 14, (2, 2, 2)), (7, 15, (3, 2, 2)),
+    (8, 2, (3, 2, 2)), (8, 4, (3, 3, 3)), (8, 5, (3, 2, 2)), (8, 6, (3, 3, 1)),
     (8, 7, (3, 2, 2)), (8, 8, (3, 3, 3)), (8, 9, (3, 2, 2)), (8, 10, (2, 2, 3)), (8, 11, (3, 3, 3)), (8, 12, (3, 3, 3)),
     (8, 13, (2, 3, 1)), (8, 14, (3, 3, 1)), (8, 15, (3, 2, 3)),
     (9, 8, (3, 3, 3)), (9, 9, (2, 2, 3)), (9, 11, (3, 2, 2)), (9, 12, (3, 3, 3)),
@@ -86,7 +87,8 @@ def test_dmma_variant_parity_fused(variant, N, counts):
         L.nk_bk5_set_variant(old)
 
 
-@pytest.mark.parametrize("N,counts", [(8, (12, 12, 12)), (9, (10, 10, 10)), (12, (10, 10, 10)),
+@pytest.mark.parametrize("N,counts", [(2, (30, 30, 30)), (4, (16, 16, 16)), (6, (12, 12, 12)),
+                                      (8, (12, 12, 12)), (9, (10, 10, 10)), (12, (10, 10, 10)),
                                       (13, (9, 9, 9)), (15, (7, 7, 7)),
                                       (14, (8, 8, 8))])
 @pytest.mark.parametrize("variant", [8, 9])
@@ -141,6 +143,30 @@ def test_stage_variant_misaligned_slice(N):
         L.nk_bk5_set_variant(old)
     wh = w.cpu().numpy().reshape(ref.shape)
     assert np.linalg.norm(wh - ref) / np.linalg.norm(ref) < 1e-12
+
+
+@pytest.mark.parametrize("N", [4, 6, 12])
+def test_stage_variant_element_subset(N):
+    """Variant 8 over an element list (the multi-rank boundary / interior
+    split): odd-length, unordered subsets -- several elements per CTA at the
+    low orders with a partial last group -- vs the oracle on those elements
+    (elements outside the list are not written)."""
+    from paper_2104_05829_b200._lib import lib
+    L = lib()
+    counts = (5, 4, 3)
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    o = om.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = np.random.default_rng(11 + N).standard_normal((m.E,) + (N + 1,) * 3)
+    ref = oop.bk5(o.basis.diff, o.G, u)
+    sel = np.random.default_rng(N).permutation(m.E)[:37].astype(np.int32)
+    old = L.nk_bk5_set_variant(8)
+    try:
+        w = nk.apply_stiffness_local(torch.as_tensor(u, device="cuda"), m,
+                                     elements=torch.as_tensor(sel, device="cuda"))
+    finally:
+        L.nk_bk5_set_variant(old)
+    wh = w.cpu().numpy().reshape(ref.shape)
+    assert np.linalg.norm(wh[sel] - ref[sel]) / np.linalg.norm(ref[sel]) < 1e-12
 
 
 def test_variant_errors():
