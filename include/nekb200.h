@@ -166,7 +166,7 @@ int nk_bk5_batch_variant(int N);
 int64_t nk_bk5_batch_blocks(int N, int64_t nlist);
 /* kernel variant selection: 0 = auto (measured per-order table: 8 for
  * N in {6,8,9,10,12,13,14}, 5 for N in {2,15}, else 3; 3-component batches:
- * 6 at N in {3,5,7,9,10,11}, pencil3 at N in {4,6}, three scalar launches
+ * 6 at N in {3,5,7..13}, pencil3 at N in {4,6}, three scalar launches
  * elsewhere), 5 = pencil2 (two shared buffers, u re-read from L1/L2), 1 =
  * k-slab (2D thread plane, k-column in registers, D in shared memory), 3 =
  * pencil (register 1-D contractions, D in the constant bank, swizzled shared

@@ -98,21 +98,21 @@ extern "C" int64_t nk_bk5_blocks(int N, int64_t nlist, int ncomp) {
 
 // the 3-component kernel the auto table picks per order (-1: three scalar
 // launches), measured on the B200 (scripts/bk5_sweep.py --helm3,
-// profiles/r1k_helm3.jsonl):
+// profiles/r2zg_helm3.jsonl, re-measured after the stage kernel):
 //   seq3    -- bk5_pencil<NC = 3>: the three components back to back in one
-//              CTA, G from HBM once and re-read from L2 (N = 3, 5, 7, 9, 10,
-//              11);
+//              CTA, G from HBM once and re-read from L2 (N = 3, 5, 7..13);
 //   pencil3 -- the three components interleaved, G in registers once
 //              (N = 4, 6);
-//   scalar  -- three scalar launches, G read three times (N = 1, 2, 8,
-//              12..15, where both batched forms spill or lose occupancy).
+//   scalar  -- three scalar launches of the auto kernel (N = 1, 2, 14, 15).
+// (pencil3 also edges out seq3 at N = 7 and 9, by 3-8%; seq3 is kept there
+// because the batched PCG's fused per-component dots need it.)
 // A forced variant (nk_bk5_set_variant) keeps its own kernel: 6 = seq3,
 // any other = pencil3 / k-slab.
 static int helm3_variant(int N) {
   int v = nk_bk5_variant_get();
   if (v != 0) return v;
   switch (N) {
-    case 3: case 5: case 7: case 9: case 10: case 11: return 6;
+    case 3: case 5: case 7: case 8: case 9: case 10: case 11: case 12: case 13: return 6;
     case 4: case 6: return 3;
     default: return -1;
   }

@@ -170,6 +170,11 @@ def config4(out):
     t = time.perf_counter() - t0
     it = [r.iterations for r in res]
     same = bool(torch.equal(xq, x3))
+    # the sequential solves run the auto SCALAR kernel (stage at N = 9) whose
+    # persistent grid sums p.Ap in a different tree than seq3's one partial
+    # per element: equal to rounding (tests/test_gpu_helm3.py pins bit
+    # identity where the partitions coincide)
+    rel = float(torch.linalg.norm(xq - x3) / torch.linalg.norm(x3))
     del xq
     prof = hs.solver.profile_iteration(b3) if hasattr(hs.solver, "profile_iteration") else None
     dof = m.E * N ** 3
@@ -190,6 +195,7 @@ def config4(out):
          "solver": type(hs.solver).__name__, "sequential_solve_s": round(t_seq, 4),
          "sequential_iterations": [r.iterations for r in rq],
          "batched_bitwise_equal_sequential": same,
+         "batched_vs_sequential_rel_l2": rel,
          "ms_per_iteration_3comp": round(t / max(it) * 1e3, 4),
          "breakdown_ms_3comp": None if prof is None else {k: round(v, 4) for k, v in prof.items()},
          "gdof_iter_per_s": round(dof * sum(it) / t / 1e9, 3), "setup_s": round(setup, 2),
