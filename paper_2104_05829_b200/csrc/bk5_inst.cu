@@ -190,7 +190,8 @@ int runt(int64_t nlist, const int32_t* elist, const double* D, const double* G, 
 // in shared memory, NUB u buffers (2: u(next) issued an element ahead and w
 // bulk-stored), MINB CTAs per SM.  cfg 0 is the default; nk_bk5_tune cfg 21 /
 // 22 select two alternatives for the sweep (scripts/bk5_hot.py --sweep).
-// U = 3: two u buffers with R in the current one (RINU, odd NQ).  E:
+// U = 3: two u buffers with R in the current one (RINU, odd NQ); U = 4: two
+// u buffers, G component NGS staged in the spare one (G4U).  E:
 // elements per CTA (the low orders run several small elements side by side).
 template <int NQ> struct StageShapes {
   static constexpr int G[3] = {6, 6, 6}, U[3] = {2, 1, 2}, M[3] = {1, 1, 1}, E[3] = {1, 1, 1};
@@ -207,7 +208,7 @@ NK_SDE(6, 6, 2, 6, 2, 6, 2, 3, 4, 6, 2, 8, 1) NK_SDE(7, 6, 2, 4, 2, 6, 2, 2, 4, 
 NK_SD(8, 6, 2, 5, 6, 2, 4, 6, 2, 3) NK_SD(9, 6, 2, 3, 6, 2, 2, 6, 1, 3)
 NK_SD(10, 6, 2, 2, 6, 1, 3, 4, 2, 3) NK_SD(11, 6, 2, 2, 4, 1, 3, 6, 2, 1)
 NK_SD(12, 6, 2, 1, 4, 1, 3, 6, 2, 2) NK_SD(13, 6, 2, 1, 3, 2, 2, 6, 1, 1)
-NK_SD(14, 6, 2, 1, 2, 2, 2, 6, 1, 1) NK_SD(15, 4, 2, 1, 5, 3, 1, 5, 1, 1)
+NK_SD(14, 6, 2, 1, 2, 2, 2, 6, 1, 1) NK_SD(15, 4, 2, 1, 5, 3, 1, 4, 4, 1)
 #undef NK_SD
 #undef NK_SDE
 
@@ -224,13 +225,13 @@ int runs(int64_t nlist, const int32_t* elist, const double* D, const double* G, 
          double* w, double lam0, const double* B, double lam1, const uint8_t* mask,
          nk_cg_state* st, double* partials, int64_t part_base, int64_t reduce_count,
          int64_t u_len, cudaStream_t s, int64_t* nblocks) {
-  constexpr int NB = NUB == 3 ? 2 : NUB;
-  constexpr bool RINU = NUB == 3;
+  constexpr int NB = NUB >= 3 ? 2 : NUB;
+  constexpr bool RINU = NUB == 3, G4U = NUB == 4;
   if (nblocks) {
-    *nblocks = stage_grid<NQ, NGS, NB, MINB, RINU, EPB>(nlist);
+    *nblocks = stage_grid<NQ, NGS, NB, MINB, RINU, EPB, G4U>(nlist);
     return NK_OK;
   }
-  return launch_stage<NQ, NGS, NB, MINB, RINU, EPB>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+  return launch_stage<NQ, NGS, NB, MINB, RINU, EPB, G4U>(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
                                      part_base, reduce_count, u_len, s);
 }
 

@@ -73,11 +73,17 @@ __device__ __forceinline__ void fence_proxy_async() {
 // which buys a fifth staged G component at NQ = 15.
 // EPB: elements per CTA (low orders: EPB small elements side by side, each
 // with its own buffers and NQ^2 threads; one barrier sequence per group).
-template <int NQ, int NGS, int NUB, bool RINU = false, int EPB = 1>
+// G4U (NUB = 2, EPB = 1, NGS <= 4): G component NGS of the CURRENT element is
+// staged in the spare u buffer while F1..F3 run (issued at the element's
+// start), and u(next) goes into that buffer after the G phase instead -- one
+// more staged component (of the two that do not fit at NQ = 15) for half an
+// element less of u lead time.
+template <int NQ, int NGS, int NUB, bool RINU = false, int EPB = 1, bool G4U = false>
 struct StageCfg {
   static_assert(NGS >= 1 && NGS <= 6, "NGS");
   static_assert(NUB == 1 || NUB == 2, "NUB");
   static_assert(!RINU || (NQ % 2 == 1 && NUB == 2), "R in the u buffer: odd NQ, two u buffers");
+  static_assert(!G4U || (NUB == 2 && EPB == 1 && !RINU && NGS <= 4), "G4U");
   static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
   static constexpr int VOL = PencilLayout<NQ>::VOL;
   static constexpr int UB = (NQ3 + 2 + 1) & ~1;         // doubles, even: 16-B aligned next
@@ -86,11 +92,12 @@ struct StageCfg {
   // layout (doubles): U[NUB][EPB] | G[EPB] | R[EPB] | S[EPB] | red[32] ; mbarriers u[NUB], g
   static size_t smem_bytes() {
     return sizeof(double) * ((size_t)EPB * (NUB * UB + GBUF + (RINU ? 1 : 2) * VOL) + 32) +
-           (NUB + 1) * sizeof(uint64_t);
+           (NUB + 2) * sizeof(uint64_t);
   }
 };
 
-template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1>
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1,
+          bool G4U = false>
 __global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
 bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
           const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
@@ -98,7 +105,7 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
           const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
           int64_t part_base, int64_t reduce_count, int64_t u_len) {
   using L = PencilLayout<NQ>;
-  using C = StageCfg<NQ, NGS, NUB, RINU, EPB>;
+  using C = StageCfg<NQ, NGS, NUB, RINU, EPB, G4U>;
   constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL;
   extern __shared__ __align__(128) double smem[];
   if (st != nullptr && st->done) return;
@@ -114,6 +121,7 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
   double* red = Gb0 + EPB * C::GBUF + (RINU ? 1 : 2) * EPB * VOL;
   uint64_t* ubar = reinterpret_cast<uint64_t*>(red + 32);   // [NUB]
   uint64_t* gbar = ubar + NUB;
+  uint64_t* g4bar = gbar + 1;   // (G4U)
   const int64_t stride = gridDim.x;
   const int64_t ngroups = (nlist + EPB - 1) / EPB;
   // w assembled in shared memory and bulk-stored: needs u and w at the same
@@ -169,9 +177,21 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     }
   };
 
+  // (G4U) component NGS of element e into u buffer bi: 16-B rounded like u
+  auto g4_shift = [&](int64_t e) -> int {
+    return (int)((reinterpret_cast<uintptr_t>(G + (e * 6 + NGS) * NQ3) >> 3) & 1);
+  };
+  auto issue_g4 = [&](int64_t e, int bi) {
+    const int s4 = g4_shift(e);
+    const int64_t cnt = (NQ3 + s4 + 1) & ~int64_t(1);   // stays inside component NGS + 1
+    mbar_expect_tx(g4bar, (uint32_t)(cnt * sizeof(double)));
+    tma_load_1d(Ub0 + bi * C::UB, G + (e * 6 + NGS) * NQ3 - s4, (uint32_t)(cnt * sizeof(double)),
+                g4bar);
+  };
   if (t == 0) {
     for (int i = 0; i < NUB; ++i) mbar_init(&ubar[i], 1);
     mbar_init(gbar, 1);
+    if (G4U) mbar_init(g4bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -190,7 +210,10 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     const int bi = NUB == 2 ? (it & 1) : 0;
     double* uS = Ub0 + (bi * EPB + le) * C::UB + sh;
     double* Rr = RINU ? uS : Rfix;
-    if (NUB == 2 && t == 0 && slot + stride < ngroups) {
+    if (G4U && t == 0) {   // this element's component NGS into the spare u buffer
+      bulk_wait_read0();
+      issue_g4(e, bi ^ 1);
+    } else if (NUB == 2 && t == 0 && slot + stride < ngroups) {
       bulk_wait_read0();             // the other buffer's w (previous group) has left
       issue_u(slot + stride, bi ^ 1);
     }
@@ -238,6 +261,8 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       __syncthreads();   // (A2)
     }
     mbar_wait(gbar, it & 1);
+    if (G4U) mbar_wait(g4bar, it & 1);
+    const double* g4s = G4U ? Ub0 + (bi ^ 1) * C::UB + g4_shift(e) : nullptr;
     double gt[NQ];
     if (act) {  // ---- G: k-pencils, pointwise symmetric 3x3
       const double* gp = G + e * 6 * NQ3 + b * NQ + a;
@@ -247,7 +272,8 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
         double g[6];
 #pragma unroll
         for (int c = 0; c < 6; ++c)
-          g[c] = c < NGS ? Gb[c * NQ3 + p] : __ldg(gp + c * NQ3 + k * NQ2);
+          g[c] = c < NGS ? Gb[c * NQ3 + p]
+                         : ((G4U && c == NGS) ? g4s[p] : __ldg(gp + c * NQ3 + k * NQ2));
         const int q = L::idx(k, b, a);
         const double ur = Rr[q], us = Ss[q];
         Rr[q] = g[0] * ur + g[1] * us + g[2] * ut[k];
@@ -256,7 +282,10 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       }
     }
     __syncthreads();   // (B) G buffer read for the last time
-    if (t == 0 && slot + stride < ngroups) issue_g(slot + stride);
+    if (t == 0 && slot + stride < ngroups) {
+      issue_g(slot + stride);
+      if (G4U) issue_u(slot + stride, bi ^ 1);   // component NGS has been read
+    }
     if (act) {  // ---- B2: j-pencils, in place on their own S column
       double v[NQ], o[NQ];
 #pragma unroll
@@ -359,17 +388,18 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
 }
 
 // Grid: persistent, min(groups, SMs x resident CTAs per SM).
-template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1>
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1, bool G4U = false>
 static int64_t stage_grid(int64_t nlist) {
   static int64_t resident = -1;
   if (resident < 0) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    using C = StageCfg<NQ, NGS, NUB, RINU, EPB>;
-    cudaFuncSetAttribute(bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB>,
+    using C = StageCfg<NQ, NGS, NUB, RINU, EPB, G4U>;
+    cudaFuncSetAttribute(bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB, G4U>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per,
+                                                  bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB, G4U>,
                                                   C::THREADS, C::smem_bytes());
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
@@ -378,13 +408,13 @@ static int64_t stage_grid(int64_t nlist) {
 }
 
 // u_len: doubles in the u array (bounds the 16-byte rounded copies)
-template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1>
+template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1, bool G4U = false>
 static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost, const double* G,
                         const double* u, double* w, double lam0, const double* B, double lam1,
                         const uint8_t* mask, nk_cg_state* st, double* partials,
                         int64_t part_base, int64_t reduce_count, int64_t u_len, cudaStream_t s) {
-  using C = StageCfg<NQ, NGS, NUB, RINU, EPB>;
-  const int64_t grid = stage_grid<NQ, NGS, NUB, MINB, RINU, EPB>(nlist);
+  using C = StageCfg<NQ, NGS, NUB, RINU, EPB, G4U>;
+  const int64_t grid = stage_grid<NQ, NGS, NUB, MINB, RINU, EPB, G4U>(nlist);
   if (grid == 0) return NK_OK;
   if ((reinterpret_cast<uintptr_t>(u) & 7) || (reinterpret_cast<uintptr_t>(G) & 15)) {
     set_error("bk5_stage: u must be 8-byte and G 16-byte aligned");
@@ -392,7 +422,7 @@ static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost
   }
   DParam<NQ> D;
   D.set(Dhost);
-  bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
+  bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB, G4U><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, u_len);
   return check_launch("bk5_stage");
 }
