@@ -73,6 +73,21 @@ __device__ __forceinline__ void fence_proxy_async() {
 // which buys a fifth staged G component at NQ = 15.
 // EPB: elements per CTA (low orders: EPB small elements side by side, each
 // with its own buffers and NQ^2 threads; one barrier sequence per group).
+// Shared layout of R and S in the stage kernels: the pencil layout, except at
+// NQ = 12 where the padded row stride 13 puts two-way conflicts on every
+// k-pencil access (the G phase and B3: 72 of the thread's 144 element-buffer
+// accesses): dense rows (R = 12) and plane stride 156 (= 12 mod 16) make the
+// k-pencil and j-column orientations conflict-free, and the i-rows -- read
+// and written with 16-byte accesses (ROW16) -- two-way.
+template <int NQ> struct StageLayout : PencilLayout<NQ> {
+  static constexpr bool ROW16 = false;
+};
+template <> struct StageLayout<12> {
+  static constexpr int R = 12, P = 156, VOL = 12 * 156;
+  static constexpr bool ROW16 = true;
+  __device__ __forceinline__ static int idx(int k, int j, int i) { return k * P + j * R + i; }
+};
+
 // G4U (NUB = 2, EPB = 1, NGS <= 4): G component NGS of the CURRENT element is
 // staged in the spare u buffer while F1..F3 run (issued at the element's
 // start), and u(next) goes into that buffer after the G phase instead -- one
@@ -85,7 +100,7 @@ struct StageCfg {
   static_assert(!RINU || (NQ % 2 == 1 && NUB == 2), "R in the u buffer: odd NQ, two u buffers");
   static_assert(!G4U || (NUB == 2 && EPB == 1 && !RINU && NGS <= 4), "G4U");
   static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
-  static constexpr int VOL = PencilLayout<NQ>::VOL;
+  static constexpr int VOL = StageLayout<NQ>::VOL;
   static constexpr int UB = (NQ3 + 2 + 1) & ~1;         // doubles, even: 16-B aligned next
   static constexpr int GBUF = (NGS * NQ3 + 1 + 1) & ~1;
   static constexpr int THREADS = EPB * NQ2;
@@ -104,7 +119,7 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
           double lam0, const double* __restrict__ B, double lam1,
           const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
           int64_t part_base, int64_t reduce_count, int64_t u_len) {
-  using L = PencilLayout<NQ>;
+  using L = StageLayout<NQ>;
   using C = StageCfg<NQ, NGS, NUB, RINU, EPB, G4U>;
   constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL;
   extern __shared__ __align__(128) double smem[];
@@ -237,8 +252,14 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
         matvec<NQ, false>(D, v, o1);
       } else {
         matvec<NQ, false>(D, v, o);
+        if (L::ROW16) {
 #pragma unroll
-        for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
+          for (int i = 0; i < NQ; i += 2)
+            *reinterpret_cast<double2*>(Rr + L::idx(b, a, i)) = make_double2(o[i], o[i + 1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) Rr[L::idx(b, a, i)] = o[i];
+        }
       }
       // ---- F2: j-pencils (i = a, k = b) -> S
 #pragma unroll
@@ -307,13 +328,29 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     __syncthreads();
     if (act) {  // ---- B1: i-pencils + epilogue
       double v[NQ], o[NQ];
+      double sr[NQ];
+      if (L::ROW16) {
 #pragma unroll
-      for (int m = 0; m < NQ; ++m) v[m] = Rr[L::idx(b, a, m)];
+        for (int m = 0; m < NQ; m += 2) {
+          const double2 pr = *reinterpret_cast<const double2*>(Rr + L::idx(b, a, m));
+          const double2 ps = *reinterpret_cast<const double2*>(Ss + L::idx(b, a, m));
+          v[m] = pr.x;
+          v[m + 1] = pr.y;
+          sr[m] = ps.x;
+          sr[m + 1] = ps.y;
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) {
+          v[m] = Rr[L::idx(b, a, m)];
+          sr[m] = Ss[L::idx(b, a, m)];
+        }
+      }
       matvec<NQ, true>(D, v, o);
       const int64_t off = e * NQ3 + b * NQ2 + a * NQ;
       double res[NQ];
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) res[i] = lam0 * (o[i] + Ss[L::idx(b, a, i)]);
+      for (int i = 0; i < NQ; ++i) res[i] = lam0 * (o[i] + sr[i]);
       double* urow = uS + b * NQ2 + a * NQ;   // NUB = 2: still this element's u
       if (B != nullptr || st != nullptr) {
         double urw[NQ];

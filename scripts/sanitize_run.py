@@ -55,6 +55,41 @@ for N, counts in ((8, (20, 20, 1)), (12, (15, 20, 1)), (12, (3, 3, 3)), (13, (10
 torch.cuda.synchronize()
 print("sanitize run (stage) ok")
 
+# round-2 paths: the stage kernel with several elements per CTA (N = 6) and
+# its alternative shapes (cfg 21 / 22: RINU, G4U at N = 14), the capped
+# grid-stride fused-dot launches (pencil N = 3, 5; pencil2 N = 2; N = 1), the
+# FDM on the FP64 tensor cores (N = 5, 9)
+for N, counts, variant, cfg in ((6, (14, 14, 1), 8, 0), (14, (11, 11, 2), 8, 21),
+                                (14, (11, 11, 2), 8, 22), (3, (40, 20, 1), 0, 0),
+                                (5, (20, 20, 1), 0, 0), (2, (40, 40, 1), 0, 0),
+                                (1, (60, 60, 2), 0, 0)):
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    L.nk_bk5_set_variant(variant)
+    L.nk_bk5_tune(cfg, 1)
+    nk.apply_stiffness_local(u, m)
+    op = nk.PoissonOperator(m)
+    b = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(torch.float64)
+    nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-6, max_iter=3, use_graph=False,
+                split_step=True).solve(b)
+    L.nk_bk5_set_variant(0)
+    L.nk_bk5_tune(0, 1)
+for N in (5, 9):
+    m = nk.build_box_mesh((1, 1, 1), (3, 2, 2), N, deformation=("sine", 0.05))
+    op = nk.PoissonOperator(m)
+    r = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    nk.gs_op(op.gs, r)
+    for kind in ("asm", "ras"):
+        L.nk_set_knob(3, 1)
+        sm = nk.SchwarzSmoother(op, kind)
+        z = torch.empty_like(r)
+        sm.apply(r, z)
+        L.nk_set_knob(3, 2)
+torch.cuda.synchronize()
+print("sanitize run (round-2 paths) ok")
+
 # SURVEY.md §8f kernels: p-multigrid (interp3, cheb_step, dense matvec, the
 # nested coarse PCG + cg_gate), Schwarz (fdm FP64/FP32, schwarz_post, ext gs),
 # projection (multi_wdot, multi_axpy, vscale), the BK5 variant selection
