@@ -250,8 +250,19 @@ class JacobiPreconditioner:
 
 
 # orders whose fused BP5 step stays one kernel (N = 7: the TMA pipeline,
-# 0.117 vs 0.138 ms split); elsewhere FusedPCG splits it (split_step)
+# 0.117 vs 0.138 ms split); elsewhere FusedPCG splits it (split_step) once the
+# rank's mesh is large enough that the 4th launch pays for itself: measured
+# crossovers (scripts/split_crossover.py, profiles/r2zj_split_crossover*.jsonl,
+# per-iteration time fused vs split): ~1-2M local points at N <= 5 (the split
+# step is 10-30% SLOWER below), ~0.5-0.8M at N = 6..11, none at N >= 12.
 SPLIT_STEP_OFF = (7,)
+
+
+def split_min_points(N):
+    """Local-point threshold of FusedPCG's automatic split_step rule."""
+    if N >= 12:
+        return 0
+    return 2_000_000 if N <= 5 else 600_000
 
 
 class FusedPCG:
@@ -268,10 +279,11 @@ class FusedPCG:
 
     split_step (one rank, fused gs): run nk_bk5_pcg's vector head as its own
     coalesced pass (nk_cg_xpstep) followed by nk_bk5 with the fused p.Ap --
-    4 kernels per iteration.  None = auto: on at the orders where it measured
-    faster than the fused kernel (every N except 7, whose fused step is the
-    TMA pipeline; profiles/r1m_bp5_split.jsonl: 1.02-1.15x at N = 1, 2,
-    4..6, 8..15, a tie at N = 3).
+    4 kernels per iteration.  None = auto: on where it measured faster than
+    the fused kernel -- every N except 7 (whose fused step is the TMA
+    pipeline) once the mesh has split_min_points(N) local points
+    (profiles/r2zj_split_crossover*.jsonl: 1.05-1.30x at the configs[1]
+    sizes; below the crossover the fused step wins by up to 30%).
 
     gather_segments (one rank, fused gs; off by default): the update also
     folds the edge / vertex segments itself (nk_cg_update_gs_seg: every
@@ -328,7 +340,8 @@ class FusedPCG:
                 self.gcodes = None
         self.launches_per_iter = 3    # bk5_pcg, gs (all | non-pair segments), update
         if split_step is None:
-            split_step = op.mesh.N not in SPLIT_STEP_OFF
+            split_step = (op.mesh.N not in SPLIT_STEP_OFF and
+                          op.mesh.n_local >= split_min_points(op.mesh.N))
         self.split = bool(split_step) and self.codes is not None
         if self.split:
             self.launches_per_iter = 4    # xpstep, bk5 (+p.Ap), gs non-pair, update
