@@ -1,4 +1,4 @@
-"""Multi-rank host logic over torch.distributed/gloo on CPU (world size 2, 4):
+"""Multi-rank host logic over torch.distributed/gloo on CPU (world size 2, 4, 8):
 RCB partition -> collective id discovery (build_halo_plan) -> pairwise
 exchange (RankComm.exchange) -> canonical-order combine.  The device kernels
 are replaced here by a numpy executor of the SAME plan arrays (test helper,
@@ -83,7 +83,11 @@ def _worker(rank, world, port, outdir, counts, N, bc):
 
 @pytest.mark.parametrize("world,counts,N,bc", [(2, (4, 2, 2), 3, "dirichlet"),
                                                (4, (4, 4, 2), 2, "periodic"),
-                                               (4, (3, 3, 3), 3, "neumann")])
+                                               (4, (3, 3, 3), 3, "neumann"),
+                                               # the 8-GPU layout of configs[2]/[3]: a 2x2x2
+                                               # RCB block grid, one vertex held by 8 ranks
+                                               (8, (4, 4, 4), 2, "dirichlet"),
+                                               (8, (4, 4, 4), 1, "periodic")])
 def test_distributed_gs_equals_global_oracle(world, counts, N, bc):
     import torch.multiprocessing as mp
     from oracle import gs as ogs
