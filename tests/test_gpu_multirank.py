@@ -69,7 +69,21 @@ def _worker(rank, world, port, outdir, counts, N, transport="auto"):
         sp = nk.FusedPCG(op, jac, tol=1e-8, max_iter=500, use_graph=(transport == "ipc"),
                          split_step=True)
         rs = sp.solve(torch.as_tensor(b, device="cuda"))
+        # the public boundary-first overlapped QQ^T across
+        # ranks: BK5 of a random field on the boundary elements, halo start,
+        # interior BK5 || exchange, combine == BK5 everywhere then gs_op
+        ug = np.random.default_rng(5).standard_normal((g.E, nq3))
+        ut = torch.as_tensor(ug[mine].ravel(), device="cuda")
+        field = torch.zeros_like(ut)
+
+        def local_work(elems):
+            nk.apply_stiffness_local(ut, m, out=field, elements=elems)
+
+        nk.gs_op_overlapped(op.gs, local_work, field)
+        ovl = field.cpu().numpy().copy()
+        ref_ovl = nk.gs_op(op.gs, nk.apply_stiffness_local(ut, m)).cpu().numpy()
         np.savez(os.path.join(outdir, f"r{rank}.npz"), mine=mine, ids=m.ids.cpu().numpy(),
+                 ovl=ovl, ref_ovl=ref_ovl,
                  transport=op.gs.transport, graph=graph, fused=fused,
                  w=w, gsw=gsw, x=x, it=res.iterations, hist=hist,
                  x_full=rf.x.cpu().numpy(), it_full=rf.iterations,
@@ -123,6 +137,14 @@ def test_two_ranks_one_gpu_gs_and_pcg(N, transport):
         assert np.array_equal(r["x_full"], r["x"])
         assert abs(int(r["it_split"]) - o.iterations) <= 1
     assert int(res[0]["it"]) == int(res[1]["it"])
+    # overlapped QQ^T: bit-identical to the non-overlapped schedule, and the
+    # assembled field equals the global oracle's QQ^T A_L u on each rank
+    ug = np.random.default_rng(5).standard_normal((g.E, nq3))
+    glob = ogs.gs_op(g.ids, oop.bk5(g.basis.diff, g.G, ug.reshape(sh)).ravel()).reshape(g.E, nq3)
+    for r in res:
+        assert np.array_equal(r["ovl"], r["ref_ovl"])
+        loc = glob[r["mine"]].ravel()
+        assert np.linalg.norm(r["ovl"] - loc) <= 1e-12 * np.linalg.norm(loc)
     assert np.max(np.abs(xg.ravel() - o.x)) < 1e-7 * np.max(np.abs(o.x))
     assert np.max(np.abs(xs.ravel() - o.x)) < 1e-7 * np.max(np.abs(o.x))
 
