@@ -444,6 +444,12 @@ int nk_cheb_step(int64_t n, const double* r, const double* Aq, const double* inv
  * assembled coarse operator, coarse_solve SPEC.md:519-527). */
 int nk_dense_matvec(int64_t n, const double* A, const double* x, double* y,
                     const nk_cg_state* st, nk_stream_t stream);
+/* the same with A stored in FP32 (products and sums in FP64): the coarse
+ * inverse of the 32-bit smoothing mode, half the streamed bytes.  Row pitch
+ * lda >= n, a multiple of 4, with A's columns n..lda-1 zero and x holding lda
+ * finite entries; A and x 16-byte aligned. */
+int nk_dense_matvec32(int64_t n, int64_t lda, const float* A, const double* x, double* y,
+                      const nk_cg_state* st, nk_stream_t stream);
 
 /* inner->done = 1 when outer->done: a nested solve (the iterative coarse
  * solve inside a p-multigrid preconditioner) becomes a no-op once the outer

@@ -101,6 +101,7 @@ _SIGS = {
     "nk_interp3": ([_I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _I32, _P, _P], _I32),
     "nk_cheb_step": ([_I64, _P, _P, _P, _P, _P, _P, _D, _D, _I32, _P, _P], _I32),
     "nk_dense_matvec": ([_I64, _P, _P, _P, _P, _P], _I32),
+    "nk_dense_matvec32": ([_I64, _I64, _P, _P, _P, _P, _P], _I32),
     "nk_multi_wdot_partials_len": ([], _I64),
     "nk_multi_wdot": ([_I64, _I32, _P, _I64, _P, _P, _P, _P, _P], _I32),
     "nk_multi_axpy": ([_I64, _I32, _P, _D, _P, _I64, _P, _P, _P], _I32),

@@ -10,7 +10,8 @@
 //                1/8-ish of that; prolongation reads the coarse field, reads +
 //                writes the fine one (17 B per fine point with the mask).
 //   nk_cheb_step 32-56 B per point.
-//   nk_dense_matvec  8 n^2 B (the explicit inverse of the coarse operator).
+//   nk_dense_matvec  8 n^2 B (the explicit inverse of the coarse operator);
+//   nk_dense_matvec32 the same with the inverse stored in FP32 (4 n^2 B).
 #include "common.cuh"
 
 namespace nk {
@@ -135,6 +136,52 @@ dense_matvec_kernel(int64_t n, const double* __restrict__ A, const double* __res
       for (int64_t c = lane; c < n; c += 32) s = fma(__ldcs(a + c), __ldg(x + c), s);
     }
     s = warp_sum(s);
+    if (lane == 0) y[row] = s;
+  }
+}
+
+// y = A x with A stored in FP32 (the 32-bit smoothing mode's coarse inverse:
+// half the bytes of the streamed n^2 matrix), products and sums in FP64.
+// Same warp-per-row structure, four 16-B (4-float) loads in flight per lane.
+__global__ void __launch_bounds__(256)
+dense_matvec32_kernel(int64_t n, int64_t lda, const float* __restrict__ A,
+                      const double* __restrict__ x, double* __restrict__ y,
+                      const nk_cg_state* st) {
+  if (st != nullptr && st->done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n;
+       row += warps) {
+    const float* a = A + row * lda;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t c = 0;
+    {   // lda: a multiple of 4, columns n..lda-1 of A zero, x[n..lda) finite
+      const float4* a4 = reinterpret_cast<const float4*>(a);
+      const double2* x2 = reinterpret_cast<const double2*>(x);
+      const int64_t n4 = lda >> 2;
+      int64_t q = lane;
+      for (; q + 96 < n4; q += 128) {
+        float4 av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) av[u] = __ldcs(a4 + q + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2 xa = __ldg(x2 + 2 * (q + 32 * u)), xb = __ldg(x2 + 2 * (q + 32 * u) + 1);
+          double& acc = u == 0 ? s0 : (u == 1 ? s1 : (u == 2 ? s2 : s3));
+          acc = fma((double)av[u].w, xb.y, fma((double)av[u].z, xb.x,
+                fma((double)av[u].y, xa.y, fma((double)av[u].x, xa.x, acc))));
+        }
+      }
+      for (; q < n4; q += 32) {
+        const float4 av = __ldcs(a4 + q);
+        const double2 xa = __ldg(x2 + 2 * q), xb = __ldg(x2 + 2 * q + 1);
+        s0 = fma((double)av.w, xb.y, fma((double)av.z, xb.x,
+             fma((double)av.y, xa.y, fma((double)av.x, xa.x, s0))));
+      }
+      c = n;
+    }
+    for (int64_t cc = c + lane; cc < n; cc += 32) s0 = fma((double)__ldcs(a + cc), __ldg(x + cc), s0);
+    double s = warp_sum((s0 + s1) + (s2 + s3));
     if (lane == 0) y[row] = s;
   }
 }
@@ -325,4 +372,20 @@ extern "C" int nk_dense_matvec(int64_t n, const double* A, const double* x, doub
   if (n == 0) return NK_OK;
   dense_matvec_kernel<<<grid_stride(n, 8, 16 * 148), 256, 0, S(stream)>>>(n, A, x, y, st);
   return check_launch("dense_matvec");
+}
+
+extern "C" int nk_dense_matvec32(int64_t n, int64_t lda, const float* A, const double* x,
+                                 double* y, const nk_cg_state* st, nk_stream_t stream) {
+  if (n < 0 || lda < n || (lda & 3) || (n > 0 && (!A || !x || !y))) {
+    set_error("dense_matvec32: invalid arguments (lda >= n, a multiple of 4)");
+    return NK_ERR_INVALID;
+  }
+  if (n > 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(x)) & 15)) {
+    set_error("dense_matvec32: A and x must be 16-byte aligned");
+    return NK_ERR_INVALID;
+  }
+  if (n == 0) return NK_OK;
+  dense_matvec32_kernel<<<grid_stride(n, 8, 16 * 148), 256, 0, S(stream)>>>(n, lda, A, x, y,
+                                                                            st);
+  return check_launch("dense_matvec32");
 }

@@ -314,6 +314,12 @@ class MultigridHierarchy:
         if singular:
             Ainv = Ainv - 1.0 / float(nu) ** 2
         lv.Ainv = Ainv.contiguous()
+        # 32-bit smoothing mode: the coarse inverse streams as FP32 (half the
+        # bytes of the one n^2 pass per V-cycle; sums stay FP64)
+        lv.Ainv32, lv.lda = None, (nu + 3) // 4 * 4
+        if self.smoother_precision == 32:
+            lv.Ainv32 = torch.zeros((nu, lv.lda), dtype=torch.float32, device=dev)
+            lv.Ainv32[:, :nu] = Ainv.float()
         lv.nu = nu
         # representative local copy of each kept unique id, and the scatter map
         # (masked points -> slot nu, which stays zero)
@@ -323,7 +329,7 @@ class MultigridHierarchy:
         rep.scatter_reduce_(0, uid[kept], pos[kept], reduce="amin", include_self=False)
         lv.rep = rep.to(torch.int32)
         lv.scat = torch.where(kept, uid, torch.full_like(uid, nu)).to(torch.int32)
-        lv.ru = torch.zeros(nu, dtype=torch.float64, device=dev)
+        lv.ru = torch.zeros((nu + 3) // 4 * 4, dtype=torch.float64, device=dev)   # lda-padded
         lv.eu = torch.zeros(nu + 1, dtype=torch.float64, device=dev)
 
     # ---------------------------------------------------------------- apply
@@ -405,8 +411,12 @@ class MultigridHierarchy:
                 c._iteration()
             return
         check(L.nk_gather(lv.nu, ptr(lv.rep), ptr(r), ptr(lv.ru), ptr(st), s), "gather")
-        check(L.nk_dense_matvec(lv.nu, ptr(lv.Ainv), ptr(lv.ru), ptr(lv.eu), ptr(st), s),
-              "dense_matvec")
+        if getattr(lv, "Ainv32", None) is not None:
+            check(L.nk_dense_matvec32(lv.nu, lv.lda, ptr(lv.Ainv32), ptr(lv.ru), ptr(lv.eu),
+                                      ptr(st), s), "dense_matvec32")
+        else:
+            check(L.nk_dense_matvec(lv.nu, ptr(lv.Ainv), ptr(lv.ru), ptr(lv.eu), ptr(st), s),
+                  "dense_matvec")
         check(L.nk_gather(lv.n, ptr(lv.scat), ptr(lv.eu), ptr(lv.e), ptr(st), s), "gather")
 
     def _vcycle(self, k, r, st):

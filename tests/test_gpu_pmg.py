@@ -213,3 +213,28 @@ def test_iterative_coarse_solve():
     assert float((rp.x - xd).abs().max()) < 1e-6 * float(xd.abs().max())
     with pytest.raises(nk.ContractError):
         nk.MultigridHierarchy(op, coarse="amg")
+
+
+@pytest.mark.parametrize("n", [1, 7, 64, 6859])
+def test_dense_matvec32_matches_fp64(n):
+    """nk_dense_matvec32 (the 32-bit smoothing mode's coarse inverse, FP32
+    storage, FP64 sums; row pitch lda = n rounded up to 4, zero padded) vs the
+    FP64 dense matvec: the FP32 rounding of A only (<= 1e-6 relative)."""
+    from paper_2104_05829_b200._lib import check, lib, ptr
+    L = lib()
+    g = torch.Generator(device="cuda").manual_seed(n)
+    A = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    lda = (n + 3) // 4 * 4
+    A32 = torch.zeros((n, lda), dtype=torch.float32, device="cuda")
+    A32[:, :n] = A.float()
+    x = torch.zeros(lda, dtype=torch.float64, device="cuda")
+    x[:n] = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    y64 = torch.empty(n, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    check(L.nk_dense_matvec32(n, lda, ptr(A32), ptr(x), ptr(y), None, s), "dense_matvec32")
+    check(L.nk_dense_matvec(n, ptr(A), ptr(x), ptr(y64), None, s), "dense_matvec")
+    ref = A32[:, :n].double() @ x[:n]
+    assert float(torch.linalg.norm(y - ref)) <= 1e-12 * float(torch.linalg.norm(ref))
+    assert float(torch.linalg.norm(y - y64)) <= 1e-6 * float(torch.linalg.norm(y64))
+    assert L.nk_dense_matvec32(n, lda + 1, ptr(A32), ptr(x), ptr(y), None, s) != 0
