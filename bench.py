@@ -663,8 +663,14 @@ def run_ours(args):
             "e2e": {"value": round(e2e_val, 4), "unit": "GDOF/s",
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "ms_per_step": round(e2e_ms, 4), "bitwise_equal_to_device_path": e2e_ok,
-                    "path": "apply_stiffness_local(pinned host u) -> pinned host w; 6 tapered chunks, "
-                            "H2D/BK5/D2H overlapped on 3 streams (cached CUDA graph)"},
+                    "path": ("apply_stiffness_local(pinned host u) -> pinned host w; 8 tapered "
+                             "chunks: copy-engine H2D per chunk overlapped with the stage BK5 "
+                             "kernel, which writes w straight into the pinned host buffer with "
+                             "cp.async.bulk stores (device -> host over PCIe, no D2H copies); "
+                             "cached CUDA graph"
+                             if N in nk.kernels._HostStream.DIRECT_ORDERS else
+                             "apply_stiffness_local(pinned host u) -> pinned host w; 6 tapered "
+                             "chunks, H2D/BK5/D2H overlapped on 3 streams (cached CUDA graph)")},
             "gpu_launches": launches,
             "roofline_context": ceiling,
             "bp5": bp5,

@@ -119,11 +119,22 @@ class _HostStream:
     2.5 ms with the pencil kernels (16-B pieces); copy-engine H2D + k-slab
     writing w straight to host is 0.85-0.88 ms on a warm L2 but 0.99 ms under
     bench.py's cold-L2 protocol, vs 0.90 ms for this pipeline (floor: 0.66-0.74
-    ms for concurrent H2D + D2H copies of the same bytes)."""
+    ms for concurrent H2D + D2H copies of the same bytes).
+
+    direct (round 2, orders in DIRECT_ORDERS, pinned buffers): copy-engine H2D
+    per chunk, and the stage kernel (bk5_stage.cuh) writes each chunk's w
+    straight into the pinned host buffer with its cp.async.bulk stores -- whole
+    4-KB element images over PCIe, no D2H copies and no copy-out tail:
+    0.855 ms with 8 chunks vs 0.902 ms for the copy pipeline at N = 7 under
+    bench.py's cold-L2 protocol (scripts/e2e_ab.py, profiles/r2zl_e2e_ab.json),
+    bit-identical."""
+
+    DIRECT_ORDERS = (7,)
 
     def __init__(self, mesh, nchunks):
         import torch
         self.mesh, self.nchunks = mesh, nchunks
+        self.direct = mesh.N in self.DIRECT_ORDERS
         n = mesh.n_local
         self.ud = torch.empty(n, dtype=torch.float64, device=mesh.device)
         self.wd = torch.empty(n, dtype=torch.float64, device=mesh.device)
@@ -168,6 +179,9 @@ class _HostStream:
 
     def _issue(self, uh, wh):
         import torch
+        if self.direct and uh.is_pinned() and wh.is_pinned() and \
+                (uh.data_ptr() | wh.data_ptr()) % 16 == 0:
+            return self._issue_direct(uh, wh)
         m = self.mesh
         nq3 = m.nq ** 3
         L = lib()
@@ -195,8 +209,35 @@ class _HostStream:
                 wh[a:b].copy_(self.wd[a:b], non_blocking=True)
         main.wait_stream(self.s_out)
 
+    def _issue_direct(self, uh, wh):
+        import torch
+        m = self.mesh
+        nq3 = m.nq ** 3
+        L = lib()
+        D = m.basis.diff
+        bounds = self._bounds(m.E)
+        main = torch.cuda.current_stream()
+        self.s_in.wait_stream(main)
+        old = L.nk_bk5_set_variant(BK5_VARIANTS["stage"])   # bulk w stores (host memory)
+        try:
+            for c in range(self.nchunks):
+                a, b = int(bounds[c]) * nq3, int(bounds[c + 1]) * nq3
+                with torch.cuda.stream(self.s_in):
+                    self.ud[a:b].copy_(uh[a:b], non_blocking=True)
+                    e1 = torch.cuda.Event()
+                    e1.record(self.s_in)
+                self.s_cmp.wait_event(e1)
+                e0, ne = int(bounds[c]), int(bounds[c + 1] - bounds[c])
+                check(L.nk_bk5(m.N, ne, ptr(D), m.G.data_ptr() + e0 * 6 * nq3 * 8,
+                               self.ud.data_ptr() + a * 8, wh.data_ptr() + a * 8, 1.0, None,
+                               0.0, 1, ne * nq3, None, None, 0, None, None, 0, 0,
+                               self.s_cmp.cuda_stream), "bk5")
+        finally:
+            L.nk_bk5_set_variant(old)
+        main.wait_stream(self.s_cmp)
 
-def apply_stiffness_local(u, mesh, basis=None, out=None, elements=None, nchunks=6):
+
+def apply_stiffness_local(u, mesh, basis=None, out=None, elements=None, nchunks=None):
     """Unassembled A_L u_L.  u: (E, nq, nq, nq) or flat,
     CUDA float64 (in place into `out` if given), or a HOST array/tensor
     (numpy or CPU torch, ideally pinned) which is streamed through the device
@@ -217,6 +258,8 @@ def apply_stiffness_local(u, mesh, basis=None, out=None, elements=None, nchunks=
             wh = torch.as_tensor(out).reshape(-1)
         else:
             wh = torch.empty(mesh.n_local, dtype=torch.float64, pin_memory=t.is_pinned())
+        if nchunks is None:   # measured best: 8 direct-mode chunks, 6 copy-pipeline chunks
+            nchunks = 8 if mesh.N in _HostStream.DIRECT_ORDERS else 6
         hs = getattr(mesh, "_host_stream", None)
         if hs is None or hs.nchunks != nchunks:
             hs = mesh._host_stream = _HostStream(mesh, nchunks)

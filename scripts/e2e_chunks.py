@@ -100,10 +100,15 @@ def hybrid(k):
 
 
 out3 = {}
-for v in (0, 1):
+for v in (0, 1, 8):
     old = L.nk_bk5_set_variant(v)
-    for k in (2, 4, 8, 16):
+    for k in (2, 4, 6, 8, 12, 16):
         out3[f"hybrid_v{v}_k{k}"] = round(t(lambda: hybrid(k)), 4)
+    if v == 8:   # the stage kernel's bulk stores (cp.async.bulk) into pinned host memory
+        hybrid(8)
+        torch.cuda.synchronize()
+        out3["hybrid_v8_equal"] = bool(torch.allclose(wh, ref, rtol=1e-12, atol=0))
+        out3["hybrid_v8_bitwise"] = bool(torch.equal(wh, ref))
     L.nk_bk5_set_variant(old)
 hybrid(8)
 torch.cuda.synchronize()
