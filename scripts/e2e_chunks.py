@@ -67,9 +67,14 @@ ref = nk.apply_stiffness_local(uh.cuda(), m, out=wd).cpu()
 zc()
 torch.cuda.synchronize()
 out2 = {"zero_copy_ms": round(t(zc), 4), "zero_copy_equal": bool(torch.equal(wh, ref))}
-for v in (3, 5, 1):
+for v in (3, 5, 1, 8):
     old = L.nk_bk5_set_variant(v)
     out2[f"zero_copy_ms_variant{v}"] = round(t(zc), 4)
+    if v == 8:   # stage: TMA bulk loads of u from and bulk stores of w to pinned host memory
+        wh.zero_()
+        zc()
+        torch.cuda.synchronize()
+        out2["zero_copy_variant8_bitwise"] = bool(torch.equal(wh, ref))
     L.nk_bk5_set_variant(old)
 print(json.dumps(out2))
 

@@ -497,8 +497,9 @@ def test_bk5_variants_match_oracle(variant_guard, variant, N):
 
 
 def test_host_streamed_apply_matches_device_path():
-    """numpy / pinned-host input goes through the chunked H2D-BK5-D2H
-    pipeline; results must equal the device path bit for bit."""
+    """numpy / pinned-host input goes through the chunked host pipeline (direct
+    mode at N = 7: the stage kernel writes w into host memory; else H2D-BK5-D2H
+    copies); results must equal the device path bit for bit."""
     N = 7
     m, o = both_meshes((5, 3, 2), N)
     rng = np.random.default_rng(3)
@@ -508,9 +509,21 @@ def test_host_streamed_apply_matches_device_path():
     assert isinstance(wn, np.ndarray) and np.array_equal(wn, wd)
     uh = torch.as_tensor(u).pin_memory()
     wh = torch.empty_like(uh).pin_memory()
-    for chunks in (1, 7, 30):
-        nk.apply_stiffness_local(uh, m, out=wh, nchunks=chunks)
-        assert np.array_equal(wh.numpy(), wd)
+    from paper_2104_05829_b200 import kernels as K
+    saved = K._HostStream.DIRECT_ORDERS
+    try:
+        # N = 7: direct mode (H2D copies + the stage kernel's bulk stores into
+        # the pinned host w), then the H2D / BK5 / D2H copy pipeline
+        for direct in (saved, ()):
+            K._HostStream.DIRECT_ORDERS = direct
+            m._host_stream = None
+            for chunks in (None, 1, 7, 30):
+                wh.zero_()
+                nk.apply_stiffness_local(uh, m, out=wh, nchunks=chunks)
+                assert np.array_equal(wh.numpy(), wd), (direct, chunks)
+    finally:
+        K._HostStream.DIRECT_ORDERS = saved
+        m._host_stream = None
     assert rel_l2(wd, oop.bk5(o.basis.diff, o.G, u)) < BK5_TOL
 
 
