@@ -30,26 +30,36 @@ namespace nk {
 // D[q][N-m]) / 2, M[m] = D[mid][m]: about half the multiply-adds and half the
 // D-hat operand fetches of the direct product (the rounding differs from it
 // at the 1e-16 level).  eo holds the forward tables, then the transposed ones.
+// Every table row starts on an even index and the struct is 16-byte aligned
+// with eo first, so consecutive coefficient pairs (m, m+1), m even, sit in one
+// 16-byte constant-bank chunk: one LDCU.128 feeds two DFMAs without uniform-
+// register shuffles (rows of odd length H + ODD or H used to straddle chunks).
 template <int NQ>
-struct DParam {
-  static constexpr int H = NQ / 2, ODD = NQ & 1;
-  static constexpr int EOF_ = H * (H + ODD) + H * H + ODD * H;   // one direction
+struct alignas(16) DParam {
+  static constexpr int H = NQ / 2, ODD = NQ & 1, HE = H + ODD;
+  static constexpr int SE = (HE + 1) & ~1, SO = (H + 1) & ~1;   // even row strides
+  static constexpr int OO = H * SE, OM = OO + H * SO;           // O rows, middle row
+  static constexpr int EOF_ = (OM + ODD * H + 1) & ~1;          // one direction (even)
+  __host__ __device__ static constexpr int ei(int q, int m) { return q * SE + m; }
+  __host__ __device__ static constexpr int oi(int q, int m) { return OO + q * SO + m; }
+  __host__ __device__ static constexpr int mi(int m) { return OM + m; }
+  double eo[2 * EOF_ > 0 ? 2 * EOF_ : 2];
   double d[NQ * NQ];   // row-major D[a][m] = h_m'(xi_a)
-  double eo[2 * EOF_ > 0 ? 2 * EOF_ : 1];
   void set(const double* Dh) {   // host
     for (int q = 0; q < NQ * NQ; ++q) d[q] = Dh[q];
+    for (int q = 0; q < (2 * EOF_ > 0 ? 2 * EOF_ : 2); ++q) eo[q] = 0.0;
     for (int tr = 0; tr < 2; ++tr) {
       double* T = eo + tr * EOF_;
       auto A = [&](int q, int m) { return tr ? Dh[m * NQ + q] : Dh[q * NQ + m]; };
       for (int q = 0; q < H; ++q) {
         for (int m = 0; m < H; ++m) {
-          T[q * (H + ODD) + m] = 0.5 * (A(q, m) + A(q, NQ - 1 - m));
-          T[H * (H + ODD) + q * H + m] = 0.5 * (A(q, m) - A(q, NQ - 1 - m));
+          T[ei(q, m)] = 0.5 * (A(q, m) + A(q, NQ - 1 - m));
+          T[oi(q, m)] = 0.5 * (A(q, m) - A(q, NQ - 1 - m));
         }
-        if (ODD) T[q * (H + ODD) + H] = A(q, H);
+        if (ODD) T[ei(q, H)] = A(q, H);
       }
       if (ODD)
-        for (int m = 0; m < H; ++m) T[H * (H + ODD) + H * H + m] = A(H, m);
+        for (int m = 0; m < H; ++m) T[mi(m)] = A(H, m);
     }
   }
 };

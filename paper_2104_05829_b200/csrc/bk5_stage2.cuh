@@ -72,17 +72,17 @@ __device__ __forceinline__ void matvec_half(const DParam<NQ>& D, const double (&
     double e = 0.0, o = 0.0;
 #pragma unroll
     for (int m = 0; m < H; ++m) {
-      e = fma(D.eo[OFF + q * HE + m], s[m], e);
-      o = fma(D.eo[OFF + H * HE + q * H + m], d[m], o);
+      e = fma(D.eo[OFF + DParam<NQ>::ei(q, m)], s[m], e);
+      o = fma(D.eo[OFF + DParam<NQ>::oi(q, m)], d[m], o);
     }
-    if (ODD) e = fma(D.eo[OFF + q * HE + H], v[H], e);
+    if (ODD) e = fma(D.eo[OFF + DParam<NQ>::ei(q, H)], v[H], e);
     out[2 * (q - HS::P0)] = o + e;
     out[2 * (q - HS::P0) + 1] = o - e;
   }
   if (HS::MID) {
     double mm = 0.0;
 #pragma unroll
-    for (int m = 0; m < H; ++m) mm = fma(D.eo[OFF + H * HE + H * H + m], d[m], mm);
+    for (int m = 0; m < H; ++m) mm = fma(D.eo[OFF + DParam<NQ>::mi(m)], d[m], mm);
     out[HS::CNT - 1] = mm;
   }
 }
