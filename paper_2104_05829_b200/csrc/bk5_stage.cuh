@@ -1,5 +1,6 @@
 // BK5 variant 8, "stage": persistent CTAs whose element operands are staged
-// in shared memory by the TMA engine, for the high orders (N + 1 = NQ in 8..15).
+// in shared memory by the TMA engine (auto at N = 6, 8, 9, 10, 12, 13, 14;
+// serves N + 1 = NQ in 3, 5..16).
 //
 // Why: ncu source-level stall sampling of the register-pencil kernels at
 // N = 12 (bk5_pencil<13>) and N = 15 (bk5_pencil2<16>) puts 48-56% of the
@@ -12,17 +13,20 @@
 // cp.async.bulk (SASS UBLKCP, mbarrier transaction counts) while the CTA
 // computes the current one, so every phase reads shared memory:
 //
+//   (start)      issue u(next) into the other u buffer (NUB = 2)
 //   wait u_bar   F1 i-pencils  u row (shared)     -> ur -> R
 //                F2 j-pencils  u column (shared)  -> us -> S
 //                F3 k-pencils  u column (shared)  -> ut (registers)
-//   sync (A)     u buffer free: issue u(next)
+//   sync (A)
 //   wait g_bar   G  k-pencils  G (shared; components >= NGS from L2) -> gr, gs
 //                   in place in R, S; gt (registers)
 //   sync (B)     G buffer free: issue G(next)
 //   B2 j-pencils S column  -> D^T gs in place      ; sync
 //   B3 k-pencils S column += D^T gt                 ; sync
-//   B1 i-pencils w = lam0 (D^T R row + S row) [+ lam1 B u, mask, u.w] -> HBM
-//   sync (C)
+//   B1 i-pencils w = lam0 (D^T R row + S row) [+ lam1 B u, mask, u.w]
+//                -> the element's spent u buffer
+//   sync (C)     one bulk store (cp.async.bulk.global.shared) of w -> HBM (or,
+//                through the UVA, pinned host memory: the e2e direct path)
 //
 // The contractions are the register pencils of bk5_pencil.cuh (even-odd D-hat
 // in the constant bank, 12 shared accesses per point as in pencil2).  The
@@ -35,7 +39,11 @@
 // when a copy would run past the allocation, is stored by a plain load.
 // NGS of the six G components are staged (all six when the CTA fits); the
 // rest are read from global memory after a bulk L2 prefetch issued one
-// element ahead.  HBM per point: u 8 + G 48 + w 8 B (the BK5 roofline).
+// element ahead.  Below N = 7 a CTA runs EPB small elements side by side.
+// Shapes and alternative modes (RINU, G4U, NUB = 1): StageShapes in
+// bk5_inst.cu.  N = 15 (one u row = 128 B) is bk5_stage16 below, with
+// tensor-map copies and the 128-byte swizzle.  HBM per point: u 8 + G 48 +
+// w 8 B (the BK5 roofline).
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
