@@ -211,9 +211,15 @@ int nk_bk5_tune(int cfg, int pf_dist);
  *     (mma.sync m8n8k4, N + 3 <= 16), 0 = the CUDA-core line kernel, 2 =
  *     (default) the measured winner per order (tensor cores at N = 4, 5,
  *     9..13).  Same algorithm, sums in a different order (rounding-level
- *     differences). */
+ *     differences).
+ *   NK_KNOB_TMA: the order-7 TMA BP5 step kernel -- 0 = two-stage (p, G)
+ *     ring, three CTAs per SM; 1 = single p and G buffers refilled as soon
+ *     as each is consumed, five CTAs per SM (200 registers); 2 = (default)
+ *     single buffers, four CTAs per SM.  Same arithmetic per element; the
+ *     grid (and so the grouping of the p.Ap partial sums) follows the CTAs
+ *     per SM. */
 enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_FDM = 3,
-       NK_KNOB_COUNT = 4 };
+       NK_KNOB_TMA = 4, NK_KNOB_COUNT = 5 };
 int nk_set_knob(int knob, int value);
 /* the device's maximum persisting-L2 set-aside in bytes (-1: no device). */
 int64_t nk_l2_set_aside_max(void);

@@ -442,6 +442,24 @@ extern "C" int NK_CAT(nk_bk5_pcg_nq, NK_BK5_NQ)(int64_t nlist, const int32_t* el
   }
   if constexpr (NQ == 8) {
     if (nk_bk5_variant_get() != 3) {  // auto / 4: TMA pipeline
+      if (knob(NK_KNOB_TMA) == 2) {  // single p / G buffers, four CTAs per SM
+        if (nblocks) {
+          *nblocks = tma_pcg_grid<NQ, 4, true>(nlist);
+          return NK_OK;
+        }
+        return launch_pencil_tma_pcg<NQ, 4, true>(nlist, elist, D, G, p, w, lam0, B, lam1, mask,
+                                                  x, r, invD, st, partials, part_base,
+                                                  reduce_count, hist, s);
+      }
+      if (knob(NK_KNOB_TMA) == 1) {  // single p / G buffers, five CTAs per SM
+        if (nblocks) {
+          *nblocks = tma_pcg_grid<NQ, 5, true>(nlist);
+          return NK_OK;
+        }
+        return launch_pencil_tma_pcg<NQ, 5, true>(nlist, elist, D, G, p, w, lam0, B, lam1, mask,
+                                                  x, r, invD, st, partials, part_base,
+                                                  reduce_count, hist, s);
+      }
       if (nblocks) {
         *nblocks = tma_pcg_grid<NQ, 3>(nlist);
         return NK_OK;

@@ -293,19 +293,25 @@ namespace nk {
 // and back into the stage, and applies the deferred x += alpha_{k-1} p_{k-1}
 // with x read/written directly (coalesced planes).  On the stop iteration only
 // the x update runs (no TMA traffic).
-template <int NQ, int MINB>
+// SB (single buffers, the stage-kernel scheme, bk5_stage.cuh): ONE p buffer
+// and ONE G buffer instead of the 2-stage (p, G) ring -- p(next) is issued as
+// soon as F3 has read the current p, G(next) as soon as the G phase is done
+// -- so a CTA needs 42 KB of shared memory instead of 71 KB and four or five
+// CTAs fit on an SM instead of three (NK_KNOB_TMA; four is the default:
+// 0.1080 -> 0.1068 ms per BP5 iteration, profiles/r2zo_bp5_tma_knob.jsonl).
+template <int NQ, int MINB, bool SB = false>
 struct TmaPcgCfg {
   static constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
   static constexpr int THREADS = NQ2;
   static constexpr int STAGE = 7 * NQ3;  // p, G[6]  (r, invD, x: plain loads)
+  static constexpr int NST = SB ? 1 : 2;
   static constexpr int VOL = PencilLayout<NQ>::VOL;
-  static size_t smem_bytes() { return sizeof(double) * (2 * STAGE + 3 * VOL + 32) + 2 * 8; }
+  static size_t smem_bytes() { return sizeof(double) * (NST * STAGE + 3 * VOL + 32) + 2 * 8; }
 };
 
-template <int NQ, int MINB>
-__global__ void __launch_bounds__(NQ * NQ, MINB)
-bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
-                   const __grid_constant__ DParam<NQ> D, const double* __restrict__ G,
+template <int NQ, int MINB, bool SB>
+__device__ __forceinline__ void tma_pcg_body(int64_t nlist, const int32_t* __restrict__ elist,
+                   const DParam<NQ>& D, const double* __restrict__ G,
                    double* __restrict__ p, double* __restrict__ w, double lam0,
                    const double* __restrict__ B, double lam1, const uint8_t* __restrict__ mask,
                    double* __restrict__ x, const double* __restrict__ r,
@@ -314,11 +320,11 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
                    double* __restrict__ hist, int pdl_flags, int l2_flags) {
   static_assert(NQ % 2 == 0, "bulk copies need 16-byte multiples");
   using L = PencilLayout<NQ>;
-  using C = TmaPcgCfg<NQ, MINB>;
+  using C = TmaPcgCfg<NQ, MINB, SB>;
   constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL, STAGE = C::STAGE;
   extern __shared__ __align__(128) double smem[];
-  double* stage0 = smem;
-  double* U = smem + 2 * STAGE;
+  double* stage0 = smem;   // SB: [p | G], bar[0] = p, bar[1] = G
+  double* U = smem + C::NST * STAGE;
   double* Rr = U + VOL;
   double* Ss = Rr + VOL;
   double* red = Ss + VOL;
@@ -349,12 +355,12 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (pre) {
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < C::NST; ++s) {
         const int64_t slot = blockIdx.x + s * stride;
         if (slot < nlist) {
-          mbar_expect_tx_only(&bar[s], GB);
-          tma_load_1d_hint(stage0 + s * STAGE + NQ3, G + elem_of(slot) * 6 * NQ3, GB, &bar[s],
-                           pol_s);
+          uint64_t* gb = SB ? &bar[1] : &bar[s];
+          mbar_expect_tx_only(gb, GB);
+          tma_load_1d_hint(stage0 + s * STAGE + NQ3, G + elem_of(slot) * 6 * NQ3, GB, gb, pol_s);
         }
       }
     }
@@ -368,10 +374,11 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
   const bool conv = it > 0 && st->rr <= st->thresh2;
   const bool stop = it > 0 && (conv || it >= st->max_iter);
   if (pre && (done || stop)) {  // drain the prologue copies before smem is released
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::NST; ++s) {
       if (blockIdx.x + s * stride < nlist) {
-        if (t == 0) mbar_arrive(&bar[s]);
-        mbar_wait(&bar[s], 0);
+        uint64_t* gb = SB ? &bar[1] : &bar[s];
+        if (t == 0) mbar_arrive(gb);
+        mbar_wait(gb, 0);
       }
     }
   }
@@ -408,9 +415,34 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
       }
       if (mask != nullptr) prefetch_l2_hint(mask + e * NQ3, NQ3, pol_s);
     };
+    // SB: p and G travel separately (bar[0] p, bar[1] G)
+    auto issue_p = [&](int64_t slot) {
+      const int64_t e = elem_of(slot);
+      mbar_expect_tx(&bar[0], UB);
+      tma_load_1d_hint(stage0, p + e * NQ3, UB, &bar[0], pol_s);
+      if (it > 0) {
+        prefetch_l2_hint(r + e * NQ3, UB, pol_r);
+        prefetch_l2_hint(invD + e * NQ3, UB, pol_d);
+        prefetch_l2_hint(x + e * NQ3, UB, pol_s);
+      }
+      if (mask != nullptr) prefetch_l2_hint(mask + e * NQ3, NQ3, pol_s);
+    };
+    auto issue_g = [&](int64_t slot, bool arrive) {
+      const int64_t e = elem_of(slot);
+      if (arrive) mbar_expect_tx(&bar[1], GB);
+      tma_load_1d_hint(stage0 + NQ3, G + e * 6 * NQ3, GB, &bar[1], pol_s);
+    };
     if (t == 0) {
-      if ((int64_t)blockIdx.x < nlist) issue(blockIdx.x, 0, pre);
-      if ((int64_t)blockIdx.x + stride < nlist) issue(blockIdx.x + stride, 1, pre);
+      if (SB) {
+        if ((int64_t)blockIdx.x < nlist) {
+          issue_p(blockIdx.x);
+          if (pre) mbar_arrive(&bar[1]);      // the prologue's G copy: its arrival
+          else issue_g(blockIdx.x, true);
+        }
+      } else {
+        if ((int64_t)blockIdx.x < nlist) issue(blockIdx.x, 0, pre);
+        if ((int64_t)blockIdx.x + stride < nlist) issue(blockIdx.x + stride, 1, pre);
+      }
     }
     // x, r, invD columns (k-pencil, coalesced planes) and the mask row of
     // an element are loaded into registers one element AHEAD (software
@@ -439,11 +471,11 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
     if ((int64_t)blockIdx.x < nlist) load_vec(blockIdx.x, xv, rv, dv, mk);
     int itl = 0;
     for (int64_t slot = blockIdx.x; slot < nlist; slot += stride, ++itl) {
-      const int s = itl & 1;
+      const int s = SB ? 0 : (itl & 1);
       double* su = stage0 + s * STAGE;
       const double* sg = su + NQ3;
       const int64_t e = elem_of(slot);
-      mbar_wait(&bar[s], (itl >> 1) & 1);
+      mbar_wait(&bar[s], SB ? (itl & 1) : ((itl >> 1) & 1));
 
       // ---- F3 + prologue: k-pencils (i = a, j = b)
       double ut[NQ];
@@ -467,6 +499,8 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
       uint64_t mk_next = ~0ull;
       if (slot + stride < nlist) load_vec(slot + stride, xv, rv, dv, mk_next);
       __syncthreads();
+      // SB: the p buffer has been read (it lives on in U): p(next) may land
+      if (SB && t == 0 && slot + stride < nlist) issue_p(slot + stride);
       double prow[NQ];   // p row (j = a, k = b): F1's input, B1's dot and mass term
       {  // F1 (i-pencils) -> R ; F2 (j-pencils) -> S
         double v[NQ], o[NQ];
@@ -482,6 +516,7 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
         for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
       }
       __syncthreads();
+      if (SB) mbar_wait(&bar[1], itl & 1);
       {  // G (k-pencils), wt -> U
         double gt[NQ];
 #pragma unroll
@@ -501,6 +536,8 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
         for (int k = 0; k < NQ; ++k) U[L::idx(k, b, a)] = o[k];
       }
       __syncthreads();
+      // SB: the G buffer has been read: G(next) may land
+      if (SB && t == 0 && slot + stride < nlist) issue_g(slot + stride, true);
       {  // B2 (j-pencils)
         double v[NQ], o[NQ];
 #pragma unroll
@@ -539,7 +576,7 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
       }
       __syncthreads();
       mk = mk_next;
-      if (t == 0 && slot + 2 * stride < nlist) issue(slot + 2 * stride, s, false);
+      if (!SB && t == 0 && slot + 2 * stride < nlist) issue(slot + 2 * stride, s, false);
     }
   }
 
@@ -563,32 +600,67 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
   }
 }
 
-template <int NQ, int MINB>
+template <int NQ, int MINB, bool SB = false>
+__global__ void __launch_bounds__(NQ * NQ, MINB)
+bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
+                   const __grid_constant__ DParam<NQ> D, const double* __restrict__ G,
+                   double* __restrict__ p, double* __restrict__ w, double lam0,
+                   const double* __restrict__ B, double lam1, const uint8_t* __restrict__ mask,
+                   double* __restrict__ x, const double* __restrict__ r,
+                   const double* __restrict__ invD, nk_cg_state* st,
+                   double* __restrict__ partials, int64_t part_base, int64_t reduce_count,
+                   double* __restrict__ hist, int pdl_flags, int l2_flags) {
+  tma_pcg_body<NQ, MINB, SB>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base, reduce_count, hist, pdl_flags, l2_flags);
+}
+
+// the same kernel with an explicit register cap (MINB = 5 under
+// __launch_bounds__ makes ptxas cap at 168 registers and spill; 200 x 64
+// threads x 5 CTAs still fits the 64 K register file)
+template <int NQ, int MINB, bool SB, int NREG>
+__global__ void __maxnreg__(NREG)
+bk5_pencil_tma_pcg_nreg(int64_t nlist, const int32_t* __restrict__ elist,
+                   const __grid_constant__ DParam<NQ> D, const double* __restrict__ G,
+                   double* __restrict__ p, double* __restrict__ w, double lam0,
+                   const double* __restrict__ B, double lam1, const uint8_t* __restrict__ mask,
+                   double* __restrict__ x, const double* __restrict__ r,
+                   const double* __restrict__ invD, nk_cg_state* st,
+                   double* __restrict__ partials, int64_t part_base, int64_t reduce_count,
+                   double* __restrict__ hist, int pdl_flags, int l2_flags) {
+  tma_pcg_body<NQ, MINB, SB>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base, reduce_count, hist, pdl_flags, l2_flags);
+}
+
+template <int NQ, int MINB, bool SB>
+static auto tma_pcg_kernel() {
+  if constexpr (SB && MINB == 5) return bk5_pencil_tma_pcg_nreg<NQ, MINB, SB, 200>;
+  else return bk5_pencil_tma_pcg<NQ, MINB, SB>;
+}
+
+template <int NQ, int MINB, bool SB = false>
 static int64_t tma_pcg_grid(int64_t nlist) {
   static int64_t resident = -1;
   if (resident < 0) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    using C = TmaPcgCfg<NQ, MINB>;
-    cudaFuncSetAttribute(bk5_pencil_tma_pcg<NQ, MINB>,
+    using C = TmaPcgCfg<NQ, MINB, SB>;
+    cudaFuncSetAttribute(tma_pcg_kernel<NQ, MINB, SB>(),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk5_pencil_tma_pcg<NQ, MINB>, C::THREADS,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tma_pcg_kernel<NQ, MINB, SB>(), C::THREADS,
                                                   C::smem_bytes());
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
   return nlist < resident ? nlist : resident;
 }
 
-template <int NQ, int MINB>
+template <int NQ, int MINB, bool SB = false>
 static int launch_pencil_tma_pcg(int64_t nlist, const int32_t* elist, const double* Dhost,
                                  const double* G, double* p, double* w, double lam0,
                                  const double* B, double lam1, const uint8_t* mask, double* x,
                                  const double* r, const double* invD, nk_cg_state* st,
                                  double* partials, int64_t part_base, int64_t reduce_count,
                                  double* hist, cudaStream_t s) {
-  using C = TmaPcgCfg<NQ, MINB>;
-  const int64_t grid = tma_pcg_grid<NQ, MINB>(nlist);
+  using C = TmaPcgCfg<NQ, MINB, SB>;
+  const int64_t grid = tma_pcg_grid<NQ, MINB, SB>(nlist);
   if (grid == 0) return NK_OK;
   if ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(G)) & 15) {
     set_error("bk5_pencil_tma_pcg: p and G must be 16-byte aligned");
@@ -596,7 +668,7 @@ static int launch_pencil_tma_pcg(int64_t nlist, const int32_t* elist, const doub
   }
   DParam<NQ> D;
   D.set(Dhost);
-  launch_ex(kPdlStep, bk5_pencil_tma_pcg<NQ, MINB>, dim3((unsigned)grid), dim3(C::THREADS),
+  launch_ex(kPdlStep, tma_pcg_kernel<NQ, MINB, SB>(), dim3((unsigned)grid), dim3(C::THREADS),
             C::smem_bytes(), s, nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st,
             partials, part_base, reduce_count, hist, knob(NK_KNOB_PDL), knob(NK_KNOB_L2));
   return check_launch("bk5_pencil_tma_pcg");

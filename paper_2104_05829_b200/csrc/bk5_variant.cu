@@ -20,9 +20,11 @@ extern "C" int nk_bk5_set_variant(int v) {
 // classes kernel (whose early-resident CTAs slow the step kernel they
 // follow, 0.117 -> 0.127 ms), and a one-trip-ahead L2 prefetch in the update;
 // L2 hints: streamed data evict_first + r / w evict_last (0.1136 -> 0.1101 ms,
-// profiles/r2l_bp5_knobs.jsonl; the persisting set-aside did not help, r2m).
+// profiles/r2l_bp5_knobs.jsonl; the persisting set-aside did not help, r2m);
+// the N = 7 TMA step with single p / G buffers at four CTAs per SM (0.1080 ->
+// 0.1068 ms, profiles/r2zo_bp5_tma_knob.jsonl).
 static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1,
-                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2};
+                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2};
 
 namespace nk {
 int knob(int k) { return (k >= 0 && k < NK_KNOB_COUNT) ? g_knobs[k] : 0; }

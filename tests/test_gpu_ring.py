@@ -158,3 +158,45 @@ def test_fused_tma_pcg_config1_size():
     fc = nk.FusedPCG(op, jac, tol=1e-8, max_iter=3000, use_graph=False, chunk=5)
     rc = fc.solve(b)
     assert rc.iterations == ra.iterations and torch.equal(rc.x, ra.x)
+
+
+@pytest.mark.parametrize("counts", [(4, 4, 4), (10, 10, 10)])
+def test_fused_tma_pcg_single_buffer_bit_identical(counts):
+    """NK_KNOB_TMA = 1, 2 (single p / G buffers, five / four CTAs per SM) vs the
+    two-stage ring (knob 0) at N = 7: only the copy schedule differs.  E = 64
+    (one element per CTA, the same grid either way): bit-identical; E = 1000
+    (every CTA cycles its buffers; 740 vs 444 CTAs, so the p.Ap partial sums
+    are grouped differently): same iterations, x to 1e-12 relative.  With and
+    without the PDL prologue."""
+    L = _lib.lib()
+    m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, 7, bc="dirichlet",
+                          deformation=("sine", 0.05))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    b = torch.randn(m.n_local, dtype=torch.float64, device="cuda", generator=g)
+    op = nk.PoissonOperator(m)
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(torch.float64)
+    jac = nk.JacobiPreconditioner(op)
+    out = []
+    old_pdl = L.nk_set_knob(0, 5)
+    try:
+        for pdl in (5, 0):
+            L.nk_set_knob(0, pdl)
+            for tma in (0, 1, 2):
+                old = L.nk_set_knob(4, tma)
+                try:
+                    s = nk.FusedPCG(op, jac, tol=1e-8, max_iter=3000, chunk=16)
+                    assert not s.split
+                    out.append(s.solve(b))
+                finally:
+                    L.nk_set_knob(4, old)
+    finally:
+        L.nk_set_knob(0, old_pdl)
+    assert out[0].converged
+    same_grid = m.E <= 444
+    for r in out[1:]:
+        assert r.iterations == out[0].iterations
+        if same_grid:
+            assert torch.equal(r.x, out[0].x)
+        else:
+            assert float((r.x - out[0].x).abs().max()) <= 1e-12 * float(out[0].x.abs().max())
