@@ -22,9 +22,10 @@ extern "C" int nk_bk5_set_variant(int v) {
 // L2 hints: streamed data evict_first + r / w evict_last (0.1136 -> 0.1101 ms,
 // profiles/r2l_bp5_knobs.jsonl; the persisting set-aside did not help, r2m);
 // the N = 7 TMA step with single p / G buffers at four CTAs per SM (0.1080 ->
-// 0.1068 ms, profiles/r2zo_bp5_tma_knob.jsonl).
+// 0.1068 ms, profiles/r2zo_bp5_tma_knob.jsonl); the fused gs update
+// software-pipelined two deep (0.1066 -> 0.1049 ms, r2zp_bp5_cg_pipe.jsonl).
 static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1,
-                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2};
+                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2, 2};
 
 namespace nk {
 int knob(int k) { return (k >= 0 && k < NK_KNOB_COUNT) ? g_knobs[k] : 0; }

@@ -264,7 +264,14 @@ __device__ __forceinline__ void gs_point_seg(int32_t c, double own, double pv, i
 // during trip k, so each trip's loads are L2 hits and HBM streams
 // continuously.
 // Batched like cg_update_kernel: gridDim.y components at cstride.
-template <bool SEG>
+// PIPE (NK_KNOB_CG_PIPE): software-pipelined across trips -- trip k + 1's
+// code / invD / r / w are loaded into registers while trip k's partner
+// gather and update run, so a trip waits on ONE dependent load (the
+// partner, whose code is already in a register) instead of code -> partner.
+// Same per-thread point order and accumulation (bit-identical).
+// PIPE2: two deep -- the code runs two trips ahead and the partner load
+// one trip ahead, so no load of a trip is issued in the trip that uses it.
+template <bool SEG, int PIPE = 0>
 __global__ void __launch_bounds__(kVecThreads, 4)
 cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restrict__ w,
                         const double* __restrict__ invD, const int32_t* __restrict__ code,
@@ -328,6 +335,79 @@ cg_update_gs_vec_kernel(int64_t n, double* __restrict__ r, const double* __restr
   if (threadIdx.x == 0)
     for (int k = 1; k <= pf; ++k) pf_trip(k, false, true);
   int64_t k = 0;
+  if constexpr (PIPE == 2) {
+    static_assert(!SEG, "two-deep pipeline: pair / unshared codes only");
+    double2 rv = make_double2(0, 0), av = make_double2(0, 0);
+    double px = 0.0, py = 0.0;
+    int2 cv1 = make_int2(-1, -1);
+    if (gtid < np) {
+      rv = ld2_hint(r + 2 * gtid, pol_r);
+      av = ldg2_hint(w + 2 * gtid, pol_r);
+      if (cv.x >= 0) px = w[cv.x];
+      if (cv.y >= 0) py = w[cv.y];
+      if (gtid + nthr < np) cv1 = ldg2i_hint(code + 2 * (gtid + nthr), pol_s);
+    }
+    for (int64_t q = gtid; q < np; q += nthr, ++k) {
+      if (pf > 0 && threadIdx.x == 0) pf_trip(k + 1 + pf, true, true);
+      const int64_t qn = q + nthr;
+      double2 dvn = make_double2(0, 0), rvn = make_double2(0, 0), avn = make_double2(0, 0);
+      double pxn = 0.0, pyn = 0.0;
+      int2 cv2 = make_int2(-1, -1);
+      if (qn < np) {
+        if (hz) dvn = ldg2_hint(invD + 2 * qn, pol_d);
+        rvn = ld2_hint(r + 2 * qn, pol_r);
+        avn = ldg2_hint(w + 2 * qn, pol_r);
+        if (cv1.x >= 0) pxn = w[cv1.x];
+        if (cv1.y >= 0) pyn = w[cv1.y];
+        if (qn + nthr < np) cv2 = ldg2i_hint(code + 2 * (qn + nthr), pol_s);
+      }
+      double2 wv;
+      gs_point_seg(cv.x, av.x, px, 0, av.x, wv.x, rcp_tab);
+      gs_point_seg(cv.y, av.y, py, 0, av.y, wv.y, rcp_tab);
+      double xd = 0.0;
+      upd_point<true>(alpha, xd, rv.x, 0.0, av.x, dv.x, wv.x, hz, acc);
+      upd_point<true>(alpha, xd, rv.y, 0.0, av.y, dv.y, wv.y, hz, acc);
+      st2_hint(r + 2 * q, rv, pol_r);
+      cv = cv1;
+      cv1 = cv2;
+      dv = dvn;
+      rv = rvn;
+      av = avn;
+      px = pxn;
+      py = pyn;
+    }
+  } else if constexpr (PIPE == 1) {
+    double2 rv = make_double2(0, 0), av = make_double2(0, 0);
+    if (gtid < np) {
+      rv = ld2_hint(r + 2 * gtid, pol_r);
+      av = ldg2_hint(w + 2 * gtid, pol_r);
+    }
+    for (int64_t q = gtid; q < np; q += nthr, ++k) {
+      if (pf > 0 && threadIdx.x == 0) pf_trip(k + 1 + pf, true, true);
+      int mx, my;
+      const double px = gather(cv.x, mx), py = gather(cv.y, my);
+      const int64_t qn = q + nthr;
+      int2 cvn = make_int2(-1, -1);
+      double2 dvn = make_double2(0, 0), rvn = make_double2(0, 0), avn = make_double2(0, 0);
+      if (qn < np) {
+        cvn = ldg2i_hint(code + 2 * qn, pol_s);
+        if (hz) dvn = ldg2_hint(invD + 2 * qn, pol_d);
+        rvn = ld2_hint(r + 2 * qn, pol_r);
+        avn = ldg2_hint(w + 2 * qn, pol_r);
+      }
+      double2 wv;
+      gs_point_seg(cv.x, av.x, px, mx, av.x, wv.x, rcp_tab);
+      gs_point_seg(cv.y, av.y, py, my, av.y, wv.y, rcp_tab);
+      double xd = 0.0;
+      upd_point<true>(alpha, xd, rv.x, 0.0, av.x, dv.x, wv.x, hz, acc);
+      upd_point<true>(alpha, xd, rv.y, 0.0, av.y, dv.y, wv.y, hz, acc);
+      st2_hint(r + 2 * q, rv, pol_r);
+      cv = cvn;
+      dv = dvn;
+      rv = rvn;
+      av = avn;
+    }
+  } else
   for (int64_t q = gtid; q < np; q += nthr, ++k) {
     if (pf > 0 && threadIdx.x == 0) pf_trip(k + 1 + pf, true, true);
     if (q != gtid) {
@@ -530,6 +610,12 @@ extern "C" int nk_cg_update_gs_seg(int64_t n, int ncomp, int64_t cstride, double
     if (segtab)
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<true>, g, dim3(kVecThreads), 0, s, n, r, w,
                 invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
+    else if (knob(NK_KNOB_CG_PIPE) == 2)
+      launch_ex(kPdlVec, cg_update_gs_vec_kernel<false, 2>, g, dim3(kVecThreads), 0, s, n, r,
+                w, invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
+    else if (knob(NK_KNOB_CG_PIPE) == 1)
+      launch_ex(kPdlVec, cg_update_gs_vec_kernel<false, 1>, g, dim3(kVecThreads), 0, s, n, r,
+                w, invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
     else
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<false>, g, dim3(kVecThreads), 0, s, n, r, w,
                 invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));

@@ -4,7 +4,7 @@ For each (PDL, CG_UPDATE) setting: FusedPCG on the configs[3] per-GPU box
 (E = 20^3, N = 7 deformed; other orders with --orders), 100-iteration graph
 replays (best of 7), plus one converged solve whose iteration count and x
 must be bit-identical across settings (the knobs change scheduling only).
-    python scripts/bp5_knobs.py [--orders 7,5,9] [--settings pdl:pf[:gather[:l2[:tma]]],...]
+    python scripts/bp5_knobs.py [--orders 7,5,9] [--settings pdl:pf[:gather[:l2[:tma[:pipe]]]],...]
         > profiles/<tag>_bp5_knobs.jsonl
 """
 import argparse
@@ -27,8 +27,8 @@ L = _lib.lib()
 print(json.dumps({"l2_set_aside_max_bytes": int(L.nk_l2_set_aside_max())}), flush=True)
 counts = tuple(int(c) for c in a.counts.split(","))
 settings = [tuple(int(v) for v in s.split(":")) for s in a.settings.split(",")]
-# pdl:cg_update_pf[:gather[:l2[:tma]]]
-settings = [st + (0, 0, 0)[len(st) - 2:] if len(st) < 5 else st for st in settings]
+# pdl:cg_update_pf[:gather[:l2[:tma[:pipe]]]]
+settings = [st + (0, 0, 2, 0)[len(st) - 2:] if len(st) < 6 else st for st in settings]
 
 for N in (int(o) for o in a.orders.split(",")):
     m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
@@ -38,9 +38,10 @@ for N in (int(o) for o in a.orders.split(",")):
     nk.gs_op(op0.gs, b)
     b *= m.mask.reshape(-1).to(torch.float64)
     ref = None
-    for pdl, cgu, gat, l2, tma in settings:
+    for pdl, cgu, gat, l2, tma, pipe in settings:
         old = (L.nk_set_knob(0, pdl), L.nk_set_knob(1, cgu), L.nk_set_knob(2, l2))
         old_tma = L.nk_set_knob(4, tma)
+        old_pipe = L.nk_set_knob(5, pipe)
         op = nk.PoissonOperator(m)
         s = nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-30, max_iter=100, chunk=100,
                         gather_segments=bool(gat))
@@ -62,7 +63,7 @@ for N in (int(o) for o in a.orders.split(",")):
             ref = (res.iterations, x)
         same = res.iterations == ref[0] and bool(torch.equal(x, ref[1]))
         print(json.dumps({"N": N, "E": m.E, "pdl": pdl, "cg_update_pf": cgu,
-                          "gather_segments": bool(gat), "l2": l2, "tma": tma, "launches_per_iter": s.launches_per_iter,
+                          "gather_segments": bool(gat), "l2": l2, "tma": tma, "cg_pipe": pipe, "launches_per_iter": s.launches_per_iter,
                           "split": bool(s.split), "ms_per_iter": round(min(ts), 5),
                           "ms_per_iter_median": round(sorted(ts)[len(ts) // 2], 5),
                           "solve_iterations": res.iterations,
@@ -70,3 +71,4 @@ for N in (int(o) for o in a.orders.split(",")):
         for kk, v in enumerate(old):
             L.nk_set_knob(kk, v)
         L.nk_set_knob(4, old_tma)
+        L.nk_set_knob(5, old_pipe)

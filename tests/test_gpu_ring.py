@@ -200,3 +200,34 @@ def test_fused_tma_pcg_single_buffer_bit_identical(counts):
             assert torch.equal(r.x, out[0].x)
         else:
             assert float((r.x - out[0].x).abs().max()) <= 1e-12 * float(out[0].x.abs().max())
+
+
+@pytest.mark.parametrize("counts,N", [((3, 3, 3), 5), ((10, 10, 10), 7), ((20, 20, 20), 7)])
+def test_cg_update_gs_pipelined_bit_identical(counts, N):
+    """NK_KNOB_CG_PIPE = 1, 2 (nk_cg_update_gs software-pipelined one / two
+    deep across its grid-stride trips) vs 0: same per-thread point order and accumulation,
+    so the converged fused-gs solve is bit-identical -- at E = 8000 every
+    thread runs ~7 trips, so the carried registers are exercised."""
+    L = _lib.lib()
+    m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, bc="dirichlet",
+                          deformation=("sine", 0.05))
+    g = torch.Generator(device="cuda").manual_seed(5)
+    b = torch.randn(m.n_local, dtype=torch.float64, device="cuda", generator=g)
+    op = nk.PoissonOperator(m)
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(torch.float64)
+    jac = nk.JacobiPreconditioner(op)
+    out = []
+    for pipe in (0, 1, 2):
+        old = L.nk_set_knob(5, pipe)
+        try:
+            s = nk.FusedPCG(op, jac, tol=1e-8, max_iter=3000, chunk=16, split_step=False)
+            assert s.codes is not None
+            out.append(s.solve(b))
+        finally:
+            L.nk_set_knob(5, old)
+    assert out[0].converged
+    for o in out[1:]:
+        assert o.iterations == out[0].iterations
+        assert o.residual_history == out[0].residual_history
+        assert torch.equal(o.x, out[0].x)
