@@ -165,7 +165,7 @@ int nk_bk5_batch_variant(int N);
  * -- the reduce_count of a single launch, the minimum part_stride. */
 int64_t nk_bk5_batch_blocks(int N, int64_t nlist);
 /* kernel variant selection: 0 = auto (measured per-order table: 8 for
- * N in {6,8,9,10,12,13,14}, 5 for N in {2,15}, else 3; 3-component batches:
+ * N in {6,8,9,10,12,13,14,15}, 5 for N = 2, else 3; 3-component batches:
  * 6 at N in {3,5,7..13}, pencil3 at N in {4,6}, three scalar launches
  * elsewhere), 5 = pencil2 (two shared buffers, u re-read from L1/L2), 1 =
  * k-slab (2D thread plane, k-column in registers, D in shared memory), 3 =
@@ -178,7 +178,10 @@ int64_t nk_bk5_batch_blocks(int N, int64_t nlist);
  * element's u and G moved into shared memory by cp.async.bulk while the
  * current one computes, w assembled in shared memory and bulk-stored,
  * several elements per CTA below N = 7; N+1 in 3, 5..16, else pencil),
- * 9 = stage2 (stage with two threads per pencil, N+1 in 9..15).  N = 1 always runs its point-per-lane kernel
+ * 9 = stage2 (stage with two threads per pencil, N+1 in 9..15), 10 = pair
+ * (one element per thread-block cluster of two CTAs split by k-planes:
+ * multicast u, all six G components staged, gt exchanged through
+ * distributed shared memory; N+1 = 16).  N = 1 always runs its point-per-lane kernel
  * unless 1 is set.  Variants 3/4/5/7/8 serve ncomp = 1; with them forced,
  * ncomp = 3 uses pencil3 (k-slab for 1) or three scalar launches.  Returns
  * the previous value. */

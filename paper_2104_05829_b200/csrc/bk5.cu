@@ -80,10 +80,11 @@ static int kvariant_for(int N) {
   if (v == 7) return N >= 8 ? 7 : 3;   // dmma: N + 1 >= 9
   if (v == 8) return (N >= 2 && N != 3) ? 8 : 3;   // stage: N + 1 in 3, 5..16
   if (v == 9) return (N >= 8 && N <= 14) ? 9 : 3;   // stage2: N + 1 in 9..15
+  if (v == 10) return N == 15 ? 10 : 3;             // pair: N + 1 = 16
   switch (N) {   // measured: profiles/r2s_bk5_order_sweep_evenodd.jsonl, r2x_stage_sweep.jsonl,
                  // r2ze_stage_low.jsonl
-    case 2: case 15: return 5;                                               // pencil2
-    case 6: case 8: case 9: case 10: case 12: case 13: case 14: return 8;   // stage (TMA-staged u, G)
+    case 2: return 5;                                                        // pencil2
+    case 6: case 8: case 9: case 10: case 12: case 13: case 14: case 15: return 8;   // stage
     default: return 3;                                      // pencil
   }
 }

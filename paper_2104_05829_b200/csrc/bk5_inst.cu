@@ -6,6 +6,7 @@
 #include "bk5_dmma.cuh"
 #include "bk5_stage.cuh"
 #include "bk5_stage2.cuh"
+#include "bk5_pair.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -356,6 +357,14 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
   }
 #if NK_BK5_NQ == 16
   if constexpr (NQ == 16) {
+    if (variant == 10 && ncomp == 1) {   // one element per CTA pair (bk5_pair.cuh)
+      if (nblocks) {
+        *nblocks = pair16_grid(nlist);
+        return NK_OK;
+      }
+      return launch_pair16(nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials,
+                           part_base, reduce_count, cstride, s);
+    }
     if (variant == 8 && ncomp == 1) {   // tensor-map (swizzled) staging (bk5_stage.cuh)
       if (nblocks) {
         *nblocks = stage16_grid(nlist);

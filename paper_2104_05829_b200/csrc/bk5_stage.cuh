@@ -527,8 +527,10 @@ bk5_stage16(int64_t nlist, const int32_t* __restrict__ elist, const __grid_const
   constexpr int NQ = 16, NQ2 = C::NQ2, NQ3 = C::NQ3, NGS = C::NGS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (st != nullptr && st->done) return;
-  double* Ub0 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                          ~uintptr_t(1023));
+  // 1024-B aligned (128-byte swizzle atoms), as an offset from smem_raw so
+  // that the compiler keeps the shared address space (LDS / STS, not generic
+  // LD / ST through the long scoreboard)
+  double* Ub0 = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   double* Gb = Ub0 + 2 * NQ3;
   double* Ss = Gb + NGS * NQ3;
   double* red = Ss + NQ3;
@@ -708,7 +710,8 @@ bk5_stage16(int64_t nlist, const int32_t* __restrict__ elist, const __grid_const
 // 2-D tensor map over an array of rows of 16 doubles (128 B), box 16 x 256
 // (one N = 15 element), 128-byte swizzle.  cuTensorMapEncodeTiled is fetched
 // through the runtime's driver entry point (no link against libcuda).
-inline int encode_rows16(CUtensorMap* map, const double* base, int64_t ndoubles) {
+inline int encode_rows16(CUtensorMap* map, const double* base, int64_t ndoubles,
+                         unsigned box_rows = 256) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (enc == nullptr) {
     cudaDriverEntryPointQueryResult q;
@@ -722,7 +725,7 @@ inline int encode_rows16(CUtensorMap* map, const double* base, int64_t ndoubles)
   }
   cuuint64_t dims[2] = {16, (cuuint64_t)(ndoubles / 16)};
   cuuint64_t strides[1] = {16 * sizeof(double)};
-  cuuint32_t box[2] = {16, 256};
+  cuuint32_t box[2] = {16, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

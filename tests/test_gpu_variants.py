@@ -50,7 +50,8 @@ def test_select_variant_and_parity(N):
     (8, 7, (3, 2, 2)), (8, 8, (3, 3, 3)), (8, 9, (3, 2, 2)), (8, 10, (2, 2, 3)), (8, 11, (3, 3, 3)), (8, 12, (3, 3, 3)),
     (8, 13, (2, 3, 1)), (8, 14, (3, 3, 1)), (8, 15, (3, 2, 3)),
     (9, 8, (3, 3, 3)), (9, 9, (2, 2, 3)), (9, 11, (3, 2, 2)), (9, 12, (3, 3, 3)),
-    (9, 13, (2, 3, 1)), (9, 14, (3, 3, 1))])
+    (9, 13, (2, 3, 1)), (9, 14, (3, 3, 1)),
+    (10, 15, (3, 3, 3)), (10, 15, (1, 1, 1)), (10, 15, (7, 6, 5))])
 def test_dmma_variant_parity_fused(variant, N, counts):
     """Variant 7 (FP64 tensor-core contractions, bk5_dmma.cuh) and variant 8
     (TMA-staged operands, bk5_stage.cuh): persistent CTAs that each take
@@ -73,7 +74,7 @@ def test_dmma_variant_parity_fused(variant, N, counts):
         w = torch.empty_like(ut)
         st = torch.zeros(256, dtype=torch.uint8, device="cuda")
         nb = int(L.nk_bk5_blocks(N, m.E, 1))
-        assert 1 <= nb <= m.E
+        assert 1 <= nb <= (2 if variant == 10 else 1) * m.E
         part = torch.zeros(nb, dtype=torch.float64, device="cuda")
         s = torch.cuda.current_stream().cuda_stream
         check(L.nk_bk5(N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(ut), ptr(w), lam0, ptr(m.B),
@@ -167,6 +168,36 @@ def test_stage_variant_element_subset(N):
         L.nk_bk5_set_variant(old)
     wh = w.cpu().numpy().reshape(ref.shape)
     assert np.linalg.norm(wh[sel] - ref[sel]) / np.linalg.norm(ref[sel]) < 1e-12
+
+
+@pytest.mark.parametrize("counts,subset", [((7, 7, 7), 0), ((9, 9, 9), 0), ((5, 4, 3), 37)])
+def test_pair_variant_ring_and_subset(counts, subset):
+    """Variant 10 (one N = 15 element per CTA pair, bk5_pair.cuh): E = 343 /
+    729 (every cluster cycles its u / G / exchange buffers and both mbarrier
+    phases several times) and an odd, unordered element subset -- vs the
+    oracle at 1e-12, and vs variant 5 (pencil2) to rounding."""
+    from paper_2104_05829_b200._lib import lib
+    L = lib()
+    N = 15
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    o = om.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = np.random.default_rng(17).standard_normal((m.E,) + (N + 1,) * 3)
+    ref = oop.bk5(o.basis.diff, o.G, u)
+    ut = torch.as_tensor(u, device="cuda")
+    sel = (np.random.default_rng(1).permutation(m.E)[:subset].astype(np.int32)
+           if subset else np.arange(m.E, dtype=np.int32))
+    kw = {"elements": torch.as_tensor(sel, device="cuda")} if subset else {}
+    old = L.nk_bk5_set_variant(10)
+    try:
+        w10 = nk.apply_stiffness_local(ut, m, **kw)
+        L.nk_bk5_set_variant(5)
+        w5 = nk.apply_stiffness_local(ut, m, **kw)
+    finally:
+        L.nk_bk5_set_variant(old)
+    a10 = w10.cpu().numpy().reshape(ref.shape)[sel]
+    a5 = w5.cpu().numpy().reshape(ref.shape)[sel]
+    assert np.linalg.norm(a10 - ref[sel]) / np.linalg.norm(ref[sel]) < 1e-12
+    assert np.linalg.norm(a10 - a5) / np.linalg.norm(a5) < 1e-13
 
 
 def test_variant_errors():
