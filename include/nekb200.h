@@ -221,11 +221,14 @@ int nk_bk5_tune(int cfg, int pf_dist);
  *     single buffers, four CTAs per SM.  Same arithmetic per element; the
  *     grid (and so the grouping of the p.Ap partial sums) follows the CTAs
  *     per SM.
- *   NK_KNOB_CG_PIPE: nk_cg_update_gs 16-B kernel -- 1 = software-pipelined
- *     across grid-stride trips (the next trip's code / invD / r / w loaded
- *     while the current trip's partner gather runs); 2 = (default) two deep
- *     (codes two trips ahead, partner values one trip ahead); 0 = per-trip
- *     loads.  Bit-identical. */
+ *   NK_KNOB_CG_PIPE: bits 0-1: nk_cg_update_gs 16-B kernel -- 1 =
+ *     software-pipelined across grid-stride trips (the next trip's code /
+ *     invD / r / w loaded while the current trip's partner gather runs); 2 =
+ *     two deep (codes two trips ahead, partner values one trip ahead); 0 =
+ *     per-trip loads (bit-identical to each other).  Bit 4: the CG vector
+ *     kernels' grid capped at 4 x 148 blocks instead of 8 x 148 (a different
+ *     but still fixed, device-independent grouping of the dot partial sums).
+ *     Default 6. */
 enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_FDM = 3,
        NK_KNOB_TMA = 4, NK_KNOB_CG_PIPE = 5, NK_KNOB_COUNT = 6 };
 int nk_set_knob(int knob, int value);

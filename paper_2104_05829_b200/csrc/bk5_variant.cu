@@ -23,9 +23,11 @@ extern "C" int nk_bk5_set_variant(int v) {
 // profiles/r2l_bp5_knobs.jsonl; the persisting set-aside did not help, r2m);
 // the N = 7 TMA step with single p / G buffers at four CTAs per SM (0.1080 ->
 // 0.1068 ms, profiles/r2zo_bp5_tma_knob.jsonl); the fused gs update
-// software-pipelined two deep (0.1066 -> 0.1049 ms, r2zp_bp5_cg_pipe.jsonl).
+// software-pipelined two deep (0.1066 -> 0.1049 ms, r2zp_bp5_cg_pipe.jsonl)
+// on a 4 x 148-block grid for every CG vector kernel (N = 3: 0.0330 ->
+// 0.0309 ms, N = 9: 0.2235 -> 0.2171 ms, N = 7 neutral; r2zr_bp5_vec_grid.jsonl).
 static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1,
-                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2, 2};
+                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2, 6};
 
 namespace nk {
 int knob(int k) { return (k >= 0 && k < NK_KNOB_COUNT) ? g_knobs[k] : 0; }

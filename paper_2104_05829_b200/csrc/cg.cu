@@ -11,10 +11,13 @@
 
 namespace nk {
 
+// NK_KNOB_CG_PIPE bit 4: cap at 4 x 148 blocks (one resident wave of the
+// 64-register update kernels) instead of 8 x 148
 static int64_t vec_grid(int64_t n) {
+  const int64_t cap = (knob(NK_KNOB_CG_PIPE) & 4) ? kVecMaxBlocks / 2 : kVecMaxBlocks;
   int64_t g = (n + kVecThreads - 1) / kVecThreads;
   if (g < 1) g = 1;
-  if (g > kVecMaxBlocks) g = kVecMaxBlocks;
+  if (g > cap) g = cap;
   return g;
 }
 
@@ -610,10 +613,10 @@ extern "C" int nk_cg_update_gs_seg(int64_t n, int ncomp, int64_t cstride, double
     if (segtab)
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<true>, g, dim3(kVecThreads), 0, s, n, r, w,
                 invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
-    else if (knob(NK_KNOB_CG_PIPE) == 2)
+    else if ((knob(NK_KNOB_CG_PIPE) & 3) == 2)
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<false, 2>, g, dim3(kVecThreads), 0, s, n, r,
                 w, invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
-    else if (knob(NK_KNOB_CG_PIPE) == 1)
+    else if ((knob(NK_KNOB_CG_PIPE) & 3) == 1)
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<false, 1>, g, dim3(kVecThreads), 0, s, n, r,
                 w, invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
     else

@@ -62,13 +62,13 @@ def test_knobs(L):
     kernels = 5, one-trip L2 prefetch in the update = 1, L2 hints: streamed
     data evict_first + r / w evict_last = 3, FDM per-order auto table = 2,
     single-buffer order-7 TMA step at four CTAs per SM = 2, two-deep
-    pipelined fused gs update = 2)."""
+    pipelined fused gs update on a 4 x 148-block grid = 6)."""
     assert L.nk_set_knob(0, 5) == 5 and L.nk_set_knob(1, 1) == 1
     assert L.nk_set_knob(2, 3) == 3 and L.nk_set_knob(3, 2) == 2
     old = L.nk_set_knob(0, 0)
     assert L.nk_set_knob(0, old) == 0
     assert L.nk_set_knob(4, 2) == 2
-    assert L.nk_set_knob(5, 2) == 2
+    assert L.nk_set_knob(5, 6) == 6
     assert L.nk_set_knob(6, 1) == -1 and L.nk_set_knob(-1, 0) == -1
 
 
