@@ -228,9 +228,12 @@ int nk_bk5_tune(int cfg, int pf_dist);
  *     per-trip loads (bit-identical to each other).  Bit 4: the CG vector
  *     kernels' grid capped at 4 x 148 blocks instead of 8 x 148 (a different
  *     but still fixed, device-independent grouping of the dot partial sums).
- *     Default 6. */
+ *     Default 6.
+ *   NK_KNOB_STAGE_PCG: nk_bk5_pcg at N + 1 in 9..15 (no element list) -- 1 =
+ *     the stage kernel with the Jacobi-PCG head fused into its F3 pass
+ *     (TMA-staged p and G); 0 = the register-pencil fused step. */
 enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_FDM = 3,
-       NK_KNOB_TMA = 4, NK_KNOB_CG_PIPE = 5, NK_KNOB_COUNT = 6 };
+       NK_KNOB_TMA = 4, NK_KNOB_CG_PIPE = 5, NK_KNOB_STAGE_PCG = 6, NK_KNOB_COUNT = 7 };
 int nk_set_knob(int knob, int value);
 /* the device's maximum persisting-L2 set-aside in bytes (-1: no device). */
 int64_t nk_l2_set_aside_max(void);

@@ -424,6 +424,30 @@ extern "C" int NK_CAT(nk_local_diag_nq, NK_BK5_NQ)(int64_t nelem, const double* 
   return check_launch("local_diag");
 }
 
+// the stage kernel with the PCG head fused (bk5_stage.cuh, PCG = true) at
+// N + 1 in 9..15: whole-array steps only (u_len = nlist elements)
+constexpr int kNotServed = -1000;
+template <int NQ>
+static int run_stage_pcg(int64_t nlist, const double* D, const double* G, double* p, double* w,
+                         double lam0, const double* B, double lam1, const uint8_t* mask,
+                         double* x, const double* r, const double* invD, nk_cg_state* st,
+                         double* partials, int64_t part_base, int64_t reduce_count,
+                         double* hist, cudaStream_t s, int64_t* nblocks) {
+  if constexpr (NQ >= 9 && NQ <= 15) {
+    using SD = StageShapes<NQ>;
+    static_assert(SD::U[0] == 2 && SD::E[0] == 1, "stage PCG: two u buffers, one element");
+    if (nblocks) {
+      *nblocks = stage_pcg_grid<NQ, SD::G[0], SD::M[0]>(nlist);
+      return NK_OK;
+    }
+    return launch_stage_pcg<NQ, SD::G[0], SD::M[0]>(nlist, D, G, p, w, lam0, B, lam1, mask, x, r,
+                                                    invD, st, partials, part_base, reduce_count,
+                                                    hist, s);
+  } else {
+    return kNotServed;
+  }
+}
+
 extern "C" int NK_CAT(nk_bk5_pcg_nq, NK_BK5_NQ)(int64_t nlist, const int32_t* elist,
                                                const double* D, const double* G, double* p,
                                                double* w, double lam0, const double* B,
@@ -475,6 +499,14 @@ extern "C" int NK_CAT(nk_bk5_pcg_nq, NK_BK5_NQ)(int64_t nlist, const int32_t* el
       }
       return launch_pencil_tma_pcg<NQ, 3>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r,
                                           invD, st, partials, part_base, reduce_count, hist, s);
+    }
+  }
+  {
+    const int v = nk_bk5_variant_get();
+    if (elist == nullptr && knob(NK_KNOB_STAGE_PCG) && (v == 0 || v == 8)) {
+      const int rc = run_stage_pcg<NQ>(nlist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st,
+                                       partials, part_base, reduce_count, hist, s, nblocks);
+      if (rc != kNotServed) return rc;
     }
   }
   if (nblocks) {

@@ -119,19 +119,43 @@ struct StageCfg {
   }
 };
 
+// PCG (nk_bk5_pcg, the fused BP5 step; EPB = 1, two u buffers, R in its own
+// buffer): u is the search direction p.  The element's x / r / invD columns
+// are read in the F3 pass (k-pencils: this thread's own column of the staged
+// p image, coalesced planes) and the Jacobi-PCG head is applied there --
+// deferred x += alpha p, p = invD r + beta p, written to global memory and
+// back into the staged image -- before F1 / F2 read it (one extra barrier);
+// the stop test and the last-block bookkeeping follow bk5_pencil_tma_pcg.
+// Same per-point arithmetic and the same p.Ap partial grouping as the split
+// step (nk_cg_xpstep + this kernel's fused dot): bit-identical solves.
 template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1,
-          bool G4U = false>
+          bool G4U = false, bool PCG = false>
 __global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
 bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constant__ DParam<NQ> D,
           const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ w,
           double lam0, const double* __restrict__ B, double lam1,
           const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
-          int64_t part_base, int64_t reduce_count, int64_t u_len) {
+          int64_t part_base, int64_t reduce_count, int64_t u_len, double* __restrict__ x = nullptr,
+          const double* __restrict__ r = nullptr, const double* __restrict__ invD = nullptr,
+          double* __restrict__ hist = nullptr) {
   using L = StageLayout<NQ>;
   using C = StageCfg<NQ, NGS, NUB, RINU, EPB, G4U>;
+  static_assert(!PCG || (EPB == 1 && NUB == 2 && !RINU && !G4U), "PCG: EPB 1, two u buffers");
   constexpr int NQ2 = C::NQ2, NQ3 = C::NQ3, VOL = C::VOL;
   extern __shared__ __align__(128) double smem[];
   if (st != nullptr && st->done) return;
+  // PCG: the iteration's scalars (bk5_pencil_tma_pcg)
+  int cgit = 0;
+  bool conv = false, stop = false;
+  double alpha_prev = 0.0, beta = 0.0;
+  if constexpr (PCG) {
+    cgit = st->iter;
+    conv = cgit > 0 && st->rr <= st->thresh2;
+    stop = cgit > 0 && (conv || cgit >= st->max_iter);
+    alpha_prev = st->alpha;
+    const double rz = st->rz;
+    beta = cgit == 0 ? 0.0 : (st->flexible ? (-alpha_prev * st->zap) / rz : st->rz_new / rz);
+  }
   const int t = threadIdx.x;
   const int le = EPB == 1 ? 0 : t / NQ2;       // this thread's element of the group
   const int tt = t - le * NQ2;
@@ -182,6 +206,11 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       const bool tail = u_copy(s0, cnt, sh);
       double* dst = Ub0 + (bi * EPB + l) * C::UB;
       tma_load_1d(dst, u + s0 - sh, (uint32_t)(cnt * sizeof(double)), &ubar[bi]);
+      if (PCG && cgit > 0) {   // the PCG head's columns: towards L2 one element ahead
+        prefetch_l2(x + s0 - sh, cnt * (int64_t)sizeof(double));
+        prefetch_l2(r + s0 - sh, cnt * (int64_t)sizeof(double));
+        prefetch_l2(invD + s0 - sh, cnt * (int64_t)sizeof(double));
+      }
       if (tail) {                                         // the one uncovered double
         dst[cnt] = u[s0 - sh + cnt];
         fence_proxy_async();                              // before later bulk writes
@@ -211,6 +240,17 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     tma_load_1d(Ub0 + bi * C::UB, G + (e * 6 + NGS) * NQ3 - s4, (uint32_t)(cnt * sizeof(double)),
                 g4bar);
   };
+  double dot = 0.0;
+  if (PCG && stop) {   // the final deferred x update only
+    for (int64_t slot = blockIdx.x; slot < ngroups; slot += stride) {
+      const int64_t e = elem_of(slot);
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const int64_t q = e * NQ3 + k * NQ2 + tt;
+        x[q] = fma(alpha_prev, u[q], x[q]);
+      }
+    }
+  }
   if (t == 0) {
     for (int i = 0; i < NUB; ++i) mbar_init(&ubar[i], 1);
     mbar_init(gbar, 1);
@@ -218,15 +258,14 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (t == 0 && (int64_t)blockIdx.x < ngroups) {
+  if (t == 0 && (int64_t)blockIdx.x < ngroups && !(PCG && stop)) {
     issue_u(blockIdx.x, 0);
     issue_g(blockIdx.x);
   }
   __syncthreads();   // the tail store (if any) before the first F1
 
-  double dot = 0.0;
   int it = 0;
-  for (int64_t slot = blockIdx.x; slot < ngroups; slot += stride, ++it) {
+  for (int64_t slot = blockIdx.x; slot < ((PCG && stop) ? 0 : ngroups); slot += stride, ++it) {
     const bool act = EPB == 1 || slot * EPB + le < nlist;
     const int64_t e = act ? elem_of(slot * EPB + le) : 0;
     const int sh = phase_of(e);
@@ -242,6 +281,32 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     }
     mbar_wait(&ubar[bi], NUB == 2 ? ((it >> 1) & 1) : (it & 1));
     double ut[NQ], o1[NQ];
+    if constexpr (PCG) {   // ---- F3 + the PCG head on this thread's k-column
+      double v[NQ];
+      const int64_t q0 = e * NQ3 + b * NQ + a;
+      if (cgit > 0) {
+        double xv[NQ], rv[NQ], dv[NQ];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) {
+          xv[m] = x[q0 + m * NQ2];
+          rv[m] = __ldg(r + q0 + m * NQ2);
+          dv[m] = __ldg(invD + q0 + m * NQ2);
+        }
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) {
+          const double pv = uS[m * NQ2 + b * NQ + a];
+          x[q0 + m * NQ2] = fma(alpha_prev, pv, xv[m]);
+          v[m] = fma(beta, pv, dv[m] * rv[m]);
+          uS[m * NQ2 + b * NQ + a] = v[m];
+          const_cast<double*>(u)[q0 + m * NQ2] = v[m];
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) v[m] = uS[m * NQ2 + b * NQ + a];
+      }
+      matvec<NQ, false>(D, v, ut);
+      __syncthreads();   // (P) the updated p image before F1 / F2
+    }
     if (act) {  // ---- F1: i-pencils (j = a, k = b) -> R (RINU: o1, written after (A))
       double v[NQ], o[NQ];
       const double* row = uS + b * NQ2 + a * NQ;
@@ -275,10 +340,11 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
       matvec<NQ, false>(D, v, o);
 #pragma unroll
       for (int j = 0; j < NQ; ++j) Ss[L::idx(b, j, a)] = o[j];
-      // ---- F3: k-pencils (i = a, j = b) -> ut
+      if constexpr (!PCG) {   // ---- F3: k-pencils (i = a, j = b) -> ut
 #pragma unroll
-      for (int m = 0; m < NQ; ++m) v[m] = uS[m * NQ2 + b * NQ + a];
-      matvec<NQ, false>(D, v, ut);
+        for (int m = 0; m < NQ; ++m) v[m] = uS[m * NQ2 + b * NQ + a];
+        matvec<NQ, false>(D, v, ut);
+      }
     }
     __syncthreads();   // (A)
     if (NUB == 1 && t == 0 && slot + stride < ngroups) issue_u(slot + stride, 0);
@@ -427,7 +493,20 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) {
       double sres[1];
       reduce_partials<1>(partials, reduce_count, 0, sres, red);
-      if (t == 0) st->pAp = sres[0];
+      if (t == 0) {
+        if constexpr (PCG) {
+          if (cgit > 0 && hist) hist[cgit] = sqrt(st->rr);
+          if (stop) {
+            st->converged = conv ? 1 : 0;
+            st->done = 1;
+          } else {
+            st->pAp = sres[0];
+            if (cgit > 0) st->rz = st->rz_new;
+          }
+        } else {
+          st->pAp = sres[0];
+        }
+      }
     }
   }
 }
@@ -470,6 +549,46 @@ static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost
   bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB, G4U><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
       nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, u_len);
   return check_launch("bk5_stage");
+}
+
+// The fused BP5 step on the stage kernel (PCG = true; nk_bk5_pcg at
+// N + 1 in 9..15 without an element list).
+template <int NQ, int NGS, int MINB>
+static int64_t stage_pcg_grid(int64_t nlist) {
+  static int64_t resident = -1;
+  if (resident < 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    using C = StageCfg<NQ, NGS, 2>;
+    auto kern = bk5_stage<NQ, NGS, 2, MINB, false, 1, false, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::THREADS, C::smem_bytes());
+    resident = (int64_t)sms * (per > 0 ? per : 1);
+  }
+  return nlist < resident ? nlist : resident;
+}
+
+template <int NQ, int NGS, int MINB>
+static int launch_stage_pcg(int64_t nlist, const double* Dhost, const double* G, double* p,
+                            double* w, double lam0, const double* B, double lam1,
+                            const uint8_t* mask, double* x, const double* r, const double* invD,
+                            nk_cg_state* st, double* partials, int64_t part_base,
+                            int64_t reduce_count, double* hist, cudaStream_t s) {
+  using C = StageCfg<NQ, NGS, 2>;
+  const int64_t grid = stage_pcg_grid<NQ, NGS, MINB>(nlist);
+  if (grid == 0) return NK_OK;
+  if ((reinterpret_cast<uintptr_t>(p) & 7) || (reinterpret_cast<uintptr_t>(G) & 15)) {
+    set_error("bk5_stage (PCG): p must be 8-byte and G 16-byte aligned");
+    return NK_ERR_INVALID;
+  }
+  DParam<NQ> D;
+  D.set(Dhost);
+  bk5_stage<NQ, NGS, 2, MINB, false, 1, false, true>
+      <<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
+          nlist, nullptr, D, G, p, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count,
+          nlist * (int64_t)C::NQ3, x, r, invD, hist);
+  return check_launch("bk5_stage_pcg");
 }
 
 #if defined(NK_BK5_NQ) && NK_BK5_NQ == 16   // one translation unit owns the N = 15 kernel

@@ -27,7 +27,7 @@ extern "C" int nk_bk5_set_variant(int v) {
 // on a 4 x 148-block grid for every CG vector kernel (N = 3: 0.0330 ->
 // 0.0309 ms, N = 9: 0.2235 -> 0.2171 ms, N = 7 neutral; r2zr_bp5_vec_grid.jsonl).
 static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1,
-                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2, 6};
+                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2, 6, 1};
 
 namespace nk {
 int knob(int k) { return (k >= 0 && k < NK_KNOB_COUNT) ? g_knobs[k] : 0; }

@@ -250,12 +250,15 @@ class JacobiPreconditioner:
 
 
 # orders whose fused BP5 step stays one kernel (N = 7: the TMA pipeline,
-# 0.117 vs 0.138 ms split); elsewhere FusedPCG splits it (split_step) once the
-# rank's mesh is large enough that the 4th launch pays for itself: measured
-# crossovers (scripts/split_crossover.py, profiles/r2zj_split_crossover*.jsonl,
-# per-iteration time fused vs split): ~1-2M local points at N <= 5 (the split
-# step is 10-30% SLOWER below), ~0.5-0.8M at N = 6..11, none at N >= 12.
-SPLIT_STEP_OFF = (7,)
+# 0.117 vs 0.138 ms split; N = 8, 9, 12: the stage kernel with the PCG head
+# fused, 0.110 / 0.111 / 0.113 vs 0.118 / 0.118 / 0.120 ms split,
+# profiles/r2zt_stage_pcg.jsonl); elsewhere FusedPCG splits it (split_step)
+# once the rank's mesh is large enough that the 4th launch pays for itself:
+# measured crossovers (scripts/split_crossover.py,
+# profiles/r2zj_split_crossover*.jsonl, per-iteration time fused vs split):
+# ~1-2M local points at N <= 5 (the split step is 10-30% SLOWER below),
+# ~0.5-0.8M at N = 6..11, none at N >= 12.
+SPLIT_STEP_OFF = (7, 8, 9, 12)
 
 
 def split_min_points(N):
@@ -280,8 +283,9 @@ class FusedPCG:
     split_step (one rank, fused gs): run nk_bk5_pcg's vector head as its own
     coalesced pass (nk_cg_xpstep) followed by nk_bk5 with the fused p.Ap --
     4 kernels per iteration.  None = auto: on where it measured faster than
-    the fused kernel -- every N except 7 (whose fused step is the TMA
-    pipeline) once the mesh has split_min_points(N) local points
+    the fused kernel -- every N not in SPLIT_STEP_OFF (7: the TMA pipeline;
+    8, 9, 12: the stage kernel with the PCG head fused) once the mesh has
+    split_min_points(N) local points
     (profiles/r2zj_split_crossover*.jsonl: 1.05-1.30x at the configs[1]
     sizes; below the crossover the fused step wins by up to 30%).
 

@@ -69,7 +69,8 @@ def test_knobs(L):
     assert L.nk_set_knob(0, old) == 0
     assert L.nk_set_knob(4, 2) == 2
     assert L.nk_set_knob(5, 6) == 6
-    assert L.nk_set_knob(6, 1) == -1 and L.nk_set_knob(-1, 0) == -1
+    assert L.nk_set_knob(6, 1) == 1
+    assert L.nk_set_knob(7, 1) == -1 and L.nk_set_knob(-1, 0) == -1
 
 
 @pytest.mark.parametrize("counts,N,bc", [((3, 2, 2), 3, "dirichlet"), ((4, 4, 4), 7, "periodic"),

@@ -383,7 +383,8 @@ def test_fused_pcg_split_step(counts, N, lam1):
         assert ra.residual_history == rb.residual_history
         assert torch.equal(ra.x, rb.x)
     sc = nk.FusedPCG(op, jac, tol=1e-9, max_iter=3000)
-    assert sc.split == (N != 7 and m.n_local >= nk.solvers.split_min_points(N))
+    assert sc.split == (N not in nk.solvers.SPLIT_STEP_OFF and
+                        m.n_local >= nk.solvers.split_min_points(N))
     rc = sc.solve(b)
     assert rc.converged and abs(rc.iterations - rb.iterations) <= 1
     Ax = torch.empty_like(b)

@@ -231,3 +231,32 @@ def test_cg_update_gs_pipelined_bit_identical(counts, N):
         assert o.iterations == out[0].iterations
         assert o.residual_history == out[0].residual_history
         assert torch.equal(o.x, out[0].x)
+
+
+@pytest.mark.parametrize("N,counts", [(8, (3, 3, 3)), (8, (10, 10, 10)), (9, (4, 3, 3)),
+                                      (10, (3, 3, 2)), (11, (3, 3, 3)), (12, (3, 2, 2)),
+                                      (13, (2, 2, 3)), (14, (3, 3, 3))])
+def test_stage_pcg_step_matches_split(N, counts):
+    """nk_bk5_pcg on the stage kernel with the PCG head fused into its F3
+    pass (N + 1 in 9..15, NK_KNOB_STAGE_PCG) against the split step
+    (nk_cg_xpstep + the stage BK5 with the fused p.Ap): the same per-point
+    arithmetic and the same partial-sum grouping, so iterations, residual
+    history and x are bit-identical; E = 1000 at N = 8 cycles every CTA's
+    buffers several times."""
+    m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, bc="dirichlet",
+                          deformation=("sine", 0.05))
+    g = torch.Generator(device="cuda").manual_seed(9)
+    b = torch.randn(m.n_local, dtype=torch.float64, device="cuda", generator=g)
+    op = nk.PoissonOperator(m)
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(torch.float64)
+    jac = nk.JacobiPreconditioner(op)
+    fused = nk.FusedPCG(op, jac, tol=1e-8, max_iter=3000, chunk=16, split_step=False)
+    split = nk.FusedPCG(op, jac, tol=1e-8, max_iter=3000, chunk=16, split_step=True)
+    rf, rs = fused.solve(b), split.solve(b)
+    assert rf.converged and rf.iterations == rs.iterations
+    assert rf.residual_history == rs.residual_history
+    assert torch.equal(rf.x, rs.x)
+    Ax = torch.empty_like(b)
+    op(rf.x.reshape(-1), out=Ax)
+    assert float(torch.linalg.norm(Ax - b)) <= 2e-8 * float(torch.linalg.norm(b))
