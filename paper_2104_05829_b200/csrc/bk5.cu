@@ -81,6 +81,7 @@ static int kvariant_for(int N) {
   if (v == 8) return (N >= 2 && N != 3) ? 8 : 3;   // stage: N + 1 in 3, 5..16
   if (v == 9) return (N >= 8 && N <= 14) ? 9 : 3;   // stage2: N + 1 in 9..15
   if (v == 10) return N == 15 ? 10 : 3;             // pair: N + 1 = 16
+  if (v == 11) return N == 2 ? 11 : 3;              // point: N + 1 = 3
   switch (N) {   // measured: profiles/r2s_bk5_order_sweep_evenodd.jsonl, r2x_stage_sweep.jsonl,
                  // r2ze_stage_low.jsonl
     case 2: return 5;                                                        // pencil2

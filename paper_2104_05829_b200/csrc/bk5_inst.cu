@@ -7,6 +7,7 @@
 #include "bk5_stage.cuh"
 #include "bk5_stage2.cuh"
 #include "bk5_pair.cuh"
+#include "bk5_point.cuh"
 
 #ifndef NK_BK5_NQ
 #error "compile with -DNK_BK5_NQ=<N+1>"
@@ -287,6 +288,20 @@ extern "C" int NK_CAT(nk_bk5_kslab_nq, NK_BK5_NQ)(int ncomp, int64_t nlist, cons
                                                       mask, st, partials, part_base, reduce_count);
       return check_launch("bk5_n1");
     }
+  }
+  if constexpr (NQ == 3) {
+    // point per thread (bk5_point.cuh): whole-array calls with 16-byte
+    // aligned u and G; element lists and other alignments take pencil2
+    if (variant == 11 && ncomp == 1 && elist == nullptr &&
+        ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(G)) & 15) == 0) {
+      if (nblocks) {
+        *nblocks = point3_blocks(nlist);
+        return NK_OK;
+      }
+      return launch_point3(nlist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base,
+                           reduce_count, s);
+    }
+    if (variant == 11) variant = 5;
   }
   if constexpr (NQ == 4 || NQ == 6 || NQ == 8) {
     if (variant == 4 && ncomp == 1) {

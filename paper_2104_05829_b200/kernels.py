@@ -338,7 +338,7 @@ def extract_diagonal(mesh, basis=None, spec="stiffness", gs=None, assemble=True)
 
 # BK5 variants (nk_bk5_set_variant): declaration order = tie-break order
 BK5_VARIANTS = {"kslab": 1, "pencil": 3, "pencil_tma": 4, "pencil2": 5, "seq3": 6, "dmma": 7,
-                "stage": 8, "stage2": 9, "pair": 10}
+                "stage": 8, "stage2": 9, "pair": 10, "point": 11}
 _VARIANT_REPORT = []
 
 
@@ -346,7 +346,7 @@ def bk5_variant_eligible(name, N, ncomp=1):
     """Which BK5 variants serve an order (the analogue of SPEC.md:426's
     "N_q=12 -> full3d not eligible"): pencil-TMA needs N+1 in {4, 6, 8};
     dmma (FP64 tensor cores, two 8-row tiles) N+1 in 9..16; stage (TMA-staged
-    operands) N+1 in 3, 5..16, stage2 N+1 in 9..15, pair N+1 = 16; seq3 serves
+    operands) N+1 in 3, 5..16, stage2 N+1 in 9..15, pair N+1 = 16, point N+1 = 3; seq3 serves
     3-component batches only."""
     if name not in BK5_VARIANTS:
         return False
@@ -360,6 +360,8 @@ def bk5_variant_eligible(name, N, ncomp=1):
         return ncomp == 1 and 9 <= N + 1 <= 15
     if name == "pair":    # one element per CTA pair (cluster; bk5_pair.cuh)
         return ncomp == 1 and N + 1 == 16
+    if name == "point":   # one thread per point (bk5_point.cuh)
+        return ncomp == 1 and N + 1 == 3
     if name == "seq3":   # 3 components back to back per CTA (bk5_pencil NC = 3)
         return ncomp == 3
     return True

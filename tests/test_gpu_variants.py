@@ -51,7 +51,8 @@ def test_select_variant_and_parity(N):
     (8, 13, (2, 3, 1)), (8, 14, (3, 3, 1)), (8, 15, (3, 2, 3)),
     (9, 8, (3, 3, 3)), (9, 9, (2, 2, 3)), (9, 11, (3, 2, 2)), (9, 12, (3, 3, 3)),
     (9, 13, (2, 3, 1)), (9, 14, (3, 3, 1)),
-    (10, 15, (3, 3, 3)), (10, 15, (1, 1, 1)), (10, 15, (7, 6, 5))])
+    (10, 15, (3, 3, 3)), (10, 15, (1, 1, 1)), (10, 15, (7, 6, 5)),
+    (11, 2, (3, 2, 2)), (11, 2, (7, 5, 3)), (11, 2, (30, 30, 30))])
 def test_dmma_variant_parity_fused(variant, N, counts):
     """Variant 7 (FP64 tensor-core contractions, bk5_dmma.cuh) and variant 8
     (TMA-staged operands, bk5_stage.cuh): persistent CTAs that each take
