@@ -181,7 +181,9 @@ int64_t nk_bk5_batch_blocks(int N, int64_t nlist);
  * 9 = stage2 (stage with two threads per pencil, N+1 in 9..15), 10 = pair
  * (one element per thread-block cluster of two CTAs split by k-planes:
  * multicast u, all six G components staged, gt exchanged through
- * distributed shared memory; N+1 = 16).  N = 1 always runs its point-per-lane kernel
+ * distributed shared memory; N+1 = 16), 11 = point (one thread per point,
+ * element groups staged by cp.async.bulk; N+1 = 3, whole-array calls with
+ * 16-byte aligned u and G, else pencil2).  N = 1 always runs its point-per-lane kernel
  * unless 1 is set.  Variants 3/4/5/7/8 serve ncomp = 1; with them forced,
  * ncomp = 3 uses pencil3 (k-slab for 1) or three scalar launches.  Returns
  * the previous value. */
