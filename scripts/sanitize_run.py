@@ -112,3 +112,27 @@ for N, counts in ((5, (2, 2, 2)), (4, (3, 2, 1))):
     nk.kernels.reset_kernel_variant()
 torch.cuda.synchronize()
 print("sanitize run (pMG / Schwarz / projection) ok")
+
+# late round-2 kernels: the single-buffer TMA BP5 step (N = 7, several
+# elements per CTA), the pipelined gs update (grid-stride trips), the stage
+# kernel with the fused PCG head (N = 8, 12), the N = 15 CTA-pair cluster
+# kernel (variant 10: multicast u, st.async exchange), the N = 2 point kernel
+# (variant 11, odd last group) and the stage16 kernel after the shared
+# address-space fix
+for N, counts, variant, split in ((7, (12, 12, 4), 0, False), (8, (10, 10, 3), 0, False),
+                                  (12, (4, 4, 3), 0, False), (15, (5, 4, 3), 10, True),
+                                  (15, (5, 4, 3), 8, True), (2, (7, 5, 3), 11, True)):
+    m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
+    u = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    L.nk_bk5_set_variant(variant)
+    nk.apply_stiffness_local(u, m)
+    nk.apply_helmholtz_local(u, m, 0.5, 2.0)
+    op = nk.PoissonOperator(m)
+    b = torch.randn(m.n_local, dtype=torch.float64, device="cuda")
+    nk.gs_op(op.gs, b)
+    b *= m.mask.reshape(-1).to(torch.float64)
+    nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-6, max_iter=4, use_graph=False,
+                split_step=split).solve(b)
+    L.nk_bk5_set_variant(0)
+torch.cuda.synchronize()
+print("sanitize run (late round-2 kernels) ok")
