@@ -237,6 +237,19 @@ int nk_bk5_tune(int cfg, int pf_dist);
 enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_FDM = 3,
        NK_KNOB_TMA = 4, NK_KNOB_CG_PIPE = 5, NK_KNOB_STAGE_PCG = 6, NK_KNOB_COUNT = 7 };
 int nk_set_knob(int knob, int value);
+/* chunk-gated stage BK5 (the host-buffer e2e stream, kernels.py
+ * _HostStream): while set (non-null), stage-kernel launches (variant 8, no
+ * element list) wait before staging element e's u until the device u64 at
+ * `gate` is >= e + 1 -- the copy engine writes there the element count each
+ * H2D chunk completes, so one persistent kernel consumes the chunks as they
+ * land.  The pointer is captured into the launch (CUDA graphs keep it);
+ * set nullptr afterwards.  A gate that never arrives times out after ~2 s
+ * (wrong results, no hang). */
+int nk_bk5_set_gate(const void* gate);
+/* stream-ordered 64-bit write of `value` to device memory `dptr` by the GPU
+ * front end (cuStreamWriteValue64), after all prior work on `stream`; the
+ * chunk gate's writer (no copy engine, no SM; graph-capturable). */
+int nk_stream_write_u64(void* dptr, uint64_t value, nk_stream_t stream);
 /* the device's maximum persisting-L2 set-aside in bytes (-1: no device). */
 int64_t nk_l2_set_aside_max(void);
 

@@ -68,6 +68,8 @@ _SIGS = {
     "nk_bk5_set_variant": ([_I32], _I32),
     "nk_bk5_tune": ([_I32, _I32], _I32),
     "nk_set_knob": ([_I32, _I32], _I32),
+    "nk_bk5_set_gate": ([_P], _I32),
+    "nk_stream_write_u64": ([_P, ctypes.c_uint64, _P], _I32),
     "nk_l2_set_aside_max": ([], _I64),
     "nk_local_diag": ([_I32, _I64, _P, _P, _D, _P, _D, _P, _P], _I32),
     "nk_gs_op": ([_I64, _P, _P, _P, _I32, _I32, _I64, _P, _P], _I32),

@@ -128,6 +128,32 @@ struct StageCfg {
 // the stop test and the last-block bookkeeping follow bk5_pencil_tma_pcg.
 // Same per-point arithmetic and the same p.Ap partial grouping as the split
 // step (nk_cg_xpstep + this kernel's fused dot): bit-identical solves.
+// Chunk-gated input (nk_bk5_set_gate; the host-buffer e2e stream): u arrives
+// in element order by copy-engine chunks, each followed by a copy of the
+// element count it completes into *gate; thread 0 waits until the elements
+// a u copy covers are in before issuing it.  Bounded spin (~2 s) so a
+// missing gate write cannot hang the device.
+__device__ __forceinline__ void gate_wait(const unsigned long long* gate, int64_t need) {
+  const long long t0 = clock64();
+  unsigned ns = 256;
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(gate) : "memory");
+    if ((int64_t)v >= need) break;
+    if (clock64() - t0 > 4000000000LL) break;
+    __nanosleep(ns);   // hundreds of CTAs poll one line: back off (chunks are ~10s of us apart)
+    if (ns < 4096) ns <<= 1;
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ bool gate_ready(const unsigned long long* gate, int64_t need) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(gate) : "memory");
+  return (int64_t)v >= need;
+}
+
 template <int NQ, int NGS, int NUB, int MINB, bool RINU = false, int EPB = 1,
           bool G4U = false, bool PCG = false>
 __global__ void __launch_bounds__(EPB * NQ * NQ, MINB)
@@ -137,7 +163,7 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
           const uint8_t* __restrict__ mask, nk_cg_state* st, double* __restrict__ partials,
           int64_t part_base, int64_t reduce_count, int64_t u_len, double* __restrict__ x = nullptr,
           const double* __restrict__ r = nullptr, const double* __restrict__ invD = nullptr,
-          double* __restrict__ hist = nullptr) {
+          double* __restrict__ hist = nullptr, const unsigned long long* gate = nullptr) {
   using L = StageLayout<NQ>;
   using C = StageCfg<NQ, NGS, NUB, RINU, EPB, G4U>;
   static_assert(!PCG || (EPB == 1 && NUB == 2 && !RINU && !G4U), "PCG: EPB 1, two u buffers");
@@ -188,7 +214,12 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     if (tail) cnt -= 2;
     return tail;
   };
+  auto gate_need = [&](int64_t grp) -> int64_t {   // elements group grp's copy covers
+    return (grp + 1) * EPB < nlist ? (grp + 1) * EPB : nlist;
+  };
+  bool upend = false;   // (thread 0, gated input) this group's u is not issued yet
   auto issue_u = [&](int64_t grp, int bi) {
+    if (gate != nullptr) gate_wait(gate, gate_need(grp));
     int64_t tot = 0;
     for (int l = 0; l < EPB; ++l) {
       if (grp * EPB + l >= nlist) break;
@@ -275,9 +306,19 @@ bk5_stage(int64_t nlist, const int32_t* __restrict__ elist, const __grid_constan
     if (G4U && t == 0) {   // this element's component NGS into the spare u buffer
       bulk_wait_read0();
       issue_g4(e, bi ^ 1);
-    } else if (NUB == 2 && t == 0 && slot + stride < ngroups) {
-      bulk_wait_read0();             // the other buffer's w (previous group) has left
-      issue_u(slot + stride, bi ^ 1);
+    } else if (NUB == 2 && t == 0) {
+      if (upend) {   // gated: this group's u was not in yet one group ago
+        issue_u(slot, bi);
+        upend = false;
+      }
+      if (slot + stride < ngroups) {
+        bulk_wait_read0();           // the other buffer's w (previous group) has left
+        // gated input: never block the current group on the next one's chunk
+        if (gate == nullptr || gate_ready(gate, gate_need(slot + stride)))
+          issue_u(slot + stride, bi ^ 1);
+        else
+          upend = true;
+      }
     }
     mbar_wait(&ubar[bi], NUB == 2 ? ((it >> 1) & 1) : (it & 1));
     double ut[NQ], o1[NQ];
@@ -546,8 +587,10 @@ static int launch_stage(int64_t nlist, const int32_t* elist, const double* Dhost
   }
   DParam<NQ> D;
   D.set(Dhost);
+  const unsigned long long* gate = elist == nullptr ? bk5_gate() : nullptr;
   bk5_stage<NQ, NGS, NUB, MINB, RINU, EPB, G4U><<<(unsigned)grid, C::THREADS, C::smem_bytes(), s>>>(
-      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, u_len);
+      nlist, elist, D, G, u, w, lam0, B, lam1, mask, st, partials, part_base, reduce_count, u_len,
+      nullptr, nullptr, nullptr, nullptr, gate);
   return check_launch("bk5_stage");
 }
 

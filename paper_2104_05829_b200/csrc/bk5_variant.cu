@@ -32,6 +32,10 @@ static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1,
 namespace nk {
 int knob(int k) { return (k >= 0 && k < NK_KNOB_COUNT) ? g_knobs[k] : 0; }
 
+static const unsigned long long* g_gate = nullptr;
+const unsigned long long* bk5_gate() { return g_gate; }
+void set_gate_ptr(const void* p) { g_gate = static_cast<const unsigned long long*>(p); }
+
 void l2_apply_set_aside() {
   static int applied = 0;   // the device default: no set-aside
   const int want = (g_knobs[NK_KNOB_L2] & kL2SetAside) ? 1 : 0;
@@ -62,4 +66,9 @@ extern "C" int nk_set_knob(int k, int value) {
   g_knobs[k] = value;
   if (k == NK_KNOB_L2) nk::l2_apply_set_aside();   // a host call: never inside a capture
   return old;
+}
+
+extern "C" int nk_bk5_set_gate(const void* gate) {
+  nk::set_gate_ptr(gate);
+  return NK_OK;
 }

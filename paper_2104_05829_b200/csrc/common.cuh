@@ -33,6 +33,9 @@ inline int check_launch(const char* what) {
 
 // Process-wide tuning knobs (nk_set_knob, include/nekb200.h): NK_KNOB_*.
 int knob(int k);
+// nk_bk5_set_gate: element-count gate of the streamed (chunk-gated) stage BK5
+const unsigned long long* bk5_gate();
+void set_gate_ptr(const void* p);
 
 // Programmatic dependent launch (PDL).  A kernel launched by launch_ex with
 // the knob on may be scheduled while its predecessor in the stream is still

@@ -5,6 +5,8 @@
 // 134M-point configurations do not spend minutes in host numpy.
 #include <climits>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace nk {
@@ -305,4 +307,34 @@ extern "C" int nk_l2_flush(void* buf, int64_t bytes, nk_stream_t stream) {
   int4* second = (int4*)buf + half16;
   l2_clean_kernel<<<148 * 8, 256, 0, S(stream)>>>(second, half16, (int*)buf);
   return check_launch("l2_clean");
+}
+
+// Stream-ordered 64-bit write by the GPU front end (cuStreamWriteValue64: no
+// copy engine, no SM), ordered after all prior work of the stream; capturable
+// into CUDA graphs (memory-operation node).  The chunk gate of the streamed
+// host-buffer BK5 (nk_bk5_set_gate).
+extern "C" int nk_stream_write_u64(void* dptr, uint64_t value, nk_stream_t stream) {
+  typedef CUresult (*Fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+  static Fn fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", reinterpret_cast<void**>(&fn),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr) {
+      fn = nullptr;
+      set_error("stream_write_u64: cuStreamWriteValue64 unavailable");
+      return NK_ERR_CUDA;
+    }
+  }
+  if (!dptr) {
+    set_error("stream_write_u64: null pointer");
+    return NK_ERR_INVALID;
+  }
+  const CUresult r = fn(reinterpret_cast<CUstream>(S(stream)),
+                        reinterpret_cast<CUdeviceptr>(dptr), value, 0);
+  if (r != CUDA_SUCCESS) {
+    set_error("stream_write_u64: cuStreamWriteValue64 failed (%d)", (int)r);
+    return NK_ERR_CUDA;
+  }
+  return NK_OK;
 }

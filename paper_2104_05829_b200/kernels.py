@@ -130,6 +130,11 @@ class _HostStream:
     bit-identical."""
 
     DIRECT_ORDERS = (7,)
+    # direct mode as ONE chunk-gated stage kernel (nk_bk5_set_gate) instead of
+    # one kernel per chunk: correct, measured slower (0.883 vs 0.860 ms at 8
+    # chunks, worse with more chunks: every chunk boundary stalls each
+    # persistent CTA on the arrival frontier; profiles/r2zw_e2e_stream.json)
+    STREAM = False
 
     def __init__(self, mesh, nchunks):
         import torch
@@ -140,6 +145,9 @@ class _HostStream:
         self.wd = torch.empty(n, dtype=torch.float64, device=mesh.device)
         self.s_in, self.s_cmp, self.s_out = (torch.cuda.Stream(device=mesh.device) for _ in range(3))
         self.graphs = {}
+        # stream mode: the device gate the kernel polls (element count of the
+        # H2D chunks landed so far)
+        self.gate = torch.zeros(1, dtype=torch.int64, device=mesh.device)
 
     def run(self, uh, wh, use_graph=True):
         """uh, wh: contiguous float64 host tensors.  Pinned buffers: the whole
@@ -209,7 +217,50 @@ class _HostStream:
                 wh[a:b].copy_(self.wd[a:b], non_blocking=True)
         main.wait_stream(self.s_out)
 
+    def _issue_stream(self, uh, wh):
+        """Direct mode, one kernel: the H2D chunks (and behind each, the
+        element count it completes into the device gate) run on the copy
+        engine while ONE persistent stage kernel, launched concurrently,
+        stages each element's u as soon as its chunk has landed and bulk-
+        stores w into the pinned host buffer -- no per-chunk kernel ramp /
+        tail gaps in the device -> host write stream."""
+        import torch
+        m = self.mesh
+        nq3 = m.nq ** 3
+        L = lib()
+        bounds = self._bounds(m.E)
+        main = torch.cuda.current_stream()
+        self.s_in.wait_stream(main)
+        check(L.nk_stream_write_u64(self.gate.data_ptr(), 0, self.s_in.cuda_stream),
+              "stream_write_u64")
+        with torch.cuda.stream(self.s_in):
+            ev0 = torch.cuda.Event()
+            ev0.record(self.s_in)
+        self.s_cmp.wait_event(ev0)
+        with torch.cuda.stream(self.s_in):
+            for c in range(self.nchunks):
+                a, b = int(bounds[c]) * nq3, int(bounds[c + 1]) * nq3
+                self.ud[a:b].copy_(uh[a:b], non_blocking=True)
+                # the element count this chunk completes, written by the GPU
+                # front end once the copy is done (a tiny H2D copy per chunk
+                # measured ~20 us each)
+                check(L.nk_stream_write_u64(self.gate.data_ptr(), int(bounds[c + 1]),
+                                            self.s_in.cuda_stream), "stream_write_u64")
+        old = L.nk_bk5_set_variant(BK5_VARIANTS["stage"])
+        L.nk_bk5_set_gate(self.gate.data_ptr())
+        try:
+            check(L.nk_bk5(m.N, m.E, ptr(m.basis.diff), ptr(m.G), self.ud.data_ptr(),
+                           wh.data_ptr(), 1.0, None, 0.0, 1, m.n_local, None, None, 0, None,
+                           None, 0, 0, self.s_cmp.cuda_stream), "bk5")
+        finally:
+            L.nk_bk5_set_gate(None)
+            L.nk_bk5_set_variant(old)
+        main.wait_stream(self.s_cmp)
+        main.wait_stream(self.s_in)
+
     def _issue_direct(self, uh, wh):
+        if self.STREAM:
+            return self._issue_stream(uh, wh)
         import torch
         m = self.mesh
         nq3 = m.nq ** 3

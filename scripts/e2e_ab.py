@@ -1,7 +1,8 @@
 """A/B of the host-buffer e2e apply (bench.py's protocol: L2 flushed, then
 apply_stiffness_local on pinned host u / w, CUDA events around the call):
 the copy pipeline (H2D / BK5 / D2H) vs the direct mode (H2D + stage-kernel
-bulk stores into host memory), alternating in one process."""
+bulk stores into host memory, one kernel per chunk) vs the stream mode (one
+chunk-gated stage kernel over all chunks), alternating in one process."""
 import json
 import os
 import statistics
@@ -23,9 +24,11 @@ flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 s = torch.cuda.current_stream()
 res = {}
 for rnd in range(4):
-    for mode, orders in (("copy", ()), ("direct", (7,))):
-        for nch in (6, 8):
+    for mode, orders, stream in (("copy", (), False), ("direct", (7,), False),
+                                 ("stream", (7,), True)):
+        for nch in ((6, 8) if mode != "stream" else (8, 16, 32)):
             K._HostStream.DIRECT_ORDERS = orders
+            K._HostStream.STREAM = stream
             m._host_stream = None
             for _ in range(3):
                 nk.apply_stiffness_local(uh, m, out=wh, nchunks=nch)

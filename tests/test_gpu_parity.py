@@ -511,19 +511,23 @@ def test_host_streamed_apply_matches_device_path():
     uh = torch.as_tensor(u).pin_memory()
     wh = torch.empty_like(uh).pin_memory()
     from paper_2104_05829_b200 import kernels as K
-    saved = K._HostStream.DIRECT_ORDERS
+    saved, saved_stream = K._HostStream.DIRECT_ORDERS, K._HostStream.STREAM
     try:
-        # N = 7: direct mode (H2D copies + the stage kernel's bulk stores into
-        # the pinned host w), then the H2D / BK5 / D2H copy pipeline
-        for direct in (saved, ()):
+        # N = 7: stream mode (one chunk-gated stage kernel), direct mode (one
+        # stage kernel per chunk; both bulk-store w into the pinned host w),
+        # then the H2D / BK5 / D2H copy pipeline; every case twice (the
+        # second call replays the cached graph: the gate must be re-armed)
+        for direct, stream in ((saved, True), (saved, False), ((), False)):
             K._HostStream.DIRECT_ORDERS = direct
+            K._HostStream.STREAM = stream
             m._host_stream = None
             for chunks in (None, 1, 7, 30):
-                wh.zero_()
-                nk.apply_stiffness_local(uh, m, out=wh, nchunks=chunks)
-                assert np.array_equal(wh.numpy(), wd), (direct, chunks)
+                for _ in range(2):
+                    wh.zero_()
+                    nk.apply_stiffness_local(uh, m, out=wh, nchunks=chunks)
+                    assert np.array_equal(wh.numpy(), wd), (direct, stream, chunks)
     finally:
-        K._HostStream.DIRECT_ORDERS = saved
+        K._HostStream.DIRECT_ORDERS, K._HostStream.STREAM = saved, saved_stream
         m._host_stream = None
     assert rel_l2(wd, oop.bk5(o.basis.diff, o.G, u)) < BK5_TOL
 
