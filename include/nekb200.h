@@ -230,7 +230,9 @@ int nk_bk5_tune(int cfg, int pf_dist);
  *     per-trip loads (bit-identical to each other).  Bit 4: the CG vector
  *     kernels' grid capped at 4 x 148 blocks instead of 8 x 148 (a different
  *     but still fixed, device-independent grouping of the dot partial sums).
- *     Default 6.
+ *     Default 6.  Applies to vectors of up to 2^24 points; larger ones (HBM-
+ *     streamed, not L2-resident) always run the per-trip form on 8 x 148
+ *     blocks (measured faster there).
  *   NK_KNOB_STAGE_PCG: nk_bk5_pcg at N + 1 in 9..15 (no element list) -- 1 =
  *     the stage kernel with the Jacobi-PCG head fused into its F3 pass
  *     (TMA-staged p and G); 0 = the register-pencil fused step. */

@@ -11,10 +11,19 @@
 
 namespace nk {
 
+// NK_KNOB_CG_PIPE applies to vectors up to kPipeMaxN points, whose w / r
+// stay largely L2-resident between the BK5 step and the update; above that
+// (pure HBM streaming, e.g. configs[2] / [4] on one GPU) the pipelined
+// update measured 7% slower (E = 64^3, N = 7: 3.72 vs 3.45 ms per BP5
+// iteration, profiles/r2zy_large_n_knobs.jsonl), so large vectors run the
+// per-trip form on the 8 x 148-block grid.
+constexpr int64_t kPipeMaxN = int64_t(1) << 24;
+static int cg_pipe(int64_t n) { return n <= kPipeMaxN ? knob(NK_KNOB_CG_PIPE) : 0; }
+
 // NK_KNOB_CG_PIPE bit 4: cap at 4 x 148 blocks (one resident wave of the
 // 64-register update kernels) instead of 8 x 148
 static int64_t vec_grid(int64_t n) {
-  const int64_t cap = (knob(NK_KNOB_CG_PIPE) & 4) ? kVecMaxBlocks / 2 : kVecMaxBlocks;
+  const int64_t cap = (cg_pipe(n) & 4) ? kVecMaxBlocks / 2 : kVecMaxBlocks;
   int64_t g = (n + kVecThreads - 1) / kVecThreads;
   if (g < 1) g = 1;
   if (g > cap) g = cap;
@@ -613,10 +622,10 @@ extern "C" int nk_cg_update_gs_seg(int64_t n, int ncomp, int64_t cstride, double
     if (segtab)
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<true>, g, dim3(kVecThreads), 0, s, n, r, w,
                 invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
-    else if ((knob(NK_KNOB_CG_PIPE) & 3) == 2)
+    else if ((cg_pipe(n) & 3) == 2)
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<false, 2>, g, dim3(kVecThreads), 0, s, n, r,
                 w, invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
-    else if ((knob(NK_KNOB_CG_PIPE) & 3) == 1)
+    else if ((cg_pipe(n) & 3) == 1)
       launch_ex(kPdlVec, cg_update_gs_vec_kernel<false, 1>, g, dim3(kVecThreads), 0, s, n, r,
                 w, invD, code, segtab, st, partials, cstride, pf, knob(NK_KNOB_L2));
     else

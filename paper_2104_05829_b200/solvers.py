@@ -849,6 +849,10 @@ class FusedPCG3:
         return x3, results
 
 
+# orders where the lockstep 3-component PCG beats three scalar solves
+BATCHED_HELM3_ORDERS = (10, 11, 12, 13)
+
+
 class HelmholtzVectorSolver:
     """Viscous substep solve:
     per-component Jacobi-PCG on H = lam0 A + lam1 B, e.g. lam0 = 1/Re,
@@ -865,8 +869,15 @@ class HelmholtzVectorSolver:
         self.tol, self.max_iter, self.chunk = tol, max_iter, chunk
         multi = self.op.gs.comm is not None and self.op.gs.comm.size > 1
         # batched (FusedPCG3, lockstep, G once per iteration for the three
-        # components): one rank; several ranks solve the components in turn
-        self.batched = (not multi) if batched is None else bool(batched)
+        # components): one rank, at the orders where it measured faster than
+        # three scalar FusedPCG solves -- the scalar step carries the round-2
+        # kernels (TMA step at N = 7, stage step with the fused PCG head,
+        # pipelined gs update), which outweigh reading G three times except
+        # at N = 10..13 (profiles/r2zz_helm3_batched_vs_seq.jsonl: e.g.
+        # configs[4], N = 9: 233 vs 249 ms; N = 12: 73 vs 70 ms); several
+        # ranks solve the components in turn
+        self.batched = ((not multi and mesh.N in BATCHED_HELM3_ORDERS) if batched is None
+                        else bool(batched))
         self._solver = None
         self.mesh = mesh
 

@@ -79,7 +79,9 @@ def test_fused_pcg3_vs_oracle_and_counters():
     m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, bc="dirichlet", deformation=("sine", 0.05))
     o = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, bc="dirichlet", deformation=("sine", 0.05))
     op = nk.PoissonOperator(m, lam0=lam0, lam1=lam1)
-    hv = nk.HelmholtzVectorSolver(m, lam0, lam1, tol=1e-8, max_iter=1000)
+    # auto: three scalar solves at N = 9 (measured faster), batched forced here
+    assert not nk.HelmholtzVectorSolver(m, lam0, lam1).batched
+    hv = nk.HelmholtzVectorSolver(m, lam0, lam1, tol=1e-8, max_iter=1000, batched=True)
     assert hv.batched and isinstance(hv.solver, nk.FusedPCG3)
     b3 = _rhs3(m, op, 7)
     COUNTERS.reset()
