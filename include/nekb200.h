@@ -70,6 +70,8 @@ typedef struct {
   int32_t max_iter;
   int32_t flexible;
   uint32_t ticket[4]; /* last-block-done counters (self-resetting)           */
+  uint32_t gen;       /* grid-barrier generation (nk_bk5_pcg_gs; monotonic)   */
+  uint32_t pad_;
 } nk_cg_state;
 
 /* ------------------------------------------------------------------ misc */
@@ -235,9 +237,15 @@ int nk_bk5_tune(int cfg, int pf_dist);
  *     blocks (measured faster there).
  *   NK_KNOB_STAGE_PCG: nk_bk5_pcg at N + 1 in 9..15 (no element list) -- 1 =
  *     the stage kernel with the Jacobi-PCG head fused into its F3 pass
- *     (TMA-staged p and G); 0 = the register-pencil fused step. */
+ *     (TMA-staged p and G); 0 = the register-pencil fused step.
+ *   NK_KNOB_GS_TAIL: nk_bk5_pcg_gs -- 1 = fold the edge / vertex gs into
+ *     the persistent N = 7 TMA step behind a grid barrier (one launch,
+ *     bit-identical); 0 (default: measured 5-7% slower per BP5 iteration
+ *     in graph replay, profiles/r2zzc_gs_tail_ab.jsonl) = nk_bk5_pcg
+ *     followed by nk_gs_op_classes. */
 enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_FDM = 3,
-       NK_KNOB_TMA = 4, NK_KNOB_CG_PIPE = 5, NK_KNOB_STAGE_PCG = 6, NK_KNOB_COUNT = 7 };
+       NK_KNOB_TMA = 4, NK_KNOB_CG_PIPE = 5, NK_KNOB_STAGE_PCG = 6, NK_KNOB_GS_TAIL = 7,
+       NK_KNOB_COUNT = 8 };
 int nk_set_knob(int knob, int value);
 /* chunk-gated stage BK5 (the host-buffer e2e stream, kernels.py
  * _HostStream): while set (non-null), stage-kernel launches (variant 8, no
@@ -269,6 +277,21 @@ int nk_bk5_pcg(int N, int64_t nelem, const double* D, const double* G, double* p
                const double* invD, nk_cg_state* st, double* partials, int64_t part_base,
                int64_t reduce_count, double* hist, nk_stream_t stream);
 int64_t nk_bk5_pcg_blocks(int N, int64_t nlist);
+/* nk_bk5_pcg over all elements (no element list) followed by the
+ * gather-scatter (+) of w over a classes plan -- on one rank, the >= 3-member
+ * (edge / vertex) segments that nk_cg_update_gs leaves out (SPEC.md:479-487:
+ * the operator + gs_op pair of one PCG iteration; the class table is
+ * nk_gs_op_classes's).  Where the step kernel is persistent (N = 7 TMA step,
+ * NK_KNOB_GS_TAIL) the gs runs inside it after a grid barrier, in the same
+ * lane order and fold as nk_gs_op_classes -- bit-identical, one launch
+ * fewer; otherwise the two launches.  Returns nk_bk5_pcg's status. */
+int nk_bk5_pcg_gs(int N, int64_t nelem, const double* D, const double* G, double* p, double* w,
+                  double lam0, const double* B, double lam1, const uint8_t* mask, double* x,
+                  const double* r, const double* invD, nk_cg_state* st, double* partials,
+                  int64_t reduce_count, double* hist, int nclass, const int32_t* sizes,
+                  const int64_t* nsegs, const int32_t* const* members, nk_stream_t stream);
+/* 1 if nk_bk5_pcg_gs at order N runs as one launch under the current knobs */
+int nk_bk5_pcg_gs_fused(int N);
 
 /* closed-form diag(lam0*A_e + lam1*B_e) per element (extract_diagonal
  * before assembly) */

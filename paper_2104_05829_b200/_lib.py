@@ -38,6 +38,7 @@ class CGState(ctypes.Structure):
         ("iter", ctypes.c_int32), ("done", ctypes.c_int32), ("converged", ctypes.c_int32),
         ("breakdown", ctypes.c_int32), ("max_iter", ctypes.c_int32),
         ("flexible", ctypes.c_int32), ("ticket", ctypes.c_uint32 * 4),
+        ("gen", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
     ]
 
 
@@ -65,6 +66,9 @@ _SIGS = {
     "nk_bk5_pcg": ([_I32, _I64, _P, _P, _P, _P, _D, _P, _D, _P, _P, _I64, _P, _P, _P, _P, _P,
                     _I64, _I64, _P, _P], _I32),
     "nk_bk5_pcg_blocks": ([_I32, _I64], _I64),
+    "nk_bk5_pcg_gs": ([_I32, _I64, _P, _P, _P, _P, _D, _P, _D, _P, _P, _P, _P, _P, _P, _I64,
+                       _P, _I32, _P, _P, _P, _P], _I32),
+    "nk_bk5_pcg_gs_fused": ([_I32], _I32),
     "nk_bk5_set_variant": ([_I32], _I32),
     "nk_bk5_tune": ([_I32, _I32], _I32),
     "nk_set_knob": ([_I32, _I32], _I32),

@@ -256,3 +256,50 @@ extern "C" int nk_bk5_pcg(int N, int64_t nelem, const double* D, const double* G
   return pcg_table[N](n, elem_list, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials,
                       part_base, reduce_count, hist, S(stream), nullptr);
 }
+
+// ---------------------------------------------- the step + edge/vertex gs
+extern "C" int nk_bk5_pcg_gs_fused(int N) {
+  return (knob(NK_KNOB_GS_TAIL) && N == 7 && nk_bk5_variant_get() != 3) ? 1 : 0;
+}
+
+extern "C" int nk_bk5_pcg_gs(int N, int64_t nelem, const double* D, const double* G, double* p,
+                             double* w, double lam0, const double* B, double lam1,
+                             const uint8_t* mask, double* x, const double* r,
+                             const double* invD, nk_cg_state* st, double* partials,
+                             int64_t reduce_count, double* hist, int nclass,
+                             const int32_t* sizes, const int64_t* nsegs,
+                             const int32_t* const* members, nk_stream_t stream) {
+  if (nclass < 0 || nclass > NK_GS_MAX_CLASSES || (nclass > 0 && (!sizes || !nsegs || !members))) {
+    set_error("bk5_pcg_gs: invalid class table (max %d classes)", NK_GS_MAX_CLASSES);
+    return NK_ERR_INVALID;
+  }
+  GsTail T{};
+  int64_t warps = 0;
+  int k = 0;
+  for (int c = 0; c < nclass; ++c) {
+    if (nsegs[c] <= 0) continue;
+    if (sizes[c] < 1 || sizes[c] > 32 || !members[c]) {
+      set_error("bk5_pcg_gs: class %d invalid (size %d; 1..32 allowed)", c, sizes[c]);
+      return NK_ERR_INVALID;
+    }
+    int mp = 1;
+    while (mp < sizes[c]) mp <<= 1;
+    T.M[k] = sizes[c];
+    T.Mp[k] = mp;
+    T.lanes[k] = nsegs[c] * mp;
+    T.mem[k] = members[c];
+    T.wstart[k] = warps;
+    warps += (T.lanes[k] + 31) / 32;
+    ++k;
+  }
+  T.n = k;
+  T.wstart[k] = warps;
+  const bool offer = k > 0 && nk_bk5_pcg_gs_fused(N);
+  gs_tail_set(offer ? &T : nullptr);
+  const int rc = nk_bk5_pcg(N, nelem, D, G, p, w, lam0, B, lam1, mask, nullptr, 0, x, r, invD, st,
+                            partials, 0, reduce_count, hist, stream);
+  const bool used = offer && gs_tail_used();
+  gs_tail_set(nullptr);
+  if (rc != NK_OK || used || k == 0) return rc;
+  return nk_gs_op_classes(nclass, sizes, nsegs, members, w, NK_OP_ADD, 1, 0, st, stream);
+}

@@ -27,10 +27,20 @@ extern "C" int nk_bk5_set_variant(int v) {
 // on a 4 x 148-block grid for every CG vector kernel (N = 3: 0.0330 ->
 // 0.0309 ms, N = 9: 0.2235 -> 0.2171 ms, N = 7 neutral; r2zr_bp5_vec_grid.jsonl).
 static int g_knobs[NK_KNOB_COUNT] = {nk::kPdlStep | nk::kPdlVec, 1,
-                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2, 6, 1};
+                                     nk::kL2StreamFirst | nk::kL2ReuseLast, 2, 2, 6, 1, 0};
 
 namespace nk {
 int knob(int k) { return (k >= 0 && k < NK_KNOB_COUNT) ? g_knobs[k] : 0; }
+
+static const GsTail* g_tail = nullptr;
+static bool g_tail_used = false;
+const GsTail* gs_tail_offer() { return g_tail; }
+void gs_tail_set(const GsTail* t) {
+  g_tail = t;
+  g_tail_used = false;
+}
+void gs_tail_mark_used() { g_tail_used = true; }
+bool gs_tail_used() { return g_tail_used; }
 
 static const unsigned long long* g_gate = nullptr;
 const unsigned long long* bk5_gate() { return g_gate; }

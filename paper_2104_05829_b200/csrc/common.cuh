@@ -37,6 +37,27 @@ int knob(int k);
 const unsigned long long* bk5_gate();
 void set_gate_ptr(const void* p);
 
+// The edge / vertex gather-scatter folded into the tail of the single-rank
+// fused BP5 step (nk_bk5_pcg_gs, NK_KNOB_GS_TAIL): the >= 3-member segments
+// of a classes plan, one lane per member as in gs_classes_kernel, laid out
+// as virtual warps of 32 lanes -- class c owns warps [wstart[c], wstart[c+1]),
+// its nseg * Mp lanes padded to a whole warp so no warp mixes classes.
+struct GsTail {
+  int n;                                  // classes; 0 = no tail
+  int M[NK_GS_MAX_CLASSES];               // members per segment
+  int Mp[NK_GS_MAX_CLASSES];              // M rounded up to a power of two
+  int64_t lanes[NK_GS_MAX_CLASSES];       // nseg * Mp
+  const int32_t* mem[NK_GS_MAX_CLASSES];  // member-major local indices
+  int64_t wstart[NK_GS_MAX_CLASSES + 1];
+};
+// host side: nk_bk5_pcg_gs offers its tail to the step launcher for the
+// duration of one nk_bk5_pcg call; a launcher that folds it in marks it used
+// (anything else leaves it to a separate nk_gs_op_classes launch).
+const GsTail* gs_tail_offer();
+void gs_tail_set(const GsTail* t);
+void gs_tail_mark_used();
+bool gs_tail_used();
+
 // Programmatic dependent launch (PDL).  A kernel launched by launch_ex with
 // the knob on may be scheduled while its predecessor in the stream is still
 // running; it executes its static-operand prologue (plan indices, G tiles,

@@ -298,7 +298,8 @@ class FusedPCG:
     vertex points; profiles/r2j_bp5_knobs.jsonl)."""
 
     def __init__(self, op, prec, tol=1e-8, max_iter=1000, flexible=False, chunk=16,
-                 use_graph=True, fuse_gs=True, split_step=None, gather_segments=False):
+                 use_graph=True, fuse_gs=True, split_step=None, gather_segments=False,
+                 gs_tail=None):
         import torch
         self.op, self.prec = op, prec
         self.tol, self.max_iter, self.flexible = float(tol), int(max_iter), bool(flexible)
@@ -351,6 +352,17 @@ class FusedPCG:
             self.launches_per_iter = 4    # xpstep, bk5 (+p.Ap), gs non-pair, update
         if self.gcodes is not None:
             self.launches_per_iter -= 1   # no gs pass
+        # the edge / vertex gs as the tail of the persistent step kernel
+        # (nk_bk5_pcg_gs: one launch fewer, bit-identical; N = 7 TMA step,
+        # NK_KNOB_GS_TAIL -- off by default: 5-7% slower per iteration in
+        # graph replay, profiles/r2zzc_gs_tail_ab.jsonl)
+        plan = self.codes[1] if self.codes is not None else None
+        can_tail = (self.comm is None and not self.split and self.gcodes is None and
+                    plan is not None and plan.rest is None and
+                    bool(lib().nk_bk5_pcg_gs_fused(op.mesh.N)))
+        self.gs_tail = can_tail if gs_tail is None else (bool(gs_tail) and can_tail)
+        if self.gs_tail:
+            self.launches_per_iter = 2    # bk5_pcg + gs tail, update
 
     def _allreduce(self, a, b):
         if self.comm is not None:
@@ -378,6 +390,8 @@ class FusedPCG:
             elif self.split:
                 self._split_head(L, s)
                 self._edge_vertex_gs()
+            elif self.gs_tail:
+                self._step_gs_tail(L, s)
             else:
                 self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
                                   self.part_bk5, self.hist, gs=False)
@@ -392,6 +406,18 @@ class FusedPCG:
                              ptr(self.wt), ptr(self.mult), ptr(self.st), ptr(self.part_cg), s),
               "cg_update")
         self._allreduce(2, 5)                                            # rz_new rr zap
+
+    def _step_gs_tail(self, L, s):
+        """nk_bk5_pcg_gs: the fused step with the >= 3-member gs folded into
+        its tail after a grid barrier (same bits as nk_bk5_pcg + the gs pass)."""
+        op, m, pl = self.op, self.op.mesh, self.codes[1]
+        nb = int(L.nk_bk5_pcg_blocks(m.N, m.E))
+        check(L.nk_bk5_pcg_gs(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p), ptr(self.w),
+                              op.lam0, ptr(m.B) if op.lam1 != 0.0 else None, op.lam1,
+                              ptr(m.mask), ptr(self.x), ptr(self.r), ptr(self.invD),
+                              ptr(self.st), ptr(self.part_bk5), nb, ptr(self.hist),
+                              pl.nclass, ptr(pl.sizes), ptr(pl.nsegs), ptr(pl.ptrs), s),
+              "bk5_pcg_gs")
 
     def _edge_vertex_gs(self):
         """The gs pass over the >= 3-member segments, unless the update
@@ -463,6 +489,8 @@ class FusedPCG:
             if split:
                 self._split_head(L, s, mid_event=ev[1])
                 ev = ev[1:]   # the remaining indices line up with the 3-kernel form
+            elif self.gs_tail:
+                self._step_gs_tail(L, s)
             else:
                 nb = int(L.nk_bk5_pcg_blocks(m.N, m.E))
                 check(L.nk_bk5_pcg(m.N, m.E, ptr(m.basis.diff), ptr(m.G), ptr(self.p),
@@ -472,7 +500,8 @@ class FusedPCG:
                                    ptr(self.hist), s), "bk5_pcg")
             ev[1].record()
             if fused:
-                self._edge_vertex_gs()
+                if not self.gs_tail:
+                    self._edge_vertex_gs()
                 ev[2].record()
                 self._update_gs(L, s)
                 ev[3].record()
@@ -489,8 +518,8 @@ class FusedPCG:
             for q, nm in enumerate(names):
                 acc[nm] += ev[q].elapsed_time(ev[q + 1])
         self.st.copy_(st_save)
-        if self.gcodes is not None:
-            acc.pop("gs_nonpair")    # folded into the update (gathered segments)
+        if self.gcodes is not None or self.gs_tail:
+            acc.pop("gs_nonpair")    # folded into the update / the step's tail
         return {k: v / reps for k, v in acc.items()}
 
     def init(self, b):

@@ -51,8 +51,10 @@ def test_version_error_and_state_layout(L):
     assert b"invalid" in L.nk_last_error()
     with pytest.raises(_lib.ContractError):
         _lib.check(rc, "gs_plan_build")
-    # nk_cg_state is 13 doubles-worth of bytes with the documented field order
-    assert _lib.CG_STATE_BYTES == 104
+    # nk_cg_state is 14 doubles-worth of bytes with the documented field order
+    # (the grid-barrier generation word of nk_bk5_pcg_gs last)
+    assert _lib.CG_STATE_BYTES == 112
+    assert _lib.CGState.gen.offset == 104
     assert _lib.CGState.done.offset == 68
 
 
@@ -62,7 +64,8 @@ def test_knobs(L):
     kernels = 5, one-trip L2 prefetch in the update = 1, L2 hints: streamed
     data evict_first + r / w evict_last = 3, FDM per-order auto table = 2,
     single-buffer order-7 TMA step at four CTAs per SM = 2, two-deep
-    pipelined fused gs update on a 4 x 148-block grid = 6)."""
+    pipelined fused gs update on a 4 x 148-block grid = 6, the stage kernel
+    with the PCG head fused = 1, the edge / vertex gs as the step's tail = 0: measured slower)."""
     assert L.nk_set_knob(0, 5) == 5 and L.nk_set_knob(1, 1) == 1
     assert L.nk_set_knob(2, 3) == 3 and L.nk_set_knob(3, 2) == 2
     old = L.nk_set_knob(0, 0)
@@ -70,7 +73,8 @@ def test_knobs(L):
     assert L.nk_set_knob(4, 2) == 2
     assert L.nk_set_knob(5, 6) == 6
     assert L.nk_set_knob(6, 1) == 1
-    assert L.nk_set_knob(7, 1) == -1 and L.nk_set_knob(-1, 0) == -1
+    assert L.nk_set_knob(7, 0) == 0
+    assert L.nk_set_knob(8, 1) == -1 and L.nk_set_knob(-1, 0) == -1
 
 
 @pytest.mark.parametrize("counts,N,bc", [((3, 2, 2), 3, "dirichlet"), ((4, 4, 4), 7, "periodic"),
