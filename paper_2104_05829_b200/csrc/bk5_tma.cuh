@@ -362,7 +362,7 @@ __device__ __forceinline__ void gs_tail_fold(const GsTail& T, double* w, int lan
   }
 }
 
-template <int NQ, int MINB, bool SB>
+template <int NQ, int MINB, bool SB, bool TAIL>
 __device__ __forceinline__ void tma_pcg_body(int64_t nlist, const int32_t* __restrict__ elist,
                    const DParam<NQ>& D, const double* __restrict__ G,
                    double* __restrict__ p, double* __restrict__ w, double lam0,
@@ -652,7 +652,7 @@ __device__ __forceinline__ void tma_pcg_body(int64_t nlist, const int32_t* __res
       }
     }
   };
-  if (tail.n > 0 && !stop) {  // every CTA of the grid takes this branch
+  if (TAIL && tail.n > 0 && !stop) {  // every CTA of the grid takes this branch
     const int lane = t & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (t >> 5);
@@ -686,7 +686,7 @@ __device__ __forceinline__ void tma_pcg_body(int64_t nlist, const int32_t* __res
   if (reduce_count > 0 && last_block(&st->ticket[0], gridDim.x)) finish();
 }
 
-template <int NQ, int MINB, bool SB = false>
+template <int NQ, int MINB, bool SB = false, bool TAIL = false>
 __global__ void __launch_bounds__(NQ * NQ, MINB)
 bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
                    const __grid_constant__ DParam<NQ> D, const double* __restrict__ G,
@@ -697,7 +697,7 @@ bk5_pencil_tma_pcg(int64_t nlist, const int32_t* __restrict__ elist,
                    double* __restrict__ partials, int64_t part_base, int64_t reduce_count,
                    double* __restrict__ hist, int pdl_flags, int l2_flags,
                    const __grid_constant__ GsTail tail) {
-  tma_pcg_body<NQ, MINB, SB>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base, reduce_count, hist, pdl_flags, l2_flags, tail);
+  tma_pcg_body<NQ, MINB, SB, TAIL>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base, reduce_count, hist, pdl_flags, l2_flags, tail);
 }
 
 // the same kernel with an explicit register cap (MINB = 5 under
@@ -714,16 +714,16 @@ bk5_pencil_tma_pcg_nreg(int64_t nlist, const int32_t* __restrict__ elist,
                    double* __restrict__ partials, int64_t part_base, int64_t reduce_count,
                    double* __restrict__ hist, int pdl_flags, int l2_flags,
                    const __grid_constant__ GsTail tail) {
-  tma_pcg_body<NQ, MINB, SB>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base, reduce_count, hist, pdl_flags, l2_flags, tail);
+  tma_pcg_body<NQ, MINB, SB, false>(nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st, partials, part_base, reduce_count, hist, pdl_flags, l2_flags, tail);
 }
 
-template <int NQ, int MINB, bool SB>
+template <int NQ, int MINB, bool SB, bool TAIL = false>
 static auto tma_pcg_kernel() {
-  if constexpr (SB && MINB == 5) return bk5_pencil_tma_pcg_nreg<NQ, MINB, SB, 200>;
-  else return bk5_pencil_tma_pcg<NQ, MINB, SB>;
+  if constexpr (SB && MINB == 5 && !TAIL) return bk5_pencil_tma_pcg_nreg<NQ, MINB, SB, 200>;
+  else return bk5_pencil_tma_pcg<NQ, MINB, SB, TAIL>;
 }
 
-template <int NQ, int MINB, bool SB = false>
+template <int NQ, int MINB, bool SB = false, bool TAIL = false>
 static int64_t tma_pcg_grid(int64_t nlist) {
   static int64_t resident = -1;
   if (resident < 0) {
@@ -731,9 +731,9 @@ static int64_t tma_pcg_grid(int64_t nlist) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     using C = TmaPcgCfg<NQ, MINB, SB>;
-    cudaFuncSetAttribute(tma_pcg_kernel<NQ, MINB, SB>(),
+    cudaFuncSetAttribute(tma_pcg_kernel<NQ, MINB, SB, TAIL>(),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tma_pcg_kernel<NQ, MINB, SB>(), C::THREADS,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tma_pcg_kernel<NQ, MINB, SB, TAIL>(), C::THREADS,
                                                   C::smem_bytes());
     resident = (int64_t)sms * (per > 0 ? per : 1);
   }
@@ -757,9 +757,17 @@ static int launch_pencil_tma_pcg(int64_t nlist, const int32_t* elist, const doub
   DParam<NQ> D;
   D.set(Dhost);
   GsTail tail{};
-  if (const GsTail* off = gs_tail_offer(); off != nullptr && elist == nullptr) {
-    tail = *off;   // the grid is persistent (<= resident CTAs): a barrier is safe
+  // the tail variant (its own instantiation: the plain step keeps its
+  // register count) needs the same grid, all of it resident, for the barrier
+  if (const GsTail* off = gs_tail_offer();
+      off != nullptr && elist == nullptr && tma_pcg_grid<NQ, MINB, SB, true>(nlist) == grid) {
+    tail = *off;
     gs_tail_mark_used();
+    launch_ex(kPdlStep, tma_pcg_kernel<NQ, MINB, SB, true>(), dim3((unsigned)grid),
+              dim3(C::THREADS), C::smem_bytes(), s, nlist, elist, D, G, p, w, lam0, B, lam1,
+              mask, x, r, invD, st, partials, part_base, reduce_count, hist, knob(NK_KNOB_PDL),
+              knob(NK_KNOB_L2), tail);
+    return check_launch("bk5_pencil_tma_pcg(gs tail)");
   }
   launch_ex(kPdlStep, tma_pcg_kernel<NQ, MINB, SB>(), dim3((unsigned)grid), dim3(C::THREADS),
             C::smem_bytes(), s, nlist, elist, D, G, p, w, lam0, B, lam1, mask, x, r, invD, st,

@@ -24,6 +24,7 @@ ap.add_argument("--pdl", default="", help="comma list of NK_KNOB_PDL values to s
 a = ap.parse_args()
 from paper_2104_05829_b200 import _lib  # noqa: E402
 L = _lib.lib()
+L.nk_set_knob(7, 1)   # NK_KNOB_GS_TAIL: lets FusedPCG(gs_tail=True) fold the tail
 counts = tuple(int(c) for c in a.counts.split(","))
 N = 7
 m = nk.build_box_mesh((1, 1, 1), counts, N, deformation=("sine", 0.05))
