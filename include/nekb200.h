@@ -242,7 +242,8 @@ int nk_bk5_tune(int cfg, int pf_dist);
  *     the persistent N = 7 TMA step behind a grid barrier (one launch,
  *     bit-identical); 0 (default: measured 5-7% slower per BP5 iteration
  *     in graph replay, profiles/r2zzc_gs_tail_ab.jsonl) = nk_bk5_pcg
- *     followed by nk_gs_op_classes. */
+ *     followed by nk_gs_op_classes.  2 = nk_cg_update_gs_cls runs the same
+ *     gs at the start of the update kernel (grid barrier, then the update). */
 enum { NK_KNOB_PDL = 0, NK_KNOB_CG_UPDATE = 1, NK_KNOB_L2 = 2, NK_KNOB_FDM = 3,
        NK_KNOB_TMA = 4, NK_KNOB_CG_PIPE = 5, NK_KNOB_STAGE_PCG = 6, NK_KNOB_GS_TAIL = 7,
        NK_KNOB_COUNT = 8 };
@@ -434,6 +435,16 @@ int nk_cg_update(int64_t n, double* x, double* r, const double* p, const double*
  * (SPEC.md:479-487). */
 int nk_cg_update_gs(int64_t n, double* r, const double* w, const double* invD,
                     const int32_t* code, nk_cg_state* st, double* partials, nk_stream_t stream);
+
+/* nk_gs_op_classes (+) on w over a classes plan -- the >= 3-member
+ * segments -- followed by nk_cg_update_gs: under NK_KNOB_GS_TAIL = 2 (16-B
+ * aligned r / w / invD, the pipelined update) ONE launch, the gs run by the
+ * update kernel's grid before a grid barrier, bit-identical; otherwise the
+ * two launches. */
+int nk_cg_update_gs_cls(int64_t n, double* r, double* w, const double* invD, const int32_t* code,
+                        int nclass, const int32_t* sizes, const int64_t* nsegs,
+                        const int32_t* const* members, nk_cg_state* st, double* partials,
+                        nk_stream_t stream);
 
 /* The vector head of nk_bk5_pcg as its own coalesced pass (iteration
  * k = st->iter): k > 0: stop test on st->rr, x += alpha_{k-1} p,

@@ -69,6 +69,7 @@ _SIGS = {
     "nk_bk5_pcg_gs": ([_I32, _I64, _P, _P, _P, _P, _D, _P, _D, _P, _P, _P, _P, _P, _P, _I64,
                        _P, _I32, _P, _P, _P, _P], _I32),
     "nk_bk5_pcg_gs_fused": ([_I32], _I32),
+    "nk_cg_update_gs_cls": ([_I64, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "nk_bk5_set_variant": ([_I32], _I32),
     "nk_bk5_tune": ([_I32, _I32], _I32),
     "nk_set_knob": ([_I32, _I32], _I32),

@@ -259,7 +259,7 @@ extern "C" int nk_bk5_pcg(int N, int64_t nelem, const double* D, const double* G
 
 // ---------------------------------------------- the step + edge/vertex gs
 extern "C" int nk_bk5_pcg_gs_fused(int N) {
-  return (knob(NK_KNOB_GS_TAIL) && N == 7 && nk_bk5_variant_get() != 3) ? 1 : 0;
+  return (knob(NK_KNOB_GS_TAIL) == 1 && N == 7 && nk_bk5_variant_get() != 3) ? 1 : 0;
 }
 
 extern "C" int nk_bk5_pcg_gs(int N, int64_t nelem, const double* D, const double* G, double* p,
@@ -269,31 +269,10 @@ extern "C" int nk_bk5_pcg_gs(int N, int64_t nelem, const double* D, const double
                              int64_t reduce_count, double* hist, int nclass,
                              const int32_t* sizes, const int64_t* nsegs,
                              const int32_t* const* members, nk_stream_t stream) {
-  if (nclass < 0 || nclass > NK_GS_MAX_CLASSES || (nclass > 0 && (!sizes || !nsegs || !members))) {
-    set_error("bk5_pcg_gs: invalid class table (max %d classes)", NK_GS_MAX_CLASSES);
-    return NK_ERR_INVALID;
-  }
   GsTail T{};
-  int64_t warps = 0;
-  int k = 0;
-  for (int c = 0; c < nclass; ++c) {
-    if (nsegs[c] <= 0) continue;
-    if (sizes[c] < 1 || sizes[c] > 32 || !members[c]) {
-      set_error("bk5_pcg_gs: class %d invalid (size %d; 1..32 allowed)", c, sizes[c]);
-      return NK_ERR_INVALID;
-    }
-    int mp = 1;
-    while (mp < sizes[c]) mp <<= 1;
-    T.M[k] = sizes[c];
-    T.Mp[k] = mp;
-    T.lanes[k] = nsegs[c] * mp;
-    T.mem[k] = members[c];
-    T.wstart[k] = warps;
-    warps += (T.lanes[k] + 31) / 32;
-    ++k;
-  }
-  T.n = k;
-  T.wstart[k] = warps;
+  const int rcb = gs_tail_build(T, nclass, sizes, nsegs, members);
+  if (rcb != NK_OK) return rcb;
+  const int k = T.n;
   const bool offer = k > 0 && nk_bk5_pcg_gs_fused(N);
   gs_tail_set(offer ? &T : nullptr);
   const int rc = nk_bk5_pcg(N, nelem, D, G, p, w, lam0, B, lam1, mask, nullptr, 0, x, r, invD, st,

@@ -309,59 +309,6 @@ struct TmaPcgCfg {
   static size_t smem_bytes() { return sizeof(double) * (NST * STAGE + 3 * VOL + 32) + 2 * 8; }
 };
 
-// ---- the edge / vertex gs as the step's tail (nk_bk5_pcg_gs) ------------
-// After the element loop every CTA meets a grid barrier (the grid is
-// persistent: at most the resident CTA count), then the CTA's warps work
-// through virtual warps gw, gw + nw, ... of the GsTail, kTailU at a time:
-// all member-index loads, then all value loads, then per slot the same
-// shuffle fold as gs_classes_kernel (member order, ascending local index)
-// -- bit-identical to the separate nk_gs_op_classes launch.
-constexpr int kTailU = 8;
-
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* a) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void gs_tail_idx(const GsTail& T, int64_t v0, int64_t nw, int lane,
-                                            int (&idx)[kTailU], int (&cls)[kTailU]) {
-  const int64_t W = T.wstart[T.n];
-#pragma unroll
-  for (int u = 0; u < kTailU; ++u) {
-    const int64_t v = v0 + (int64_t)u * nw;
-    int c = -1, ix = -1;
-    if (v < W) {
-      c = 0;
-      while (c + 1 < T.n && v >= T.wstart[c + 1]) ++c;
-      const int64_t l = (v - T.wstart[c]) * 32 + lane;
-      if (l < T.lanes[c]) ix = __ldg(T.mem[c] + l);
-    }
-    idx[u] = ix;
-    cls[u] = c;
-  }
-}
-
-// w was written by other CTAs of this grid: L2 loads (ld.global.cg), never
-// the read-only path
-__device__ __forceinline__ void gs_tail_fold(const GsTail& T, double* w, int lane,
-                                             const int (&idx)[kTailU], const int (&cls)[kTailU]) {
-  double v[kTailU];
-#pragma unroll
-  for (int u = 0; u < kTailU; ++u) v[u] = idx[u] >= 0 ? __ldcg(w + idx[u]) : 0.0;
-#pragma unroll
-  for (int u = 0; u < kTailU; ++u) {
-    const int c = cls[u];   // warp-uniform
-    if (c < 0) continue;
-    const int M = T.M[c], Mp = T.Mp[c];
-    const int m = lane & (Mp - 1);
-    double acc = v[u];
-    for (int j = 1; j < M; ++j) acc = acc + __shfl_down_sync(0xffffffffu, v[u], j, Mp);
-    const double res = __shfl_sync(0xffffffffu, acc, lane - m);
-    if (idx[u] >= 0) w[idx[u]] = res;
-  }
-}
-
 template <int NQ, int MINB, bool SB, bool TAIL>
 __device__ __forceinline__ void tma_pcg_body(int64_t nlist, const int32_t* __restrict__ elist,
                    const DParam<NQ>& D, const double* __restrict__ G,
@@ -659,24 +606,8 @@ __device__ __forceinline__ void tma_pcg_body(int64_t nlist, const int32_t* __res
     const int64_t W = tail.wstart[tail.n];
     int idx[kTailU], cls[kTailU];
     gs_tail_idx(tail, gw, nw, lane, idx, cls);  // plan data: in flight across the barrier
-    __shared__ int s_last;
-    __syncthreads();
-    if (t == 0) {  // grid barrier: arrival ticket[0] (self-resetting), release st->gen
-      const uint32_t g0 = ld_acquire_u32(&st->gen);
-      __threadfence();
-      const uint32_t old = atomicAdd(&st->ticket[0], 1u);
-      s_last = old == gridDim.x - 1;
-      if (s_last) {
-        st->ticket[0] = 0u;
-        __threadfence();
-        atomicAdd(&st->gen, 1u);
-      } else {
-        while (ld_acquire_u32(&st->gen) == g0) __nanosleep(32);
-      }
-      __threadfence();
-    }
-    __syncthreads();
-    if (s_last && reduce_count > 0) finish();
+    const bool last = grid_barrier(st);
+    if (last && reduce_count > 0) finish();
     for (int64_t v0 = gw; v0 < W; v0 += (int64_t)kTailU * nw) {
       if (v0 != gw) gs_tail_idx(tail, v0, nw, lane, idx, cls);
       gs_tail_fold(tail, w, lane, idx, cls);

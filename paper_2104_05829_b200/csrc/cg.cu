@@ -654,6 +654,179 @@ extern "C" int nk_cg_update_gs(int64_t n, double* r, const double* w, const doub
   return nk_cg_update_gs_batch(n, 1, 0, r, w, invD, code, st, partials, stream);
 }
 
+// nk_cg_update_gs_cls, NK_KNOB_GS_TAIL = 2: the gs over the >= 3-member
+// segments run by the update kernel itself before its first trip (one launch
+// instead of gs_classes_kernel + cg_update_gs_vec_kernel<false, 2>).  The
+// grid is one resident wave (vec_grid: 4 x 148 blocks of 256 threads), so
+// after its share of the segments every CTA meets a grid barrier, then runs
+// the two-deep pipelined update of cg_update_gs_vec_kernel<false, 2> (same
+// per-thread point order and accumulation: bit-identical) with w read through
+// coherent (non-.nc) loads, since this launch wrote it.
+__global__ void __launch_bounds__(kVecThreads, 4)
+cg_update_gs_pre_kernel(int64_t n, double* __restrict__ r, double* w,
+                        const double* __restrict__ invD, const int32_t* __restrict__ code,
+                        nk_cg_state* st, double* __restrict__ partials,
+                        const __grid_constant__ GsTail tail, int pf, int l2_flags) {
+  __shared__ double red[3 * 32];
+  __shared__ double rcp_tab[256];
+  for (int q = threadIdx.x; q < 256; q += blockDim.x) rcp_tab[q] = q ? 1.0 / (double)q : 0.0;
+  const bool hz = invD != nullptr;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t np = n >> 1;
+  const uint64_t pol_s = l2_policy(l2_flags & kL2StreamFirst ? 1 : 0);   // code
+  const uint64_t pol_r = l2_policy(l2_flags & kL2ReuseLast ? 2 : 0);     // r, w
+  const uint64_t pol_d = l2_policy(l2_flags & kL2InvDLast ? 2 : 0);      // invD
+  auto pf_trip = [&](int64_t k, bool stat, bool dyn) {
+    const int64_t q0 = k * nthr + (int64_t)blockIdx.x * blockDim.x;
+    if (q0 >= np) return;
+    const int64_t cnt = np - q0 < (int64_t)blockDim.x ? np - q0 : (int64_t)blockDim.x;
+    if (stat) {
+      prefetch_l2_hint(code + 2 * q0, cnt * 8, pol_s);
+      if (hz) prefetch_l2_hint(invD + 2 * q0, cnt * 16, pol_d);
+    }
+    if (dyn) {
+      prefetch_l2_hint(r + 2 * q0, cnt * 16, pol_r);
+      prefetch_l2_hint(w + 2 * q0, cnt * 16, pol_r);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int k = 1; k <= pf; ++k) pf_trip(k, true, false);
+  int2 cv = gtid < np ? ldg2i_hint(code + 2 * gtid, pol_s) : make_int2(-1, -1);
+  double2 dv = (gtid < np && hz) ? ldg2_hint(invD + 2 * gtid, pol_d) : make_double2(0, 0);
+  // the gs plan is static: the first round's member indices before pdl_wait
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t W = tail.wstart[tail.n];
+  int idx[kTailU], cls[kTailU];
+  gs_tail_idx(tail, gw, nw, lane, idx, cls);
+  pdl_wait();
+  pdl_trigger();
+  if (st->done) return;               // uniform over the grid: before the barrier
+  __syncthreads();
+  const double pAp = st->pAp;
+  if (!(pAp > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->breakdown = 1;
+      st->done = 1;
+    }
+    return;
+  }
+  const double alpha = st->rz / pAp;
+  for (int64_t v0 = gw; v0 < W; v0 += (int64_t)kTailU * nw) {
+    if (v0 != gw) gs_tail_idx(tail, v0, nw, lane, idx, cls);
+    gs_tail_fold(tail, w, lane, idx, cls);
+  }
+  grid_barrier(st);
+  UpdAcc acc;
+  if (threadIdx.x == 0)
+    for (int k = 1; k <= pf; ++k) pf_trip(k, false, true);
+  int64_t k = 0;
+  double2 rv = make_double2(0, 0), av = make_double2(0, 0);
+  double px = 0.0, py = 0.0;
+  int2 cv1 = make_int2(-1, -1);
+  if (gtid < np) {
+    rv = ld2_hint(r + 2 * gtid, pol_r);
+    av = ld2_hint(w + 2 * gtid, pol_r);
+    if (cv.x >= 0) px = __ldcg(w + cv.x);
+    if (cv.y >= 0) py = __ldcg(w + cv.y);
+    if (gtid + nthr < np) cv1 = ldg2i_hint(code + 2 * (gtid + nthr), pol_s);
+  }
+  for (int64_t q = gtid; q < np; q += nthr, ++k) {
+    if (pf > 0 && threadIdx.x == 0) pf_trip(k + 1 + pf, true, true);
+    const int64_t qn = q + nthr;
+    double2 dvn = make_double2(0, 0), rvn = make_double2(0, 0), avn = make_double2(0, 0);
+    double pxn = 0.0, pyn = 0.0;
+    int2 cv2 = make_int2(-1, -1);
+    if (qn < np) {
+      if (hz) dvn = ldg2_hint(invD + 2 * qn, pol_d);
+      rvn = ld2_hint(r + 2 * qn, pol_r);
+      avn = ld2_hint(w + 2 * qn, pol_r);
+      if (cv1.x >= 0) pxn = __ldcg(w + cv1.x);
+      if (cv1.y >= 0) pyn = __ldcg(w + cv1.y);
+      if (qn + nthr < np) cv2 = ldg2i_hint(code + 2 * (qn + nthr), pol_s);
+    }
+    double2 wv;
+    gs_point_seg(cv.x, av.x, px, 0, av.x, wv.x, rcp_tab);
+    gs_point_seg(cv.y, av.y, py, 0, av.y, wv.y, rcp_tab);
+    double xd = 0.0;
+    upd_point<true>(alpha, xd, rv.x, 0.0, av.x, dv.x, wv.x, hz, acc);
+    upd_point<true>(alpha, xd, rv.y, 0.0, av.y, dv.y, wv.y, hz, acc);
+    st2_hint(r + 2 * q, rv, pol_r);
+    cv = cv1;
+    cv1 = cv2;
+    dv = dvn;
+    rv = rvn;
+    av = avn;
+    px = pxn;
+    py = pyn;
+  }
+  if ((n & 1) && gtid == 0) {
+    const int64_t t = n - 1;
+    double xd = 0.0, at = 0.0, wq = 0.0;
+    const int32_t c = code[t];
+    const double pt = c >= 0 ? __ldcg(w + c) : 0.0;
+    gs_point_seg(c, __ldcg(w + t), pt, 0, at, wq, rcp_tab);
+    upd_point<true>(alpha, xd, r[t], 0.0, at, hz ? invD[t] : 0.0, wq, hz, acc);
+  }
+  double v[3] = {acc.rr, acc.rz, acc.zap};
+  block_sum<3>(v, red);
+  const int nb = gridDim.x;
+  if (threadIdx.x == 0) {
+    partials[0 * kVecMaxBlocks + blockIdx.x] = v[0];
+    partials[1 * kVecMaxBlocks + blockIdx.x] = v[1];
+    partials[2 * kVecMaxBlocks + blockIdx.x] = v[2];
+  }
+  if (last_block(&st->ticket[1], nb)) {
+    double sres[3];
+    reduce_partials<3>(partials, nb, kVecMaxBlocks, sres, red);
+    if (threadIdx.x == 0) {
+      st->rr = sres[0];
+      if (hz) st->rz_new = sres[1];
+      st->zap = sres[2];
+      st->alpha = alpha;
+      st->iter = st->iter + 1;
+    }
+  }
+}
+
+extern "C" int nk_cg_update_gs_cls(int64_t n, double* r, double* w, const double* invD,
+                                   const int32_t* code, int nclass, const int32_t* sizes,
+                                   const int64_t* nsegs, const int32_t* const* members,
+                                   nk_cg_state* st, double* partials, nk_stream_t stream) {
+  if (n < 0 || !r || !w || !code || !st || !partials) {
+    set_error("cg_update_gs_cls: invalid arguments");
+    return NK_ERR_INVALID;
+  }
+  GsTail T{};
+  int rc = gs_tail_build(T, nclass, sizes, nsegs, members);
+  if (rc != NK_OK) return rc;
+  bool fuse = T.n > 0 && knob(NK_KNOB_GS_TAIL) == 2 && aligned16(r, w, invD) &&
+              ((uintptr_t)code & 7) == 0 && (cg_pipe(n) & 3) == 2;
+  const int64_t g = vec_grid(n);
+  if (fuse) {
+    static int per = -1, sms = 0;
+    if (per < 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_update_gs_pre_kernel, kVecThreads, 0);
+    }
+    fuse = (int64_t)per * sms >= g;   // the barrier needs the whole grid resident
+  }
+  if (!fuse) {
+    if (T.n > 0) {
+      rc = nk_gs_op_classes(nclass, sizes, nsegs, members, w, NK_OP_ADD, 1, 0, st, stream);
+      if (rc != NK_OK) return rc;
+    }
+    return nk_cg_update_gs(n, r, w, invD, code, st, partials, stream);
+  }
+  launch_ex(kPdlVec, cg_update_gs_pre_kernel, dim3((unsigned)g), dim3(kVecThreads), 0, S(stream),
+            n, r, w, invD, code, st, partials, T, knob(NK_KNOB_CG_UPDATE), knob(NK_KNOB_L2));
+  return check_launch("cg_update_gs_pre");
+}
+
 extern "C" int nk_cg_pupdate(int64_t n, const double* r, double* p, const double* invD,
                              const double* z, nk_cg_state* st, double* hist, nk_stream_t stream) {
   if (n < 0 || !r || !p || !st) {

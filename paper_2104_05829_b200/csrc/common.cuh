@@ -53,6 +53,9 @@ struct GsTail {
 // host side: nk_bk5_pcg_gs offers its tail to the step launcher for the
 // duration of one nk_bk5_pcg call; a launcher that folds it in marks it used
 // (anything else leaves it to a separate nk_gs_op_classes launch).
+// validate a nk_gs_op_classes class table into a GsTail (T.n = 0: nothing)
+int gs_tail_build(GsTail& T, int nclass, const int32_t* sizes, const int64_t* nsegs,
+                  const int32_t* const* members);
 const GsTail* gs_tail_offer();
 void gs_tail_set(const GsTail* t);
 void gs_tail_mark_used();
@@ -241,6 +244,85 @@ __device__ __forceinline__ bool last_block(uint32_t* ticket, uint32_t nblocks) {
   __syncthreads();
   if (is_last) __threadfence();
   return is_last;
+}
+
+// ---- the edge / vertex gs inside a persistent kernel (nk_bk5_pcg_gs's
+// step tail, nk_cg_update_gs's gs prologue) -------------------------------
+// The kernel's warps (grid persistent: at most the resident CTA count) work
+// through virtual warps gw, gw + nw, ... of the GsTail, kTailU at a time:
+// all member-index loads, then all value loads, then per slot the same
+// shuffle fold as gs_classes_kernel (member order, ascending local index)
+// -- bit-identical to the separate nk_gs_op_classes launch.
+constexpr int kTailU = 8;
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+
+// Grid barrier for a grid whose CTAs are all resident: arrival on
+// st->ticket[0] (self-resetting, so last_block users of ticket[0] in other
+// launches see 0), release through the monotonic st->gen.  Prior global
+// writes of every CTA are visible after it.  Returns true in the one CTA
+// that arrived last.  Every thread of every CTA must call it.
+__device__ __forceinline__ bool grid_barrier(nk_cg_state* st) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t g0 = ld_acquire_u32(&st->gen);
+    __threadfence();
+    const uint32_t old = atomicAdd(&st->ticket[0], 1u);
+    s_last = old == gridDim.x - 1;
+    if (s_last) {
+      st->ticket[0] = 0u;
+      __threadfence();
+      atomicAdd(&st->gen, 1u);
+    } else {
+      while (ld_acquire_u32(&st->gen) == g0) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
+__device__ __forceinline__ void gs_tail_idx(const GsTail& T, int64_t v0, int64_t nw, int lane,
+                                            int (&idx)[kTailU], int (&cls)[kTailU]) {
+  const int64_t W = T.wstart[T.n];
+#pragma unroll
+  for (int u = 0; u < kTailU; ++u) {
+    const int64_t v = v0 + (int64_t)u * nw;
+    int c = -1, ix = -1;
+    if (v < W) {
+      c = 0;
+      while (c + 1 < T.n && v >= T.wstart[c + 1]) ++c;
+      const int64_t l = (v - T.wstart[c]) * 32 + lane;
+      if (l < T.lanes[c]) ix = __ldg(T.mem[c] + l);
+    }
+    idx[u] = ix;
+    cls[u] = c;
+  }
+}
+
+// w was written by other CTAs of this grid: L2 loads (ld.global.cg), never
+// the read-only path
+__device__ __forceinline__ void gs_tail_fold(const GsTail& T, double* w, int lane,
+                                             const int (&idx)[kTailU], const int (&cls)[kTailU]) {
+  double v[kTailU];
+#pragma unroll
+  for (int u = 0; u < kTailU; ++u) v[u] = idx[u] >= 0 ? __ldcg(w + idx[u]) : 0.0;
+#pragma unroll
+  for (int u = 0; u < kTailU; ++u) {
+    const int c = cls[u];   // warp-uniform
+    if (c < 0) continue;
+    const int M = T.M[c], Mp = T.Mp[c];
+    const int m = lane & (Mp - 1);
+    double acc = v[u];
+    for (int j = 1; j < M; ++j) acc = acc + __shfl_down_sync(0xffffffffu, v[u], j, Mp);
+    const double res = __shfl_sync(0xffffffffu, acc, lane - m);
+    if (idx[u] >= 0) w[idx[u]] = res;
+  }
 }
 
 // Fixed-order sum of partials[0..n) by one block; valid in thread 0.

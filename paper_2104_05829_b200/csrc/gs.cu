@@ -141,6 +141,36 @@ static unsigned grid_for(int64_t n, int threads) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
 }
 
+int gs_tail_build(GsTail& T, int nclass, const int32_t* sizes, const int64_t* nsegs,
+                  const int32_t* const* members) {
+  T = GsTail{};
+  if (nclass < 0 || nclass > NK_GS_MAX_CLASSES || (nclass > 0 && (!sizes || !nsegs || !members))) {
+    set_error("gs classes: invalid class table (max %d classes)", NK_GS_MAX_CLASSES);
+    return NK_ERR_INVALID;
+  }
+  int64_t warps = 0;
+  int k = 0;
+  for (int c = 0; c < nclass; ++c) {
+    if (nsegs[c] <= 0) continue;
+    if (sizes[c] < 1 || sizes[c] > 32 || !members[c]) {
+      set_error("gs classes: class %d invalid (size %d; 1..32 allowed)", c, sizes[c]);
+      return NK_ERR_INVALID;
+    }
+    int mp = 1;
+    while (mp < sizes[c]) mp <<= 1;
+    T.M[k] = sizes[c];
+    T.Mp[k] = mp;
+    T.lanes[k] = nsegs[c] * mp;
+    T.mem[k] = members[c];
+    T.wstart[k] = warps;
+    warps += (T.lanes[k] + 31) / 32;
+    ++k;
+  }
+  T.n = k;
+  T.wstart[k] = warps;
+  return NK_OK;
+}
+
 }  // namespace nk
 
 using namespace nk;

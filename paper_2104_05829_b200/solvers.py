@@ -387,16 +387,16 @@ class FusedPCG:
                     self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
                                       self.part_bk5, self.hist, local=self.codes[1])
                 self._allreduce(1, 2)                                    # pAp
-            elif self.split:
-                self._split_head(L, s)
-                self._edge_vertex_gs()
             elif self.gs_tail:
                 self._step_gs_tail(L, s)
+                self._update_gs(L, s)
             else:
-                self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
-                                  self.part_bk5, self.hist, gs=False)
-                self._edge_vertex_gs()
-            self._update_gs(L, s)
+                if self.split:
+                    self._split_head(L, s)
+                else:
+                    self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
+                                      self.part_bk5, self.hist, gs=False)
+                self._gs_update(L, s)
             self._allreduce(2, 5)                                        # rz_new rr zap
             return
         self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st, self.part_bk5,
@@ -424,6 +424,19 @@ class FusedPCG:
         gathers them itself."""
         if self.gcodes is None:
             self.codes[1].run(self.w, "+", 1, self.n, self.st)
+
+    def _gs_update(self, L, s):
+        """The edge / vertex gs pass + the update: nk_cg_update_gs_cls (one
+        launch under NK_KNOB_GS_TAIL = 2, else the same two launches)."""
+        pl = self.codes[1]
+        if self.gcodes is not None or pl.rest is not None:
+            self._edge_vertex_gs()
+            self._update_gs(L, s)
+            return
+        check(L.nk_cg_update_gs_cls(self.n, ptr(self.r), ptr(self.w), ptr(self.invD),
+                                    ptr(self.codes[0]), pl.nclass, ptr(pl.sizes), ptr(pl.nsegs),
+                                    ptr(pl.ptrs), ptr(self.st), ptr(self.part_cg), s),
+              "cg_update_gs_cls")
 
     def _update_gs(self, L, s):
         """nk_cg_update_gs (face pairs folded in) or, with gathered segments,

@@ -20,6 +20,8 @@ import paper_2104_05829_b200 as nk  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--counts", default="20,20,20")
 ap.add_argument("--reps", type=int, default=15)
+ap.add_argument("--mode2", action="store_true",
+                help="NK_KNOB_GS_TAIL = 2 (gs at the start of the update kernel) vs 0")
 ap.add_argument("--pdl", default="", help="comma list of NK_KNOB_PDL values to sweep")
 a = ap.parse_args()
 from paper_2104_05829_b200 import _lib  # noqa: E402
@@ -39,9 +41,11 @@ for pdl in pdls:
     old = L.nk_set_knob(0, pdl)
   solvers = {}
   for tail in (True, False):
+    if a.mode2:
+        L.nk_set_knob(7, 2 if tail else 0)
     s = nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-30, max_iter=100, chunk=100,
-                    split_step=False, gs_tail=tail)
-    s.solve(b)
+                    split_step=False, gs_tail=tail and not a.mode2)
+    s.solve(b)   # captures the graph under the current knob
     solvers[tail] = s
   ts = {True: [], False: []}
   for _ in range(a.reps):
@@ -59,8 +63,10 @@ for pdl in pdls:
     L.nk_set_knob(0, old)
 res = {}
 for tail in (True, False):
+    if a.mode2:
+        L.nk_set_knob(7, 2 if tail else 0)
     sc = nk.FusedPCG(op, nk.JacobiPreconditioner(op), tol=1e-8, max_iter=3000, chunk=16,
-                     split_step=False, gs_tail=tail)
+                     split_step=False, gs_tail=tail and not a.mode2)
     res[tail] = sc.solve(b)
     print(json.dumps({"N": N, "counts": counts, "gs_tail": tail,
                       "launches_per_iter": solvers[tail].launches_per_iter,

@@ -122,3 +122,32 @@ def test_gs_tail_off_for_other_orders_and_ranks():
     op = nk.PoissonOperator(m)
     s = nk.FusedPCG(op, nk.JacobiPreconditioner(op), split_step=False, gs_tail=True)
     assert not s.gs_tail and s.launches_per_iter == 3
+
+
+@pytest.mark.parametrize("counts,N,bc,lam1,split", [((4, 4, 4), 7, "dirichlet", 0.0, False),
+                                                    ((10, 10, 10), 7, "periodic", 1.0, False),
+                                                    ((20, 20, 20), 7, "dirichlet", 0.0, False),
+                                                    ((5, 4, 3), 3, "neumann", 0.5, True),
+                                                    ((6, 6, 6), 8, "dirichlet", 0.0, True)])
+def test_gs_in_update_bit_identical(counts, N, bc, lam1, split):
+    """NK_KNOB_GS_TAIL = 2: nk_cg_update_gs_cls runs the edge / vertex gs
+    inside the update kernel before a grid barrier (one launch instead of
+    two): same iterations, residual history and solution bit for bit as the
+    separate passes (knob 0), graph-replayed, on the fused and split steps."""
+    L = _lib.lib()
+    m = nk.build_box_mesh((1.0, 1.0, 1.0), counts, N, bc=bc, deformation=("sine", 0.05))
+    o = om.build_box_mesh((1.0, 1.0, 1.0), counts, N, bc=bc, deformation=("sine", 0.05))
+    op = nk.PoissonOperator(m, lam1=lam1)
+    jac = nk.JacobiPreconditioner(op)
+    b = _rhs(m, o, 11)
+    max_iter = 60 if m.E >= 8000 else 3000
+    res = {}
+    for knob in (2, 0):
+        L.nk_set_knob(KNOB_GS_TAIL, knob)
+        s = nk.FusedPCG(op, jac, tol=1e-9, max_iter=max_iter, split_step=split, gs_tail=False)
+        res[knob] = s.solve(b)
+    assert res[2].iterations == res[0].iterations
+    assert res[2].residual_history == res[0].residual_history
+    assert torch.equal(res[2].x, res[0].x)
+    if max_iter == 3000:
+        assert res[2].converged
