@@ -387,6 +387,7 @@ class FusedPCG:
                     self.op.apply_pcg(self.p, self.w, self.x, self.r, self.invD, self.st,
                                       self.part_bk5, self.hist, local=self.codes[1])
                 self._allreduce(1, 2)                                    # pAp
+                self._update_gs(L, s)
             elif self.gs_tail:
                 self._step_gs_tail(L, s)
                 self._update_gs(L, s)
