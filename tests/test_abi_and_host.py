@@ -211,3 +211,31 @@ def test_bc_normalisation():
         normalize_bc({"x-": "periodic"})
     with pytest.raises(ValueError):
         normalize_bc("slip")
+
+
+def test_gs_fold_entry_points_reject_bad_class_tables(L):
+    """nk_bk5_pcg_gs / nk_cg_update_gs_cls validate their class table (as
+    nk_gs_op_classes does) before any device work: too many classes, a
+    class wider than a warp, null members -> NK_ERR_INVALID with a message."""
+    import ctypes
+
+    from paper_2104_05829_b200 import _lib
+    dummy = ctypes.c_void_p(16)
+    sizes = np.array([4, 40], np.int32)
+    nsegs = np.array([3, 1], np.int64)
+    mem = np.array([16, 16], np.uint64)
+    rc = L.nk_cg_update_gs_cls(8, dummy, dummy, dummy, dummy, 2, sizes.ctypes.data,
+                               nsegs.ctypes.data, mem.ctypes.data, dummy, dummy, None)
+    assert rc == _lib.NK_ERR_INVALID and b"class 1 invalid" in L.nk_last_error()
+    rc = L.nk_cg_update_gs_cls(8, dummy, dummy, dummy, dummy, 17, sizes.ctypes.data,
+                               nsegs.ctypes.data, mem.ctypes.data, dummy, dummy, None)
+    assert rc == _lib.NK_ERR_INVALID and b"max 16 classes" in L.nk_last_error()
+    rc = L.nk_cg_update_gs_cls(-1, dummy, dummy, dummy, dummy, 0, None, None, None, dummy,
+                               dummy, None)
+    assert rc == _lib.NK_ERR_INVALID
+    mem0 = np.array([16, 0], np.uint64)
+    sizes_ok = np.array([4, 8], np.int32)
+    rc = L.nk_bk5_pcg_gs(7, 8, dummy, dummy, dummy, dummy, 1.0, None, 0.0, None, dummy, dummy,
+                         dummy, dummy, dummy, 8, None, 2, sizes_ok.ctypes.data,
+                         nsegs.ctypes.data, mem0.ctypes.data, None)
+    assert rc == _lib.NK_ERR_INVALID and b"class 1 invalid" in L.nk_last_error()
