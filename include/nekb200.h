@@ -445,6 +445,9 @@ int nk_cg_update_gs_cls(int64_t n, double* r, double* w, const double* invD, con
                         int nclass, const int32_t* sizes, const int64_t* nsegs,
                         const int32_t* const* members, nk_cg_state* st, double* partials,
                         nk_stream_t stream);
+/* 1 if nk_cg_update_gs_cls on n points is one launch under the current
+ * knobs (16-byte aligned operands assumed) */
+int nk_cg_update_gs_cls_fused(int64_t n);
 
 /* The vector head of nk_bk5_pcg as its own coalesced pass (iteration
  * k = st->iter): k > 0: stop test on st->rr, x += alpha_{k-1} p,

@@ -70,6 +70,7 @@ _SIGS = {
                        _P, _I32, _P, _P, _P, _P], _I32),
     "nk_bk5_pcg_gs_fused": ([_I32], _I32),
     "nk_cg_update_gs_cls": ([_I64, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P], _I32),
+    "nk_cg_update_gs_cls_fused": ([_I64], _I32),
     "nk_bk5_set_variant": ([_I32], _I32),
     "nk_bk5_tune": ([_I32, _I32], _I32),
     "nk_set_knob": ([_I32, _I32], _I32),

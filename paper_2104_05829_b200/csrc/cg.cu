@@ -791,6 +791,24 @@ cg_update_gs_pre_kernel(int64_t n, double* __restrict__ r, double* w,
   }
 }
 
+static bool gs_pre_resident(int64_t g) {
+  static int per = -1, sms = 0;
+  if (per < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_update_gs_pre_kernel, kVecThreads,
+                                                      0) != cudaSuccess)
+      per = 0;
+  }
+  return (int64_t)per * sms >= g;   // the barrier needs the whole grid resident
+}
+
+extern "C" int nk_cg_update_gs_cls_fused(int64_t n) {
+  return (knob(NK_KNOB_GS_TAIL) == 2 && (cg_pipe(n) & 3) == 2 && gs_pre_resident(vec_grid(n)))
+             ? 1 : 0;
+}
+
 extern "C" int nk_cg_update_gs_cls(int64_t n, double* r, double* w, const double* invD,
                                    const int32_t* code, int nclass, const int32_t* sizes,
                                    const int64_t* nsegs, const int32_t* const* members,
@@ -805,16 +823,7 @@ extern "C" int nk_cg_update_gs_cls(int64_t n, double* r, double* w, const double
   bool fuse = T.n > 0 && knob(NK_KNOB_GS_TAIL) == 2 && aligned16(r, w, invD) &&
               ((uintptr_t)code & 7) == 0 && (cg_pipe(n) & 3) == 2;
   const int64_t g = vec_grid(n);
-  if (fuse) {
-    static int per = -1, sms = 0;
-    if (per < 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_update_gs_pre_kernel, kVecThreads, 0);
-    }
-    fuse = (int64_t)per * sms >= g;   // the barrier needs the whole grid resident
-  }
+  if (fuse) fuse = gs_pre_resident(g);
   if (!fuse) {
     if (T.n > 0) {
       rc = nk_gs_op_classes(nclass, sizes, nsegs, members, w, NK_OP_ADD, 1, 0, st, stream);

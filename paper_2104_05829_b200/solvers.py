@@ -363,6 +363,9 @@ class FusedPCG:
         self.gs_tail = can_tail if gs_tail is None else (bool(gs_tail) and can_tail)
         if self.gs_tail:
             self.launches_per_iter = 2    # bk5_pcg + gs tail, update
+        elif (can_tail or (self.comm is None and self.gcodes is None and plan is not None and
+                           plan.rest is None)) and lib().nk_cg_update_gs_cls_fused(n):
+            self.launches_per_iter -= 1   # gs inside the update (NK_KNOB_GS_TAIL = 2)
 
     def _allreduce(self, a, b):
         if self.comm is not None:

@@ -145,6 +145,7 @@ def test_gs_in_update_bit_identical(counts, N, bc, lam1, split):
     for knob in (2, 0):
         L.nk_set_knob(KNOB_GS_TAIL, knob)
         s = nk.FusedPCG(op, jac, tol=1e-9, max_iter=max_iter, split_step=split, gs_tail=False)
+        assert s.launches_per_iter == (3 if split else 2) + (knob == 0)
         res[knob] = s.solve(b)
     assert res[2].iterations == res[0].iterations
     assert res[2].residual_history == res[0].residual_history
